@@ -1,0 +1,130 @@
+/*
+ * vsp_gpu.h — C ABI of the B200-native (sm_100a) VS-prefill path.
+ *
+ * Drop-in for the reference's hot-path operator API (header-only C++, namespace vsp,
+ * /root/reference/proj/include/vsprefill). Every entry point here replaces one reference
+ * function, batched over heads and operating on caller-owned DEVICE buffers:
+ *
+ *   vsp_indexer_scores   <- vsp::indexer_forward          indexer.hpp:116-120 (+ :77-113)
+ *   vsp_select           <- vsp::select_pattern           sparsity.hpp:105-114
+ *                           (cumulative_budget :51-79, topk_indices :83-97,
+ *                            inject_offset_zero :99-101)
+ *   vsp_vs_attn_fwd      <- vsp::sparse_attention         attention.hpp:150-194
+ *                           (merge_row_columns merge.hpp:18-56, fused on the fly)
+ *   vsp_dense_attn_fwd   <- vsp::blockwise_attention      attention.hpp:96-145
+ *   vsp_vs_aggregate     <- vsp::aggregate_streaming      vsaggregate.hpp:62-127
+ *                           + vsp::combine_scores         vsaggregate.hpp:133-157
+ *   vsp_recall_from_lse  <- vsp::attention_recall         attention.hpp:198-215
+ *
+ * Layouts (all row-major, innermost last):
+ *   Q [n, hq, d] bf16, K/V [n, hkv, d] bf16, O [n, hq, d] bf16, LSE [hq, n] fp32,
+ *   scores A_v/A_s [hkv, n] fp32, index lists I_v/I_s [hkv, cap] int32 ascending with
+ *   counts k_v/k_s [hkv] int32. Q head h uses KV head h / (hq / hkv) (GQA), and a KV
+ *   head's pattern is shared by its Q heads (the reference models one KV group as one
+ *   head). d must be 128 for the attention kernels.
+ *
+ * Semantics are the reference's: logit scale 1/sqrt(d) (attention.hpp:31); slash offset
+ * o = i - j; offset 0 always injected into I_s; top-k ties to the lower index; output
+ * index lists ascending; cumulative threshold with tau - 1e-12 slack.
+ *
+ * Errors: every call returns a vsp_status. VSP_EINVAL carries the reference's exception
+ * text (e.g. "uncovered query row 0") in vsp_last_error() (thread-local). Calls are
+ * stream-ordered and asynchronous unless a flag asks for validation. There is no CPU
+ * fallback: without a sm_100 device every compute call returns VSP_ECUDA.
+ */
+#ifndef VSP_GPU_H
+#define VSP_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VSP_API __attribute__((visibility("default")))
+#else
+#define VSP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    VSP_OK = 0,
+    VSP_EINVAL = 1,   /* std::invalid_argument in the reference */
+    VSP_ERUNTIME = 2, /* std::runtime_error */
+    VSP_ECUDA = 3,
+    VSP_ENCCL = 4
+} vsp_status;
+
+/* Slash mapping (reference indexer.hpp:22): 0 = Reverse (default), 1 = Identity. */
+enum { VSP_SLASH_REVERSE = 0, VSP_SLASH_IDENTITY = 1 };
+/* Group reduce (vsaggregate.hpp:131): 0 = Mean, 1 = Sum. */
+enum { VSP_REDUCE_MEAN = 0, VSP_REDUCE_SUM = 1 };
+/* vsp_vs_attn_fwd flags */
+enum { VSP_VALIDATE = 1 /* sync + check sortedness/range/coverage like the reference */ };
+
+/* Reference BudgetConfig (sparsity.hpp:22-36). max_budget < 0 means "no maximum". */
+typedef struct {
+    double tau_v;
+    double tau_s;
+    int64_t min_budget;
+    int64_t max_budget;
+} vsp_budget;
+
+typedef struct vsp_ctx vsp_ctx;
+
+VSP_API const char* vsp_last_error(void);
+VSP_API const char* vsp_version(void);
+
+VSP_API int vsp_create(vsp_ctx** ctx, int device);
+VSP_API int vsp_destroy(vsp_ctx* ctx);
+
+/* ---- K1: VSIndexer scoring -------------------------------------------------------
+ * X_t = [K_t | V_t] (per KV head), Z = SiLU(X W_U + b_U), logit_v = Z w_v + b_v,
+ * raw_s = Z w_s + b_s, logit_s[o] = raw_s[n-1-o] (Reverse) or raw_s[o] (Identity),
+ * A_v = softmax(logit_v), A_s = softmax(logit_s) over all n.
+ * w_u: bf16 [hkv, 2d, d_h] (rows 0..d-1 multiply K, d..2d-1 multiply V; indexer.hpp:119),
+ * b_u/w_v/w_s: fp32 [hkv, d_h], b_v/b_s: fp32 [hkv]. logits_v/logits_s may be NULL. */
+VSP_API size_t vsp_indexer_workspace_size(int n, int hkv, int d_h);
+VSP_API int vsp_indexer_scores(vsp_ctx* ctx, const void* k, const void* v, int n, int hkv, int d, int d_h,
+                       const void* w_u, const float* b_u, const float* w_v, const float* b_v,
+                       const float* w_s, const float* b_s, int slash_mapping, float* a_v,
+                       float* a_s, float* logits_v, float* logits_s, void* workspace,
+                       void* stream);
+
+/* ---- K2: adaptive cumulative-threshold top-k selection ---------------------------
+ * budgets: HOST array [hkv]. Outputs I_v/I_s [hkv, cap] (cap >= n + 1), k_v/k_s [hkv].
+ * Index sets are bit-exact with select_pattern on the same scores widened to f64. */
+VSP_API size_t vsp_select_workspace_size(int n, int hkv);
+VSP_API int vsp_select(vsp_ctx* ctx, const float* a_v, const float* a_s, int n, int hkv,
+               const vsp_budget* budgets, int* i_v, int* k_v, int* i_s, int* k_s, int cap,
+               void* workspace, void* stream);
+
+/* ---- K3: fused vertical-slash sparse attention forward --------------------------- */
+VSP_API size_t vsp_vs_attn_workspace_size(int n, int hkv, int cap);
+VSP_API int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                    int hkv, int d, const int* i_v, const int* k_v, const int* i_s,
+                    const int* k_s, int cap, float scale, void* o, float* lse, void* workspace,
+                    int flags, void* stream);
+
+/* ---- K4: dense causal attention forward (the speed-up denominator) ---------------- */
+VSP_API int vsp_dense_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                       int hkv, int d, float scale, void* o, float* lse, void* stream);
+
+/* ---- K5: ground-truth vertical/slash aggregation ----------------------------------
+ * A_v[g][j] = reduce_{h in group g} sum_i A_h[i,j] (/ n if normalized),
+ * A_s[g][o] = reduce_{h in group g} sum_i A_h[i,i-o]. lse: [hq, n] from K4 (pass 1),
+ * or NULL to compute it. */
+VSP_API size_t vsp_aggregate_workspace_size(int n, int hq);
+VSP_API int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, int hq, int hkv, int d,
+                     float scale, const float* lse, int reduce, int normalized, float* a_v,
+                     float* a_s, void* workspace, void* stream);
+
+/* ---- recall from LSE pairs: mean_i exp(lse_sparse - lse_dense) per Q head ---------- */
+VSP_API int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n,
+                        int hq, float* recall_per_head, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSP_GPU_H */

@@ -1,0 +1,289 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU checker for the sm_100a VS-prefill path.
+
+Two libraries, both f64 and single-threaded per head:
+  * ``port()`` — vsp_oracle.c, a plain-C restatement of the reference hot path
+    (every function cites the reference file:line it follows);
+  * ``ref()``  — oracle/_ref/libvspref.so: the UNMODIFIED reference headers from
+    /root/reference/proj/include wrapped in extern "C" (ref_shim.cpp). Built only
+    where /root/reference exists; the .so travels to the GPU box with the repo.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference)
+may import this package. The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "_build", "libvsp_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libvspref.so")
+
+_f64p = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i64 = ctypes.c_int64
+_cp = ctypes.c_char_p
+
+
+class OracleError(ValueError):
+    """Mirrors the reference's std::invalid_argument (same message text)."""
+
+
+def build(quiet: bool = True) -> None:
+    r = subprocess.run(["make", "-C", HERE], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + r.stdout + r.stderr)
+
+
+def _bind(lib, prefix: str):
+    sig = {
+        "merge_row_columns": (_i64, [_i64p, _i64, _i64p, _i64, _i64, _i64p, _cp, ctypes.c_size_t]),
+        "merge_path_partition": (ctypes.c_int, [_i64p, _i64, _i64p, _i64, _i64, _i64p, _cp, ctypes.c_size_t]),
+        "cumulative_budget": (ctypes.c_int, [_f64p, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                             _i64, _i64, _i64p, _cp, ctypes.c_size_t]),
+        "topk_indices": (ctypes.c_int, [_f64p, _i64, _i64, _i64p, _cp, ctypes.c_size_t]),
+        "select_pattern": (ctypes.c_int, [_f64p, _f64p, _i64, ctypes.c_double, ctypes.c_double, _i64, _i64,
+                                          _i64p, _i64p, _i64p, _i64p, _cp, ctypes.c_size_t]),
+        "indexer_forward": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64, _f64p, _f64p, _f64p,
+                                           ctypes.c_double, _f64p, ctypes.c_double, ctypes.c_int,
+                                           _f64p, _f64p, _f64p, _f64p, _cp, ctypes.c_size_t]),
+        "aggregate_streaming": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64, ctypes.c_int,
+                                               _f64p, _f64p, _cp, ctypes.c_size_t]),
+    }
+    if prefix == "vso_":
+        sig["blockwise_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64,
+                                                     _f64p, _i64, _f64p, _cp, ctypes.c_size_t])
+        sig["sparse_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64p, _i64,
+                                                  _i64p, _i64, _i64, _f64p, _i64, _f64p, _cp, ctypes.c_size_t])
+        sig["combine_scores"] = (None, [_i64, _i64, _f64p, _f64p, ctypes.c_int, _f64p, _f64p])
+    else:
+        sig["blockwise_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64,
+                                                     _f64p, _i64, _cp, ctypes.c_size_t])
+        sig["sparse_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64p, _i64,
+                                                  _i64p, _i64, _i64, _f64p, _i64, _cp, ctypes.c_size_t])
+        sig["combine_scores"] = (ctypes.c_int, [_i64, _i64, _f64p, _f64p, ctypes.c_int, _f64p, _f64p, _cp,
+                                                ctypes.c_size_t])
+        sig["attention_recall"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64p, _i64, _i64p, _i64,
+                                                  _f64p, _cp, ctypes.c_size_t])
+        sig["layer_vs_prefill"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64, _f64p, _f64p,
+                                                  _f64p, _f64p, _f64p, _f64p, ctypes.c_double, ctypes.c_double,
+                                                  _i64, _i64, _i64, ctypes.c_int, _f64p, _i64p, _i64p, _cp,
+                                                  ctypes.c_size_t])
+        sig["layer_dense"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64, ctypes.c_int,
+                                             _f64p, _cp, ctypes.c_size_t])
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, prefix + name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def _f(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_f64p)
+
+
+def _i(a: np.ndarray):
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_i64p)
+
+
+class _Oracle:
+    """numpy front-end over either library; per-head functions take [n, d] arrays."""
+
+    def __init__(self, so: str, prefix: str):
+        if not os.path.exists(so):
+            build()
+        if not os.path.exists(so):
+            raise FileNotFoundError(so)
+        self.lib = _bind(ctypes.CDLL(so), prefix)
+        self.p = prefix
+        self.is_ref = prefix == "vspref_"
+
+    def _call(self, name, *args):
+        err = ctypes.create_string_buffer(512)
+        rc = getattr(self.lib, self.p + name)(*args, err, 512)
+        return rc, err.value.decode()
+
+    def _check(self, rc, msg):
+        if rc != 0:
+            raise OracleError(msg)
+
+    # ---- merge
+    def merge_row_columns(self, iv, is_, i):
+        iv = np.ascontiguousarray(iv, np.int64)
+        is_ = np.ascontiguousarray(is_, np.int64)
+        out = np.zeros(len(iv) + len(is_) + 1, np.int64)
+        rc, msg = self._call("merge_row_columns", _i(iv), len(iv), _i(is_), len(is_), int(i), _i(out))
+        if rc < 0:
+            raise OracleError(msg)
+        return out[:rc].copy()
+
+    def merge_path_partition(self, a, b, p):
+        a = np.ascontiguousarray(a, np.int64)
+        b = np.ascontiguousarray(b, np.int64)
+        cuts = np.zeros(2 * (max(p, 1) + 1), np.int64)
+        rc, msg = self._call("merge_path_partition", _i(a), len(a), _i(b), len(b), int(p), _i(cuts))
+        self._check(rc, msg)
+        return [tuple(c) for c in cuts.reshape(-1, 2)]
+
+    # ---- attention (one head; q/k/v [n, d] f64)
+    def blockwise_attention(self, q, k, v, block=64, want_lse=False):
+        q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
+        n, d = q.shape
+        o = np.zeros((n, d))
+        if self.is_ref:
+            rc, msg = self._call("blockwise_attention", n, d, _f(q), d, _f(k), d, _f(v), d, block, _f(o), d)
+            self._check(rc, msg)
+            return o
+        lse = np.zeros(n)
+        rc, msg = self._call("blockwise_attention", n, d, _f(q), d, _f(k), d, _f(v), d, block, _f(o), d, _f(lse))
+        self._check(rc, msg)
+        return (o, lse) if want_lse else o
+
+    def sparse_attention(self, q, k, v, iv, is_, block=32, want_lse=False):
+        q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
+        iv = np.ascontiguousarray(iv, np.int64)
+        is_ = np.ascontiguousarray(is_, np.int64)
+        n, d = q.shape
+        o = np.zeros((n, d))
+        if self.is_ref:
+            rc, msg = self._call("sparse_attention", n, d, _f(q), d, _f(k), d, _f(v), d, _i(iv), len(iv), _i(is_),
+                                 len(is_), block, _f(o), d)
+            self._check(rc, msg)
+            return o
+        lse = np.zeros(n)
+        rc, msg = self._call("sparse_attention", n, d, _f(q), d, _f(k), d, _f(v), d, _i(iv), len(iv), _i(is_),
+                             len(is_), block, _f(o), d, _f(lse))
+        self._check(rc, msg)
+        return (o, lse) if want_lse else o
+
+    def attention_recall(self, q, k, iv, is_):
+        assert self.is_ref
+        q, k = (np.ascontiguousarray(x, np.float64) for x in (q, k))
+        iv = np.ascontiguousarray(iv, np.int64)
+        is_ = np.ascontiguousarray(is_, np.int64)
+        n, d = q.shape
+        r = np.zeros(1)
+        rc, msg = self._call("attention_recall", n, d, _f(q), d, _f(k), d, _i(iv), len(iv), _i(is_), len(is_), _f(r))
+        self._check(rc, msg)
+        return float(r[0])
+
+    # ---- selection
+    def cumulative_budget(self, scores, tau, tau_v=0.9, tau_s=0.9, min_budget=1, max_budget=-1):
+        s = np.ascontiguousarray(scores, np.float64)
+        k = np.zeros(1, np.int64)
+        rc, msg = self._call("cumulative_budget", _f(s), len(s), float(tau), float(tau_v), float(tau_s),
+                             int(min_budget), int(max_budget), _i(k))
+        self._check(rc, msg)
+        return int(k[0])
+
+    def topk_indices(self, scores, k):
+        s = np.ascontiguousarray(scores, np.float64)
+        out = np.zeros(max(int(k), 1), np.int64)
+        rc, msg = self._call("topk_indices", _f(s), len(s), int(k), _i(out))
+        self._check(rc, msg)
+        return out[: int(k)].copy()
+
+    def select_pattern(self, sv, ss, tau_v=0.9, tau_s=0.9, min_budget=1, max_budget=-1):
+        sv = np.ascontiguousarray(sv, np.float64)
+        ss = np.ascontiguousarray(ss, np.float64)
+        n = len(sv)
+        iv = np.zeros(n + 1, np.int64)
+        is_ = np.zeros(n + 1, np.int64)
+        kv = np.zeros(1, np.int64)
+        ks = np.zeros(1, np.int64)
+        rc, msg = self._call("select_pattern", _f(sv), _f(ss), n, float(tau_v), float(tau_s), int(min_budget),
+                             int(max_budget), _i(iv), _i(kv), _i(is_), _i(ks))
+        self._check(rc, msg)
+        return iv[: kv[0]].copy(), is_[: ks[0]].copy()
+
+    # ---- indexer (one KV head): params dict with w_u [2d, d_h], b_u, w_v, b_v, w_s, b_s
+    def indexer_forward(self, k, v, params, reverse=True):
+        k, v = (np.ascontiguousarray(x, np.float64) for x in (k, v))
+        n, d = k.shape
+        w_u = np.ascontiguousarray(params["w_u"], np.float64)
+        d_h = w_u.shape[1]
+        b_u, w_v, w_s = (np.ascontiguousarray(params[x], np.float64) for x in ("b_u", "w_v", "w_s"))
+        outs = [np.zeros(n) for _ in range(4)]
+        rc, msg = self._call("indexer_forward", n, d, _f(k), d, _f(v), d, d_h, _f(w_u), _f(b_u), _f(w_v),
+                             float(params["b_v"]), _f(w_s), float(params["b_s"]), int(bool(reverse)),
+                             *[_f(o) for o in outs])
+        self._check(rc, msg)
+        return dict(logits_v=outs[0], logits_s=outs[1], pred_v=outs[2], pred_s=outs[3])
+
+    # ---- aggregation (one head)
+    def aggregate_streaming(self, q, k, block=64, normalized=True):
+        q, k = (np.ascontiguousarray(x, np.float64) for x in (q, k))
+        n, d = q.shape
+        vert = np.zeros(n)
+        sl = np.zeros(n)
+        rc, msg = self._call("aggregate_streaming", n, d, _f(q), d, _f(k), d, int(block), int(bool(normalized)),
+                             _f(vert), _f(sl))
+        self._check(rc, msg)
+        return vert, sl
+
+    def combine_scores(self, verts, slashes, mean=True):
+        v = np.ascontiguousarray(np.stack(verts), np.float64)
+        s = np.ascontiguousarray(np.stack(slashes), np.float64)
+        h, n = v.shape
+        vo = np.zeros(n)
+        so = np.zeros(n)
+        if self.is_ref:
+            rc, msg = self._call("combine_scores", h, n, _f(v), _f(s), int(bool(mean)), _f(vo), _f(so))
+            self._check(rc, msg)
+        else:
+            getattr(self.lib, "vso_combine_scores")(h, n, _f(v), _f(s), int(bool(mean)), _f(vo), _f(so))
+        return vo, so
+
+    # ---- whole layer through the reference API (ref only), threaded over heads
+    def layer_vs_prefill(self, q, k, v, params, tau_v, tau_s, min_budget, max_budget, block=32, threads=1):
+        assert self.is_ref
+        n, hq, d = q.shape
+        hkv = k.shape[1]
+        q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
+        w_u = np.ascontiguousarray(params["w_u"], np.float64)
+        d_h = w_u.shape[2]
+        b_u, w_v, w_s, b_v, b_s = (np.ascontiguousarray(params[x], np.float64) for x in ("b_u", "w_v", "w_s",
+                                                                                            "b_v", "b_s"))
+        o = np.zeros((n, hq, d))
+        kv = np.zeros(hkv, np.int64)
+        ks = np.zeros(hkv, np.int64)
+        rc, msg = self._call("layer_vs_prefill", n, hq, hkv, d, _f(q), _f(k), _f(v), d_h, _f(w_u), _f(b_u), _f(w_v),
+                             _f(b_v), _f(w_s), _f(b_s), float(tau_v), float(tau_s), int(min_budget),
+                             int(max_budget), int(block), int(threads), _f(o), _i(kv), _i(ks))
+        self._check(rc, msg)
+        return o, kv, ks
+
+    def layer_dense(self, q, k, v, block=64, threads=1):
+        assert self.is_ref
+        n, hq, d = q.shape
+        hkv = k.shape[1]
+        q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
+        o = np.zeros((n, hq, d))
+        rc, msg = self._call("layer_dense", n, hq, hkv, d, _f(q), _f(k), _f(v), int(block), int(threads), _f(o))
+        self._check(rc, msg)
+        return o
+
+
+_cache: dict = {}
+
+
+def port() -> _Oracle:
+    if "port" not in _cache:
+        _cache["port"] = _Oracle(PORT_SO, "vso_")
+    return _cache["port"]
+
+
+def ref() -> _Oracle:
+    """The reference itself (raises FileNotFoundError if it was never built)."""
+    if "ref" not in _cache:
+        _cache["ref"] = _Oracle(REF_SO, "vspref_")
+    return _cache["ref"]
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)

@@ -1,0 +1,304 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrappers that call the UNMODIFIED reference library, compiled straight
+// from /root/reference/proj/include (header-only C++20; nothing is copied into this
+// repo). Built by oracle/Makefile into oracle/_ref/libvspref.so. Used to pin the C
+// oracle (tests/golden/make_golden.py) and as the reference CPU arm of bench.py.
+//
+// Argument conventions match oracle/vsp_oracle.c: matrices are (base, row_stride)
+// f64, index lists are int64, errors return 1 with the exception text in err.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "vsprefill/attention.hpp"
+#include "vsprefill/indexer.hpp"
+#include "vsprefill/merge.hpp"
+#include "vsprefill/sparsity.hpp"
+#include "vsprefill/vsaggregate.hpp"
+
+namespace {
+
+int set_err(char* err, size_t errlen, const char* msg) {
+    if (err && errlen) {
+        std::strncpy(err, msg, errlen - 1);
+        err[errlen - 1] = '\0';
+    }
+    return 1;
+}
+
+vsp::Matrix gather(const double* base, int64_t stride, int64_t rows, int64_t cols) {
+    vsp::Matrix m(static_cast<size_t>(rows), static_cast<size_t>(cols));
+    for (int64_t t = 0; t < rows; ++t)
+        std::memcpy(m.row_ptr(t), base + t * stride, sizeof(double) * cols);
+    return m;
+}
+
+std::vector<size_t> idx(const int64_t* p, int64_t n) {
+    std::vector<size_t> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) v[i] = static_cast<size_t>(p[i]);
+    return v;
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        return set_err(err, errlen, e.what());
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t vspref_merge_row_columns(const int64_t* iv, int64_t kv, const int64_t* is, int64_t ks,
+                                 int64_t i, int64_t* out, char* err, size_t errlen) {
+    int64_t cnt = -1;
+    guarded(err, errlen, [&] {
+        auto cols = vsp::merge_row_columns(idx(iv, kv), idx(is, ks), static_cast<size_t>(i));
+        for (size_t t = 0; t < cols.size(); ++t) out[t] = static_cast<int64_t>(cols[t]);
+        cnt = static_cast<int64_t>(cols.size());
+    });
+    return cnt;
+}
+
+int vspref_merge_path_partition(const int64_t* a, int64_t na, const int64_t* b, int64_t nb,
+                                int64_t p, int64_t* cuts, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        auto c = vsp::merge_path_partition(idx(a, na), idx(b, nb), static_cast<size_t>(p));
+        for (size_t s = 0; s < c.size(); ++s) {
+            cuts[2 * s] = static_cast<int64_t>(c[s].a);
+            cuts[2 * s + 1] = static_cast<int64_t>(c[s].b);
+        }
+    });
+}
+
+int vspref_blockwise_attention(int64_t n, int64_t d, const double* q, int64_t qs, const double* k,
+                               int64_t ks, const double* v, int64_t vs, int64_t block, double* o,
+                               int64_t os, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        vsp::AttentionInputs in(gather(q, qs, n, d), gather(k, ks, n, d), gather(v, vs, n, d));
+        auto out = vsp::blockwise_attention(in, static_cast<size_t>(block));
+        for (int64_t t = 0; t < n; ++t) std::memcpy(o + t * os, out.o.row_ptr(t), sizeof(double) * d);
+    });
+}
+
+int vspref_sparse_attention(int64_t n, int64_t d, const double* q, int64_t qs, const double* k,
+                            int64_t ks, const double* v, int64_t vs, const int64_t* iv, int64_t kv,
+                            const int64_t* is, int64_t ksl, int64_t block, double* o, int64_t os,
+                            char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        vsp::AttentionInputs in(gather(q, qs, n, d), gather(k, ks, n, d), gather(v, vs, n, d));
+        vsp::SparsePattern pat{idx(iv, kv), idx(is, ksl)};
+        auto out = vsp::sparse_attention(in, pat, static_cast<size_t>(block));
+        for (int64_t t = 0; t < n; ++t) std::memcpy(o + t * os, out.o.row_ptr(t), sizeof(double) * d);
+    });
+}
+
+// attention.hpp:52-75 + :198-215 (materialises n x n; small n only)
+int vspref_attention_recall(int64_t n, int64_t d, const double* q, int64_t qs, const double* k,
+                            int64_t ks, const int64_t* iv, int64_t kv, const int64_t* is,
+                            int64_t ksl, double* recall, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        auto a = vsp::attention_matrix(gather(q, qs, n, d), gather(k, ks, n, d));
+        *recall = vsp::attention_recall(a, vsp::SparsePattern{idx(iv, kv), idx(is, ksl)});
+    });
+}
+
+static vsp::BudgetConfig budget(double tau_v, double tau_s, int64_t min_b, int64_t max_b) {
+    vsp::BudgetConfig c;
+    c.tau_v = tau_v;
+    c.tau_s = tau_s;
+    c.min_budget = static_cast<size_t>(min_b < 0 ? 0 : min_b);
+    if (max_b >= 0) c.max_budget = static_cast<size_t>(max_b);
+    return c;
+}
+
+int vspref_cumulative_budget(const double* scores, int64_t n, double tau, double tau_v,
+                             double tau_s, int64_t min_b, int64_t max_b, int64_t* k_out, char* err,
+                             size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<double> s(scores, scores + n);
+        *k_out = static_cast<int64_t>(vsp::cumulative_budget(s, tau, budget(tau_v, tau_s, min_b, max_b)));
+    });
+}
+
+int vspref_topk_indices(const double* scores, int64_t n, int64_t k, int64_t* out, char* err,
+                        size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<double> s(scores, scores + n);
+        auto r = vsp::topk_indices(s, static_cast<size_t>(k));
+        for (size_t t = 0; t < r.size(); ++t) out[t] = static_cast<int64_t>(r[t]);
+    });
+}
+
+int vspref_select_pattern(const double* sv, const double* ss, int64_t n, double tau_v, double tau_s,
+                          int64_t min_b, int64_t max_b, int64_t* iv, int64_t* kv, int64_t* is,
+                          int64_t* ks, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        vsp::VSScores sc;
+        sc.vertical.assign(sv, sv + n);
+        sc.slash.assign(ss, ss + n);
+        sc.normalized = true;
+        auto sel = vsp::select_pattern(sc, budget(tau_v, tau_s, min_b, max_b));
+        for (size_t t = 0; t < sel.i_v.size(); ++t) iv[t] = static_cast<int64_t>(sel.i_v[t]);
+        for (size_t t = 0; t < sel.i_s.size(); ++t) is[t] = static_cast<int64_t>(sel.i_s[t]);
+        *kv = static_cast<int64_t>(sel.i_v.size());
+        *ks = static_cast<int64_t>(sel.i_s.size());
+    });
+}
+
+static vsp::IndexerParams params(int64_t d, int64_t d_h, const double* w_u, const double* b_u,
+                                 const double* w_v, double b_v, const double* w_s, double b_s) {
+    vsp::IndexerParams p;
+    p.d_h = static_cast<size_t>(d_h);
+    p.w_u = vsp::Matrix(static_cast<size_t>(2 * d), static_cast<size_t>(d_h),
+                        std::vector<double>(w_u, w_u + 2 * d * d_h));
+    p.b_u.assign(b_u, b_u + d_h);
+    p.w_v.assign(w_v, w_v + d_h);
+    p.b_v = b_v;
+    p.w_s.assign(w_s, w_s + d_h);
+    p.b_s = b_s;
+    return p;
+}
+
+int vspref_indexer_forward(int64_t n, int64_t d, const double* k, int64_t ks, const double* v,
+                           int64_t vs, int64_t d_h, const double* w_u, const double* b_u,
+                           const double* w_v, double b_v, const double* w_s, double b_s,
+                           int reverse, double* logits_v, double* logits_s, double* pred_v,
+                           double* pred_s, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        auto acts = vsp::indexer_forward(params(d, d_h, w_u, b_u, w_v, b_v, w_s, b_s),
+                                         gather(k, ks, n, d), gather(v, vs, n, d),
+                                         reverse ? vsp::SlashMapping::Reverse : vsp::SlashMapping::Identity);
+        std::copy(acts.logits_v.begin(), acts.logits_v.end(), logits_v);
+        std::copy(acts.logits_s.begin(), acts.logits_s.end(), logits_s);
+        std::copy(acts.pred_v.begin(), acts.pred_v.end(), pred_v);
+        std::copy(acts.pred_s.begin(), acts.pred_s.end(), pred_s);
+    });
+}
+
+int vspref_aggregate_streaming(int64_t n, int64_t d, const double* q, int64_t qs, const double* k,
+                               int64_t ks, int64_t block, int normalized, double* vertical,
+                               double* slash, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        vsp::Matrix qm = gather(q, qs, n, d), km = gather(k, ks, n, d);
+        vsp::AttentionInputs in(qm, km, km);  // V is unused by aggregation
+        auto s = vsp::aggregate_streaming(in, static_cast<size_t>(block), normalized != 0);
+        std::copy(s.vertical.begin(), s.vertical.end(), vertical);
+        std::copy(s.slash.begin(), s.slash.end(), slash);
+    });
+}
+
+int vspref_combine_scores(int64_t heads, int64_t n, const double* v_in, const double* s_in, int mean,
+                          double* v_out, double* s_out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<vsp::VSScores> hs(static_cast<size_t>(heads));
+        for (int64_t h = 0; h < heads; ++h) {
+            hs[h].vertical.assign(v_in + h * n, v_in + (h + 1) * n);
+            hs[h].slash.assign(s_in + h * n, s_in + (h + 1) * n);
+            hs[h].normalized = true;
+        }
+        auto c = vsp::combine_scores(hs, mean ? vsp::GroupReduce::Mean : vsp::GroupReduce::Sum);
+        std::copy(c.vertical.begin(), c.vertical.end(), v_out);
+        std::copy(c.slash.begin(), c.slash.end(), s_out);
+    });
+}
+
+// Whole-layer VS prefill through the reference API, threaded over heads with
+// std::thread (each reference call is a pure per-head function).
+// Tensors are token-major f64: q [n, hq, d], k/v [n, hkv, d]; indexer params per KV
+// head: w_u [hkv, 2d, d_h], b_u/w_v/w_s [hkv, d_h], b_v/b_s [hkv]. Output o [n, hq, d].
+// k_v/k_s (out, [hkv]) report the selected budgets.
+int vspref_layer_vs_prefill(int64_t n, int64_t hq, int64_t hkv, int64_t d, const double* q,
+                            const double* k, const double* v, int64_t d_h, const double* w_u,
+                            const double* b_u, const double* w_v, const double* b_v,
+                            const double* w_s, const double* b_s, double tau_v, double tau_s,
+                            int64_t min_b, int64_t max_b, int64_t block, int n_threads, double* o,
+                            int64_t* k_v, int64_t* k_s, char* err, size_t errlen) {
+    const int64_t group = hq / hkv;
+    std::vector<vsp::SparsePattern> pats(static_cast<size_t>(hkv));
+    std::vector<std::string> errs;
+    std::atomic<int64_t> next{0};
+    std::atomic<int> failed{0};
+    std::string first_err;
+    auto run_pool = [&](int64_t items, auto&& body) {
+        next = 0;
+        std::vector<std::thread> pool;
+        const int nt = std::max(1, std::min<int>(n_threads, static_cast<int>(items)));
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&] {
+                for (int64_t it; (it = next.fetch_add(1)) < items;) {
+                    try {
+                        body(it);
+                    } catch (const std::exception& e) {
+                        if (failed.exchange(1) == 0) first_err = e.what();
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+    };
+    run_pool(hkv, [&](int64_t g) {
+        auto p = params(d, d_h, w_u + g * 2 * d * d_h, b_u + g * d_h, w_v + g * d_h, b_v[g],
+                        w_s + g * d_h, b_s[g]);
+        auto acts = vsp::indexer_forward(p, gather(k + g * d, hkv * d, n, d),
+                                         gather(v + g * d, hkv * d, n, d));
+        vsp::VSScores sc{acts.pred_v, acts.pred_s, true};
+        auto sel = vsp::select_pattern(sc, budget(tau_v, tau_s, min_b, max_b));
+        k_v[g] = static_cast<int64_t>(sel.k_v());
+        k_s[g] = static_cast<int64_t>(sel.k_s());
+        pats[g] = sel.pattern();
+    });
+    if (failed) return set_err(err, errlen, first_err.c_str());
+    run_pool(hq, [&](int64_t h) {
+        const int64_t g = h / group;
+        vsp::AttentionInputs in(gather(q + h * d, hq * d, n, d), gather(k + g * d, hkv * d, n, d),
+                                gather(v + g * d, hkv * d, n, d));
+        auto out = vsp::sparse_attention(in, pats[g], static_cast<size_t>(block));
+        for (int64_t t = 0; t < n; ++t)
+            std::memcpy(o + (t * hq + h) * d, out.o.row_ptr(t), sizeof(double) * d);
+    });
+    if (failed) return set_err(err, errlen, first_err.c_str());
+    return 0;
+}
+
+// Dense causal layer through blockwise_attention (attention.hpp:96-145), threaded.
+int vspref_layer_dense(int64_t n, int64_t hq, int64_t hkv, int64_t d, const double* q,
+                       const double* k, const double* v, int64_t block, int n_threads, double* o,
+                       char* err, size_t errlen) {
+    const int64_t group = hq / hkv;
+    std::atomic<int64_t> next{0};
+    std::atomic<int> failed{0};
+    std::string first_err;
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, std::min<int>(n_threads, static_cast<int>(hq)));
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+            for (int64_t h; (h = next.fetch_add(1)) < hq;) {
+                try {
+                    const int64_t g = h / group;
+                    vsp::AttentionInputs in(gather(q + h * d, hq * d, n, d),
+                                            gather(k + g * d, hkv * d, n, d),
+                                            gather(v + g * d, hkv * d, n, d));
+                    auto out = vsp::blockwise_attention(in, static_cast<size_t>(block));
+                    for (int64_t r = 0; r < n; ++r)
+                        std::memcpy(o + (r * hq + h) * d, out.o.row_ptr(r), sizeof(double) * d);
+                } catch (const std::exception& e) {
+                    if (failed.exchange(1) == 0) first_err = e.what();
+                }
+            }
+        });
+    for (auto& th : pool) th.join();
+    if (failed) return set_err(err, errlen, first_err.c_str());
+    return 0;
+}
+
+}  // extern "C"

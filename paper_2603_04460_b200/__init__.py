@@ -1,0 +1,314 @@
+"""B200-native VS-prefill path (arxiv 2603.04460) behind the reference's operator API.
+
+Host-side mirror of the reference's hot-path functions (namespace ``vsp`` in
+/root/reference/proj/include/vsprefill) over the C ABI in include/vsp_gpu.h, which
+dispatches to hand-written sm_100a kernels (tcgen05/TMEM/TMA). Torch tensors are used
+only as device-memory carriers. There is no CPU fallback: every call fails loudly when
+the extension (libvsp_gpu.so) or an sm_100 device is missing.
+
+    reference                                  here
+    ---------------------------------------    ------------------------------------
+    vsp::indexer_forward   indexer.hpp:116      indexer_forward(k, v, params)
+    vsp::select_pattern    sparsity.hpp:105     select_pattern(a_v, a_s, budget)
+    vsp::sparse_attention  attention.hpp:150    sparse_attention(q, k, v, pattern)
+    vsp::blockwise_attention attention.hpp:96   blockwise_attention(q, k, v)
+    vsp::aggregate_streaming vsaggregate.hpp:62 aggregate_streaming(q, k)
+      + combine_scores     vsaggregate.hpp:133    (group reduce fused)
+    vsp::attention_recall  attention.hpp:198    attention_recall(lse_sparse, lse_dense)
+
+Tensors are batched over heads: Q [n, Hq, 128], K/V [n, Hkv, 128] bf16 (Q head h reads
+KV head h // (Hq // Hkv)); one VS pattern per KV head, shared by its Q heads.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+import os
+from typing import Optional, Sequence
+
+import torch
+
+__all__ = [
+    "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
+    "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
+    "aggregate_streaming", "attention_recall", "vs_prefill", "lib_path", "load_library",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "libvsp_gpu.so")
+
+VSP_OK, VSP_EINVAL, VSP_ERUNTIME, VSP_ECUDA, VSP_ENCCL = range(5)
+
+
+class VspError(ValueError):
+    """VSP_EINVAL: the reference would have thrown std::invalid_argument (same text)."""
+
+
+class VspRuntimeError(RuntimeError):
+    """VSP_ECUDA / VSP_ERUNTIME / VSP_ENCCL."""
+
+
+class _Budget(ctypes.Structure):
+    _fields_ = [("tau_v", ctypes.c_double), ("tau_s", ctypes.c_double),
+                ("min_budget", ctypes.c_int64), ("max_budget", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libvsp_gpu.so (building it first if absent). Raises if it cannot be had."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        from . import _build
+        _build.build()
+    lib = ctypes.CDLL(lib_path)
+    vp, i, f, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t
+    lib.vsp_last_error.restype = ctypes.c_char_p
+    lib.vsp_version.restype = ctypes.c_char_p
+    lib.vsp_create.argtypes = [ctypes.POINTER(vp), i]
+    lib.vsp_destroy.argtypes = [vp]
+    lib.vsp_indexer_workspace_size.restype = sz
+    lib.vsp_indexer_workspace_size.argtypes = [i, i, i]
+    lib.vsp_indexer_scores.argtypes = [vp, vp, vp, i, i, i, i, vp, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp]
+    lib.vsp_select_workspace_size.restype = sz
+    lib.vsp_select_workspace_size.argtypes = [i, i]
+    lib.vsp_select.argtypes = [vp, vp, vp, i, i, ctypes.POINTER(_Budget), vp, vp, vp, vp, i, vp, vp]
+    lib.vsp_vs_attn_workspace_size.restype = sz
+    lib.vsp_vs_attn_workspace_size.argtypes = [i, i, i]
+    lib.vsp_vs_attn_fwd.argtypes = [vp, vp, vp, vp, i, i, i, i, vp, vp, vp, vp, i, f, vp, vp, vp, i, vp]
+    lib.vsp_dense_attn_fwd.argtypes = [vp, vp, vp, vp, i, i, i, i, f, vp, vp, vp]
+    lib.vsp_aggregate_workspace_size.restype = sz
+    lib.vsp_aggregate_workspace_size.argtypes = [i, i]
+    lib.vsp_vs_aggregate.argtypes = [vp, vp, vp, i, i, i, i, f, vp, i, i, vp, vp, vp, vp]
+    lib.vsp_recall_from_lse.argtypes = [vp, vp, vp, i, i, vp, vp]
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc == VSP_OK:
+        return
+    msg = _lib.vsp_last_error().decode()
+    if rc == VSP_EINVAL:
+        raise VspError(msg)
+    raise VspRuntimeError(msg)
+
+
+_ctx: dict = {}
+
+
+def _context(device: torch.device):
+    lib = load_library()
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _ctx:
+        h = ctypes.c_void_p()
+        _check(lib.vsp_create(ctypes.byref(h), idx))
+        _ctx[idx] = h
+    return _ctx[idx]
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    key = (str(device), "ws")
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def _need_cuda(*ts: torch.Tensor):
+    for t in ts:
+        if not t.is_cuda:
+            raise VspRuntimeError("vsp: tensors must live on an sm_100 CUDA device (no CPU fallback)")
+
+
+# ---------------------------------------------------------------------- data types
+
+@dataclasses.dataclass
+class BudgetConfig:
+    """sparsity.hpp:22-36. max_budget None = no maximum."""
+    tau_v: float = 0.9
+    tau_s: float = 0.9
+    min_budget: int = 1
+    max_budget: Optional[int] = None
+
+    def _c(self) -> _Budget:
+        return _Budget(self.tau_v, self.tau_s, int(self.min_budget),
+                       -1 if self.max_budget is None else int(self.max_budget))
+
+
+@dataclasses.dataclass
+class IndexerParams:
+    """indexer.hpp:34-49, batched over KV heads. w_u [Hkv, 2d, d_h] bf16 (rows 0..d-1
+    multiply K, d..2d-1 multiply V), b_u/w_v/w_s [Hkv, d_h] fp32, b_v/b_s [Hkv] fp32."""
+    w_u: torch.Tensor
+    b_u: torch.Tensor
+    w_v: torch.Tensor
+    b_v: torch.Tensor
+    w_s: torch.Tensor
+    b_s: torch.Tensor
+
+    @property
+    def d_h(self) -> int:
+        return self.w_u.shape[2]
+
+
+@dataclasses.dataclass
+class SelectedIndices:
+    """sparsity.hpp:38-46, batched: i_v/i_s [Hkv, cap] int32, k_v/k_s [Hkv] int32."""
+    i_v: torch.Tensor
+    k_v: torch.Tensor
+    i_s: torch.Tensor
+    k_s: torch.Tensor
+
+    def lists(self, g: int):
+        kv, ks = int(self.k_v[g]), int(self.k_s[g])
+        return self.i_v[g, :kv].cpu().tolist(), self.i_s[g, :ks].cpu().tolist()
+
+
+def make_indexer_params(hkv: int, d: int, d_h: int, generator: torch.Generator, head_sigma: float = 0.0,
+                        device="cuda") -> IndexerParams:
+    """make_indexer_params (indexer.hpp:53-64) batched: W_U ~ U(+-1/sqrt(2d)); heads zero
+    (exactly uniform scores) unless head_sigma > 0 (heads ~ N(0, sigma^2))."""
+    lim = 1.0 / math.sqrt(2 * d)
+    w_u = (torch.rand(hkv, 2 * d, d_h, generator=generator) * 2 - 1) * lim
+    w_v = torch.randn(hkv, d_h, generator=generator) * head_sigma
+    w_s = torch.randn(hkv, d_h, generator=generator) * head_sigma
+    z = torch.zeros(hkv, d_h)
+    return IndexerParams(w_u.to(device=device, dtype=torch.bfloat16), z.to(device), w_v.to(device),
+                         torch.zeros(hkv, device=device), w_s.to(device), torch.zeros(hkv, device=device))
+
+
+# ---------------------------------------------------------------------- operators
+
+def indexer_forward(k: torch.Tensor, v: torch.Tensor, p: IndexerParams, mapping: str = "reverse",
+                    want_logits: bool = False):
+    """indexer_forward (indexer.hpp:116-120) for every KV head -> (A_v, A_s) [Hkv, n] fp32
+    (+ logits_v, logits_s when want_logits)."""
+    _need_cuda(k, v)
+    n, hkv, d = k.shape
+    lib = load_library()
+    dev = k.device
+    a_v = torch.empty(hkv, n, device=dev, dtype=torch.float32)
+    a_s = torch.empty_like(a_v)
+    lv = torch.empty_like(a_v) if want_logits else None
+    ls = torch.empty_like(a_v) if want_logits else None
+    ws = _workspace(dev, lib.vsp_indexer_workspace_size(n, hkv, p.d_h))
+    _check(lib.vsp_indexer_scores(_context(dev), _ptr(k), _ptr(v), n, hkv, d, p.d_h, _ptr(p.w_u), _ptr(p.b_u),
+                                  _ptr(p.w_v), _ptr(p.b_v), _ptr(p.w_s), _ptr(p.b_s),
+                                  0 if mapping == "reverse" else 1, _ptr(a_v), _ptr(a_s), _ptr(lv), _ptr(ls),
+                                  _ptr(ws), _stream(dev)))
+    return (a_v, a_s, lv, ls) if want_logits else (a_v, a_s)
+
+
+def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget) -> SelectedIndices:
+    """select_pattern (sparsity.hpp:105-114) per KV head. budget: BudgetConfig or a list of
+    them (one per KV head, e.g. per-layer/per-head budgets)."""
+    _need_cuda(a_v, a_s)
+    hkv, n = a_v.shape
+    budgets = list(budget) if isinstance(budget, (list, tuple)) else [budget] * hkv
+    arr = (_Budget * hkv)(*[b._c() for b in budgets])
+    lib = load_library()
+    dev = a_v.device
+    cap = n + 1
+    i_v = torch.empty(hkv, cap, device=dev, dtype=torch.int32)
+    i_s = torch.empty_like(i_v)
+    k_v = torch.empty(hkv, device=dev, dtype=torch.int32)
+    k_s = torch.empty_like(k_v)
+    ws = _workspace(dev, lib.vsp_select_workspace_size(n, hkv))
+    _check(lib.vsp_select(_context(dev), _ptr(a_v.contiguous()), _ptr(a_s.contiguous()), n, hkv, arr, _ptr(i_v),
+                          _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(ws), _stream(dev)))
+    return SelectedIndices(i_v, k_v, i_s, k_s)
+
+
+def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern: SelectedIndices,
+                     validate: bool = True, out: Optional[torch.Tensor] = None,
+                     lse: Optional[torch.Tensor] = None):
+    """sparse_attention (attention.hpp:150-194) for every Q head -> (O [n, Hq, d] bf16,
+    LSE [Hq, n] fp32). validate=True reproduces the reference's checks and messages
+    (merge.hpp:21-26, attention.hpp:161-163) at the cost of one stream sync."""
+    _need_cuda(q, k, v)
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    lib = load_library()
+    dev = q.device
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
+    cap = pattern.i_v.shape[1]
+    ws = _workspace(dev, lib.vsp_vs_attn_workspace_size(n, hkv, cap))
+    _check(lib.vsp_vs_attn_fwd(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, _ptr(pattern.i_v),
+                               _ptr(pattern.k_v), _ptr(pattern.i_s), _ptr(pattern.k_s), cap,
+                               1.0 / math.sqrt(d), _ptr(o), _ptr(lse), _ptr(ws), 1 if validate else 0,
+                               _stream(dev)))
+    return o, lse
+
+
+def blockwise_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: Optional[torch.Tensor] = None,
+                        lse: Optional[torch.Tensor] = None):
+    """blockwise_attention (attention.hpp:96-145): dense causal, every Q head."""
+    _need_cuda(q, k, v)
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    lib = load_library()
+    dev = q.device
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
+    _check(lib.vsp_dense_attn_fwd(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, 1.0 / math.sqrt(d),
+                                  _ptr(o), _ptr(lse), _stream(dev)))
+    return o, lse
+
+
+def aggregate_streaming(q: torch.Tensor, k: torch.Tensor, lse: Optional[torch.Tensor] = None,
+                        reduce: str = "mean", normalized: bool = True):
+    """aggregate_streaming (vsaggregate.hpp:62-127) for every Q head, group-reduced per KV
+    head with combine_scores (vsaggregate.hpp:133-157) -> (A_v, A_s) [Hkv, n] fp32."""
+    _need_cuda(q, k)
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    lib = load_library()
+    dev = q.device
+    a_v = torch.empty(hkv, n, device=dev, dtype=torch.float32)
+    a_s = torch.empty_like(a_v)
+    ws = _workspace(dev, lib.vsp_aggregate_workspace_size(n, hq))
+    _check(lib.vsp_vs_aggregate(_context(dev), _ptr(q), _ptr(k), n, hq, hkv, d, 1.0 / math.sqrt(d), _ptr(lse),
+                                0 if reduce == "mean" else 1, int(normalized), _ptr(a_v), _ptr(a_s), _ptr(ws),
+                                _stream(dev)))
+    return a_v, a_s
+
+
+def attention_recall(lse_sparse: torch.Tensor, lse_dense: torch.Tensor) -> torch.Tensor:
+    """attention_recall (attention.hpp:198-215) without the n x n matrix: row i's covered
+    mass is exp(LSE_sparse_i - LSE_dense_i). Returns recall per Q head [Hq] fp32."""
+    _need_cuda(lse_sparse, lse_dense)
+    hq, n = lse_sparse.shape
+    dev = lse_sparse.device
+    out = torch.empty(hq, device=dev, dtype=torch.float32)
+    _check(load_library().vsp_recall_from_lse(_context(dev), _ptr(lse_sparse), _ptr(lse_dense), n, hq, _ptr(out),
+                                              _stream(dev)))
+    return out
+
+
+def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
+               mapping: str = "reverse"):
+    """The whole VS-prefill hot path of one layer: indexer -> selection -> sparse attention.
+    Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
+    Returns (O, LSE, SelectedIndices)."""
+    a_v, a_s = indexer_forward(k, v, params, mapping)
+    pat = select_pattern(a_v, a_s, budget)
+    o, lse = sparse_attention(q, k, v, pat, validate=False)
+    return o, lse, pat

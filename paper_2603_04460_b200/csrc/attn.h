@@ -1,0 +1,50 @@
+// attn.h — internal launch interface of the attention kernels (K3 sparse, K4 dense).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "tma_host.h"
+
+namespace vsp_attn {
+
+struct __align__(64) AttnParams {
+    CUtensorMap map_q;   // [n, hq, 128] bf16, box {64, 1, 128}
+    CUtensorMap map_k;   // [n, hkv, 128]
+    CUtensorMap map_v;
+    CUtensorMap map_kv;  // gathered verticals [hkv, kvcap, 128], box {64, 128, 1}
+    CUtensorMap map_vv;
+    __nv_bfloat16* o;    // [n, hq, 128]
+    float* lse;          // [hq, n] or null
+    const int* tile_lists;
+    const uint32_t* vbits;
+    const uint32_t* sbits;
+    int list_stride;
+    int bm_words;
+    int n, hq, hkv;
+    float scale;
+};
+
+struct AttnArgs {
+    const void* q;  // [n, hq, 128] bf16
+    const void* k;  // [n, hkv, 128] bf16
+    const void* v;  // [n, hkv, 128] bf16
+    void* o;        // [n, hq, 128] bf16
+    float* lse;     // [hq, n] fp32, may be null
+    int n, hq, hkv;
+    float scale;
+};
+
+struct SparseArgs {
+    const int* iv;  // [hkv, cap] ascending column indices
+    const int* kv;  // [hkv] counts
+    const int* is;  // [hkv, cap] ascending slash offsets
+    const int* ks;  // [hkv]
+    int cap;
+};
+
+cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream);
+size_t sparse_workspace_bytes(int n, int hkv, int cap);
+cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream);
+
+}  // namespace vsp_attn

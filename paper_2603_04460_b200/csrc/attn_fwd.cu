@@ -1,0 +1,588 @@
+// attn_fwd.cu — K4 dense causal attention and K3 vertical-slash sparse attention on
+// sm_100a (tcgen05 + TMEM + TMA), one shared pipeline.
+//
+// Replaces, per Q head:
+//   vsp::blockwise_attention  (reference attention.hpp:96-145)   -> dense mode
+//   vsp::sparse_attention     (reference attention.hpp:150-194) + merge_row_columns
+//                             (merge.hpp:18-56)                  -> sparse mode
+//
+// CTA = one 128-row query block x TWO Q heads of the same KV group (GQA: both Q tiles
+// share every K/V tile). 12 warps:
+//   warp 0      TMA producer (Q once, then K/V tiles through a ring)
+//   warp 1      MMA issuer: S_h = Q_h K^T (SS), O_h += P_h V (TS, P read from TMEM)
+//   warps 4-7   softmax/epilogue for Q tile 0 (thread = query row = TMEM lane)
+//   warps 8-11  softmax/epilogue for Q tile 1
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_h (bf16) aliases
+// the first 64 columns of S_h. The MMA order PV_h(j-1) -> S_h(j) keeps the alias safe
+// because tcgen05.mma executes in issue order; the S_full commit after S_h(j) therefore
+// also proves PV_h(j-1) finished, which is when the softmax warps may rescale O_h.
+// Online softmax runs in the exp2 domain with lazy rescaling (only when the running max
+// grows by more than 2^8), exactly the same math as the reference's per-row rescale.
+//
+// Sparse mode: per (KV head, query block) a tile list built by vs_plan_kernel. Entry
+// e >= 0 is a "slash span" tile: K/V rows [e, e+128) of the original tensors, element
+// mask (i-j) in I_s  AND  j not in I_v  AND  j <= i  (from n-bit bitmaps). Entry e < 0
+// is gathered vertical tile t = -e-1: rows [128t, 128t+128) of K[I_v], V[I_v] (gathered
+// once per head), mask r < #{I_v <= i}. Every covered (i, j) pair is visited exactly once,
+// which is the reference's duplicate-free per-row union.
+#include <cuda_bf16.h>
+
+#include "attn.h"
+#include "sm100.cuh"
+
+using namespace vsp_sm100;
+
+namespace vsp_attn {
+
+constexpr int kBlock = 128;     // query rows per tile and key rows per tile
+constexpr int kHeadDim = 128;
+constexpr int kNumK = 2;        // K smem stages
+constexpr int kNumV = 2;        // V smem stages
+constexpr int kTileBytes = kBlock * kHeadDim * 2;   // 32 KB (two 16 KB d-halves)
+constexpr int kHalfBytes = kTileBytes / 2;
+constexpr int kSmemBytes = (2 + kNumK + kNumV) * kTileBytes + 1024;
+constexpr int kThreads = 384;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct Smem {
+    uint64_t bar_q;
+    uint64_t k_full[kNumK], k_empty[kNumK];
+    uint64_t v_full[kNumV], v_empty[kNumV];
+    uint64_t s_full[2], p_full[2], o_done[2];
+    uint32_t tmem_base;
+};
+
+// Bits [start, start+128) of a bitmap as four words, word k bit b <-> bit start+32k+b.
+// Bits below 0 and at/above nbits are zero (bitmaps are padded by one zero word).
+VSP_DEVICE void window128(const uint32_t* __restrict__ bm, int start, int nwords, uint32_t (&w)[4]) {
+    const int ws = start >> 5;  // floor division (arithmetic shift)
+    const uint32_t sh = static_cast<uint32_t>(start) & 31u;
+    uint32_t raw[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int idx = ws + k;
+        raw[k] = (idx >= 0 && idx < nwords) ? __ldg(bm + idx) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = __funnelshift_r(raw[k], raw[k + 1], sh);
+}
+
+template <bool kSparse>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = base;                                  // 2 tiles
+    uint8_t* sK = base + 2 * kTileBytes;                 // kNumK tiles
+    uint8_t* sV = sK + kNumK * kTileBytes;               // kNumV tiles
+    __shared__ Smem sm;
+
+    const int heads_per_pair = p.hq / 2;
+    const int num_qb = (p.n + kBlock - 1) / kBlock;
+    // heaviest query blocks first (causal work grows with the block index)
+    const int qb = num_qb - 1 - static_cast<int>(blockIdx.x) / heads_per_pair;
+    const int pair = static_cast<int>(blockIdx.x) % heads_per_pair;
+    const int h0 = 2 * pair;
+    const int g = h0 / (p.hq / p.hkv);
+    const int i0 = qb * kBlock;
+
+    // ---- tile list
+    int num_tiles;
+    const int* tiles = nullptr;
+    int vcnt0 = 0;
+    if constexpr (kSparse) {
+        const int* hdr = p.tile_lists + (static_cast<size_t>(g) * num_qb + qb) * p.list_stride;
+        num_tiles = hdr[0];
+        vcnt0 = hdr[1];
+        tiles = hdr + 2;
+    } else {
+        num_tiles = qb + 1;
+    }
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(&sm.bar_q, 1);
+        for (int s = 0; s < kNumK; ++s) {
+            mbar_init(&sm.k_full[s], 1);
+            mbar_init(&sm.k_empty[s], 1);
+        }
+        for (int s = 0; s < kNumV; ++s) {
+            mbar_init(&sm.v_full[s], 1);
+            mbar_init(&sm.v_empty[s], 1);
+        }
+        for (int w = 0; w < 2; ++w) {
+            mbar_init(&sm.s_full[w], 1);
+            mbar_init(&sm.p_full[w], 4);
+            mbar_init(&sm.o_done[w], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        // =========================== TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&p.map_q);
+            tma_prefetch_desc(&p.map_k);
+            tma_prefetch_desc(&p.map_v);
+            if constexpr (kSparse) {
+                tma_prefetch_desc(&p.map_kv);
+                tma_prefetch_desc(&p.map_vv);
+            }
+            mbar_arrive_expect_tx(&sm.bar_q, 2 * kTileBytes);
+            for (int w = 0; w < 2; ++w)
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(sQ + w * kTileBytes + hf * kHalfBytes, &p.map_q, &sm.bar_q, hf * 64,
+                                h0 + w, i0);
+            for (int j = 0; j < num_tiles; ++j) {
+                int e = kSparse ? __ldg(tiles + j) : j * kBlock;
+                const bool gathered = kSparse && e < 0;
+                const int row = gathered ? (-e - 1) * kBlock : e;
+                const int ks = j % kNumK;
+                if (j >= kNumK) mbar_wait(&sm.k_empty[ks], ((j / kNumK) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
+                for (int hf = 0; hf < 2; ++hf) {
+                    if (gathered)
+                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, &p.map_kv, &sm.k_full[ks],
+                                    hf * 64, row, g);
+                    else
+                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, &p.map_k, &sm.k_full[ks],
+                                    hf * 64, g, row);
+                }
+                const int vs = j % kNumV;
+                if (j >= kNumV) mbar_wait(&sm.v_empty[vs], ((j / kNumV) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
+                for (int hf = 0; hf < 2; ++hf) {
+                    if (gathered)
+                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, &p.map_vv, &sm.v_full[vs],
+                                    hf * 64, row, g);
+                    else
+                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, &p.map_v, &sm.v_full[vs],
+                                    hf * 64, g, row);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // =========================== MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(128, 128, false, true);
+            const uint32_t q_addr = smem_u32(sQ);
+            const uint32_t k_addr = smem_u32(sK);
+            const uint32_t v_addr = smem_u32(sV);
+            auto issue_pv = [&](int w, int jj) {
+                const int vs = jj % kNumV;
+                const uint32_t o_t = tmem + 256 + w * 128;
+                const uint32_t p_t = tmem + w * 128;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint64_t bdesc = umma_desc_sw128(v_addr + vs * kTileBytes + k * 2048, kHalfBytes, 1024);
+                    umma_ts(o_t, p_t + k * 8, bdesc, idesc_pv, (jj > 0 || k > 0) ? 1u : 0u);
+                }
+            };
+            auto issue_s = [&](int w, int jj) {
+                const int ks = jj % kNumK;
+                const uint32_t s_t = tmem + w * 128;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
+                    const uint64_t adesc = umma_desc_sw128(q_addr + w * kTileBytes + off, 16, 1024);
+                    const uint64_t bdesc = umma_desc_sw128(k_addr + ks * kTileBytes + off, 16, 1024);
+                    umma_ss(s_t, adesc, bdesc, idesc_qk, k > 0 ? 1u : 0u);
+                }
+            };
+            mbar_wait(&sm.bar_q, 0);
+            if (num_tiles == 0) {  // nothing covered: release the epilogue
+                umma_commit(&sm.o_done[0]);
+                umma_commit(&sm.o_done[1]);
+            }
+            for (int j = 0; j < num_tiles; ++j) {
+                const int ks = j % kNumK;
+                mbar_wait(&sm.k_full[ks], (j / kNumK) & 1);
+                tc_fence_after();
+                for (int w = 0; w < 2; ++w) {
+                    if (j > 0) {
+                        mbar_wait(&sm.p_full[w], (j - 1) & 1);
+                        if (w == 0) mbar_wait(&sm.v_full[(j - 1) % kNumV], ((j - 1) / kNumV) & 1);
+                        tc_fence_after();
+                        issue_pv(w, j - 1);
+                        if (w == 1) umma_commit(&sm.v_empty[(j - 1) % kNumV]);
+                    }
+                    issue_s(w, j);
+                    umma_commit(&sm.s_full[w]);
+                }
+                umma_commit(&sm.k_empty[ks]);
+            }
+            const int jl = num_tiles - 1;
+            for (int w = 0; w < 2 && num_tiles > 0; ++w) {
+                mbar_wait(&sm.p_full[w], jl & 1);
+                if (w == 0) mbar_wait(&sm.v_full[jl % kNumV], (jl / kNumV) & 1);
+                tc_fence_after();
+                issue_pv(w, jl);
+                umma_commit(&sm.o_done[w]);
+            }
+        }
+    } else if (warp >= 4) {
+        // =========================== softmax + epilogue
+        const int w = (warp - 4) >> 2;             // Q tile / head within the pair
+        const int quarter = warp & 3;              // TMEM lane quarter
+        const int r = quarter * 32 + lane;         // row within the block
+        const int i = i0 + r;                      // query row
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const uint32_t s_t = lane_base + w * 128;
+        const uint32_t o_t = lane_base + 256 + w * 128;
+        const float sl2 = p.scale * kLog2e;
+
+        // sparse: #{I_v <= i} = vcnt0 + popcount(vbits over [i0, i])
+        int vcnt_i = 0;
+        if constexpr (kSparse) {
+            uint32_t vw[4];
+            window128(p.vbits + static_cast<size_t>(g) * p.bm_words, i0, p.bm_words, vw);
+            int c = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int lo = 32 * k;
+                if (r >= lo + 31) c += __popc(vw[k]);
+                else if (r >= lo) c += __popc(vw[k] & (0xffffffffu >> (31 - (r - lo))));
+            }
+            vcnt_i = vcnt0 + c;
+        }
+
+        float m_used = -INFINITY;
+        float l = 0.f;
+        for (int j = 0; j < num_tiles; ++j) {
+            // ---- mask for this tile: bit c of mk[c>>5] = column allowed
+            uint32_t mk[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+            bool masked = false;
+            if constexpr (kSparse) {
+                const int e = __ldg(tiles + j);
+                if (e < 0) {
+                    const int lim = vcnt_i - (-e - 1) * kBlock;  // allowed gathered rows: c < lim
+                    if (lim < kBlock) {
+                        masked = true;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int b = lim - 32 * k;
+                            mk[k] = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
+                        }
+                    }
+                } else {
+                    masked = true;
+                    uint32_t vw[4], sw[4];
+                    window128(p.vbits + static_cast<size_t>(g) * p.bm_words, e, p.bm_words, vw);
+                    window128(p.sbits + static_cast<size_t>(g) * p.bm_words, i - e - 127, p.bm_words, sw);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) mk[k] = __brev(sw[3 - k]) & ~vw[k];
+                }
+            } else {
+                if (j == qb) {  // diagonal tile: c <= r
+                    masked = true;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int b = r - 32 * k + 1;
+                        mk[k] = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
+                    }
+                }
+            }
+
+            mbar_wait(&sm.s_full[w], j & 1);
+            tc_fence_after();
+            float x[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t u[32];
+                tmem_ld32(s_t + c * 32, u);
+                tmem_wait_ld();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) x[c * 32 + t] = __uint_as_float(u[t]) * sl2;
+            }
+            if (masked) {
+#pragma unroll
+                for (int c = 0; c < 128; ++c)
+                    if (!((mk[c >> 5] >> (c & 31)) & 1u)) x[c] = -INFINITY;
+            }
+            float mx = x[0];
+#pragma unroll
+            for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
+            const float m_new = fmaxf(m_used, mx);
+            const bool need = (m_used == -INFINITY) ? (m_new > -INFINITY) : (m_new > m_used + kRescaleThreshold);
+            if (__any_sync(0xffffffffu, need)) {
+                const float m_next = need ? m_new : m_used;
+                const float f = (m_used == -INFINITY) ? 0.f : ex2_approx(m_used - m_next);
+                l *= f;
+                m_used = m_next;
+                if (j > 0) {  // O holds PV(0..j-1); PV(j-1) is complete (see header)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t u[32];
+                        tmem_ld32(o_t + c * 32, u);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) u[t] = __float_as_uint(__uint_as_float(u[t]) * f);
+                        tmem_st32(o_t + c * 32, u);
+                    }
+                }
+            }
+            const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const float a = ex2_approx(x[c * 64 + 2 * t] - m_eff);
+                    const float b = ex2_approx(x[c * 64 + 2 * t + 1] - m_eff);
+                    l += a + b;
+                    pk[t] = pack_bf16x2(a, b);
+                }
+                tmem_st32(s_t + c * 32, pk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full[w]);
+        }
+
+        // ---- epilogue: O / l -> bf16 [n, Hq, d]; LSE (natural log of sum exp(scaled logits))
+        mbar_wait(&sm.o_done[w], 0);
+        tc_fence_after();
+        const int h = h0 + w;
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = p.o + (static_cast<size_t>(i) * p.hq + h) * kHeadDim;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t u[32];
+            tmem_ld32(o_t + c * 32, u);
+            tmem_wait_ld();
+            if (num_tiles == 0) {
+#pragma unroll
+                for (int t = 0; t < 32; ++t) u[t] = 0u;
+            }
+            if (i < p.n) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    uint4 v;
+                    v.x = pack_bf16x2(__uint_as_float(u[8 * t + 0]) * inv_l, __uint_as_float(u[8 * t + 1]) * inv_l);
+                    v.y = pack_bf16x2(__uint_as_float(u[8 * t + 2]) * inv_l, __uint_as_float(u[8 * t + 3]) * inv_l);
+                    v.z = pack_bf16x2(__uint_as_float(u[8 * t + 4]) * inv_l, __uint_as_float(u[8 * t + 5]) * inv_l);
+                    v.w = pack_bf16x2(__uint_as_float(u[8 * t + 6]) * inv_l, __uint_as_float(u[8 * t + 7]) * inv_l);
+                    dst[t] = v;
+                }
+            }
+        }
+        if (i < p.n && p.lse != nullptr)
+            p.lse[static_cast<size_t>(h) * p.n + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_free<512>(tmem);
+}
+
+// ------------------------------------------------------------------ sparse planning
+
+// Bitmaps (bit j of vbits[g] <=> j in I_v[g]; bit o of sbits[g] <=> o in I_s[g]).
+// Caller zeroes them first. grid (ceil(cap/256), hkv).
+__global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
+                                     const int* __restrict__ is, const int* __restrict__ ks, int cap,
+                                     int n, int bm_words, uint32_t* vbits, uint32_t* sbits) {
+    const int g = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < kv[g]) {
+        const int j = iv[static_cast<size_t>(g) * cap + t];
+        if (j >= 0 && j < n)  // columns >= n are never reached by any row (j <= i < n)
+            atomicOr(vbits + static_cast<size_t>(g) * bm_words + (j >> 5), 1u << (j & 31));
+    }
+    if (t < ks[g]) {
+        const int o = is[static_cast<size_t>(g) * cap + t];
+        if (o >= 0 && o < n)
+            atomicOr(sbits + static_cast<size_t>(g) * bm_words + (o >> 5), 1u << (o & 31));
+    }
+}
+
+// Kv[g][r] = K[I_v[g][r]][g], r < kvcap (rows >= k_v zero). grid (kvcap, hkv), 16 threads.
+__global__ void gather_vertical_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                                       const int* __restrict__ iv, const int* __restrict__ kv, int cap,
+                                       int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg) {
+    const int g = blockIdx.y;
+    const int r = blockIdx.x;
+    const int t = threadIdx.x;  // 16 x 16 B = 256 B = one row of d=128 bf16
+    uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+    if (r < kv[g]) {
+        const int j = min(max(iv[static_cast<size_t>(g) * cap + r], 0), n - 1);
+        a = reinterpret_cast<const uint4*>(k + (static_cast<size_t>(j) * hkv + g) * kHeadDim)[t];
+        b = reinterpret_cast<const uint4*>(v + (static_cast<size_t>(j) * hkv + g) * kHeadDim)[t];
+    }
+    reinterpret_cast<uint4*>(kg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = a;
+    reinterpret_cast<uint4*>(vg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = b;
+}
+
+VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Per (KV head g, query block qb): header {num_tiles, vcnt0} then entries (see file
+// header). Slash spans: for offsets o <= i_last (ascending I_s walked from the largest
+// offset down, i.e. ascending column start) the column intervals [max(0,i0-o), i_last-o]
+// are merged and covered greedily by disjoint 128-row tiles.
+__global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
+                               const int* __restrict__ is, const int* __restrict__ ks, int cap, int n,
+                               int num_qb, int list_stride, int* __restrict__ lists) {
+    const int g = blockIdx.y;
+    const int qb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qb >= num_qb) return;
+    const int i0 = qb * kBlock;
+    const int ilast = min(i0 + kBlock - 1, n - 1);
+    const int* ivg = iv + static_cast<size_t>(g) * cap;
+    const int* isg = is + static_cast<size_t>(g) * cap;
+    const int k_v = kv[g], k_s = ks[g];
+    int* out = lists + (static_cast<size_t>(g) * num_qb + qb) * list_stride;
+    int cnt = 0;
+    const int cv = upper_bound_i(ivg, k_v, ilast);
+    out[1] = upper_bound_i(ivg, k_v, i0 - 1);
+    const int ntv = (cv + kBlock - 1) / kBlock;
+    for (int t = 0; t < ntv; ++t) out[2 + cnt++] = -(t + 1);
+    int s = upper_bound_i(isg, k_s, ilast);
+    int cur = 0, a = -1, b = -1;
+    auto emit = [&](int lo, int hi) {
+        int st = max(lo, cur);
+        while (st <= hi) {
+            out[2 + cnt++] = st;
+            st += kBlock;
+        }
+        cur = max(cur, st);
+    };
+    for (int t = s - 1; t >= 0; --t) {
+        const int o = __ldg(isg + t);
+        const int lo = max(0, i0 - o), hi = ilast - o;
+        if (a < 0) {
+            a = lo;
+            b = hi;
+        } else if (lo <= b + 1) {
+            b = max(b, hi);
+        } else {
+            emit(a, b);
+            a = lo;
+            b = hi;
+        }
+    }
+    if (a >= 0) emit(a, b);
+    out[0] = cnt;
+}
+
+// ------------------------------------------------------------------ host launchers
+
+static bool make_qkv_maps(AttnParams& p, const void* q, const void* k, const void* v) {
+    const uint32_t box[3] = {64, 1, kBlock};
+    const uint64_t dq[3] = {kHeadDim, (uint64_t)p.hq, (uint64_t)p.n};
+    const uint64_t sq[2] = {kHeadDim * 2, (uint64_t)p.hq * kHeadDim * 2};
+    const uint64_t dk[3] = {kHeadDim, (uint64_t)p.hkv, (uint64_t)p.n};
+    const uint64_t sk[2] = {kHeadDim * 2, (uint64_t)p.hkv * kHeadDim * 2};
+    return vsp_host::make_map_bf16(&p.map_q, q, 3, dq, sq, box) &&
+           vsp_host::make_map_bf16(&p.map_k, k, 3, dk, sk, box) &&
+           vsp_host::make_map_bf16(&p.map_v, v, 3, dk, sk, box);
+}
+
+cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
+    AttnParams p{};
+    p.n = a.n;
+    p.hq = a.hq;
+    p.hkv = a.hkv;
+    p.scale = a.scale;
+    p.o = static_cast<__nv_bfloat16*>(a.o);
+    p.lse = a.lse;
+    if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(attn_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr_set = true;
+    }
+    const int num_qb = (a.n + kBlock - 1) / kBlock;
+    dim3 grid(num_qb * (a.hq / 2));
+    attn_fwd_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    return cudaGetLastError();
+}
+
+size_t sparse_workspace_bytes(int n, int hkv, int cap) {
+    const int num_qb = (n + kBlock - 1) / kBlock;
+    const int kvcap = ((cap + kBlock - 1) / kBlock) * kBlock;
+    const int bm_words = (n + 31) / 32 + 1;
+    const int list_stride = 2 + kvcap / kBlock + num_qb + 3;
+    size_t bytes = 0;
+    auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
+    add(static_cast<size_t>(hkv) * kvcap * kHeadDim * 2);  // Kv
+    add(static_cast<size_t>(hkv) * kvcap * kHeadDim * 2);  // Vv
+    add(static_cast<size_t>(hkv) * bm_words * 4 * 2);      // bitmaps
+    add(static_cast<size_t>(hkv) * num_qb * list_stride * 4);
+    return bytes;
+}
+
+cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream) {
+    AttnParams p{};
+    p.n = a.n;
+    p.hq = a.hq;
+    p.hkv = a.hkv;
+    p.scale = a.scale;
+    p.o = static_cast<__nv_bfloat16*>(a.o);
+    p.lse = a.lse;
+    if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
+    const int num_qb = (a.n + kBlock - 1) / kBlock;
+    const int kvcap = ((s.cap + kBlock - 1) / kBlock) * kBlock;
+    const int bm_words = (a.n + 31) / 32 + 1;
+    const int list_stride = 2 + kvcap / kBlock + num_qb + 3;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    auto take = [&](size_t b) {
+        uint8_t* r = ws;
+        ws += (b + 255) & ~size_t(255);
+        return r;
+    };
+    auto* kg = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(a.hkv) * kvcap * kHeadDim * 2));
+    auto* vg = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(a.hkv) * kvcap * kHeadDim * 2));
+    auto* bits = reinterpret_cast<uint32_t*>(take(static_cast<size_t>(a.hkv) * bm_words * 4 * 2));
+    auto* lists = reinterpret_cast<int*>(take(static_cast<size_t>(a.hkv) * num_qb * list_stride * 4));
+    p.vbits = bits;
+    p.sbits = bits + static_cast<size_t>(a.hkv) * bm_words;
+    p.bm_words = bm_words;
+    p.tile_lists = lists;
+    p.list_stride = list_stride;
+
+    const uint32_t box[3] = {64, kBlock, 1};
+    const uint64_t dg[3] = {kHeadDim, (uint64_t)kvcap, (uint64_t)a.hkv};
+    const uint64_t sg[2] = {kHeadDim * 2, (uint64_t)kvcap * kHeadDim * 2};
+    if (!vsp_host::make_map_bf16(&p.map_kv, kg, 3, dg, sg, box) ||
+        !vsp_host::make_map_bf16(&p.map_vv, vg, 3, dg, sg, box))
+        return cudaErrorInvalidValue;
+
+    cudaError_t e = cudaMemsetAsync(bits, 0, static_cast<size_t>(a.hkv) * bm_words * 4 * 2, stream);
+    if (e != cudaSuccess) return e;
+    build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, a.hkv), 256, 0, stream>>>(
+        s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words);
+    gather_vertical_kernel<<<dim3(kvcap, a.hkv), 16, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
+        a.n, a.hkv, kvcap, kg, vg);
+    vs_plan_kernel<<<dim3((num_qb + 127) / 128, a.hkv), 128, 0, stream>>>(
+        s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(attn_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr_set = true;
+    }
+    dim3 grid(num_qb * (a.hq / 2));
+    attn_fwd_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace vsp_attn

@@ -1,0 +1,255 @@
+// capi.cu — the C ABI (include/vsp_gpu.h): argument checks with the reference's error
+// texts, workspace sizing, and dispatch to the sm_100a kernels. No CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/vsp_gpu.h"
+#include "aggregate.h"
+#include "attn.h"
+#include "indexer.h"
+#include "select.h"
+
+struct vsp_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int* d_flags = nullptr;  // [1024] validation results
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_err(cudaError_t e, const char* where) {
+    return set_err(VSP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define VSP_CHECK_CTX(ctx)                                                         \
+    do {                                                                           \
+        if (!(ctx)) return set_err(VSP_EINVAL, "vsp: null context");               \
+        if (cudaSetDevice((ctx)->device) != cudaSuccess)                           \
+            return set_err(VSP_ECUDA, "vsp: cannot select device");                \
+    } while (0)
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Strict ascending order, non-negative entries, and row-0 coverage, per KV head.
+__global__ void validate_pattern_kernel(const int* iv, const int* kv, const int* is, const int* ks,
+                                        int cap, int* flags) {
+    const int g = blockIdx.x;
+    const int nv = kv[g], ns = ks[g];
+    const int* a = iv + static_cast<size_t>(g) * cap;
+    const int* b = is + static_cast<size_t>(g) * cap;
+    int f = 0;
+    for (int t = threadIdx.x; t < nv; t += blockDim.x) {
+        if (a[t] < 0) f |= 8;
+        if (t > 0 && !(a[t - 1] < a[t])) f |= 1;
+    }
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+        if (b[t] < 0) f |= 8;
+        if (t > 0 && !(b[t - 1] < b[t])) f |= 2;
+    }
+    if (threadIdx.x == 0) {
+        const bool covered0 = (nv > 0 && a[0] == 0) || (ns > 0 && b[0] == 0);
+        if (!covered0) f |= 4;
+        if (nv < 0 || ns < 0 || nv > cap || ns > cap) f |= 16;
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    __shared__ int acc;
+    if (threadIdx.x == 0) acc = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(&acc, f);
+    __syncthreads();
+    if (threadIdx.x == 0) flags[g] = acc;
+}
+
+__global__ void recall_kernel(const float* ls, const float* ld, int n, float* out) {
+    const int h = blockIdx.x;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const size_t x = static_cast<size_t>(h) * n + i;
+        acc += exp(static_cast<double>(ls[x]) - static_cast<double>(ld[x]));
+    }
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[h] = static_cast<float>(t / n);
+    }
+}
+
+int check_attn_shapes(int n, int hq, int hkv, int d) {
+    if (n < 1) return set_err(VSP_EINVAL, "attention inputs: empty sequence");
+    if (hkv < 1 || hq < hkv || hq % hkv != 0)
+        return set_err(VSP_EINVAL, "attention inputs: hq must be a positive multiple of hkv");
+    if ((hq / hkv) % 2 != 0)
+        return set_err(VSP_EINVAL, "vsp: GQA group size must be even (two Q heads per CTA)");
+    if (d != 128) return set_err(VSP_EINVAL, "vsp: head dim must be 128");
+    return VSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vsp_last_error(void) { return g_err.c_str(); }
+const char* vsp_version(void) { return "vsp-b200 0.1 (sm_100a)"; }
+
+int vsp_create(vsp_ctx** out, int device) {
+    if (!out) return set_err(VSP_EINVAL, "vsp_create: null output");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return set_err(VSP_ECUDA, "vsp_create: no CUDA device (the VS-prefill path has no CPU fallback)");
+    if (device < 0 || device >= count) return set_err(VSP_EINVAL, "vsp_create: bad device ordinal");
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_err(e, "vsp_create");
+    if (prop.major != 10)
+        return set_err(VSP_ECUDA, "vsp_create: an sm_100 (B200) device is required, got sm_" +
+                                      std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* ctx = new vsp_ctx();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    cudaSetDevice(device);
+    e = cudaMalloc(&ctx->d_flags, 1024 * sizeof(int));
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_err(e, "vsp_create");
+    }
+    *out = ctx;
+    return VSP_OK;
+}
+
+int vsp_destroy(vsp_ctx* ctx) {
+    if (!ctx) return VSP_OK;
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->d_flags);
+    delete ctx;
+    return VSP_OK;
+}
+
+// ------------------------------------------------------------------ attention
+int vsp_dense_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                       int hkv, int d, float scale, void* o, float* lse, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_attn_shapes(n, hq, hkv, d);
+    if (rc) return rc;
+    vsp_attn::AttnArgs a{q, k, v, o, lse, n, hq, hkv, scale};
+    cudaError_t e = vsp_attn::launch_dense(a, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_dense_attn_fwd");
+}
+
+size_t vsp_vs_attn_workspace_size(int n, int hkv, int cap) {
+    return vsp_attn::sparse_workspace_bytes(n, hkv, cap);
+}
+
+int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                    int hkv, int d, const int* i_v, const int* k_v, const int* i_s, const int* k_s,
+                    int cap, float scale, void* o, float* lse, void* workspace, int flags,
+                    void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_attn_shapes(n, hq, hkv, d);
+    if (rc) return rc;
+    if (cap < 1) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: cap must be >= 1");
+    if (!workspace) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: workspace required");
+    cudaStream_t st = as_stream(stream);
+    if (flags & VSP_VALIDATE) {
+        if (hkv > 1024) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: too many heads to validate");
+        validate_pattern_kernel<<<hkv, 256, 0, st>>>(i_v, k_v, i_s, k_s, cap, ctx->d_flags);
+        int hflags[1024];
+        cudaError_t e = cudaMemcpyAsync(hflags, ctx->d_flags, sizeof(int) * hkv, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_fwd(validate)");
+        for (int g = 0; g < hkv; ++g) {
+            // same precedence as the reference: merge_row_columns validates i_v, then i_s
+            // (merge.hpp:21-26), then sparse_attention reports the uncovered row (:161-163)
+            if (hflags[g] & 16) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: index count exceeds cap");
+            if (hflags[g] & 8) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: negative index");
+            if (hflags[g] & 1) return set_err(VSP_EINVAL, "merge_row_columns: i_v not strictly ascending");
+            if (hflags[g] & 2) return set_err(VSP_EINVAL, "merge_row_columns: i_s not strictly ascending");
+            if (hflags[g] & 4) return set_err(VSP_EINVAL, "uncovered query row 0");
+        }
+    }
+    vsp_attn::AttnArgs a{q, k, v, o, lse, n, hq, hkv, scale};
+    vsp_attn::SparseArgs s{i_v, k_v, i_s, k_s, cap};
+    cudaError_t e = vsp_attn::launch_sparse(a, s, workspace, st);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_attn_fwd");
+}
+
+int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n, int hq,
+                        float* recall_per_head, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (n < 1 || hq < 1) return set_err(VSP_EINVAL, "vsp_recall_from_lse: bad shape");
+    recall_kernel<<<hq, 512, 0, as_stream(stream)>>>(lse_sparse, lse_dense, n, recall_per_head);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_recall_from_lse");
+}
+
+// ------------------------------------------------------------------ indexer
+size_t vsp_indexer_workspace_size(int n, int hkv, int d_h) { return vsp_indexer::workspace_bytes(n, hkv, d_h); }
+
+int vsp_indexer_scores(vsp_ctx* ctx, const void* k, const void* v, int n, int hkv, int d, int d_h,
+                       const void* w_u, const float* b_u, const float* w_v, const float* b_v,
+                       const float* w_s, const float* b_s, int slash_mapping, float* a_v, float* a_s,
+                       float* logits_v, float* logits_s, void* workspace, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (n < 1) return set_err(VSP_EINVAL, "indexer_forward: empty input");
+    if (d != 128) return set_err(VSP_EINVAL, "vsp: head dim must be 128");
+    if (d_h < 1 || d_h % 256 != 0) return set_err(VSP_EINVAL, "vsp_indexer_scores: d_h must be a multiple of 256");
+    if (slash_mapping != VSP_SLASH_REVERSE && slash_mapping != VSP_SLASH_IDENTITY)
+        return set_err(VSP_EINVAL, "vsp_indexer_scores: bad slash mapping");
+    if (!workspace) return set_err(VSP_EINVAL, "vsp_indexer_scores: workspace required");
+    vsp_indexer::Args a{k, v, n, hkv, d_h, w_u, b_u, w_v, b_v, w_s, b_s,
+                        slash_mapping == VSP_SLASH_REVERSE, a_v, a_s, logits_v, logits_s};
+    cudaError_t e = vsp_indexer::launch(a, workspace, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_indexer_scores");
+}
+
+// ------------------------------------------------------------------ selection
+size_t vsp_select_workspace_size(int n, int hkv) { return vsp_select_k::workspace_bytes(n, hkv); }
+
+int vsp_select(vsp_ctx* ctx, const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets,
+               int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* workspace, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (n < 1) return set_err(VSP_EINVAL, "cumulative_budget: empty scores");
+    if (cap < n + 1) return set_err(VSP_EINVAL, "vsp_select: cap must be >= n + 1");
+    if (!budgets) return set_err(VSP_EINVAL, "vsp_select: null budgets");
+    for (int g = 0; g < hkv; ++g) {  // BudgetConfig::check (sparsity.hpp:27-35)
+        const vsp_budget& b = budgets[g];
+        if (!(b.tau_v > 0.0 && b.tau_v <= 1.0)) return set_err(VSP_EINVAL, "budget config: tau_v must be in (0, 1]");
+        if (!(b.tau_s > 0.0 && b.tau_s <= 1.0)) return set_err(VSP_EINVAL, "budget config: tau_s must be in (0, 1]");
+        if (b.min_budget < 1) return set_err(VSP_EINVAL, "budget config: min_budget must be >= 1");
+        if (b.max_budget >= 0 && b.min_budget > b.max_budget)
+            return set_err(VSP_EINVAL, "budget config: min_budget exceeds max_budget");
+    }
+    if (!workspace) return set_err(VSP_EINVAL, "vsp_select: workspace required");
+    cudaError_t e = vsp_select_k::launch(a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, workspace,
+                                          as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_select");
+}
+
+// ------------------------------------------------------------------ aggregation
+size_t vsp_aggregate_workspace_size(int n, int hq) { return vsp_aggregate::workspace_bytes(n, hq); }
+
+int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, int hq, int hkv, int d, float scale,
+                     const float* lse, int reduce, int normalized, float* a_v, float* a_s, void* workspace,
+                     void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_attn_shapes(n, hq, hkv, d);
+    if (rc) return rc;
+    if (reduce != VSP_REDUCE_MEAN && reduce != VSP_REDUCE_SUM)
+        return set_err(VSP_EINVAL, "vsp_vs_aggregate: bad reduce");
+    if (!workspace) return set_err(VSP_EINVAL, "vsp_vs_aggregate: workspace required");
+    vsp_aggregate::Args a{q, k, n, hq, hkv, scale, lse, reduce == VSP_REDUCE_MEAN, normalized != 0, a_v, a_s};
+    cudaError_t e = vsp_aggregate::launch(a, workspace, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_aggregate");
+}
+
+}  // extern "C"

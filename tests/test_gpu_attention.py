@@ -1,0 +1,138 @@
+"""GPU parity of K4 (dense causal) and K3 (VS sparse) attention vs the f64 oracle.
+
+Mirrors the reference's attention tests (tests/test_attention.cpp) at bf16/fp32 precision:
+  FullVerticalEqualsFull :118-127, MatchesMaskedSoftmaxOracle :129-143,
+  BlockSizeIrrelevant :145-155, UncoveredRowThrows :157-170,
+  BlockwiseAttention.EquivalentToFullAcrossSizes :99-109, SPEC.md:153 (I_s={0} -> O=V).
+Tolerances (stated): O max|d| <= 2e-2, mean|d| <= 2e-3, LSE max|d| <= 1e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+from helpers import (assert_attn_close, f64, oracle_dense, oracle_sparse, pattern_tensors, qkv)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vsp():
+    import paper_2603_04460_b200 as m
+    m.load_library()
+    return m
+
+
+@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (7, 4, 2), (128, 4, 1), (300, 4, 2), (512, 8, 2)])
+def test_dense_matches_oracle(vsp, n, hq, hkv):
+    q, k, v = qkv(n, hq, hkv, seed=n)
+    o, lse = vsp.blockwise_attention(q, k, v)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = oracle_dense(q, k, v)
+    assert_attn_close(o, lse, o_ref, lse_ref)
+
+
+def test_dense_long_vs_torch(vsp):
+    """n = 4096 (config 1 length), against torch fp32 SDPA on the same bf16 values."""
+    n, hq, hkv = 4096, 8, 2
+    q, k, v = qkv(n, hq, hkv, seed=7)
+    o, lse = vsp.blockwise_attention(q, k, v)
+    qf = q.float().permute(1, 0, 2)
+    kf = k.float().repeat_interleave(hq // hkv, dim=1).permute(1, 0, 2)
+    vf = v.float().repeat_interleave(hq // hkv, dim=1).permute(1, 0, 2)
+    ref = torch.nn.functional.scaled_dot_product_attention(qf, kf, vf, is_causal=True).permute(1, 0, 2)
+    err = (o.float() - ref).abs()
+    assert err.max().item() <= 2e-2 and err.mean().item() <= 2e-3
+    s = (qf @ kf.transpose(1, 2)) / np.sqrt(128)
+    s = s.masked_fill(torch.triu(torch.ones(n, n, dtype=torch.bool, device=s.device), 1), float("-inf"))
+    lse_ref = torch.logsumexp(s, dim=-1)
+    assert (lse - lse_ref).abs().max().item() <= 1e-3
+
+
+def _random_pattern(rng, n, kv, ks):
+    iv = sorted(rng.choice(n, size=min(kv, n), replace=False).tolist())
+    is_ = sorted(set(rng.choice(n, size=min(ks, n), replace=False).tolist()) | {0})
+    return iv, is_
+
+
+@pytest.mark.parametrize("n,hq,hkv,kv,ks", [(64, 2, 1, 5, 4), (300, 4, 2, 20, 12), (512, 4, 1, 40, 30),
+                                            (700, 8, 2, 100, 60)])
+def test_sparse_matches_masked_oracle(vsp, n, hq, hkv, kv, ks):
+    rng = np.random.default_rng(n)
+    q, k, v = qkv(n, hq, hkv, seed=n + 1)
+    lists = [_random_pattern(rng, n, kv, ks) for _ in range(hkv)]
+    o, lse = vsp.sparse_attention(q, k, v, pattern_tensors(lists, n))
+    torch.cuda.synchronize()
+    o_ref, lse_ref = oracle_sparse(q, k, v, lists)
+    assert_attn_close(o, lse, o_ref, lse_ref)
+
+
+def test_sparse_clustered_offsets(vsp):
+    """Local band + periodic offsets (the structured case the speed claim rests on)."""
+    n, hq, hkv = 1024, 4, 1
+    q, k, v = qkv(n, hq, hkv, seed=3)
+    is_ = sorted(set(range(0, 64)) | set(range(256, 300)) | {511, 700})
+    iv = [0, 1, 2, 3, 100, 101, 500, 900]
+    o, lse = vsp.sparse_attention(q, k, v, pattern_tensors([(iv, is_)], n))
+    o_ref, lse_ref = oracle_sparse(q, k, v, [(iv, is_)])
+    assert_attn_close(o, lse, o_ref, lse_ref)
+
+
+def test_full_vertical_equals_dense(vsp):
+    n, hq, hkv = 384, 4, 1
+    q, k, v = qkv(n, hq, hkv, seed=11)
+    o_s, lse_s = vsp.sparse_attention(q, k, v, pattern_tensors([(list(range(n)), [0])], n))
+    o_d, lse_d = vsp.blockwise_attention(q, k, v)
+    assert (o_s.float() - o_d.float()).abs().max().item() <= 1e-2
+    assert (lse_s - lse_d).abs().max().item() <= 1e-4
+
+
+def test_diagonal_only_returns_v(vsp):
+    """I_v = {}, I_s = {0}: every row attends only to itself -> O = V."""
+    n, hq, hkv = 200, 2, 1
+    q, k, v = qkv(n, hq, hkv, seed=5)
+    o, _ = vsp.sparse_attention(q, k, v, pattern_tensors([([], [0])], n))
+    for h in range(hq):
+        assert torch.equal(o[:, h], v[:, 0])
+
+
+def test_hand_pattern_block_irrelevant(vsp):
+    """test_attention.cpp:145-155 pattern; the GPU result is one fixed blocking."""
+    n, hq, hkv = 48, 2, 1
+    q, k, v = qkv(n, hq, hkv, seed=9)
+    lists = [([0, 3, 17, 39], [0, 2, 9])]
+    o, lse = vsp.sparse_attention(q, k, v, pattern_tensors(lists, n))
+    for block in (1, 7, 1000):
+        o_ref, lse_ref = oracle_sparse(q, k, v, lists, block=block)
+        assert_attn_close(o, lse, o_ref, lse_ref)
+
+
+def test_uncovered_row_raises(vsp):
+    n = 16
+    q, k, v = qkv(n, 2, 1, seed=1)
+    with pytest.raises(vsp.VspError, match="^uncovered query row 0$"):
+        vsp.sparse_attention(q, k, v, pattern_tensors([([5], [3])], n))
+
+
+def test_unsorted_raises(vsp):
+    n = 16
+    q, k, v = qkv(n, 2, 1, seed=1)
+    with pytest.raises(vsp.VspError, match="i_v not strictly ascending"):
+        vsp.sparse_attention(q, k, v, pattern_tensors([([3, 1], [0])], n))
+    with pytest.raises(vsp.VspError, match="i_s not strictly ascending"):
+        vsp.sparse_attention(q, k, v, pattern_tensors([([1], [0, 4, 4])], n))
+
+
+def test_recall_from_lse_matches_reference_recall(vsp):
+    import oracle
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    n, hq, hkv = 256, 2, 1
+    q, k, v = qkv(n, hq, hkv, seed=21)
+    lists = [([0, 5, 77], [0, 1, 2, 3, 40])]
+    _, lse_s = vsp.sparse_attention(q, k, v, pattern_tensors(lists, n))
+    _, lse_d = vsp.blockwise_attention(q, k, v)
+    rec = vsp.attention_recall(lse_s, lse_d).cpu().numpy()
+    qn, kn = f64(q), f64(k)
+    for h in range(hq):
+        ref = oracle.ref().attention_recall(qn[:, h], kn[:, 0], *lists[0])
+        assert abs(rec[h] - ref) <= 1e-3
