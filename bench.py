@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py — VS-prefill hot path on B200 (BASELINE.json config[2]).
+
+One step = one layer of the VS-prefill path on this rank's KV heads:
+    K1 indexer scores -> K2 adaptive selection -> K3 fused VS sparse attention
+at LLaMA-3.1-8B attention geometry (32 Q / 8 KV heads, d=128), n = 131072, synthetic
+planted-structure Q/K/V (paper_2603_04460_b200/synth.py), inputs resident in HBM
+(Q alone is 1.07 GB > the 126 MB L2, so no flush is needed between steps).
+
+Multi-GPU (torchrun, one rank per GPU): KV heads are sharded 8/N per rank with no
+collective on the data path; value = n / max-over-ranks step time
+(strong scaling: the layer is fixed, heads split). The NCCL all-gather that would
+assemble O is timed separately (`allgather_ms`), not inside the step.
+
+Extra keys: dense_ms / speedup_vs_dense (this build's own K4 dense causal kernel on the
+same heads), recall (mean_i exp(LSE_sparse - LSE_dense), attention.hpp:198-215 without
+the n x n matrix), element and tile density, roofline of K3, the reference CPU path on a
+bounded row-prefix sample (cpu_baseline), e2e through host buffers, clocks during timing.
+
+`--impl reference` runs the reference's own CPU implementation (oracle/_ref, the
+unmodified headers; the oracle port if that .so is absent) on the same workload sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "prefill attn tokens/s @128k LLaMA-8B geom, 1/2/4/8 B200; speedup vs own dense"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--d-h", type=int, default=1024)
+    ap.add_argument("--tau-v", type=float, default=0.9)
+    ap.add_argument("--tau-s", type=float, default=0.9)
+    ap.add_argument("--min-budget", type=int, default=1)
+    ap.add_argument("--max-budget", type=int, default=2048)
+    ap.add_argument("--head-sigma", type=float, default=0.3)
+    ap.add_argument("--seed", type=int, default=2026)
+    ap.add_argument("--cpu-sample", type=int, default=2048, help="row-prefix sample for the CPU reference")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def covered_pairs(pat, n: int, hkv: int) -> np.ndarray:
+    """Exact covered (i, j) pairs per KV head of a VS pattern:
+    sum_v (n - v) + sum_o (n - o) - #{(v, o): v + o < n} (vertical/slash overlap)."""
+    out = np.zeros(hkv, np.int64)
+    kv = pat.k_v.cpu().numpy()
+    ks = pat.k_s.cpu().numpy()
+    for g in range(hkv):
+        iv = pat.i_v[g, : kv[g]].long()
+        is_ = pat.i_s[g, : ks[g]].long()
+        iv = iv[iv < n]
+        is_ = is_[is_ < n]
+        a = int((n - iv).sum()) + int((n - is_).sum())
+        # overlap: for each v, offsets o <= n - 1 - v
+        ov = int(torch.searchsorted(is_.contiguous(), (n - 1 - iv).contiguous(), right=True).sum()) if len(iv) else 0
+        out[g] = a - ov
+    return out
+
+
+def synth_layer(args, device):
+    from paper_2603_04460_b200.synth import planted_layer
+    q, k, v, plants = planted_layer(args.n, args.hq, args.hkv, seed=args.seed, device=device)
+    import paper_2603_04460_b200 as vsp
+    g = torch.Generator().manual_seed(args.seed + 7)
+    params = vsp.make_indexer_params(args.hkv, 128, args.d_h, g, head_sigma=args.head_sigma, device=device)
+    return q, k, v, params
+
+
+def shard(x, r, world, dim):
+    size = x.shape[dim] // world
+    return x.narrow(dim, r * size, size).contiguous()
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def cpu_reference(args, q, k, v, params, rows: int, threads: int, repeats: int = 1):
+    """The reference's own CPU implementation (oracle/_ref) on rows [0, rows) of the layer,
+    all heads, threaded over heads. Returns (tokens/s, seconds, kind)."""
+    import oracle
+    kind = "reference" if oracle.have_ref() else "port"
+    qn = q[:rows].float().cpu().numpy().astype(np.float64)
+    kn = k[:rows].float().cpu().numpy().astype(np.float64)
+    vn = v[:rows].float().cpu().numpy().astype(np.float64)
+    prm = dict(w_u=params.w_u.float().cpu().numpy().astype(np.float64),
+               b_u=params.b_u.cpu().numpy().astype(np.float64), w_v=params.w_v.cpu().numpy().astype(np.float64),
+               w_s=params.w_s.cpu().numpy().astype(np.float64), b_v=params.b_v.cpu().numpy().astype(np.float64),
+               b_s=params.b_s.cpu().numpy().astype(np.float64))
+    lib = oracle.ref() if kind == "reference" else None
+    if lib is None:
+        raise RuntimeError("oracle/_ref not built; the reference arm needs the reference library")
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        lib.layer_vs_prefill(qn, kn, vn, prm, args.tau_v, args.tau_s, args.min_budget,
+                             args.max_budget if args.max_budget >= 0 else -1, block=32, threads=threads)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return rows / t, t, kind
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    q, k, v, params = synth_layer(args, dev)
+    threads = os.cpu_count() or 1
+    rows = args.cpu_sample
+    for _ in range(args.warmup):
+        cpu_reference(args, q, k, v, params, rows, threads)
+    ts = []
+    for _ in range(args.steps):
+        _, t, kind = cpu_reference(args, q, k, v, params, rows, threads)
+        ts.append(t)
+    t = float(np.mean(ts))
+    val = rows / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config[2] LLaMA-3.1-8B geometry layer (32Q/8KV, d=128), n=%d; CPU sample = rows "
+                               "[0,%d) of the same layer, all heads" % (args.n, rows),
+                   "n": args.n, "hq": args.hq, "hkv": args.hkv, "d_h": args.d_h,
+                   "budget": {"tau_v": args.tau_v, "tau_s": args.tau_s, "min": args.min_budget, "max": args.max_budget}},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
+                         "sample": f"rows [0,{rows}) of the n={args.n} layer, 32 Q heads; indexer+select+sparse "
+                                   f"through the reference API; per-row cost grows with i so this overstates the "
+                                   f"reference's full-length throughput"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    assert args.hkv % world == 0, "KV heads must divide across ranks"
+    import paper_2603_04460_b200 as vsp
+
+    n = args.n
+    q_full, k_full, v_full, params_full = synth_layer(args, dev)
+    hq_r, hkv_r = args.hq // world, args.hkv // world
+    q = shard(q_full, rank, world, 1)
+    k = shard(k_full, rank, world, 1)
+    v = shard(v_full, rank, world, 1)
+    params = vsp.IndexerParams(*[shard(getattr(params_full, f), rank, world, 0)
+                                 for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
+    budget = vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
+                              None if args.max_budget < 0 else args.max_budget)
+    o = torch.empty_like(q)
+    lse = torch.empty(hq_r, n, device=dev)
+
+    def step():
+        a_v, a_s = vsp.indexer_forward(k, v, params)
+        pat = vsp.select_pattern(a_v, a_s, budget)
+        vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
+        return pat
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(args.warmup, 1)):
+        pat = step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events; max over ranks)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            pat = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t_max = torch.tensor([ms], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
+    ms_step = float(t_max.item())
+
+    # ---- component timings (same heads, untimed by the contract, for the roofline)
+    def timed(fn, reps=3):
+        fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    a_v, a_s = vsp.indexer_forward(k, v, params)
+    pat = vsp.select_pattern(a_v, a_s, budget)
+    ms_indexer = timed(lambda: vsp.indexer_forward(k, v, params))
+    ms_select = timed(lambda: vsp.select_pattern(a_v, a_s, budget))
+    ms_attn = timed(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse))
+    tiles, tiles_dense = vsp.sparse_tile_stats(n, hkv_r, pat.i_v.shape[1], dev)
+    o_d = torch.empty_like(q)
+    lse_d = torch.empty_like(lse)
+    ms_dense = timed(lambda: vsp.blockwise_attention(q, k, v, out=o_d, lse=lse_d))
+    vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
+    recall = float(vsp.attention_recall(lse, lse_d).mean().item())
+    pairs_kv = covered_pairs(pat, n, hkv_r)
+    grp = args.hq // args.hkv
+    pairs_q = int(pairs_kv.sum()) * grp
+    dense_pairs = hq_r * n * (n + 1) // 2
+    alg_flops = 4.0 * 128 * pairs_q
+    pk, pk_kind = peaks()
+    peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    achieved_tf = alg_flops / (ms_attn * 1e-3) / 1e12
+    tile_tf = 4.0 * 128 * 128 * 128 * tiles * grp / (ms_attn * 1e-3) / 1e12
+    dense_tf = 4.0 * 128 * dense_pairs / (ms_dense * 1e-3) / 1e12
+    kv_list = pat.k_v.cpu().tolist()
+    ks_list = pat.k_s.cpu().tolist()
+
+    allgather_ms = None
+    if world > 1:
+        full = torch.empty(world * hq_r, n, 128, dtype=q.dtype, device=dev)
+        oh = o.permute(1, 0, 2).contiguous()  # head-major shard
+        allgather_ms = timed(lambda: torch.distributed.all_gather_into_tensor(full, oh), reps=3)
+
+    # ---- e2e through the public API with host buffers (H2D inputs, D2H output every step)
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        kh = k.cpu().pin_memory()
+        vh = v.cpu().pin_memory()
+        oh_ = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            kd.copy_(kh, non_blocking=True)
+            vd.copy_(vh, non_blocking=True)
+            a_v_, a_s_ = vsp.indexer_forward(kd, vd, params)
+            pt = vsp.select_pattern(a_v_, a_s_, budget)
+            vsp.sparse_attention(qd, kd, vd, pt, validate=False, out=o, lse=lse)
+            oh_.copy_(o, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": n / (float(e2e_ms.item()) * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2),
+               "d2h_bytes_per_step": int(oh_.numel() * 2), "ms_per_step": float(e2e_ms.item())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params_full, args.cpu_sample, threads)
+            cpu = {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
+                   "sample": f"rows [0,{args.cpu_sample}) of the same layer, all 32 Q heads, indexer+select+sparse "
+                             f"through the reference API, {secs:.1f} s wall; per-row cost grows with i, so this "
+                             f"overstates the reference's 128k throughput"}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    launches_per_step = 2 + 1 + 5  # indexer gemm+softmax, select, memset+bitmaps+gather+plan+attention
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config[2]: LLaMA-3.1-8B attention geometry single layer, KV-head sharded",
+                       "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
+                       "indexer": f"random-init VSIndexer, heads ~ N(0, {args.head_sigma}^2)",
+                       "budget": {"tau_v": args.tau_v, "tau_s": args.tau_s, "min": args.min_budget,
+                                  "max": args.max_budget},
+                       "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
+                                 "> L2 so no flush between steps", "parallelism": f"kv-head shard x{world}"},
+            "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,
+            "indexer_ms": ms_indexer, "select_ms": ms_select, "recall": recall,
+            "density": pairs_q / dense_pairs, "tile_density": tiles / tiles_dense,
+            "k_v": kv_list, "k_s": ks_list, "dense_tflops": dense_tf, "allgather_ms": allgather_ms,
+            "roofline": {"bound": "tensor", "kernel": "vs_attn_fwd (K3)", "achieved": achieved_tf,
+                         "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": None,
+                         "peak_kind": f"{pk_kind} bf16 sustained",
+                         "executed_tile_tflops": tile_tf, "executed_tile_frac": tile_tf / peak_tf},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,11 +94,12 @@ VSP_API int vsp_indexer_scores(vsp_ctx* ctx, const void* k, const void* v, int n
 
 /* ---- K2: adaptive cumulative-threshold top-k selection ---------------------------
  * budgets: HOST array [hkv]. Outputs I_v/I_s [hkv, cap] (cap >= n + 1), k_v/k_s [hkv].
- * Index sets are bit-exact with select_pattern on the same scores widened to f64. */
+ * Index sets are bit-exact with select_pattern on the same scores widened to f64.
+ * flags & VSP_VALIDATE: sync and report the reference's score checks (sparsity.hpp:60-61). */
 VSP_API size_t vsp_select_workspace_size(int n, int hkv);
 VSP_API int vsp_select(vsp_ctx* ctx, const float* a_v, const float* a_s, int n, int hkv,
                const vsp_budget* budgets, int* i_v, int* k_v, int* i_s, int* k_s, int cap,
-               void* workspace, void* stream);
+               void* workspace, int flags, void* stream);
 
 /* ---- K3: fused vertical-slash sparse attention forward --------------------------- */
 VSP_API size_t vsp_vs_attn_workspace_size(int n, int hkv, int cap);
@@ -106,6 +107,12 @@ VSP_API int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const vo
                     int hkv, int d, const int* i_v, const int* k_v, const int* i_s,
                     const int* k_s, int cap, float scale, void* o, float* lse, void* workspace,
                     int flags, void* stream);
+
+/* Statistics of the last vsp_vs_attn_fwd on `workspace` (stream-ordered, synchronises):
+ * tiles_out[0] = 128x128 KV tiles visited per KV head summed over query blocks and heads,
+ * tiles_out[1] = tiles the dense causal kernel visits for the same heads. */
+VSP_API int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace,
+                                   int64_t* tiles_out, void* stream);
 
 /* ---- K4: dense causal attention forward (the speed-up denominator) ---------------- */
 VSP_API int vsp_dense_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,

@@ -76,7 +76,7 @@ def load_library():
     lib.vsp_indexer_scores.argtypes = [vp, vp, vp, i, i, i, i, vp, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp]
     lib.vsp_select_workspace_size.restype = sz
     lib.vsp_select_workspace_size.argtypes = [i, i]
-    lib.vsp_select.argtypes = [vp, vp, vp, i, i, ctypes.POINTER(_Budget), vp, vp, vp, vp, i, vp, vp]
+    lib.vsp_select.argtypes = [vp, vp, vp, i, i, ctypes.POINTER(_Budget), vp, vp, vp, vp, i, vp, i, vp]
     lib.vsp_vs_attn_workspace_size.restype = sz
     lib.vsp_vs_attn_workspace_size.argtypes = [i, i, i]
     lib.vsp_vs_attn_fwd.argtypes = [vp, vp, vp, vp, i, i, i, i, vp, vp, vp, vp, i, f, vp, vp, vp, i, vp]
@@ -85,6 +85,7 @@ def load_library():
     lib.vsp_aggregate_workspace_size.argtypes = [i, i]
     lib.vsp_vs_aggregate.argtypes = [vp, vp, vp, i, i, i, i, f, vp, i, i, vp, vp, vp, vp]
     lib.vsp_recall_from_lse.argtypes = [vp, vp, vp, i, i, vp, vp]
+    lib.vsp_vs_attn_tile_stats.argtypes = [vp, i, i, i, vp, ctypes.POINTER(ctypes.c_int64), vp]
     _lib = lib
     return lib
 
@@ -216,7 +217,7 @@ def indexer_forward(k: torch.Tensor, v: torch.Tensor, p: IndexerParams, mapping:
     return (a_v, a_s, lv, ls) if want_logits else (a_v, a_s)
 
 
-def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget) -> SelectedIndices:
+def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget, validate: bool = False) -> SelectedIndices:
     """select_pattern (sparsity.hpp:105-114) per KV head. budget: BudgetConfig or a list of
     them (one per KV head, e.g. per-layer/per-head budgets)."""
     _need_cuda(a_v, a_s)
@@ -232,7 +233,7 @@ def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget) -> SelectedIndi
     k_s = torch.empty_like(k_v)
     ws = _workspace(dev, lib.vsp_select_workspace_size(n, hkv))
     _check(lib.vsp_select(_context(dev), _ptr(a_v.contiguous()), _ptr(a_s.contiguous()), n, hkv, arr, _ptr(i_v),
-                          _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(ws), _stream(dev)))
+                          _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(ws), 1 if validate else 0, _stream(dev)))
     return SelectedIndices(i_v, k_v, i_s, k_s)
 
 
@@ -256,6 +257,16 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern:
                                1.0 / math.sqrt(d), _ptr(o), _ptr(lse), _ptr(ws), 1 if validate else 0,
                                _stream(dev)))
     return o, lse
+
+
+def sparse_tile_stats(n: int, hkv: int, cap: int, device) -> tuple:
+    """(KV tiles visited by the last sparse_attention on `device`, tiles dense would visit),
+    per KV head summed over query blocks. Synchronises the stream."""
+    lib = load_library()
+    ws = _ws_cache[(str(device), "ws")]
+    out = (ctypes.c_int64 * 2)()
+    _check(lib.vsp_vs_attn_tile_stats(_context(device), n, hkv, cap, _ptr(ws), out, _stream(device)))
+    return int(out[0]), int(out[1])
 
 
 def blockwise_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: Optional[torch.Tensor] = None,

@@ -48,3 +48,8 @@ size_t sparse_workspace_bytes(int n, int hkv, int cap);
 cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream);
 
 }  // namespace vsp_attn
+
+namespace vsp_attn {
+cudaError_t sparse_tile_stats(int n, int hkv, int cap, const void* workspace, long long* tiles_out,
+                              cudaStream_t stream);
+}

@@ -586,3 +586,41 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
 }
 
 }  // namespace vsp_attn
+
+namespace vsp_attn {
+
+__global__ void tile_stats_kernel(const int* lists, int total_lists, int list_stride, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total_lists; t += gridDim.x * blockDim.x)
+        s += static_cast<unsigned long long>(lists[static_cast<size_t>(t) * list_stride]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+cudaError_t sparse_tile_stats(int n, int hkv, int cap, const void* workspace, long long* tiles_out,
+                              cudaStream_t stream) {
+    const int num_qb = (n + kBlock - 1) / kBlock;
+    const int kvcap = ((cap + kBlock - 1) / kBlock) * kBlock;
+    const int bm_words = (n + 31) / 32 + 1;
+    const int list_stride = 2 + kvcap / kBlock + num_qb + 3;
+    size_t off = 0;
+    auto skip = [&](size_t b) { off += (b + 255) & ~size_t(255); };
+    skip(static_cast<size_t>(hkv) * kvcap * kHeadDim * 2);
+    skip(static_cast<size_t>(hkv) * kvcap * kHeadDim * 2);
+    skip(static_cast<size_t>(hkv) * bm_words * 4 * 2);
+    const int* lists = reinterpret_cast<const int*>(static_cast<const uint8_t*>(workspace) + off);
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(d, 0, sizeof(unsigned long long), stream);
+    tile_stats_kernel<<<64, 256, 0, stream>>>(lists, hkv * num_qb, list_stride, d);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d, stream);
+    e = cudaStreamSynchronize(stream);
+    tiles_out[0] = static_cast<long long>(h);
+    tiles_out[1] = static_cast<long long>(hkv) * num_qb * (num_qb + 1) / 2;
+    return e;
+}
+
+}  // namespace vsp_attn

@@ -216,7 +216,7 @@ int vsp_indexer_scores(vsp_ctx* ctx, const void* k, const void* v, int n, int hk
 size_t vsp_select_workspace_size(int n, int hkv) { return vsp_select_k::workspace_bytes(n, hkv); }
 
 int vsp_select(vsp_ctx* ctx, const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets,
-               int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* workspace, void* stream) {
+               int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* workspace, int flags, void* stream) {
     VSP_CHECK_CTX(ctx);
     if (n < 1) return set_err(VSP_EINVAL, "cumulative_budget: empty scores");
     if (cap < n + 1) return set_err(VSP_EINVAL, "vsp_select: cap must be >= n + 1");
@@ -230,9 +230,24 @@ int vsp_select(vsp_ctx* ctx, const float* a_v, const float* a_s, int n, int hkv,
             return set_err(VSP_EINVAL, "budget config: min_budget exceeds max_budget");
     }
     if (!workspace) return set_err(VSP_EINVAL, "vsp_select: workspace required");
-    cudaError_t e = vsp_select_k::launch(a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, workspace,
-                                          as_stream(stream));
-    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_select");
+    if (hkv > 128) return set_err(VSP_EINVAL, "vsp_select: at most 128 KV heads per call");
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = vsp_select_k::launch(a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, workspace, st);
+    if (e != cudaSuccess) return cuda_err(e, "vsp_select");
+    if (flags & VSP_VALIDATE) {
+        int hs[256];
+        e = cudaMemcpyAsync(hs, vsp_select_k::status_ptr(workspace, n, hkv), sizeof(int) * 2 * hkv,
+                            cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_err(e, "vsp_select(validate)");
+        for (int g = 0; g < hkv; ++g)
+            for (int dir = 0; dir < 2; ++dir) {  // vertical budget is computed first (sparsity.hpp:108-109)
+                const int code = hs[dir * hkv + g];
+                if (code == 1) return set_err(VSP_EINVAL, "cumulative_budget: negative score");
+                if (code == 2) return set_err(VSP_EINVAL, "cumulative_budget: scores do not sum to 1");
+            }
+    }
+    return VSP_OK;
 }
 
 // ------------------------------------------------------------------ aggregation
@@ -253,3 +268,15 @@ int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, int hq, 
 }
 
 }  // extern "C"
+
+extern "C" int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace,
+                                      int64_t* tiles_out, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (!workspace || !tiles_out) return set_err(VSP_EINVAL, "vsp_vs_attn_tile_stats: null argument");
+    long long t[2];
+    cudaError_t e = vsp_attn::sparse_tile_stats(n, hkv, cap, workspace, t, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_tile_stats");
+    tiles_out[0] = t[0];
+    tiles_out[1] = t[1];
+    return VSP_OK;
+}

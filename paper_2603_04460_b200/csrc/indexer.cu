@@ -1,0 +1,267 @@
+// indexer.cu — K1: VSIndexer scoring on sm_100a.
+//
+// Replaces vsp::indexer_forward (reference indexer.hpp:116-120 -> :77-113), per KV head g:
+//   X_t = [K_t | V_t]                      (hconcat, indexer.hpp:119)
+//   Y   = X W_U + b_U ; Z = SiLU(Y)        (:84-92)
+//   logit_v[t] = Z_t w_v + b_v ; raw_s[t] = Z_t w_s + b_s      (:93-105)
+//   logit_s[o] = raw_s[n-1-o] (Reverse) | raw_s[o] (Identity)   (:106-109, :26-28)
+//   A_v = softmax(logit_v), A_s = softmax(logit_s) over all n   (:110-111)
+//
+// GEMM kernel: CTA = 128 tokens x one KV head. A = X tile (K-major, 4 x [128 x 64] SW128
+// boxes straight from the K and V tensors: the concatenation is free). B = W_U streamed in
+// [64 K-rows x 256 N] MN-major stages (the reference's [2d, d_h] row-major layout, no
+// transpose). tcgen05.mma M=128 N=256 into two TMEM accumulators (double-buffered over
+// 256-wide hidden chunks) so the SiLU / two-head epilogue of chunk c overlaps the MMA of
+// chunk c+1. The [n, d_h] activation never leaves the SM: only two fp32 logits per token
+// are written. The softmax over n is a second, tiny kernel (fp64 normaliser).
+#include <cuda_bf16.h>
+
+#include "indexer.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+using namespace vsp_sm100;
+
+namespace vsp_indexer {
+
+constexpr int kTok = 128;
+constexpr int kChunkN = 256;
+constexpr int kStageK = 64;
+constexpr int kStages = 4;
+constexpr int kABytes = kTok * 256 * 2;             // 64 KB
+constexpr int kStageBytes = kStageK * kChunkN * 2;  // 32 KB
+constexpr int kMaxDh = 2048;
+constexpr int kThreads = 192;                       // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+
+struct __align__(64) Params {
+    CUtensorMap map_k, map_v, map_w;
+    const float* b_u;
+    const float* w_v;
+    const float* w_s;
+    const float* b_v;
+    const float* b_s;
+    float* logit_v;  // [hkv, n]
+    float* logit_s;  // [hkv, n] (mapping applied)
+    int n, hkv, d_h;
+    int reverse;
+};
+
+struct Smem {
+    uint64_t bar_a;
+    uint64_t full[kStages], empty[kStages];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+
+VSP_DEVICE float silu_f(float y) { return y * __frcp_rn(1.f + __expf(-y)); }
+
+__global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = base + kABytes;
+    float* s_bu = reinterpret_cast<float*>(sB + kStages * kStageBytes);
+    float* s_wv = s_bu + kMaxDh;
+    float* s_ws = s_wv + kMaxDh;
+    __shared__ Smem sm;
+
+    const int g = blockIdx.y;
+    const int t0 = blockIdx.x * kTok;
+    const int num_chunks = p.d_h / kChunkN;
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    for (int i = threadIdx.x; i < p.d_h; i += blockDim.x) {
+        s_bu[i] = p.b_u[static_cast<size_t>(g) * p.d_h + i];
+        s_wv[i] = p.w_v[static_cast<size_t>(g) * p.d_h + i];
+        s_ws[i] = p.w_s[static_cast<size_t>(g) * p.d_h + i];
+    }
+    if (warp == 0 && lane == 0) {
+        mbar_init(&sm.bar_a, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&sm.acc_full[a], 1);
+            mbar_init(&sm.acc_empty[a], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&p.map_k);
+            tma_prefetch_desc(&p.map_v);
+            tma_prefetch_desc(&p.map_w);
+            mbar_arrive_expect_tx(&sm.bar_a, kABytes);
+            for (int hf = 0; hf < 2; ++hf) {
+                tma_load_3d(sA + hf * 16384, &p.map_k, &sm.bar_a, hf * 64, g, t0);
+                tma_load_3d(sA + (2 + hf) * 16384, &p.map_v, &sm.bar_a, hf * 64, g, t0);
+            }
+            int it = 0;
+            for (int c = 0; c < num_chunks; ++c) {
+                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                    const int s = it % kStages;
+                    if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
+                    for (int nb = 0; nb < kChunkN / 64; ++nb)
+                        tma_load_3d(sB + s * kStageBytes + nb * 8192, &p.map_w, &sm.full[s], c * kChunkN + nb * 64,
+                                    ks * kStageK, g);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
+            const uint32_t a_addr = smem_u32(sA);
+            const uint32_t b_addr = smem_u32(sB);
+            mbar_wait(&sm.bar_a, 0);
+            int it = 0;
+            for (int c = 0; c < num_chunks; ++c) {
+                const int acc = c & 1;
+                if (c >= 2) mbar_wait(&sm.acc_empty[acc], ((c >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                    const int s = it % kStages;
+                    mbar_wait(&sm.full[s], (it / kStages) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kStageK / 16; ++kk) {
+                        const int kg = ks * kStageK + kk * 16;  // global K index (feature)
+                        const uint64_t adesc =
+                            umma_desc_sw128(a_addr + (kg >> 6) * 16384 + (kg & 63) * 2, 16, 1024);
+                        const uint64_t bdesc = umma_desc_sw128(b_addr + s * kStageBytes + kk * 2048, 8192, 1024);
+                        umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&sm.empty[s]);
+                }
+                umma_commit(&sm.acc_full[acc]);
+            }
+        }
+    } else {
+        // epilogue warps 2..5: TMEM lane quarter = warp % 4
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const int t = t0 + r;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        float lv = 0.f, ls = 0.f;
+        for (int c = 0; c < num_chunks; ++c) {
+            const int acc = c & 1;
+            mbar_wait(&sm.acc_full[acc], (c >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int q = 0; q < kChunkN / 32; ++q) {
+                uint32_t u[32];
+                tmem_ld32(lane_base + acc * kChunkN + q * 32, u);
+                tmem_wait_ld();
+                const int col0 = c * kChunkN + q * 32;
+#pragma unroll
+                for (int x = 0; x < 32; ++x) {
+                    const float z = silu_f(__uint_as_float(u[x]) + s_bu[col0 + x]);
+                    lv = fmaf(z, s_wv[col0 + x], lv);
+                    ls = fmaf(z, s_ws[col0 + x], ls);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
+        }
+        if (t < p.n) {
+            p.logit_v[static_cast<size_t>(g) * p.n + t] = lv + p.b_v[g];
+            const int o = p.reverse ? p.n - 1 - t : t;
+            p.logit_s[static_cast<size_t>(g) * p.n + o] = ls + p.b_s[g];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_free<512>(tmem);
+}
+
+// Softmax over n per (head, direction), fp32 exp with an fp64 normaliser so that the
+// scores sum to 1 within fp32 rounding (select's |sum - 1| <= 1e-6 check, sparsity.hpp:61).
+// grid (hkv, 2), 1024 threads.
+__global__ void __launch_bounds__(1024) softmax_rows_kernel(const float* __restrict__ lv, const float* __restrict__ ls,
+                                                           float* __restrict__ av, float* __restrict__ as, int n) {
+    const int g = blockIdx.x;
+    const float* x = (blockIdx.y == 0 ? lv : ls) + static_cast<size_t>(g) * n;
+    float* y = (blockIdx.y == 0 ? av : as) + static_cast<size_t>(g) * n;
+    __shared__ float red_f[32];
+    __shared__ double red_d[32];
+    float m = -INFINITY;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, x[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red_f[threadIdx.x] : -INFINITY;
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red_f[0] = v;
+    }
+    __syncthreads();
+    m = red_f[0];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += static_cast<double>(expf(x[i] - m));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red_d[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red_d[0] = v;
+    }
+    __syncthreads();
+    const double inv = 1.0 / red_d[0];
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        y[i] = static_cast<float>(static_cast<double>(expf(x[i] - m)) * inv);
+}
+
+constexpr int kSmemBytes = kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 1024;
+
+size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
+    return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;
+}
+
+cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
+    if (a.d_h > kMaxDh || a.d_h % kChunkN != 0) return cudaErrorInvalidValue;
+    Params p{};
+    const uint32_t box[3] = {64, 1, kTok};
+    const uint64_t dk[3] = {128, (uint64_t)a.hkv, (uint64_t)a.n};
+    const uint64_t sk[2] = {128 * 2, (uint64_t)a.hkv * 128 * 2};
+    const uint32_t wbox[3] = {64, kStageK, 1};
+    const uint64_t dw[3] = {(uint64_t)a.d_h, 256, (uint64_t)a.hkv};
+    const uint64_t sw[2] = {(uint64_t)a.d_h * 2, (uint64_t)a.d_h * 256 * 2};
+    if (!vsp_host::make_map_bf16(&p.map_k, a.k, 3, dk, sk, box) ||
+        !vsp_host::make_map_bf16(&p.map_v, a.v, 3, dk, sk, box) ||
+        !vsp_host::make_map_bf16(&p.map_w, a.w_u, 3, dw, sw, wbox))
+        return cudaErrorInvalidValue;
+    float* lv = a.logits_v ? a.logits_v : static_cast<float*>(workspace);
+    float* ls = a.logits_s ? a.logits_s : static_cast<float*>(workspace) + static_cast<size_t>(a.hkv) * a.n;
+    p.b_u = a.b_u;
+    p.w_v = a.w_v;
+    p.w_s = a.w_s;
+    p.b_v = a.b_v;
+    p.b_s = a.b_s;
+    p.logit_v = lv;
+    p.logit_s = ls;
+    p.n = a.n;
+    p.hkv = a.hkv;
+    p.d_h = a.d_h;
+    p.reverse = a.reverse ? 1 : 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(indexer_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr = true;
+    }
+    dim3 grid((a.n + kTok - 1) / kTok, a.hkv);
+    indexer_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    softmax_rows_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(lv, ls, a.a_v, a.a_s, a.n);
+    return cudaGetLastError();
+}
+
+}  // namespace vsp_indexer

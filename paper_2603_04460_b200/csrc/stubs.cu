@@ -2,14 +2,6 @@
 #include "aggregate.h"
 #include "indexer.h"
 #include "select.h"
-namespace vsp_indexer {
-size_t workspace_bytes(int, int, int) { return 256; }
-cudaError_t launch(const Args&, void*, cudaStream_t) { return cudaErrorNotSupported; }
-}
-namespace vsp_select_k {
-size_t workspace_bytes(int, int) { return 256; }
-cudaError_t launch(const float*, const float*, int, int, const vsp_budget*, int*, int*, int*, int*, int, void*, cudaStream_t) { return cudaErrorNotSupported; }
-}
 namespace vsp_aggregate {
 size_t workspace_bytes(int, int) { return 256; }
 cudaError_t launch(const Args&, void*, cudaStream_t) { return cudaErrorNotSupported; }

@@ -1,0 +1,232 @@
+"""GPU parity of K1 (indexer scoring) and K2 (selection) against the oracle.
+
+K1 mirrors test_indexer.cpp: ZeroHeadsGiveUniformPredictions :101-111, SingleTokenIsCertain
+:113-121, MatchesStraightLineOracle :123-142, SlashMappingAnchorsAtLastToken :144-167.
+Tolerances (bf16 K, V, W_U; fp32 accumulation): logits |d| <= 3e-2, A relative <= 5e-2 on
+entries >= 1e-6, and sum(A) = 1 +- 1e-6.
+
+K2 mirrors test_sparsity.cpp (DyadicHandValues :22-32, ClampsToMinAndMax :34-46,
+TopK.HandValuesWithTies :93-104, MatchesFullSortOracle :116-126, SelectPattern.* :133-167):
+index sets must be BIT-EXACT with select_pattern run on the same fp32 scores widened to f64.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from helpers import f64
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_vectors.json")))["cases"]
+
+
+@pytest.fixture(scope="module")
+def vsp():
+    import paper_2603_04460_b200 as m
+    m.load_library()
+    return m
+
+
+def _params(vsp, hkv, d_h, seed, sigma=0.3, bias=0.3):
+    g = torch.Generator().manual_seed(seed)
+    p = vsp.make_indexer_params(hkv, 128, d_h, g, head_sigma=sigma)
+    p.b_u = (torch.randn(hkv, d_h, generator=g) * bias).cuda()
+    p.b_v = torch.tensor([0.1 * (i + 1) for i in range(hkv)]).cuda()
+    p.b_s = torch.tensor([-0.2 * (i + 1) for i in range(hkv)]).cuda()
+    return p
+
+
+def _oracle_indexer(k, v, p, g, reverse=True):
+    prm = dict(w_u=f64(p.w_u[g]), b_u=f64(p.b_u[g]), w_v=f64(p.w_v[g]), b_v=float(p.b_v[g]), w_s=f64(p.w_s[g]),
+               b_s=float(p.b_s[g]))
+    return oracle.port().indexer_forward(f64(k[:, g]), f64(v[:, g]), prm, reverse=reverse)
+
+
+@pytest.mark.parametrize("n,hkv,d_h,mapping", [(300, 2, 256, "reverse"), (1000, 1, 1024, "identity"),
+                                               (129, 2, 512, "reverse")])
+def test_indexer_matches_oracle(vsp, n, hkv, d_h, mapping):
+    g = torch.Generator().manual_seed(n)
+    k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    p = _params(vsp, hkv, d_h, seed=n)
+    a_v, a_s, lv, ls = vsp.indexer_forward(k, v, p, mapping=mapping, want_logits=True)
+    torch.cuda.synchronize()
+    for h in range(hkv):
+        r = _oracle_indexer(k, v, p, h, reverse=(mapping == "reverse"))
+        assert np.abs(f64(lv[h]) - r["logits_v"]).max() <= 3e-2
+        assert np.abs(f64(ls[h]) - r["logits_s"]).max() <= 3e-2
+        for got, want in ((a_v[h], r["pred_v"]), (a_s[h], r["pred_s"])):
+            gg = f64(got)
+            assert abs(gg.sum() - 1.0) <= 1e-6
+            m = want >= 1e-6
+            assert (np.abs(gg[m] - want[m]) / want[m]).max() <= 5e-2
+
+
+def test_indexer_zero_heads_uniform_and_single_token(vsp):
+    n, hkv = 777, 2
+    g = torch.Generator().manual_seed(1)
+    k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    p = vsp.make_indexer_params(hkv, 128, 256, g, head_sigma=0.0)
+    a_v, a_s = vsp.indexer_forward(k, v, p)
+    want = np.float32(1.0 / n)
+    assert (a_v.cpu().numpy() == want).all() and (a_s.cpu().numpy() == want).all()
+    a_v1, a_s1 = vsp.indexer_forward(k[:1].contiguous(), v[:1].contiguous(), p)
+    assert (a_v1.cpu().numpy() == 1.0).all() and (a_s1.cpu().numpy() == 1.0).all()
+
+
+def test_indexer_slash_mapping_anchor(vsp):
+    """One hidden unit carrying K feature 0 = t: Reverse puts silu(n-1-o) at offset o."""
+    n, d_h = 40, 256
+    k = torch.zeros(n, 1, 128)
+    k[:, 0, 0] = torch.arange(n, dtype=torch.float32)
+    k = k.to(torch.bfloat16).cuda()
+    v = torch.zeros(n, 1, 128, dtype=torch.bfloat16, device="cuda")
+    w_u = torch.zeros(1, 256, d_h)
+    w_u[0, 0, 0] = 1.0
+    z = torch.zeros(1, d_h, device="cuda")
+    w_s = torch.zeros(1, d_h, device="cuda")
+    w_s[0, 0] = 1.0
+    p = vsp.IndexerParams(w_u.to(torch.bfloat16).cuda(), z, z.clone(), torch.zeros(1, device="cuda"), w_s,
+                          torch.zeros(1, device="cuda"))
+    silu = lambda x: x / (1 + math.exp(-x))  # noqa: E731
+    _, a_rev, _, ls_rev = vsp.indexer_forward(k, v, p, "reverse", want_logits=True)
+    _, a_id, _, ls_id = vsp.indexer_forward(k, v, p, "identity", want_logits=True)
+    for o in range(n):
+        assert abs(ls_rev[0, o].item() - silu(n - 1 - o)) <= 1e-4 * max(1, n - 1 - o)
+        assert abs(ls_id[0, o].item() - silu(o)) <= 1e-4 * max(1, o)
+    assert int(a_rev[0].argmax()) == 0 and int(a_id[0].argmax()) == n - 1
+
+
+# ------------------------------------------------------------------------- selection
+
+def _select_gpu(vsp, sv, ss, budget):
+    a_v = torch.tensor(np.asarray(sv, np.float32)).reshape(1, -1).cuda()
+    a_s = torch.tensor(np.asarray(ss, np.float32)).reshape(1, -1).cuda()
+    pat = vsp.select_pattern(a_v, a_s, budget)
+    return pat.lists(0)
+
+
+def _budget(vsp, tau_v, tau_s, mn=1, mx=-1):
+    return vsp.BudgetConfig(tau_v, tau_s, mn, None if mx < 0 else mx)
+
+
+def test_select_golden_exact_cases(vsp):
+    """Cases whose scores are exact in fp32 compare directly against the reference's output."""
+    for c in GOLD["select_pattern"][:2]:
+        iv, is_ = _select_gpu(vsp, c["sv"], c["ss"], _budget(vsp, c["tau_v"], c["tau_s"], c["min"], c["max"]))
+        assert iv == c["i_v"] and is_ == c["i_s"]
+
+
+def test_select_dyadic_budget_table(vsp):
+    s = [0.5, 0.25, 0.125, 0.125]
+    for tau, k in ((0.5, 1), (0.6, 2), (0.75, 2), (0.76, 3), (0.875, 3), (0.9, 4), (1.0, 4)):
+        iv, _ = _select_gpu(vsp, s, s, _budget(vsp, tau, 0.5))
+        assert len(iv) == k, (tau, iv)
+    iv, _ = _select_gpu(vsp, s, s, _budget(vsp, 0.5, 0.5, 3))
+    assert len(iv) == 3
+    iv, _ = _select_gpu(vsp, s, s, _budget(vsp, 1.0, 0.5, 1, 2))
+    assert iv == [0, 1]
+
+
+def test_select_ties_low_index(vsp):
+    # TopK.HandValuesWithTies via a budget pinned to k (min = max = k)
+    for scores, k, want in (([0.2, 0.5, 0.2, 0.1], 2, [0, 1]), ([0.2, 0.5, 0.2, 0.1], 3, [0, 1, 2]),
+                            ([0.3, 0.2, 0.2, 0.3], 2, [0, 3]), ([0.3, 0.2, 0.2, 0.3], 3, [0, 1, 3]),
+                            ([0.1, 0.4, 0.4, 0.1], 2, [1, 2])):
+        iv, is_ = _select_gpu(vsp, scores, scores, _budget(vsp, 0.5, 0.5, k, k))
+        assert iv == want
+        assert is_ == (want if want[0] == 0 else [0] + want)
+
+
+def _check_against_oracle(vsp, a_v, a_s, budgets):
+    pat = vsp.select_pattern(a_v, a_s, budgets)
+    port = oracle.port()
+    for g in range(a_v.shape[0]):
+        b = budgets[g]
+        want_v, want_s = port.select_pattern(f64(a_v[g]), f64(a_s[g]), b.tau_v, b.tau_s, b.min_budget,
+                                             -1 if b.max_budget is None else b.max_budget)
+        got_v, got_s = pat.lists(g)
+        assert got_v == want_v.tolist(), f"head {g} vertical"
+        assert got_s == want_s.tolist(), f"head {g} slash"
+    return pat
+
+
+@pytest.mark.parametrize("n", [1, 2, 37, 5000, 131072])
+def test_select_matches_oracle_random(vsp, n):
+    rng = np.random.default_rng(n)
+    hkv = 4
+    sig = torch.tensor(rng.uniform(0.1, 4.0, size=(hkv, 1)), dtype=torch.float64)
+    # f64 softmax then fp32: sums stay within 1e-6 of 1 (the reference's check) at any n
+    a_v = torch.softmax(torch.randn(hkv, n, generator=torch.Generator().manual_seed(n), dtype=torch.float64) * sig,
+                        dim=1).float().cuda()
+    a_s = torch.softmax(torch.randn(hkv, n, generator=torch.Generator().manual_seed(n + 1), dtype=torch.float64) * sig,
+                        dim=1).float().cuda()
+    budgets = [vsp.BudgetConfig(float(rng.uniform(0.05, 1.0)), float(rng.uniform(0.05, 1.0)),
+                                int(rng.integers(1, 5)), None if g % 2 else int(rng.integers(5, 2 * n + 6)))
+               for g in range(hkv)]
+    _check_against_oracle(vsp, a_v, a_s, budgets)
+
+
+def test_select_quantized_ties_vs_oracle(vsp):
+    rng = np.random.default_rng(5)
+    for n in (50, 3000):
+        c = rng.integers(0, 8, size=(2, n)).astype(np.float64)
+        c[:, 0] += 1
+        a = (c / c.sum(axis=1, keepdims=True)).astype(np.float32)
+        a_v = torch.tensor(a[:1]).cuda()
+        a_s = torch.tensor(a[1:]).cuda()
+        for tau in (0.1, 0.5, 0.93):
+            _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(tau, tau, 1, None)])
+
+
+def test_select_uniform_zero_heads(vsp):
+    n = 1000
+    a = torch.full((1, n), 1.0 / n, dtype=torch.float32, device="cuda")
+    pat = _check_against_oracle(vsp, a, a, [vsp.BudgetConfig(0.9, 0.25, 1, None)])
+    iv, is_ = pat.lists(0)
+    assert iv == list(range(len(iv))) and is_ == list(range(len(is_)))
+
+
+def test_select_exact_fallback_boundary(vsp):
+    """tau chosen so the prefix mass hits tau - 1e-12 exactly: exercises the sequential-f64
+    fallback (the fast path cannot prove the decision)."""
+    s = [0.125] * 8
+    for tau in (0.5 + 1e-12, 0.5 + 2e-12, 0.5 + 5e-13):
+        iv, _ = _select_gpu(vsp, s, s, _budget(vsp, tau, 0.5))
+        want = oracle.port().cumulative_budget(np.float64(np.float32(s)), tau)
+        assert len(iv) == want, tau
+
+
+def test_select_validation_messages(vsp):
+    a = torch.tensor([[0.5, 0.6, -0.1]], device="cuda")
+    ok = torch.tensor([[0.5, 0.25, 0.25]], device="cuda")
+    with pytest.raises(vsp.VspError, match="negative score"):
+        vsp.select_pattern(a, ok, vsp.BudgetConfig(), validate=True)
+    bad = torch.tensor([[0.4, 0.4, 0.1]], device="cuda")
+    with pytest.raises(vsp.VspError, match="do not sum to 1"):
+        vsp.select_pattern(ok, bad, vsp.BudgetConfig(), validate=True)
+    with pytest.raises(vsp.VspError, match="tau_v must be in"):
+        vsp.select_pattern(ok, ok, vsp.BudgetConfig(tau_v=1.5))
+    with pytest.raises(vsp.VspError, match="min_budget exceeds max_budget"):
+        vsp.select_pattern(ok, ok, vsp.BudgetConfig(min_budget=5, max_budget=3))
+
+
+def test_vs_prefill_end_to_end(vsp):
+    """indexer -> select -> sparse attention on one layer; indices bit-exact vs oracle select on
+    the GPU scores, O vs the oracle sparse attention on the GPU indices."""
+    from helpers import assert_attn_close, oracle_sparse, qkv
+    n, hq, hkv = 640, 4, 2
+    q, k, v = qkv(n, hq, hkv, seed=42)
+    p = _params(vsp, hkv, 256, seed=3, sigma=0.5)
+    budget = vsp.BudgetConfig(0.5, 0.5, 1, None)
+    o, lse, pat = vsp.vs_prefill(q, k, v, p, budget)
+    a_v, a_s = vsp.indexer_forward(k, v, p)
+    _check_against_oracle(vsp, a_v, a_s, [budget] * hkv)
+    lists = [pat.lists(g) for g in range(hkv)]
+    o_ref, lse_ref = oracle_sparse(q, k, v, lists)
+    assert_attn_close(o, lse, o_ref, lse_ref)
