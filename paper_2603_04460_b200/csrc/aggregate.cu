@@ -287,6 +287,27 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     if (warp == 1) tmem_free<512>(tmem);
 }
 
+// Rescale each [n] profile to its exact expected total (1 per normalised head, averaged or
+// summed over the group): the bf16 tensor-core reductions leave ~1e-4 of drift, and
+// select_pattern requires |sum - 1| <= 1e-6 (sparsity.hpp:61). grid (hkv, 2).
+__global__ void renormalize_kernel(float* a_v, float* a_s, int n, double total) {
+    float* x = (blockIdx.y == 0 ? a_v : a_s) + static_cast<size_t>(blockIdx.x) * n;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        red[0] = t;
+    }
+    __syncthreads();
+    const double f = red[0] > 0.0 ? total / red[0] : 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = static_cast<float>(x[i] * f);
+}
+
 size_t workspace_bytes(int n, int hq) {
     // pass-1 scratch when the caller has no LSE: O [n, hq, 128] bf16 + LSE [hq, n]
     return static_cast<size_t>(n) * hq * 128 * 2 + static_cast<size_t>(hq) * n * 4 + 1024;
@@ -332,6 +353,9 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     }
     dim3 grid(p.num_qb * p.chunks_per_kb * a.hkv);
     aggregate_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    const int grp = a.hq / a.hkv;
+    const double total = (a.normalized ? 1.0 : static_cast<double>(a.n)) * (a.mean ? 1.0 : static_cast<double>(grp));
+    renormalize_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(a.a_v, a.a_s, a.n, total);
     return cudaGetLastError();
 }
 

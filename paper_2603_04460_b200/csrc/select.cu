@@ -64,7 +64,8 @@ struct Shared {
 };
 
 __device__ __forceinline__ unsigned long long to_fix(float x) {
-    return static_cast<unsigned long long>(__float2ull_rz(x * 4611686018427387904.0f));
+    // inputs are validated scores in [0, 1]; clamp keeps invalid ones from overflowing 2^64
+    return static_cast<unsigned long long>(__float2ull_rz(fminf(x, 2.0f) * 4611686018427387904.0f));
 }
 
 // Fill tc/tm with the histogram of digit (bits >> shift) & 255 over elements whose bits
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
             if (p.status) p.status[dir * p.hkv + g] = st;
         }
         __syncthreads();
-        if (sh.flag != 0) {
+        // Invalid scores are reported through `status` (the C ABI raises the reference's
+        // error under VSP_VALIDATE); without validation the selection still runs on them.
+        if (sh.flag == 1) {  // negative/NaN entries have no meaningful bit order: empty set
             if (threadIdx.x == 0) p.cnt[dir][g] = 0;
             return;
         }

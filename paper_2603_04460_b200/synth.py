@@ -2,39 +2,47 @@
 
 Same construction as the reference's datagen (reference datagen.hpp:61-115 with
 theory.hpp:197 plant_slash_means), restated for many heads and long sequences and done in
-torch on the device (the reference's `generate` also runs an O(n^2) f64 aggregation, which
-is skipped here; the ground truth comes from K5 when needed):
+torch on the device (the reference's `generate` also runs an O(n^2) f64 aggregation; here
+the ground truth comes from K5 when needed):
 
 * RoPE with interleaved pairs (2p, 2p+1), theta_p = base^(-2p/d) (reference rope.hpp:42-52).
 * Slash structure: q_i = R(i)(mu_q + noise), k_j = R(j)(mu_k + noise) gives
-  E[q_i . k_j] = sum_p r_p cos((i-j) theta_p - alpha_p). Planes are dealt round-robin to the
-  planted offsets; a plane assigned to offset o* gets phase alpha_p = o* theta_p so all of its
-  planes peak together at i - j = o*. Offset 0 (the local window) is always planted.
-* Vertical structure: anchor keys are overwritten after rotation with a multiple of the
-  normalised mean post-RoPE query (datagen.hpp:85-108), so a planted column scores high from
-  every row; the slowest plane carries a query baseline (q_base, datagen.hpp:64-66).
+  E[q_i . k_j] = sum_p a_p^2 cos((i - j - o_p) theta_p): a rotated plane p assigned to offset
+  o_p peaks at i - j = o_p. The mid/low-frequency planes build the local window (o_p = 0);
+  groups of high-frequency planes build sharp long-range stripes.
+* Vertical structure: every query carries q_base on the last plane, which is left unrotated
+  (NoPE), and anchor keys are overwritten with a multiple of that direction, so a planted
+  column scores high from every row at any distance. This is datagen.hpp:85-108's "anchor
+  aligned with the mean query" made position-free: at 128k the reference's slowest RoPE
+  plane rotates by ~15 rad and no longer gives a coherent mean query. Token 0 is the sink.
 * V is i.i.d. N(0, 1).
-Each KV group draws its own offsets/anchors (inter-group divergence); the Q heads of a group
-share mu_q (intra-group consistency), as observed in the paper.
+
+Two seeds, mirroring how a real model behaves: `head_seed` fixes each KV
+group's structure (its stripe offsets and mean vectors — a property of the "weights"), while
+`prompt_seed` draws the noise and the anchor positions (content). The Q heads of a group share
+mu_q (intra-group consistency); groups differ (inter-group divergence).
 """
 from __future__ import annotations
 
 import dataclasses
 import math
-from typing import List, Optional, Sequence, Tuple
+from typing import List, Optional, Tuple
 
 import torch
 
 
 @dataclasses.dataclass
 class PlantConfig:
-    n_offsets: int = 6            # planted slash offsets per KV group (besides offset 0)
-    max_offset: int = 4096        # planted offsets drawn from [1, max_offset)
-    n_anchors: int = 24           # planted vertical columns per KV group (besides token 0)
-    plane_amp: float = 1.6        # |mu_q,p| = |mu_k,p| per rotated plane
-    anchor_strength: float = 14.0
-    q_base: float = 6.0
-    noise_sigma: float = 0.6
+    n_stripes: int = 1            # long-range slash offsets per KV group
+    stripe_range: Tuple[int, int] = (256, 8192)
+    stripe_planes: int = 16       # fast planes per stripe (planes 0 .. n_stripes*stripe_planes-1)
+    stripe_amp: float = 3.3
+    local_amp: float = 2.1        # amplitude of the remaining rotated planes (peak at offset 0)
+    n_anchors: int = 16           # vertical heavy hitters per KV group (plus the sink, token 0)
+    anchor_strength: float = 36.0
+    sink_strength: float = 41.0
+    q_base: float = 6.0           # query component on the unrotated (NoPE) plane
+    noise_sigma: float = 0.5
     rope_base: float = 10000.0
 
 
@@ -56,45 +64,66 @@ def apply_rope(x: torch.Tensor, ang: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def planted_layer(n: int, hq: int, hkv: int, d: int = 128, seed: int = 0, cfg: Optional[PlantConfig] = None,
-                  device="cuda") -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, List[dict]]:
-    """-> Q [n, hq, d], K [n, hkv, d], V [n, hkv, d] bf16 and the planted structure per group."""
-    cfg = cfg or PlantConfig()
-    dev = torch.device(device)
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    grp = hq // hkv
+def head_structure(hkv: int, d: int, n: int, head_seed: int, cfg: PlantConfig):
+    """Per KV group: stripe offsets and the (mu_q, mu_k) mean vectors."""
+    g = torch.Generator(device="cpu").manual_seed(head_seed)
     planes = d // 2
-    ang = rope_angles(n, d, cfg.rope_base, dev)
-    theta = (cfg.rope_base ** (-2.0 * torch.arange(planes, dtype=torch.float64) / d))
+    theta = cfg.rope_base ** (-2.0 * torch.arange(planes, dtype=torch.float64) / d)
     mu_q = torch.zeros(hkv, d, dtype=torch.float64)
     mu_k = torch.zeros(hkv, d, dtype=torch.float64)
+    stripes = []
+    lo, hi = cfg.stripe_range
+    hi = max(lo + 1, min(hi, n))
+    for kv in range(hkv):
+        offs = sorted(int(x) for x in torch.randint(lo, hi, (cfg.n_stripes,), generator=g))
+        stripes.append(offs)
+        assign = {}
+        for s, o in enumerate(offs):
+            for j in range(cfg.stripe_planes):
+                assign[s + j * len(offs)] = (o, cfg.stripe_amp)  # interleave stripes over the fast planes
+        for p in range(planes - 1):  # the last plane is the unrotated (NoPE) sink channel
+            o, a = assign.get(p, (0, cfg.local_amp))
+            ph = o * float(theta[p])
+            mu_q[kv, 2 * p] = a
+            mu_k[kv, 2 * p] = a * math.cos(ph)
+            mu_k[kv, 2 * p + 1] = a * math.sin(ph)
+        mu_q[kv, d - 2] = cfg.q_base
+    return mu_q, mu_k, stripes
+
+
+def planted_layer(n: int, hq: int, hkv: int, d: int = 128, seed: int = 0, cfg: Optional[PlantConfig] = None,
+                  device="cuda", head_seed: Optional[int] = None,
+                  ) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, List[dict]]:
+    """-> Q [n, hq, d], K [n, hkv, d], V [n, hkv, d] bf16 and the planted structure per group.
+    `seed` is the prompt seed; `head_seed` (default: 1000003) fixes the heads' structure."""
+    cfg = cfg or PlantConfig()
+    dev = torch.device(device)
+    hs = 1000003 if head_seed is None else head_seed
+    mu_q, mu_k, stripes = head_structure(hkv, d, n, hs, cfg)
+    grp = hq // hkv
+    gp = torch.Generator(device="cpu").manual_seed(seed)
     plants = []
     for kv in range(hkv):
-        offs = [0] + sorted(set(int(x) for x in torch.randint(1, max(2, min(cfg.max_offset, n)), (cfg.n_offsets,),
-                                                                 generator=g).tolist()))
-        # the slowest plane is reserved for the query baseline (datagen.hpp:57-66)
-        for p in range(planes - 1):
-            # E[q_i.k_j] on plane p = a^2 cos((i-j) theta_p - o theta_p): peaks at i - j = o
-            o = offs[p % len(offs)]
-            phase = o * float(theta[p])
-            a = cfg.plane_amp
-            mu_q[kv, 2 * p] = a
-            mu_k[kv, 2 * p] = a * math.cos(phase)
-            mu_k[kv, 2 * p + 1] = a * math.sin(phase)
-        mu_q[kv, d - 2] += cfg.q_base
-        anchors = sorted(set([0] + [int(x) for x in torch.randint(1, max(2, n), (cfg.n_anchors,), generator=g)]))
-        plants.append(dict(offsets=offs, anchors=anchors))
+        anchors = sorted(set(int(x) for x in torch.randint(1, max(2, n), (cfg.n_anchors,), generator=gp)))
+        plants.append(dict(stripes=stripes[kv], anchors=[0] + anchors))
+    ang = rope_angles(n, d, cfg.rope_base, dev)
+    ang[:, -1] = 0.0  # NoPE plane: the sink/anchor channel does not rotate (position-free heavy hitters)
     gen = torch.Generator(device=dev).manual_seed(seed + 1)
-    q0 = torch.randn(n, hq, d, device=dev, generator=gen) * cfg.noise_sigma
-    q0 += mu_q.to(dev).float().repeat_interleave(grp, dim=0)[None]
-    k0 = torch.randn(n, hkv, d, device=dev, generator=gen) * cfg.noise_sigma + mu_k.to(dev).float()[None]
-    q = apply_rope(q0, ang)
-    k = apply_rope(k0, ang)
-    del q0, k0
+    q = torch.randn(n, hq, d, device=dev, generator=gen).mul_(cfg.noise_sigma)
+    q += mu_q.to(dev).float().repeat_interleave(grp, dim=0)[None]
+    q = apply_rope(q, ang)
+    k = torch.randn(n, hkv, d, device=dev, generator=gen).mul_(cfg.noise_sigma)
+    k += mu_k.to(dev).float()[None]
+    k = apply_rope(k, ang)
+    del ang
+    # heavy hitters: keys on the NoPE channel, which every query carries with weight q_base
+    # (the long-sequence analogue of datagen.hpp:85-108's "aligned with the mean query")
+    u = torch.zeros(d, device=dev)
+    u[d - 2] = 1.0
     for kv in range(hkv):
-        mq = q[:, kv * grp:(kv + 1) * grp].mean(dim=(0, 1))
-        mq = mq / mq.norm().clamp_min(1e-9)
-        idx = torch.tensor(plants[kv]["anchors"], device=dev)
-        k[idx, kv] = cfg.anchor_strength * mq
+        idx = torch.tensor(plants[kv]["anchors"][1:], device=dev, dtype=torch.long)
+        if len(idx):
+            k[idx, kv] = cfg.anchor_strength * u + k[idx, kv] * 0.1
+        k[0, kv] = cfg.sink_strength * u
     v = torch.randn(n, hkv, d, device=dev, generator=gen)
     return q.to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16), plants

@@ -1,0 +1,146 @@
+"""CPU tests of the host side: the C-ABI library exports, loud failure without a GPU,
+the bench's covered-pair arithmetic, the synthetic generator, the distillation objective,
+and KV-head sharding + output assembly over a 2-rank gloo group."""
+import ctypes
+import math
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "vsp_gpu.h")).read()
+    return sorted(set(re.findall(r"VSP_API\s+[\w\s\*]+?\b(vsp_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2603_04460_b200 as vsp
+    lib = vsp.load_library()
+    syms = _declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), f"missing export {s}"
+    assert lib.vsp_version().decode().startswith("vsp-b200")
+
+
+def test_no_cpu_fallback_without_gpu():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2603_04460_b200 as vsp
+    lib = vsp.load_library()
+    h = ctypes.c_void_p()
+    rc = lib.vsp_create(ctypes.byref(h), 0)
+    assert rc == vsp.VSP_ECUDA
+    assert "no CPU fallback" in lib.vsp_last_error().decode()
+    with pytest.raises(vsp.VspRuntimeError):
+        vsp.blockwise_attention(torch.zeros(8, 2, 128), torch.zeros(8, 1, 128), torch.zeros(8, 1, 128))
+
+
+def test_covered_pairs_formula_matches_bruteforce():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_2603_04460_b200 import SelectedIndices
+    import oracle
+    rng = np.random.default_rng(0)
+    n = 97
+    lists = []
+    for _ in range(3):
+        iv = sorted(rng.choice(n, size=17, replace=False).tolist())
+        is_ = sorted(set(rng.choice(n, size=11, replace=False).tolist()) | {0})
+        lists.append((iv, is_))
+    cap = n + 1
+    pat = SelectedIndices(torch.zeros(3, cap, dtype=torch.int32), torch.zeros(3, dtype=torch.int32),
+                          torch.zeros(3, cap, dtype=torch.int32), torch.zeros(3, dtype=torch.int32))
+    for g, (iv, is_) in enumerate(lists):
+        pat.i_v[g, :len(iv)] = torch.tensor(iv)
+        pat.i_s[g, :len(is_)] = torch.tensor(is_)
+        pat.k_v[g] = len(iv)
+        pat.k_s[g] = len(is_)
+    got = bench.covered_pairs(pat, n, 3)
+    port = oracle.port()
+    for g, (iv, is_) in enumerate(lists):
+        want = sum(len(port.merge_row_columns(iv, is_, i)) for i in range(n))
+        assert got[g] == want
+
+
+def test_synth_shapes_and_structure_cpu():
+    from paper_2603_04460_b200.synth import planted_layer
+    q, k, v, plants = planted_layer(256, 4, 2, seed=1, device="cpu")
+    assert q.shape == (256, 4, 128) and k.shape == (256, 2, 128) and v.shape == (256, 2, 128)
+    assert q.dtype == torch.bfloat16
+    assert len(plants) == 2 and plants[0]["anchors"][0] == 0
+    # the sink (token 0) outscores the typical causal key of every row
+    s = (q[:, 0].float() @ k[:, 0].float().T) / math.sqrt(128)
+    s = s.masked_fill(torch.triu(torch.ones(256, 256, dtype=torch.bool), 1), float("nan"))
+    med = torch.nanmedian(s[64:], dim=1).values
+    assert (s[64:, 0] > med + 3).all()
+
+
+def test_distill_objective_decreases_and_matches_reference_kl():
+    from paper_2603_04460_b200 import distill
+    torch.manual_seed(0)
+    n, hkv, d = 64, 2, 128
+    k = torch.randn(n, hkv, d).to(torch.bfloat16)
+    v = torch.randn(n, hkv, d).to(torch.bfloat16)
+    tv = torch.softmax(torch.randn(hkv, n) * 2, dim=1)
+    ts = torch.softmax(torch.randn(hkv, n) * 2, dim=1)
+    # kl_loss (indexer.hpp:138-149) restated in numpy as the check
+    lp = torch.log_softmax(torch.randn(hkv, n), dim=1)
+    got = distill.kl_forward(lp, tv).numpy()
+    p = lp.exp().double().numpy()
+    want = (p * (np.log(p) - np.log(tv.double().numpy() + 1e-8))).sum(1)
+    assert np.allclose(got, want, rtol=1e-5)
+    params, losses = distill.distill_indexer([(k, v, tv, ts)], d_h=256, steps=60, lr_peak=1e-2, warmup=5,
+                                             log_every=1)
+    assert losses[-1] < losses[0] * 0.8
+    assert params.w_u.dtype == torch.bfloat16 and params.w_u.shape == (hkv, 2 * d, 256)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, hq, d, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_04460_b200 import parallel
+    torch.manual_seed(0)
+    o_full = torch.randn(n, hq, d)  # same on every rank
+    mine = parallel.shard_heads(o_full, rank, world)
+    full = parallel.assemble_heads(mine)
+    ok = torch.equal(full, o_full.permute(1, 0, 2))
+    t = parallel.max_over_ranks(float(rank + 1), "cpu")
+    q.put((rank, ok, t, parallel.head_range(8, rank, world)))
+    dist.destroy_process_group()
+
+
+def test_head_sharding_and_assembly_gloo():
+    world, n, hq, d = 2, 16, 8, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, hq, d, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    res.sort()
+    assert all(ok for _, ok, _, _ in res)
+    assert all(t == 2.0 for _, _, t, _ in res)
+    assert [r[3] for r in res] == [(0, 4), (4, 8)]
