@@ -51,11 +51,15 @@ def parse():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d-h", type=int, default=1024)
-    ap.add_argument("--tau-v", type=float, default=0.9)
-    ap.add_argument("--tau-s", type=float, default=0.9)
+    ap.add_argument("--indexer", choices=["distilled", "random"], default="distilled")
+    ap.add_argument("--train-prompts", type=int, default=2)
+    ap.add_argument("--distill-steps", type=int, default=200)
+    ap.add_argument("--recall-target", type=float, default=0.9)
+    ap.add_argument("--tau-v", type=float, default=None, help="fix tau_v (skips calibration)")
+    ap.add_argument("--tau-s", type=float, default=None)
     ap.add_argument("--min-budget", type=int, default=1)
-    ap.add_argument("--max-budget", type=int, default=2048)
-    ap.add_argument("--head-sigma", type=float, default=0.3)
+    ap.add_argument("--max-budget", type=int, default=-1)
+    ap.add_argument("--head-sigma", type=float, default=0.3, help="random indexer head scale")
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--cpu-sample", type=int, default=2048, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -134,13 +138,58 @@ def covered_pairs(pat, n: int, hkv: int) -> np.ndarray:
     return out
 
 
-def synth_layer(args, device):
+def synth_layer(args, device, seed=None):
+    """The held-out prompt (seed = args.seed) of the planted layer, all heads."""
     from paper_2603_04460_b200.synth import planted_layer
-    q, k, v, plants = planted_layer(args.n, args.hq, args.hkv, seed=args.seed, device=device)
+    q, k, v, _ = planted_layer(args.n, args.hq, args.hkv, seed=args.seed if seed is None else seed, device=device)
+    return q, k, v
+
+
+def prepare_indexer(args, device, rank, world):
+    """This rank's indexer parameters and budget. distilled: KL-distilled on
+    `train_prompts` other prompts of the same heads (K5 ground truth), budget calibrated on
+    training prompt 0 to reach `recall_target`. random: the reference's make_indexer_params
+    with N(0, head_sigma^2) heads. Returns (params, budget, info)."""
     import paper_2603_04460_b200 as vsp
-    g = torch.Generator().manual_seed(args.seed + 7)
-    params = vsp.make_indexer_params(args.hkv, 128, args.d_h, g, head_sigma=args.head_sigma, device=device)
-    return q, k, v, params
+    from paper_2603_04460_b200 import calibrate
+    info = {}
+    if args.indexer == "random":
+        g = torch.Generator().manual_seed(args.seed + 7)
+        full = vsp.make_indexer_params(args.hkv, 128, args.d_h, g, head_sigma=args.head_sigma, device=device)
+        params = vsp.IndexerParams(*[shard(getattr(full, f), rank, world, 0)
+                                     for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
+        info["indexer"] = f"random-init VSIndexer (make_indexer_params), heads ~ N(0, {args.head_sigma}^2)"
+    else:
+        t0 = time.time()
+        prompts = []
+        for i in range(args.train_prompts):
+            q, k, v = synth_layer(args, device, seed=args.seed + 101 + i)
+            prompts.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
+            del q, k, v
+        params, losses = calibrate.train_indexer(prompts, args.d_h, steps=args.distill_steps)
+        info["indexer"] = (f"VSIndexer distilled on GPU (KL to K5 ground truth, AdamW, {args.distill_steps} steps) "
+                           f"on {args.train_prompts} training prompts of the same heads; held-out prompt timed")
+        info["distill_loss_first_last"] = [x for x in losses if x == x][:1] + [losses[-1]]
+        info["prep_s"] = None
+    if args.tau_v is not None and args.tau_s is not None:
+        budget = vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
+                                  None if args.max_budget < 0 else args.max_budget)
+        info["budget_source"] = "fixed by flags"
+    else:
+        if args.indexer == "distilled":
+            del prompts
+        # a validation prompt, distinct from the training prompts and the timed prompt
+        q, k, v = synth_layer(args, device, seed=args.seed + 201)
+        cq, ck, cv = shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)
+        del q, k, v
+        budget, pt = calibrate.calibrate_budget(cq, ck, cv, params, args.recall_target, min_budget=args.min_budget,
+                                                max_budget=None if args.max_budget < 0 else args.max_budget)
+        info["budget_source"] = (f"calibrated on a validation prompt for recall >= {args.recall_target}: "
+                                 f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
+        del cq, ck, cv
+    if args.indexer == "distilled":
+        info["prep_s"] = round(time.time() - t0, 1)
+    return params, budget, info
 
 
 def shard(x, r, world, dim):
@@ -180,7 +229,9 @@ def run_reference(args):
     if rank != 0:
         return
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    q, k, v, params = synth_layer(args, dev)
+    params, budget, _ = prepare_indexer(args, dev, 0, 1)
+    args.tau_v, args.tau_s = budget.tau_v, budget.tau_s
+    q, k, v = synth_layer(args, dev)
     threads = os.cpu_count() or 1
     rows = args.cpu_sample
     for _ in range(args.warmup):
@@ -226,15 +277,14 @@ def main():
     import paper_2603_04460_b200 as vsp
 
     n = args.n
-    q_full, k_full, v_full, params_full = synth_layer(args, dev)
+    params, budget, prep_info = prepare_indexer(args, dev, rank, world)
+    q_full, k_full, v_full = synth_layer(args, dev)
     hq_r, hkv_r = args.hq // world, args.hkv // world
     q = shard(q_full, rank, world, 1)
     k = shard(k_full, rank, world, 1)
     v = shard(v_full, rank, world, 1)
-    params = vsp.IndexerParams(*[shard(getattr(params_full, f), rank, world, 0)
-                                 for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
-    budget = vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
-                              None if args.max_budget < 0 else args.max_budget)
+    if world > 1:
+        del q_full, k_full, v_full
     o = torch.empty_like(q)
     lse = torch.empty(hq_r, n, device=dev)
 
@@ -350,7 +400,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params_full, args.cpu_sample, threads)
+            args.tau_v, args.tau_s = budget.tau_v, budget.tau_s
+            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params, args.cpu_sample, threads)
             cpu = {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
                    "sample": f"rows [0,{args.cpu_sample}) of the same layer, all 32 Q heads, indexer+select+sparse "
                              f"through the reference API, {secs:.1f} s wall; per-row cost grows with i, so this "
@@ -367,9 +418,10 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "config[2]: LLaMA-3.1-8B attention geometry single layer, KV-head sharded",
                        "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
-                       "indexer": f"random-init VSIndexer, heads ~ N(0, {args.head_sigma}^2)",
-                       "budget": {"tau_v": args.tau_v, "tau_s": args.tau_s, "min": args.min_budget,
-                                  "max": args.max_budget},
+                       "indexer": prep_info["indexer"],
+                       "budget": {"tau_v": budget.tau_v, "tau_s": budget.tau_s, "min": args.min_budget,
+                                  "max": args.max_budget, "source": prep_info["budget_source"]},
+                       "prep": {k_: v_ for k_, v_ in prep_info.items() if k_ not in ("indexer", "budget_source")},
                        "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
                                  "> L2 so no flush between steps", "parallelism": f"kv-head shard x{world}"},
             "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,

@@ -278,8 +278,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     uint32_t vw[4], sw[4];
                     window128(p.vbits + static_cast<size_t>(g) * p.bm_words, e, p.bm_words, vw);
                     window128(p.sbits + static_cast<size_t>(g) * p.bm_words, i - e - 127, p.bm_words, sw);
+                    if (vcnt0 >= 0) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) mk[k] = __brev(sw[3 - k]) & ~vw[k];
+                        for (int k = 0; k < 4; ++k) mk[k] = __brev(sw[3 - k]) & ~vw[k];
+                    } else {  // dense-masked block: verticals come from this tile too (j <= i)
+                        const int lim = i - e + 1;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int b = lim - 32 * k;
+                            const uint32_t causal = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
+                            mk[k] = __brev(sw[3 - k]) | (vw[k] & causal);
+                        }
+                    }
                 }
             } else {
                 if (j == qb) {  // diagonal tile: c <= r
@@ -480,6 +490,14 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
         }
     }
     if (a >= 0) emit(a, b);
+    if (cnt >= qb + 1) {
+        // the VS tiles would visit at least as many tiles as the dense causal row of tiles:
+        // switch this block to dense-masked mode (header vcnt0 = -1), columns [0, i0+127]
+        // with mask (j in I_v OR i-j in I_s) AND j <= i — never slower than K4.
+        for (int t = 0; t <= qb; ++t) out[2 + t] = t * kBlock;
+        cnt = qb + 1;
+        out[1] = -1;
+    }
     out[0] = cnt;
 }
 
