@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
+    // register split: the producer/MMA warpgroup needs few, the softmax warpgroups hold a
 
     if (warp == 0) {
         // =========================== TMA producer
@@ -302,26 +303,30 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 }
             }
 
+            // tcgen05.ld/st are warp-collective: the masked path must be warp-uniform (lanes
+            // that need no mask carry all-ones words)
+            masked = __any_sync(0xffffffffu, masked);
             mbar_wait(&sm.s_full[w], j & 1);
             tc_fence_after();
-            float x[128];
+            // pass 1: row max of the raw logits q.k (TMEM is re-read in pass 2 rather than
+            // holding 128 values in registers)
+            float mx = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t u[32];
                 tmem_ld32(s_t + c * 32, u);
                 tmem_wait_ld();
+                if (masked) {  // write the masked logits back so pass 2 is mask-free
 #pragma unroll
-                for (int t = 0; t < 32; ++t) x[c * 32 + t] = __uint_as_float(u[t]) * sl2;
+                    for (int t = 0; t < 32; ++t)
+                        if (!((mk[c] >> t) & 1u)) u[t] = 0xff800000u;  // -inf
+                    tmem_st32(s_t + c * 32, u);
+                }
+#pragma unroll
+                for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(u[t]));
             }
-            if (masked) {
-#pragma unroll
-                for (int c = 0; c < 128; ++c)
-                    if (!((mk[c >> 5] >> (c & 31)) & 1u)) x[c] = -INFINITY;
-            }
-            float mx = x[0];
-#pragma unroll
-            for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
-            const float m_new = fmaxf(m_used, mx);
+            if (masked) tmem_wait_st();
+            const float m_new = fmaxf(m_used, mx * sl2);
             const bool need = (m_used == -INFINITY) ? (m_new > -INFINITY) : (m_new > m_used + kRescaleThreshold);
             if (__any_sync(0xffffffffu, need)) {
                 const float m_next = need ? m_new : m_used;
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 l *= f;
                 m_used = m_next;
                 if (j > 0) {  // O holds PV(0..j-1); PV(j-1) is complete (see header)
-#pragma unroll
+#pragma unroll 1
                     for (int c = 0; c < 4; ++c) {
                         uint32_t u[32];
                         tmem_ld32(o_t + c * 32, u);
@@ -341,18 +346,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 }
             }
             const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
+            const float2 scl = make_float2(sl2, sl2);
+            const float2 neg_m = make_float2(-m_eff, -m_eff);
+            float2 lsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};
+            // pass 2: p = 2^(s * scale * log2e - m), packed to bf16 pairs and written over the
+            // already-consumed S columns (chunk c's P lands in [16c, 16c+16) < 32c)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t pk[32];
+            for (int c = 0; c < 4; ++c) {
+                uint32_t u[32];
+                tmem_ld32(s_t + c * 32, u);
+                tmem_wait_ld();
+                uint32_t pk[16];
 #pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    const float a = ex2_approx(x[c * 64 + 2 * t] - m_eff);
-                    const float b = ex2_approx(x[c * 64 + 2 * t + 1] - m_eff);
-                    l += a + b;
-                    pk[t] = pack_bf16x2(a, b);
+                for (int t = 0; t < 16; ++t) {
+                    const float2 y =
+                        ffma2(make_float2(__uint_as_float(u[2 * t]), __uint_as_float(u[2 * t + 1])), scl, neg_m);
+                    float2 e;
+                    if ((t & 3) == 3) {  // 1 pair in 4 on the FMA pipe: balances MUFU against FMA
+                        e = exp2_poly2(y);
+                    } else {
+                        e.x = ex2_approx(y.x);
+                        e.y = ex2_approx(y.y);
+                    }
+                    lsum[t & 3] = fadd2(lsum[t & 3], e);
+                    pk[t] = pack_bf16x2(e.x, e.y);
                 }
-                tmem_st32(s_t + c * 32, pk);
+                tmem_st16(s_t + c * 16, pk);
             }
+            l += ((lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y)) + ((lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y));
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();

@@ -31,7 +31,7 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTok * 256 * 2;             // 64 KB
 constexpr int kStageBytes = kStageK * kChunkN * 2;  // 32 KB
 constexpr int kMaxDh = 2048;
-constexpr int kThreads = 192;                       // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+constexpr int kThreads = 320;                       // warp0 TMA, warp1 MMA, warps 2-9 epilogue
 
 struct __align__(64) Params {
     CUtensorMap map_k, map_v, map_w;
@@ -53,7 +53,13 @@ struct Smem {
     uint32_t tmem_base;
 };
 
-VSP_DEVICE float silu_f(float y) { return y * __frcp_rn(1.f + __expf(-y)); }
+// SiLU via one MUFU op: y * sigmoid(y) = h + h * tanh(h), h = y / 2 (overflow-free for any y)
+VSP_DEVICE float silu_f(float y) {
+    const float h = 0.5f * y;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
 
 __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&sm.acc_full[a], 1);
-            mbar_init(&sm.acc_empty[a], 4);
+            mbar_init(&sm.acc_empty[a], 8);
         }
         fence_barrier_init();
     }
@@ -145,37 +151,58 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             }
         }
     } else {
-        // epilogue warps 2..5: TMEM lane quarter = warp % 4
+        // epilogue warps 2..9: TMEM lane quarter = warp % 4; part = which 128-column half of
+        // each 256-wide accumulator chunk this warp reduces (two warps per lane quarter)
         const int quarter = warp & 3;
+        const int part = (warp - 2) >> 2;
         const int r = quarter * 32 + lane;
         const int t = t0 + r;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        float lv = 0.f, ls = 0.f;
+        float lv[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};  // independent chains
         for (int c = 0; c < num_chunks; ++c) {
             const int acc = c & 1;
             mbar_wait(&sm.acc_full[acc], (c >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int q = 0; q < kChunkN / 32; ++q) {
+            for (int q = 0; q < kChunkN / 64; ++q) {
                 uint32_t u[32];
-                tmem_ld32(lane_base + acc * kChunkN + q * 32, u);
+                const int cc = part * (kChunkN / 2) + q * 32;
+                tmem_ld32(lane_base + acc * kChunkN + cc, u);
                 tmem_wait_ld();
-                const int col0 = c * kChunkN + q * 32;
+                const int col0 = c * kChunkN + cc;
+                const float4* bu4 = reinterpret_cast<const float4*>(s_bu + col0);
+                const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
+                const float4* ws4 = reinterpret_cast<const float4*>(s_ws + col0);
 #pragma unroll
-                for (int x = 0; x < 32; ++x) {
-                    const float z = silu_f(__uint_as_float(u[x]) + s_bu[col0 + x]);
-                    lv = fmaf(z, s_wv[col0 + x], lv);
-                    ls = fmaf(z, s_ws[col0 + x], ls);
+                for (int x4 = 0; x4 < 8; ++x4) {
+                    const float4 b = bu4[x4], wv = wv4[x4], ws = ws4[x4];
+                    const float bb[4] = {b.x, b.y, b.z, b.w};
+                    const float vv[4] = {wv.x, wv.y, wv.z, wv.w};
+                    const float sv[4] = {ws.x, ws.y, ws.z, ws.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float z = silu_f(__uint_as_float(u[4 * x4 + e]) + bb[e]);
+                        lv[e] = fmaf(z, vv[e], lv[e]);
+                        ls[e] = fmaf(z, sv[e], ls[e]);
+                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
         }
-        if (t < p.n) {
-            p.logit_v[static_cast<size_t>(g) * p.n + t] = lv + p.b_v[g];
+        float sv_ = (lv[0] + lv[1]) + (lv[2] + lv[3]);
+        float ss_ = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        float* xch = s_ws + kMaxDh;  // 2 x 128 floats past the parameters
+        if (part == 1) {
+            xch[r] = sv_;
+            xch[128 + r] = ss_;
+        }
+        named_bar_sync(1, 256);
+        if (part == 0 && t < p.n) {
+            p.logit_v[static_cast<size_t>(g) * p.n + t] = sv_ + xch[r] + p.b_v[g];
             const int o = p.reverse ? p.n - 1 - t : t;
-            p.logit_s[static_cast<size_t>(g) * p.n + o] = ls + p.b_s[g];
+            p.logit_s[static_cast<size_t>(g) * p.n + o] = ss_ + xch[128 + r] + p.b_s[g];
         }
     }
     tc_fence_before();
@@ -221,7 +248,7 @@ __global__ void __launch_bounds__(1024) softmax_rows_kernel(const float* __restr
         y[i] = static_cast<float>(static_cast<double>(expf(x[i] - m)) * inv);
 }
 
-constexpr int kSmemBytes = kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 1024;
+constexpr int kSmemBytes = kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 256 * 4 + 1024;
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
     return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;

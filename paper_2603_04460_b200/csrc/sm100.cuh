@@ -213,6 +213,53 @@ VSP_DEVICE float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Packed fp32x2 arithmetic (one FFMA2/FADD2 per two lanes of work, sm_100+).
+VSP_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+VSP_DEVICE float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// 2^x for x <= ~8 on the FMA/ALU pipes (no MUFU): 2^floor(x) * p(frac), p a degree-3
+// minimax fit of 2^f on [0, 1) (max rel. error 8.6e-5, far below bf16's 2^-9).
+VSP_DEVICE float2 exp2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    float2 t;  // t = x + 1.5*2^23 rounded toward -inf: low mantissa bits hold floor(x)
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\t"
+        "add.rm.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(t.x), "=f"(t.y)
+        : "f"(x.x), "f"(x.y), "f"(12582912.f));
+    const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+    float2 p = ffma2(f, make_float2(0.07706156598808621f, 0.07706156598808621f),
+                     make_float2(0.22765097328083891f, 0.22765097328083891f));
+    p = ffma2(p, f, make_float2(0.6951154508159124f, 0.6951154508159124f));
+    p = ffma2(p, f, make_float2(1.f, 1.f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+template <uint32_t kRegs>
+VSP_DEVICE void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+template <uint32_t kRegs>
+VSP_DEVICE void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+
 VSP_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
