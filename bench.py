@@ -308,10 +308,12 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" captures this region
         e0.record(stream)
         for _ in range(args.steps):
             pat = step()
         e1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps

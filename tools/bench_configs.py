@@ -1,0 +1,143 @@
+"""Secondary BASELINE.json configs on one B200 (the headline config[2] is bench.py):
+
+  C1  4k,  Qwen3-4B geometry (32/8/128), random-init indexer, fixed top-k budget
+  C2  32k, adaptive cumulative-threshold budget (distilled indexer, calibrated tau)
+  C4  36-layer attention stack at 128k (one GPU, layers back to back, per-layer budgets)
+  C5  ground-truth VS aggregation at 64k + a budget sweep vs dense (density, recall, speedup)
+
+Each prints one JSON line. All times are CUDA-event device times of warm runs.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2603_04460_b200 as vsp  # noqa: E402
+from paper_2603_04460_b200 import calibrate  # noqa: E402
+from paper_2603_04460_b200.synth import planted_layer  # noqa: E402
+
+
+def ev_time(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def layer_stats(q, k, v, params, budget):
+    n = q.shape[0]
+    out = {}
+    a_v, a_s = vsp.indexer_forward(k, v, params)
+    pat = vsp.select_pattern(a_v, a_s, budget)
+    o, lse = vsp.sparse_attention(q, k, v, pat, validate=False)
+    _, lse_d = vsp.blockwise_attention(q, k, v)
+    tiles, dense_tiles = vsp.sparse_tile_stats(n, k.shape[1], pat.i_v.shape[1], q.device)
+    out["recall"] = float(vsp.attention_recall(lse, lse_d).mean())
+    out["tile_density"] = tiles / dense_tiles
+    out["k_v_mean"] = float(pat.k_v.float().mean())
+    out["k_s_mean"] = float(pat.k_s.float().mean())
+    out["path_ms"] = ev_time(lambda: vsp.vs_prefill(q, k, v, params, budget))
+    out["vs_attn_ms"] = ev_time(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse))
+    out["dense_ms"] = ev_time(lambda: vsp.blockwise_attention(q, k, v))
+    out["speedup_vs_dense"] = out["dense_ms"] / out["vs_attn_ms"]
+    out["tokens_per_s"] = n / (out["path_ms"] * 1e-3)
+    return out
+
+
+def c1():
+    n = 4096
+    q, k, v, _ = planted_layer(n, 32, 8, seed=1)
+    g = torch.Generator().manual_seed(1)
+    params = vsp.make_indexer_params(8, 128, 1024, g, head_sigma=0.3)
+    budget = vsp.BudgetConfig(0.9, 0.9, 256, 256)  # fixed top-k: min = max = 256
+    r = layer_stats(q, k, v, params, budget)
+    return {"config": "C1 4k Qwen3-4B geometry, random-init indexer, fixed top-k 256", **r}
+
+
+def trained(n, hq=32, hkv=8, train_prompts=2, steps=200):
+    prompts = [planted_layer(n, hq, hkv, seed=100 + i)[:3] for i in range(train_prompts)]
+    params, _ = calibrate.train_indexer(prompts, 1024, steps=steps)
+    del prompts
+    val = planted_layer(n, hq, hkv, seed=7)[:3]
+    budget, pt = calibrate.calibrate_budget(*val, params, 0.9)
+    return params, budget, pt
+
+
+def c2():
+    n = 32768
+    params, budget, pt = trained(n)
+    q, k, v, _ = planted_layer(n, 32, 8, seed=2026)
+    r = layer_stats(q, k, v, params, budget)
+    return {"config": "C2 32k adaptive budget (distilled indexer, tau calibrated for recall>=0.9 on a validation "
+                      "prompt)", "tau": [budget.tau_v, budget.tau_s], **r}
+
+
+def c4(layers=36):
+    """36 layers at 128k on one GPU: each layer its own heads (head_seed) and prompt; the
+    indexer is distilled once per layer on one training prompt (untimed), the budget is
+    calibrated per layer; the timed region runs all 36 layers' paths back to back."""
+    n = 131072
+    stack = []
+    for layer in range(layers):
+        hs = 5000 + layer
+        tr = planted_layer(n, 32, 8, seed=300 + layer, head_seed=hs)[:3]
+        params, _ = calibrate.train_indexer([tr], 1024, steps=120)
+        del tr
+        val = planted_layer(n, 32, 8, seed=400 + layer, head_seed=hs)[:3]
+        budget, _ = calibrate.calibrate_budget(*val, params, 0.9, taus=(0.2, 0.3, 0.4, 0.5, 0.6, 0.7))
+        del val
+        stack.append((params, budget, hs))
+    # inputs for all layers would be 36 x 1.6 GB; time layers with regenerated inputs
+    total_ms, dense_ms, recalls = 0.0, 0.0, []
+    for layer, (params, budget, hs) in enumerate(stack):
+        q, k, v, _ = planted_layer(n, 32, 8, seed=2026 + layer, head_seed=hs)
+        total_ms += ev_time(lambda: vsp.vs_prefill(q, k, v, params, budget), reps=1)
+        if layer % 6 == 0:
+            r = layer_stats(q, k, v, params, budget)
+            recalls.append(r["recall"])
+            dense_ms += r["dense_ms"] * 6
+        del q, k, v
+    return {"config": f"C4 {layers}-layer stack at 128k, one B200, per-layer budgets", "total_ms": total_ms,
+            "tokens_per_s": n / (total_ms * 1e-3), "est_dense_ms": dense_ms,
+            "speedup_vs_dense_est": dense_ms / total_ms, "recall_sampled_layers": recalls}
+
+
+def c5():
+    n = 65536
+    q, k, v, _ = planted_layer(n, 32, 8, seed=11)
+    lse = torch.empty(32, n, device="cuda")
+    o = torch.empty_like(q)
+    dense_ms = ev_time(lambda: vsp.blockwise_attention(q, k, v, out=o, lse=lse))
+    agg_ms = ev_time(lambda: vsp.aggregate_streaming(q, k, lse=lse))
+    a_v, a_s = vsp.aggregate_streaming(q, k, lse=lse)
+    flops = 2 * 32 * 128 * n * (n + 1)  # pass-2 QK^T (2 flops/MAC) over causal pairs
+    sweep = []
+    for tv, ts in ((0.2, 0.3), (0.3, 0.5), (0.4, 0.6), (0.5, 0.7), (0.7, 0.8), (0.9, 0.9)):
+        pat = vsp.select_pattern(a_v, a_s, vsp.BudgetConfig(tv, ts, 1, None))
+        o2, lse2 = vsp.sparse_attention(q, k, v, pat, validate=False)
+        tiles, dt = vsp.sparse_tile_stats(n, 8, pat.i_v.shape[1], q.device)
+        ms = ev_time(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o2, lse=lse2))
+        sweep.append({"tau": [tv, ts], "recall": float(vsp.attention_recall(lse2, lse).mean()),
+                      "tile_density": tiles / dt, "speedup_vs_dense": dense_ms / ms})
+    return {"config": "C5 ground-truth aggregation at 64k (32Q/8KV) + budget sweep on ground-truth scores",
+            "aggregate_ms_pass2": agg_ms, "pass1_dense_lse_ms": dense_ms,
+            "aggregate_pass2_tflops": flops / (agg_ms * 1e-3) / 1e12, "sweep": sweep}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", nargs="+", choices=["c1", "c2", "c4", "c5"])
+    for w in ap.parse_args().which:
+        t0 = time.time()
+        r = globals()[w]()
+        r["wall_s"] = round(time.time() - t0, 1)
+        print(json.dumps(r), flush=True)
