@@ -172,8 +172,8 @@ def prepare_indexer(args, device, rank, world):
         info["distill_loss_first_last"] = [x for x in losses if x == x][:1] + [losses[-1]]
         info["prep_s"] = None
     if args.tau_v is not None and args.tau_s is not None:
-        budget = vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
-                                  None if args.max_budget < 0 else args.max_budget)
+        budget = [vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
+                                   None if args.max_budget < 0 else args.max_budget)] * (args.hkv // world)
         info["budget_source"] = "fixed by flags"
     else:
         if args.indexer == "distilled":
@@ -184,8 +184,9 @@ def prepare_indexer(args, device, rank, world):
         del q, k, v
         budget, pt = calibrate.calibrate_budget(cq, ck, cv, params, args.recall_target, min_budget=args.min_budget,
                                                 max_budget=None if args.max_budget < 0 else args.max_budget)
-        info["budget_source"] = (f"calibrated on a validation prompt for recall >= {args.recall_target}: "
-                                 f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
+        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) calibrated on a validation prompt for recall >= "
+                                 f"{args.recall_target}: recall {pt['recall']:.4f}, tile density "
+                                 f"{pt['tile_density']:.4f}")
         del cq, ck, cv
     if args.indexer == "distilled":
         info["prep_s"] = round(time.time() - t0, 1)
@@ -199,7 +200,7 @@ def shard(x, r, world, dim):
 
 # --------------------------------------------------------------------------- reference arm
 
-def cpu_reference(args, q, k, v, params, rows: int, threads: int, repeats: int = 1):
+def cpu_reference(args, q, k, v, params, budgets, rows: int, threads: int, repeats: int = 1):
     """The reference's own CPU implementation (oracle/_ref) on rows [0, rows) of the layer,
     all heads, threaded over heads. Returns (tokens/s, seconds, kind)."""
     import oracle
@@ -217,8 +218,9 @@ def cpu_reference(args, q, k, v, params, rows: int, threads: int, repeats: int =
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
-        lib.layer_vs_prefill(qn, kn, vn, prm, args.tau_v, args.tau_s, args.min_budget,
-                             args.max_budget if args.max_budget >= 0 else -1, block=32, threads=threads)
+        lib.layer_vs_prefill(qn, kn, vn, prm, [b.tau_v for b in budgets], [b.tau_s for b in budgets],
+                             args.min_budget, args.max_budget if args.max_budget >= 0 else -1, block=32,
+                             threads=threads)
         times.append(time.perf_counter() - t0)
     t = min(times)
     return rows / t, t, kind
@@ -230,15 +232,14 @@ def run_reference(args):
         return
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     params, budget, _ = prepare_indexer(args, dev, 0, 1)
-    args.tau_v, args.tau_s = budget.tau_v, budget.tau_s
     q, k, v = synth_layer(args, dev)
     threads = os.cpu_count() or 1
     rows = args.cpu_sample
     for _ in range(args.warmup):
-        cpu_reference(args, q, k, v, params, rows, threads)
+        cpu_reference(args, q, k, v, params, budget, rows, threads)
     ts = []
     for _ in range(args.steps):
-        _, t, kind = cpu_reference(args, q, k, v, params, rows, threads)
+        _, t, kind = cpu_reference(args, q, k, v, params, budget, rows, threads)
         ts.append(t)
     t = float(np.mean(ts))
     val = rows / t
@@ -249,7 +250,8 @@ def run_reference(args):
         "config": {"workload": "config[2] LLaMA-3.1-8B geometry layer (32Q/8KV, d=128), n=%d; CPU sample = rows "
                                "[0,%d) of the same layer, all heads" % (args.n, rows),
                    "n": args.n, "hq": args.hq, "hkv": args.hkv, "d_h": args.d_h,
-                   "budget": {"tau_v": args.tau_v, "tau_s": args.tau_s, "min": args.min_budget, "max": args.max_budget}},
+                   "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
+                              "min": args.min_budget, "max": args.max_budget}},
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
                          "sample": f"rows [0,{rows}) of the n={args.n} layer, 32 Q heads; indexer+select+sparse "
                                    f"through the reference API; per-row cost grows with i so this overstates the "
@@ -402,8 +404,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            args.tau_v, args.tau_s = budget.tau_v, budget.tau_s
-            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params, args.cpu_sample, threads)
+            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params, budget, args.cpu_sample, threads)
             cpu = {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
                    "sample": f"rows [0,{args.cpu_sample}) of the same layer, all 32 Q heads, indexer+select+sparse "
                              f"through the reference API, {secs:.1f} s wall; per-row cost grows with i, so this "
@@ -421,7 +422,8 @@ def main():
             "config": {"workload": "config[2]: LLaMA-3.1-8B attention geometry single layer, KV-head sharded",
                        "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
                        "indexer": prep_info["indexer"],
-                       "budget": {"tau_v": budget.tau_v, "tau_s": budget.tau_s, "min": args.min_budget,
+                       "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
+                                  "min": args.min_budget,
                                   "max": args.max_budget, "source": prep_info["budget_source"]},
                        "prep": {k_: v_ for k_, v_ in prep_info.items() if k_ not in ("indexer", "budget_source")},
                        "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "

@@ -109,8 +109,9 @@ VSP_API int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const vo
                     int flags, void* stream);
 
 /* Statistics of the last vsp_vs_attn_fwd on `workspace` (stream-ordered, synchronises):
- * tiles_out[0] = 128x128 KV tiles visited per KV head summed over query blocks and heads,
- * tiles_out[1] = tiles the dense causal kernel visits for the same heads. */
+ * tiles_out[0] = 128x128 KV tiles visited, summed over query blocks and KV heads,
+ * tiles_out[1] = tiles the dense causal kernel visits for the same heads,
+ * tiles_out[2 + g] = tiles of KV head g (tiles_out holds 2 + hkv entries). */
 VSP_API int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace,
                                    int64_t* tiles_out, void* stream);
 

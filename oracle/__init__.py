@@ -69,7 +69,7 @@ def _bind(lib, prefix: str):
         sig["attention_recall"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64p, _i64, _i64p, _i64,
                                                   _f64p, _cp, ctypes.c_size_t])
         sig["layer_vs_prefill"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64, _f64p, _f64p,
-                                                  _f64p, _f64p, _f64p, _f64p, ctypes.c_double, ctypes.c_double,
+                                                  _f64p, _f64p, _f64p, _f64p, _f64p, _f64p,
                                                   _i64, _i64, _i64, ctypes.c_int, _f64p, _i64p, _i64p, _cp,
                                                   ctypes.c_size_t])
         sig["layer_dense"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64, ctypes.c_int,
@@ -241,9 +241,12 @@ class _Oracle:
 
     # ---- whole layer through the reference API (ref only), threaded over heads
     def layer_vs_prefill(self, q, k, v, params, tau_v, tau_s, min_budget, max_budget, block=32, threads=1):
+        """tau_v / tau_s: scalars or one value per KV head."""
         assert self.is_ref
         n, hq, d = q.shape
         hkv = k.shape[1]
+        tau_v = np.ascontiguousarray(np.broadcast_to(np.asarray(tau_v, np.float64), (hkv,)))
+        tau_s = np.ascontiguousarray(np.broadcast_to(np.asarray(tau_s, np.float64), (hkv,)))
         q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
         w_u = np.ascontiguousarray(params["w_u"], np.float64)
         d_h = w_u.shape[2]
@@ -253,7 +256,7 @@ class _Oracle:
         kv = np.zeros(hkv, np.int64)
         ks = np.zeros(hkv, np.int64)
         rc, msg = self._call("layer_vs_prefill", n, hq, hkv, d, _f(q), _f(k), _f(v), d_h, _f(w_u), _f(b_u), _f(w_v),
-                             _f(b_v), _f(w_s), _f(b_s), float(tau_v), float(tau_s), int(min_budget),
+                             _f(b_v), _f(w_s), _f(b_s), _f(tau_v), _f(tau_s), int(min_budget),
                              int(max_budget), int(block), int(threads), _f(o), _i(kv), _i(ks))
         self._check(rc, msg)
         return o, kv, ks

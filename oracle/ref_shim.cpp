@@ -221,7 +221,7 @@ int vspref_combine_scores(int64_t heads, int64_t n, const double* v_in, const do
 int vspref_layer_vs_prefill(int64_t n, int64_t hq, int64_t hkv, int64_t d, const double* q,
                             const double* k, const double* v, int64_t d_h, const double* w_u,
                             const double* b_u, const double* w_v, const double* b_v,
-                            const double* w_s, const double* b_s, double tau_v, double tau_s,
+                            const double* w_s, const double* b_s, const double* tau_v, const double* tau_s,
                             int64_t min_b, int64_t max_b, int64_t block, int n_threads, double* o,
                             int64_t* k_v, int64_t* k_s, char* err, size_t errlen) {
     const int64_t group = hq / hkv;
@@ -252,7 +252,7 @@ int vspref_layer_vs_prefill(int64_t n, int64_t hq, int64_t hkv, int64_t d, const
         auto acts = vsp::indexer_forward(p, gather(k + g * d, hkv * d, n, d),
                                          gather(v + g * d, hkv * d, n, d));
         vsp::VSScores sc{acts.pred_v, acts.pred_s, true};
-        auto sel = vsp::select_pattern(sc, budget(tau_v, tau_s, min_b, max_b));
+        auto sel = vsp::select_pattern(sc, budget(tau_v[g], tau_s[g], min_b, max_b));
         k_v[g] = static_cast<int64_t>(sel.k_v());
         k_s[g] = static_cast<int64_t>(sel.k_s());
         pats[g] = sel.pattern();

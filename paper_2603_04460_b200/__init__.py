@@ -259,13 +259,15 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern:
     return o, lse
 
 
-def sparse_tile_stats(n: int, hkv: int, cap: int, device) -> tuple:
-    """(KV tiles visited by the last sparse_attention on `device`, tiles dense would visit),
-    per KV head summed over query blocks. Synchronises the stream."""
+def sparse_tile_stats(n: int, hkv: int, cap: int, device, per_head: bool = False) -> tuple:
+    """(KV tiles visited by the last sparse_attention on `device`, tiles dense would visit)
+    summed over query blocks and KV heads [, tiles per KV head]. Synchronises the stream."""
     lib = load_library()
     ws = _ws_cache[(str(device), "ws")]
-    out = (ctypes.c_int64 * 2)()
+    out = (ctypes.c_int64 * (2 + hkv))()
     _check(lib.vsp_vs_attn_tile_stats(_context(device), n, hkv, cap, _ptr(ws), out, _stream(device)))
+    if per_head:
+        return int(out[0]), int(out[1]), [int(out[2 + g]) for g in range(hkv)]
     return int(out[0]), int(out[1])
 
 

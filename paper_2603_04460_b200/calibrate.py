@@ -40,25 +40,35 @@ def train_indexer(prompts: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tens
 
 def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
                      taus: Sequence[float] = DEFAULT_TAUS, min_budget: int = 1,
-                     max_budget: Optional[int] = None) -> Tuple[BudgetConfig, dict]:
-    """Grid over (tau_v, tau_s); keep the cheapest pattern (fewest KV tiles) whose recall
-    reaches the target on this prompt. Falls back to the highest-recall point."""
+                     max_budget: Optional[int] = None) -> Tuple[List[BudgetConfig], dict]:
+    """Per KV head, grid over (tau_v, tau_s) and keep the cheapest pattern (fewest KV tiles)
+    whose recall (mean over the head's Q heads) reaches the target on this prompt; a head
+    that never reaches it keeps its highest-recall point. Returns one BudgetConfig per KV
+    head (select_pattern accepts per-head budgets) and a summary."""
     n, hq, d = q.shape
     hkv = k.shape[1]
+    grp = hq // hkv
     _, lse_d = blockwise_attention(q, k, v)
     a_v, a_s = indexer_forward(k, v, params)
     o = torch.empty_like(q)
     lse = torch.empty_like(lse_d)
-    best, best_any = None, None
+    best = [None] * hkv      # (tiles, recall, tv, ts) meeting the target
+    best_any = [None] * hkv  # highest recall
+    dense_tiles = 1
     for tv, ts in itertools.product(taus, taus):
-        b = BudgetConfig(tv, ts, min_budget, max_budget)
-        pat = select_pattern(a_v, a_s, b)
+        pat = select_pattern(a_v, a_s, BudgetConfig(tv, ts, min_budget, max_budget))
         sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
-        tiles, dense_tiles = sparse_tile_stats(n, hkv, pat.i_v.shape[1], q.device)
-        rec = float(attention_recall(lse, lse_d).mean().item())
-        pt = dict(tau_v=tv, tau_s=ts, recall=rec, tiles=tiles, tile_density=tiles / dense_tiles)
-        if best_any is None or rec > best_any[1]["recall"]:
-            best_any = (b, pt)
-        if rec >= recall_target and (best is None or tiles < best[1]["tiles"]):
-            best = (b, pt)
-    return best if best is not None else best_any
+        _, dense_tiles, per_head = sparse_tile_stats(n, hkv, pat.i_v.shape[1], q.device, per_head=True)
+        rec_q = attention_recall(lse, lse_d).view(hkv, grp).mean(dim=1).tolist()
+        for g in range(hkv):
+            pt = (per_head[g], rec_q[g], tv, ts)
+            if best_any[g] is None or pt[1] > best_any[g][1]:
+                best_any[g] = pt
+            if pt[1] >= recall_target and (best[g] is None or pt[0] < best[g][0]):
+                best[g] = pt
+    chosen = [best[g] if best[g] is not None else best_any[g] for g in range(hkv)]
+    budgets = [BudgetConfig(c[2], c[3], min_budget, max_budget) for c in chosen]
+    summary = dict(recall=sum(c[1] for c in chosen) / hkv,
+                   tile_density=sum(c[0] for c in chosen) / dense_tiles,
+                   per_head=[dict(tau_v=c[2], tau_s=c[3], recall=round(c[1], 4)) for c in chosen])
+    return budgets, summary

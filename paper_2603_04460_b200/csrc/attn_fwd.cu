@@ -27,6 +27,8 @@
 // which is the reference's duplicate-free per-row union.
 #include <cuda_bf16.h>
 
+#include <vector>
+
 #include "attn.h"
 #include "sm100.cuh"
 
@@ -629,14 +631,17 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
 
 namespace vsp_attn {
 
-__global__ void tile_stats_kernel(const int* lists, int total_lists, int list_stride, unsigned long long* out) {
+// per-KV-head sums of the tile-list lengths; grid (hkv), out[g] += count
+__global__ void tile_stats_kernel(const int* lists, int num_qb, int list_stride, unsigned long long* out) {
+    const int g = blockIdx.x;
     unsigned long long s = 0;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total_lists; t += gridDim.x * blockDim.x)
-        s += static_cast<unsigned long long>(lists[static_cast<size_t>(t) * list_stride]);
+    for (int t = threadIdx.x; t < num_qb; t += blockDim.x)
+        s += static_cast<unsigned long long>(lists[(static_cast<size_t>(g) * num_qb + t) * list_stride]);
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out + g, s);
 }
 
+// tiles_out: [0] total tiles, [1] dense tiles, [2 + g] tiles of KV head g
 cudaError_t sparse_tile_stats(int n, int hkv, int cap, const void* workspace, long long* tiles_out,
                               cudaStream_t stream) {
     const int num_qb = (n + kBlock - 1) / kBlock;
@@ -650,15 +655,20 @@ cudaError_t sparse_tile_stats(int n, int hkv, int cap, const void* workspace, lo
     skip(static_cast<size_t>(hkv) * bm_words * 4 * 2);
     const int* lists = reinterpret_cast<const int*>(static_cast<const uint8_t*>(workspace) + off);
     unsigned long long* d = nullptr;
-    cudaError_t e = cudaMallocAsync(&d, sizeof(unsigned long long), stream);
+    cudaError_t e = cudaMallocAsync(&d, sizeof(unsigned long long) * hkv, stream);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(d, 0, sizeof(unsigned long long), stream);
-    tile_stats_kernel<<<64, 256, 0, stream>>>(lists, hkv * num_qb, list_stride, d);
-    unsigned long long h = 0;
-    cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaMemsetAsync(d, 0, sizeof(unsigned long long) * hkv, stream);
+    tile_stats_kernel<<<hkv, 256, 0, stream>>>(lists, num_qb, list_stride, d);
+    std::vector<unsigned long long> h(hkv);
+    cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * hkv, cudaMemcpyDeviceToHost, stream);
     cudaFreeAsync(d, stream);
     e = cudaStreamSynchronize(stream);
-    tiles_out[0] = static_cast<long long>(h);
+    long long total = 0;
+    for (int g = 0; g < hkv; ++g) {
+        tiles_out[2 + g] = static_cast<long long>(h[g]);
+        total += static_cast<long long>(h[g]);
+    }
+    tiles_out[0] = total;
     tiles_out[1] = static_cast<long long>(hkv) * num_qb * (num_qb + 1) / 2;
     return e;
 }

@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/vsp_gpu.h"
 #include "aggregate.h"
@@ -273,10 +274,9 @@ extern "C" int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, con
                                       int64_t* tiles_out, void* stream) {
     VSP_CHECK_CTX(ctx);
     if (!workspace || !tiles_out) return set_err(VSP_EINVAL, "vsp_vs_attn_tile_stats: null argument");
-    long long t[2];
-    cudaError_t e = vsp_attn::sparse_tile_stats(n, hkv, cap, workspace, t, as_stream(stream));
+    std::vector<long long> t(2 + hkv);
+    cudaError_t e = vsp_attn::sparse_tile_stats(n, hkv, cap, workspace, t.data(), as_stream(stream));
     if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_tile_stats");
-    tiles_out[0] = t[0];
-    tiles_out[1] = t[1];
+    for (int x = 0; x < 2 + hkv; ++x) tiles_out[x] = t[x];
     return VSP_OK;
 }
