@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--max-budget", type=int, default=-1)
     ap.add_argument("--head-sigma", type=float, default=0.3, help="random indexer head scale")
     ap.add_argument("--seed", type=int, default=2026)
-    ap.add_argument("--cpu-sample", type=int, default=2048, help="row-prefix sample for the CPU reference")
+    ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()

@@ -41,10 +41,12 @@ def train_indexer(prompts: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tens
 def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
                      taus: Sequence[float] = DEFAULT_TAUS, min_budget: int = 1,
                      max_budget: Optional[int] = None) -> Tuple[List[BudgetConfig], dict]:
-    """Per KV head, grid over (tau_v, tau_s) and keep the cheapest pattern (fewest KV tiles)
-    whose recall (mean over the head's Q heads) reaches the target on this prompt; a head
-    that never reaches it keeps its highest-recall point. Returns one BudgetConfig per KV
-    head (select_pattern accepts per-head budgets) and a summary."""
+    """Per KV head, grid over (tau_v, tau_s); then pick one grid point per head so that the
+    total KV-tile count is minimal while the MEAN recall over heads reaches the target (the
+    paper's accuracy target is an average; heads trade budget). Solved with a Lagrangian
+    sweep: for multiplier lam each head minimises tiles - lam * recall, and lam is bisected
+    to the cheapest feasible point. Returns one BudgetConfig per KV head (select_pattern
+    accepts per-head budgets) and a summary."""
     n, hq, d = q.shape
     hkv = k.shape[1]
     grp = hq // hkv
@@ -52,8 +54,7 @@ def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
     a_v, a_s = indexer_forward(k, v, params)
     o = torch.empty_like(q)
     lse = torch.empty_like(lse_d)
-    best = [None] * hkv      # (tiles, recall, tv, ts) meeting the target
-    best_any = [None] * hkv  # highest recall
+    points = [[] for _ in range(hkv)]  # (tiles, recall, tv, ts)
     dense_tiles = 1
     for tv, ts in itertools.product(taus, taus):
         pat = select_pattern(a_v, a_s, BudgetConfig(tv, ts, min_budget, max_budget))
@@ -61,12 +62,27 @@ def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
         _, dense_tiles, per_head = sparse_tile_stats(n, hkv, pat.i_v.shape[1], q.device, per_head=True)
         rec_q = attention_recall(lse, lse_d).view(hkv, grp).mean(dim=1).tolist()
         for g in range(hkv):
-            pt = (per_head[g], rec_q[g], tv, ts)
-            if best_any[g] is None or pt[1] > best_any[g][1]:
-                best_any[g] = pt
-            if pt[1] >= recall_target and (best[g] is None or pt[0] < best[g][0]):
-                best[g] = pt
-    chosen = [best[g] if best[g] is not None else best_any[g] for g in range(hkv)]
+            points[g].append((per_head[g], rec_q[g], tv, ts))
+
+    def pick(lam):
+        return [min(pts, key=lambda p: (p[0] - lam * p[1], -p[1])) for pts in points]
+
+    def mean_recall(ch):
+        return sum(c[1] for c in ch) / hkv
+
+    hi = float(dense_tiles) * 1e3
+    chosen = pick(hi)
+    if mean_recall(chosen) >= recall_target:
+        lo = 0.0
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            if mean_recall(pick(mid)) >= recall_target:
+                hi = mid
+            else:
+                lo = mid
+        chosen = pick(hi)
+    else:  # unreachable target: the highest-recall point per head
+        chosen = [max(pts, key=lambda p: (p[1], -p[0])) for pts in points]
     budgets = [BudgetConfig(c[2], c[3], min_budget, max_budget) for c in chosen]
     summary = dict(recall=sum(c[1] for c in chosen) / hkv,
                    tile_density=sum(c[0] for c in chosen) / dense_tiles,

@@ -441,13 +441,15 @@ __global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __re
     }
 }
 
-// Kv[g][r] = K[I_v[g][r]][g], r < kvcap (rows >= k_v zero). grid (kvcap, hkv), 16 threads.
+// Kv[g][r] = K[I_v[g][r]][g], r < kvcap (rows >= k_v zero). grid (kvcap/16, hkv), 256 threads:
+// 16 rows per block, 16 threads x 16 B per 256 B row.
 __global__ void gather_vertical_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                                        const int* __restrict__ iv, const int* __restrict__ kv, int cap,
                                        int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg) {
     const int g = blockIdx.y;
-    const int r = blockIdx.x;
-    const int t = threadIdx.x;  // 16 x 16 B = 256 B = one row of d=128 bf16
+    const int r = blockIdx.x * 16 + (threadIdx.x >> 4);
+    const int t = threadIdx.x & 15;
+    if (r >= kvcap) return;
     uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
     if (r < kv[g]) {
         const int j = min(max(iv[static_cast<size_t>(g) * cap + r], 0), n - 1);
@@ -472,11 +474,17 @@ VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
 // header). Slash spans: for offsets o <= i_last (ascending I_s walked from the largest
 // offset down, i.e. ascending column start) the column intervals [max(0,i0-o), i_last-o]
 // are merged and covered greedily by disjoint 128-row tiles.
+// One warp per (KV head, query block). Walking the offsets from the largest down gives
+// intervals [lo, hi] = [max(0, i0-o), i_last-o] with lo and hi both non-decreasing, so a
+// merged range is [lo of its first interval, hi of its last] and a range breaks exactly where
+// lo_next > hi_prev + 1. 32 offsets are classified per step (coalesced loads, ballot of the
+// breaks); lane 0 emits the finished ranges' tiles in order. grid (ceil(num_qb/4), hkv), 128.
 __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
                                const int* __restrict__ is, const int* __restrict__ ks, int cap, int n,
                                int num_qb, int list_stride, int* __restrict__ lists) {
     const int g = blockIdx.y;
-    const int qb = blockIdx.x * blockDim.x + threadIdx.x;
+    const int qb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (qb >= num_qb) return;
     const int i0 = qb * kBlock;
     const int ilast = min(i0 + kBlock - 1, n - 1);
@@ -484,45 +492,56 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
     const int* isg = is + static_cast<size_t>(g) * cap;
     const int k_v = kv[g], k_s = ks[g];
     int* out = lists + (static_cast<size_t>(g) * num_qb + qb) * list_stride;
-    int cnt = 0;
     const int cv = upper_bound_i(ivg, k_v, ilast);
-    out[1] = upper_bound_i(ivg, k_v, i0 - 1);
+    const int vc0 = upper_bound_i(ivg, k_v, i0 - 1);
     const int ntv = (cv + kBlock - 1) / kBlock;
-    for (int t = 0; t < ntv; ++t) out[2 + cnt++] = -(t + 1);
-    int s = upper_bound_i(isg, k_s, ilast);
-    int cur = 0, a = -1, b = -1;
-    auto emit = [&](int lo, int hi) {
-        int st = max(lo, cur);
-        while (st <= hi) {
-            out[2 + cnt++] = st;
-            st += kBlock;
-        }
-        cur = max(cur, st);
+    for (int t = lane; t < ntv; t += 32) out[2 + t] = -(t + 1);
+    int cnt = ntv;
+    const int s = upper_bound_i(isg, k_s, ilast);
+    int cur = 0, a = -1, b = -1;  // open range [a, b] (lane-uniform state)
+    auto emit = [&](int lo, int hi) {  // lane-uniform: every lane computes, lanes write
+        const int st0 = max(lo, cur);
+        const int m = st0 <= hi ? (hi - st0) / kBlock + 1 : 0;
+        for (int x = lane; x < m; x += 32) out[2 + cnt + x] = st0 + x * kBlock;
+        cnt += m;
+        if (m) cur = st0 + m * kBlock;
     };
-    for (int t = s - 1; t >= 0; --t) {
-        const int o = __ldg(isg + t);
+    const int limit = qb + 1;  // stop as soon as dense-masked mode is certain
+    for (int base = s - 1; base >= 0 && cnt < limit; base -= 32) {
+        const int t = base - lane;
+        const bool valid = t >= 0;
+        const int o = valid ? __ldg(isg + t) : 0;
         const int lo = max(0, i0 - o), hi = ilast - o;
-        if (a < 0) {
-            a = lo;
-            b = hi;
-        } else if (lo <= b + 1) {
-            b = max(b, hi);
-        } else {
-            emit(a, b);
-            a = lo;
-            b = hi;
+        const int prev_hi = __shfl_up_sync(0xffffffffu, hi, 1);
+        bool brk = valid && (lane == 0 ? (a >= 0 && lo > b + 1) : (lo > prev_hi + 1));
+        const unsigned bm = __ballot_sync(0xffffffffu, brk);
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (a < 0) a = __shfl_sync(0xffffffffu, lo, 0);  // first interval opens the first range
+        unsigned rem = bm;
+        while (rem) {  // close the open range at each break, open the next one
+            const int e = __ffs(rem) - 1;
+            rem &= rem - 1;
+            const int b_close = e == 0 ? b : __shfl_sync(0xffffffffu, hi, e - 1);
+            emit(a, b_close);
+            a = __shfl_sync(0xffffffffu, lo, e);
         }
+        const int last = 31 - __clz(vm);
+        b = __shfl_sync(0xffffffffu, hi, last);
     }
-    if (a >= 0) emit(a, b);
-    if (cnt >= qb + 1) {
+    if (a >= 0 && cnt < limit) emit(a, b);
+    const bool dense_mode = cnt >= limit;
+    if (dense_mode) {
         // the VS tiles would visit at least as many tiles as the dense causal row of tiles:
         // switch this block to dense-masked mode (header vcnt0 = -1), columns [0, i0+127]
         // with mask (j in I_v OR i-j in I_s) AND j <= i — never slower than K4.
-        for (int t = 0; t <= qb; ++t) out[2 + t] = t * kBlock;
-        cnt = qb + 1;
-        out[1] = -1;
+        __syncwarp();
+        for (int t = lane; t < limit; t += 32) out[2 + t] = t * kBlock;
+        cnt = limit;
     }
-    out[0] = cnt;
+    if (lane == 0) {
+        out[0] = cnt;
+        out[1] = dense_mode ? -1 : vc0;
+    }
 }
 
 // ------------------------------------------------------------------ host launchers
@@ -612,10 +631,10 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
     if (e != cudaSuccess) return e;
     build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, a.hkv), 256, 0, stream>>>(
         s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words);
-    gather_vertical_kernel<<<dim3(kvcap, a.hkv), 16, 0, stream>>>(
+    gather_vertical_kernel<<<dim3(kvcap / 16, a.hkv), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
         a.n, a.hkv, kvcap, kg, vg);
-    vs_plan_kernel<<<dim3((num_qb + 127) / 128, a.hkv), 128, 0, stream>>>(
+    vs_plan_kernel<<<dim3((num_qb + 3) / 4, a.hkv), 128, 0, stream>>>(
         s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists);
     static bool attr_set = false;
     if (!attr_set) {

@@ -77,6 +77,22 @@ def test_sparse_clustered_offsets(vsp):
     assert_attn_close(o, lse, o_ref, lse_ref)
 
 
+def test_sparse_many_ranges_plan(vsp):
+    """>32 slash offsets per query block mixing tight clusters, isolated offsets and offsets
+    beyond i0 (clipped intervals): exercises the warp-parallel range merge of vs_plan_kernel."""
+    n, hq, hkv = 2048, 4, 2
+    q, k, v = qkv(n, hq, hkv, seed=17)
+    rng = np.random.default_rng(17)
+    lists = []
+    for g in range(hkv):
+        is_ = set(range(0, 40)) | set(range(300, 333)) | set(rng.choice(n, size=150, replace=False).tolist())
+        iv = sorted(rng.choice(n, size=70, replace=False).tolist())
+        lists.append((iv, sorted(is_)))
+    o, lse = vsp.sparse_attention(q, k, v, pattern_tensors(lists, n))
+    o_ref, lse_ref = oracle_sparse(q, k, v, lists)
+    assert_attn_close(o, lse, o_ref, lse_ref)
+
+
 def test_full_vertical_equals_dense(vsp):
     n, hq, hkv = 384, 4, 1
     q, k, v = qkv(n, hq, hkv, seed=11)
