@@ -52,9 +52,12 @@ def parse():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d-h", type=int, default=1024)
     ap.add_argument("--indexer", choices=["distilled", "random"], default="distilled")
-    ap.add_argument("--train-prompts", type=int, default=2)
-    ap.add_argument("--distill-steps", type=int, default=200)
+    ap.add_argument("--train-prompts", type=int, default=4)
+    ap.add_argument("--val-prompts", type=int, default=2)
+    ap.add_argument("--distill-steps", type=int, default=300)
     ap.add_argument("--recall-target", type=float, default=0.9)
+    ap.add_argument("--calib-margin", type=float, default=0.015,
+                    help="calibrate the budget for recall_target + margin on the validation prompt")
     ap.add_argument("--tau-v", type=float, default=None, help="fix tau_v (skips calibration)")
     ap.add_argument("--tau-s", type=float, default=None)
     ap.add_argument("--min-budget", type=int, default=1)
@@ -68,6 +71,17 @@ def parse():
 
 
 # --------------------------------------------------------------------------- helpers
+
+def k3_traffic():
+    """DRAM bytes (read + write) per K3 launch from the committed `ncu --set full` capture of
+    this bench's timed region (profiles/k3_traffic.json, written by tools/k3_traffic.py), or None."""
+    path = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["bytes_per_launch"]
+    except Exception:
+        return None
+
 
 def peaks():
     try:
@@ -178,16 +192,20 @@ def prepare_indexer(args, device, rank, world):
     else:
         if args.indexer == "distilled":
             del prompts
-        # a validation prompt, distinct from the training prompts and the timed prompt
-        q, k, v = synth_layer(args, device, seed=args.seed + 201)
-        cq, ck, cv = shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)
-        del q, k, v
-        budget, pt = calibrate.calibrate_budget(cq, ck, cv, params, args.recall_target, min_budget=args.min_budget,
+        # validation prompts, distinct from the training prompts and the timed prompt
+        vals = []
+        for i in range(args.val_prompts):
+            q, k, v = synth_layer(args, device, seed=args.seed + 201 + i)
+            vals.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
+            del q, k, v
+        budget, pt = calibrate.calibrate_budget(vals, params=params,
+                                                recall_target=args.recall_target + args.calib_margin,
+                                                min_budget=args.min_budget,
                                                 max_budget=None if args.max_budget < 0 else args.max_budget)
-        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) calibrated on a validation prompt for recall >= "
-                                 f"{args.recall_target}: recall {pt['recall']:.4f}, tile density "
-                                 f"{pt['tile_density']:.4f}")
-        del cq, ck, cv
+        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) calibrated on {args.val_prompts} validation prompts "
+                                 f"(worst case) for mean recall >= {args.recall_target} + {args.calib_margin}: "
+                                 f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
+        del vals
     if args.indexer == "distilled":
         info["prep_s"] = round(time.time() - t0, 1)
     return params, budget, info
@@ -352,6 +370,8 @@ def main():
     pairs_q = int(pairs_kv.sum()) * grp
     dense_pairs = hq_r * n * (n + 1) // 2
     alg_flops = 4.0 * 128 * pairs_q
+    # compulsory bytes of one K3 launch: read Q, K, V of these heads once, write O and LSE
+    alg_bytes = (q.numel() + k.numel() + v.numel() + o.numel()) * 2 + lse.numel() * 4
     pk, pk_kind = peaks()
     peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     achieved_tf = alg_flops / (ms_attn * 1e-3) / 1e12
@@ -433,7 +453,8 @@ def main():
             "density": pairs_q / dense_pairs, "tile_density": tiles / tiles_dense,
             "k_v": kv_list, "k_s": ks_list, "dense_tflops": dense_tf, "allgather_ms": allgather_ms,
             "roofline": {"bound": "tensor", "kernel": "vs_attn_fwd (K3)", "achieved": achieved_tf,
-                         "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": None,
+                         "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+                         "traffic": k3_traffic(), "algorithmic_bytes": alg_bytes,
                          "peak_kind": f"{pk_kind} bf16 sustained",
                          "executed_tile_tflops": tile_tf, "executed_tile_frac": tile_tf / peak_tf},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,

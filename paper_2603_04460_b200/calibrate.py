@@ -38,7 +38,7 @@ def train_indexer(prompts: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tens
                            log_every=max(1, steps // 10))
 
 
-def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
+def calibrate_budget(q, k=None, v=None, params: IndexerParams = None, recall_target: float = 0.9,
                      taus: Sequence[float] = DEFAULT_TAUS, min_budget: int = 1,
                      max_budget: Optional[int] = None) -> Tuple[List[BudgetConfig], dict]:
     """Per KV head, grid over (tau_v, tau_s); then pick one grid point per head so that the
@@ -46,23 +46,31 @@ def calibrate_budget(q, k, v, params: IndexerParams, recall_target: float = 0.9,
     paper's accuracy target is an average; heads trade budget). Solved with a Lagrangian
     sweep: for multiplier lam each head minimises tiles - lam * recall, and lam is bisected
     to the cheapest feasible point. Returns one BudgetConfig per KV head (select_pattern
-    accepts per-head budgets) and a summary."""
-    n, hq, d = q.shape
-    hkv = k.shape[1]
+    accepts per-head budgets) and a summary. With several validation prompts each grid point
+    is scored by its worst case (most tiles, least recall) over them."""
+    prompts = [(q, k, v)] if torch.is_tensor(q) else list(q)  # one prompt or a list of them
+    n, hq, d = prompts[0][0].shape
+    hkv = prompts[0][1].shape[1]
     grp = hq // hkv
-    _, lse_d = blockwise_attention(q, k, v)
-    a_v, a_s = indexer_forward(k, v, params)
-    o = torch.empty_like(q)
-    lse = torch.empty_like(lse_d)
-    points = [[] for _ in range(hkv)]  # (tiles, recall, tv, ts)
+    grid = list(itertools.product(taus, taus))
+    worst = {}  # (g, grid index) -> [tiles, recall]
     dense_tiles = 1
-    for tv, ts in itertools.product(taus, taus):
-        pat = select_pattern(a_v, a_s, BudgetConfig(tv, ts, min_budget, max_budget))
-        sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
-        _, dense_tiles, per_head = sparse_tile_stats(n, hkv, pat.i_v.shape[1], q.device, per_head=True)
-        rec_q = attention_recall(lse, lse_d).view(hkv, grp).mean(dim=1).tolist()
-        for g in range(hkv):
-            points[g].append((per_head[g], rec_q[g], tv, ts))
+    for pq, pk, pv in prompts:
+        _, lse_d = blockwise_attention(pq, pk, pv)
+        a_v, a_s = indexer_forward(pk, pv, params)
+        o = torch.empty_like(pq)
+        lse = torch.empty_like(lse_d)
+        for gi, (tv, ts) in enumerate(grid):
+            pat = select_pattern(a_v, a_s, BudgetConfig(tv, ts, min_budget, max_budget))
+            sparse_attention(pq, pk, pv, pat, validate=False, out=o, lse=lse)
+            _, dense_tiles, per_head = sparse_tile_stats(n, hkv, pat.i_v.shape[1], pq.device, per_head=True)
+            rec_q = attention_recall(lse, lse_d).view(hkv, grp).mean(dim=1).tolist()
+            for g in range(hkv):
+                w = worst.setdefault((g, gi), [0, 1.0])
+                w[0] = max(w[0], per_head[g])
+                w[1] = min(w[1], rec_q[g])
+    points = [[(worst[(g, gi)][0], worst[(g, gi)][1], tv, ts) for gi, (tv, ts) in enumerate(grid)]
+              for g in range(hkv)]
 
     def pick(lam):
         return [min(pts, key=lambda p: (p[0] - lam * p[1], -p[1])) for pts in points]

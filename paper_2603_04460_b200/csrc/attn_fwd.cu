@@ -313,19 +313,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             // pass 1: row max of the raw logits q.k (TMEM is re-read in pass 2 rather than
             // holding 128 values in registers)
             float mx = -INFINITY;
+            {
+                uint32_t u[4][32];  // all four loads in flight before the first wait
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t u[32];
-                tmem_ld32(s_t + c * 32, u);
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_t + c * 32, u[c]);
                 tmem_wait_ld();
-                if (masked) {  // write the masked logits back so pass 2 is mask-free
 #pragma unroll
-                    for (int t = 0; t < 32; ++t)
-                        if (!((mk[c] >> t) & 1u)) u[t] = 0xff800000u;  // -inf
-                    tmem_st32(s_t + c * 32, u);
+                for (int c = 0; c < 4; ++c) {
+                    if (masked) {  // write the masked logits back so pass 2 is mask-free
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            if (!((mk[c] >> t) & 1u)) u[c][t] = 0xff800000u;  // -inf
+                        tmem_st32(s_t + c * 32, u[c]);
+                    }
+#pragma unroll
+                    for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(u[c][t]));
                 }
-#pragma unroll
-                for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(u[t]));
             }
             if (masked) tmem_wait_st();
             const float m_new = fmaxf(m_used, mx * sl2);
@@ -354,27 +357,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                               make_float2(0.f, 0.f)};
             // pass 2: p = 2^(s * scale * log2e - m), packed to bf16 pairs and written over the
             // already-consumed S columns (chunk c's P lands in [16c, 16c+16) < 32c)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t u[32];
-                tmem_ld32(s_t + c * 32, u);
+            {
+                uint32_t u[2][32];  // ping-pong: chunk c+1 is loading while chunk c computes
+                tmem_ld32(s_t, u[0]);
                 tmem_wait_ld();
-                uint32_t pk[16];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const float2 y =
-                        ffma2(make_float2(__uint_as_float(u[2 * t]), __uint_as_float(u[2 * t + 1])), scl, neg_m);
-                    float2 e;
-                    if ((t & 3) == 3) {  // 1 pair in 4 on the FMA pipe: balances MUFU against FMA
-                        e = exp2_poly2(y);
-                    } else {
-                        e.x = ex2_approx(y.x);
-                        e.y = ex2_approx(y.y);
+                for (int c = 0; c < 4; ++c) {
+                    if (c < 3) tmem_ld32(s_t + (c + 1) * 32, u[(c + 1) & 1]);
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) {
+                        const float2 y = ffma2(make_float2(__uint_as_float(u[c & 1][2 * t]),
+                                                           __uint_as_float(u[c & 1][2 * t + 1])),
+                                               scl, neg_m);
+                        float2 e;
+                        if ((0x5454u >> t) & 1u) {  // 3 pairs in 8 on the FMA pipe (MUFU/FMA balance)
+                            e = exp2_poly2(y);
+                        } else {
+                            e.x = ex2_approx(y.x);
+                            e.y = ex2_approx(y.y);
+                        }
+                        lsum[t & 3] = fadd2(lsum[t & 3], e);
+                        pk[t] = pack_bf16x2(e.x, e.y);
                     }
-                    lsum[t & 3] = fadd2(lsum[t & 3], e);
-                    pk[t] = pack_bf16x2(e.x, e.y);
+                    tmem_st16(s_t + c * 16, pk);
+                    if (c < 3) tmem_wait_ld();
                 }
-                tmem_st16(s_t + c * 16, pk);
             }
             l += ((lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y)) + ((lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y));
             tmem_wait_st();

@@ -54,7 +54,7 @@ for P in args.prompts:
     torch.cuda.synchronize()
     rec = vsp.attention_recall(lse, lse_d).mean().item()
     print(f"P={P} steps={args.steps} train {train_s:.1f}s loss {losses[0]:.3f}->{losses[-1]:.3f} heldout KL {kl:.3f} | "
-          f"val-calibrated tau=({budget.tau_v},{budget.tau_s}) val recall {pt['recall']:.3f} | TEST recall {rec:.4f} "
+          f"val-calibrated tau={[(b.tau_v, b.tau_s) for b in budget]} val recall {pt['recall']:.3f} | TEST recall {rec:.4f} "
           f"tile density {tiles / dt:.4f} k_v {pat.k_v.float().mean():.0f} k_s {pat.k_s.float().mean():.0f} "
           f"speedup {dense_ms / e0.elapsed_time(e1):.2f}x")
     # oracle selection on ground truth for reference
