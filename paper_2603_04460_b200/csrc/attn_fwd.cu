@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     // register split: the producer/MMA warpgroup needs few, the softmax warpgroups hold a
 
     if (warp == 0) {
-        // =========================== TMA producer
-        if (lane == 0) {
+        // =========================== TMA producer (warp-uniform loop, elected issuer)
+        if (elect_one()) {
             tma_prefetch_desc(&p.map_q);
             tma_prefetch_desc(&p.map_k);
             tma_prefetch_desc(&p.map_v);
@@ -144,93 +144,101 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int hf = 0; hf < 2; ++hf)
                     tma_load_3d(sQ + w * kTileBytes + hf * kHalfBytes, &p.map_q, &sm.bar_q, hf * 64,
                                 h0 + w, i0);
-            for (int j = 0; j < num_tiles; ++j) {
-                int e = kSparse ? __ldg(tiles + j) : j * kBlock;
-                const bool gathered = kSparse && e < 0;
-                const int row = gathered ? (-e - 1) * kBlock : e;
-                const int ks = j % kNumK;
-                if (j >= kNumK) mbar_wait(&sm.k_empty[ks], ((j / kNumK) & 1) ^ 1);
+        }
+        __syncwarp();
+        for (int j = 0; j < num_tiles; ++j) {
+            int e = kSparse ? __ldg(tiles + j) : j * kBlock;
+            const bool gathered = kSparse && e < 0;
+            const int row = gathered ? (-e - 1) * kBlock : e;
+            const CUtensorMap* mk_ = gathered ? &p.map_kv : &p.map_k;
+            const CUtensorMap* mv_ = gathered ? &p.map_vv : &p.map_v;
+            const int c1 = gathered ? row : g, c2 = gathered ? g : row;
+            const int ks = j % kNumK;
+            if (j >= kNumK) mbar_wait(&sm.k_empty[ks], ((j / kNumK) & 1) ^ 1);
+            if (elect_one()) {
                 mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
-                for (int hf = 0; hf < 2; ++hf) {
-                    if (gathered)
-                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, &p.map_kv, &sm.k_full[ks],
-                                    hf * 64, row, g);
-                    else
-                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, &p.map_k, &sm.k_full[ks],
-                                    hf * 64, g, row);
-                }
-                const int vs = j % kNumV;
-                if (j >= kNumV) mbar_wait(&sm.v_empty[vs], ((j / kNumV) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
-                for (int hf = 0; hf < 2; ++hf) {
-                    if (gathered)
-                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, &p.map_vv, &sm.v_full[vs],
-                                    hf * 64, row, g);
-                    else
-                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, &p.map_v, &sm.v_full[vs],
-                                    hf * 64, g, row);
-                }
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, mk_, &sm.k_full[ks], hf * 64, c1, c2);
             }
+            __syncwarp();
+            const int vs = j % kNumV;
+            if (j >= kNumV) mbar_wait(&sm.v_empty[vs], ((j / kNumV) & 1) ^ 1);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, mv_, &sm.v_full[vs], hf * 64, c1, c2);
+            }
+            __syncwarp();
         }
     } else if (warp == 1) {
         // =========================== MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
-            const uint32_t idesc_pv = umma_idesc_bf16(128, 128, false, true);
-            const uint32_t q_addr = smem_u32(sQ);
-            const uint32_t k_addr = smem_u32(sK);
-            const uint32_t v_addr = smem_u32(sV);
-            auto issue_pv = [&](int w, int jj) {
-                const int vs = jj % kNumV;
-                const uint32_t o_t = tmem + 256 + w * 128;
-                const uint32_t p_t = tmem + w * 128;
+        // The whole warp walks the schedule (warp-uniform control flow keeps descriptors in
+        // uniform registers); one elected lane issues each batch of tcgen05.mma / commit.
+        const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
+        const uint32_t idesc_pv = umma_idesc_bf16(128, 128, false, true);
+        // descriptor bases; per-k offsets are added to the 14-bit start-address field
+        const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);
+        const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
+        const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sV), kHalfBytes, 1024);
+        auto issue_pv = [&](int w, int jj) {
+            const uint64_t vd = v_desc0 + static_cast<uint64_t>(((jj % kNumV) * kTileBytes) >> 4);
+            const uint32_t o_t = tmem + 256 + w * 128;
+            const uint32_t p_t = tmem + w * 128;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint64_t bdesc = umma_desc_sw128(v_addr + vs * kTileBytes + k * 2048, kHalfBytes, 1024);
-                    umma_ts(o_t, p_t + k * 8, bdesc, idesc_pv, (jj > 0 || k > 0) ? 1u : 0u);
-                }
-            };
-            auto issue_s = [&](int w, int jj) {
-                const int ks = jj % kNumK;
-                const uint32_t s_t = tmem + w * 128;
+            for (int k = 0; k < 8; ++k)
+                umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
+                        (jj > 0 || k > 0) ? 1u : 0u);
+        };
+        auto issue_s = [&](int w, int jj) {
+            const uint64_t qd = q_desc0 + static_cast<uint64_t>((w * kTileBytes) >> 4);
+            const uint64_t kd = k_desc0 + static_cast<uint64_t>(((jj % kNumK) * kTileBytes) >> 4);
+            const uint32_t s_t = tmem + w * 128;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t off = (k >> 2) * kHalfBytes + (k & 3) * 32;
-                    const uint64_t adesc = umma_desc_sw128(q_addr + w * kTileBytes + off, 16, 1024);
-                    const uint64_t bdesc = umma_desc_sw128(k_addr + ks * kTileBytes + off, 16, 1024);
-                    umma_ss(s_t, adesc, bdesc, idesc_qk, k > 0 ? 1u : 0u);
-                }
-            };
-            mbar_wait(&sm.bar_q, 0);
-            if (num_tiles == 0) {  // nothing covered: release the epilogue
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t off = static_cast<uint64_t>(((k >> 2) * kHalfBytes + (k & 3) * 32) >> 4);
+                umma_ss(s_t, qd + off, kd + off, idesc_qk, k > 0 ? 1u : 0u);
+            }
+        };
+        mbar_wait(&sm.bar_q, 0);
+        if (num_tiles == 0) {  // nothing covered: release the epilogue
+            if (elect_one()) {
                 umma_commit(&sm.o_done[0]);
                 umma_commit(&sm.o_done[1]);
             }
-            for (int j = 0; j < num_tiles; ++j) {
-                const int ks = j % kNumK;
-                mbar_wait(&sm.k_full[ks], (j / kNumK) & 1);
-                tc_fence_after();
-                for (int w = 0; w < 2; ++w) {
+            __syncwarp();
+        }
+        for (int j = 0; j < num_tiles; ++j) {
+            const int ks = j % kNumK;
+            mbar_wait(&sm.k_full[ks], (j / kNumK) & 1);
+            tc_fence_after();
+            for (int w = 0; w < 2; ++w) {
+                if (j > 0) {
+                    mbar_wait(&sm.p_full[w], (j - 1) & 1);
+                    if (w == 0) mbar_wait(&sm.v_full[(j - 1) % kNumV], ((j - 1) / kNumV) & 1);
+                    tc_fence_after();
+                }
+                if (elect_one()) {
                     if (j > 0) {
-                        mbar_wait(&sm.p_full[w], (j - 1) & 1);
-                        if (w == 0) mbar_wait(&sm.v_full[(j - 1) % kNumV], ((j - 1) / kNumV) & 1);
-                        tc_fence_after();
                         issue_pv(w, j - 1);
                         if (w == 1) umma_commit(&sm.v_empty[(j - 1) % kNumV]);
                     }
                     issue_s(w, j);
                     umma_commit(&sm.s_full[w]);
+                    if (w == 1) umma_commit(&sm.k_empty[ks]);
                 }
-                umma_commit(&sm.k_empty[ks]);
+                __syncwarp();
             }
-            const int jl = num_tiles - 1;
-            for (int w = 0; w < 2 && num_tiles > 0; ++w) {
-                mbar_wait(&sm.p_full[w], jl & 1);
-                if (w == 0) mbar_wait(&sm.v_full[jl % kNumV], (jl / kNumV) & 1);
-                tc_fence_after();
+        }
+        const int jl = num_tiles - 1;
+        for (int w = 0; w < 2 && num_tiles > 0; ++w) {
+            mbar_wait(&sm.p_full[w], jl & 1);
+            if (w == 0) mbar_wait(&sm.v_full[jl % kNumV], (jl / kNumV) & 1);
+            tc_fence_after();
+            if (elect_one()) {
                 issue_pv(w, jl);
                 umma_commit(&sm.o_done[w]);
             }
+            __syncwarp();
         }
     } else if (warp >= 4) {
         // =========================== softmax + epilogue

@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     const uint32_t tmem = sm.tmem_base;
 
     if (warp == 0) {
-        if (lane == 0) {
+        // TMA producer: warp-uniform loop, one elected lane issues
+        if (elect_one()) {
             tma_prefetch_desc(&p.map_k);
             tma_prefetch_desc(&p.map_v);
             tma_prefetch_desc(&p.map_w);
@@ -110,44 +111,49 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                 tma_load_3d(sA + hf * 16384, &p.map_k, &sm.bar_a, hf * 64, g, t0);
                 tma_load_3d(sA + (2 + hf) * 16384, &p.map_v, &sm.bar_a, hf * 64, g, t0);
             }
-            int it = 0;
-            for (int c = 0; c < num_chunks; ++c) {
-                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                    const int s = it % kStages;
-                    if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+        }
+        __syncwarp();
+        int it = 0;
+        for (int c = 0; c < num_chunks; ++c) {
+            for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                const int s = it % kStages;
+                if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+                if (elect_one()) {
                     mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
                     for (int nb = 0; nb < kChunkN / 64; ++nb)
                         tma_load_3d(sB + s * kStageBytes + nb * 8192, &p.map_w, &sm.full[s], c * kChunkN + nb * 64,
                                     ks * kStageK, g);
                 }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
-            const uint32_t a_addr = smem_u32(sA);
-            const uint32_t b_addr = smem_u32(sB);
-            mbar_wait(&sm.bar_a, 0);
-            int it = 0;
-            for (int c = 0; c < num_chunks; ++c) {
-                const int acc = c & 1;
-                if (c >= 2) mbar_wait(&sm.acc_empty[acc], ((c >> 1) & 1) ^ 1);
+        // MMA issuer: warp-uniform loop, one elected lane issues each batch
+        const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
+        const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
+        const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), 8192, 1024);
+        mbar_wait(&sm.bar_a, 0);
+        int it = 0;
+        for (int c = 0; c < num_chunks; ++c) {
+            const int acc = c & 1;
+            if (c >= 2) mbar_wait(&sm.acc_empty[acc], ((c >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                const int s = it % kStages;
+                mbar_wait(&sm.full[s], (it / kStages) & 1);
                 tc_fence_after();
-                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                    const int s = it % kStages;
-                    mbar_wait(&sm.full[s], (it / kStages) & 1);
-                    tc_fence_after();
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < kStageK / 16; ++kk) {
                         const int kg = ks * kStageK + kk * 16;  // global K index (feature)
-                        const uint64_t adesc =
-                            umma_desc_sw128(a_addr + (kg >> 6) * 16384 + (kg & 63) * 2, 16, 1024);
-                        const uint64_t bdesc = umma_desc_sw128(b_addr + s * kStageBytes + kk * 2048, 8192, 1024);
+                        const uint64_t adesc = a_desc0 + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4);
+                        const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kStageBytes + kk * 2048) >> 4);
                         umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&sm.empty[s]);
+                    if (ks == 256 / kStageK - 1) umma_commit(&sm.acc_full[acc]);
                 }
-                umma_commit(&sm.acc_full[acc]);
+                __syncwarp();
             }
         }
     } else {
@@ -163,12 +169,14 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             const int acc = c & 1;
             mbar_wait(&sm.acc_full[acc], (c >> 1) & 1);
             tc_fence_after();
-#pragma unroll 1
+            uint32_t ub[2][32];  // ping-pong: the next 32 columns load while these compute
+            tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / 2), ub[0]);
+            tmem_wait_ld();
+#pragma unroll
             for (int q = 0; q < kChunkN / 64; ++q) {
-                uint32_t u[32];
+                uint32_t* u = ub[q & 1];
                 const int cc = part * (kChunkN / 2) + q * 32;
-                tmem_ld32(lane_base + acc * kChunkN + cc, u);
-                tmem_wait_ld();
+                if (q + 1 < kChunkN / 64) tmem_ld32(lane_base + acc * kChunkN + cc + 32, ub[(q + 1) & 1]);
                 const int col0 = c * kChunkN + cc;
                 const float4* bu4 = reinterpret_cast<const float4*>(s_bu + col0);
                 const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
@@ -186,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                         ls[e] = fmaf(z, sv[e], ls[e]);
                     }
                 }
+                if (q + 1 < kChunkN / 64) tmem_wait_ld();
             }
             tc_fence_before();
             __syncwarp();
