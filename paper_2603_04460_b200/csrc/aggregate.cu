@@ -117,77 +117,89 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     const uint32_t t_dia[2] = {tmem + 288, tmem + 320};
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elect_one()) {
             tma_prefetch_desc(&p.map_q);
             tma_prefetch_desc(&p.map_k);
             mbar_arrive_expect_tx(&sm.bar_k, kTile);
             for (int hf = 0; hf < 2; ++hf)
                 tma_load_3d(base + kOffK + hf * kHalf, &p.map_k, &sm.bar_k, hf * 64, g, j0);
-            for (int it = 0; it < num_items; ++it) {
-                const int t = t_first + it / grp;
-                const int h = g * grp + it % grp;
-                const int s = it & 1;
-                if (it >= 2) mbar_wait(&sm.q_empty[s], ((it >> 1) & 1) ^ 1);
+        }
+        __syncwarp();
+        for (int it = 0; it < num_items; ++it) {
+            const int t = t_first + it / grp;
+            const int h = g * grp + it % grp;
+            const int s = it & 1;
+            if (it >= 2) mbar_wait(&sm.q_empty[s], ((it >> 1) & 1) ^ 1);
+            if (elect_one()) {
                 mbar_arrive_expect_tx(&sm.q_full[s], kTile);
                 for (int hf = 0; hf < 2; ++hf)
                     tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
                                 (jb + t) * kBlock);
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
-            const uint32_t idesc_red = umma_idesc_bf16(128, 16, true, false);
-            const uint32_t k_addr = smem_u32(base + kOffK);
-            const uint32_t q_addr = smem_u32(base + kOffQ);
-            const uint32_t p_addr = smem_u32(base + kOffP);
-            const uint32_t ps_addr = smem_u32(base + kOffPS);
-            const uint32_t ones_addr = smem_u32(base + kOffOnes);
-            auto issue_s = [&](int it) {
-                const int s = it & 1;
-                mbar_wait(&sm.q_full[s], (it >> 1) & 1);
-                if (it >= 2) mbar_wait(&sm.s_free[s], ((it >> 1) & 1) ^ 1);
-                tc_fence_after();
+        // MMA issuer: warp-uniform loop, one elected lane issues each batch
+        const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
+        const uint32_t idesc_red = umma_idesc_bf16(128, 16, true, false);
+        const uint64_t k_desc0 = umma_desc_sw128(smem_u32(base + kOffK), 16, 1024);
+        const uint64_t q_desc0 = umma_desc_sw128(smem_u32(base + kOffQ), 16, 1024);
+        const uint64_t ones_desc0 = umma_desc_sw128(smem_u32(base + kOffOnes), 16, 1024);
+        const uint32_t p_addr = smem_u32(base + kOffP);
+        const uint32_t ps_addr = smem_u32(base + kOffPS);
+        auto issue_s = [&](int it) {
+            const int s = it & 1;
+            mbar_wait(&sm.q_full[s], (it >> 1) & 1);
+            if (it >= 2) mbar_wait(&sm.s_free[s], ((it >> 1) & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-                    umma_ss(tmem + s * 128, umma_desc_sw128(q_addr + s * kTile + off, 16, 1024),
-                            umma_desc_sw128(k_addr + off, 16, 1024), idesc_qk, k > 0 ? 1u : 0u);
+                    const uint64_t off = static_cast<uint64_t>(((k >> 2) * kHalf + (k & 3) * 32) >> 4);
+                    umma_ss(tmem + s * 128, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off, k_desc0 + off,
+                            idesc_qk, k > 0 ? 1u : 0u);
                 }
                 umma_commit(&sm.s_full[s]);
                 umma_commit(&sm.q_empty[s]);
-            };
-            // reduction: D[tm] (+)= A^T . 1, A = [128 rows x 128 cols] bf16 (two 16 KB halves)
-            auto issue_red = [&](uint32_t d_t, uint32_t a_base, bool acc) {
+            }
+            __syncwarp();
+        };
+        // reduction: D[tm] (+)= A^T . 1, A = [128 rows x 128 cols] bf16 (two 16 KB halves)
+        auto issue_red = [&](uint32_t d_t, uint32_t a_base, bool acc) {
+            const uint64_t a0 = umma_desc_sw128(a_base, kHalf, 1024);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint64_t adesc = umma_desc_sw128(a_base + k * 2048, kHalf, 1024);
-                    const uint64_t bdesc = umma_desc_sw128(ones_addr + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024);
-                    umma_ss(d_t, adesc, bdesc, idesc_red, (acc || k > 0) ? 1u : 0u);
-                }
-            };
-            mbar_wait(&sm.bar_k, 0);
-            issue_s(0);
-            if (num_items > 1) issue_s(1);
-            for (int it = 0; it < num_items; ++it) {
-                const int tl = it / grp;            // local t index
-                const int t = t_first + tl;
-                const int hi = it % grp;
-                mbar_wait(&sm.p_full, it & 1);
-                tc_fence_after();
+            for (int k = 0; k < 8; ++k)
+                umma_ss(d_t, a0 + static_cast<uint64_t>((k * 2048) >> 4),
+                        ones_desc0 + static_cast<uint64_t>(((k >> 2) * 2048 + (k & 3) * 32) >> 4), idesc_red,
+                        (acc || k > 0) ? 1u : 0u);
+        };
+        mbar_wait(&sm.bar_k, 0);
+        issue_s(0);
+        if (num_items > 1) issue_s(1);
+        for (int it = 0; it < num_items; ++it) {
+            const int tl = it / grp;            // local t index
+            const int t = t_first + tl;
+            const int hi = it % grp;
+            mbar_wait(&sm.p_full, it & 1);
+            tc_fence_after();
+            if (elect_one()) {
                 issue_red(t_col, p_addr, it > 0);
                 if (t >= 1) issue_red(t_dia[(t - 1) & 1], ps_addr, !(tl == 0 && hi == 0));
-                if (hi == 0 && tl >= 1) {
-                    // the accumulator of block t last held block t-2, flushed after the
-                    // previous query block (flush arrival tl-1)
-                    mbar_wait(&sm.flush_done, (tl - 1) & 1);
-                    tc_fence_after();
-                }
+            }
+            __syncwarp();
+            if (hi == 0 && tl >= 1) {
+                // the accumulator of block t last held block t-2, flushed after the
+                // previous query block (flush arrival tl-1)
+                mbar_wait(&sm.flush_done, (tl - 1) & 1);
+                tc_fence_after();
+            }
+            if (elect_one()) {
                 issue_red(t_dia[t & 1], ps_addr + 2 * kHalf, hi != 0);
                 umma_commit(&sm.p_free);
                 if (hi == grp - 1) umma_commit(&sm.d_done);
-                if (it + 2 < num_items) issue_s(it + 2);
             }
+            __syncwarp();
+            if (it + 2 < num_items) issue_s(it + 2);
         }
     } else if (warp >= 4) {
         const int quarter = warp & 3;

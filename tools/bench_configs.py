@@ -78,7 +78,7 @@ def c2():
     q, k, v, _ = planted_layer(n, 32, 8, seed=2026)
     r = layer_stats(q, k, v, params, budget)
     return {"config": "C2 32k adaptive budget (distilled indexer, tau calibrated for recall>=0.9 on a validation "
-                      "prompt)", "tau": [budget.tau_v, budget.tau_s], **r}
+                      "prompt)", "tau": [[b.tau_v, b.tau_s] for b in budget], **r}
 
 
 def c4(layers=36):
