@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--heads-per-chunk", type=int, default=1,
+                    help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
+    ap.add_argument("--e2e-heads-per-chunk", type=int, default=2)
     return ap.parse_args()
 
 
@@ -308,7 +311,14 @@ def main():
     o = torch.empty_like(q)
     lse = torch.empty(hq_r, n, device=dev)
 
+    hpc = args.heads_per_chunk
+
     def step():
+        # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3, pipelined over KV-head chunks
+        _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse)
+        return pat
+
+    def step_unfused():
         a_v, a_s = vsp.indexer_forward(k, v, params)
         pat = vsp.select_pattern(a_v, a_s, budget)
         vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
@@ -356,6 +366,7 @@ def main():
 
     a_v, a_s = vsp.indexer_forward(k, v, params)
     pat = vsp.select_pattern(a_v, a_s, budget)
+    ms_unfused = timed(step_unfused)
     ms_indexer = timed(lambda: vsp.indexer_forward(k, v, params))
     ms_select = timed(lambda: vsp.select_pattern(a_v, a_s, budget))
     ms_attn = timed(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse))
@@ -393,16 +404,12 @@ def main():
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
         oh_ = torch.empty(o.shape, dtype=o.dtype).pin_memory()
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
 
         def e2e_step():
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            vd.copy_(vh, non_blocking=True)
-            a_v_, a_s_ = vsp.indexer_forward(kd, vd, params)
-            pt = vsp.select_pattern(a_v_, a_s_, budget)
-            vsp.sparse_attention(qd, kd, vd, pt, validate=False, out=o, lse=lse)
-            oh_.copy_(o, non_blocking=True)
+            # one host-buffer C-ABI call: H2D of Q/K/V, K1->K2->K3, D2H of O and LSE, pipelined per chunk
+            vsp.vs_prefill_host(qh, kh, vh, params, budget, heads_per_chunk=args.e2e_heads_per_chunk,
+                                out=oh_, lse=lse_h, device=dev)
 
         e2e_step()
         barrier()
@@ -418,7 +425,9 @@ def main():
             torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": n / (float(e2e_ms.item()) * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2),
-               "d2h_bytes_per_step": int(oh_.numel() * 2), "ms_per_step": float(e2e_ms.item())}
+               "d2h_bytes_per_step": int(oh_.numel() * 2 + lse_h.numel() * 4), "ms_per_step": float(e2e_ms.item()),
+               "api": "vsp_vs_prefill_host (pinned host Q/K/V in, host O/LSE out)",
+               "heads_per_chunk": args.e2e_heads_per_chunk}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -433,7 +442,8 @@ def main():
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
 
-    launches_per_step = 2 + 1 + 5  # indexer gemm+softmax, select, memset+bitmaps+gather+plan+attention
+    # per KV-head chunk: indexer gemm + softmax, select, bitmaps + gather + plan, attention
+    launches_per_step = 7 * ((hkv_r + hpc - 1) // hpc)
     if rank == 0:
         line = {
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
@@ -449,6 +459,7 @@ def main():
                        "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
                                  "> L2 so no flush between steps", "parallelism": f"kv-head shard x{world}"},
             "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,
+            "unfused_ms": ms_unfused, "heads_per_chunk": hpc,
             "indexer_ms": ms_indexer, "select_ms": ms_select, "recall": recall,
             "density": pairs_q / dense_pairs, "tile_density": tiles / tiles_dense,
             "k_v": kv_list, "k_s": ks_list, "dense_tflops": dense_tf, "allgather_ms": allgather_ms,

@@ -115,6 +115,37 @@ VSP_API int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const vo
 VSP_API int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace,
                                    int64_t* tiles_out, void* stream);
 
+/* ---- the whole VS-prefill layer: K1 -> K2 -> K3 in one call ------------------------
+ * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads, but
+ * pipelined over KV-head chunks of `heads_per_chunk` (0 = 1): the scoring, selection and
+ * tile planning of chunk c+1 run on a high-priority side stream while chunk c's attention
+ * runs on `stream`. a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
+ * individual calls). Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp
+ * :154-185) on the device. */
+VSP_API size_t vsp_vs_prefill_workspace_size(int n, int hkv, int d_h, int cap);
+VSP_API int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq, int hkv,
+                           int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                           const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                           const vsp_budget* budgets, float* a_v, float* a_s, int* i_v, int* k_v, int* i_s,
+                           int* k_s, int cap, void* o, float* lse, void* workspace, int heads_per_chunk,
+                           void* stream);
+
+/* ---- the layer from HOST buffers (the reference's own calling convention) ----------
+ * The reference operators take and return host memory (std::vector; attention.hpp:150,
+ * tools/vsprefill.cpp:154-185). This entry point does the same: Q/K/V are read from host
+ * memory (pinned for asynchronous copies) and O [n, hq, 128] bf16, LSE [hq, n] (nullable)
+ * and the per-head budgets k_v/k_s [hkv] (nullable) are written back to host memory. The
+ * copies are pipelined with the compute per KV-head chunk: chunk c's K/V/Q travel on one
+ * copy engine while chunk c-1 is scored and attended, and chunk c-1's O returns on the
+ * other copy engine. workspace: device memory of vsp_vs_prefill_host_workspace_size bytes
+ * (it holds the device copies of the inputs and outputs). Stream-ordered on `stream`. */
+VSP_API size_t vsp_vs_prefill_host_workspace_size(int n, int hq, int hkv, int d_h);
+VSP_API int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_h, const void* v_h, int n, int hq,
+                                int hkv, int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                                const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                                const vsp_budget* budgets, void* o_h, float* lse_h, int* k_v_h, int* k_s_h,
+                                void* workspace, int heads_per_chunk, void* stream);
+
 /* ---- K4: dense causal attention forward (the speed-up denominator) ---------------- */
 VSP_API int vsp_dense_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
                        int hkv, int d, float scale, void* o, float* lse, void* stream);

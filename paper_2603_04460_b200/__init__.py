@@ -32,7 +32,7 @@ import torch
 __all__ = [
     "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
     "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
-    "aggregate_streaming", "attention_recall", "vs_prefill", "lib_path", "load_library",
+    "aggregate_streaming", "attention_recall", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "lib_path", "load_library",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -86,6 +86,14 @@ def load_library():
     lib.vsp_vs_aggregate.argtypes = [vp, vp, vp, i, i, i, i, f, vp, i, i, vp, vp, vp, vp]
     lib.vsp_recall_from_lse.argtypes = [vp, vp, vp, i, i, vp, vp]
     lib.vsp_vs_attn_tile_stats.argtypes = [vp, i, i, i, vp, ctypes.POINTER(ctypes.c_int64), vp]
+    lib.vsp_vs_prefill_host_workspace_size.restype = sz
+    lib.vsp_vs_prefill_host_workspace_size.argtypes = [i, i, i, i]
+    lib.vsp_vs_prefill_host.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
+                                         ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, i, vp])
+    lib.vsp_vs_prefill_workspace_size.restype = sz
+    lib.vsp_vs_prefill_workspace_size.argtypes = [i, i, i, i]
+    lib.vsp_vs_prefill.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
+                                    ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, vp])
     _lib = lib
     return lib
 
@@ -317,10 +325,81 @@ def attention_recall(lse_sparse: torch.Tensor, lse_dense: torch.Tensor) -> torch
 
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
-               mapping: str = "reverse"):
-    """The whole VS-prefill hot path of one layer: indexer -> selection -> sparse attention.
-    Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
+               mapping: str = "reverse", heads_per_chunk: int = 1, out: Optional[torch.Tensor] = None,
+               lse: Optional[torch.Tensor] = None):
+    """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
+    indexer -> selection -> sparse attention, pipelined over KV-head chunks so that the
+    scoring/selection/planning of chunk c+1 overlaps chunk c's attention. Mirrors
+    `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
+    Same results as indexer_forward + select_pattern + sparse_attention.
     Returns (O, LSE, SelectedIndices)."""
+    _need_cuda(q, k, v)
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    budgets = list(budget) if isinstance(budget, (list, tuple)) else [budget] * hkv
+    if len(budgets) != hkv:
+        raise VspError("vs_prefill: one BudgetConfig per KV head required")
+    arr = (_Budget * hkv)(*[b._c() for b in budgets])
+    lib = load_library()
+    dev = q.device
+    cap = n + 1
+    a_v = torch.empty(hkv, n, device=dev, dtype=torch.float32)
+    a_s = torch.empty_like(a_v)
+    i_v = torch.empty(hkv, cap, device=dev, dtype=torch.int32)
+    i_s = torch.empty_like(i_v)
+    k_v = torch.empty(hkv, device=dev, dtype=torch.int32)
+    k_s = torch.empty_like(k_v)
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
+    ws = _workspace(dev, lib.vsp_vs_prefill_workspace_size(n, hkv, params.d_h, cap))
+    _check(lib.vsp_vs_prefill(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h,
+                              _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
+                              _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
+                              _ptr(a_v), _ptr(a_s), _ptr(i_v), _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(o),
+                              _ptr(lse), _ptr(ws), int(heads_per_chunk), _stream(dev)))
+    return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
+
+
+def vs_prefill_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
+                    mapping: str = "reverse", heads_per_chunk: int = 2, out: Optional[torch.Tensor] = None,
+                    lse: Optional[torch.Tensor] = None, budgets_out: bool = False, device=None):
+    """vs_prefill from HOST tensors (pinned CPU memory for overlap), like the reference's
+    own operators which take host vectors: one C-ABI call (vsp_vs_prefill_host) that pipelines
+    H2D copies, scoring/selection, attention and the D2H of O per KV-head chunk.
+    Returns (O, LSE) as host tensors (+ (k_v, k_s) host tensors when budgets_out).
+    Stream-ordered: synchronise the current stream before reading the results."""
+    for t in (q, k, v):
+        if t.is_cuda or not t.is_contiguous():
+            raise VspError("vs_prefill_host: q, k, v must be contiguous host tensors")
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    budgets = list(budget) if isinstance(budget, (list, tuple)) else [budget] * hkv
+    if len(budgets) != hkv:
+        raise VspError("vs_prefill: one BudgetConfig per KV head required")
+    arr = (_Budget * hkv)(*[b._c() for b in budgets])
+    lib = load_library()
+    dev = torch.device(device) if device is not None else params.w_u.device
+    o = out if out is not None else torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    lse = lse if lse is not None else torch.empty(hq, n, dtype=torch.float32, pin_memory=True)
+    kv = torch.empty(hkv, dtype=torch.int32, pin_memory=True) if budgets_out else None
+    ks = torch.empty(hkv, dtype=torch.int32, pin_memory=True) if budgets_out else None
+    key = (str(dev), "host_ws")
+    need = lib.vsp_vs_prefill_host_workspace_size(n, hq, hkv, params.d_h)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < need:
+        ws = _ws_cache[key] = torch.empty(need, dtype=torch.uint8, device=dev)
+    _check(lib.vsp_vs_prefill_host(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h,
+                                   _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
+                                   _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
+                                   _ptr(o), _ptr(lse), _ptr(kv), _ptr(ks), _ptr(ws), int(heads_per_chunk),
+                                   _stream(dev)))
+    return (o, lse, kv, ks) if budgets_out else (o, lse)
+
+
+def vs_prefill_unfused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
+                       mapping: str = "reverse"):
+    """vs_prefill as three separate operator calls (indexer_forward, select_pattern,
+    sparse_attention) on one stream: the parity twin of the fused call."""
     a_v, a_s = indexer_forward(k, v, params, mapping)
     pat = select_pattern(a_v, a_s, budget)
     o, lse = sparse_attention(q, k, v, pat, validate=False)

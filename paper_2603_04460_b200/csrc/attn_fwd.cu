@@ -80,11 +80,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     uint8_t* sV = sK + kNumK * kTileBytes;               // kNumV tiles
     __shared__ Smem sm;
 
-    const int heads_per_pair = p.hq / 2;
+    const int heads_per_pair = p.npairs;  // Q-head pairs in this launch, starting at p.pair0
     const int num_qb = (p.n + kBlock - 1) / kBlock;
     // heaviest query blocks first (causal work grows with the block index)
     const int qb = num_qb - 1 - static_cast<int>(blockIdx.x) / heads_per_pair;
-    const int pair = static_cast<int>(blockIdx.x) % heads_per_pair;
+    const int pair = p.pair0 + static_cast<int>(blockIdx.x) % heads_per_pair;
     const int h0 = 2 * pair;
     const int g = h0 / (p.hq / p.hkv);
     const int i0 = qb * kBlock;
@@ -442,8 +442,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 // Caller zeroes them first. grid (ceil(cap/256), hkv).
 __global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
                                      const int* __restrict__ is, const int* __restrict__ ks, int cap,
-                                     int n, int bm_words, uint32_t* vbits, uint32_t* sbits) {
-    const int g = blockIdx.y;
+                                     int n, int bm_words, uint32_t* vbits, uint32_t* sbits, int g0) {
+    const int g = g0 + static_cast<int>(blockIdx.y);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < kv[g]) {
         const int j = iv[static_cast<size_t>(g) * cap + t];
@@ -461,8 +461,8 @@ __global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __re
 // 16 rows per block, 16 threads x 16 B per 256 B row.
 __global__ void gather_vertical_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                                        const int* __restrict__ iv, const int* __restrict__ kv, int cap,
-                                       int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg) {
-    const int g = blockIdx.y;
+                                       int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg, int g0) {
+    const int g = g0 + static_cast<int>(blockIdx.y);
     const int r = blockIdx.x * 16 + (threadIdx.x >> 4);
     const int t = threadIdx.x & 15;
     if (r >= kvcap) return;
@@ -497,8 +497,8 @@ VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
 // breaks); lane 0 emits the finished ranges' tiles in order. grid (ceil(num_qb/4), hkv), 128.
 __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
                                const int* __restrict__ is, const int* __restrict__ ks, int cap, int n,
-                               int num_qb, int list_stride, int* __restrict__ lists) {
-    const int g = blockIdx.y;
+                               int num_qb, int list_stride, int* __restrict__ lists, int g0) {
+    const int g = g0 + static_cast<int>(blockIdx.y);
     const int qb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (qb >= num_qb) return;
@@ -588,7 +588,9 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
         attr_set = true;
     }
     const int num_qb = (a.n + kBlock - 1) / kBlock;
-    dim3 grid(num_qb * (a.hq / 2));
+    p.pair0 = 0;
+    p.npairs = a.hq / 2;
+    dim3 grid(num_qb * p.npairs);
     attn_fwd_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
     return cudaGetLastError();
 }
@@ -607,7 +609,11 @@ size_t sparse_workspace_bytes(int n, int hkv, int cap) {
     return bytes;
 }
 
-cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream) {
+// phase: 1 = plan (bitmaps, vertical gather, tile lists), 2 = attention kernel, 3 = both;
+// only KV heads [g0, g0 + count) are touched, so head ranges can be pipelined on streams.
+cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
+                          int count, int phase) {
+    if (count < 0) count = a.hkv - g0;
     AttnParams p{};
     p.n = a.n;
     p.hq = a.hq;
@@ -643,22 +649,32 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         !vsp_host::make_map_bf16(&p.map_vv, vg, 3, dg, sg, box))
         return cudaErrorInvalidValue;
 
-    cudaError_t e = cudaMemsetAsync(bits, 0, static_cast<size_t>(a.hkv) * bm_words * 4 * 2, stream);
-    if (e != cudaSuccess) return e;
-    build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, a.hkv), 256, 0, stream>>>(
-        s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words);
-    gather_vertical_kernel<<<dim3(kvcap / 16, a.hkv), 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
-        a.n, a.hkv, kvcap, kg, vg);
-    vs_plan_kernel<<<dim3((num_qb + 3) / 4, a.hkv), 128, 0, stream>>>(
-        s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attn_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr_set = true;
+    if (phase & 1) {
+        const size_t words = static_cast<size_t>(bm_words);
+        cudaError_t e = cudaMemsetAsync(bits + static_cast<size_t>(g0) * words, 0, count * words * 4, stream);
+        if (e == cudaSuccess)
+            e = cudaMemsetAsync(bits + (static_cast<size_t>(a.hkv) + g0) * words, 0, count * words * 4, stream);
+        if (e != cudaSuccess) return e;
+        build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, count), 256, 0, stream>>>(
+            s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words, g0);
+        gather_vertical_kernel<<<dim3(kvcap / 16, count), 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
+            a.n, a.hkv, kvcap, kg, vg, g0);
+        vs_plan_kernel<<<dim3((num_qb + 3) / 4, count), 128, 0, stream>>>(
+            s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists, g0);
     }
-    dim3 grid(num_qb * (a.hq / 2));
-    attn_fwd_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    if (phase & 2) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(attn_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+            attr_set = true;
+        }
+        const int pairs_per_group = (a.hq / a.hkv) / 2;
+        p.pair0 = g0 * pairs_per_group;
+        p.npairs = count * pairs_per_group;
+        dim3 grid(num_qb * p.npairs);
+        attn_fwd_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    }
     return cudaGetLastError();
 }
 

@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
+#include <cmath>
 #include <string>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/vsp_gpu.h"
@@ -16,6 +19,15 @@ struct vsp_ctx {
     int device = 0;
     int sm_count = 0;
     int* d_flags = nullptr;  // [1024] validation results
+    // vsp_vs_prefill pipelining: high-priority side stream and per-chunk events
+    static constexpr int kMaxChunks = 64;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_start = nullptr;
+    cudaEvent_t ev_chunk[kMaxChunks] = {};
+    // vsp_vs_prefill_host: copy-engine streams and their events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_host0 = nullptr, ev_host1 = nullptr;
+    cudaEvent_t ev_kv[kMaxChunks] = {}, ev_q[kMaxChunks] = {}, ev_attn[kMaxChunks] = {};
 };
 
 namespace {
@@ -120,6 +132,19 @@ int vsp_create(vsp_ctx** out, int device) {
     ctx->sm_count = prop.multiProcessorCount;
     cudaSetDevice(device);
     e = cudaMalloc(&ctx->d_flags, 1024 * sizeof(int));
+    if (e == cudaSuccess) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&ctx->ev_start, &ctx->ev_host0, &ctx->ev_host1})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    for (int c = 0; c < vsp_ctx::kMaxChunks && e == cudaSuccess; ++c) {
+        for (cudaEvent_t* ev : {&ctx->ev_chunk[c], &ctx->ev_kv[c], &ctx->ev_q[c], &ctx->ev_attn[c]})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         delete ctx;
         return cuda_err(e, "vsp_create");
@@ -132,6 +157,13 @@ int vsp_destroy(vsp_ctx* ctx) {
     if (!ctx) return VSP_OK;
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_flags);
+    for (cudaStream_t st : {ctx->side, ctx->h2d, ctx->d2h})
+        if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_host0, ctx->ev_host1})
+        if (ev) cudaEventDestroy(ev);
+    for (int c = 0; c < vsp_ctx::kMaxChunks; ++c)
+        for (cudaEvent_t ev : {ctx->ev_chunk[c], ctx->ev_kv[c], ctx->ev_q[c], ctx->ev_attn[c]})
+            if (ev) cudaEventDestroy(ev);
     delete ctx;
     return VSP_OK;
 }
@@ -279,4 +311,195 @@ extern "C" int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, con
     if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_tile_stats");
     for (int x = 0; x < 2 + hkv; ++x) tiles_out[x] = t[x];
     return VSP_OK;
+}
+
+// ------------------------------------------------------------------ fused layer
+namespace {
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+struct PrefillDev {
+    const void *q, *k, *v;
+    const void* w_u;
+    const float *b_u, *w_v, *b_v, *w_s, *b_s;
+    float *a_v, *a_s;
+    int *i_v, *k_v, *i_s, *k_s;
+    void* o;
+    float* lse;
+};
+
+int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping, const vsp_budget* budgets,
+                  const void* workspace, int heads_per_chunk, const char* who) {
+    int rc = check_attn_shapes(n, hq, hkv, d);
+    if (rc) return rc;
+    const std::string w(who);
+    if (d_h < 1 || d_h % 256 != 0) return set_err(VSP_EINVAL, w + ": d_h must be a multiple of 256");
+    if (cap < n + 1) return set_err(VSP_EINVAL, w + ": cap must be >= n + 1");
+    if (!workspace || !budgets) return set_err(VSP_EINVAL, w + ": null workspace or budgets");
+    if (hkv > 128) return set_err(VSP_EINVAL, w + ": at most 128 KV heads per call");
+    if (slash_mapping != VSP_SLASH_REVERSE && slash_mapping != VSP_SLASH_IDENTITY)
+        return set_err(VSP_EINVAL, w + ": bad slash mapping");
+    for (int g = 0; g < hkv; ++g) {
+        const vsp_budget& b = budgets[g];
+        if (!(b.tau_v > 0.0 && b.tau_v <= 1.0)) return set_err(VSP_EINVAL, "budget config: tau_v must be in (0, 1]");
+        if (!(b.tau_s > 0.0 && b.tau_s <= 1.0)) return set_err(VSP_EINVAL, "budget config: tau_s must be in (0, 1]");
+        if (b.min_budget < 1) return set_err(VSP_EINVAL, "budget config: min_budget must be >= 1");
+        if (b.max_budget >= 0 && b.min_budget > b.max_budget)
+            return set_err(VSP_EINVAL, "budget config: min_budget exceeds max_budget");
+    }
+    const int hpc = heads_per_chunk < 1 ? 1 : heads_per_chunk;
+    if ((hkv + hpc - 1) / hpc > vsp_ctx::kMaxChunks) return set_err(VSP_EINVAL, w + ": too many chunks");
+    return VSP_OK;
+}
+
+// Enqueue K1 -> K2 -> plan on the side stream and K3 on `main`, chunk by chunk. Chunk c's
+// scoring waits for kv_ready[c] and its attention for q_ready[c] (copy-engine events of
+// the host-buffer entry; null = inputs already resident); attn_done[c] is recorded after
+// chunk c's attention when non-null.
+cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, int hkv, int d, int d_h, int cap,
+                            int slash_mapping, const vsp_budget* budgets, void* workspace, int hpc,
+                            cudaStream_t main, const cudaEvent_t* kv_ready, const cudaEvent_t* q_ready,
+                            const cudaEvent_t* attn_done) {
+    const int chunks = (hkv + hpc - 1) / hpc;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    void* ws_ix = ws;
+    ws += align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
+    void* ws_sel = ws;
+    ws += align256(vsp_select_k::workspace_bytes(n, hkv));
+    void* ws_attn = ws;
+    cudaStream_t side = ctx->side;
+    cudaError_t e = cudaEventRecord(ctx->ev_start, main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
+    vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d))};
+    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+    for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
+        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        if (kv_ready) e = cudaStreamWaitEvent(side, kv_ready[c], 0);
+        vsp_indexer::Args ia{p.k, p.v, n, hkv, d_h, p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s,
+                             slash_mapping == VSP_SLASH_REVERSE, p.a_v, p.a_s, nullptr, nullptr, g0, cnt};
+        if (e == cudaSuccess) e = vsp_indexer::launch(ia, ws_ix, side);
+        if (e == cudaSuccess)
+            e = vsp_select_k::launch(p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s, cap, ws_sel, side,
+                                     g0, cnt);
+        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, side, g0, cnt, 1);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[c], side);
+    }
+    for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
+        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        e = cudaStreamWaitEvent(main, ctx->ev_chunk[c], 0);
+        if (e == cudaSuccess && q_ready) e = cudaStreamWaitEvent(main, q_ready[c], 0);
+        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, g0, cnt, 2);
+        if (e == cudaSuccess && attn_done) e = cudaEventRecord(attn_done[c], main);
+    }
+    return e;
+}
+
+size_t host_staging_bytes(int n, int hq, int hkv, int cap) {
+    const size_t row = 128 * 2;
+    return align256(size_t(n) * hq * row) * 2 + align256(size_t(n) * hkv * row) * 2 +
+           align256(size_t(hq) * n * 4) + align256(size_t(hkv) * n * 4) * 2 + align256(size_t(hkv) * cap * 4) * 2 +
+           align256(size_t(hkv) * 4) * 2;
+}
+}  // namespace
+
+extern "C" size_t vsp_vs_prefill_workspace_size(int n, int hkv, int d_h, int cap) {
+    return align256(vsp_indexer::workspace_bytes(n, hkv, d_h)) + align256(vsp_select_k::workspace_bytes(n, hkv)) +
+           align256(vsp_attn::sparse_workspace_bytes(n, hkv, cap));
+}
+
+extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq, int hkv,
+                              int d, int d_h, const void* w_u, const float* b_u, const float* w_v, const float* b_v,
+                              const float* w_s, const float* b_s, int slash_mapping, const vsp_budget* budgets,
+                              float* a_v, float* a_s, int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* o,
+                              float* lse, void* workspace, int heads_per_chunk, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, heads_per_chunk,
+                           "vsp_vs_prefill");
+    if (rc) return rc;
+    PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse};
+    cudaError_t e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace,
+                                    heads_per_chunk < 1 ? 1 : heads_per_chunk, as_stream(stream), nullptr, nullptr,
+                                    nullptr);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill");
+}
+
+extern "C" size_t vsp_vs_prefill_host_workspace_size(int n, int hq, int hkv, int d_h) {
+    const int cap = n + 1;
+    return vsp_vs_prefill_workspace_size(n, hkv, d_h, cap) + host_staging_bytes(n, hq, hkv, cap);
+}
+
+extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_h, const void* v_h, int n, int hq,
+                                   int hkv, int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                                   const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                                   const vsp_budget* budgets, void* o_h, float* lse_h, int* k_v_h, int* k_s_h,
+                                   void* workspace, int heads_per_chunk, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    const int cap = n + 1;
+    int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, heads_per_chunk,
+                           "vsp_vs_prefill_host");
+    if (rc) return rc;
+    if (!q_h || !k_h || !v_h || !o_h) return set_err(VSP_EINVAL, "vsp_vs_prefill_host: null host buffer");
+    const int hpc = heads_per_chunk < 1 ? 1 : heads_per_chunk;
+    const int chunks = (hkv + hpc - 1) / hpc, grp = hq / hkv;
+    const size_t row = 128 * 2;
+    // device staging after the prefill workspace
+    uint8_t* base = static_cast<uint8_t*>(workspace);
+    uint8_t* s = base + vsp_vs_prefill_workspace_size(n, hkv, d_h, cap);
+    auto take = [&](size_t bytes) {
+        uint8_t* r = s;
+        s += align256(bytes);
+        return r;
+    };
+    uint8_t* q_d = take(size_t(n) * hq * row);
+    uint8_t* o_d = take(size_t(n) * hq * row);
+    uint8_t* k_d = take(size_t(n) * hkv * row);
+    uint8_t* v_d = take(size_t(n) * hkv * row);
+    float* lse_d = reinterpret_cast<float*>(take(size_t(hq) * n * 4));
+    float* av_d = reinterpret_cast<float*>(take(size_t(hkv) * n * 4));
+    float* as_d = reinterpret_cast<float*>(take(size_t(hkv) * n * 4));
+    int* iv_d = reinterpret_cast<int*>(take(size_t(hkv) * cap * 4));
+    int* is_d = reinterpret_cast<int*>(take(size_t(hkv) * cap * 4));
+    int* kv_d = reinterpret_cast<int*>(take(size_t(hkv) * 4));
+    int* ks_d = reinterpret_cast<int*>(take(size_t(hkv) * 4));
+
+    cudaStream_t main = as_stream(stream);
+    cudaError_t e = cudaEventRecord(ctx->ev_host0, main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->h2d, ctx->ev_host0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->d2h, ctx->ev_host0, 0);
+    // H2D per chunk: this chunk's K and V columns (strided rows of cnt heads), then its Q heads
+    const uint8_t* qh = static_cast<const uint8_t*>(q_h);
+    const uint8_t* kh = static_cast<const uint8_t*>(k_h);
+    const uint8_t* vh = static_cast<const uint8_t*>(v_h);
+    for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
+        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        const size_t kvoff = size_t(g0) * row, kvw = size_t(cnt) * row, kvp = size_t(hkv) * row;
+        e = cudaMemcpy2DAsync(k_d + kvoff, kvp, kh + kvoff, kvp, kvw, n, cudaMemcpyHostToDevice, ctx->h2d);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(v_d + kvoff, kvp, vh + kvoff, kvp, kvw, n, cudaMemcpyHostToDevice, ctx->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_kv[c], ctx->h2d);
+        const size_t qoff = size_t(g0) * grp * row, qw = size_t(cnt) * grp * row, qp = size_t(hq) * row;
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(q_d + qoff, qp, qh + qoff, qp, qw, n, cudaMemcpyHostToDevice, ctx->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q[c], ctx->h2d);
+    }
+    PrefillDev p{q_d, k_d, v_d, w_u, b_u, w_v, b_v, w_s, b_s, av_d, as_d, iv_d, kv_d, is_d, ks_d, o_d, lse_d};
+    if (e == cudaSuccess)
+        e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, hpc, main, ctx->ev_kv,
+                            ctx->ev_q, ctx->ev_attn);
+    // D2H per chunk as its attention lands: O columns, LSE rows
+    uint8_t* oh = static_cast<uint8_t*>(o_h);
+    for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
+        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        const size_t qoff = size_t(g0) * grp * row, qw = size_t(cnt) * grp * row, qp = size_t(hq) * row;
+        e = cudaStreamWaitEvent(ctx->d2h, ctx->ev_attn[c], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(oh + qoff, qp, o_d + qoff, qp, qw, n, cudaMemcpyDeviceToHost, ctx->d2h);
+        if (e == cudaSuccess && lse_h)
+            e = cudaMemcpyAsync(lse_h + size_t(g0) * grp * n, lse_d + size_t(g0) * grp * n,
+                                size_t(cnt) * grp * n * 4, cudaMemcpyDeviceToHost, ctx->d2h);
+    }
+    if (e == cudaSuccess && k_v_h) e = cudaMemcpyAsync(k_v_h, kv_d, size_t(hkv) * 4, cudaMemcpyDeviceToHost, ctx->d2h);
+    if (e == cudaSuccess && k_s_h) e = cudaMemcpyAsync(k_s_h, ks_d, size_t(hkv) * 4, cudaMemcpyDeviceToHost, ctx->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_host1, ctx->d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ctx->ev_host1, 0);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_host");
 }

@@ -43,6 +43,7 @@ struct __align__(64) Params {
     float* logit_v;  // [hkv, n]
     float* logit_s;  // [hkv, n] (mapping applied)
     int n, hkv, d_h;
+    int g0;
     int reverse;
 };
 
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     float* s_ws = s_wv + kMaxDh;
     __shared__ Smem sm;
 
-    const int g = blockIdx.y;
+    const int g = p.g0 + static_cast<int>(blockIdx.y);
     const int t0 = blockIdx.x * kTok;
     const int num_chunks = p.d_h / kChunkN;
     const uint32_t warp = warp_id();
@@ -223,8 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
 // scores sum to 1 within fp32 rounding (select's |sum - 1| <= 1e-6 check, sparsity.hpp:61).
 // grid (hkv, 2), 1024 threads.
 __global__ void __launch_bounds__(1024) softmax_rows_kernel(const float* __restrict__ lv, const float* __restrict__ ls,
-                                                           float* __restrict__ av, float* __restrict__ as, int n) {
-    const int g = blockIdx.x;
+                                                           float* __restrict__ av, float* __restrict__ as, int n, int g0) {
+    const int g = g0 + static_cast<int>(blockIdx.x);
     const float* x = (blockIdx.y == 0 ? lv : ls) + static_cast<size_t>(g) * n;
     float* y = (blockIdx.y == 0 ? av : as) + static_cast<size_t>(g) * n;
     __shared__ float red_f[32];
@@ -294,9 +295,11 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
         cudaFuncSetAttribute(indexer_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr = true;
     }
-    dim3 grid((a.n + kTok - 1) / kTok, a.hkv);
+    const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
+    p.g0 = a.g0;
+    dim3 grid((a.n + kTok - 1) / kTok, count);
     indexer_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
-    softmax_rows_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(lv, ls, a.a_v, a.a_s, a.n);
+    softmax_rows_kernel<<<dim3(count, 2), 1024, 0, stream>>>(lv, ls, a.a_v, a.a_s, a.n, a.g0);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,8 @@ struct Args {
     float* a_s;       // [hkv, n]
     float* logits_v;  // [hkv, n] or null
     float* logits_s;  // [hkv, n] or null
+    int g0 = 0;       // first KV head of this launch (head-range launches for pipelining)
+    int count = -1;   // number of KV heads (-1: all from g0)
 };
 
 size_t workspace_bytes(int n, int hkv, int d_h);

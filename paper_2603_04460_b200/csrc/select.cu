@@ -41,6 +41,7 @@ struct Params {
     uint32_t* scratch;  // [2*hkv, 2 * npow2]
     int* status;        // [2*hkv]: 0 ok, 1 negative score, 2 sum != 1
     int n, hkv, cap, npow2;
+    int g0;  // first KV head of this launch
     double tau[2][kMaxHeads];
     long long min_b[kMaxHeads];
     long long max_b[kMaxHeads];
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
     uint32_t* scanbuf = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Shared));  // 64 words
 
     const int dir = blockIdx.y;
-    const int g = blockIdx.x;
+    const int g = p.g0 + static_cast<int>(blockIdx.x);
     const int n = p.n;
     const float* x = p.a[dir] + static_cast<size_t>(g) * n;
     const double tau = p.tau[dir][g];
@@ -423,10 +424,10 @@ size_t workspace_bytes(int n, int hkv) {
 }
 
 cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets, int* i_v,
-                   int* k_v, int* i_s, int* k_s, int cap, void* workspace, cudaStream_t stream) {
+                   int* k_v, int* i_s, int* k_s, int cap, void* workspace, cudaStream_t stream, int g0, int count) {
     if (hkv > kMaxHeads) return cudaErrorInvalidValue;
-    static Params p;  // large param block; copied into the launch
-    p = Params{};
+    if (count < 0) count = hkv - g0;
+    Params p{};  // ~3 KB parameter block, copied into the launch
     p.a[0] = a_v;
     p.a[1] = a_s;
     p.idx[0] = i_v;
@@ -452,7 +453,8 @@ cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp
         cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    select_kernel<<<dim3(hkv, 2), kThreads, smem, stream>>>(p);
+    p.g0 = g0;
+    select_kernel<<<dim3(count, 2), kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

@@ -10,7 +10,7 @@ namespace vsp_select_k {
 size_t workspace_bytes(int n, int hkv);
 cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets,
                    int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* workspace,
-                   cudaStream_t stream);
+                   cudaStream_t stream, int g0 = 0, int count = -1);
 // Per-(direction, head) validation status written by the last launch on this workspace:
 // [2*hkv] ints, dir-major: 0 ok, 1 negative score, 2 scores do not sum to 1.
 const int* status_ptr(void* workspace, int n, int hkv);

@@ -230,3 +230,63 @@ def test_vs_prefill_end_to_end(vsp):
     lists = [pat.lists(g) for g in range(hkv)]
     o_ref, lse_ref = oracle_sparse(q, k, v, lists)
     assert_attn_close(o, lse, o_ref, lse_ref)
+
+
+@pytest.mark.parametrize("hpc", [1, 3, 4, 0])
+def test_vs_prefill_fused_matches_unfused(vsp, hpc):
+    """The pipelined one-call layer (vsp_vs_prefill, chunks on a side stream) is bit-identical
+    to the three operator calls, including a ragged last chunk (hkv=4, 3 heads per chunk)
+    and per-KV-head budgets."""
+    from helpers import qkv
+    n, hq, hkv = 1100, 8, 4
+    q, k, v = qkv(n, hq, hkv, seed=7)
+    p = _params(vsp, hkv, 256, seed=5, sigma=0.5)
+    budgets = [vsp.BudgetConfig(0.3 + 0.15 * g, 0.6 - 0.1 * g, 1 + g, None if g != 2 else 40) for g in range(hkv)]
+    o_f, lse_f, pat_f = vsp.vs_prefill(q, k, v, p, budgets, heads_per_chunk=hpc)
+    o_u, lse_u, pat_u = vsp.vs_prefill_unfused(q, k, v, p, budgets)
+    torch.cuda.synchronize()
+    assert torch.equal(pat_f.k_v, pat_u.k_v) and torch.equal(pat_f.k_s, pat_u.k_s)
+    for g in range(hkv):
+        assert pat_f.lists(g) == pat_u.lists(g)
+    assert torch.equal(o_f, o_u)
+    assert torch.equal(lse_f, lse_u)
+
+
+def test_vs_prefill_rejects_bad_budget_count(vsp):
+    from helpers import qkv
+    q, k, v = qkv(256, 4, 2, seed=1)
+    p = _params(vsp, 2, 256, seed=1, sigma=0.5)
+    with pytest.raises(vsp.VspError, match="one BudgetConfig per KV head"):
+        vsp.vs_prefill(q, k, v, p, [vsp.BudgetConfig()] * 3)
+    with pytest.raises(vsp.VspError, match="tau_s must be in"):
+        vsp.vs_prefill(q, k, v, p, vsp.BudgetConfig(0.9, 0.0))
+
+
+@pytest.mark.parametrize("hpc", [1, 3])
+def test_vs_prefill_host_matches_device(vsp, hpc):
+    """The host-buffer layer call (pipelined H2D / compute / D2H per KV-head chunk) returns
+    exactly the device call's O, LSE and budgets."""
+    from helpers import qkv
+    n, hq, hkv = 1100, 8, 4
+    q, k, v = qkv(n, hq, hkv, seed=9)
+    p = _params(vsp, hkv, 256, seed=6, sigma=0.5)
+    budgets = [vsp.BudgetConfig(0.4 + 0.1 * g, 0.5, 1, None) for g in range(hkv)]
+    o_d, lse_d, pat = vsp.vs_prefill(q, k, v, p, budgets)
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    o_h, lse_h, kv_h, ks_h = vsp.vs_prefill_host(qh, kh, vh, p, budgets, heads_per_chunk=hpc, budgets_out=True)
+    torch.cuda.synchronize()
+    assert torch.equal(o_h, o_d.cpu())
+    assert torch.equal(lse_h, lse_d.cpu())
+    assert torch.equal(kv_h, pat.k_v.cpu()) and torch.equal(ks_h, pat.k_s.cpu())
+    # pageable host memory is accepted too (copies are then synchronous)
+    o_p, lse_p = vsp.vs_prefill_host(q.cpu(), k.cpu(), v.cpu(), p, budgets, heads_per_chunk=hpc)
+    torch.cuda.synchronize()
+    assert torch.equal(o_p, o_d.cpu())
+
+
+def test_vs_prefill_host_rejects_device_tensors(vsp):
+    from helpers import qkv
+    q, k, v = qkv(256, 4, 2, seed=1)
+    p = _params(vsp, 2, 256, seed=1, sigma=0.5)
+    with pytest.raises(vsp.VspError, match="contiguous host tensors"):
+        vsp.vs_prefill_host(q, k.cpu(), v.cpu(), p, vsp.BudgetConfig())
