@@ -67,9 +67,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--heads-per-chunk", type=int, default=1,
+    ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
-    ap.add_argument("--e2e-heads-per-chunk", type=int, default=2)
+    ap.add_argument("--e2e-heads-per-chunk", type=int, default=1)
     return ap.parse_args()
 
 
@@ -443,7 +443,7 @@ def main():
                    "sample": f"failed: {ex}"}
 
     # per KV-head chunk: indexer gemm + softmax, select, bitmaps + gather + plan, attention
-    launches_per_step = 7 * ((hkv_r + hpc - 1) // hpc)
+    launches_per_step = 7 * (((hkv_r + hpc - 1) // hpc) if hpc > 0 else min(2, hkv_r))
     if rank == 0:
         line = {
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,

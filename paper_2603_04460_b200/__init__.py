@@ -325,7 +325,7 @@ def attention_recall(lse_sparse: torch.Tensor, lse_dense: torch.Tensor) -> torch
 
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
-               mapping: str = "reverse", heads_per_chunk: int = 1, out: Optional[torch.Tensor] = None,
+               mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
                lse: Optional[torch.Tensor] = None):
     """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
     indexer -> selection -> sparse attention, pipelined over KV-head chunks so that the
@@ -361,7 +361,7 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
 
 
 def vs_prefill_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
-                    mapping: str = "reverse", heads_per_chunk: int = 2, out: Optional[torch.Tensor] = None,
+                    mapping: str = "reverse", heads_per_chunk: int = 1, out: Optional[torch.Tensor] = None,
                     lse: Optional[torch.Tensor] = None, budgets_out: bool = False, device=None):
     """vs_prefill from HOST tensors (pinned CPU memory for overlap), like the reference's
     own operators which take host vectors: one C-ABI call (vsp_vs_prefill_host) that pipelines

@@ -317,6 +317,20 @@ extern "C" int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, con
 namespace {
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// KV-head chunk schedule of the pipelined layer: hpc > 0 gives uniform chunks of hpc heads;
+// hpc == 0 (automatic) runs the first KV head alone, so attention starts after scoring and
+// selecting one head, and the remaining heads as one chunk whose preparation overlaps it.
+int num_chunks(int hkv, int hpc) { return hpc > 0 ? (hkv + hpc - 1) / hpc : (hkv > 1 ? 2 : 1); }
+void chunk_range(int c, int hkv, int hpc, int& g0, int& cnt) {
+    if (hpc > 0) {
+        g0 = c * hpc;
+        cnt = std::min(hpc, hkv - g0);
+    } else {
+        g0 = c == 0 ? 0 : 1;
+        cnt = c == 0 ? 1 : hkv - 1;
+    }
+}
+
 struct PrefillDev {
     const void *q, *k, *v;
     const void* w_u;
@@ -346,8 +360,8 @@ int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_map
         if (b.max_budget >= 0 && b.min_budget > b.max_budget)
             return set_err(VSP_EINVAL, "budget config: min_budget exceeds max_budget");
     }
-    const int hpc = heads_per_chunk < 1 ? 1 : heads_per_chunk;
-    if ((hkv + hpc - 1) / hpc > vsp_ctx::kMaxChunks) return set_err(VSP_EINVAL, w + ": too many chunks");
+    if (heads_per_chunk < 0) return set_err(VSP_EINVAL, w + ": heads_per_chunk must be >= 0");
+    if (num_chunks(hkv, heads_per_chunk) > vsp_ctx::kMaxChunks) return set_err(VSP_EINVAL, w + ": too many chunks");
     return VSP_OK;
 }
 
@@ -359,7 +373,7 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
                             int slash_mapping, const vsp_budget* budgets, void* workspace, int hpc,
                             cudaStream_t main, const cudaEvent_t* kv_ready, const cudaEvent_t* q_ready,
                             const cudaEvent_t* attn_done) {
-    const int chunks = (hkv + hpc - 1) / hpc;
+    const int chunks = num_chunks(hkv, hpc);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     void* ws_ix = ws;
     ws += align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
@@ -372,7 +386,8 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
     vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d))};
     vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
-        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        int g0, cnt;
+        chunk_range(c, hkv, hpc, g0, cnt);
         if (kv_ready) e = cudaStreamWaitEvent(side, kv_ready[c], 0);
         vsp_indexer::Args ia{p.k, p.v, n, hkv, d_h, p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s,
                              slash_mapping == VSP_SLASH_REVERSE, p.a_v, p.a_s, nullptr, nullptr, g0, cnt};
@@ -384,7 +399,8 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[c], side);
     }
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
-        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        int g0, cnt;
+        chunk_range(c, hkv, hpc, g0, cnt);
         e = cudaStreamWaitEvent(main, ctx->ev_chunk[c], 0);
         if (e == cudaSuccess && q_ready) e = cudaStreamWaitEvent(main, q_ready[c], 0);
         if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, g0, cnt, 2);
@@ -417,7 +433,7 @@ extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const 
     if (rc) return rc;
     PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse};
     cudaError_t e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace,
-                                    heads_per_chunk < 1 ? 1 : heads_per_chunk, as_stream(stream), nullptr, nullptr,
+                                    heads_per_chunk, as_stream(stream), nullptr, nullptr,
                                     nullptr);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill");
 }
@@ -438,8 +454,8 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
                            "vsp_vs_prefill_host");
     if (rc) return rc;
     if (!q_h || !k_h || !v_h || !o_h) return set_err(VSP_EINVAL, "vsp_vs_prefill_host: null host buffer");
-    const int hpc = heads_per_chunk < 1 ? 1 : heads_per_chunk;
-    const int chunks = (hkv + hpc - 1) / hpc, grp = hq / hkv;
+    const int hpc = heads_per_chunk;
+    const int chunks = num_chunks(hkv, hpc), grp = hq / hkv;
     const size_t row = 128 * 2;
     // device staging after the prefill workspace
     uint8_t* base = static_cast<uint8_t*>(workspace);
@@ -470,7 +486,8 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
     const uint8_t* kh = static_cast<const uint8_t*>(k_h);
     const uint8_t* vh = static_cast<const uint8_t*>(v_h);
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
-        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        int g0, cnt;
+        chunk_range(c, hkv, hpc, g0, cnt);
         const size_t kvoff = size_t(g0) * row, kvw = size_t(cnt) * row, kvp = size_t(hkv) * row;
         e = cudaMemcpy2DAsync(k_d + kvoff, kvp, kh + kvoff, kvp, kvw, n, cudaMemcpyHostToDevice, ctx->h2d);
         if (e == cudaSuccess)
@@ -488,7 +505,8 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
     // D2H per chunk as its attention lands: O columns, LSE rows
     uint8_t* oh = static_cast<uint8_t*>(o_h);
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
-        const int g0 = c * hpc, cnt = std::min(hpc, hkv - g0);
+        int g0, cnt;
+        chunk_range(c, hkv, hpc, g0, cnt);
         const size_t qoff = size_t(g0) * grp * row, qw = size_t(cnt) * grp * row, qp = size_t(hq) * row;
         e = cudaStreamWaitEvent(ctx->d2h, ctx->ev_attn[c], 0);
         if (e == cudaSuccess)

@@ -7,31 +7,44 @@
 //         output ascending
 //   inject_offset_zero(I_s)               (:99-101)
 //
-// One CTA (1024 threads) per (head, direction); no sort on the fast path:
+// One 8-CTA thread-block cluster per (head, direction); each CTA owns a contiguous 1/8 of
+// the n scores, the CTAs exchange their radix histograms through distributed shared memory
+// and every CTA takes the same decisions. No sort on the fast path:
 //   1. mass radix-select: 4 MSB-first passes over the fp32 bit pattern (non-negative floats
 //      order like their bits). Per-warp private histograms of (count, mass) where mass is
-//      u64 fixed point x*2^62 (exact to 2^-62 per element, deterministic integer atomics).
-//      The crossing value v*, the count and mass strictly above it give k.
+//      u64 fixed point x*2^62 (exact to 2^-62 per element, deterministic integer sums);
+//      lanes of a warp that hit the same bucket are merged first (match.any + redux), so the
+//      concentrated score distributions of real layers do not serialise on one bucket.
+//      The crossing value v*, the count and mass strictly above it give k. The first pass
+//      also performs the reference's score validation.
 //   2. exactness guard: the reference sums the sorted doubles sequentially in f64. If our
 //      exact prefix masses at k-1 and k sit farther from the threshold than the worst-case
 //      f64 rounding of that sequential sum, k is provably identical. Otherwise (rare: the
 //      crossing lands within ~1e-11 of tau) the CTA falls back to the reference algorithm
 //      verbatim: bitonic sort of the scores in scratch, then a sequential f64 sum.
-//   3. count radix-select for the k-th largest value T and the number of ties to take.
-//   4. ordered compaction (two block scans per 8192-element chunk) writes indices ascending,
-//      taking equal-to-T elements lowest index first; offset 0 is injected for slash.
+//   3. only when min/max clamping or the fallback moved k: count radix-select for the k-th
+//      largest value T (otherwise T = v* and the ties to take follow from pass 1).
+//   4. ordered compaction: per-CTA counts of elements above T and equal to T are known from
+//      the exchanged histograms, so each CTA writes its slice's indices ascending at its
+//      own offset (two block scans per chunk), ties to T lowest index first; offset 0 is
+//      injected for slash.
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "select.h"
 
 namespace vsp_select_k {
 
-constexpr int kThreads = 1024;
+namespace cg = cooperative_groups;
+
+constexpr int kCluster = 8;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 8;
 constexpr int kMaxHeads = 128;
+constexpr uint32_t kNoBucket = 256u;
 constexpr double kFixScale = 4611686018427387904.0;  // 2^62
 
 struct Params {
@@ -47,21 +60,28 @@ struct Params {
     long long max_b[kMaxHeads];
 };
 
+// What one CTA publishes to its cluster each pass (double-buffered by pass parity).
+struct Exchange {
+    uint32_t c[256];
+    unsigned long long m[256];
+    int bad, big;
+    long long k;  // fallback result (rank 0)
+};
+
 struct Shared {
     uint32_t hc[kWarps][256];
     unsigned long long hm[kWarps][256];
-    uint32_t tc[256];
+    Exchange ex[2];
+    uint32_t tc[256];            // cluster-wide histogram of the current pass
     unsigned long long tm[256];
-    uint32_t scan_a[kWarps];
-    uint32_t scan_b[kWarps];
+    uint32_t loc[kCluster][256]; // per-rank counts of the current pass
+    uint32_t rank_above[kCluster];
+    uint32_t rank_eq[kCluster];
+    uint32_t scan[64];
     unsigned long long red[kWarps];
-    int flag;
-    uint32_t prefix;
-    uint32_t cnt_above;
-    unsigned long long mass_above;
     int found;
-    int ambiguous;
-    long long k;
+    int bad, big;
+    long long base_pos, eq_base;
 };
 
 __device__ __forceinline__ unsigned long long to_fix(float x) {
@@ -69,26 +89,57 @@ __device__ __forceinline__ unsigned long long to_fix(float x) {
     return static_cast<unsigned long long>(__float2ull_rz(fminf(x, 2.0f) * 4611686018427387904.0f));
 }
 
-// Fill tc/tm with the histogram of digit (bits >> shift) & 255 over elements whose bits
-// above (shift + 8) equal `prefix`. with_mass = false skips the mass atomics.
-__device__ void histogram(Shared& sh, const float* __restrict__ x, int n, uint32_t prefix, int shift, bool with_mass) {
-    const int warp = threadIdx.x >> 5;
-    for (int b = threadIdx.x & 31; b < 256; b += 32) {
+// Local histogram of digit (bits >> shift) & 255 over this CTA's slice [lo, hi), restricted
+// to elements whose bits above (shift + 8) equal `prefix`, published to ex[parity]; then
+// the cluster-wide histogram (tc, tm) and the per-rank counts (loc) are gathered over DSMEM.
+// `validate` also records negative/NaN (bad) and > 1.5 (big) scores.
+__device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const float* __restrict__ x, int lo,
+                                  int hi, uint32_t prefix, int shift, bool with_mass, bool validate, int parity) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = lane; b < 256; b += 32) {
         sh.hc[warp][b] = 0;
         sh.hm[warp][b] = 0ull;
     }
-    __syncthreads();
+    __syncwarp();
     const uint32_t hi_mask = (shift + 8 >= 32) ? 0u : (0xffffffffu << (shift + 8));
-    for (int i = threadIdx.x; i < n; i += kThreads) {
-        const float v = __ldg(x + i);
-        const uint32_t bits = __float_as_uint(v);
-        if ((bits & hi_mask) == (prefix & hi_mask)) {
-            const uint32_t b = (bits >> shift) & 255u;
-            atomicAdd(&sh.hc[warp][b], 1u);
-            if (with_mass) atomicAdd(&sh.hm[warp][b], to_fix(v));
+    int bad = 0, big = 0;
+    const int span = hi - lo;
+    const int iters = span > 0 ? (span + kThreads - 1) / kThreads : 0;  // uniform across the CTA
+    for (int it = 0; it < iters; ++it) {
+        const int i = lo + it * kThreads + threadIdx.x;
+        float v = 0.f;
+        uint32_t key = kNoBucket;
+        if (i < hi) {
+            v = __ldg(x + i);
+            const uint32_t bits = __float_as_uint(v);
+            if (validate) {
+                if (!(v >= 0.f)) bad = 1;
+                else if (v > 1.5f) big = 1;
+            }
+            if ((bits & hi_mask) == (prefix & hi_mask)) key = (bits >> shift) & 255u;
         }
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        const bool leader = lane == __ffs(peers) - 1;
+        if (with_mass) {
+            const unsigned long long f = key != kNoBucket ? to_fix(v) : 0ull;
+            const uint32_t s0 = __reduce_add_sync(peers, static_cast<uint32_t>(f & 0x1fffffu));
+            const uint32_t s1 = __reduce_add_sync(peers, static_cast<uint32_t>((f >> 21) & 0x1fffffu));
+            const uint32_t s2 = __reduce_add_sync(peers, static_cast<uint32_t>(f >> 42));
+            if (leader && key != kNoBucket)
+                sh.hm[warp][key] += static_cast<unsigned long long>(s0) + (static_cast<unsigned long long>(s1) << 21) +
+                                    (static_cast<unsigned long long>(s2) << 42);
+        }
+        // one leader per distinct key per warp: plain read-modify-write of the warp's own row
+        if (leader && key != kNoBucket) sh.hc[warp][key] += __popc(peers);
+        __syncwarp();
     }
-    __syncthreads();
+    if (validate) {
+        bad = __syncthreads_or(bad);
+        big = __syncthreads_or(big);
+    } else {
+        __syncthreads();
+    }
+    Exchange& mine = sh.ex[parity];
     if (threadIdx.x < 256) {
         uint32_t c = 0;
         unsigned long long m = 0;
@@ -96,30 +147,57 @@ __device__ void histogram(Shared& sh, const float* __restrict__ x, int n, uint32
             c += sh.hc[w][threadIdx.x];
             m += sh.hm[w][threadIdx.x];
         }
+        mine.c[threadIdx.x] = c;
+        mine.m[threadIdx.x] = m;
+    }
+    if (threadIdx.x == 0) {
+        mine.bad = bad;
+        mine.big = big;
+    }
+    cluster.sync();
+    if (threadIdx.x < 256) {
+        uint32_t c = 0;
+        unsigned long long m = 0;
+#pragma unroll
+        for (int r = 0; r < kCluster; ++r) {
+            const Exchange* e = cluster.map_shared_rank(&mine, r);
+            const uint32_t cr = e->c[threadIdx.x];
+            sh.loc[r][threadIdx.x] = cr;
+            c += cr;
+            if (with_mass) m += e->m[threadIdx.x];
+        }
         sh.tc[threadIdx.x] = c;
         sh.tm[threadIdx.x] = m;
+    }
+    if (validate && threadIdx.x == 0) {
+        int b = 0, g = 0;
+        for (int r = 0; r < kCluster; ++r) {
+            const Exchange* e = cluster.map_shared_rank(&mine, r);
+            b |= e->bad;
+            g |= e->big;
+        }
+        sh.bad = b;
+        sh.big = g;
     }
     __syncthreads();
 }
 
 // Warp 0 scans buckets from 255 down and finds the first bucket where
-// base + cumulative(key) >= target (key = mass if use_mass else count). Writes found bucket
-// (or -1) and the totals strictly above it into sh.
+// base + cumulative(key) >= target (key = mass if use_mass else count). Returns the bucket
+// (or -1) and the totals strictly above it.
 __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long target, bool use_mass,
-                         int& bucket, unsigned long long& above_key, uint32_t& above_cnt, unsigned long long& above_mass) {
+                         int& bucket, uint32_t& above_cnt, unsigned long long& above_mass) {
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         // lane L owns buckets 255-8L ... 248-8L (descending)
-        unsigned long long seg = 0;
+        unsigned long long seg = 0, segm = 0;
         uint32_t segc = 0;
-        unsigned long long segm = 0;
         for (int t = 0; t < 8; ++t) {
             const int b = 255 - 8 * lane - t;
             seg += use_mass ? sh.tm[b] : sh.tc[b];
             segc += sh.tc[b];
             segm += sh.tm[b];
         }
-        // exclusive prefix over lanes
         unsigned long long pre = seg, prec = segc, prem = segm;
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long a = __shfl_up_sync(0xffffffffu, pre, o);
@@ -136,13 +214,12 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
         prem -= segm;
         int hit = -1;
         unsigned long long run = base + pre, runc = prec, runm = prem;
-        unsigned long long hk = 0, hc = 0, hm = 0;
+        unsigned long long hc = 0, hm = 0;
         for (int t = 0; t < 8; ++t) {
             const int b = 255 - 8 * lane - t;
             const unsigned long long key = use_mass ? sh.tm[b] : sh.tc[b];
             if (hit < 0 && run + key >= target && sh.tc[b] > 0) {
                 hit = b;
-                hk = run - base;
                 hc = runc;
                 hm = runm;
             }
@@ -153,12 +230,10 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
         const unsigned ballot = __ballot_sync(0xffffffffu, hit >= 0);
         const int first = ballot ? __ffs(ballot) - 1 : 0;
         hit = __shfl_sync(0xffffffffu, hit, first);
-        hk = __shfl_sync(0xffffffffu, hk, first);
         hc = __shfl_sync(0xffffffffu, hc, first);
         hm = __shfl_sync(0xffffffffu, hm, first);
         if (lane == 0) {
             sh.found = ballot ? hit : -1;
-            sh.red[0] = hk;
             sh.red[1] = hc;
             sh.red[2] = hm;
         }
@@ -166,9 +241,19 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
     }
     __syncthreads();
     bucket = sh.found;
-    above_key = bucket >= 0 ? sh.red[0] : 0;
     above_cnt = bucket >= 0 ? static_cast<uint32_t>(sh.red[1]) : 0;
     above_mass = bucket >= 0 ? sh.red[2] : 0;
+    // per-rank counts strictly above the chosen bucket, and (last pass) equal to it
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (bucket >= 0 && warp < kCluster) {
+        uint32_t s = 0;
+        for (int b = bucket + 1 + lane; b < 256; b += 32) s += sh.loc[warp][b];
+        s = __reduce_add_sync(0xffffffffu, s);
+        if (lane == 0) {
+            sh.rank_above[warp] += s;
+            sh.rank_eq[warp] = sh.loc[warp][bucket];
+        }
+    }
     __syncthreads();
 }
 
@@ -183,14 +268,14 @@ __device__ uint32_t block_scan(uint32_t v, uint32_t* buf, uint32_t& total) {
     if (lane == 31) buf[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = buf[lane];
+        uint32_t w = lane < kWarps ? buf[lane] : 0u;
         uint32_t wi = w;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t a = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= o) wi += a;
         }
         buf[lane] = wi - w;
-        if (lane == 31) buf[32 + 0] = wi;  // stash total just past the warp slots (buf has >= 33)
+        if (lane == 31) buf[32] = wi;
     }
     __syncthreads();
     const uint32_t res = buf[warp] + inc - v;
@@ -199,65 +284,61 @@ __device__ uint32_t block_scan(uint32_t v, uint32_t* buf, uint32_t& total) {
     return res;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_constant__ Params p) {
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
+    select_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
-    uint32_t* scanbuf = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Shared));  // 64 words
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
 
     const int dir = blockIdx.y;
-    const int g = p.g0 + static_cast<int>(blockIdx.x);
+    const int g = p.g0 + static_cast<int>(blockIdx.x) / kCluster;
     const int n = p.n;
     const float* x = p.a[dir] + static_cast<size_t>(g) * n;
     const double tau = p.tau[dir][g];
-
-    // ---- validation (sparsity.hpp:60-61): non-negative, sum within 1e-6 of 1
-    {
-        int bad = 0, big = 0;
-        unsigned long long s = 0;
-        for (int i = threadIdx.x; i < n; i += kThreads) {
-            const float v = __ldg(x + i);
-            if (!(v >= 0.f)) bad = 1;       // negative or NaN
-            else if (v > 1.5f) big = 1;     // cannot sum to 1 without negatives
-            else s += to_fix(v);
-        }
-        bad = __syncthreads_or(bad);
-        big = __syncthreads_or(big);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long t = 0;
-            for (int w = 0; w < kWarps; ++w) t += sh.red[w];
-            const double total = static_cast<double>(t) / kFixScale;
-            int st = 0;
-            if (bad) st = 1;
-            else if (big || fabs(total - 1.0) > 1e-6) st = 2;
-            sh.flag = st;
-            if (p.status) p.status[dir * p.hkv + g] = st;
-        }
-        __syncthreads();
-        // Invalid scores are reported through `status` (the C ABI raises the reference's
-        // error under VSP_VALIDATE); without validation the selection still runs on them.
-        if (sh.flag == 1) {  // negative/NaN entries have no meaningful bit order: empty set
-            if (threadIdx.x == 0) p.cnt[dir][g] = 0;
-            return;
-        }
+    const int slice = (n + kCluster - 1) / kCluster;
+    const int lo = min(n, rank * slice), hi = min(n, lo + slice);
+    if (threadIdx.x < kCluster) {
+        sh.rank_above[threadIdx.x] = 0;
+        sh.rank_eq[threadIdx.x] = 0;
     }
+    __syncthreads();
+    int parity = 0;
 
-    // ---- 1. mass radix-select
+    // ---- 1. mass radix-select; pass 0 also validates (sparsity.hpp:60-61)
     const double thr = tau - 1e-12;
-    const unsigned long long thr_fx =
-        thr <= 0.0 ? 0ull : static_cast<unsigned long long>(thr * kFixScale);
+    const unsigned long long thr_fx = thr <= 0.0 ? 0ull : static_cast<unsigned long long>(thr * kFixScale);
     uint32_t prefix = 0, cnt_above = 0;
-    unsigned long long mass_above = 0;
+    unsigned long long mass_above = 0, total_fx = 0;
     bool never = false;
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
-        histogram(sh, x, n, prefix, shift, true);
+        cluster_histogram(sh, cluster, x, lo, hi, prefix, shift, true, pass == 0, parity);
+        parity ^= 1;
+        if (pass == 0) {
+            if (threadIdx.x < 32) {
+                unsigned long long t = 0;
+                for (int b = threadIdx.x; b < 256; b += 32) t += sh.tm[b];
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (threadIdx.x == 0) sh.red[0] = t;
+            }
+            __syncthreads();
+            total_fx = sh.red[0];
+            const double total = static_cast<double>(total_fx) / kFixScale;
+            const int st = sh.bad ? 1 : ((sh.big || fabs(total - 1.0) > 1e-6) ? 2 : 0);
+            if (rank == 0 && threadIdx.x == 0 && p.status) p.status[dir * p.hkv + g] = st;
+            // Invalid scores are reported through `status` (the C ABI raises the reference's
+            // error under VSP_VALIDATE); negative/NaN entries have no bit order: empty set.
+            if (st == 1) {
+                if (rank == 0 && threadIdx.x == 0) p.cnt[dir][g] = 0;
+                cluster.sync();  // no CTA leaves while others may still read its histograms
+                return;
+            }
+        }
         int bucket;
-        unsigned long long ak, am;
+        unsigned long long am;
         uint32_t ac;
-        scan_top(sh, mass_above, thr_fx, true, bucket, ak, ac, am);
+        scan_top(sh, mass_above, thr_fx, true, bucket, ac, am);
         if (bucket < 0) {
             never = true;
             break;
@@ -266,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
         cnt_above += ac;
         mass_above += am;
     }
-    long long k;
+    long long k, need_eq = 0;
     bool ambiguous = false;
     // worst-case |reference sequential f64 sum - our exact fixed-point sum|, doubled
     const double k_err = 2.0 * static_cast<double>(n) * (1.1102230246251565e-16 + 2.168404344971009e-19);
@@ -274,16 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
         // the whole vector's mass stays below the threshold: k = n unless that is within
         // rounding of the reference's sequential sum (then the exact fallback decides)
         k = n;
-        unsigned long long t = 0;
-        for (int i = threadIdx.x; i < n; i += kThreads) t += to_fix(__ldg(x + i));
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = t;
-        __syncthreads();
-        unsigned long long tt = 0;
-        for (int w = 0; w < kWarps; ++w) tt += sh.red[w];
-        __syncthreads();
-        const double total = static_cast<double>(tt) / kFixScale;
-        ambiguous = !(thr - total > k_err);
+        ambiguous = !(thr - static_cast<double>(total_fx) / kFixScale > k_err);
     } else {
         const float vstar = __uint_as_float(prefix);
         const unsigned long long fv = to_fix(vstar);
@@ -293,106 +365,126 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
         if (m < 1) m = 1;
         if (m > c_eq) m = c_eq;
         k = static_cast<long long>(cnt_above) + static_cast<long long>(m);
+        need_eq = static_cast<long long>(m);
         const double pk = (static_cast<double>(mass_above) + static_cast<double>(m) * static_cast<double>(fv)) / kFixScale;
         const double pk1 = (static_cast<double>(mass_above) + static_cast<double>(m - 1) * static_cast<double>(fv)) / kFixScale;
         ambiguous = !(pk - thr > k_err) || !(k == 1 || thr - pk1 > k_err);
     }
 
-    // ---- 2. exact fallback: the reference algorithm verbatim (sort desc, sequential f64 sum)
+    // ---- 2. exact fallback: the reference algorithm verbatim (sort desc, sequential f64
+    // sum), run by rank 0 and broadcast over DSMEM
     if (ambiguous) {
-        uint32_t* s = p.scratch + static_cast<size_t>(dir * p.hkv + g) * 2 * p.npow2;
-        const int np2 = p.npow2;
-        for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? __float_as_uint(__ldg(x + i)) : 0u;
-        __syncthreads();
-        // bitonic sort, descending (non-negative float bits order like values)
-        for (int size = 2; size <= np2; size <<= 1) {
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int t = threadIdx.x; t < np2 / 2; t += kThreads) {
-                    const int lo = 2 * t - (t & (stride - 1));
-                    const int hi = lo + stride;
-                    const bool desc = ((lo & size) == 0);
-                    const uint32_t a = s[lo], b = s[hi];
-                    if (desc ? (a < b) : (a > b)) {
-                        s[lo] = b;
-                        s[hi] = a;
+        if (rank == 0) {
+            uint32_t* s = p.scratch + static_cast<size_t>(dir * p.hkv + g) * 2 * p.npow2;
+            const int np2 = p.npow2;
+            for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? __float_as_uint(__ldg(x + i)) : 0u;
+            __syncthreads();
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int t = threadIdx.x; t < np2 / 2; t += kThreads) {
+                        const int a_i = 2 * t - (t & (stride - 1));
+                        const int b_i = a_i + stride;
+                        const bool desc = ((a_i & size) == 0);
+                        const uint32_t a = s[a_i], b = s[b_i];
+                        if (desc ? (a < b) : (a > b)) {
+                            s[a_i] = b;
+                            s[b_i] = a;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            if (threadIdx.x == 0) {
+                long long kk = n;
+                double cum = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    cum += static_cast<double>(__uint_as_float(s[i]));
+                    if (cum >= thr) {
+                        kk = i + 1;
+                        break;
                     }
                 }
-                __syncthreads();
+                sh.ex[0].k = kk;
             }
         }
-        if (threadIdx.x == 0) {
-            long long kk = n;
-            double cum = 0.0;
-            for (int i = 0; i < n; ++i) {
-                cum += static_cast<double>(__uint_as_float(s[i]));
-                if (cum >= thr) {
-                    kk = i + 1;
-                    break;
-                }
-            }
-            sh.k = kk;
-        }
-        __syncthreads();
-        k = sh.k;
+        cluster.sync();
+        k = cluster.map_shared_rank(&sh.ex[0], 0)->k;
+        cluster.sync();
     }
 
     // clamp (sparsity.hpp:75-78)
+    const long long k_mass = k;
     const long long mn = p.min_b[g] < n ? p.min_b[g] : n;
     if (k < mn) k = mn;
     long long upper = n;
     if (p.max_b[g] >= 0 && p.max_b[g] < upper) upper = p.max_b[g];
     if (k > upper) k = upper;
 
-    // ---- 3. count radix-select for the k-th largest value
-    prefix = 0;
-    uint32_t gt = 0;  // count strictly greater than the current prefix range
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        histogram(sh, x, n, prefix, shift, false);
-        int bucket;
-        unsigned long long ak, am;
-        uint32_t ac;
-        scan_top(sh, gt, static_cast<unsigned long long>(k), false, bucket, ak, ac, am);
-        prefix |= static_cast<uint32_t>(bucket) << shift;
-        gt += ac;
+    // ---- 3. count radix-select for the k-th largest value (only if pass 1 does not give it)
+    if (never || ambiguous || k != k_mass) {
+        if (threadIdx.x < kCluster) sh.rank_above[threadIdx.x] = 0;
+        __syncthreads();
+        prefix = 0;
+        uint32_t gt = 0;
+        for (int pass = 0; pass < 4; ++pass) {
+            const int shift = 24 - 8 * pass;
+            cluster_histogram(sh, cluster, x, lo, hi, prefix, shift, false, false, parity);
+            parity ^= 1;
+            int bucket;
+            unsigned long long am;
+            uint32_t ac;
+            scan_top(sh, gt, static_cast<unsigned long long>(k), false, bucket, ac, am);
+            prefix |= static_cast<uint32_t>(bucket) << shift;
+            gt += ac;
+        }
+        need_eq = k - gt;
     }
     const uint32_t tbits = prefix;
-    const long long need_eq = k - gt;
 
-    // ---- 4. ordered compaction
+    // ---- 4. ordered compaction: this CTA's offset from the per-rank counts
+    if (threadIdx.x == 0) {
+        long long pos = 0, eqb = 0;
+        for (int r = 0; r < rank; ++r) {
+            const long long take = min(static_cast<long long>(sh.rank_eq[r]), max(0ll, need_eq - eqb));
+            pos += sh.rank_above[r] + take;
+            eqb += sh.rank_eq[r];
+        }
+        sh.base_pos = pos;
+        sh.eq_base = eqb;
+    }
+    __syncthreads();
     int* out = p.idx[dir] + static_cast<size_t>(g) * p.cap;
     const bool inject = (dir == 1);
-    // is index 0 selected? (needed up front to shift the slash list by one)
     int zero_sel;
     {
         const uint32_t b0 = __float_as_uint(__ldg(x));
         zero_sel = (b0 > tbits) || (b0 == tbits && need_eq > 0);
     }
     const int shift_out = (inject && !zero_sel) ? 1 : 0;
-    uint32_t sel_base = 0, eq_base = 0;
+    long long sel_base = sh.base_pos + shift_out;
+    long long eq_base = sh.eq_base;
     const int chunk = kThreads * kItems;
-    for (int c0 = 0; c0 < n; c0 += chunk) {
+    for (int c0 = lo; c0 < hi; c0 += chunk) {
         const int i0 = c0 + threadIdx.x * kItems;
         uint32_t bits[kItems];
         uint32_t n_eq = 0;
 #pragma unroll
         for (int t = 0; t < kItems; ++t) {
             const int i = i0 + t;
-            bits[t] = i < n ? __float_as_uint(__ldg(x + i)) : 0u;
-            n_eq += (i < n && bits[t] == tbits) ? 1u : 0u;
+            bits[t] = i < hi ? __float_as_uint(__ldg(x + i)) : 0u;
+            n_eq += (i < hi && bits[t] == tbits) ? 1u : 0u;
         }
         uint32_t eq_tot;
-        uint32_t eq_pre = block_scan(n_eq, scanbuf, eq_tot) + eq_base;
-        uint32_t n_sel = 0;
-        uint32_t flags = 0;
+        long long eq_pre = block_scan(n_eq, sh.scan, eq_tot) + eq_base;
+        uint32_t n_sel = 0, flags = 0;
 #pragma unroll
         for (int t = 0; t < kItems; ++t) {
             const int i = i0 + t;
             bool s = false;
-            if (i < n) {
+            if (i < hi) {
                 if (bits[t] > tbits) s = true;
                 else if (bits[t] == tbits) {
-                    s = static_cast<long long>(eq_pre) < need_eq;
+                    s = eq_pre < need_eq;
                     ++eq_pre;
                 }
             }
@@ -400,17 +492,18 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
             n_sel += s ? 1u : 0u;
         }
         uint32_t sel_tot;
-        uint32_t pos = block_scan(n_sel, scanbuf, sel_tot) + sel_base + shift_out;
+        long long pos = block_scan(n_sel, sh.scan, sel_tot) + sel_base;
 #pragma unroll
         for (int t = 0; t < kItems; ++t)
             if ((flags >> t) & 1u) out[pos++] = i0 + t;
         sel_base += sel_tot;
         eq_base += eq_tot;
     }
-    if (threadIdx.x == 0) {
+    if (rank == 0 && threadIdx.x == 0) {
         if (shift_out) out[0] = 0;
         p.cnt[dir][g] = static_cast<int>(k) + shift_out;
     }
+    cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
 
 static int next_pow2(int n) {
@@ -447,14 +540,14 @@ cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp
         p.min_b[g] = budgets[g].min_budget;
         p.max_b[g] = budgets[g].max_budget;
     }
-    const int smem = static_cast<int>(sizeof(Shared)) + 64 * sizeof(uint32_t);
+    const int smem = static_cast<int>(sizeof(Shared));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     p.g0 = g0;
-    select_kernel<<<dim3(count, 2), kThreads, smem, stream>>>(p);
+    select_kernel<<<dim3(count * kCluster, 2), kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

@@ -174,7 +174,7 @@ def test_select_matches_oracle_random(vsp, n):
 
 def test_select_quantized_ties_vs_oracle(vsp):
     rng = np.random.default_rng(5)
-    for n in (50, 3000):
+    for n in (50, 3000, 131072):
         c = rng.integers(0, 8, size=(2, n)).astype(np.float64)
         c[:, 0] += 1
         a = (c / c.sum(axis=1, keepdims=True)).astype(np.float32)
@@ -182,6 +182,9 @@ def test_select_quantized_ties_vs_oracle(vsp):
         a_s = torch.tensor(a[1:]).cuda()
         for tau in (0.1, 0.5, 0.93):
             _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(tau, tau, 1, None)])
+        # clamped budgets take the count radix-select path; ties straddle the cluster's slices
+        _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(0.1, 0.93, n // 3 + 1, None)])
+        _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(0.93, 0.5, 1, n // 5 + 2)])
 
 
 def test_select_uniform_zero_heads(vsp):
