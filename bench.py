@@ -443,7 +443,7 @@ def main():
                    "sample": f"failed: {ex}"}
 
     # per KV-head chunk: indexer gemm + softmax, select, bitmaps + gather + plan, attention
-    launches_per_step = 7 * (((hkv_r + hpc - 1) // hpc) if hpc > 0 else min(2, hkv_r))
+    launches_per_step = 7 * (((hkv_r + hpc - 1) // hpc) if hpc > 0 else (2 if hkv_r > 1 else 1))
     if rank == 0:
         line = {
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,

@@ -117,8 +117,7 @@ VSP_API int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const 
 
 /* ---- the whole VS-prefill layer: K1 -> K2 -> K3 in one call ------------------------
  * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads, but
- * pipelined over KV-head chunks of `heads_per_chunk` heads (0 = automatic: the first
- * KV head alone, then the rest in one chunk): the scoring, selection and
+ * pipelined over KV-head chunks of `heads_per_chunk` heads (0 = automatic: two halves): the scoring, selection and
  * tile planning of chunk c+1 run on a high-priority side stream while chunk c's attention
  * runs on `stream`. a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
  * individual calls). Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp

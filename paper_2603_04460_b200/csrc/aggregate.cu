@@ -70,7 +70,9 @@ VSP_DEVICE uint32_t sw128_off(int r, int c) {
 
 __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // offset from smem_raw (not a cast through an integer) so the compiler keeps the
+    // shared state space and emits LDS/STS rather than generic LD/ST
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ Smem sm;
     const int grp = p.hq / p.hkv;
 

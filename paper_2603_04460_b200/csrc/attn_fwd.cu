@@ -74,7 +74,9 @@ VSP_DEVICE void window128(const uint32_t* __restrict__ bm, int start, int nwords
 template <bool kSparse>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // offset from smem_raw (not a cast through an integer) so the compiler keeps the
+    // shared state space and emits LDS/STS rather than generic LD/ST
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sQ = base;                                  // 2 tiles
     uint8_t* sK = base + 2 * kTileBytes;                 // kNumK tiles
     uint8_t* sV = sK + kNumK * kTileBytes;               // kNumV tiles

@@ -318,17 +318,18 @@ namespace {
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // KV-head chunk schedule of the pipelined layer: hpc > 0 gives uniform chunks of hpc heads;
-// hpc == 0 (automatic) runs the first KV head alone, so attention starts after scoring and
-// selecting one head, and the remaining heads as one chunk whose preparation overlaps it.
-int num_chunks(int hkv, int hpc) { return hpc > 0 ? (hkv + hpc - 1) / hpc : (hkv > 1 ? 2 : 1); }
+// hpc == 0 (automatic) uses two halves: the second half's scoring and selection overlap
+// the first half's attention, and each attention launch still spans enough heads to
+// balance its long and short CTAs (tools/sched_sweep.py: profiles/r01_schedule_sweep.json).
+int auto_hpc(int hkv) { return (hkv + 1) / 2; }
+int num_chunks(int hkv, int hpc) {
+    if (hpc <= 0) hpc = auto_hpc(hkv);
+    return (hkv + hpc - 1) / hpc;
+}
 void chunk_range(int c, int hkv, int hpc, int& g0, int& cnt) {
-    if (hpc > 0) {
-        g0 = c * hpc;
-        cnt = std::min(hpc, hkv - g0);
-    } else {
-        g0 = c == 0 ? 0 : 1;
-        cnt = c == 0 ? 1 : hkv - 1;
-    }
+    if (hpc <= 0) hpc = auto_hpc(hkv);
+    g0 = c * hpc;
+    cnt = std::min(hpc, hkv - g0);
 }
 
 struct PrefillDev {

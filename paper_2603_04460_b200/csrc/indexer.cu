@@ -7,13 +7,15 @@
 //   logit_s[o] = raw_s[n-1-o] (Reverse) | raw_s[o] (Identity)   (:106-109, :26-28)
 //   A_v = softmax(logit_v), A_s = softmax(logit_s) over all n   (:110-111)
 //
-// GEMM kernel: CTA = 128 tokens x one KV head. A = X tile (K-major, 4 x [128 x 64] SW128
-// boxes straight from the K and V tensors: the concatenation is free). B = W_U streamed in
-// [64 K-rows x 256 N] MN-major stages (the reference's [2d, d_h] row-major layout, no
-// transpose). tcgen05.mma M=128 N=256 into two TMEM accumulators (double-buffered over
-// 256-wide hidden chunks) so the SiLU / two-head epilogue of chunk c overlaps the MMA of
-// chunk c+1. The [n, d_h] activation never leaves the SM: only two fp32 logits per token
-// are written. The softmax over n is a second, tiny kernel (fp64 normaliser).
+// GEMM kernel (persistent, one CTA per SM): work item = 128 tokens x one KV head, walked
+// head-major so concurrent CTAs share W_U in L2. A = X tile (K-major, 4 x [128 x 64] SW128
+// boxes straight from the K and V tensors: the concatenation is free), double-buffered
+// across work items. B = W_U streamed in [32 K-rows x 256 N] MN-major stages (the
+// reference's [2d, d_h] row-major layout, no transpose). tcgen05.mma M=128 N=256 into two
+// TMEM accumulators (double-buffered over 256-wide hidden chunks, continuing across work
+// items) so the SiLU / two-head epilogue of chunk c overlaps the MMA of chunk c+1. The
+// [n, d_h] activation never leaves the SM: only two fp32 logits per token are written.
+// The softmax over n is a second, tiny kernel (fp64 normaliser).
 #include <cuda_bf16.h>
 
 #include "indexer.h"
@@ -26,10 +28,10 @@ namespace vsp_indexer {
 
 constexpr int kTok = 128;
 constexpr int kChunkN = 256;
-constexpr int kStageK = 64;
+constexpr int kStageK = 32;
 constexpr int kStages = 4;
-constexpr int kABytes = kTok * 256 * 2;             // 64 KB
-constexpr int kStageBytes = kStageK * kChunkN * 2;  // 32 KB
+constexpr int kABytes = kTok * 256 * 2;             // 64 KB per token tile
+constexpr int kStageBytes = kStageK * kChunkN * 2;  // 16 KB
 constexpr int kMaxDh = 2048;
 constexpr int kThreads = 320;                       // warp0 TMA, warp1 MMA, warps 2-9 epilogue
 
@@ -43,55 +45,58 @@ struct __align__(64) Params {
     float* logit_v;  // [hkv, n]
     float* logit_s;  // [hkv, n] (mapping applied)
     int n, hkv, d_h;
-    int g0;
+    int g0, count;   // KV heads [g0, g0 + count)
+    int tiles;       // token tiles per head
     int reverse;
 };
 
 struct Smem {
-    uint64_t bar_a;
+    uint64_t a_full[2], a_empty[2];
     uint64_t full[kStages], empty[kStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
 };
 
 // SiLU via one MUFU op: y * sigmoid(y) = h + h * tanh(h), h = y / 2 (overflow-free for any y)
-VSP_DEVICE float silu_f(float y) {
-    const float h = 0.5f * y;
+VSP_DEVICE float tanh_f(float h) {
     float t;
     asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
-    return fmaf(h, t, h);
+    return t;
 }
 
+// Persistent: one CTA per SM walks work items w = blockIdx.x + i * gridDim.x, head-major
+// (w / tiles = head, w % tiles = 128-token tile), so the CTAs of one wave stream the same
+// W_U from L2. The X tile is double-buffered across work items and the W_U stream and the
+// TMEM accumulators run continuously across them, so loads, MMAs and the epilogue of
+// consecutive tiles overlap.
 __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = base;
-    uint8_t* sB = base + kABytes;
-    float* s_bu = reinterpret_cast<float*>(sB + kStages * kStageBytes);
-    float* s_wv = s_bu + kMaxDh;
+    // offset from smem_raw (not a cast through an integer) so the compiler keeps the
+    // shared state space and emits LDS/STS rather than generic LD/ST
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = base;                        // 2 x 64 KB
+    uint8_t* sB = base + 2 * kABytes;          // kStages x 16 KB
+    float* s_bh = reinterpret_cast<float*>(sB + kStages * kStageBytes);  // b_U / 2
+    float* s_wv = s_bh + kMaxDh;
     float* s_ws = s_wv + kMaxDh;
+    float* s_xch = s_ws + kMaxDh;              // 2 x 256 floats (tile parity)
     __shared__ Smem sm;
 
-    const int g = p.g0 + static_cast<int>(blockIdx.y);
-    const int t0 = blockIdx.x * kTok;
     const int num_chunks = p.d_h / kChunkN;
+    const int total = p.tiles * p.count;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
-    for (int i = threadIdx.x; i < p.d_h; i += blockDim.x) {
-        s_bu[i] = p.b_u[static_cast<size_t>(g) * p.d_h + i];
-        s_wv[i] = p.w_v[static_cast<size_t>(g) * p.d_h + i];
-        s_ws[i] = p.w_s[static_cast<size_t>(g) * p.d_h + i];
-    }
     if (warp == 0 && lane == 0) {
-        mbar_init(&sm.bar_a, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sm.a_full[b], 1);
+            mbar_init(&sm.a_empty[b], 1);
+            mbar_init(&sm.acc_full[b], 1);
+            mbar_init(&sm.acc_empty[b], 8);
+        }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&sm.acc_full[a], 1);
-            mbar_init(&sm.acc_empty[a], 8);
         }
         fence_barrier_init();
     }
@@ -107,54 +112,71 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             tma_prefetch_desc(&p.map_k);
             tma_prefetch_desc(&p.map_v);
             tma_prefetch_desc(&p.map_w);
-            mbar_arrive_expect_tx(&sm.bar_a, kABytes);
-            for (int hf = 0; hf < 2; ++hf) {
-                tma_load_3d(sA + hf * 16384, &p.map_k, &sm.bar_a, hf * 64, g, t0);
-                tma_load_3d(sA + (2 + hf) * 16384, &p.map_v, &sm.bar_a, hf * 64, g, t0);
-            }
         }
         __syncwarp();
-        int it = 0;
-        for (int c = 0; c < num_chunks; ++c) {
-            for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                const int s = it % kStages;
-                if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
-                    for (int nb = 0; nb < kChunkN / 64; ++nb)
-                        tma_load_3d(sB + s * kStageBytes + nb * 8192, &p.map_w, &sm.full[s], c * kChunkN + nb * 64,
-                                    ks * kStageK, g);
+        int it = 0, j = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
+            const int g = p.g0 + w / p.tiles;
+            const int t0 = (w % p.tiles) * kTok;
+            const int buf = j & 1;
+            if (j >= 2) mbar_wait(&sm.a_empty[buf], ((j >> 1) & 1) ^ 1);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&sm.a_full[buf], kABytes);
+                uint8_t* a = sA + buf * kABytes;
+                for (int hf = 0; hf < 2; ++hf) {
+                    tma_load_3d(a + hf * 16384, &p.map_k, &sm.a_full[buf], hf * 64, g, t0);
+                    tma_load_3d(a + (2 + hf) * 16384, &p.map_v, &sm.a_full[buf], hf * 64, g, t0);
                 }
-                __syncwarp();
+            }
+            __syncwarp();
+            for (int c = 0; c < num_chunks; ++c) {
+                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                    const int s = it % kStages;
+                    if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
+                        for (int nb = 0; nb < kChunkN / 64; ++nb)
+                            tma_load_3d(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
+                                        c * kChunkN + nb * 64, ks * kStageK, g);
+                    }
+                    __syncwarp();
+                }
             }
         }
     } else if (warp == 1) {
         // MMA issuer: warp-uniform loop, one elected lane issues each batch
         const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
-        const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
-        const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), 8192, 1024);
-        mbar_wait(&sm.bar_a, 0);
-        int it = 0;
-        for (int c = 0; c < num_chunks; ++c) {
-            const int acc = c & 1;
-            if (c >= 2) mbar_wait(&sm.acc_empty[acc], ((c >> 1) & 1) ^ 1);
-            tc_fence_after();
-            for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                const int s = it % kStages;
-                mbar_wait(&sm.full[s], (it / kStages) & 1);
+        const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), kStageK * 128, 1024);
+        int it = 0, cc = 0, j = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
+            const int buf = j & 1;
+            const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + buf * kABytes), 16, 1024);
+            mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
+            for (int c = 0; c < num_chunks; ++c, ++cc) {
+                const int acc = cc & 1;
+                if (cc >= 2) mbar_wait(&sm.acc_empty[acc], ((cc >> 1) & 1) ^ 1);
                 tc_fence_after();
-                if (elect_one()) {
+                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                    const int s = it % kStages;
+                    mbar_wait(&sm.full[s], (it / kStages) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < kStageK / 16; ++kk) {
-                        const int kg = ks * kStageK + kk * 16;  // global K index (feature)
-                        const uint64_t adesc = a_desc0 + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4);
-                        const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kStageBytes + kk * 2048) >> 4);
-                        umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kStageK / 16; ++kk) {
+                            const int kg = ks * kStageK + kk * 16;  // global K index (feature)
+                            const uint64_t adesc =
+                                a_desc0 + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4);
+                            const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kStageBytes + kk * 2048) >> 4);
+                            umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        umma_commit(&sm.empty[s]);
+                        if (ks == 256 / kStageK - 1) {
+                            umma_commit(&sm.acc_full[acc]);
+                            if (c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
+                        }
                     }
-                    umma_commit(&sm.empty[s]);
-                    if (ks == 256 / kStageK - 1) umma_commit(&sm.acc_full[acc]);
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
     } else {
@@ -163,56 +185,73 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         const int quarter = warp & 3;
         const int part = (warp - 2) >> 2;
         const int r = quarter * 32 + lane;
-        const int t = t0 + r;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        float lv[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};  // independent chains
-        for (int c = 0; c < num_chunks; ++c) {
-            const int acc = c & 1;
-            mbar_wait(&sm.acc_full[acc], (c >> 1) & 1);
-            tc_fence_after();
-            uint32_t ub[2][32];  // ping-pong: the next 32 columns load while these compute
-            tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / 2), ub[0]);
-            tmem_wait_ld();
-#pragma unroll
-            for (int q = 0; q < kChunkN / 64; ++q) {
-                uint32_t* u = ub[q & 1];
-                const int cc = part * (kChunkN / 2) + q * 32;
-                if (q + 1 < kChunkN / 64) tmem_ld32(lane_base + acc * kChunkN + cc + 32, ub[(q + 1) & 1]);
-                const int col0 = c * kChunkN + cc;
-                const float4* bu4 = reinterpret_cast<const float4*>(s_bu + col0);
-                const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
-                const float4* ws4 = reinterpret_cast<const float4*>(s_ws + col0);
-#pragma unroll
-                for (int x4 = 0; x4 < 8; ++x4) {
-                    const float4 b = bu4[x4], wv = wv4[x4], ws = ws4[x4];
-                    const float bb[4] = {b.x, b.y, b.z, b.w};
-                    const float vv[4] = {wv.x, wv.y, wv.z, wv.w};
-                    const float sv[4] = {ws.x, ws.y, ws.z, ws.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float z = silu_f(__uint_as_float(u[4 * x4 + e]) + bb[e]);
-                        lv[e] = fmaf(z, vv[e], lv[e]);
-                        ls[e] = fmaf(z, sv[e], ls[e]);
-                    }
+        const int et = threadIdx.x - 64;  // 0..255
+        int cc = 0, j = 0, cur_g = -1;
+        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
+            const int g = p.g0 + w / p.tiles;
+            const int t = (w % p.tiles) * kTok + r;
+            if (g != cur_g) {  // head change: everyone is past the previous tile's exchange
+                for (int i = et; i < p.d_h; i += 256) {
+                    s_bh[i] = 0.5f * p.b_u[static_cast<size_t>(g) * p.d_h + i];
+                    s_wv[i] = p.w_v[static_cast<size_t>(g) * p.d_h + i];
+                    s_ws[i] = p.w_s[static_cast<size_t>(g) * p.d_h + i];
                 }
-                if (q + 1 < kChunkN / 64) tmem_wait_ld();
+                named_bar_sync(1, 256);
+                cur_g = g;
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
-        }
-        float sv_ = (lv[0] + lv[1]) + (lv[2] + lv[3]);
-        float ss_ = (ls[0] + ls[1]) + (ls[2] + ls[3]);
-        float* xch = s_ws + kMaxDh;  // 2 x 128 floats past the parameters
-        if (part == 1) {
-            xch[r] = sv_;
-            xch[128 + r] = ss_;
-        }
-        named_bar_sync(1, 256);
-        if (part == 0 && t < p.n) {
-            p.logit_v[static_cast<size_t>(g) * p.n + t] = sv_ + xch[r] + p.b_v[g];
-            const int o = p.reverse ? p.n - 1 - t : t;
-            p.logit_s[static_cast<size_t>(g) * p.n + o] = ss_ + xch[128 + r] + p.b_s[g];
+            float2 lv = make_float2(0.f, 0.f), ls = make_float2(0.f, 0.f);
+            float2 lv1 = lv, ls1 = ls;  // two independent chains per dot
+            for (int c = 0; c < num_chunks; ++c, ++cc) {
+                const int acc = cc & 1;
+                mbar_wait(&sm.acc_full[acc], (cc >> 1) & 1);
+                tc_fence_after();
+                uint32_t ub[2][32];  // ping-pong: the next 32 columns load while these compute
+                tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / 2), ub[0]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < kChunkN / 64; ++q) {
+                    uint32_t* u = ub[q & 1];
+                    const int col = part * (kChunkN / 2) + q * 32;
+                    if (q + 1 < kChunkN / 64) tmem_ld32(lane_base + acc * kChunkN + col + 32, ub[(q + 1) & 1]);
+                    const int col0 = c * kChunkN + col;
+                    const float4* bh4 = reinterpret_cast<const float4*>(s_bh + col0);
+                    const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
+                    const float4* ws4 = reinterpret_cast<const float4*>(s_ws + col0);
+#pragma unroll
+                    for (int x4 = 0; x4 < 8; ++x4) {
+                        const float4 b = bh4[x4], wv = wv4[x4], ws = ws4[x4];
+                        // h = y/2 + b/2 ; z = h + h tanh(h) ; packed f32x2 for everything but MUFU
+                        const float2 h0 = ffma2(make_float2(__uint_as_float(u[4 * x4]), __uint_as_float(u[4 * x4 + 1])),
+                                                make_float2(0.5f, 0.5f), make_float2(b.x, b.y));
+                        const float2 h1 = ffma2(make_float2(__uint_as_float(u[4 * x4 + 2]), __uint_as_float(u[4 * x4 + 3])),
+                                                make_float2(0.5f, 0.5f), make_float2(b.z, b.w));
+                        const float2 z0 = ffma2(h0, make_float2(tanh_f(h0.x), tanh_f(h0.y)), h0);
+                        const float2 z1 = ffma2(h1, make_float2(tanh_f(h1.x), tanh_f(h1.y)), h1);
+                        lv = ffma2(z0, make_float2(wv.x, wv.y), lv);
+                        ls = ffma2(z0, make_float2(ws.x, ws.y), ls);
+                        lv1 = ffma2(z1, make_float2(wv.z, wv.w), lv1);
+                        ls1 = ffma2(z1, make_float2(ws.z, ws.w), ls1);
+                    }
+                    if (q + 1 < kChunkN / 64) tmem_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
+            }
+            const float sv = (lv.x + lv.y) + (lv1.x + lv1.y);
+            const float ss = (ls.x + ls.y) + (ls1.x + ls1.y);
+            float* xch = s_xch + (j & 1) * 256;
+            if (part == 1) {
+                xch[r] = sv;
+                xch[128 + r] = ss;
+            }
+            named_bar_sync(1, 256);
+            if (part == 0 && t < p.n) {
+                p.logit_v[static_cast<size_t>(g) * p.n + t] = sv + xch[r] + p.b_v[g];
+                const int o = p.reverse ? p.n - 1 - t : t;
+                p.logit_s[static_cast<size_t>(g) * p.n + o] = ss + xch[128 + r] + p.b_s[g];
+            }
         }
     }
     tc_fence_before();
@@ -258,7 +297,7 @@ __global__ void __launch_bounds__(1024) softmax_rows_kernel(const float* __restr
         y[i] = static_cast<float>(static_cast<double>(expf(x[i] - m)) * inv);
 }
 
-constexpr int kSmemBytes = kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 256 * 4 + 1024;
+constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 512 * 4 + 1024;
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
     return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;
@@ -268,6 +307,7 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     if (a.d_h > kMaxDh || a.d_h % kChunkN != 0) return cudaErrorInvalidValue;
     Params p{};
     const uint32_t box[3] = {64, 1, kTok};
+    static_assert(kSmemBytes <= 227 * 1024, "indexer smem");
     const uint64_t dk[3] = {128, (uint64_t)a.hkv, (uint64_t)a.n};
     const uint64_t sk[2] = {128 * 2, (uint64_t)a.hkv * 128 * 2};
     const uint32_t wbox[3] = {64, kStageK, 1};
@@ -297,8 +337,16 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     }
     const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
     p.g0 = a.g0;
-    dim3 grid((a.n + kTok - 1) / kTok, count);
-    indexer_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    p.count = count;
+    p.tiles = (a.n + kTok - 1) / kTok;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int work = p.tiles * count;
+    indexer_gemm_kernel<<<work < sms ? work : sms, kThreads, kSmemBytes, stream>>>(p);
     softmax_rows_kernel<<<dim3(count, 2), 1024, 0, stream>>>(lv, ls, a.a_v, a.a_s, a.n, a.g0);
     return cudaGetLastError();
 }
