@@ -381,6 +381,8 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
     void* ws_sel = ws;
     ws += align256(vsp_select_k::workspace_bytes(n, hkv));
     void* ws_attn = ws;
+    float* lv = static_cast<float*>(ws_ix);  // logits [hkv, n] x 2 in the indexer workspace
+    float* ls = lv + static_cast<size_t>(hkv) * n;
     cudaStream_t side = ctx->side;
     cudaError_t e = cudaEventRecord(ctx->ev_start, main);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
@@ -390,12 +392,13 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         int g0, cnt;
         chunk_range(c, hkv, hpc, g0, cnt);
         if (kv_ready) e = cudaStreamWaitEvent(side, kv_ready[c], 0);
+        // logits only (a_v null); the selection clusters softmax them and write A_v / A_s
         vsp_indexer::Args ia{p.k, p.v, n, hkv, d_h, p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s,
-                             slash_mapping == VSP_SLASH_REVERSE, p.a_v, p.a_s, nullptr, nullptr, g0, cnt};
+                             slash_mapping == VSP_SLASH_REVERSE, nullptr, nullptr, lv, ls, g0, cnt};
         if (e == cudaSuccess) e = vsp_indexer::launch(ia, ws_ix, side);
         if (e == cudaSuccess)
-            e = vsp_select_k::launch(p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s, cap, ws_sel, side,
-                                     g0, cnt);
+            e = vsp_select_k::launch_from_logits(lv, ls, p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s,
+                                                 cap, ws_sel, side, g0, cnt);
         if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, side, g0, cnt, 1);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[c], side);
     }

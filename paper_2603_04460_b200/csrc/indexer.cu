@@ -15,10 +15,11 @@
 // TMEM accumulators (double-buffered over 256-wide hidden chunks, continuing across work
 // items) so the SiLU / two-head epilogue of chunk c overlaps the MMA of chunk c+1. The
 // [n, d_h] activation never leaves the SM: only two fp32 logits per token are written.
-// The softmax over n is a second, tiny kernel (fp64 normaliser).
+// The softmax over n runs in the selection clusters (select.cu, fp64 normaliser).
 #include <cuda_bf16.h>
 
 #include "indexer.h"
+#include "select.h"
 #include "sm100.cuh"
 #include "tma_host.h"
 
@@ -259,44 +260,6 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     if (warp == 1) tmem_free<512>(tmem);
 }
 
-// Softmax over n per (head, direction), fp32 exp with an fp64 normaliser so that the
-// scores sum to 1 within fp32 rounding (select's |sum - 1| <= 1e-6 check, sparsity.hpp:61).
-// grid (hkv, 2), 1024 threads.
-__global__ void __launch_bounds__(1024) softmax_rows_kernel(const float* __restrict__ lv, const float* __restrict__ ls,
-                                                           float* __restrict__ av, float* __restrict__ as, int n, int g0) {
-    const int g = g0 + static_cast<int>(blockIdx.x);
-    const float* x = (blockIdx.y == 0 ? lv : ls) + static_cast<size_t>(g) * n;
-    float* y = (blockIdx.y == 0 ? av : as) + static_cast<size_t>(g) * n;
-    __shared__ float red_f[32];
-    __shared__ double red_d[32];
-    float m = -INFINITY;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, x[i]);
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float v = threadIdx.x < (blockDim.x >> 5) ? red_f[threadIdx.x] : -INFINITY;
-        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (threadIdx.x == 0) red_f[0] = v;
-    }
-    __syncthreads();
-    m = red_f[0];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s += static_cast<double>(expf(x[i] - m));
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double v = threadIdx.x < (blockDim.x >> 5) ? red_d[threadIdx.x] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) red_d[0] = v;
-    }
-    __syncthreads();
-    const double inv = 1.0 / red_d[0];
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-        y[i] = static_cast<float>(static_cast<double>(expf(x[i] - m)) * inv);
-}
-
 constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 512 * 4 + 1024;
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
@@ -347,8 +310,11 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     }
     const int work = p.tiles * count;
     indexer_gemm_kernel<<<work < sms ? work : sms, kThreads, kSmemBytes, stream>>>(p);
-    softmax_rows_kernel<<<dim3(count, 2), 1024, 0, stream>>>(lv, ls, a.a_v, a.a_s, a.n, a.g0);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    // A_v / A_s: the cluster softmax shared with the selection kernel (a_v null: logits only,
+    // the layer path softmaxes inside selection)
+    if (e == cudaSuccess && a.a_v) e = vsp_select_k::launch_softmax(lv, ls, a.a_v, a.a_s, a.n, a.g0, count, stream);
+    return e;
 }
 
 }  // namespace vsp_indexer

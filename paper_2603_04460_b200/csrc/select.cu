@@ -8,13 +8,18 @@
 //   inject_offset_zero(I_s)               (:99-101)
 //
 // One 8-CTA thread-block cluster per (head, direction); each CTA owns a contiguous 1/8 of
-// the n scores, the CTAs exchange their radix histograms through distributed shared memory
-// and every CTA takes the same decisions. No sort on the fast path:
+// the n scores, keeps it in shared memory for all passes, the CTAs exchange their radix
+// histograms through distributed shared memory and every CTA takes the same decisions.
+// On the layer path the kernel starts from the indexer's logits and performs the softmax
+// itself (cluster-wide max and fp64 normaliser, indexer.hpp:110-111), writing A_v / A_s as
+// it goes; the standalone softmax kernel for vsp_indexer_scores runs the same code, so both
+// paths produce bit-identical scores. No sort on the fast path:
 //   1. mass radix-select: 4 MSB-first passes over the fp32 bit pattern (non-negative floats
 //      order like their bits). Per-warp private histograms of (count, mass) where mass is
 //      u64 fixed point x*2^62 (exact to 2^-62 per element, deterministic integer sums);
-//      lanes of a warp that hit the same bucket are merged first (match.any + redux), so the
-//      concentrated score distributions of real layers do not serialise on one bucket.
+//      the lanes of a warp that share the warp's most common buckets are merged with
+//      full-warp reductions first, so the concentrated score distributions of real layers
+//      do not serialise on one bucket.
 //      The crossing value v*, the count and mass strictly above it give k. The first pass
 //      also performs the reference's score validation.
 //   2. exactness guard: the reference sums the sorted doubles sequentially in f64. If our
@@ -44,15 +49,18 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 8;
 constexpr int kMaxHeads = 128;
+constexpr int kMergeRounds = 2;
 constexpr uint32_t kNoBucket = 256u;
 constexpr double kFixScale = 4611686018427387904.0;  // 2^62
+constexpr int kMaxCachedSlice = 36864;                 // floats of one CTA's slice kept in smem
 
 struct Params {
-    const float* a[2];  // a_v, a_s  [hkv, n]
-    int* idx[2];        // i_v, i_s  [hkv, cap]
-    int* cnt[2];        // k_v, k_s  [hkv]
-    uint32_t* scratch;  // [2*hkv, 2 * npow2]
-    int* status;        // [2*hkv]: 0 ok, 1 negative score, 2 sum != 1
+    const float* a[2];       // a_v, a_s  [hkv, n] (scores; written here when from logits)
+    const float* logits[2];  // null, or logits_v / logits_s [hkv, n] to softmax first
+    int* idx[2];             // i_v, i_s  [hkv, cap]
+    int* cnt[2];             // k_v, k_s  [hkv]
+    uint32_t* scratch;       // [2*hkv, 2 * npow2]
+    int* status;             // [2*hkv]: 0 ok, 1 negative score, 2 sum != 1
     int n, hkv, cap, npow2;
     int g0;  // first KV head of this launch
     double tau[2][kMaxHeads];
@@ -60,10 +68,12 @@ struct Params {
     long long max_b[kMaxHeads];
 };
 
-// What one CTA publishes to its cluster each pass (double-buffered by pass parity).
+// What one CTA publishes to its cluster per exchange step (double-buffered by step parity).
 struct Exchange {
     uint32_t c[256];
     unsigned long long m[256];
+    double sum;
+    float mx;
     int bad, big;
     long long k;  // fallback result (rank 0)
 };
@@ -79,8 +89,11 @@ struct Shared {
     uint32_t rank_eq[kCluster];
     uint32_t scan[64];
     unsigned long long red[kWarps];
+    double red_d[kWarps];
+    float red_f[kWarps];
     int found;
     int bad, big;
+    uint32_t x0;  // bits of score 0 (slash offset 0)
     long long base_pos, eq_base;
 };
 
@@ -89,12 +102,85 @@ __device__ __forceinline__ unsigned long long to_fix(float x) {
     return static_cast<unsigned long long>(__float2ull_rz(fminf(x, 2.0f) * 4611686018427387904.0f));
 }
 
-// Local histogram of digit (bits >> shift) & 255 over this CTA's slice [lo, hi), restricted
+__device__ __forceinline__ int slice_of(int n, int rank, int& lo, int& hi) {
+    const int slice = (n + kCluster - 1) / kCluster;
+    lo = min(n, rank * slice);
+    hi = min(n, lo + slice);
+    return slice;
+}
+
+// Cluster-wide softmax of one logit row (indexer.hpp:110-111): max, fp64 sum of exp, and
+// the normalised fp32 scores, written to `out` (global) and, when cached, to xs (this CTA's
+// slice in shared memory, which also holds the logits on entry). The reduction order is a
+// function of (n, thread and cluster shape) only, so every caller gets identical bits.
+template <bool kCached>
+__device__ void cluster_softmax(Shared& sh, cg::cluster_group& cluster, const float* __restrict__ logits, float* xs,
+                                int lo, int hi, float* __restrict__ out, int& parity) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int len = hi - lo;
+    auto src = [&](int i) { return kCached ? xs[i] : __ldg(logits + lo + i); };
+    float mx = -INFINITY;
+    for (int i = threadIdx.x; i < len; i += kThreads) mx = fmaxf(mx, src(i));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sh.red_f[warp] = mx;
+    __syncthreads();
+    Exchange& e1 = sh.ex[parity];
+    if (threadIdx.x == 0) {
+        float v = -INFINITY;
+        for (int w = 0; w < kWarps; ++w) v = fmaxf(v, sh.red_f[w]);
+        e1.mx = v;
+    }
+    cluster.sync();
+    float m = -INFINITY;
+    for (int r = 0; r < kCluster; ++r) m = fmaxf(m, cluster.map_shared_rank(&e1, r)->mx);
+    parity ^= 1;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < len; i += kThreads) s += static_cast<double>(expf(src(i) - m));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sh.red_d[warp] = s;
+    __syncthreads();
+    Exchange& e2 = sh.ex[parity];
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < kWarps; ++w) v += sh.red_d[w];
+        e2.sum = v;
+    }
+    cluster.sync();
+    double tot = 0.0;
+    for (int r = 0; r < kCluster; ++r) tot += cluster.map_shared_rank(&e2, r)->sum;
+    parity ^= 1;
+    const double inv = 1.0 / tot;
+    if (threadIdx.x == 0) sh.x0 = __float_as_uint(static_cast<float>(static_cast<double>(expf(__ldg(logits) - m)) * inv));
+    for (int i = threadIdx.x; i < len; i += kThreads) {
+        const float v = static_cast<float>(static_cast<double>(expf(src(i) - m)) * inv);
+        if (kCached) xs[i] = v;
+        out[lo + i] = v;
+    }
+    __syncthreads();
+}
+
+template <bool kCached>
+__device__ void load_slice(float* xs, const float* __restrict__ x, int lo, int hi) {
+    const int len = hi - lo;
+    int i = threadIdx.x;
+    for (; i + 3 * kThreads < len; i += 4 * kThreads) {
+        const float a = __ldg(x + lo + i), b = __ldg(x + lo + i + kThreads), c = __ldg(x + lo + i + 2 * kThreads),
+                    d = __ldg(x + lo + i + 3 * kThreads);
+        xs[i] = a;
+        xs[i + kThreads] = b;
+        xs[i + 2 * kThreads] = c;
+        xs[i + 3 * kThreads] = d;
+    }
+    for (; i < len; i += kThreads) xs[i] = __ldg(x + lo + i);
+    __syncthreads();
+}
+
+// Local histogram of digit (bits >> shift) & 255 over this CTA's slice xs[0, len), restricted
 // to elements whose bits above (shift + 8) equal `prefix`, published to ex[parity]; then
 // the cluster-wide histogram (tc, tm) and the per-rank counts (loc) are gathered over DSMEM.
 // `validate` also records negative/NaN (bad) and > 1.5 (big) scores.
-__device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const float* __restrict__ x, int lo,
-                                  int hi, uint32_t prefix, int shift, bool with_mass, bool validate, int parity) {
+__device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const float* xs, int len, uint32_t prefix,
+                                  int shift, bool with_mass, bool validate, int& parity) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int b = lane; b < 256; b += 32) {
         sh.hc[warp][b] = 0;
@@ -103,14 +189,13 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
     __syncwarp();
     const uint32_t hi_mask = (shift + 8 >= 32) ? 0u : (0xffffffffu << (shift + 8));
     int bad = 0, big = 0;
-    const int span = hi - lo;
-    const int iters = span > 0 ? (span + kThreads - 1) / kThreads : 0;  // uniform across the CTA
+    const int iters = len > 0 ? (len + kThreads - 1) / kThreads : 0;  // uniform across the CTA
     for (int it = 0; it < iters; ++it) {
-        const int i = lo + it * kThreads + threadIdx.x;
+        const int i = it * kThreads + threadIdx.x;
         float v = 0.f;
         uint32_t key = kNoBucket;
-        if (i < hi) {
-            v = __ldg(x + i);
+        if (i < len) {
+            v = xs[i];
             const uint32_t bits = __float_as_uint(v);
             if (validate) {
                 if (!(v >= 0.f)) bad = 1;
@@ -118,19 +203,35 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
             }
             if ((bits & hi_mask) == (prefix & hi_mask)) key = (bits >> shift) & 255u;
         }
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        const bool leader = lane == __ffs(peers) - 1;
-        if (with_mass) {
-            const unsigned long long f = key != kNoBucket ? to_fix(v) : 0ull;
-            const uint32_t s0 = __reduce_add_sync(peers, static_cast<uint32_t>(f & 0x1fffffu));
-            const uint32_t s1 = __reduce_add_sync(peers, static_cast<uint32_t>((f >> 21) & 0x1fffffu));
-            const uint32_t s2 = __reduce_add_sync(peers, static_cast<uint32_t>(f >> 42));
-            if (leader && key != kNoBucket)
-                sh.hm[warp][key] += static_cast<unsigned long long>(s0) + (static_cast<unsigned long long>(s1) << 21) +
-                                    (static_cast<unsigned long long>(s2) << 42);
+        const unsigned long long f = (with_mass && key != kNoBucket) ? to_fix(v) : 0ull;
+        uint32_t rem = __ballot_sync(0xffffffffu, key != kNoBucket);
+        // merge the lanes sharing the first remaining lane's bucket with full-warp reductions
+        // (mass exact: three 21-bit pieces summed in u32), at most kMergeRounds times
+#pragma unroll
+        for (int round = 0; round < kMergeRounds; ++round) {
+            if (!rem) break;
+            const int src = __ffs(rem) - 1;
+            const uint32_t k0 = __shfl_sync(0xffffffffu, key, src);
+            const bool mine = key == k0;
+            const uint32_t grp = __ballot_sync(0xffffffffu, mine);
+            if (with_mass) {
+                const uint32_t s0 = __reduce_add_sync(0xffffffffu, mine ? static_cast<uint32_t>(f & 0x1fffffu) : 0u);
+                const uint32_t s1 =
+                    __reduce_add_sync(0xffffffffu, mine ? static_cast<uint32_t>((f >> 21) & 0x1fffffu) : 0u);
+                const uint32_t s2 = __reduce_add_sync(0xffffffffu, mine ? static_cast<uint32_t>(f >> 42) : 0u);
+                if (lane == src)
+                    sh.hm[warp][k0] += static_cast<unsigned long long>(s0) + (static_cast<unsigned long long>(s1) << 21) +
+                                       (static_cast<unsigned long long>(s2) << 42);
+            }
+            if (lane == src) sh.hc[warp][k0] += __popc(grp);
+            rem &= ~grp;
         }
-        // one leader per distinct key per warp: plain read-modify-write of the warp's own row
-        if (leader && key != kNoBucket) sh.hc[warp][key] += __popc(peers);
+        __syncwarp();
+        // the rest (spread buckets, rarely conflicting) go through shared-memory atomics
+        if ((rem >> lane) & 1u) {
+            atomicAdd(&sh.hc[warp][key], 1u);
+            if (with_mass) atomicAdd(&sh.hm[warp][key], f);
+        }
         __syncwarp();
     }
     if (validate) {
@@ -179,6 +280,7 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
         sh.bad = b;
         sh.big = g;
     }
+    parity ^= 1;
     __syncthreads();
 }
 
@@ -284,10 +386,12 @@ __device__ uint32_t block_scan(uint32_t v, uint32_t* buf, uint32_t& total) {
     return res;
 }
 
+template <bool kCached>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     select_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+    float* cache = reinterpret_cast<float*>(smem_raw + sizeof(Shared));
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = static_cast<int>(cluster.block_rank());
 
@@ -296,14 +400,26 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     const int n = p.n;
     const float* x = p.a[dir] + static_cast<size_t>(g) * n;
     const double tau = p.tau[dir][g];
-    const int slice = (n + kCluster - 1) / kCluster;
-    const int lo = min(n, rank * slice), hi = min(n, lo + slice);
+    int lo, hi;
+    slice_of(n, rank, lo, hi);
     if (threadIdx.x < kCluster) {
         sh.rank_above[threadIdx.x] = 0;
         sh.rank_eq[threadIdx.x] = 0;
     }
     __syncthreads();
     int parity = 0;
+    // this CTA's slice of the scores: shared memory when it fits, else global (L2)
+    if (p.logits[dir]) {
+        const float* lg = p.logits[dir] + static_cast<size_t>(g) * n;
+        if (kCached) load_slice<true>(cache, lg, lo, hi);
+        cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, const_cast<float*>(x), parity);
+    } else {
+        if (kCached) load_slice<true>(cache, x, lo, hi);
+        if (threadIdx.x == 0) sh.x0 = __float_as_uint(__ldg(x));
+        __syncthreads();
+    }
+    const float* xs = kCached ? cache : x + lo;
+    const int len = hi - lo;
 
     // ---- 1. mass radix-select; pass 0 also validates (sparsity.hpp:60-61)
     const double thr = tau - 1e-12;
@@ -313,8 +429,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     bool never = false;
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
-        cluster_histogram(sh, cluster, x, lo, hi, prefix, shift, true, pass == 0, parity);
-        parity ^= 1;
+        cluster_histogram(sh, cluster, xs, len, prefix, shift, true, pass == 0, parity);
         if (pass == 0) {
             if (threadIdx.x < 32) {
                 unsigned long long t = 0;
@@ -377,7 +492,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         if (rank == 0) {
             uint32_t* s = p.scratch + static_cast<size_t>(dir * p.hkv + g) * 2 * p.npow2;
             const int np2 = p.npow2;
-            for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? __float_as_uint(__ldg(x + i)) : 0u;
+            // plain loads: on the logits path x was written by this cluster (no .nc cache)
+            for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? __float_as_uint(x[i]) : 0u;
             __syncthreads();
             for (int size = 2; size <= np2; size <<= 1) {
                 for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -428,8 +544,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t gt = 0;
         for (int pass = 0; pass < 4; ++pass) {
             const int shift = 24 - 8 * pass;
-            cluster_histogram(sh, cluster, x, lo, hi, prefix, shift, false, false, parity);
-            parity ^= 1;
+            cluster_histogram(sh, cluster, xs, len, prefix, shift, false, false, parity);
             int bucket;
             unsigned long long am;
             uint32_t ac;
@@ -457,7 +572,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     const bool inject = (dir == 1);
     int zero_sel;
     {
-        const uint32_t b0 = __float_as_uint(__ldg(x));
+        const uint32_t b0 = sh.x0;
         zero_sel = (b0 > tbits) || (b0 == tbits && need_eq > 0);
     }
     const int shift_out = (inject && !zero_sel) ? 1 : 0;
@@ -471,7 +586,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < kItems; ++t) {
             const int i = i0 + t;
-            bits[t] = i < hi ? __float_as_uint(__ldg(x + i)) : 0u;
+            bits[t] = i < hi ? __float_as_uint(xs[i - lo]) : 0u;
             n_eq += (i < hi && bits[t] == tbits) ? 1u : 0u;
         }
         uint32_t eq_tot;
@@ -506,6 +621,28 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
 
+// Standalone cluster softmax of logit rows (vsp_indexer_scores): the same code as the
+// layer path's fused softmax, so both produce identical scores. grid (count * 8, 2).
+template <bool kCached>
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
+    softmax_kernel(const float* __restrict__ lv, const float* __restrict__ ls, float* av, float* as, int n, int g0) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+    float* cache = reinterpret_cast<float*>(smem_raw + sizeof(Shared));
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int g = g0 + static_cast<int>(blockIdx.x) / kCluster;
+    const size_t row = static_cast<size_t>(g) * n;
+    const float* lg = (blockIdx.y == 0 ? lv : ls) + row;
+    float* out = (blockIdx.y == 0 ? av : as) + row;
+    int lo, hi;
+    slice_of(n, rank, lo, hi);
+    int parity = 0;
+    if (kCached) load_slice<true>(cache, lg, lo, hi);
+    cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, out, parity);
+    cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
+}
+
 static int next_pow2(int n) {
     int p = 1;
     while (p < n) p <<= 1;
@@ -516,13 +653,28 @@ size_t workspace_bytes(int n, int hkv) {
     return static_cast<size_t>(2 * hkv) * 2 * next_pow2(n) * sizeof(uint32_t) + 2 * hkv * sizeof(int) + 512;
 }
 
-cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets, int* i_v,
-                   int* k_v, int* i_s, int* k_s, int cap, void* workspace, cudaStream_t stream, int g0, int count) {
+namespace {
+bool cached_slice(int n) { return (n + kCluster - 1) / kCluster <= kMaxCachedSlice; }
+int smem_bytes(int n) {
+    return static_cast<int>(sizeof(Shared)) + (cached_slice(n) ? ((n + kCluster - 1) / kCluster) * 4 : 0);
+}
+template <typename K>
+void allow_smem(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Shared)) + kMaxCachedSlice * 4);
+}
+}  // namespace
+
+cudaError_t launch_impl(const float* lv, const float* ls, const float* a_v, const float* a_s, int n, int hkv,
+                        const vsp_budget* budgets, int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* workspace,
+                        cudaStream_t stream, int g0, int count) {
     if (hkv > kMaxHeads) return cudaErrorInvalidValue;
     if (count < 0) count = hkv - g0;
     Params p{};  // ~3 KB parameter block, copied into the launch
     p.a[0] = a_v;
     p.a[1] = a_s;
+    p.logits[0] = lv;
+    p.logits[1] = ls;
     p.idx[0] = i_v;
     p.idx[1] = i_s;
     p.cnt[0] = k_v;
@@ -540,14 +692,46 @@ cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp
         p.min_b[g] = budgets[g].min_budget;
         p.max_b[g] = budgets[g].max_budget;
     }
-    const int smem = static_cast<int>(sizeof(Shared));
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        allow_smem(select_kernel<true>);
+        allow_smem(select_kernel<false>);
         attr = true;
     }
     p.g0 = g0;
-    select_kernel<<<dim3(count * kCluster, 2), kThreads, smem, stream>>>(p);
+    const dim3 grid(count * kCluster, 2);
+    if (cached_slice(n))
+        select_kernel<true><<<grid, kThreads, smem_bytes(n), stream>>>(p);
+    else
+        select_kernel<false><<<grid, kThreads, smem_bytes(n), stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch(const float* a_v, const float* a_s, int n, int hkv, const vsp_budget* budgets, int* i_v,
+                   int* k_v, int* i_s, int* k_s, int cap, void* workspace, cudaStream_t stream, int g0, int count) {
+    return launch_impl(nullptr, nullptr, a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, workspace, stream, g0,
+                       count);
+}
+
+cudaError_t launch_from_logits(const float* lv, const float* ls, float* a_v, float* a_s, int n, int hkv,
+                               const vsp_budget* budgets, int* i_v, int* k_v, int* i_s, int* k_s, int cap,
+                               void* workspace, cudaStream_t stream, int g0, int count) {
+    return launch_impl(lv, ls, a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, workspace, stream, g0, count);
+}
+
+cudaError_t launch_softmax(const float* lv, const float* ls, float* a_v, float* a_s, int n, int g0, int count,
+                           cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        allow_smem(softmax_kernel<true>);
+        allow_smem(softmax_kernel<false>);
+        attr = true;
+    }
+    const dim3 grid(count * kCluster, 2);
+    if (cached_slice(n))
+        softmax_kernel<true><<<grid, kThreads, smem_bytes(n), stream>>>(lv, ls, a_v, a_s, n, g0);
+    else
+        softmax_kernel<false><<<grid, kThreads, smem_bytes(n), stream>>>(lv, ls, a_v, a_s, n, g0);
     return cudaGetLastError();
 }
 

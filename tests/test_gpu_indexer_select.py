@@ -79,6 +79,25 @@ def test_indexer_zero_heads_uniform_and_single_token(vsp):
     assert (a_v1.cpu().numpy() == 1.0).all() and (a_s1.cpu().numpy() == 1.0).all()
 
 
+@pytest.mark.parametrize("n", [9, 4099, 300001])
+def test_indexer_softmax_exact_normaliser(vsp, n):
+    """A_v / A_s are the fp32 rounding of softmax(logits) with an fp64 normaliser (at n past
+    the shared-memory-cached slice size too): compare with float64 softmax of the logits."""
+    hkv = 1
+    g = torch.Generator().manual_seed(n)
+    k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    p = vsp.make_indexer_params(hkv, 128, 256, g, head_sigma=1.0)
+    a_v, a_s, lv, ls = vsp.indexer_forward(k, v, p, want_logits=True)
+    for a, lg in ((a_v, lv), (a_s, ls)):
+        want = torch.softmax(lg.double(), dim=1)
+        got = a.double()
+        assert abs(float(got.sum()) - 1.0) <= 1e-6
+        # fp32 exp of the fp32 difference (x - max): relative error <= ~2^-24 * |x - max| + 2 ulp
+        rel_tol = 4e-7 * max(1.0, float((lg - lg.max()).abs().max()))
+        assert float(((got - want).abs() / want.clamp_min(1e-30)).max()) <= rel_tol
+
+
 def test_indexer_slash_mapping_anchor(vsp):
     """One hidden unit carrying K feature 0 = t: Reverse puts silu(n-1-o) at offset o."""
     n, d_h = 40, 256
@@ -156,7 +175,7 @@ def _check_against_oracle(vsp, a_v, a_s, budgets):
     return pat
 
 
-@pytest.mark.parametrize("n", [1, 2, 37, 5000, 131072])
+@pytest.mark.parametrize("n", [1, 2, 37, 5000, 131072, 300001])
 def test_select_matches_oracle_random(vsp, n):
     rng = np.random.default_rng(n)
     hkv = 4
