@@ -163,6 +163,36 @@ VSP_API int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, 
 VSP_API int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n,
                         int hq, float* recall_per_head, void* stream);
 
+/* ---- interchange formats (host files; no device work) ------------------------------
+ * The reference's on-disk formats, so GPU outputs can be diffed against the reference CLI
+ * pipeline and one checkpoint drives both paths. Errors carry the reference's message text;
+ * std::runtime_error maps to VSP_ERUNTIME, std::invalid_argument to VSP_EINVAL.
+ *
+ * VSTN tensor (tensor_io.hpp:14-88): "VSTN", u32 version=1, u32 ndim, u64 dims[ndim],
+ * little-endian f64 row-major payload. rank = 1 / 2 reproduce read_vector / read_tensor
+ * (rank mismatch is an error with the reference text); rank <= 0 accepts any rank.
+ * `count` must equal the product of the file's dims (query it with vsp_tensor_header). */
+VSP_API int vsp_tensor_header(const char* path, int* ndim, uint64_t* dims, int max_dims);
+VSP_API int vsp_read_tensor(const char* path, int rank, double* data, uint64_t count);
+VSP_API int vsp_write_tensor(const char* path, int ndim, const uint64_t* dims, const double* data);
+
+/* VSCK indexer checkpoint, one per KV head (indexer.hpp:450-499, save_checkpoint /
+ * load_checkpoint): "VSCK", u32 version=1, u32 d, u32 d_h, then W_U [2d x d_h], b_U [d_h],
+ * w_v [d_h], b_v, w_s [d_h], b_s as little-endian f64. */
+VSP_API int vsp_checkpoint_header(const char* path, int* d, int* d_h);
+VSP_API int vsp_load_checkpoint(const char* path, int d, int d_h, double* w_u, double* b_u, double* w_v,
+                                double* b_v, double* w_s, double* b_s);
+VSP_API int vsp_save_checkpoint(const char* path, int d, int d_h, const double* w_u, const double* b_u,
+                                const double* w_v, double b_v, const double* w_s, double b_s);
+
+/* "V: ..." / "S: ..." index text (sparsity.hpp:187-245, write_indices / read_indices): one line
+ * per direction, ascending. vsp_read_indices fills up to `cap` entries per direction and
+ * rejects unsorted, negative or malformed lines with the reference's messages. */
+VSP_API int vsp_write_indices(const char* path, const int64_t* i_v, int64_t k_v, const int64_t* i_s,
+                              int64_t k_s);
+VSP_API int vsp_read_indices(const char* path, int64_t* i_v, int64_t* k_v, int64_t* i_s, int64_t* k_s,
+                             int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

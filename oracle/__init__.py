@@ -290,3 +290,97 @@ def ref() -> _Oracle:
 
 def have_ref() -> bool:
     return os.path.exists(REF_SO)
+
+
+# ---------------------------------------------------------------------- interchange formats
+# The reference's own VSTN / VSCK / index-text writers and readers (tensor_io.hpp,
+# indexer.hpp:450-499, sparsity.hpp:187-245) through oracle/_ref; used only to pin the
+# C-ABI implementations in csrc/formats.cpp (tests/test_formats.py, make_format_golden.py).
+
+class RefFormats:
+    """Returns (kind, value): kind "ok" or the reference's exception type
+    ("invalid_argument" / "runtime_error") with its message as value."""
+
+    def __init__(self):
+        lib = ctypes.CDLL(REF_SO)
+        cp, sz, i64, f64 = ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_double
+        lib.vspref_write_matrix.argtypes = [cp, i64, i64, _f64p, cp, sz]
+        lib.vspref_write_vector.argtypes = [cp, i64, _f64p, cp, sz]
+        lib.vspref_read_tensor.argtypes = [cp, ctypes.c_int, _i64p, _f64p, i64, cp, sz]
+        lib.vspref_save_checkpoint.argtypes = [cp, i64, i64, _f64p, _f64p, _f64p, f64, _f64p, f64, cp, sz]
+        lib.vspref_load_checkpoint.argtypes = [cp, _i64p, i64, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, cp, sz]
+        lib.vspref_write_indices.argtypes = [cp, _i64p, i64, _i64p, i64, cp, sz]
+        lib.vspref_read_indices.argtypes = [cp, _i64p, _i64p, _i64p, _i64p, i64, cp, sz]
+        self.lib = lib
+
+    @staticmethod
+    def _res(rc, err, value=None):
+        if rc == 0:
+            return "ok", value
+        return ("invalid_argument" if rc == 1 else "runtime_error"), err.value.decode()
+
+    def write_matrix(self, path, m):
+        m = np.ascontiguousarray(m, np.float64)
+        err = ctypes.create_string_buffer(512)
+        return self._res(self.lib.vspref_write_matrix(os.fsencode(path), m.shape[0], m.shape[1], _f(m), err, 512), err)
+
+    def write_vector(self, path, v):
+        v = np.ascontiguousarray(v, np.float64)
+        err = ctypes.create_string_buffer(512)
+        return self._res(self.lib.vspref_write_vector(os.fsencode(path), v.size, _f(v), err, 512), err)
+
+    def read(self, path, rank):
+        cap = max(os.path.getsize(path) // 8, 1) if os.path.exists(path) else 1
+        shape = np.zeros(2, np.int64)
+        data = np.zeros(cap, np.float64)
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.vspref_read_tensor(os.fsencode(path), rank, _i(shape), _f(data), cap, err, 512)
+        if rc:
+            return self._res(rc, err)
+        shp = (int(shape[0]), int(shape[1])) if rank == 2 else (int(shape[0]),)
+        return "ok", data[:int(np.prod(shp))].reshape(shp)
+
+    def save_checkpoint(self, path, w_u, b_u, w_v, b_v, w_s, b_s):
+        w_u = np.ascontiguousarray(w_u, np.float64)
+        b_u, w_v, w_s = (np.ascontiguousarray(x, np.float64) for x in (b_u, w_v, w_s))
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.vspref_save_checkpoint(os.fsencode(path), w_u.shape[0], w_u.shape[1], _f(w_u), _f(b_u),
+                                             _f(w_v), float(b_v), _f(w_s), float(b_s), err, 512)
+        return self._res(rc, err)
+
+    def load_checkpoint(self, path):
+        dims = np.zeros(2, np.int64)
+        err = ctypes.create_string_buffer(512)
+        z = np.zeros(1)
+        bv, bs = np.zeros(1), np.zeros(1)
+        rc = self.lib.vspref_load_checkpoint(os.fsencode(path), _i(dims), 0, _f(z), _f(z), _f(z), _f(bv), _f(z),
+                                             _f(bs), err, 512)
+        if rc:
+            return self._res(rc, err)
+        in_dim, dh = int(dims[0]), int(dims[1])
+        w_u, b_u, w_v, w_s = np.zeros((in_dim, dh)), np.zeros(dh), np.zeros(dh), np.zeros(dh)
+        rc = self.lib.vspref_load_checkpoint(os.fsencode(path), _i(dims), dh, _f(w_u), _f(b_u), _f(w_v), _f(bv),
+                                             _f(w_s), _f(bs), err, 512)
+        return self._res(rc, err, {"w_u": w_u, "b_u": b_u, "w_v": w_v, "b_v": float(bv[0]), "w_s": w_s,
+                                   "b_s": float(bs[0])})
+
+    def write_indices(self, path, iv, is_):
+        a = np.ascontiguousarray(iv, np.int64)
+        b = np.ascontiguousarray(is_, np.int64)
+        err = ctypes.create_string_buffer(512)
+        return self._res(self.lib.vspref_write_indices(os.fsencode(path), _i(a), a.size, _i(b), b.size, err, 512),
+                         err)
+
+    def read_indices(self, path):
+        cap = max(os.path.getsize(path), 1) if os.path.exists(path) else 1
+        a, b = np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+        kv, ks = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.vspref_read_indices(os.fsencode(path), _i(a), _i(kv), _i(b), _i(ks), cap, err, 512)
+        return self._res(rc, err, (a[:int(kv[0])].tolist(), b[:int(ks[0])].tolist()))
+
+
+def ref_formats() -> RefFormats:
+    if "fmt" not in _cache:
+        _cache["fmt"] = RefFormats()
+    return _cache["fmt"]

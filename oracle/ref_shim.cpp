@@ -20,6 +20,7 @@
 #include "vsprefill/indexer.hpp"
 #include "vsprefill/merge.hpp"
 #include "vsprefill/sparsity.hpp"
+#include "vsprefill/tensor_io.hpp"
 #include "vsprefill/vsaggregate.hpp"
 
 namespace {
@@ -52,6 +53,20 @@ int guarded(char* err, size_t errlen, F&& f) {
         return 0;
     } catch (const std::exception& e) {
         return set_err(err, errlen, e.what());
+    }
+}
+
+// Formats: 1 = std::invalid_argument, 2 = std::runtime_error (the types the tests assert).
+template <class F>
+int typed(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return set_err(err, errlen, e.what());
+    } catch (const std::runtime_error& e) {
+        set_err(err, errlen, e.what());
+        return 2;
     }
 }
 
@@ -299,6 +314,88 @@ int vspref_layer_dense(int64_t n, int64_t hq, int64_t hkv, int64_t d, const doub
     for (auto& th : pool) th.join();
     if (failed) return set_err(err, errlen, first_err.c_str());
     return 0;
+}
+
+// ---- interchange formats (tensor_io.hpp, indexer.hpp:450-499, sparsity.hpp:187-245) ----
+
+int vspref_write_matrix(const char* path, int64_t rows, int64_t cols, const double* data, char* err,
+                        size_t errlen) {
+    return typed(err, errlen, [&] { vsp::write_tensor(path, gather(data, cols, rows, cols)); });
+}
+
+int vspref_write_vector(const char* path, int64_t n, const double* data, char* err, size_t errlen) {
+    return typed(err, errlen, [&] { vsp::write_tensor(path, std::vector<double>(data, data + n)); });
+}
+
+// rank 2 -> read_tensor, rank 1 -> read_vector; shape_out[0..1] and data (cap values)
+int vspref_read_tensor(const char* path, int rank, int64_t* shape_out, double* data, int64_t cap, char* err,
+                       size_t errlen) {
+    return typed(err, errlen, [&] {
+        std::vector<double> v;
+        if (rank == 2) {
+            vsp::Matrix m = vsp::read_tensor(path);
+            shape_out[0] = static_cast<int64_t>(m.rows);
+            shape_out[1] = static_cast<int64_t>(m.cols);
+            v = std::move(m.data);
+        } else {
+            v = vsp::read_vector(path);
+            shape_out[0] = static_cast<int64_t>(v.size());
+        }
+        std::memcpy(data, v.data(), sizeof(double) * std::min<int64_t>(cap, static_cast<int64_t>(v.size())));
+    });
+}
+
+int vspref_save_checkpoint(const char* path, int64_t in_dim, int64_t d_h, const double* w_u, const double* b_u,
+                           const double* w_v, double b_v, const double* w_s, double b_s, char* err, size_t errlen) {
+    return typed(err, errlen, [&] {
+        vsp::IndexerParams p;
+        p.d_h = static_cast<size_t>(d_h);
+        p.w_u = gather(w_u, d_h, in_dim, d_h);
+        p.b_u.assign(b_u, b_u + d_h);
+        p.w_v.assign(w_v, w_v + d_h);
+        p.w_s.assign(w_s, w_s + d_h);
+        p.b_v = b_v;
+        p.b_s = b_s;
+        vsp::save_checkpoint(p, path);
+    });
+}
+
+// dims_out = {in_dim, d_h}; buffers sized by the caller (query with a first call, cap 0)
+int vspref_load_checkpoint(const char* path, int64_t* dims_out, int64_t cap_dh, double* w_u, double* b_u,
+                           double* w_v, double* b_v, double* w_s, double* b_s, char* err, size_t errlen) {
+    return typed(err, errlen, [&] {
+        vsp::IndexerParams p = vsp::load_checkpoint(path);
+        dims_out[0] = static_cast<int64_t>(p.in_dim());
+        dims_out[1] = static_cast<int64_t>(p.d_h);
+        if (cap_dh < static_cast<int64_t>(p.d_h)) return;
+        std::memcpy(w_u, p.w_u.data.data(), sizeof(double) * p.w_u.data.size());
+        std::memcpy(b_u, p.b_u.data(), sizeof(double) * p.d_h);
+        std::memcpy(w_v, p.w_v.data(), sizeof(double) * p.d_h);
+        std::memcpy(w_s, p.w_s.data(), sizeof(double) * p.d_h);
+        *b_v = p.b_v;
+        *b_s = p.b_s;
+    });
+}
+
+int vspref_write_indices(const char* path, const int64_t* iv, int64_t kv, const int64_t* is, int64_t ks, char* err,
+                         size_t errlen) {
+    return typed(err, errlen, [&] {
+        vsp::SelectedIndices sel;
+        sel.i_v = idx(iv, kv);
+        sel.i_s = idx(is, ks);
+        vsp::write_indices(path, sel);
+    });
+}
+
+int vspref_read_indices(const char* path, int64_t* iv, int64_t* kv, int64_t* is, int64_t* ks, int64_t cap,
+                        char* err, size_t errlen) {
+    return typed(err, errlen, [&] {
+        vsp::SelectedIndices sel = vsp::read_indices(std::string(path));
+        *kv = static_cast<int64_t>(sel.i_v.size());
+        *ks = static_cast<int64_t>(sel.i_s.size());
+        for (int64_t t = 0; t < std::min<int64_t>(cap, *kv); ++t) iv[t] = static_cast<int64_t>(sel.i_v[t]);
+        for (int64_t t = 0; t < std::min<int64_t>(cap, *ks); ++t) is[t] = static_cast<int64_t>(sel.i_s[t]);
+    });
 }
 
 }  // extern "C"

@@ -14,6 +14,15 @@
 #include "attn.h"
 #include "indexer.h"
 #include "select.h"
+#include "vsp_error.h"
+
+namespace vsp_detail {
+thread_local std::string g_err;
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace vsp_detail
 
 struct vsp_ctx {
     int device = 0;
@@ -32,12 +41,7 @@ struct vsp_ctx {
 
 namespace {
 
-thread_local std::string g_err;
-
-int set_err(int code, const std::string& msg) {
-    g_err = msg;
-    return code;
-}
+using vsp_detail::set_err;
 int cuda_err(cudaError_t e, const char* where) {
     return set_err(VSP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
@@ -112,7 +116,7 @@ int check_attn_shapes(int n, int hq, int hkv, int d) {
 
 extern "C" {
 
-const char* vsp_last_error(void) { return g_err.c_str(); }
+const char* vsp_last_error(void) { return vsp_detail::g_err.c_str(); }
 const char* vsp_version(void) { return "vsp-b200 0.1 (sm_100a)"; }
 
 int vsp_create(vsp_ctx** out, int device) {
