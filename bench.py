@@ -308,20 +308,25 @@ def main():
     v = shard(v_full, rank, world, 1)
     if world > 1:
         del q_full, k_full, v_full
-    o = torch.empty_like(q)
-    lse = torch.empty(hq_r, n, device=dev)
+    # O is written head-major straight into this rank's slab of the full [Hq, n, d] output
+    # (VSP_O_HEAD_MAJOR): the slab is the in-place all-gather send buffer (parallel.py)
+    from paper_2603_04460_b200 import parallel
+    o_full = torch.empty(args.hq, n, 128, dtype=q.dtype, device=dev)
+    lse_full = torch.empty(args.hq, n, device=dev)
+    o = parallel.head_slab(o_full, rank, world)
+    lse = parallel.head_slab(lse_full, rank, world)
 
     hpc = args.heads_per_chunk
 
     def step():
         # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3, pipelined over KV-head chunks
-        _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse)
+        _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse, head_major=True)
         return pat
 
     def step_unfused():
         a_v, a_s = vsp.indexer_forward(k, v, params)
         pat = vsp.select_pattern(a_v, a_s, budget)
-        vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
+        vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse, head_major=True)
         return pat
 
     def barrier():
@@ -369,12 +374,12 @@ def main():
     ms_unfused = timed(step_unfused)
     ms_indexer = timed(lambda: vsp.indexer_forward(k, v, params))
     ms_select = timed(lambda: vsp.select_pattern(a_v, a_s, budget))
-    ms_attn = timed(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse))
+    ms_attn = timed(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse, head_major=True))
     tiles, tiles_dense = vsp.sparse_tile_stats(n, hkv_r, pat.i_v.shape[1], dev)
     o_d = torch.empty_like(q)
     lse_d = torch.empty_like(lse)
     ms_dense = timed(lambda: vsp.blockwise_attention(q, k, v, out=o_d, lse=lse_d))
-    vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse)
+    vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse, head_major=True)
     recall = float(vsp.attention_recall(lse, lse_d).mean().item())
     pairs_kv = covered_pairs(pat, n, hkv_r)
     grp = args.hq // args.hkv
@@ -393,9 +398,10 @@ def main():
 
     allgather_ms = None
     if world > 1:
-        full = torch.empty(world * hq_r, n, 128, dtype=q.dtype, device=dev)
-        oh = o.permute(1, 0, 2).contiguous()  # head-major shard
-        allgather_ms = timed(lambda: torch.distributed.all_gather_into_tensor(full, oh), reps=3)
+        # one in-place ncclAllGather of the head-major slabs (O and LSE) through the C ABI
+        comm = parallel.VspComm(dev)
+        allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
+        comm.close()
 
     # ---- e2e through the public API with host buffers (H2D inputs, D2H output every step)
     e2e = None
@@ -403,7 +409,7 @@ def main():
         qh = q.cpu().pin_memory()
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
-        oh_ = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+        oh_ = torch.empty(q.shape, dtype=q.dtype).pin_memory()
         lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
 
         def e2e_step():

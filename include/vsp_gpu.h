@@ -61,7 +61,12 @@ enum { VSP_SLASH_REVERSE = 0, VSP_SLASH_IDENTITY = 1 };
 /* Group reduce (vsaggregate.hpp:131): 0 = Mean, 1 = Sum. */
 enum { VSP_REDUCE_MEAN = 0, VSP_REDUCE_SUM = 1 };
 /* vsp_vs_attn_fwd flags */
-enum { VSP_VALIDATE = 1 /* sync + check sortedness/range/coverage like the reference */ };
+enum {
+    VSP_VALIDATE = 1,     /* sync + check sortedness/range/coverage like the reference */
+    VSP_O_HEAD_MAJOR = 2  /* write O head-major [hq, n, 128] (the reference's per-head n x d
+                             matrices) instead of token-major [n, hq, 128]; a rank's heads are
+                             then one contiguous slab, the in-place all-gather send buffer */
+};
 
 /* Reference BudgetConfig (sparsity.hpp:22-36). max_budget < 0 means "no maximum". */
 typedef struct {
@@ -128,7 +133,7 @@ VSP_API int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const voi
                            const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
                            const vsp_budget* budgets, float* a_v, float* a_s, int* i_v, int* k_v, int* i_s,
                            int* k_s, int cap, void* o, float* lse, void* workspace, int heads_per_chunk,
-                           void* stream);
+                           int flags, void* stream);
 
 /* ---- the layer from HOST buffers (the reference's own calling convention) ----------
  * The reference operators take and return host memory (std::vector; attention.hpp:150,
@@ -162,6 +167,21 @@ VSP_API int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, 
 /* ---- recall from LSE pairs: mean_i exp(lse_sparse - lse_dense) per Q head ---------- */
 VSP_API int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n,
                         int hq, float* recall_per_head, void* stream);
+
+/* ---- multi-GPU output assembly --------------------------------------
+ * KV heads shard across ranks with no collective on the data path. The only exchange is
+ * assembling O: each rank writes its Q heads with VSP_O_HEAD_MAJOR into their slab of the
+ * full head-major O [hq, n, d] (pass o = o_full + first_head * n * d), then
+ * vsp_allgather_heads runs ONE in-place ncclAllGather over NVLink (plus one for LSE
+ * [hq, n] when lse_full is non-null). Rank r owns heads [r*hq/world, (r+1)*hq/world).
+ * NCCL is dlopen'ed on first use. The unique id (vsp_comm_id_bytes() bytes) is made on
+ * one rank and shipped to the others by the caller (the reference has no transport). */
+typedef struct vsp_comm vsp_comm;
+VSP_API size_t vsp_comm_id_bytes(void);
+VSP_API int vsp_comm_unique_id(uint8_t* id);
+VSP_API int vsp_comm_init(vsp_comm** comm, int world, int rank, const uint8_t* id, int device);
+VSP_API int vsp_comm_destroy(vsp_comm* comm);
+VSP_API int vsp_allgather_heads(vsp_comm* comm, void* o_full, float* lse_full, int n, int hq, int d, void* stream);
 
 /* ---- interchange formats (host files; no device work) ------------------------------
  * The reference's on-disk formats, so GPU outputs can be diffed against the reference CLI

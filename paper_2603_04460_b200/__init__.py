@@ -39,6 +39,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_PKG, "libvsp_gpu.so")
 
 VSP_OK, VSP_EINVAL, VSP_ERUNTIME, VSP_ECUDA, VSP_ENCCL = range(5)
+VSP_VALIDATE, VSP_O_HEAD_MAJOR = 1, 2
 
 
 class VspError(ValueError):
@@ -93,7 +94,7 @@ def load_library():
     lib.vsp_vs_prefill_workspace_size.restype = sz
     lib.vsp_vs_prefill_workspace_size.argtypes = [i, i, i, i]
     lib.vsp_vs_prefill.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
-                                    ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, vp])
+                                    ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, i, vp])
     _lib = lib
     return lib
 
@@ -247,23 +248,25 @@ def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget, validate: bool 
 
 def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern: SelectedIndices,
                      validate: bool = True, out: Optional[torch.Tensor] = None,
-                     lse: Optional[torch.Tensor] = None):
+                     lse: Optional[torch.Tensor] = None, head_major: bool = False):
     """sparse_attention (attention.hpp:150-194) for every Q head -> (O [n, Hq, d] bf16,
     LSE [Hq, n] fp32). validate=True reproduces the reference's checks and messages
-    (merge.hpp:21-26, attention.hpp:161-163) at the cost of one stream sync."""
+    (merge.hpp:21-26, attention.hpp:161-163) at the cost of one stream sync.
+    head_major=True writes O as [Hq, n, d] (the reference's per-head matrices)."""
     _need_cuda(q, k, v)
     n, hq, d = q.shape
     hkv = k.shape[1]
     lib = load_library()
     dev = q.device
-    o = out if out is not None else torch.empty_like(q)
+    o = out if out is not None else (torch.empty(hq, n, d, dtype=q.dtype, device=dev) if head_major
+                                     else torch.empty_like(q))
     lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
     cap = pattern.i_v.shape[1]
     ws = _workspace(dev, lib.vsp_vs_attn_workspace_size(n, hkv, cap))
     _check(lib.vsp_vs_attn_fwd(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, _ptr(pattern.i_v),
                                _ptr(pattern.k_v), _ptr(pattern.i_s), _ptr(pattern.k_s), cap,
-                               1.0 / math.sqrt(d), _ptr(o), _ptr(lse), _ptr(ws), 1 if validate else 0,
-                               _stream(dev)))
+                               1.0 / math.sqrt(d), _ptr(o), _ptr(lse), _ptr(ws),
+                               (1 if validate else 0) | (VSP_O_HEAD_MAJOR if head_major else 0), _stream(dev)))
     return o, lse
 
 
@@ -326,12 +329,13 @@ def attention_recall(lse_sparse: torch.Tensor, lse_dense: torch.Tensor) -> torch
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
                mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
-               lse: Optional[torch.Tensor] = None):
+               lse: Optional[torch.Tensor] = None, head_major: bool = False):
     """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
     indexer -> selection -> sparse attention, pipelined over KV-head chunks so that the
     scoring/selection/planning of chunk c+1 overlaps chunk c's attention. Mirrors
     `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
     Same results as indexer_forward + select_pattern + sparse_attention.
+    head_major=True writes O as [Hq, n, d] (e.g. a slab of the full output on a shard rank).
     Returns (O, LSE, SelectedIndices)."""
     _need_cuda(q, k, v)
     n, hq, d = q.shape
@@ -349,14 +353,16 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
     i_s = torch.empty_like(i_v)
     k_v = torch.empty(hkv, device=dev, dtype=torch.int32)
     k_s = torch.empty_like(k_v)
-    o = out if out is not None else torch.empty_like(q)
+    o = out if out is not None else (torch.empty(hq, n, d, dtype=q.dtype, device=dev) if head_major
+                                     else torch.empty_like(q))
     lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
     ws = _workspace(dev, lib.vsp_vs_prefill_workspace_size(n, hkv, params.d_h, cap))
     _check(lib.vsp_vs_prefill(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h,
                               _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
                               _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
                               _ptr(a_v), _ptr(a_s), _ptr(i_v), _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(o),
-                              _ptr(lse), _ptr(ws), int(heads_per_chunk), _stream(dev)))
+                              _ptr(lse), _ptr(ws), int(heads_per_chunk), VSP_O_HEAD_MAJOR if head_major else 0,
+                              _stream(dev)))
     return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
 
 

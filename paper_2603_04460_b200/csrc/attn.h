@@ -14,8 +14,9 @@ struct __align__(64) AttnParams {
     CUtensorMap map_v;
     CUtensorMap map_kv;  // gathered verticals [hkv, kvcap, 128], box {64, 128, 1}
     CUtensorMap map_vv;
-    __nv_bfloat16* o;    // [n, hq, 128]
+    __nv_bfloat16* o;    // row i of head h at o + i * o_tok_stride + h * o_head_stride
     float* lse;          // [hq, n] or null
+    long long o_tok_stride, o_head_stride;  // elements: [n, hq, 128] -> (hq*128, 128); head-major -> (128, n*128)
     const int* tile_lists;
     const uint32_t* vbits;
     const uint32_t* sbits;
@@ -30,10 +31,11 @@ struct AttnArgs {
     const void* q;  // [n, hq, 128] bf16
     const void* k;  // [n, hkv, 128] bf16
     const void* v;  // [n, hkv, 128] bf16
-    void* o;        // [n, hq, 128] bf16
+    void* o;        // [n, hq, 128] bf16 (token-major) or [hq, n, 128] (o_head_major)
     float* lse;     // [hq, n] fp32, may be null
     int n, hq, hkv;
     float scale;
+    bool o_head_major = false;
 };
 
 struct SparseArgs {

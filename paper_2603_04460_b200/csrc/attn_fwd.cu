@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         tc_fence_after();
         const int h = h0 + w;
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow = p.o + (static_cast<size_t>(i) * p.hq + h) * kHeadDim;
+        __nv_bfloat16* orow = p.o + static_cast<long long>(i) * p.o_tok_stride + static_cast<long long>(h) * p.o_head_stride;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t u[32];
@@ -564,6 +564,11 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
 
 // ------------------------------------------------------------------ host launchers
 
+static void set_o_layout(AttnParams& p, const AttnArgs& a) {
+    p.o_tok_stride = a.o_head_major ? kHeadDim : static_cast<long long>(a.hq) * kHeadDim;
+    p.o_head_stride = a.o_head_major ? static_cast<long long>(a.n) * kHeadDim : kHeadDim;
+}
+
 static bool make_qkv_maps(AttnParams& p, const void* q, const void* k, const void* v) {
     const uint32_t box[3] = {64, 1, kBlock};
     const uint64_t dq[3] = {kHeadDim, (uint64_t)p.hq, (uint64_t)p.n};
@@ -583,6 +588,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     p.scale = a.scale;
     p.o = static_cast<__nv_bfloat16*>(a.o);
     p.lse = a.lse;
+    set_o_layout(p, a);
     if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
@@ -623,6 +629,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
     p.scale = a.scale;
     p.o = static_cast<__nv_bfloat16*>(a.o);
     p.lse = a.lse;
+    set_o_layout(p, a);
     if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     const int kvcap = ((s.cap + kBlock - 1) / kBlock) * kBlock;

@@ -214,7 +214,8 @@ int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, i
             if (hflags[g] & 4) return set_err(VSP_EINVAL, "uncovered query row 0");
         }
     }
-    vsp_attn::AttnArgs a{q, k, v, o, lse, n, hq, hkv, scale};
+    if (flags & ~(VSP_VALIDATE | VSP_O_HEAD_MAJOR)) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: unknown flags");
+    vsp_attn::AttnArgs a{q, k, v, o, lse, n, hq, hkv, scale, (flags & VSP_O_HEAD_MAJOR) != 0};
     vsp_attn::SparseArgs s{i_v, k_v, i_s, k_s, cap};
     cudaError_t e = vsp_attn::launch_sparse(a, s, workspace, st);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_attn_fwd");
@@ -344,6 +345,7 @@ struct PrefillDev {
     int *i_v, *k_v, *i_s, *k_s;
     void* o;
     float* lse;
+    bool o_head_major;
 };
 
 int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping, const vsp_budget* budgets,
@@ -390,7 +392,7 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
     cudaStream_t side = ctx->side;
     cudaError_t e = cudaEventRecord(ctx->ev_start, main);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
-    vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d))};
+    vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
     vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
         int g0, cnt;
@@ -434,12 +436,14 @@ extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const 
                               int d, int d_h, const void* w_u, const float* b_u, const float* w_v, const float* b_v,
                               const float* w_s, const float* b_s, int slash_mapping, const vsp_budget* budgets,
                               float* a_v, float* a_s, int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* o,
-                              float* lse, void* workspace, int heads_per_chunk, void* stream) {
+                              float* lse, void* workspace, int heads_per_chunk, int flags, void* stream) {
     VSP_CHECK_CTX(ctx);
     int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, heads_per_chunk,
                            "vsp_vs_prefill");
     if (rc) return rc;
-    PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse};
+    if (flags & ~VSP_O_HEAD_MAJOR) return set_err(VSP_EINVAL, "vsp_vs_prefill: unknown flags");
+    PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse,
+                 (flags & VSP_O_HEAD_MAJOR) != 0};
     cudaError_t e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace,
                                     heads_per_chunk, as_stream(stream), nullptr, nullptr,
                                     nullptr);
@@ -506,7 +510,7 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
             e = cudaMemcpy2DAsync(q_d + qoff, qp, qh + qoff, qp, qw, n, cudaMemcpyHostToDevice, ctx->h2d);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q[c], ctx->h2d);
     }
-    PrefillDev p{q_d, k_d, v_d, w_u, b_u, w_v, b_v, w_s, b_s, av_d, as_d, iv_d, kv_d, is_d, ks_d, o_d, lse_d};
+    PrefillDev p{q_d, k_d, v_d, w_u, b_u, w_v, b_v, w_s, b_s, av_d, as_d, iv_d, kv_d, is_d, ks_d, o_d, lse_d, false};
     if (e == cudaSuccess)
         e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, hpc, main, ctx->ev_kv,
                             ctx->ev_q, ctx->ev_attn);

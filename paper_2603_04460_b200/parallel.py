@@ -3,13 +3,17 @@
 Every hot-path step is per KV head (indexer, selection, and the sparse attention of the Q
 heads in the group), so a layer splits into independent shards with NO collective on the
 data path. Rank r owns KV heads [r*Hkv/N, (r+1)*Hkv/N) and their Q heads. The only
-collective is the optional all-gather that assembles the full output: each rank's O is
-made head-major [Hq/N, n, d] so its shard is one contiguous send buffer, and
-`all_gather_into_tensor` over NCCL (NVLink/NVSwitch) lands it as [Hq, n, d].
+collective is the all-gather that assembles the full output. The sharded layer writes its
+O head-major straight into its slab of the full [Hq, n, d] buffer (`head_slab`,
+VSP_O_HEAD_MAJOR), so the slab IS the send buffer and `VspComm.allgather_heads` is one
+in-place ncclAllGather over NVLink/NVSwitch through the C ABI (vsp_allgather_heads) — no
+permute and no staging copy. `assemble_heads` is the torch.distributed equivalent for a
+token-major shard.
 """
 from __future__ import annotations
 
-from typing import Tuple
+import ctypes
+from typing import Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -44,3 +48,67 @@ def max_over_ranks(value: float, device) -> float:
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def head_slab(o_full: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    """Rank `rank`'s contiguous slab [Hq/N, n, d] of a head-major output [Hq, n, d]: the
+    `out=` of vs_prefill / sparse_attention with head_major=True, and the in-place send
+    buffer of VspComm.allgather_heads."""
+    lo, hi = head_range(o_full.shape[0], rank, world)
+    return o_full[lo:hi]
+
+
+def exchange_unique_id(make_id, group=None) -> bytes:
+    """Rank 0 makes the NCCL unique id and every rank of `group` receives it (over whatever
+    backend the group has: gloo on CPU, nccl on GPU)."""
+    box = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return box[0]
+
+
+class VspComm:
+    """An NCCL communicator owned by the C ABI (vsp_comm_init) for vsp_allgather_heads."""
+
+    def __init__(self, device: torch.device, group=None):
+        from . import _check, load_library
+        self._lib = lib = load_library()
+        lib.vsp_comm_id_bytes.restype = ctypes.c_size_t
+        lib.vsp_comm_unique_id.argtypes = [ctypes.c_char_p]
+        lib.vsp_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                      ctypes.c_int]
+        lib.vsp_comm_destroy.argtypes = [ctypes.c_void_p]
+        lib.vsp_allgather_heads.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        self._check = _check
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device
+
+        def make_id():
+            buf = ctypes.create_string_buffer(lib.vsp_comm_id_bytes())
+            _check(lib.vsp_comm_unique_id(buf))
+            return buf.raw
+
+        uid = exchange_unique_id(make_id, group) if self.world > 1 else make_id()
+        h = ctypes.c_void_p()
+        _check(lib.vsp_comm_init(ctypes.byref(h), self.world, self.rank, uid, device.index or 0))
+        self._h = h
+
+    def allgather_heads(self, o_full: torch.Tensor, lse_full: Optional[torch.Tensor] = None) -> None:
+        """In-place: this rank's slab of o_full [Hq, n, d] (and lse_full [Hq, n]) -> everywhere."""
+        hq, n, d = o_full.shape
+        st = ctypes.c_void_p(torch.cuda.current_stream(o_full.device).cuda_stream)
+        self._check(self._lib.vsp_allgather_heads(self._h, ctypes.c_void_p(o_full.data_ptr()),
+                                                  ctypes.c_void_p(lse_full.data_ptr() if lse_full is not None else 0),
+                                                  n, hq, d, st))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._check(self._lib.vsp_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

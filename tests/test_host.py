@@ -125,6 +125,32 @@ def _worker(rank, world, port, n, hq, d, q):
     full = parallel.assemble_heads(mine)
     ok = torch.equal(full, o_full.permute(1, 0, 2))
     t = parallel.max_over_ranks(float(rank + 1), "cpu")
+    # the C-ABI path: the NCCL unique id made by rank 0 (vsp_comm_unique_id) reaches every rank
+    import ctypes
+    import paper_2603_04460_b200 as vsp
+    lib = vsp.load_library()
+    lib.vsp_comm_id_bytes.restype = ctypes.c_size_t
+
+    def make_id():
+        buf = ctypes.create_string_buffer(lib.vsp_comm_id_bytes())
+        vsp._check(lib.vsp_comm_unique_id(buf))
+        return buf.raw
+
+    uid = parallel.exchange_unique_id(make_id)
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    ok_id = len(uid) == 128 and all(x == uid for x in ids)
+    # head-major slabs: each rank fills only its slab, an in-place all-gather of the slabs
+    # (vsp_allgather_heads semantics) gives the full head-major output
+    buf = torch.zeros(hq, n, d)
+    slab = parallel.head_slab(buf, rank, world)
+    lo, hi = parallel.head_range(hq, rank, world)
+    slab.copy_(o_full.permute(1, 0, 2)[lo:hi])
+    parts = [torch.empty_like(slab) for _ in range(world)]
+    dist.all_gather(parts, slab.contiguous())
+    for r_, part in enumerate(parts):
+        parallel.head_slab(buf, r_, world).copy_(part)
+    ok = ok and ok_id and torch.equal(buf, o_full.permute(1, 0, 2)) and slab.data_ptr() == buf[lo].data_ptr()
     q.put((rank, ok, t, parallel.head_range(8, rank, world)))
     dist.destroy_process_group()
 
