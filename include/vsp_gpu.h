@@ -84,6 +84,16 @@ VSP_API const char* vsp_version(void);
 VSP_API int vsp_create(vsp_ctx** ctx, int device);
 VSP_API int vsp_destroy(vsp_ctx* ctx);
 
+/* ---- the step before the path: RoPE feed ------------------------------------------
+ * apply_rope (rope.hpp:63-79) on Q [n, hq, d] and K [n, hkv, d] bf16 in ONE HBM pass:
+ * plane p of the vector at position t rotates by t * base^(-2p/d); positions null means
+ * t = row index. Out-of-place or in place (q_out == q_in). hq or hkv may be 0 to rotate one
+ * tensor. VSP_ROPE_INTERLEAVED pairs (2p, 2p+1) (the reference); VSP_ROPE_HALF_SPLIT pairs
+ * (p, p + d/2) (HF LLaMA/Qwen checkpoints). Angles in fp64, rotation in fp32, bf16 out. */
+enum { VSP_ROPE_INTERLEAVED = 0, VSP_ROPE_HALF_SPLIT = 1 };
+VSP_API int vsp_apply_rope(vsp_ctx* ctx, const void* q_in, const void* k_in, void* q_out, void* k_out, int n,
+                           int hq, int hkv, int d, const int64_t* positions, double base, int style, void* stream);
+
 /* ---- K1: VSIndexer scoring -------------------------------------------------------
  * X_t = [K_t | V_t] (per KV head), Z = SiLU(X W_U + b_U), logit_v = Z w_v + b_v,
  * raw_s = Z w_s + b_s, logit_s[o] = raw_s[n-1-o] (Reverse) or raw_s[o] (Identity),

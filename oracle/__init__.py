@@ -52,6 +52,8 @@ def _bind(lib, prefix: str):
                                            _f64p, _f64p, _f64p, _f64p, _cp, ctypes.c_size_t]),
         "aggregate_streaming": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64, ctypes.c_int,
                                                _f64p, _f64p, _cp, ctypes.c_size_t]),
+        "apply_rope": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _i64p, ctypes.c_double, _f64p, _i64, _cp,
+                                      ctypes.c_size_t]),
     }
     if prefix == "vso_":
         sig["blockwise_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64,
@@ -225,6 +227,16 @@ class _Oracle:
                              _f(vert), _f(sl))
         self._check(rc, msg)
         return vert, sl
+
+    def apply_rope(self, x, positions=None, base=10000.0):
+        """x [n, d] f64 -> rotated copy (rope.hpp:63-79)."""
+        x = np.ascontiguousarray(x, np.float64)
+        n, d = x.shape
+        out = np.zeros_like(x)
+        pos = None if positions is None else np.ascontiguousarray(positions, np.int64)
+        rc, msg = self._call("apply_rope", n, d, _f(x), d, None if pos is None else _i(pos), float(base), _f(out), d)
+        self._check(rc, msg)
+        return out
 
     def combine_scores(self, verts, slashes, mean=True):
         v = np.ascontiguousarray(np.stack(verts), np.float64)

@@ -19,6 +19,7 @@
 #include "vsprefill/attention.hpp"
 #include "vsprefill/indexer.hpp"
 #include "vsprefill/merge.hpp"
+#include "vsprefill/rope.hpp"
 #include "vsprefill/sparsity.hpp"
 #include "vsprefill/tensor_io.hpp"
 #include "vsprefill/vsaggregate.hpp"
@@ -395,6 +396,17 @@ int vspref_read_indices(const char* path, int64_t* iv, int64_t* kv, int64_t* is,
         *ks = static_cast<int64_t>(sel.i_s.size());
         for (int64_t t = 0; t < std::min<int64_t>(cap, *kv); ++t) iv[t] = static_cast<int64_t>(sel.i_v[t]);
         for (int64_t t = 0; t < std::min<int64_t>(cap, *ks); ++t) is[t] = static_cast<int64_t>(sel.i_s[t]);
+    });
+}
+
+// ---- RoPE (rope.hpp:63-79): same argument convention as vso_apply_rope
+int vspref_apply_rope(int64_t n, int64_t d, const double* x, int64_t xs, const int64_t* positions, double base,
+                      double* out, int64_t os, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const vsp::RopeConfig cfg(static_cast<size_t>(d), base);
+        const vsp::Matrix m = gather(x, xs, n, d);
+        vsp::Matrix r = positions ? vsp::apply_rope(m, idx(positions, n), cfg) : vsp::apply_rope(m, cfg);
+        for (int64_t t = 0; t < n; ++t) std::memcpy(out + t * os, r.row_ptr(t), sizeof(double) * d);
     });
 }
 

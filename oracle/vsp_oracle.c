@@ -478,3 +478,27 @@ void vso_combine_scores(int64_t heads, int64_t n, const double* v_in, const doub
         }
     }
 }
+
+/* ------------------------------------------------------------------ RoPE */
+
+/* RopeConfig (rope.hpp:13-39) + apply_rope (rope.hpp:63-79) for one head: row t of x
+ * (n x d, row stride xs) rotated by R(positions[t]) (positions NULL: t), plane p pairs
+ * (2p, 2p+1) and rotates by t * base^(-2p/d). out may alias x. */
+int vso_apply_rope(int64_t n, int64_t d, const double* x, int64_t xs, const int64_t* positions, double base,
+                   double* out, int64_t os, char* err, size_t errlen) {
+    if (d < 2 || d % 2 != 0) return fail(err, errlen, "rope head_dim must be even and >= 2");
+    if (!(base > 0.0)) return fail(err, errlen, "rope base must be positive");
+    for (int64_t i = 0; i < n; ++i) {
+        const double t = positions ? (double)positions[i] : (double)i;
+        const double* src = x + i * xs;
+        double* dst = out + i * os;
+        for (int64_t p = 0; p < d / 2; ++p) {
+            const double angle = t * pow(base, -2.0 * (double)p / (double)d);
+            const double c = cos(angle), s = sin(angle);
+            const double a = src[2 * p], b = src[2 * p + 1];
+            dst[2 * p] = c * a - s * b;
+            dst[2 * p + 1] = s * a + c * b;
+        }
+    }
+    return VSO_OK;
+}

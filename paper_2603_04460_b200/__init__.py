@@ -15,6 +15,7 @@ the extension (libvsp_gpu.so) or an sm_100 device is missing.
     vsp::aggregate_streaming vsaggregate.hpp:62 aggregate_streaming(q, k)
       + combine_scores     vsaggregate.hpp:133    (group reduce fused)
     vsp::attention_recall  attention.hpp:198    attention_recall(lse_sparse, lse_dense)
+    vsp::apply_rope        rope.hpp:63          apply_rope(x, positions, cfg) / apply_rope_qk(q, k, ...)
 
 Tensors are batched over heads: Q [n, Hq, 128], K/V [n, Hkv, 128] bf16 (Q head h reads
 KV head h // (Hq // Hkv)); one VS pattern per KV head, shared by its Q heads.
@@ -32,7 +33,7 @@ import torch
 __all__ = [
     "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
     "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
-    "aggregate_streaming", "attention_recall", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "lib_path", "load_library",
+    "aggregate_streaming", "attention_recall", "RopeConfig", "apply_rope", "apply_rope_qk", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "lib_path", "load_library",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -95,6 +96,7 @@ def load_library():
     lib.vsp_vs_prefill_workspace_size.argtypes = [i, i, i, i]
     lib.vsp_vs_prefill.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
                                     ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, i, vp])
+    lib.vsp_apply_rope.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, vp, ctypes.c_double, i, vp]
     _lib = lib
     return lib
 
@@ -204,7 +206,57 @@ def make_indexer_params(hkv: int, d: int, d_h: int, generator: torch.Generator, 
                          torch.zeros(hkv, device=device), w_s.to(device), torch.zeros(hkv, device=device))
 
 
+@dataclasses.dataclass
+class RopeConfig:
+    """rope.hpp:13-39 (theta_p = base^(-2p/head_dim)), plus the pairing style: "interleaved"
+    (2p, 2p+1), the reference's, or "half_split" (p, p + d/2) for HF checkpoints."""
+    head_dim: int = 128
+    base: float = 10000.0
+    style: str = "interleaved"
+
+    def __post_init__(self):
+        if self.head_dim < 2 or self.head_dim % 2 != 0:
+            raise VspError("rope head_dim must be even and >= 2")
+        if not self.base > 0.0:
+            raise VspError("rope base must be positive")
+        if self.style not in ("interleaved", "half_split"):
+            raise VspError("rope style must be 'interleaved' or 'half_split'")
+
+    def theta(self, p: int) -> float:
+        return self.base ** (-2.0 * p / self.head_dim)
+
+
 # ---------------------------------------------------------------------- operators
+
+def apply_rope_qk(q: Optional[torch.Tensor], k: Optional[torch.Tensor], positions: Optional[torch.Tensor] = None,
+                  cfg: Optional[RopeConfig] = None, inplace: bool = False):
+    """The RoPE feed before the path: apply_rope (rope.hpp:63-79) on Q [n, Hq, d] and K
+    [n, Hkv, d] bf16 in ONE HBM pass (vsp_apply_rope). positions: int64 [n] on the device,
+    or None for t = row index. Returns (Q', K') (the inputs themselves when inplace)."""
+    ref = q if q is not None else k
+    _need_cuda(*(t for t in (q, k) if t is not None))
+    n, _, d = ref.shape
+    cfg = cfg or RopeConfig(d)
+    if cfg.head_dim != d:
+        raise VspError("apply_rope: column count != head_dim")
+    if positions is not None:
+        if positions.numel() != n:
+            raise VspError("apply_rope: positions length != row count")
+        positions = positions.to(device=ref.device, dtype=torch.int64).contiguous()
+    qo = None if q is None else (q if inplace else torch.empty_like(q))
+    ko = None if k is None else (k if inplace else torch.empty_like(k))
+    lib = load_library()
+    _check(lib.vsp_apply_rope(_context(ref.device), _ptr(q), _ptr(k), _ptr(qo), _ptr(ko), n,
+                              0 if q is None else q.shape[1], 0 if k is None else k.shape[1], d, _ptr(positions),
+                              float(cfg.base), 0 if cfg.style == "interleaved" else 1, _stream(ref.device)))
+    return qo, ko
+
+
+def apply_rope(x: torch.Tensor, positions: Optional[torch.Tensor] = None, cfg: Optional[RopeConfig] = None,
+               inplace: bool = False) -> torch.Tensor:
+    """apply_rope (rope.hpp:63-79) for every head of x [n, H, d] bf16."""
+    return apply_rope_qk(x, None, positions, cfg, inplace)[0]
+
 
 def indexer_forward(k: torch.Tensor, v: torch.Tensor, p: IndexerParams, mapping: str = "reverse",
                     want_logits: bool = False):

@@ -13,6 +13,7 @@
 #include "aggregate.h"
 #include "attn.h"
 #include "indexer.h"
+#include "rope.h"
 #include "select.h"
 #include "vsp_error.h"
 
@@ -228,6 +229,30 @@ int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_
     recall_kernel<<<hq, 512, 0, as_stream(stream)>>>(lse_sparse, lse_dense, n, recall_per_head);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_recall_from_lse");
+}
+
+// ------------------------------------------------------------------ RoPE feed
+int vsp_apply_rope(vsp_ctx* ctx, const void* q_in, const void* k_in, void* q_out, void* k_out, int n, int hq,
+                   int hkv, int d, const int64_t* positions, double base, int style, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    // RopeConfig's own checks first (rope.hpp:19-26), then this kernel's layout limits
+    if (d < 2 || d % 2 != 0) return set_err(VSP_EINVAL, "rope head_dim must be even and >= 2");
+    if (!(base > 0.0)) return set_err(VSP_EINVAL, "rope base must be positive");
+    if (style != VSP_ROPE_INTERLEAVED && style != VSP_ROPE_HALF_SPLIT)
+        return set_err(VSP_EINVAL, "vsp_apply_rope: bad style");
+    const int unit = style == VSP_ROPE_HALF_SPLIT ? 16 : 8;
+    if (d % unit != 0 || d > 256)
+        return set_err(VSP_EINVAL, "vsp_apply_rope: head dim must be a multiple of " + std::to_string(unit) +
+                                       " and <= 256");
+    if (n < 0 || hq < 0 || hkv < 0) return set_err(VSP_EINVAL, "vsp_apply_rope: bad shape");
+    if ((hq > 0 && (!q_in || !q_out)) || (hkv > 0 && (!k_in || !k_out)))
+        return set_err(VSP_EINVAL, "vsp_apply_rope: null tensor");
+    if (n == 0 || (hq == 0 && hkv == 0)) return VSP_OK;
+    vsp_rope::Args a{static_cast<const __nv_bfloat16*>(q_in), static_cast<const __nv_bfloat16*>(k_in),
+                     static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_out), positions, n, hq, hkv, d,
+                     base, style == VSP_ROPE_HALF_SPLIT};
+    cudaError_t e = vsp_rope::launch(a, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_apply_rope");
 }
 
 // ------------------------------------------------------------------ indexer

@@ -121,6 +121,15 @@ def main():
         ag.append(dict(q=q.tolist(), k=k.tolist(), block=block, vertical=vert.tolist(), slash=sl.tolist()))
     C["aggregate_streaming"] = ag
 
+    # apply_rope (rope.hpp:63-79): row-index positions, explicit long-context positions, bases
+    rp = []
+    for n, d, base, positions in ((6, 8, 10000.0, None), (7, 128, 10000.0, [0, 1, 4095, 32768, 65537, 100000, 131071]),
+                                  (5, 128, 500000.0, [131071, 3, 77777, 12, 0]), (3, 2, 10000.0, None)):
+        x = rng.standard_normal((n, d))
+        rp.append(dict(x=x.tolist(), positions=positions, base=base,
+                       out=ref.apply_rope(x, positions, base).tolist()))
+    C["apply_rope"] = rp
+
     path = os.path.join(HERE, "reference_vectors.json")
     with open(path, "w") as f:
         json.dump(out, f)
