@@ -21,9 +21,14 @@ def sass_top(rep, k=12):
     data = rows[2:]
     iw = hdr.index("Warp Stall Sampling (All Samples)")
     isrc = hdr.index("Source")
-    tot = sum(float(r[iw] or 0) for r in data) or 1.0
-    top = sorted(data, key=lambda r: -float(r[iw] or 0))[:k]
-    return [(float(r[iw]) / tot * 100, r[isrc].strip()) for r in top]
+    def num(r):
+        try:
+            return float(r[iw] or 0)
+        except (ValueError, IndexError):  # repeated header rows of multi-kernel reports
+            return 0.0
+    tot = sum(num(r) for r in data) or 1.0
+    top = sorted(data, key=lambda r: -num(r))[:k]
+    return [(num(r) / tot * 100, r[isrc].strip()) for r in top]
 
 
 def f(d, key, scale=1.0, fmt="{:.2f}"):
