@@ -5,19 +5,29 @@
 //   pass 1: LSE_i of every row (online softmax; vsaggregate.hpp:83-103) — K4's LSE output
 //   pass 2: w = exp(s_ij - LSE_i); vertical[j] += w; slash[i - j] += w (:109-124)
 //   normalize by n (:27-33), then group Mean (or Sum).
-// The n x n weights never exist: each 128 x 128 tile of P lives in shared memory for the
-// two reductions, and both reductions run on the TENSOR cores:
-//   column sums   D_col[j] += sum_i P[i][j]      = (P^T . 1)   (A = P^T, MN-major smem view)
-//   diagonal sums D_dia[c] += sum_i P'[i][c]     = (P'^T . 1)  with the skewed copy
-//                 P'[r][c] = P[r][r - c + 128], so column c of P' is diagonal o = 128t + c - 128
-//                 (t = query block - key block); the two 128-wide halves of P' feed the
-//                 accumulators of offset blocks t-1 and t, which complete in order.
-// CTA = one 128-key block (K tile resident), one KV group, a chunk of query blocks; it walks
-// (query block, Q head) items in order. Per item: S = Q K^T (tcgen05, TMEM), softmax warps
-// turn S into P (bf16) in two smem layouts, the MMA warp issues the three reduction MMAs
-// (M=128, N=16, K=128) into TMEM accumulators. Completed offset blocks and, at the end, the
-// column sums are added to the [hkv, n] fp32 outputs (global atomics across CTAs).
+// The n x n weights never exist.
+//
+// Pass 2 works on TRANSPOSED tiles: S^T = K_J Q_I^T (tcgen05, M = 128 keys, N = 128 query
+// rows, TMEM), so the softmax thread that owns TMEM lane c holds key j = 128J + c against
+// all 128 query rows of the tile:
+//   * vertical[j] = sum over rows of P^T[c][.] — a running fp32 register sum per thread, for
+//     every query block and head the CTA visits; one atomic per key at the end.
+//   * slash: offset o = i - j = 128(t-1) + cc' - (c & 7) with t = I - J and the COARSE
+//     column cc' = r + 128 - 8*floor(c/8). The thread writes its 128 weights as bf16 to row c
+//     of a [128 x 256] shared buffer starting at cc' (a 16-byte aligned chunk: 16 plain
+//     vector stores, no per-element skew), and the tensor core reduces the columns against a
+//     SELECTOR B[c][f] = (f == c & 7) (M=128 coarse columns, N=16, K=128 keys): D[x][f] =
+//     sum over keys with c & 7 == f. The true diagonal is slash[o] = sum_f E[o + f][f], with
+//     E the coarse accumulator; that 8-term combination runs once per CTA in the flush.
+// CTA = one 128-key block J (K tile resident), one KV group, a chunk of up to 14 query
+// blocks, all Q heads of the group (two softmax warpgroups take alternate heads and
+// ping-pong against the tensor core). Every coarse offset block the CTA touches keeps its own
+// TMEM accumulator (15 x 16 columns), so nothing is flushed until the CTA ends. CTAs are
+// ordered (query chunk, group, key block) so concurrently resident CTAs stream the same Q
+// tiles from L2.
 #include <cuda_bf16.h>
+
+#include <algorithm>
 
 #include "aggregate.h"
 #include "attn.h"
@@ -31,8 +41,10 @@ namespace vsp_aggregate {
 constexpr int kBlock = 128;
 constexpr int kTile = kBlock * 128 * 2;  // 32 KB bf16 tile
 constexpr int kHalf = kTile / 2;
-constexpr int kChunk = 16;               // query blocks per CTA
-constexpr int kThreads = 256;            // warp0 TMA, warp1 MMA, warps 4-7 softmax
+constexpr int kChunk = 14;               // query blocks per CTA (15 coarse blocks in TMEM)
+constexpr int kQStages = 3;
+constexpr int kThreads = 384;            // warp0 TMA, warp1 MMA, warps 4-11 two softmax groups
+constexpr int kAccCols = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct __align__(64) Params {
@@ -40,85 +52,101 @@ struct __align__(64) Params {
     const float* lse;  // [hq, n]
     float* a_v;        // [hkv, n]
     float* a_s;
-    int n, hq, hkv, num_qb, chunks_per_kb;
+    int n, hq, hkv, num_qb, num_qc;
     float scale;       // 1/sqrt(d)
     float out_scale;   // (normalized ? 1/n : 1) * (mean ? 1/group : 1)
 };
 
 struct Smem {
     uint64_t bar_k;
-    uint64_t q_full[2], q_empty[2];
+    uint64_t q_full[kQStages], q_empty[kQStages], l_empty[kQStages];
     uint64_t s_full[2], s_free[2];
-    uint64_t p_full, p_free;
-    uint64_t d_done, flush_done;
+    uint64_t p_full, p_free, all_done;
     uint32_t tmem_base;
 };
 
-// smem: K 32K | Q ring 2 x 32K | P row-major 32K | P skew 64K | ones 4K
+// smem: K 32K | Q ring 3 x 32K | P coarse 64K (4 x [128 x 64] SW128 blocks) | selector 4K |
+//       lse ring 3 x 512 B | vertical exchange 512 B | flush staging 2 x 136 x 8 floats
 constexpr int kOffK = 0;
 constexpr int kOffQ = kTile;
-constexpr int kOffP = 3 * kTile;
-constexpr int kOffPS = 4 * kTile;
-constexpr int kOffOnes = 6 * kTile;
-constexpr int kSmemBytes = 6 * kTile + 4096 + 1024;
+constexpr int kOffP = kOffQ + kQStages * kTile;
+constexpr int kOffSel = kOffP + 2 * kTile;
+constexpr int kOffLse = kOffSel + 4096;
+constexpr int kOffVx = kOffLse + kQStages * 512;
+constexpr int kOffStage = kOffVx + 512;
+constexpr int kStageFloats = 136 * 8;
+constexpr int kSmemBytes = kOffStage + 2 * kStageFloats * 4 + 1024;
+static_assert(kSmemBytes <= 227 * 1024, "aggregate smem");
 
-// byte offset of element (row r, col c) in a [128 x 64]-bf16 SW128 K-major/MN-major block
-VSP_DEVICE uint32_t sw128_off(int r, int c) {
-    const int chunk = (c * 2) >> 4;
-    return static_cast<uint32_t>(r * 128 + (((chunk ^ (r & 7)) << 4) | ((c * 2) & 15)));
+// (query chunk, group, key block) of this CTA; chunk qc covers query blocks
+// [kChunk*qc, kChunk*qc + kChunk) and pairs with key blocks J < min(num_qb, kChunk*(qc+1)).
+VSP_DEVICE void decode_cta(const Params& p, int& qc, int& g, int& jb) {
+    int b = blockIdx.x;
+    for (qc = 0; qc < p.num_qc; ++qc) {
+        const int per = min(p.num_qb, kChunk * (qc + 1)) * p.hkv;
+        if (b < per) break;
+        b -= per;
+    }
+    const int nj = min(p.num_qb, kChunk * (qc + 1));
+    g = b / nj;
+    jb = b % nj;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // offset from smem_raw (not a cast through an integer) so the compiler keeps the
-    // shared state space and emits LDS/STS rather than generic LD/ST
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ Smem sm;
     const int grp = p.hq / p.hkv;
-
-    // block -> (key block jb, group g, chunk): heavy key blocks (small jb) first
-    const int per_g = p.num_qb * p.chunks_per_kb;
-    const int g = blockIdx.x % p.hkv;
-    const int rest = blockIdx.x / p.hkv;
-    const int jb = rest / p.chunks_per_kb;
-    const int chunk = rest % p.chunks_per_kb;
-    (void)per_g;
-    const int t_first = chunk * kChunk;                   // t = ib - jb
-    const int t_end = min(t_first + kChunk, p.num_qb - jb);
-    const uint32_t warp = warp_id(), lane = lane_id();
-    if (t_first >= t_end) return;
-    const int num_items = (t_end - t_first) * grp;
+    int qc, g, jb;
+    decode_cta(p, qc, g, jb);
+    const int i_first = max(jb, kChunk * qc);
+    const int i_end = min(p.num_qb, kChunk * (qc + 1));
+    const int t0 = i_first - jb;              // first t = I - J of this CTA
+    const int nblk = i_end - i_first;         // query blocks (>= 1)
+    const int num_items = nblk * grp;
     const int j0 = jb * kBlock;
+    const uint32_t warp = warp_id(), lane = lane_id();
+    float* lse_ring = reinterpret_cast<float*>(base + kOffLse);
 
     if (warp == 0 && lane == 0) {
         mbar_init(&sm.bar_k, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kQStages; ++s) {
             mbar_init(&sm.q_full[s], 1);
             mbar_init(&sm.q_empty[s], 1);
-            mbar_init(&sm.s_full[s], 1);
-            mbar_init(&sm.s_free[s], 4);
+            mbar_init(&sm.l_empty[s], 4);
+        }
+        for (int w = 0; w < 2; ++w) {
+            mbar_init(&sm.s_full[w], 1);
+            mbar_init(&sm.s_free[w], 4);
         }
         mbar_init(&sm.p_full, 4);
         mbar_init(&sm.p_free, 1);
-        mbar_init(&sm.d_done, 1);
-        mbar_init(&sm.flush_done, 4);
+        mbar_init(&sm.all_done, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
-    // ones operand for the reduction MMAs
+    // zero the coarse P buffer once (each row's band is fixed, the rest stays zero) and
+    // build the selector B[c][f] = (f == c & 7): K-major [16 x 128], two SW128 K-halves
     {
-        uint32_t* ones = reinterpret_cast<uint32_t*>(base + kOffOnes);
-        for (int i = threadIdx.x; i < 1024; i += blockDim.x) ones[i] = 0x3f803f80u;  // bf16 1.0 x2
+        uint4* pz = reinterpret_cast<uint4*>(base + kOffP);
+        for (int i = threadIdx.x; i < 2 * kTile / 16; i += kThreads) pz[i] = make_uint4(0, 0, 0, 0);
+        uint16_t* sel = reinterpret_cast<uint16_t*>(base + kOffSel);
+        for (int i = threadIdx.x; i < 16 * 128; i += kThreads) {
+            const int f = i >> 7, c = i & 127;
+            const int cl = c & 63;
+            const uint32_t off = (c >> 6) * 2048 + f * 128 + ((((cl >> 3) ^ (f & 7)) << 4) | ((cl & 7) << 1));
+            sel[off >> 1] = (f < 8 && f == (c & 7)) ? 0x3f80u : 0u;  // bf16 1.0
+        }
         fence_proxy_async_smem();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    const uint32_t t_col = tmem + 256;             // column sums   [128 x 16]
-    const uint32_t t_dia[2] = {tmem + 288, tmem + 320};
+    const uint32_t t_acc = tmem + 256;  // coarse accumulators: slot s at t_acc + 16 s
 
     if (warp == 0) {
+        // =========================== producer: K once; per item the Q tile (TMA) + LSE row
         if (elect_one()) {
             tma_prefetch_desc(&p.map_q);
             tma_prefetch_desc(&p.map_k);
@@ -127,173 +155,218 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                 tma_load_3d(base + kOffK + hf * kHalf, &p.map_k, &sm.bar_k, hf * 64, g, j0);
         }
         __syncwarp();
-        for (int it = 0; it < num_items; ++it) {
-            const int t = t_first + it / grp;
-            const int h = g * grp + it % grp;
-            const int s = it & 1;
-            if (it >= 2) mbar_wait(&sm.q_empty[s], ((it >> 1) & 1) ^ 1);
+        for (int k = 0; k < num_items; ++k) {
+            const int ib = i_first + k / grp;
+            const int h = g * grp + k % grp;
+            const int s = k % kQStages;
+            if (k >= kQStages) {
+                const uint32_t ph = ((k / kQStages) - 1) & 1;
+                mbar_wait(&sm.q_empty[s], ph);
+                mbar_wait(&sm.l_empty[s], ph);
+            }
+            // LSE of the tile's rows in log2 units; rows past n get +inf (weight exactly 0)
+            float4 l4;
+            const int i = ib * kBlock + 4 * lane;
+            const float* src = p.lse + static_cast<size_t>(h) * p.n;
+            l4.x = i + 0 < p.n ? __ldg(src + i + 0) * kLog2e : INFINITY;
+            l4.y = i + 1 < p.n ? __ldg(src + i + 1) * kLog2e : INFINITY;
+            l4.z = i + 2 < p.n ? __ldg(src + i + 2) * kLog2e : INFINITY;
+            l4.w = i + 3 < p.n ? __ldg(src + i + 3) * kLog2e : INFINITY;
+            reinterpret_cast<float4*>(lse_ring + s * kBlock)[lane] = l4;
+            __syncwarp();
             if (elect_one()) {
                 mbar_arrive_expect_tx(&sm.q_full[s], kTile);
                 for (int hf = 0; hf < 2; ++hf)
                     tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
-                                (jb + t) * kBlock);
+                                ib * kBlock);
             }
             __syncwarp();
         }
     } else if (warp == 1) {
-        // MMA issuer: warp-uniform loop, one elected lane issues each batch
-        const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
-        const uint32_t idesc_red = umma_idesc_bf16(128, 16, true, false);
+        // =========================== MMA issuer (warp-uniform loop, elected lane issues)
+        const uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+        const uint32_t idesc_red = umma_idesc_bf16(128, kAccCols, true, false);
         const uint64_t k_desc0 = umma_desc_sw128(smem_u32(base + kOffK), 16, 1024);
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(base + kOffQ), 16, 1024);
-        const uint64_t ones_desc0 = umma_desc_sw128(smem_u32(base + kOffOnes), 16, 1024);
+        const uint64_t sel_desc0 = umma_desc_sw128(smem_u32(base + kOffSel), 16, 1024);
         const uint32_t p_addr = smem_u32(base + kOffP);
-        const uint32_t ps_addr = smem_u32(base + kOffPS);
-        auto issue_s = [&](int it) {
-            const int s = it & 1;
-            mbar_wait(&sm.q_full[s], (it >> 1) & 1);
-            if (it >= 2) mbar_wait(&sm.s_free[s], ((it >> 1) & 1) ^ 1);
+        auto issue_s = [&](int k) {  // S^T_w = K Q^T into TMEM columns [128 w, 128 w + 128)
+            const int s = k % kQStages;
+            const int w = k & 1;
+            mbar_wait(&sm.q_full[s], (k / kQStages) & 1);
+            if (k >= 2) mbar_wait(&sm.s_free[w], ((k >> 1) - 1) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint64_t off = static_cast<uint64_t>(((k >> 2) * kHalf + (k & 3) * 32) >> 4);
-                    umma_ss(tmem + s * 128, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off, k_desc0 + off,
-                            idesc_qk, k > 0 ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t off = static_cast<uint64_t>(((kk >> 2) * kHalf + (kk & 3) * 32) >> 4);
+                    umma_ss(tmem + w * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
+                            idesc_s, kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&sm.s_full[s]);
+                umma_commit(&sm.s_full[w]);
                 umma_commit(&sm.q_empty[s]);
             }
             __syncwarp();
         };
-        // reduction: D[tm] (+)= A^T . 1, A = [128 rows x 128 cols] bf16 (two 16 KB halves)
-        auto issue_red = [&](uint32_t d_t, uint32_t a_base, bool acc) {
-            const uint64_t a0 = umma_desc_sw128(a_base, kHalf, 1024);
+        // D[slot] (+)= Pc[:, half]^T . Sel   (M = 128 coarse columns, K = 128 keys)
+        auto issue_red = [&](int slot, int half, bool acc) {
+            const uint64_t a0 = umma_desc_sw128(p_addr + half * 2 * kHalf, kHalf, 1024);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                umma_ss(d_t, a0 + static_cast<uint64_t>((k * 2048) >> 4),
-                        ones_desc0 + static_cast<uint64_t>(((k >> 2) * 2048 + (k & 3) * 32) >> 4), idesc_red,
-                        (acc || k > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 8; ++kk)
+                umma_ss(t_acc + slot * kAccCols, a0 + static_cast<uint64_t>((kk * 2048) >> 4),
+                        sel_desc0 + static_cast<uint64_t>(((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc_red,
+                        (acc || kk > 0) ? 1u : 0u);
         };
         mbar_wait(&sm.bar_k, 0);
         issue_s(0);
         if (num_items > 1) issue_s(1);
-        for (int it = 0; it < num_items; ++it) {
-            const int tl = it / grp;            // local t index
-            const int t = t_first + tl;
-            const int hi = it % grp;
-            mbar_wait(&sm.p_full, it & 1);
+        for (int k = 0; k < num_items; ++k) {
+            const int tl = k / grp, hh = k % grp;
+            const int t = t0 + tl;
+            mbar_wait(&sm.p_full, k & 1);
             tc_fence_after();
             if (elect_one()) {
-                issue_red(t_col, p_addr, it > 0);
-                if (t >= 1) issue_red(t_dia[(t - 1) & 1], ps_addr, !(tl == 0 && hi == 0));
-            }
-            __syncwarp();
-            if (hi == 0 && tl >= 1) {
-                // the accumulator of block t last held block t-2, flushed after the
-                // previous query block (flush arrival tl-1)
-                mbar_wait(&sm.flush_done, (tl - 1) & 1);
-                tc_fence_after();
-            }
-            if (elect_one()) {
-                issue_red(t_dia[t & 1], ps_addr + 2 * kHalf, hi != 0);
+                // lower half -> coarse block t-1 (slot tl), upper half -> block t (slot tl+1)
+                if (t >= 1) issue_red(tl, 0, tl > 0 || hh > 0);
+                issue_red(tl + 1, 1, hh > 0);
                 umma_commit(&sm.p_free);
-                if (hi == grp - 1) umma_commit(&sm.d_done);
+                if (k == num_items - 1) umma_commit(&sm.all_done);
             }
             __syncwarp();
-            if (it + 2 < num_items) issue_s(it + 2);
+            if (k + 2 < num_items) issue_s(k + 2);
         }
     } else if (warp >= 4) {
+        // =========================== softmax groups: WG w takes items k with k & 1 == w
+        const int w = (warp - 4) >> 2;
         const int quarter = warp & 3;
-        const int r = quarter * 32 + lane;
+        const int c = quarter * 32 + lane;  // key row (TMEM lane) within block J
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.scale * kLog2e;
-        uint8_t* sp = base + kOffP;
-        uint8_t* sps = base + kOffPS;
-        for (int it = 0; it < num_items; ++it) {
-            const int tl = it / grp;
-            const int t = t_first + tl;
-            const int h = g * grp + it % grp;
-            const int i = (jb + t) * kBlock + r;
-            const int s = it & 1;
-            const float lse2 = i < p.n ? __ldg(p.lse + static_cast<size_t>(h) * p.n + i) * kLog2e : INFINITY;
-            mbar_wait(&sm.s_full[s], (it >> 1) & 1);
+        // this thread's row of the coarse buffer starts at chunk 16 - c/8 (column 128 - 8 floor(c/8))
+        uint8_t* prow = base + kOffP + c * 128;
+        const int a0 = 16 - (c >> 3);
+        float2 vacc = make_float2(0.f, 0.f);
+        for (int k = w; k < num_items; k += 2) {
+            const int tl = k / grp;
+            const int t = t0 + tl;
+            const int s = k % kQStages;
+            const bool plain = t > 0 && (i_first + tl + 1) * kBlock <= p.n;  // no causal mask, full rows
+            mbar_wait(&sm.q_full[s], (k / kQStages) & 1);  // LSE row of this item is in the ring
+            mbar_wait(&sm.s_full[w], (k >> 1) & 1);
             tc_fence_after();
-            float x[128];
+            const float4* l4 = reinterpret_cast<const float4*>(lse_ring + s * kBlock);
+            uint32_t pk[64];
+            uint32_t u[2][32];
+            tmem_ld32(tmem + lane_base + w * 128, u[0]);
+            tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t u[32];
-                tmem_ld32(tmem + lane_base + s * 128 + c * 32, u);
-                tmem_wait_ld();
+            for (int cq = 0; cq < 4; ++cq) {
+                if (cq < 3) tmem_ld32(tmem + lane_base + w * 128 + (cq + 1) * 32, u[(cq + 1) & 1]);
+                const uint32_t* x = u[cq & 1];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) x[c * 32 + e] = __uint_as_float(u[e]);
+                for (int e4 = 0; e4 < 8; ++e4) {
+                    const float4 l = l4[cq * 8 + e4];
+                    const int r = cq * 32 + e4 * 4;
+                    float2 y0 = ffma2(make_float2(__uint_as_float(x[4 * e4]), __uint_as_float(x[4 * e4 + 1])),
+                                      make_float2(sl2, sl2), make_float2(-l.x, -l.y));
+                    float2 y1 = ffma2(make_float2(__uint_as_float(x[4 * e4 + 2]), __uint_as_float(x[4 * e4 + 3])),
+                                      make_float2(sl2, sl2), make_float2(-l.z, -l.w));
+                    float2 e0, e1;
+                    if (plain) {
+                        // 3 pairs in 8 on the FMA pipe, the rest on MUFU (the K4 balance)
+                        if ((0x54u >> e4) & 1u) {
+                            e0 = exp2_poly2(y0);
+                            e1 = exp2_poly2(y1);
+                        } else {
+                            e0.x = ex2_approx(y0.x);
+                            e0.y = ex2_approx(y0.y);
+                            e1.x = ex2_approx(y1.x);
+                            e1.y = ex2_approx(y1.y);
+                        }
+                    } else {
+                        // diagonal tile (t == 0: keep r >= c) or ragged last block (lse = +inf
+                        // there): MUFU only, so masked weights are exactly 0
+                        if (t == 0) {
+                            if (r + 0 < c) y0.x = -INFINITY;
+                            if (r + 1 < c) y0.y = -INFINITY;
+                            if (r + 2 < c) y1.x = -INFINITY;
+                            if (r + 3 < c) y1.y = -INFINITY;
+                        }
+                        e0.x = ex2_approx(y0.x);
+                        e0.y = ex2_approx(y0.y);
+                        e1.x = ex2_approx(y1.x);
+                        e1.y = ex2_approx(y1.y);
+                    }
+                    vacc = fadd2(vacc, fadd2(e0, e1));
+                    pk[r / 2] = pack_bf16x2(e0.x, e0.y);
+                    pk[r / 2 + 1] = pack_bf16x2(e1.x, e1.y);
+                }
+                if (cq < 3) tmem_wait_ld();
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.s_free[s]);
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                const bool ok = (t > 0 || c <= r) && i < p.n;  // causal on the diagonal tile
-                x[c] = ok ? ex2_approx(fmaf(x[c], sl2, -lse2)) : 0.f;
+            if (lane == 0) {
+                mbar_arrive(&sm.s_free[w]);
+                mbar_arrive(&sm.l_empty[s]);
             }
-            if (it > 0) mbar_wait(&sm.p_free, (it - 1) & 1);
-            // row-major P (two 64-column SW128 halves)
+            if (k >= 1) mbar_wait(&sm.p_free, (k - 1) & 1);
+            // 16 aligned 16-byte chunks: chunk q of the row -> coarse column 128 - 8 floor(c/8) + 8q
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf)
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const int c0 = hf * 64 + ch * 8;
-                    uint4 v;
-                    v.x = pack_bf16x2(x[c0 + 0], x[c0 + 1]);
-                    v.y = pack_bf16x2(x[c0 + 2], x[c0 + 3]);
-                    v.z = pack_bf16x2(x[c0 + 4], x[c0 + 5]);
-                    v.w = pack_bf16x2(x[c0 + 6], x[c0 + 7]);
-                    *reinterpret_cast<uint4*>(sp + hf * kHalf + r * 128 + (((ch ^ (r & 7)) << 4))) = v;
-                }
-            // skewed P': zero the row, then P'[r][r - c + 128] = P[r][c]
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
-                    *reinterpret_cast<uint4*>(sps + q4 * kHalf + r * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
-            __syncwarp();
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                const int cc = r - c + 128;  // 1..255
-                __nv_bfloat16 b = __float2bfloat16_rn(x[c]);
-                *reinterpret_cast<__nv_bfloat16*>(sps + (cc >> 6) * kHalf + sw128_off(r, cc & 63)) = b;
+            for (int q = 0; q < 16; ++q) {
+                const int a = a0 + q;  // absolute 8-column chunk, 1..31
+                *reinterpret_cast<uint4*>(prow + (a >> 3) * kHalf + (((a & 7) ^ (c & 7)) << 4)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full);
+        }
 
-            if (it % grp == grp - 1) {
-                // all heads of this query block are in: offset block t-1 is complete
-                mbar_wait(&sm.d_done, tl & 1);
-                tc_fence_after();
-                if (t >= 1) {
-                    uint32_t u[32];
-                    // only column 0 is needed (all 16 columns hold the same sums)
-                    tmem_ld32(t_dia[(t - 1) & 1] + lane_base, u);
-                    tmem_wait_ld();
-                    const int o = (t - 1) * kBlock + r;
-                    if (o < p.n) atomicAdd(p.a_s + static_cast<size_t>(g) * p.n + o, __uint_as_float(u[0]) * p.out_scale);
-                }
-                if (t == t_end - 1) {
-                    uint32_t u[32];
-                    tmem_ld32(t_dia[t & 1] + lane_base, u);
-                    tmem_wait_ld();
-                    const int o = t * kBlock + r;
-                    if (o < p.n) atomicAdd(p.a_s + static_cast<size_t>(g) * p.n + o, __uint_as_float(u[0]) * p.out_scale);
-                    tmem_ld32(t_col + lane_base, u);
-                    tmem_wait_ld();
-                    const int j = j0 + r;
-                    if (j < p.n) atomicAdd(p.a_v + static_cast<size_t>(g) * p.n + j, __uint_as_float(u[0]) * p.out_scale);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.flush_done);
+        // ---- flush (once per CTA)
+        float* vx = reinterpret_cast<float*>(base + kOffVx);
+        if (w == 1) vx[c] = vacc.x + vacc.y;
+        mbar_wait(&sm.all_done, 0);
+        tc_fence_after();
+        named_bar_sync(1, 256);
+        if (w == 0) {
+            const int j = j0 + c;
+            if (j < p.n && num_items > 0)
+                atomicAdd(p.a_v + static_cast<size_t>(g) * p.n + j, (vacc.x + vacc.y + vx[c]) * p.out_scale);
+        }
+        // slash block b = sum_f E[128 b + x + f][f]; E block b lives in slot b - t0 + 1 (slot 0
+        // only when t0 >= 1). WG w flushes blocks with (b - b_lo) % 2 == w.
+        float* stage = reinterpret_cast<float*>(base + kOffStage) + w * kStageFloats;
+        const int nslots = nblk + 1;
+        const int b_lo = max(0, t0 - 2);
+        const int b_hi = t0 + nblk - 1;
+        for (int b = b_lo + w; b <= b_hi; b += 2) {
+            const int s0 = b - t0 + 1;
+            const bool v0 = s0 >= 0 && s0 < nslots && !(s0 == 0 && t0 == 0);
+            const bool v1 = s0 + 1 >= 0 && s0 + 1 < nslots && !(s0 + 1 == 0 && t0 == 0);
+            uint32_t e[16];
+            if (v0) {
+                tmem_ld16(t_acc + s0 * kAccCols + lane_base, e);
+                tmem_wait_ld();
             }
+#pragma unroll
+            for (int f = 0; f < 8; ++f) stage[c * 8 + f] = v0 ? __uint_as_float(e[f]) : 0.f;
+            if (quarter == 0) {  // rows 128..135 of the window: first rows of block b+1
+                if (v1) {
+                    tmem_ld16(t_acc + (s0 + 1) * kAccCols + lane_base, e);
+                    tmem_wait_ld();
+                }
+                if (lane < 8) {
+#pragma unroll
+                    for (int f = 0; f < 8; ++f) stage[(128 + lane) * 8 + f] = v1 ? __uint_as_float(e[f]) : 0.f;
+                }
+            }
+            named_bar_sync(2 + w, 128);
+            float sum = 0.f;
+#pragma unroll
+            for (int f = 0; f < 8; ++f) sum += stage[(c + f) * 8 + f];
+            const int o = b * kBlock + c;
+            if (o < p.n && sum != 0.f) atomicAdd(p.a_s + static_cast<size_t>(g) * p.n + o, sum * p.out_scale);
+            named_bar_sync(2 + w, 128);
         }
     }
     tc_fence_before();
@@ -353,7 +426,7 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.hq = a.hq;
     p.hkv = a.hkv;
     p.num_qb = (a.n + kBlock - 1) / kBlock;
-    p.chunks_per_kb = (p.num_qb + kChunk - 1) / kChunk;
+    p.num_qc = (p.num_qb + kChunk - 1) / kChunk;
     p.scale = a.scale;
     p.out_scale = (a.normalized ? 1.0f / static_cast<float>(a.n) : 1.0f) *
                   (a.mean ? 1.0f / static_cast<float>(a.hq / a.hkv) : 1.0f);
@@ -365,8 +438,9 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
         cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr = true;
     }
-    dim3 grid(p.num_qb * p.chunks_per_kb * a.hkv);
-    aggregate_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    long long ctas = 0;
+    for (int qc = 0; qc < p.num_qc; ++qc) ctas += static_cast<long long>(std::min(p.num_qb, kChunk * (qc + 1))) * a.hkv;
+    aggregate_kernel<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, stream>>>(p);
     const int grp = a.hq / a.hkv;
     const double total = (a.normalized ? 1.0 : static_cast<double>(a.n)) * (a.mean ? 1.0 : static_cast<double>(grp));
     renormalize_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(a.a_v, a.a_s, a.n, total);
