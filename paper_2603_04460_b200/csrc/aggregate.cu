@@ -16,13 +16,13 @@
 //     column cc' = r + 128 - 8*floor(c/8). The thread writes its 128 weights as bf16 to row c
 //     of a [128 x 256] shared buffer starting at cc' (a 16-byte aligned chunk: 16 plain
 //     vector stores, no per-element skew), and the tensor core reduces the columns against a
-//     SELECTOR B[c][f] = (f == c & 7) (M=128 coarse columns, N=16, K=128 keys): D[x][f] =
+//     SELECTOR B[c][f] = (f == c & 7) (M=128 coarse columns, N=8, K=128 keys): D[x][f] =
 //     sum over keys with c & 7 == f. The true diagonal is slash[o] = sum_f E[o + f][f], with
 //     E the coarse accumulator; that 8-term combination runs once per CTA in the flush.
 // CTA = one 128-key block J (K tile resident), one KV group, a chunk of up to 14 query
 // blocks, all Q heads of the group (two softmax warpgroups take alternate heads and
 // ping-pong against the tensor core). Every coarse offset block the CTA touches keeps its own
-// TMEM accumulator (15 x 16 columns), so nothing is flushed until the CTA ends. CTAs are
+// TMEM accumulator (15 x 8 columns), so nothing is flushed until the CTA ends. CTAs are
 // ordered (query chunk, group, key block) so concurrently resident CTAs stream the same Q
 // tiles from L2.
 #include <cuda_bf16.h>
@@ -43,8 +43,10 @@ constexpr int kTile = kBlock * 128 * 2;  // 32 KB bf16 tile
 constexpr int kHalf = kTile / 2;
 constexpr int kChunk = 14;               // query blocks per CTA (15 coarse blocks in TMEM)
 constexpr int kQStages = 3;
+constexpr int kLStages = 6;              // LSE rows: released late (after the exps), so deeper
 constexpr int kThreads = 384;            // warp0 TMA, warp1 MMA, warps 4-11 two softmax groups
-constexpr int kAccCols = 16;
+constexpr int kAccCols = 8;              // N = 8 selector columns per coarse accumulator
+constexpr int kSBufs = 3;                // S^T TMEM buffers (items rotate through them)
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct __align__(64) Params {
@@ -59,20 +61,21 @@ struct __align__(64) Params {
 
 struct Smem {
     uint64_t bar_k;
-    uint64_t q_full[kQStages], q_empty[kQStages], l_empty[kQStages];
-    uint64_t s_full[2], s_free[2];
+    uint64_t q_full[kQStages], q_empty[kQStages];
+    uint64_t l_full[kLStages], l_empty[kLStages];
+    uint64_t s_full[kSBufs], s_free[kSBufs];
     uint64_t p_full, p_free, all_done;
     uint32_t tmem_base;
 };
 
 // smem: K 32K | Q ring 3 x 32K | P coarse 64K (4 x [128 x 64] SW128 blocks) | selector 4K |
-//       lse ring 3 x 512 B | vertical exchange 512 B | flush staging 2 x 136 x 8 floats
+//       lse ring 6 x 512 B | vertical exchange 512 B | flush staging 2 x 136 x 8 floats
 constexpr int kOffK = 0;
 constexpr int kOffQ = kTile;
 constexpr int kOffP = kOffQ + kQStages * kTile;
 constexpr int kOffSel = kOffP + 2 * kTile;
 constexpr int kOffLse = kOffSel + 4096;
-constexpr int kOffVx = kOffLse + kQStages * 512;
+constexpr int kOffVx = kOffLse + kLStages * 512;
 constexpr int kOffStage = kOffVx + 512;
 constexpr int kStageFloats = 136 * 8;
 constexpr int kSmemBytes = kOffStage + 2 * kStageFloats * 4 + 1024;
@@ -113,11 +116,14 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&sm.q_full[s], 1);
             mbar_init(&sm.q_empty[s], 1);
+        }
+        for (int s = 0; s < kLStages; ++s) {
+            mbar_init(&sm.l_full[s], 1);
             mbar_init(&sm.l_empty[s], 4);
         }
-        for (int w = 0; w < 2; ++w) {
-            mbar_init(&sm.s_full[w], 1);
-            mbar_init(&sm.s_free[w], 4);
+        for (int b = 0; b < kSBufs; ++b) {
+            mbar_init(&sm.s_full[b], 1);
+            mbar_init(&sm.s_free[b], 4);
         }
         mbar_init(&sm.p_full, 4);
         mbar_init(&sm.p_free, 1);
@@ -143,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    const uint32_t t_acc = tmem + 256;  // coarse accumulators: slot s at t_acc + 16 s
+    // TMEM: S^T buffers [0, 384); coarse accumulators: slot s at columns 384 + 8 s (15 slots)
+    const uint32_t t_acc = tmem + kSBufs * 128;
 
     if (warp == 0) {
         // =========================== producer: K once; per item the Q tile (TMA) + LSE row
@@ -159,12 +166,17 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             const int ib = i_first + k / grp;
             const int h = g * grp + k % grp;
             const int s = k % kQStages;
-            if (k >= kQStages) {
-                const uint32_t ph = ((k / kQStages) - 1) & 1;
-                mbar_wait(&sm.q_empty[s], ph);
-                mbar_wait(&sm.l_empty[s], ph);
+            if (k >= kQStages) mbar_wait(&sm.q_empty[s], ((k / kQStages) - 1) & 1);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&sm.q_full[s], kTile);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
+                                ib * kBlock);
             }
+            __syncwarp();
             // LSE of the tile's rows in log2 units; rows past n get +inf (weight exactly 0)
+            const int ls = k % kLStages;
+            if (k >= kLStages) mbar_wait(&sm.l_empty[ls], ((k / kLStages) - 1) & 1);
             float4 l4;
             const int i = ib * kBlock + 4 * lane;
             const float* src = p.lse + static_cast<size_t>(h) * p.n;
@@ -172,14 +184,9 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             l4.y = i + 1 < p.n ? __ldg(src + i + 1) * kLog2e : INFINITY;
             l4.z = i + 2 < p.n ? __ldg(src + i + 2) * kLog2e : INFINITY;
             l4.w = i + 3 < p.n ? __ldg(src + i + 3) * kLog2e : INFINITY;
-            reinterpret_cast<float4*>(lse_ring + s * kBlock)[lane] = l4;
+            reinterpret_cast<float4*>(lse_ring + ls * kBlock)[lane] = l4;
             __syncwarp();
-            if (elect_one()) {
-                mbar_arrive_expect_tx(&sm.q_full[s], kTile);
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
-                                ib * kBlock);
-            }
+            if (elect_one()) mbar_arrive(&sm.l_full[ls]);
             __syncwarp();
         }
     } else if (warp == 1) {
@@ -190,20 +197,20 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(base + kOffQ), 16, 1024);
         const uint64_t sel_desc0 = umma_desc_sw128(smem_u32(base + kOffSel), 16, 1024);
         const uint32_t p_addr = smem_u32(base + kOffP);
-        auto issue_s = [&](int k) {  // S^T_w = K Q^T into TMEM columns [128 w, 128 w + 128)
+        auto issue_s = [&](int k) {  // S^T = K Q^T into TMEM buffer k % 3
             const int s = k % kQStages;
-            const int w = k & 1;
+            const int b = k % kSBufs;
             mbar_wait(&sm.q_full[s], (k / kQStages) & 1);
-            if (k >= 2) mbar_wait(&sm.s_free[w], ((k >> 1) - 1) & 1);
+            if (k >= kSBufs) mbar_wait(&sm.s_free[b], ((k / kSBufs) - 1) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t off = static_cast<uint64_t>(((kk >> 2) * kHalf + (kk & 3) * 32) >> 4);
-                    umma_ss(tmem + w * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
+                    umma_ss(tmem + b * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
                             idesc_s, kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&sm.s_full[w]);
+                umma_commit(&sm.s_full[b]);
                 umma_commit(&sm.q_empty[s]);
             }
             __syncwarp();
@@ -223,6 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         for (int k = 0; k < num_items; ++k) {
             const int tl = k / grp, hh = k % grp;
             const int t = t0 + tl;
+            // S(k+2) goes into the buffer item k-1 (the other warpgroup) has already read: the
+            // tensor core computes it while this item's exponentials run
+            if (k + 2 < num_items) issue_s(k + 2);
             mbar_wait(&sm.p_full, k & 1);
             tc_fence_after();
             if (elect_one()) {
@@ -233,7 +243,6 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                 if (k == num_items - 1) umma_commit(&sm.all_done);
             }
             __syncwarp();
-            if (k + 2 < num_items) issue_s(k + 2);
         }
     } else if (warp >= 4) {
         // =========================== softmax groups: WG w takes items k with k & 1 == w
@@ -249,19 +258,20 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         for (int k = w; k < num_items; k += 2) {
             const int tl = k / grp;
             const int t = t0 + tl;
-            const int s = k % kQStages;
+            const int ls = k % kLStages;
             const bool plain = t > 0 && (i_first + tl + 1) * kBlock <= p.n;  // no causal mask, full rows
-            mbar_wait(&sm.q_full[s], (k / kQStages) & 1);  // LSE row of this item is in the ring
-            mbar_wait(&sm.s_full[w], (k >> 1) & 1);
+            mbar_wait(&sm.l_full[ls], (k / kLStages) & 1);
+            const int sb = k % kSBufs;
+            mbar_wait(&sm.s_full[sb], (k / kSBufs) & 1);
             tc_fence_after();
-            const float4* l4 = reinterpret_cast<const float4*>(lse_ring + s * kBlock);
+            const float4* l4 = reinterpret_cast<const float4*>(lse_ring + ls * kBlock);
             uint32_t pk[64];
             uint32_t u[2][32];
-            tmem_ld32(tmem + lane_base + w * 128, u[0]);
+            tmem_ld32(tmem + lane_base + sb * 128, u[0]);
             tmem_wait_ld();
 #pragma unroll
             for (int cq = 0; cq < 4; ++cq) {
-                if (cq < 3) tmem_ld32(tmem + lane_base + w * 128 + (cq + 1) * 32, u[(cq + 1) & 1]);
+                if (cq < 3) tmem_ld32(tmem + lane_base + sb * 128 + (cq + 1) * 32, u[(cq + 1) & 1]);
                 const uint32_t* x = u[cq & 1];
 #pragma unroll
                 for (int e4 = 0; e4 < 8; ++e4) {
@@ -306,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&sm.s_free[w]);
-                mbar_arrive(&sm.l_empty[s]);
+                mbar_arrive(&sm.s_free[sb]);
+                mbar_arrive(&sm.l_empty[ls]);
             }
             if (k >= 1) mbar_wait(&sm.p_free, (k - 1) & 1);
             // 16 aligned 16-byte chunks: chunk q of the row -> coarse column 128 - 8 floor(c/8) + 8q
