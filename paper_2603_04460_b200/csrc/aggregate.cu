@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "aggregate.h"
 #include "attn.h"
@@ -225,14 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                         (acc || kk > 0) ? 1u : 0u);
         };
         mbar_wait(&sm.bar_k, 0);
-        issue_s(0);
-        if (num_items > 1) issue_s(1);
+        for (int k = 0; k < kSBufs && k < num_items; ++k) issue_s(k);
         for (int k = 0; k < num_items; ++k) {
             const int tl = k / grp, hh = k % grp;
             const int t = t0 + tl;
-            // S(k+2) goes into the buffer item k-1 (the other warpgroup) has already read: the
-            // tensor core computes it while this item's exponentials run
-            if (k + 2 < num_items) issue_s(k + 2);
+            // tcgen05.mma runs in issue order, so the reduction of item k goes in right after
+            // its P is written (the next warpgroup waits for p_free), and S(k+3) — needed only
+            // after the other warpgroup's next item — goes in behind it
             mbar_wait(&sm.p_full, k & 1);
             tc_fence_after();
             if (elect_one()) {
@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                 if (k == num_items - 1) umma_commit(&sm.all_done);
             }
             __syncwarp();
+            if (k + kSBufs < num_items) issue_s(k + kSBufs);
         }
     } else if (warp >= 4) {
         // =========================== softmax groups: WG w takes items k with k & 1 == w
@@ -265,68 +266,86 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             mbar_wait(&sm.s_full[sb], (k / kSBufs) & 1);
             tc_fence_after();
             const float4* l4 = reinterpret_cast<const float4*>(lse_ring + ls * kBlock);
-            uint32_t pk[64];
-            uint32_t u[2][32];
-            tmem_ld32(tmem + lane_base + sb * 128, u[0]);
-            tmem_wait_ld();
+            // The exp pass is straight-line code per 32-column chunk (no per-element branches:
+            // the two variants are separate instantiations), so the scheduler can interleave
+            // the MUFU / FMA chains of 32 independent elements. Packed bf16 weights of chunk cq
+            // go back into TMEM columns [16 cq, 16 cq + 16) of the same S^T buffer (already
+            // consumed), so the row is not held in registers while waiting for the P buffer.
+            const uint32_t s_t = tmem + lane_base + sb * 128;
+            auto exp_pass = [&](auto plain_tag) {
+                constexpr bool kPlain = decltype(plain_tag)::value;
+                // diagonal tile: keep r >= c; elsewhere nothing is masked (ragged rows carry
+                // lse = +inf and come out exactly 0 on the MUFU path)
+                const int lim = t == 0 ? c : 0;
+                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f)};
+                uint32_t u[2][32];
+                tmem_ld32(s_t, u[0]);
+                tmem_wait_ld();
 #pragma unroll
-            for (int cq = 0; cq < 4; ++cq) {
-                if (cq < 3) tmem_ld32(tmem + lane_base + sb * 128 + (cq + 1) * 32, u[(cq + 1) & 1]);
-                const uint32_t* x = u[cq & 1];
+                for (int cq = 0; cq < 4; ++cq) {
+                    if (cq < 3) tmem_ld32(s_t + (cq + 1) * 32, u[(cq + 1) & 1]);
+                    const uint32_t* x = u[cq & 1];
+                    uint32_t pk[16];
 #pragma unroll
-                for (int e4 = 0; e4 < 8; ++e4) {
-                    const float4 l = l4[cq * 8 + e4];
-                    const int r = cq * 32 + e4 * 4;
-                    float2 y0 = ffma2(make_float2(__uint_as_float(x[4 * e4]), __uint_as_float(x[4 * e4 + 1])),
-                                      make_float2(sl2, sl2), make_float2(-l.x, -l.y));
-                    float2 y1 = ffma2(make_float2(__uint_as_float(x[4 * e4 + 2]), __uint_as_float(x[4 * e4 + 3])),
-                                      make_float2(sl2, sl2), make_float2(-l.z, -l.w));
-                    float2 e0, e1;
-                    if (plain) {
-                        // 3 pairs in 8 on the FMA pipe, the rest on MUFU (the K4 balance)
-                        if ((0x54u >> e4) & 1u) {
-                            e0 = exp2_poly2(y0);
-                            e1 = exp2_poly2(y1);
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const float4 l = l4[cq * 8 + e4];
+                        const int r = cq * 32 + e4 * 4;
+                        float2 y0 = ffma2(make_float2(__uint_as_float(x[4 * e4]), __uint_as_float(x[4 * e4 + 1])),
+                                          make_float2(sl2, sl2), make_float2(-l.x, -l.y));
+                        float2 y1 = ffma2(make_float2(__uint_as_float(x[4 * e4 + 2]), __uint_as_float(x[4 * e4 + 3])),
+                                          make_float2(sl2, sl2), make_float2(-l.z, -l.w));
+                        float2 e0, e1;
+                        if constexpr (kPlain) {
+                            // 3 pairs in 8 on the FMA pipe, the rest on MUFU (the K4 balance)
+                            if ((0x54u >> e4) & 1u) {
+                                e0 = exp2_poly2(y0);
+                                e1 = exp2_poly2(y1);
+                            } else {
+                                e0 = make_float2(ex2_approx(y0.x), ex2_approx(y0.y));
+                                e1 = make_float2(ex2_approx(y1.x), ex2_approx(y1.y));
+                            }
                         } else {
-                            e0.x = ex2_approx(y0.x);
-                            e0.y = ex2_approx(y0.y);
-                            e1.x = ex2_approx(y1.x);
-                            e1.y = ex2_approx(y1.y);
+                            y0.x = r + 0 >= lim ? y0.x : -INFINITY;
+                            y0.y = r + 1 >= lim ? y0.y : -INFINITY;
+                            y1.x = r + 2 >= lim ? y1.x : -INFINITY;
+                            y1.y = r + 3 >= lim ? y1.y : -INFINITY;
+                            e0 = make_float2(ex2_approx(y0.x), ex2_approx(y0.y));
+                            e1 = make_float2(ex2_approx(y1.x), ex2_approx(y1.y));
                         }
-                    } else {
-                        // diagonal tile (t == 0: keep r >= c) or ragged last block (lse = +inf
-                        // there): MUFU only, so masked weights are exactly 0
-                        if (t == 0) {
-                            if (r + 0 < c) y0.x = -INFINITY;
-                            if (r + 1 < c) y0.y = -INFINITY;
-                            if (r + 2 < c) y1.x = -INFINITY;
-                            if (r + 3 < c) y1.y = -INFINITY;
-                        }
-                        e0.x = ex2_approx(y0.x);
-                        e0.y = ex2_approx(y0.y);
-                        e1.x = ex2_approx(y1.x);
-                        e1.y = ex2_approx(y1.y);
+                        acc[(2 * e4) & 3] = fadd2(acc[(2 * e4) & 3], e0);
+                        acc[(2 * e4 + 1) & 3] = fadd2(acc[(2 * e4 + 1) & 3], e1);
+                        pk[2 * e4] = pack_bf16x2(e0.x, e0.y);
+                        pk[2 * e4 + 1] = pack_bf16x2(e1.x, e1.y);
                     }
-                    vacc = fadd2(vacc, fadd2(e0, e1));
-                    pk[r / 2] = pack_bf16x2(e0.x, e0.y);
-                    pk[r / 2 + 1] = pack_bf16x2(e1.x, e1.y);
+                    tmem_st16(s_t + cq * 16, pk);
+                    if (cq < 3) tmem_wait_ld();
                 }
-                if (cq < 3) tmem_wait_ld();
+                vacc = fadd2(vacc, fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
+            };
+            if (plain) exp_pass(std::true_type{});
+            else exp_pass(std::false_type{});
+            tmem_wait_st();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.l_empty[ls]);
+            if (k >= 1) mbar_wait(&sm.p_free, (k - 1) & 1);
+            // row c of the coarse buffer: 16 aligned 16-byte chunks, chunk q -> coarse column
+            // 128 - 8 floor(c/8) + 8q
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t pk[32];
+                tmem_ld32(s_t + h2 * 32, pk);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int a = a0 + h2 * 8 + q;  // absolute 8-column chunk, 1..31
+                    *reinterpret_cast<uint4*>(prow + (a >> 3) * kHalf + (((a & 7) ^ (c & 7)) << 4)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sm.s_free[sb]);
-                mbar_arrive(&sm.l_empty[ls]);
-            }
-            if (k >= 1) mbar_wait(&sm.p_free, (k - 1) & 1);
-            // 16 aligned 16-byte chunks: chunk q of the row -> coarse column 128 - 8 floor(c/8) + 8q
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int a = a0 + q;  // absolute 8-column chunk, 1..31
-                *reinterpret_cast<uint4*>(prow + (a >> 3) * kHalf + (((a & 7) ^ (c & 7)) << 4)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            }
+            if (lane == 0) mbar_arrive(&sm.s_free[sb]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full);
