@@ -54,8 +54,15 @@ def _bind(lib, prefix: str):
                                                _f64p, _f64p, _cp, ctypes.c_size_t]),
         "apply_rope": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _i64p, ctypes.c_double, _f64p, _i64, _cp,
                                       ctypes.c_size_t]),
+        "indexer_backward": (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _i64, _f64p, _f64p, _f64p,
+                                            ctypes.c_double, _f64p, ctypes.c_double, ctypes.c_int, _f64p, _f64p,
+                                            ctypes.c_double, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p,
+                                            _cp, ctypes.c_size_t]),
     }
     if prefix == "vso_":
+        lib.vso_adamw_step.restype = None
+        lib.vso_adamw_step.argtypes = [_i64, _f64p, _f64p, _f64p, _f64p, _i64, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double]
         sig["blockwise_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64,
                                                      _f64p, _i64, _f64p, _cp, ctypes.c_size_t])
         sig["sparse_attention"] = (ctypes.c_int, [_i64, _i64, _f64p, _i64, _f64p, _i64, _f64p, _i64, _i64p, _i64,
@@ -238,6 +245,24 @@ class _Oracle:
         self._check(rc, msg)
         return out
 
+    def indexer_backward(self, k, v, params, target_v, target_s, eps=1e-8, reverse=True):
+        """-> (loss, grads dict) of the KL distillation loss for one head (indexer.hpp:158-272)."""
+        k, v = (np.ascontiguousarray(x, np.float64) for x in (k, v))
+        n, d = k.shape
+        w_u = np.ascontiguousarray(params["w_u"], np.float64)
+        d_h = w_u.shape[1]
+        b_u, w_v, w_s = (np.ascontiguousarray(params[x], np.float64) for x in ("b_u", "w_v", "w_s"))
+        tv, ts = (np.ascontiguousarray(x, np.float64) for x in (target_v, target_s))
+        g = {"w_u": np.zeros_like(w_u), "b_u": np.zeros(d_h), "w_v": np.zeros(d_h), "w_s": np.zeros(d_h)}
+        loss, gbv, gbs = np.zeros(1), np.zeros(1), np.zeros(1)
+        rc, msg = self._call("indexer_backward", n, d, _f(k), d, _f(v), d, d_h, _f(w_u), _f(b_u), _f(w_v),
+                             float(params["b_v"]), _f(w_s), float(params["b_s"]), 1 if reverse else 0, _f(tv), _f(ts),
+                             float(eps), _f(loss), _f(g["w_u"]), _f(g["b_u"]), _f(g["w_v"]), _f(gbv), _f(g["w_s"]),
+                             _f(gbs))
+        self._check(rc, msg)
+        g["b_v"], g["b_s"] = float(gbv[0]), float(gbs[0])
+        return float(loss[0]), g
+
     def combine_scores(self, verts, slashes, mean=True):
         v = np.ascontiguousarray(np.stack(verts), np.float64)
         s = np.ascontiguousarray(np.stack(slashes), np.float64)
@@ -396,3 +421,27 @@ def ref_formats() -> RefFormats:
     if "fmt" not in _cache:
         _cache["fmt"] = RefFormats()
     return _cache["fmt"]
+
+
+def adamw_step(p, g, m, v, step_index, lr, beta1=0.9, beta2=0.999, adam_eps=1e-8, weight_decay=0.01):
+    """optimizer_step (indexer.hpp:347-363) on flat f64 arrays, in place (the C restatement)."""
+    lib = port().lib
+    lib.vso_adamw_step(p.size, _f(p), _f(g), _f(m), _f(v), int(step_index), float(lr), beta1, beta2, adam_eps,
+                       weight_decay)
+
+
+def ref_optimizer_step(d, d_h, p, g, m, v, step, steps, warmup, lr_peak):
+    """The reference's optimizer_step on one head (flat W_U | b_U | w_v | b_v | w_s | b_s), in place."""
+    lib = ctypes.CDLL(REF_SO)
+    f = lib.vspref_optimizer_step
+    f.argtypes = [_i64, _i64, _f64p, _f64p, _f64p, _f64p, _i64, _i64, _i64, ctypes.c_double, _cp, ctypes.c_size_t]
+    err = ctypes.create_string_buffer(512)
+    if f(d, d_h, _f(p), _f(g), _f(m), _f(v), step, steps, warmup, lr_peak, err, 512):
+        raise OracleError(err.value.decode())
+
+
+def ref_learning_rate(step, steps, warmup, lr_peak):
+    lib = ctypes.CDLL(REF_SO)
+    lib.vspref_learning_rate.restype = ctypes.c_double
+    lib.vspref_learning_rate.argtypes = [_i64, _i64, _i64, ctypes.c_double]
+    return lib.vspref_learning_rate(step, steps, warmup, lr_peak)

@@ -410,4 +410,84 @@ int vspref_apply_rope(int64_t n, int64_t d, const double* x, int64_t xs, const i
     });
 }
 
+// ---- distillation: indexer_backward_loss (indexer.hpp:265-272) with the product-path KL loss,
+// gradients flattened like vso_indexer_backward
+int vspref_indexer_backward(int64_t n, int64_t d, const double* k, int64_t ks, const double* v, int64_t vs,
+                            int64_t d_h, const double* w_u, const double* b_u, const double* w_v, double b_v,
+                            const double* w_s, double b_s, int reverse, const double* target_v,
+                            const double* target_s, double eps, double* loss_out, double* g_w_u, double* g_b_u,
+                            double* g_w_v, double* g_b_v, double* g_w_s, double* g_b_s, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const vsp::IndexerParams p = params(d, d_h, w_u, b_u, w_v, b_v, w_s, b_s);
+        const auto acts = vsp::indexer_forward(p, gather(k, ks, n, d), gather(v, vs, n, d),
+                                               reverse ? vsp::SlashMapping::Reverse : vsp::SlashMapping::Identity);
+        const std::vector<double> tv(target_v, target_v + n), ts(target_s, target_s + n);
+        double loss = 0.0;
+        const vsp::IndexerGrads g = vsp::indexer_backward_loss(p, acts, tv, ts, vsp::make_kl_loss(eps), &loss);
+        *loss_out = loss;
+        std::copy(g.w_u.data.begin(), g.w_u.data.end(), g_w_u);
+        std::copy(g.b_u.begin(), g.b_u.end(), g_b_u);
+        std::copy(g.w_v.begin(), g.w_v.end(), g_w_v);
+        std::copy(g.w_s.begin(), g.w_s.end(), g_w_s);
+        *g_b_v = g.b_v;
+        *g_b_s = g.b_s;
+    });
+}
+
+// ---- optimizer_step (indexer.hpp:347-363) on one head's parameters; params and the Adam
+// moments are updated in place (flattened as W_U | b_U | w_v | b_v | w_s | b_s)
+int vspref_optimizer_step(int64_t d, int64_t d_h, double* flat_p, const double* flat_g, double* flat_m,
+                          double* flat_v, int64_t step, int64_t steps, int64_t warmup, double lr_peak, char* err,
+                          size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const int64_t nw = 2 * d * d_h;
+        auto unflat = [&](const double* f) {
+            vsp::IndexerParams p = params(d, d_h, f, f + nw, f + nw + d_h, f[nw + 2 * d_h], f + nw + 2 * d_h + 1,
+                                          f[nw + 3 * d_h + 1]);
+            return p;
+        };
+        auto grads = [&](const double* f) {
+            vsp::IndexerGrads g;
+            vsp::IndexerParams q = unflat(f);
+            g.w_u = q.w_u; g.b_u = q.b_u; g.w_v = q.w_v; g.b_v = q.b_v; g.w_s = q.w_s; g.b_s = q.b_s;
+            return g;
+        };
+        vsp::IndexerParams p = unflat(flat_p);
+        vsp::OptState st{grads(flat_m), grads(flat_v)};
+        vsp::TrainConfig cfg;
+        cfg.steps = static_cast<size_t>(steps);
+        cfg.warmup_steps = static_cast<size_t>(warmup);
+        cfg.lr_peak = lr_peak;
+        vsp::optimizer_step(p, grads(flat_g), st, static_cast<size_t>(step), cfg);
+        auto flat = [&](const vsp::IndexerParams& q, double* f) {
+            std::copy(q.w_u.data.begin(), q.w_u.data.end(), f);
+            std::copy(q.b_u.begin(), q.b_u.end(), f + nw);
+            std::copy(q.w_v.begin(), q.w_v.end(), f + nw + d_h);
+            f[nw + 2 * d_h] = q.b_v;
+            std::copy(q.w_s.begin(), q.w_s.end(), f + nw + 2 * d_h + 1);
+            f[nw + 3 * d_h + 1] = q.b_s;
+        };
+        flat(p, flat_p);
+        auto flat_g2 = [&](const vsp::IndexerGrads& q, double* f) {
+            std::copy(q.w_u.data.begin(), q.w_u.data.end(), f);
+            std::copy(q.b_u.begin(), q.b_u.end(), f + nw);
+            std::copy(q.w_v.begin(), q.w_v.end(), f + nw + d_h);
+            f[nw + 2 * d_h] = q.b_v;
+            std::copy(q.w_s.begin(), q.w_s.end(), f + nw + 2 * d_h + 1);
+            f[nw + 3 * d_h + 1] = q.b_s;
+        };
+        flat_g2(st.m, flat_m);
+        flat_g2(st.v, flat_v);
+    });
+}
+
+// learning_rate (indexer.hpp:322-329)
+double vspref_learning_rate(int64_t step, int64_t steps, int64_t warmup, double lr_peak) {
+    vsp::TrainConfig cfg;
+    cfg.steps = static_cast<size_t>(steps);
+    cfg.warmup_steps = static_cast<size_t>(warmup);
+    cfg.lr_peak = lr_peak;
+    return vsp::learning_rate(static_cast<size_t>(step), cfg);
+}
+
 }  // extern "C"

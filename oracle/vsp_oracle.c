@@ -502,3 +502,122 @@ int vso_apply_rope(int64_t n, int64_t d, const double* x, int64_t xs, const int6
     }
     return VSO_OK;
 }
+
+/* ------------------------------------------------------------------ distillation (training half) */
+
+/* kl_loss_grad Forward (indexer.hpp:158-185) + softmax_backward (numerics.hpp:62-72) +
+ * indexer_backward_from_upstream (indexer.hpp:222-262) for one KV head, fused:
+ *   loss = KL(pred_v || t_v + eps) + KL(pred_s || t_s + eps)        (kl_loss :138-149)
+ *   dpred = log(pred) + 1 - log(t + eps)   (log(1e-300) for pred == 0)
+ *   dlogit = pred * (dpred - <pred, dpred>)
+ *   dlogit_s is mapped back to tokens: token slash_token_for_offset(o) gets dlogit_s[o]
+ *   g.w_v[h] = sum_i dlogit_v[i] z[i][h]; g.w_s likewise; g.b_v = sum dlogit_v; g.b_s likewise
+ *   dy = (dlogit_v[i] w_v[h] + dlogit_s[i] w_s[h]) * silu'(y[i][h]);  g.w_u = X^T dy; g.b_u = sum dy
+ * The forward is recomputed here (indexer_forward_features :77-113). Validation as kl_loss:
+ * pred/target non-negative and summing to 1 within 1e-6 (check_distribution :125-135). */
+static double silu_deriv(double x) {
+    const double s = x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+    return s + x * s * (1.0 - s);
+}
+
+static int check_dist(const double* v, int64_t n, const char* what, char* err, size_t errlen) {
+    double sum = 0.0;
+    char msg[96];
+    for (int64_t i = 0; i < n; ++i) {
+        if (v[i] < 0.0) {
+            snprintf(msg, sizeof msg, "%s has negative entries", what);
+            return fail(err, errlen, msg);
+        }
+        sum += v[i];
+    }
+    if (fabs(sum - 1.0) > 1e-6) {
+        snprintf(msg, sizeof msg, "%s does not sum to 1", what);
+        return fail(err, errlen, msg);
+    }
+    return VSO_OK;
+}
+
+static double kl_grad(const double* pred, const double* target, int64_t n, double eps, double* dlogit) {
+    double loss = 0.0, inner = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (pred[i] > 0.0) loss += pred[i] * (log(pred[i]) - log(target[i] + eps));
+        const double dp = (pred[i] > 0.0 ? log(pred[i]) : log(1e-300)) + 1.0 - log(target[i] + eps);
+        dlogit[i] = dp;
+        inner += dp * pred[i];
+    }
+    for (int64_t i = 0; i < n; ++i) dlogit[i] = pred[i] * (dlogit[i] - inner);
+    return loss;
+}
+
+int vso_indexer_backward(int64_t n, int64_t d, const double* k, int64_t ks, const double* v, int64_t vs,
+                         int64_t d_h, const double* w_u, const double* b_u, const double* w_v, double b_v,
+                         const double* w_s, double b_s, int reverse, const double* target_v,
+                         const double* target_s, double eps, double* loss_out, double* g_w_u, double* g_b_u,
+                         double* g_w_v, double* g_b_v, double* g_w_s, double* g_b_s, char* err, size_t errlen) {
+    if (eps <= 0.0) return fail(err, errlen, "kl_loss: eps must be positive");
+    double* lv = (double*)malloc(sizeof(double) * n);
+    double* ls = (double*)malloc(sizeof(double) * n);
+    double* pv = (double*)malloc(sizeof(double) * n);
+    double* ps = (double*)malloc(sizeof(double) * n);
+    double* dv = (double*)malloc(sizeof(double) * n);
+    double* dso = (double*)malloc(sizeof(double) * n);
+    double* y = (double*)malloc(sizeof(double) * d_h);
+    int rc = vso_indexer_forward(n, d, k, ks, v, vs, d_h, w_u, b_u, w_v, b_v, w_s, b_s, reverse, lv, ls, pv, ps,
+                                 err, errlen);
+    if (!rc) rc = check_dist(pv, n, "kl_loss pred", err, errlen);
+    if (!rc) rc = check_dist(target_v, n, "kl_loss target", err, errlen);
+    if (!rc) rc = check_dist(ps, n, "kl_loss pred", err, errlen);
+    if (!rc) rc = check_dist(target_s, n, "kl_loss target", err, errlen);
+    if (!rc) {
+        *loss_out = kl_grad(pv, target_v, n, eps, dv) + kl_grad(ps, target_s, n, eps, dso);
+        memset(g_w_u, 0, sizeof(double) * 2 * d * d_h);
+        memset(g_b_u, 0, sizeof(double) * d_h);
+        memset(g_w_v, 0, sizeof(double) * d_h);
+        memset(g_w_s, 0, sizeof(double) * d_h);
+        *g_b_v = 0.0;
+        *g_b_s = 0.0;
+        for (int64_t t = 0; t < n; ++t) {
+            const double dlv = dv[t];
+            const double dls = dso[reverse ? n - 1 - t : t]; /* token t fed offset slot o(t) */
+            /* y = X W_U (matrix.hpp:56-71 order) then + b_U, as indexer_forward_features :86-90 */
+            for (int64_t h = 0; h < d_h; ++h) y[h] = 0.0;
+            for (int64_t c = 0; c < 2 * d; ++c) {
+                const double xc = c < d ? k[t * ks + c] : v[t * vs + (c - d)];
+                const double* wr = w_u + c * d_h;
+                for (int64_t h = 0; h < d_h; ++h) y[h] += xc * wr[h];
+            }
+            for (int64_t h = 0; h < d_h; ++h) y[h] += b_u[h];
+            for (int64_t h = 0; h < d_h; ++h) {
+                const double z = vso_silu(y[h]);
+                g_w_v[h] += dlv * z;
+                g_w_s[h] += dls * z;
+                const double dy = (dlv * w_v[h] + dls * w_s[h]) * silu_deriv(y[h]);
+                g_b_u[h] += dy;
+                y[h] = dy;
+            }
+            *g_b_v += dlv;
+            *g_b_s += dls;
+            for (int64_t c = 0; c < 2 * d; ++c) {
+                const double xc = c < d ? k[t * ks + c] : v[t * vs + (c - d)];
+                double* gr = g_w_u + c * d_h;
+                for (int64_t h = 0; h < d_h; ++h) gr[h] += xc * y[h];
+            }
+        }
+    }
+    free(lv); free(ls); free(pv); free(ps); free(dv); free(dso); free(y);
+    return rc;
+}
+
+/* optimizer_step (indexer.hpp:347-363) over a flat parameter vector; lr from learning_rate
+ * (:322-329) is passed in. */
+void vso_adamw_step(int64_t count, double* p, const double* g, double* m, double* v, int64_t step_index, double lr,
+                    double beta1, double beta2, double adam_eps, double weight_decay) {
+    const double t = (double)(step_index + 1);
+    const double bc1 = 1.0 - pow(beta1, t), bc2 = 1.0 - pow(beta2, t);
+    for (int64_t i = 0; i < count; ++i) {
+        m[i] = beta1 * m[i] + (1.0 - beta1) * g[i];
+        v[i] = beta2 * v[i] + (1.0 - beta2) * g[i] * g[i];
+        const double mhat = m[i] / bc1, vhat = v[i] / bc2;
+        p[i] -= lr * (mhat / (sqrt(vhat) + adam_eps) + weight_decay * p[i]);
+    }
+}

@@ -130,6 +130,35 @@ def main():
                        out=ref.apply_rope(x, positions, base).tolist()))
     C["apply_rope"] = rp
 
+    # distillation: indexer_backward_loss (indexer.hpp:265-272), optimizer_step (:347-363),
+    # learning_rate (:322-329)
+    ib = []
+    for n, d, dh, rev in ((9, 4, 6, True), (13, 8, 16, False), (1, 2, 3, True)):
+        k, v = rng.standard_normal((n, d)), rng.standard_normal((n, d))
+        pr = {"w_u": rng.uniform(-0.3, 0.3, (2 * d, dh)), "b_u": rng.standard_normal(dh) * 0.1,
+              "w_v": rng.standard_normal(dh), "b_v": 0.2, "w_s": rng.standard_normal(dh), "b_s": -0.1}
+        tv, ts = rng.random(n), rng.random(n)
+        tv, ts = tv / tv.sum(), ts / ts.sum()
+        loss, g = ref.indexer_backward(k, v, pr, tv, ts, reverse=rev)
+        ib.append(dict(k=k.tolist(), v=v.tolist(), params={x: (y.tolist() if hasattr(y, "tolist") else y)
+                                                           for x, y in pr.items()},
+                       target_v=tv.tolist(), target_s=ts.tolist(), reverse=rev, loss=loss,
+                       grads={x: (y.tolist() if hasattr(y, "tolist") else y) for x, y in g.items()}))
+    C["indexer_backward"] = ib
+    d, dh = 2, 3
+    cnt = 2 * d * dh + 3 * dh + 2
+    p0, g0 = rng.standard_normal(cnt), rng.standard_normal(cnt)
+    m0, v0 = rng.standard_normal(cnt) * 0.1, rng.random(cnt) * 0.1
+    os_ = []
+    for step, steps, warmup in ((0, 10, 3), (5, 10, 3), (9, 10, 0)):
+        p1, m1, v1 = p0.copy(), m0.copy(), v0.copy()
+        oracle.ref_optimizer_step(d, dh, p1, g0, m1, v1, step, steps, warmup, 1e-3)
+        os_.append(dict(d=d, d_h=dh, p=p0.tolist(), g=g0.tolist(), m=m0.tolist(), v=v0.tolist(), step=step,
+                        steps=steps, warmup=warmup, lr_peak=1e-3,
+                        lr=oracle.ref_learning_rate(step, steps, warmup, 1e-3),
+                        p_out=p1.tolist(), m_out=m1.tolist(), v_out=v1.tolist()))
+    C["optimizer_step"] = os_
+
     path = os.path.join(HERE, "reference_vectors.json")
     with open(path, "w") as f:
         json.dump(out, f)
