@@ -183,10 +183,14 @@ def prepare_indexer(args, device, rank, world):
             q, k, v = synth_layer(args, device, seed=args.seed + 101 + i)
             prompts.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
             del q, k, v
-        params, losses = calibrate.train_indexer(prompts, args.d_h, steps=args.distill_steps)
-        info["indexer"] = (f"VSIndexer distilled on GPU (KL to K5 ground truth, AdamW, {args.distill_steps} steps) "
-                           f"on {args.train_prompts} training prompts of the same heads; held-out prompt timed")
+        tstats = {}
+        params, losses = calibrate.train_indexer(prompts, args.d_h, steps=args.distill_steps, stats=tstats)
+        info["indexer"] = (f"VSIndexer distilled on GPU (KL to K5 ground truth, AdamW, {args.distill_steps} steps; "
+                           f"sm_100a loss/backward/AdamW kernels) on {args.train_prompts} training prompts of the "
+                           f"same heads; held-out prompt timed")
         info["distill_loss_first_last"] = [x for x in losses if x == x][:1] + [losses[-1]]
+        info["distill_step_ms"] = round(tstats.get("step_ms", float("nan")), 3)
+        info["ground_truth_ms_per_prompt"] = round(tstats.get("ground_truth_ms", float("nan")), 2)
         info["prep_s"] = None
     if args.tau_v is not None and args.tau_s is not None:
         budget = [vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,

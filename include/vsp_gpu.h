@@ -130,6 +130,32 @@ VSP_API int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const vo
 VSP_API int vsp_vs_attn_tile_stats(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace,
                                    int64_t* tiles_out, void* stream);
 
+/* ---- distillation: the training half (indexer.hpp:138-434) ---------------------------
+ * vsp_indexer_loss_grad = indexer_forward + kl_loss_grad (Forward KL, eps smoothing) +
+ * indexer_backward_from_upstream for every KV head: per-head loss KL_v + KL_s into loss[hkv]
+ * (device, may be null) and the gradient, flattened in the parameter layout
+ *   W_U [hkv, 2d, d_h] | b_U [hkv, d_h] | w_v [hkv, d_h] | w_s [hkv, d_h] | b_v [hkv] | b_s [hkv]
+ * The forward reads the bf16 copy of W_U; targets are K5's normalised aggregates.
+ * vsp_adamw_step = optimizer_step (:347-363) over a flat fp32 parameter vector with the
+ * learning rate of learning_rate (:322-329) supplied by the caller; it also refreshes a
+ * bf16 shadow of the first shadow_count parameters (W_U) for the next forward. */
+typedef struct {
+    double lr;
+    double beta1;
+    double beta2;
+    double adam_eps;
+    double weight_decay;
+} vsp_adamw;
+VSP_API size_t vsp_indexer_grad_workspace_size(int n, int hkv, int d_h);
+VSP_API int vsp_indexer_loss_grad(vsp_ctx* ctx, const void* k, const void* v, int n, int hkv, int d, int d_h,
+                                  const void* w_u_bf16, const float* b_u, const float* w_v, const float* b_v,
+                                  const float* w_s, const float* b_s, int slash_mapping, const float* target_v,
+                                  const float* target_s, double kl_eps, float* loss, float* grads, void* workspace,
+                                  void* stream);
+VSP_API int vsp_adamw_step(vsp_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t count,
+                           int64_t step_index, const vsp_adamw* cfg, void* shadow_bf16, int64_t shadow_count,
+                           void* stream);
+
 /* ---- the whole VS-prefill layer: K1 -> K2 -> K3 in one call ------------------------
  * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads, but
  * pipelined over KV-head chunks of `heads_per_chunk` heads (0 = automatic: two halves): the scoring, selection and

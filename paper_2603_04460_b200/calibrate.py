@@ -29,13 +29,22 @@ def ground_truth(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
 
 
 def train_indexer(prompts: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]], d_h: int, steps: int = 200,
-                  lr_peak: float = 3e-3, seed: int = 1) -> Tuple[IndexerParams, List[float]]:
+                  lr_peak: float = 3e-3, seed: int = 1, stats: Optional[dict] = None
+                  ) -> Tuple[IndexerParams, List[float]]:
+    """K5 ground truth of each prompt, then distillation on the sm_100a training kernels.
+    stats (optional) receives ground_truth_ms (K4 LSE + K5 per prompt) and step_ms."""
     samples = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
     for q, k, v in prompts:
         a_v, a_s, _ = ground_truth(q, k, v)
         samples.append((k, v, a_v, a_s))
-    return distill_indexer(samples, d_h=d_h, steps=steps, lr_peak=lr_peak, warmup=max(1, steps // 10), seed=seed,
-                           log_every=max(1, steps // 10))
+    ev1.record()
+    out = distill_indexer(samples, d_h=d_h, steps=steps, lr_peak=lr_peak, warmup=max(1, steps // 10), seed=seed,
+                          log_every=max(1, steps // 10), stats=stats)
+    if stats is not None:
+        stats["ground_truth_ms"] = ev0.elapsed_time(ev1) / max(len(prompts), 1)
+    return out
 
 
 def calibrate_budget(q, k=None, v=None, params: IndexerParams = None, recall_target: float = 0.9,

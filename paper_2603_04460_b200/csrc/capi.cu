@@ -15,6 +15,7 @@
 #include "indexer.h"
 #include "rope.h"
 #include "select.h"
+#include "train.h"
 #include "vsp_error.h"
 
 namespace vsp_detail {
@@ -253,6 +254,42 @@ int vsp_apply_rope(vsp_ctx* ctx, const void* q_in, const void* k_in, void* q_out
                      base, style == VSP_ROPE_HALF_SPLIT};
     cudaError_t e = vsp_rope::launch(a, as_stream(stream));
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_apply_rope");
+}
+
+// ------------------------------------------------------------------ distillation
+size_t vsp_indexer_grad_workspace_size(int n, int hkv, int d_h) { return vsp_train::workspace_bytes(n, hkv, d_h); }
+
+int vsp_indexer_loss_grad(vsp_ctx* ctx, const void* k, const void* v, int n, int hkv, int d, int d_h,
+                          const void* w_u_bf16, const float* b_u, const float* w_v, const float* b_v,
+                          const float* w_s, const float* b_s, int slash_mapping, const float* target_v,
+                          const float* target_s, double kl_eps, float* loss, float* grads, void* workspace,
+                          void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (n < 1) return set_err(VSP_EINVAL, "indexer_forward: empty input");
+    if (d != 128) return set_err(VSP_EINVAL, "vsp: head dim must be 128");
+    if (d_h < 1 || d_h % 256 != 0) return set_err(VSP_EINVAL, "vsp_indexer_loss_grad: d_h must be a multiple of 256");
+    if (!(kl_eps > 0.0)) return set_err(VSP_EINVAL, "kl_loss: eps must be positive");
+    if (slash_mapping != VSP_SLASH_REVERSE && slash_mapping != VSP_SLASH_IDENTITY)
+        return set_err(VSP_EINVAL, "vsp_indexer_loss_grad: bad slash mapping");
+    if (!workspace || !grads || !target_v || !target_s)
+        return set_err(VSP_EINVAL, "vsp_indexer_loss_grad: null argument");
+    vsp_train::GradArgs a{k, v, n, hkv, d_h, w_u_bf16, b_u, w_v, b_v, w_s, b_s,
+                          slash_mapping == VSP_SLASH_REVERSE, target_v, target_s, kl_eps, loss, grads};
+    cudaError_t e = vsp_train::loss_grad(a, workspace, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_indexer_loss_grad");
+}
+
+int vsp_adamw_step(vsp_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t count,
+                   int64_t step_index, const vsp_adamw* cfg, void* shadow_bf16, int64_t shadow_count, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (!params || !grads || !m || !v || !cfg || count < 0 || step_index < 0)
+        return set_err(VSP_EINVAL, "vsp_adamw_step: bad arguments");
+    if (shadow_count < 0 || shadow_count > count || (shadow_count > 0 && !shadow_bf16))
+        return set_err(VSP_EINVAL, "vsp_adamw_step: bad shadow range");
+    vsp_train::AdamArgs a{params, grads, m, v, count, step_index, cfg->lr, cfg->beta1, cfg->beta2, cfg->adam_eps,
+                          cfg->weight_decay, shadow_bf16, shadow_count};
+    cudaError_t e = vsp_train::adamw(a, as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_adamw_step");
 }
 
 // ------------------------------------------------------------------ indexer

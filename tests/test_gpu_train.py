@@ -1,0 +1,101 @@
+"""GPU parity of the distillation kernels (csrc/train.cu) against the oracle.
+
+* vsp_indexer_loss_grad vs the f64 restatement of indexer_backward_loss (pinned bit-exact to
+  the reference in tests/test_oracle.py), on the same bf16 K, V, W_U values:
+  loss within 1e-3 relative; each gradient tensor within 3e-2 relative Frobenius error
+  (bf16 X / W_U / dY / Z operands on the tensor core, fp32 accumulation); the bias
+  gradients sum(dlogit) are ~0 analytically (|g| <= 1e-4).
+* vsp_adamw_step vs the f64 optimizer_step restatement (fp32 state: 1e-5 relative).
+* A short distillation run lowers the loss like the fp32 torch-autograd reference.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from helpers import f64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def distill():
+    import paper_2603_04460_b200 as m
+    m.load_library()
+    from paper_2603_04460_b200 import distill as d
+    return d
+
+
+def _targets(hkv, n, seed):
+    g = torch.Generator().manual_seed(seed)
+    tv = torch.softmax(torch.randn(hkv, n, generator=g) * 3, dim=1).double()
+    ts = torch.softmax(torch.randn(hkv, n, generator=g) * 3, dim=1).double()
+    tv, ts = tv / tv.sum(1, keepdim=True), ts / ts.sum(1, keepdim=True)
+    return tv.float().cuda(), ts.float().cuda()
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("n,hkv,d_h,reverse", [(300, 2, 256, True), (1000, 1, 512, False), (128, 2, 256, True)])
+def test_loss_grad_matches_oracle(distill, n, hkv, d_h, reverse):
+    g = torch.Generator().manual_seed(n + d_h)
+    k = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    v = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    tv, ts = _targets(hkv, n, seed=n)
+    tr = distill.IndexerTrainer(hkv, 128, d_h, "cuda", seed=3)
+    # non-trivial heads and biases so every gradient path is exercised
+    tr.view("w_v").copy_(torch.randn(hkv, d_h, generator=g) * 0.3)
+    tr.view("w_s").copy_(torch.randn(hkv, d_h, generator=g) * 0.3)
+    tr.view("b_u").copy_(torch.randn(hkv, d_h, generator=g) * 0.2)
+    tr.w_u_bf16.copy_(tr.view("w_u").bfloat16())
+    loss = tr.loss_grad(k, v, tv, ts, reverse=reverse)
+    torch.cuda.synchronize()
+    port = oracle.port()
+    for h in range(hkv):
+        pr = {"w_u": f64(tr.w_u_bf16[h]), "b_u": f64(tr.view("b_u")[h]), "w_v": f64(tr.view("w_v")[h]),
+              "b_v": float(tr.view("b_v")[h]), "w_s": f64(tr.view("w_s")[h]), "b_s": float(tr.view("b_s")[h])}
+        tvn, tsn = f64(tv[h]), f64(ts[h])
+        want_loss, want = port.indexer_backward(f64(k[:, h]), f64(v[:, h]), pr, tvn / tvn.sum(), tsn / tsn.sum(),
+                                                reverse=reverse)
+        assert abs(float(loss[h]) - want_loss) <= 1e-3 * abs(want_loss) + 1e-6
+        nw, nv = tr.nw // hkv, tr.nv // hkv
+        gr = tr.grads
+        got = {"w_u": f64(gr[:tr.nw].view(hkv, 256, d_h)[h]),
+               "b_u": f64(gr[tr.nw:tr.nw + tr.nv].view(hkv, d_h)[h]),
+               "w_v": f64(gr[tr.nw + tr.nv:tr.nw + 2 * tr.nv].view(hkv, d_h)[h]),
+               "w_s": f64(gr[tr.nw + 2 * tr.nv:tr.nw + 3 * tr.nv].view(hkv, d_h)[h])}
+        for key in ("w_u", "b_u", "w_v", "w_s"):
+            assert _rel(got[key], want[key]) <= 3e-2, (key, _rel(got[key], want[key]))
+        bv = float(gr[tr.nw + 3 * tr.nv + h])
+        bs = float(gr[tr.nw + 3 * tr.nv + hkv + h])
+        assert abs(bv - want["b_v"]) <= 1e-4 and abs(bs - want["b_s"]) <= 1e-4
+
+
+def test_adamw_matches_oracle(distill):
+    tr = distill.IndexerTrainer(1, 128, 256, "cuda", seed=1)
+    g = torch.Generator().manual_seed(9)
+    tr.grads.copy_(torch.randn(tr.count, generator=g))
+    p0 = f64(tr.flat).copy()
+    gr = f64(tr.grads).copy()
+    m, v = np.zeros_like(p0), np.zeros_like(p0)
+    for step in range(3):
+        tr.adamw(step, 1e-3 * (step + 1))
+        oracle.adamw_step(p0, gr, m, v, step, 1e-3 * (step + 1))
+    torch.cuda.synchronize()
+    assert np.abs(f64(tr.flat) - p0).max() <= 1e-5 * np.abs(p0).max()
+    assert torch.equal(tr.w_u_bf16.view(-1), tr.flat[:tr.nw].bfloat16())
+
+
+def test_distillation_lowers_loss_like_torch_reference(distill):
+    n, hkv = 2048, 2
+    g = torch.Generator().manual_seed(4)
+    k = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    v = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    tv, ts = _targets(hkv, n, seed=5)
+    _, l_gpu = distill.distill_indexer([(k, v, tv, ts)], d_h=256, steps=80, lr_peak=1e-2, warmup=5, log_every=1)
+    _, l_ref = distill.distill_indexer_torch([(k, v, tv, ts)], d_h=256, steps=80, lr_peak=1e-2, warmup=5, log_every=1)
+    assert abs(l_gpu[0] - l_ref[0]) <= 1e-3 * l_ref[0]      # same init, same objective
+    assert l_gpu[-1] < 0.8 * l_gpu[0]
+    assert abs(l_gpu[-1] - l_ref[-1]) <= 0.1 * l_ref[-1]     # bf16 operands vs fp32 autograd

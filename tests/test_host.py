@@ -100,7 +100,7 @@ def test_distill_objective_decreases_and_matches_reference_kl():
     p = lp.exp().double().numpy()
     want = (p * (np.log(p) - np.log(tv.double().numpy() + 1e-8))).sum(1)
     assert np.allclose(got, want, rtol=1e-5)
-    params, losses = distill.distill_indexer([(k, v, tv, ts)], d_h=256, steps=60, lr_peak=1e-2, warmup=5,
+    params, losses = distill.distill_indexer_torch([(k, v, tv, ts)], d_h=256, steps=60, lr_peak=1e-2, warmup=5,
                                              log_every=1)
     assert losses[-1] < losses[0] * 0.8
     assert params.w_u.dtype == torch.bfloat16 and params.w_u.shape == (hkv, 2 * d, 256)
