@@ -15,6 +15,12 @@
  *   vsp_vs_aggregate     <- vsp::aggregate_streaming      vsaggregate.hpp:62-127
  *                           + vsp::combine_scores         vsaggregate.hpp:133-157
  *   vsp_recall_from_lse  <- vsp::attention_recall         attention.hpp:198-215
+ *   vsp_apply_rope       <- vsp::apply_rope               rope.hpp:63-79 (Q and K, one pass)
+ *   vsp_indexer_loss_grad <- vsp::indexer_backward_loss   indexer.hpp:158-272 (KL + backward)
+ *   vsp_adamw_step       <- vsp::optimizer_step           indexer.hpp:347-363
+ *   vsp_allgather_heads  (the only collective: head-sharded O assembly)
+ *   vsp_{write,read}_tensor, vsp_{save,load}_checkpoint, vsp_{write,read}_indices
+ *                        <- tensor_io.hpp:49-88, indexer.hpp:450-499, sparsity.hpp:187-245
  *
  * Layouts (all row-major, innermost last):
  *   Q [n, hq, d] bf16, K/V [n, hkv, d] bf16, O [n, hq, d] bf16, LSE [hq, n] fp32,

@@ -10,6 +10,11 @@
 //   vsp::gpu::sparse_attention     <- vsp::sparse_attention     attention.hpp:150
 //   vsp::gpu::blockwise_attention  <- vsp::blockwise_attention  attention.hpp:96
 //   vsp::gpu::aggregate_streaming  <- vsp::aggregate_streaming  vsaggregate.hpp:62
+//   vsp::gpu::apply_rope           <- vsp::apply_rope           rope.hpp:63-79
+//   vsp::gpu::indexer_backward     <- vsp::indexer_backward     indexer.hpp:275 (Forward KL)
+//   vsp::gpu::optimizer_step       <- vsp::optimizer_step       indexer.hpp:347
+//   vsp::gpu::{write,read}_tensor, read_vector, save/load_checkpoint, write/read_indices
+//                                  <- tensor_io.hpp, indexer.hpp:450-499, sparsity.hpp:187-245
 //
 // Host f64 data is converted to the device formats (bf16 Q/K/V/W_U, fp32 scores) on the way
 // in and widened back to f64 on the way out, so results carry the GPU path's stated
@@ -24,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -204,6 +211,169 @@ inline VSScores aggregate_streaming(const AttentionInputs& in, std::size_t block
     s.slash = detail::download_f32(as, n);
     s.normalized = normalized;
     return s;
+}
+
+// rope.hpp:63-79 (interleaved planes, as the reference)
+inline Matrix apply_rope(const Matrix& x, const std::vector<std::size_t>& positions, const RopeConfig& cfg) {
+    require(x.cols == cfg.head_dim, "apply_rope: column count != head_dim");
+    require(positions.size() == x.rows, "apply_rope: positions length != row count");
+    const int n = static_cast<int>(x.rows), d = static_cast<int>(x.cols);
+    Matrix out(x.rows, x.cols);
+    if (n == 0) return out;
+    auto in = detail::upload_bf16(x);
+    detail::Buf o(static_cast<size_t>(n) * d * 2), pos(static_cast<size_t>(n) * 8);
+    std::vector<int64_t> hp(positions.begin(), positions.end());
+    detail::cuda(cudaMemcpy(pos.p, hp.data(), hp.size() * 8, cudaMemcpyHostToDevice));
+    detail::check(vsp_apply_rope(detail::context(), in->p, nullptr, o.p, nullptr, n, 1, 0, d, pos.as<int64_t>(),
+                                 cfg.base, VSP_ROPE_INTERLEAVED, nullptr));
+    return detail::download_head0(o, x.rows, x.cols, 1);
+}
+inline Matrix apply_rope(const Matrix& x, const RopeConfig& cfg) {
+    std::vector<std::size_t> positions(x.rows);
+    for (std::size_t i = 0; i < positions.size(); ++i) positions[i] = i;
+    return vsp::gpu::apply_rope(x, positions, cfg);
+}
+
+// indexer.hpp:275-282 with the product-path loss. The GPU recomputes the forward from acts.x
+// (= [K | V]); only the forward KL direction is implemented.
+inline IndexerGrads indexer_backward(const IndexerParams& p, const IndexerActivations& acts,
+                                     const std::vector<double>& target_v, const std::vector<double>& target_s,
+                                     double eps = 1e-8, KlDirection dir = KlDirection::Forward) {
+    require(dir == KlDirection::Forward, "vsp::gpu::indexer_backward: only the forward KL direction");
+    require(p.in_dim() == acts.x.cols && p.in_dim() % 2 == 0, "indexer_backward: feature width != in_dim");
+    const int n = static_cast<int>(acts.x.rows), d = static_cast<int>(p.in_dim() / 2), dh = static_cast<int>(p.d_h);
+    Matrix k(n, d), v(n, d);
+    for (int t = 0; t < n; ++t)
+        for (int c = 0; c < d; ++c) {
+            k(t, c) = acts.x(t, c);
+            v(t, c) = acts.x(t, d + c);
+        }
+    auto kb = detail::upload_bf16(k), vb = detail::upload_bf16(v), wu = detail::upload_bf16(p.w_u);
+    auto bu = detail::upload_f32(p.b_u), wv = detail::upload_f32(p.w_v), ws = detail::upload_f32(p.w_s);
+    auto bv = detail::upload_f32({p.b_v}), bs = detail::upload_f32({p.b_s});
+    auto tv = detail::upload_f32(target_v), ts = detail::upload_f32(target_s);
+    const size_t count = 2 * static_cast<size_t>(d) * dh + 3 * static_cast<size_t>(dh) + 2;
+    detail::Buf grads(count * 4), wsp(vsp_indexer_grad_workspace_size(n, 1, dh));
+    detail::check(vsp_indexer_loss_grad(detail::context(), kb->p, vb->p, n, 1, d, dh, wu->p, bu->as<float>(),
+                                        wv->as<float>(), bv->as<float>(), ws->as<float>(), bs->as<float>(),
+                                        acts.mapping == SlashMapping::Reverse ? VSP_SLASH_REVERSE : VSP_SLASH_IDENTITY,
+                                        tv->as<float>(), ts->as<float>(), eps, nullptr, grads.as<float>(), wsp.p,
+                                        nullptr));
+    const std::vector<double> g = detail::download_f32(grads, count);
+    IndexerGrads out = IndexerGrads::zeros_like(p);
+    const size_t nw = 2 * static_cast<size_t>(d) * dh;
+    std::copy(g.begin(), g.begin() + nw, out.w_u.data.begin());
+    std::copy(g.begin() + nw, g.begin() + nw + dh, out.b_u.begin());
+    std::copy(g.begin() + nw + dh, g.begin() + nw + 2 * dh, out.w_v.begin());
+    std::copy(g.begin() + nw + 2 * dh, g.begin() + nw + 3 * dh, out.w_s.begin());
+    out.b_v = g[nw + 3 * dh];
+    out.b_s = g[nw + 3 * dh + 1];
+    return out;
+}
+
+// indexer.hpp:347-363, fp32 state on the device (parameters and moments round-trip as f64)
+inline void optimizer_step(IndexerParams& p, const IndexerGrads& grads, OptState& state, std::size_t step_index,
+                           const TrainConfig& cfg) {
+    auto flat = [](const Matrix& w, const std::vector<double>& b, const std::vector<double>& wv, double bv,
+                   const std::vector<double>& ws, double bs) {
+        std::vector<double> f(w.data);
+        f.insert(f.end(), b.begin(), b.end());
+        f.insert(f.end(), wv.begin(), wv.end());
+        f.insert(f.end(), ws.begin(), ws.end());
+        f.push_back(bv);
+        f.push_back(bs);
+        return f;
+    };
+    auto unflat = [](const std::vector<double>& f, Matrix& w, std::vector<double>& b, std::vector<double>& wv,
+                     double& bv, std::vector<double>& ws, double& bs) {
+        size_t o = 0;
+        for (double& x : w.data) x = f[o++];
+        for (double& x : b) x = f[o++];
+        for (double& x : wv) x = f[o++];
+        for (double& x : ws) x = f[o++];
+        bv = f[o++];
+        bs = f[o++];
+    };
+    const auto fp = flat(p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s);
+    const auto fg = flat(grads.w_u, grads.b_u, grads.w_v, grads.b_v, grads.w_s, grads.b_s);
+    const auto fm = flat(state.m.w_u, state.m.b_u, state.m.w_v, state.m.b_v, state.m.w_s, state.m.b_s);
+    const auto fv = flat(state.v.w_u, state.v.b_u, state.v.w_v, state.v.b_v, state.v.w_s, state.v.b_s);
+    auto bp = detail::upload_f32(fp), bg = detail::upload_f32(fg), bm = detail::upload_f32(fm), bvv = detail::upload_f32(fv);
+    const vsp_adamw a{learning_rate(step_index, cfg), cfg.beta1, cfg.beta2, cfg.adam_eps, cfg.weight_decay};
+    detail::check(vsp_adamw_step(detail::context(), bp->as<float>(), bg->as<float>(), bm->as<float>(), bvv->as<float>(),
+                                 static_cast<int64_t>(fp.size()), static_cast<int64_t>(step_index), &a, nullptr, 0,
+                                 nullptr));
+    unflat(detail::download_f32(*bp, fp.size()), p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s);
+    unflat(detail::download_f32(*bm, fp.size()), state.m.w_u, state.m.b_u, state.m.w_v, state.m.b_v, state.m.w_s,
+           state.m.b_s);
+    unflat(detail::download_f32(*bvv, fp.size()), state.v.w_u, state.v.b_u, state.v.w_v, state.v.b_v, state.v.w_s,
+           state.v.b_s);
+}
+
+// ---- interchange formats through the C ABI (same bytes and error texts as the reference)
+inline void write_tensor(const std::string& path, const Matrix& m) {
+    const uint64_t dims[2] = {m.rows, m.cols};
+    detail::check(vsp_write_tensor(path.c_str(), 2, dims, m.data.data()));
+}
+inline void write_tensor(const std::string& path, const std::vector<double>& v) {
+    const uint64_t dims[1] = {v.size()};
+    detail::check(vsp_write_tensor(path.c_str(), 1, dims, v.data()));
+}
+inline Matrix read_tensor(const std::string& path) {
+    int nd = 0;
+    uint64_t dims[8] = {};
+    detail::check(vsp_tensor_header(path.c_str(), &nd, dims, 8));
+    Matrix m(nd == 2 ? dims[0] : 0, nd == 2 ? dims[1] : 0);
+    detail::check(vsp_read_tensor(path.c_str(), 2, m.data.data(), m.data.size()));
+    return m;
+}
+inline std::vector<double> read_vector(const std::string& path) {
+    int nd = 0;
+    uint64_t dims[8] = {};
+    detail::check(vsp_tensor_header(path.c_str(), &nd, dims, 8));
+    std::vector<double> v(nd == 1 ? dims[0] : 0);
+    detail::check(vsp_read_tensor(path.c_str(), 1, v.data(), v.size()));
+    return v;
+}
+inline void save_checkpoint(const IndexerParams& p, const std::string& path) {
+    p.check_shapes();
+    require(p.in_dim() % 2 == 0, "save_checkpoint: in_dim must be 2d");
+    detail::check(vsp_save_checkpoint(path.c_str(), static_cast<int>(p.in_dim() / 2), static_cast<int>(p.d_h),
+                                      p.w_u.data.data(), p.b_u.data(), p.w_v.data(), p.b_v, p.w_s.data(), p.b_s));
+}
+inline IndexerParams load_checkpoint(const std::string& path) {
+    int d = 0, dh = 0;
+    detail::check(vsp_checkpoint_header(path.c_str(), &d, &dh));
+    IndexerParams p;
+    p.d_h = static_cast<size_t>(dh);
+    p.w_u = Matrix(2 * static_cast<size_t>(d), p.d_h);
+    p.b_u.resize(p.d_h);
+    p.w_v.resize(p.d_h);
+    p.w_s.resize(p.d_h);
+    detail::check(vsp_load_checkpoint(path.c_str(), d, dh, p.w_u.data.data(), p.b_u.data(), p.w_v.data(), &p.b_v,
+                                      p.w_s.data(), &p.b_s));
+    return p;
+}
+inline void write_indices(const std::string& path, const SelectedIndices& sel) {
+    std::vector<int64_t> a(sel.i_v.begin(), sel.i_v.end()), b(sel.i_s.begin(), sel.i_s.end());
+    detail::check(vsp_write_indices(path.c_str(), a.data(), static_cast<int64_t>(a.size()), b.data(),
+                                    static_cast<int64_t>(b.size())));
+}
+inline SelectedIndices read_indices(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    long size = 1;
+    if (f) {
+        std::fseek(f, 0, SEEK_END);
+        size = std::max(1L, std::ftell(f));
+        std::fclose(f);
+    }
+    std::vector<int64_t> a(size), b(size);
+    int64_t kv = 0, ks = 0;
+    detail::check(vsp_read_indices(path.c_str(), a.data(), &kv, b.data(), &ks, size));
+    SelectedIndices sel;
+    sel.i_v.assign(a.begin(), a.begin() + kv);
+    sel.i_s.assign(b.begin(), b.begin() + ks);
+    return sel;
 }
 
 }  // namespace vsp::gpu

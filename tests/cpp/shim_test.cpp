@@ -156,6 +156,117 @@ int main() {
         det = "max rel=" + std::to_string(worst);
         return worst <= 2e-2;
     });
+    // Rope.MatchesExplicitRotationMatrix / ApplyRope.* (test_rope.cpp), d = 128, long positions
+    check("apply_rope_matches_reference", [](std::string& det) {
+        Rng rng(25);
+        const RopeConfig cfg(128, 10000.0);
+        const Matrix x = oracle::random_matrix(rng, 9, 128);
+        const std::vector<std::size_t> pos = {0, 1, 7, 4095, 32768, 65537, 100000, 131071, 3};
+        const double err = max_abs_diff(vsp::gpu::apply_rope(x, pos, cfg), vsp::apply_rope(x, pos, cfg));
+        const double err2 = max_abs_diff(vsp::gpu::apply_rope(x, cfg), vsp::apply_rope(x, cfg));
+        det = "max|d|=" + std::to_string(std::max(err, err2));
+        return err <= 3e-2 && err2 <= 3e-2;  // bf16 in and out
+    });
+    // IndexerBackward vs the reference (gradients within bf16-operand tolerance)
+    check("indexer_backward_matches_reference", [](std::string& det) {
+        Rng rng(31);
+        const size_t n = 200, d = 128, dh = 256;
+        IndexerParams p = make_indexer_params(2 * d, dh, rng);
+        for (double& w : p.w_v) w = 0.3 * rng.next_normal();
+        for (double& w : p.w_s) w = 0.3 * rng.next_normal();
+        // W_U, K, V exactly bf16-representable so both sides see the same inputs
+        auto bf = [](double x) { return static_cast<double>(__bfloat162float(__float2bfloat16(static_cast<float>(x)))); };
+        for (double& w : p.w_u.data) w = bf(w);
+        Matrix k = oracle::random_matrix(rng, n, d), v = oracle::random_matrix(rng, n, d);
+        for (double& x : k.data) x = bf(x);
+        for (double& x : v.data) x = bf(x);
+        std::vector<double> tv(n), ts(n);
+        double sv = 0, ss = 0;
+        for (size_t i = 0; i < n; ++i) {
+            tv[i] = rng.next_uniform() + 0.01;
+            ts[i] = rng.next_uniform() + 0.01;
+            sv += tv[i];
+            ss += ts[i];
+        }
+        for (size_t i = 0; i < n; ++i) {
+            tv[i] /= sv;
+            ts[i] /= ss;
+        }
+        const IndexerActivations acts = vsp::indexer_forward(p, k, v);
+        const IndexerGrads want = vsp::indexer_backward(p, acts, tv, ts);
+        const IndexerGrads got = vsp::gpu::indexer_backward(p, acts, tv, ts);
+        auto rel = [](const std::vector<double>& a, const std::vector<double>& b) {
+            double num = 0, den = 0;
+            for (size_t i = 0; i < a.size(); ++i) {
+                num += (a[i] - b[i]) * (a[i] - b[i]);
+                den += b[i] * b[i];
+            }
+            return std::sqrt(num / std::max(den, 1e-300));
+        };
+        const double e = std::max({rel(got.w_u.data, want.w_u.data), rel(got.b_u, want.b_u), rel(got.w_v, want.w_v),
+                                   rel(got.w_s, want.w_s)});
+        det = "max rel=" + std::to_string(e);
+        return e <= 3e-2 && std::fabs(got.b_v - want.b_v) <= 1e-4 && std::fabs(got.b_s - want.b_s) <= 1e-4;
+    });
+    // Optimizer.MatchesScalarAdamWOracle (test_indexer.cpp:346-380) on the device
+    check("optimizer_step_matches_reference", [](std::string& det) {
+        Rng rng(33);
+        IndexerParams p = make_indexer_params(8, 5, rng);
+        IndexerGrads g = IndexerGrads::zeros_like(p);
+        for (double& x : g.w_u.data) x = rng.next_normal();
+        for (double& x : g.w_v) x = rng.next_normal();
+        g.b_s = 0.5;
+        OptState s1 = OptState::zeros_like(p), s2 = OptState::zeros_like(p);
+        IndexerParams p1 = p, p2 = p;
+        TrainConfig cfg;
+        cfg.steps = 10;
+        cfg.warmup_steps = 2;
+        for (size_t step = 0; step < 3; ++step) {
+            vsp::optimizer_step(p1, g, s1, step, cfg);
+            vsp::gpu::optimizer_step(p2, g, s2, step, cfg);
+        }
+        double e = std::fabs(p1.b_s - p2.b_s);
+        for (size_t i = 0; i < p1.w_u.data.size(); ++i) e = std::max(e, std::fabs(p1.w_u.data[i] - p2.w_u.data[i]));
+        det = "max|d|=" + std::to_string(e);
+        return e <= 1e-6;
+    });
+    // TensorIo / Checkpoint / IndicesText: the GPU library writes the reference's bytes
+    check("formats_match_reference", [](std::string& det) {
+        Rng rng(35);
+        const Matrix m = oracle::random_matrix(rng, 5, 3);
+        vsp::write_tensor("/tmp/vsp_shim_ref.vstn", m);
+        vsp::gpu::write_tensor("/tmp/vsp_shim_gpu.vstn", m);
+        auto slurp = [](const char* f) {
+            FILE* h = std::fopen(f, "rb");
+            std::string s;
+            int c;
+            while (h && (c = std::fgetc(h)) != EOF) s.push_back(static_cast<char>(c));
+            if (h) std::fclose(h);
+            return s;
+        };
+        bool ok = slurp("/tmp/vsp_shim_ref.vstn") == slurp("/tmp/vsp_shim_gpu.vstn");
+        ok = ok && vsp::gpu::read_tensor("/tmp/vsp_shim_ref.vstn").data == m.data;
+        IndexerParams p = make_indexer_params(8, 5, rng);
+        vsp::save_checkpoint(p, "/tmp/vsp_shim_ref.vsck");
+        vsp::gpu::save_checkpoint(p, "/tmp/vsp_shim_gpu.vsck");
+        ok = ok && slurp("/tmp/vsp_shim_ref.vsck") == slurp("/tmp/vsp_shim_gpu.vsck");
+        ok = ok && vsp::gpu::load_checkpoint("/tmp/vsp_shim_ref.vsck").w_u.data == p.w_u.data;
+        SelectedIndices sel;
+        sel.i_v = {1, 3, 17};
+        sel.i_s = {0, 5};
+        vsp::write_indices("/tmp/vsp_shim_ref.txt", sel);
+        vsp::gpu::write_indices("/tmp/vsp_shim_gpu.txt", sel);
+        ok = ok && slurp("/tmp/vsp_shim_ref.txt") == slurp("/tmp/vsp_shim_gpu.txt");
+        ok = ok && vsp::gpu::read_indices("/tmp/vsp_shim_ref.txt").i_v == sel.i_v;
+        try {
+            vsp::gpu::read_tensor("/nonexistent/x.vstn");
+            ok = false;
+        } catch (const std::runtime_error& e) {
+            ok = ok && std::string(e.what()) == "cannot open tensor: /nonexistent/x.vstn";
+        }
+        det = ok ? "bytes and texts identical" : "mismatch";
+        return ok;
+    });
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }
