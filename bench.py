@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--recall-target", type=float, default=0.9)
     ap.add_argument("--calib-margin", type=float, default=0.015,
                     help="calibrate the budget for recall_target + margin on the validation prompt")
+    ap.add_argument("--tau-step", type=float, default=0.1,
+                    help="grid step of the per-head (tau_v, tau_s) calibration over (0, 1)")
     ap.add_argument("--tau-v", type=float, default=None, help="fix tau_v (skips calibration)")
     ap.add_argument("--tau-s", type=float, default=None)
     ap.add_argument("--min-budget", type=int, default=1)
@@ -205,11 +207,13 @@ def prepare_indexer(args, device, rank, world):
             q, k, v = synth_layer(args, device, seed=args.seed + 201 + i)
             vals.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
             del q, k, v
-        budget, pt = calibrate.calibrate_budget(vals, params=params,
+        taus = tuple(round(args.tau_step * i, 4) for i in range(1, int(round(1 / args.tau_step))))
+        budget, pt = calibrate.calibrate_budget(vals, params=params, taus=taus,
                                                 recall_target=args.recall_target + args.calib_margin,
                                                 min_budget=args.min_budget,
                                                 max_budget=None if args.max_budget < 0 else args.max_budget)
-        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) calibrated on {args.val_prompts} validation prompts "
+        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) on a {args.tau_step} grid, calibrated on "
+                                 f"{args.val_prompts} validation prompts "
                                  f"(worst case) for mean recall >= {args.recall_target} + {args.calib_margin}: "
                                  f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
         del vals

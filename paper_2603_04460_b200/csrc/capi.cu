@@ -389,12 +389,21 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // the first half's attention, and each attention launch still spans enough heads to
 // balance its long and short CTAs (tools/sched_sweep.py: profiles/r01_schedule_sweep.json).
 int auto_hpc(int hkv) { return (hkv + 1) / 2; }
+// hpc < 0: a lead chunk of -hpc heads (its scoring is the only exposed part), then the rest
+// as one chunk whose scoring overlaps the lead chunk's attention.
 int num_chunks(int hkv, int hpc) {
-    if (hpc <= 0) hpc = auto_hpc(hkv);
+    if (hpc < 0) return -hpc >= hkv ? 1 : 2;
+    if (hpc == 0) hpc = auto_hpc(hkv);
     return (hkv + hpc - 1) / hpc;
 }
 void chunk_range(int c, int hkv, int hpc, int& g0, int& cnt) {
-    if (hpc <= 0) hpc = auto_hpc(hkv);
+    if (hpc < 0) {
+        const int lead = std::min(-hpc, hkv);
+        g0 = c == 0 ? 0 : lead;
+        cnt = c == 0 ? lead : hkv - lead;
+        return;
+    }
+    if (hpc == 0) hpc = auto_hpc(hkv);
     g0 = c * hpc;
     cnt = std::min(hpc, hkv - g0);
 }
@@ -429,7 +438,6 @@ int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_map
         if (b.max_budget >= 0 && b.min_budget > b.max_budget)
             return set_err(VSP_EINVAL, "budget config: min_budget exceeds max_budget");
     }
-    if (heads_per_chunk < 0) return set_err(VSP_EINVAL, w + ": heads_per_chunk must be >= 0");
     if (num_chunks(hkv, heads_per_chunk) > vsp_ctx::kMaxChunks) return set_err(VSP_EINVAL, w + ": too many chunks");
     return VSP_OK;
 }
