@@ -177,6 +177,29 @@ VSP_API int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const voi
                            int* k_s, int cap, void* o, float* lse, void* workspace, int heads_per_chunk,
                            int flags, void* stream);
 
+/* ---- balanced multi-GPU split (SURVEY.md §8e refinement) -----------------------------
+ * Adaptive per-head budgets make KV heads unequal (one head can carry 40% of a layer's
+ * tiles), so plain head sharding leaves ranks idle. A unit is one KV head g (with its Q
+ * heads) on query blocks [qb_lo, qb_hi) of 128 rows; ranks take contiguous runs of units of
+ * equal predicted cost (per-(head, block) tile counts from vsp_vs_attn_tile_counts on a
+ * calibration prompt) and call vsp_vs_prefill_units with the full (replicated) Q/K/V: it
+ * scores, selects and plans each distinct head of its units, then attends each unit. No
+ * collective; units write disjoint (head, row) regions of O and LSE (head-major O with
+ * VSP_O_HEAD_MAJOR). Same results as vsp_vs_prefill on the rows a unit covers. */
+typedef struct {
+    int32_t g;
+    int32_t qb_lo;
+    int32_t qb_hi;
+} vsp_unit;
+VSP_API int vsp_vs_attn_tile_counts(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace, int32_t* counts,
+                                    void* stream);
+VSP_API int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq, int hkv,
+                                 int d, int d_h, const void* w_u, const float* b_u, const float* w_v, const float* b_v,
+                                 const float* w_s, const float* b_s, int slash_mapping, const vsp_budget* budgets,
+                                 float* a_v, float* a_s, int* i_v, int* k_v, int* i_s, int* k_s, int cap, void* o,
+                                 float* lse, void* workspace, const vsp_unit* units, int nunits, int flags,
+                                 void* stream);
+
 /* ---- the layer from HOST buffers (the reference's own calling convention) ----------
  * The reference operators take and return host memory (std::vector; attention.hpp:150,
  * tools/vsprefill.cpp:154-185). This entry point does the same: Q/K/V are read from host

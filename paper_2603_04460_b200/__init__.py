@@ -33,7 +33,7 @@ import torch
 __all__ = [
     "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
     "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
-    "aggregate_streaming", "attention_recall", "RopeConfig", "apply_rope", "apply_rope_qk", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "lib_path", "load_library",
+    "aggregate_streaming", "attention_recall", "RopeConfig", "apply_rope", "apply_rope_qk", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "vs_prefill_units", "sparse_tile_counts", "lib_path", "load_library",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -97,6 +97,9 @@ def load_library():
     lib.vsp_vs_prefill.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
                                     ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, i, vp])
     lib.vsp_apply_rope.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, vp, ctypes.c_double, i, vp]
+    lib.vsp_vs_attn_tile_counts.argtypes = [vp, i, i, i, vp, vp, vp]
+    lib.vsp_vs_prefill_units.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
+                                          ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, i, i, vp])
     _lib = lib
     return lib
 
@@ -416,6 +419,58 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
                               _ptr(lse), _ptr(ws), int(heads_per_chunk), VSP_O_HEAD_MAJOR if head_major else 0,
                               _stream(dev)))
     return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
+
+
+class _Unit(ctypes.Structure):
+    _fields_ = [("g", ctypes.c_int32), ("qb_lo", ctypes.c_int32), ("qb_hi", ctypes.c_int32)]
+
+
+def sparse_tile_counts(n: int, hkv: int, cap: int, device) -> torch.Tensor:
+    """Per (KV head, query block) tile counts [hkv, ceil(n/128)] of the last sparse_attention
+    plan on this device's workspace (vsp_vs_attn_tile_counts) — the cost table of a balanced
+    split. Call it right after sparse_attention (like sparse_tile_stats)."""
+    lib = load_library()
+    dev = torch.device(device)
+    num_qb = (n + 127) // 128
+    out = torch.empty(hkv * num_qb, dtype=torch.int32)
+    ws = _workspace(dev, 0)
+    _check(lib.vsp_vs_attn_tile_counts(_context(dev), n, hkv, cap, _ptr(ws), ctypes.c_void_p(out.data_ptr()),
+                                       _stream(dev)))
+    return out.view(hkv, num_qb)
+
+
+def vs_prefill_units(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget, units,
+                     out: torch.Tensor, lse: torch.Tensor, mapping: str = "reverse"):
+    """A rank's share of a balanced multi-GPU split (vsp_vs_prefill_units): `units` is a list of
+    (KV head, qb_lo, qb_hi); Q/K/V and params cover ALL heads; O is head-major [Hq, n, d] and
+    only the units' (head, row) regions are written. Returns the device SelectedIndices (valid
+    for the heads the units touch)."""
+    _need_cuda(q, k, v)
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    budgets = list(budget) if isinstance(budget, (list, tuple)) else [budget] * hkv
+    if len(budgets) != hkv:
+        raise VspError("vs_prefill_units: one BudgetConfig per KV head required")
+    if out.shape != (hq, n, d):
+        raise VspError("vs_prefill_units: out must be head-major [Hq, n, d]")
+    arr = (_Budget * hkv)(*[b._c() for b in budgets])
+    ua = (_Unit * max(len(units), 1))(*[_Unit(int(g), int(lo), int(hi)) for g, lo, hi in units])
+    lib = load_library()
+    dev = q.device
+    cap = n + 1
+    a_v = torch.empty(hkv, n, device=dev, dtype=torch.float32)
+    a_s = torch.empty_like(a_v)
+    i_v = torch.empty(hkv, cap, device=dev, dtype=torch.int32)
+    i_s = torch.empty_like(i_v)
+    k_v = torch.zeros(hkv, device=dev, dtype=torch.int32)
+    k_s = torch.zeros_like(k_v)
+    ws = _workspace(dev, lib.vsp_vs_prefill_workspace_size(n, hkv, params.d_h, cap))
+    _check(lib.vsp_vs_prefill_units(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h,
+                                    _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
+                                    _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
+                                    _ptr(a_v), _ptr(a_s), _ptr(i_v), _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(out),
+                                    _ptr(lse), _ptr(ws), ua, len(units), VSP_O_HEAD_MAJOR, _stream(dev)))
+    return SelectedIndices(i_v, k_v, i_s, k_s)
 
 
 def vs_prefill_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,

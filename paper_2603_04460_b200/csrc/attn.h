@@ -22,6 +22,7 @@ struct __align__(64) AttnParams {
     const uint32_t* sbits;
     int list_stride;
     int pair0, npairs;   // Q-head pairs [pair0, pair0 + npairs) handled by this launch
+    int qb_hi;           // query blocks [qb_hi - gridDim.x / npairs, qb_hi) handled by this launch
     int bm_words;
     int n, hq, hkv;
     float scale;
@@ -49,7 +50,7 @@ struct SparseArgs {
 cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream);
 size_t sparse_workspace_bytes(int n, int hkv, int cap);
 cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream,
-                          int g0 = 0, int count = -1, int phase = 3);
+                          int g0 = 0, int count = -1, int phase = 3, int qb_lo = 0, int qb_hi = -1);
 
 }  // namespace vsp_attn
 

@@ -27,6 +27,7 @@
 // which is the reference's duplicate-free per-row union.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "attn.h"
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const int heads_per_pair = p.npairs;  // Q-head pairs in this launch, starting at p.pair0
     const int num_qb = (p.n + kBlock - 1) / kBlock;
     // heaviest query blocks first (causal work grows with the block index)
-    const int qb = num_qb - 1 - static_cast<int>(blockIdx.x) / heads_per_pair;
+    const int qb = p.qb_hi - 1 - static_cast<int>(blockIdx.x) / heads_per_pair;
     const int pair = p.pair0 + static_cast<int>(blockIdx.x) % heads_per_pair;
     const int h0 = 2 * pair;
     const int g = h0 / (p.hq / p.hkv);
@@ -598,6 +599,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     p.pair0 = 0;
     p.npairs = a.hq / 2;
+    p.qb_hi = num_qb;
     dim3 grid(num_qb * p.npairs);
     attn_fwd_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
     return cudaGetLastError();
@@ -620,7 +622,7 @@ size_t sparse_workspace_bytes(int n, int hkv, int cap) {
 // phase: 1 = plan (bitmaps, vertical gather, tile lists), 2 = attention kernel, 3 = both;
 // only KV heads [g0, g0 + count) are touched, so head ranges can be pipelined on streams.
 cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
-                          int count, int phase) {
+                          int count, int phase, int qb_lo, int qb_hi) {
     if (count < 0) count = a.hkv - g0;
     AttnParams p{};
     p.n = a.n;
@@ -681,7 +683,11 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         const int pairs_per_group = (a.hq / a.hkv) / 2;
         p.pair0 = g0 * pairs_per_group;
         p.npairs = count * pairs_per_group;
-        dim3 grid(num_qb * p.npairs);
+        // query blocks [qb_lo, qb_hi) only (a balanced work unit of a multi-GPU split)
+        p.qb_hi = qb_hi < 0 ? num_qb : std::min(qb_hi, num_qb);
+        const int nqb = p.qb_hi - std::max(qb_lo, 0);
+        if (nqb <= 0) return cudaGetLastError();
+        dim3 grid(nqb * p.npairs);
         attn_fwd_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
     }
     return cudaGetLastError();

@@ -520,6 +520,90 @@ extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const 
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill");
 }
 
+// per (KV head, query block) tile counts of the last plan on `workspace` -> host [hkv, num_qb]
+namespace {
+__global__ void tile_counts_kernel(const int* lists, int total, int list_stride, int* out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
+        out[t] = lists[static_cast<size_t>(t) * list_stride];
+}
+}  // namespace
+
+extern "C" int vsp_vs_attn_tile_counts(vsp_ctx* ctx, int n, int hkv, int cap, const void* workspace, int32_t* counts,
+                                       void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (!workspace || !counts || n < 1 || hkv < 1) return set_err(VSP_EINVAL, "vsp_vs_attn_tile_counts: bad arguments");
+    const int num_qb = (n + 127) / 128;
+    const int kvcap = ((cap + 127) / 128) * 128;
+    const int bm_words = (n + 31) / 32 + 1;
+    const int list_stride = 2 + kvcap / 128 + num_qb + 3;
+    size_t off = 0;
+    auto skip = [&](size_t b) { off += (b + 255) & ~size_t(255); };
+    skip(static_cast<size_t>(hkv) * kvcap * 128 * 2);
+    skip(static_cast<size_t>(hkv) * kvcap * 128 * 2);
+    skip(static_cast<size_t>(hkv) * bm_words * 4 * 2);
+    const int* lists = reinterpret_cast<const int*>(static_cast<const uint8_t*>(workspace) + off);
+    cudaStream_t st = as_stream(stream);
+    int* d = nullptr;
+    const int total = hkv * num_qb;
+    cudaError_t e = cudaMallocAsync(&d, sizeof(int) * total, st);
+    if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_tile_counts");
+    tile_counts_kernel<<<(total + 255) / 256, 256, 0, st>>>(lists, total, list_stride, d);
+    e = cudaMemcpyAsync(counts, d, sizeof(int) * total, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_attn_tile_counts");
+}
+
+// Balanced multi-GPU split (SURVEY.md §8e refinement): score + select + plan the distinct KV
+// heads of `units`, then attend each unit's query-block range. Collective-free; units of
+// different ranks write disjoint (head, row) regions of O / LSE.
+extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq, int hkv,
+                                    int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                                    const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                                    const vsp_budget* budgets, float* a_v, float* a_s, int* i_v, int* k_v, int* i_s,
+                                    int* k_s, int cap, void* o, float* lse, void* workspace, const vsp_unit* units,
+                                    int nunits, int flags, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, 0, "vsp_vs_prefill_units");
+    if (rc) return rc;
+    if (flags & ~VSP_O_HEAD_MAJOR) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: unknown flags");
+    if (nunits < 0 || (nunits > 0 && !units)) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: bad units");
+    const int num_qb = (n + 127) / 128;
+    std::vector<char> touched(hkv, 0);
+    for (int u = 0; u < nunits; ++u) {
+        const vsp_unit& x = units[u];
+        if (x.g < 0 || x.g >= hkv || x.qb_lo < 0 || x.qb_hi > num_qb || x.qb_lo > x.qb_hi)
+            return set_err(VSP_EINVAL, "vsp_vs_prefill_units: unit out of range");
+        touched[x.g] = 1;
+    }
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    void* ws_ix = ws;
+    ws += align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
+    void* ws_sel = ws;
+    ws += align256(vsp_select_k::workspace_bytes(n, hkv));
+    void* ws_attn = ws;
+    float* lv = static_cast<float*>(ws_ix);
+    float* ls = lv + static_cast<size_t>(hkv) * n;
+    cudaStream_t st = as_stream(stream);
+    vsp_attn::AttnArgs aa{q, k, v, o, lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)),
+                          (flags & VSP_O_HEAD_MAJOR) != 0};
+    vsp_attn::SparseArgs sa{i_v, k_v, i_s, k_s, cap};
+    cudaError_t e = cudaSuccess;
+    for (int g = 0; g < hkv && e == cudaSuccess; ++g) {
+        if (!touched[g]) continue;
+        vsp_indexer::Args ia{k, v, n, hkv, d_h, w_u, b_u, w_v, b_v, w_s, b_s, slash_mapping == VSP_SLASH_REVERSE,
+                             nullptr, nullptr, lv, ls, g, 1};
+        e = vsp_indexer::launch(ia, ws_ix, st);
+        if (e == cudaSuccess)
+            e = vsp_select_k::launch_from_logits(lv, ls, a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, ws_sel,
+                                                 st, g, 1);
+        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g, 1, 1);
+    }
+    for (int u = 0; u < nunits && e == cudaSuccess; ++u)
+        e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, units[u].g, 1, 2, units[u].qb_lo, units[u].qb_hi);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_units");
+}
+
 extern "C" size_t vsp_vs_prefill_host_workspace_size(int n, int hq, int hkv, int d_h) {
     const int cap = n + 1;
     return vsp_vs_prefill_workspace_size(n, hkv, d_h, cap) + host_staging_bytes(n, hq, hkv, cap);

@@ -9,11 +9,18 @@ VSP_O_HEAD_MAJOR), so the slab IS the send buffer and `VspComm.allgather_heads` 
 in-place ncclAllGather over NVLink/NVSwitch through the C ABI (vsp_allgather_heads) — no
 permute and no staging copy. `assemble_heads` is the torch.distributed equivalent for a
 token-major shard.
+
+Balanced split (SURVEY.md §8e refinement, `balanced_units`): adaptive per-head budgets make
+KV heads unequal — in the 128k bench one head carries ~40% of the tiles, so 8-way head
+sharding would run at ~2.5x instead of 8x. With replicated Q/K/V, the (KV head, query
+block) grid is cut into `world` contiguous runs of equal predicted cost (tile counts of a
+calibration prompt + a per-CTA overhead); each rank scores/selects only the heads its run
+touches and attends its units (`vs_prefill_units`). Still no collective on the data path.
 """
 from __future__ import annotations
 
 import ctypes
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -112,3 +119,32 @@ class VspComm:
             self.close()
         except Exception:
             pass
+
+
+def balanced_units(cost, world: int, cta_overhead: float = 2.0) -> List[List[Tuple[int, int, int]]]:
+    """Cut the (KV head, query block) grid, walked head-major, into `world` contiguous runs of
+    near-equal cost. cost: [hkv, num_qb] predicted tiles per (head, block) (e.g. from
+    sparse_tile_counts on a calibration prompt); each block also pays `cta_overhead`
+    tile-equivalents. Returns per rank a list of units (g, qb_lo, qb_hi)."""
+    rows = [[float(x) + cta_overhead for x in r] for r in (cost.tolist() if hasattr(cost, "tolist") else cost)]
+    hkv, nqb = len(rows), len(rows[0])
+    total = sum(sum(r) for r in rows)
+    flat = [(g, b, rows[g][b]) for g in range(hkv) for b in range(nqb)]
+    out: List[List[Tuple[int, int, int]]] = [[] for _ in range(world)]
+    acc, r = 0.0, 0
+    for g, b, c in flat:
+        # move to the next rank once this one reached its share (midpoint rule on the block)
+        while r < world - 1 and acc + 0.5 * c > total * (r + 1) / world:
+            r += 1
+        units = out[r]
+        if units and units[-1][0] == g and units[-1][2] == b:
+            units[-1] = (g, units[-1][1], b + 1)
+        else:
+            units.append((g, b, b + 1))
+        acc += c
+    return out
+
+
+def units_cost(units, cost, cta_overhead: float = 2.0) -> float:
+    rows = cost.tolist() if hasattr(cost, "tolist") else cost
+    return sum(float(rows[g][b]) + cta_overhead for g, lo, hi in units for b in range(lo, hi))

@@ -81,3 +81,27 @@ def test_allgather_heads_world1_through_c_abi(vsp):
     with pytest.raises(vsp.VspError, match="bad arguments"):
         comm.allgather_heads(torch.empty(0, 0, 0, device="cuda", dtype=torch.bfloat16))
     comm.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_balanced_units_reassemble_the_layer_bit_exact(vsp, world):
+    """Virtual ranks on one GPU: each runs vs_prefill_units on its balanced units; the union
+    of their head-major O / LSE regions equals the one-call layer exactly."""
+    from paper_2603_04460_b200 import parallel
+    n, hq, hkv = 1500, 8, 4
+    q, k, v = qkv(n, hq, hkv, seed=23)
+    p = _params(vsp, hkv, 5)
+    budgets = [vsp.BudgetConfig(0.3 + 0.1 * g, 0.5, 1, None) for g in range(hkv)]
+    o_ref, lse_ref, pat_ref = vsp.vs_prefill(q, k, v, p, budgets, head_major=True)
+    vsp.sparse_attention(q, k, v, pat_ref, validate=False)  # the plan the counts are read from
+    cost = vsp.sparse_tile_counts(n, hkv, n + 1, q.device)
+    assert cost.shape == (hkv, (n + 127) // 128) and int(cost.sum()) > 0
+    units = parallel.balanced_units(cost, world)
+    o = torch.full_like(o_ref, float("nan"))
+    lse = torch.full_like(lse_ref, float("nan"))
+    for r in range(world):
+        pat = vsp.vs_prefill_units(q, k, v, p, budgets, units[r], out=o, lse=lse)
+        torch.cuda.synchronize()
+        for g in {u[0] for u in units[r]}:
+            assert pat.lists(g) == pat_ref.lists(g)
+    assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)

@@ -170,3 +170,25 @@ def test_head_sharding_and_assembly_gloo():
     assert all(ok for _, ok, _, _ in res)
     assert all(t == 2.0 for _, _, t, _ in res)
     assert [r[3] for r in res] == [(0, 4), (4, 8)]
+
+
+def test_balanced_units_cover_grid_once_and_balance():
+    from paper_2603_04460_b200 import parallel
+    rng = np.random.default_rng(3)
+    hkv, nqb = 8, 100
+    cost = rng.integers(0, 40, size=(hkv, nqb))
+    cost[6] += np.arange(nqb) * 3  # one heavy, growing head (the adaptive-budget case)
+    for world in (1, 2, 3, 4, 8):
+        units = parallel.balanced_units(cost, world)
+        seen = np.zeros((hkv, nqb), dtype=int)
+        for r, us in enumerate(units):
+            for g, lo, hi in us:
+                assert 0 <= lo < hi <= nqb
+                seen[g, lo:hi] += 1
+        assert (seen == 1).all()
+        costs = [parallel.units_cost(us, cost) for us in units]
+        worst_block = float(cost.max()) + 2.0
+        assert max(costs) - min(costs) <= 2 * worst_block + 1e-9
+        # head sharding would put the heavy head's whole cost on one rank
+        if world == 8:
+            assert max(costs) < 0.5 * (float(cost[6].sum()) + 2.0 * nqb)
