@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--d-h", type=int, default=1024)
     ap.add_argument("--indexer", choices=["distilled", "random"], default="distilled")
     ap.add_argument("--train-prompts", type=int, default=4)
-    ap.add_argument("--val-prompts", type=int, default=2)
+    ap.add_argument("--val-prompts", type=int, default=4)
     ap.add_argument("--distill-steps", type=int, default=300)
     ap.add_argument("--recall-target", type=float, default=0.9)
     ap.add_argument("--calib-margin", type=float, default=0.015,

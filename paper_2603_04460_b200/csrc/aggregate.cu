@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 
 #include "aggregate.h"
@@ -53,11 +54,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 struct __align__(64) Params {
     CUtensorMap map_q, map_k;
     const float* lse;  // [hq, n]
-    float* a_v;        // [hkv, n]
-    float* a_s;
+    unsigned long long* acc_v;  // [hkv, n] fixed-point (2^52) accumulators: integer atomics are
+    unsigned long long* acc_s;  // order-independent, so the aggregates are bit-reproducible
     int n, hq, hkv, num_qb, num_qc;
     float scale;       // 1/sqrt(d)
     float out_scale;   // (normalized ? 1/n : 1) * (mean ? 1/group : 1)
+    double fix_scale;  // 2^52 / (power of two >= the expected total of one profile)
 };
 
 struct Smem {
@@ -65,7 +67,7 @@ struct Smem {
     uint64_t q_full[kQStages], q_empty[kQStages];
     uint64_t l_full[kLStages], l_empty[kLStages];
     uint64_t s_full[kSBufs], s_free[kSBufs];
-    uint64_t p_full, p_free, all_done;
+    uint64_t p_full, p_free[2], all_done;  // p_free[b]: reductions of items with k & 1 == b done
     uint32_t tmem_base;
 };
 
@@ -81,6 +83,10 @@ constexpr int kOffStage = kOffVx + 512;
 constexpr int kStageFloats = 136 * 8;
 constexpr int kSmemBytes = kOffStage + 2 * kStageFloats * 4 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "aggregate smem");
+
+VSP_DEVICE unsigned long long to_fixed(float x, double scale) {
+    return static_cast<unsigned long long>(__double2ll_rn(static_cast<double>(x) * scale));
+}
 
 // (query chunk, group, key block) of this CTA; chunk qc covers query blocks
 // [kChunk*qc, kChunk*qc + kChunk) and pairs with key blocks J < min(num_qb, kChunk*(qc+1)).
@@ -127,7 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             mbar_init(&sm.s_free[b], 4);
         }
         mbar_init(&sm.p_full, 4);
-        mbar_init(&sm.p_free, 1);
+        mbar_init(&sm.p_free[0], 1);
+        mbar_init(&sm.p_free[1], 1);
         mbar_init(&sm.all_done, 1);
         fence_barrier_init();
     }
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                 // lower half -> coarse block t-1 (slot tl), upper half -> block t (slot tl+1)
                 if (t >= 1) issue_red(tl, 0, tl > 0 || hh > 0);
                 issue_red(tl + 1, 1, hh > 0);
-                umma_commit(&sm.p_free);
+                umma_commit(&sm.p_free[k & 1]);
                 if (k == num_items - 1) umma_commit(&sm.all_done);
             }
             __syncwarp();
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                                  make_float2(0.f, 0.f)};
                 uint32_t u[2][32];
                 tmem_ld32(s_t, u[0]);
-                tmem_wait_ld();
+                tmem_wait_ld(u[0]);
 #pragma unroll
                 for (int cq = 0; cq < 4; ++cq) {
                     if (cq < 3) tmem_ld32(s_t + (cq + 1) * 32, u[(cq + 1) & 1]);
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                         pk[2 * e4 + 1] = pack_bf16x2(e1.x, e1.y);
                     }
                     tmem_st16(s_t + cq * 16, pk);
-                    if (cq < 3) tmem_wait_ld();
+                    if (cq < 3) tmem_wait_ld(u[(cq + 1) & 1]);
                 }
                 vacc = fadd2(vacc, fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
             };
@@ -328,14 +335,17 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             tmem_wait_st();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.l_empty[ls]);
-            if (k >= 1) mbar_wait(&sm.p_free, (k - 1) & 1);
+            // the reduction of item k-1 (the other warpgroup's) must have read the P buffer.
+            // One barrier per item parity: a single barrier would let this warpgroup, one item
+            // ahead, match the parity of item k-3's completion and overwrite P too early.
+            if (k >= 1) mbar_wait(&sm.p_free[(k - 1) & 1], ((k - 1) >> 1) & 1);
             // row c of the coarse buffer: 16 aligned 16-byte chunks, chunk q -> coarse column
             // 128 - 8 floor(c/8) + 8q
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
                 uint32_t pk[32];
                 tmem_ld32(s_t + h2 * 32, pk);
-                tmem_wait_ld();
+                tmem_wait_ld(pk);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const int a = a0 + h2 * 8 + q;  // absolute 8-column chunk, 1..31
@@ -360,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         if (w == 0) {
             const int j = j0 + c;
             if (j < p.n && num_items > 0)
-                atomicAdd(p.a_v + static_cast<size_t>(g) * p.n + j, (vacc.x + vacc.y + vx[c]) * p.out_scale);
+                atomicAdd(p.acc_v + static_cast<size_t>(g) * p.n + j, to_fixed((vacc.x + vacc.y + vx[c]) * p.out_scale, p.fix_scale));
         }
         // slash block b = sum_f E[128 b + x + f][f]; E block b lives in slot b - t0 + 1 (slot 0
         // only when t0 >= 1). WG w flushes blocks with (b - b_lo) % 2 == w.
@@ -375,14 +385,14 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             uint32_t e[16];
             if (v0) {
                 tmem_ld16(t_acc + s0 * kAccCols + lane_base, e);
-                tmem_wait_ld();
+                tmem_wait_ld(e);
             }
 #pragma unroll
             for (int f = 0; f < 8; ++f) stage[c * 8 + f] = v0 ? __uint_as_float(e[f]) : 0.f;
             if (quarter == 0) {  // rows 128..135 of the window: first rows of block b+1
                 if (v1) {
                     tmem_ld16(t_acc + (s0 + 1) * kAccCols + lane_base, e);
-                    tmem_wait_ld();
+                    tmem_wait_ld(e);
                 }
                 if (lane < 8) {
 #pragma unroll
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
 #pragma unroll
             for (int f = 0; f < 8; ++f) sum += stage[(c + f) * 8 + f];
             const int o = b * kBlock + c;
-            if (o < p.n && sum != 0.f) atomicAdd(p.a_s + static_cast<size_t>(g) * p.n + o, sum * p.out_scale);
+            if (o < p.n && sum != 0.f) atomicAdd(p.acc_s + static_cast<size_t>(g) * p.n + o, to_fixed(sum * p.out_scale, p.fix_scale));
             named_bar_sync(2 + w, 128);
         }
     }
@@ -403,37 +413,44 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     if (warp == 1) tmem_free<512>(tmem);
 }
 
-// Rescale each [n] profile to its exact expected total (1 per normalised head, averaged or
-// summed over the group): the bf16 tensor-core reductions leave ~1e-4 of drift, and
-// select_pattern requires |sum - 1| <= 1e-6 (sparsity.hpp:61). grid (hkv, 2).
-__global__ void renormalize_kernel(float* a_v, float* a_s, int n, double total) {
-    float* x = (blockIdx.y == 0 ? a_v : a_s) + static_cast<size_t>(blockIdx.x) * n;
-    double s = 0.0;
+// Fixed-point accumulators -> fp32 profiles rescaled to their exact expected total (1 per
+// normalised head, averaged or summed over the group): the bf16 tensor-core reductions leave
+// ~1e-4 of drift, and select_pattern requires |sum - 1| <= 1e-6 (sparsity.hpp:61). The sum
+// is an exact integer, so the result does not depend on the order of the atomics. grid (hkv, 2).
+__global__ void finalize_kernel(const unsigned long long* acc_v, const unsigned long long* acc_s, float* a_v,
+                                float* a_s, int n, double total) {
+    const unsigned long long* x = (blockIdx.y == 0 ? acc_v : acc_s) + static_cast<size_t>(blockIdx.x) * n;
+    float* y = (blockIdx.y == 0 ? a_v : a_s) + static_cast<size_t>(blockIdx.x) * n;
+    unsigned long long s = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
-    __shared__ double red[32];
+    __shared__ unsigned long long red[32];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
+        unsigned long long t = 0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
         red[0] = t;
     }
     __syncthreads();
-    const double f = red[0] > 0.0 ? total / red[0] : 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = static_cast<float>(x[i] * f);
+    const double f = red[0] > 0 ? total / static_cast<double>(red[0]) : 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = static_cast<float>(static_cast<double>(x[i]) * f);
 }
 
 size_t workspace_bytes(int n, int hq) {
-    // pass-1 scratch when the caller has no LSE: O [n, hq, 128] bf16 + LSE [hq, n]
-    return static_cast<size_t>(n) * hq * 128 * 2 + static_cast<size_t>(hq) * n * 4 + 1024;
+    // fixed-point accumulators (2 x [hq >= hkv, n] u64), then the pass-1 scratch when the
+    // caller has no LSE: O [n, hq, 128] bf16 + LSE [hq, n]
+    return 2 * static_cast<size_t>(hq) * n * 8 + static_cast<size_t>(n) * hq * 128 * 2 +
+           static_cast<size_t>(hq) * n * 4 + 1024;
 }
 
 cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     const float* lse = a.lse;
+    auto* acc = static_cast<unsigned long long*>(workspace);
+    uint8_t* scratch = static_cast<uint8_t*>(workspace) + 2 * static_cast<size_t>(a.hq) * a.n * 8;
     if (lse == nullptr) {
-        auto* o = static_cast<__nv_bfloat16*>(workspace);
-        float* l = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + static_cast<size_t>(a.n) * a.hq * 128 * 2);
+        auto* o = reinterpret_cast<__nv_bfloat16*>(scratch);
+        float* l = reinterpret_cast<float*>(scratch + static_cast<size_t>(a.n) * a.hq * 128 * 2);
         vsp_attn::AttnArgs d{a.q, a.k, a.k, o, l, a.n, a.hq, a.hkv, a.scale};
         cudaError_t e = vsp_attn::launch_dense(d, stream);
         if (e != cudaSuccess) return e;
@@ -449,8 +466,8 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
         !vsp_host::make_map_bf16(&p.map_k, a.k, 3, dk, sk, box))
         return cudaErrorInvalidValue;
     p.lse = lse;
-    p.a_v = a.a_v;
-    p.a_s = a.a_s;
+    p.acc_v = acc;
+    p.acc_s = acc + static_cast<size_t>(a.hkv) * a.n;
     p.n = a.n;
     p.hq = a.hq;
     p.hkv = a.hkv;
@@ -459,8 +476,12 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.scale = a.scale;
     p.out_scale = (a.normalized ? 1.0f / static_cast<float>(a.n) : 1.0f) *
                   (a.mean ? 1.0f / static_cast<float>(a.hq / a.hkv) : 1.0f);
-    cudaError_t e = cudaMemsetAsync(a.a_v, 0, sizeof(float) * a.hkv * a.n, stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.a_s, 0, sizeof(float) * a.hkv * a.n, stream);
+    {
+        const double tot = (a.normalized ? 1.0 : static_cast<double>(a.n)) *
+                           (a.mean ? 1.0 : static_cast<double>(a.hq / a.hkv));
+        p.fix_scale = std::ldexp(1.0, 52 - static_cast<int>(std::ceil(std::log2(std::max(tot, 1.0)))));
+    }
+    cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long) * a.hkv * a.n, stream);
     if (e != cudaSuccess) return e;
     static bool attr = false;
     if (!attr) {
@@ -472,7 +493,7 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     aggregate_kernel<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, stream>>>(p);
     const int grp = a.hq / a.hkv;
     const double total = (a.normalized ? 1.0 : static_cast<double>(a.n)) * (a.mean ? 1.0 : static_cast<double>(grp));
-    renormalize_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(a.a_v, a.a_s, a.n, total);
+    finalize_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(p.acc_v, p.acc_s, a.a_v, a.a_s, a.n, total);
     return cudaGetLastError();
 }
 

@@ -330,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_t + c * 32, u[c]);
                 tmem_wait_ld();
 #pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_reg_fence(u[c]);
+#pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (masked) {  // write the masked logits back so pass 2 is mask-free
 #pragma unroll
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     for (int c = 0; c < 4; ++c) {
                         uint32_t u[32];
                         tmem_ld32(o_t + c * 32, u);
-                        tmem_wait_ld();
+                        tmem_wait_ld(u);
 #pragma unroll
                         for (int t = 0; t < 32; ++t) u[t] = __float_as_uint(__uint_as_float(u[t]) * f);
                         tmem_st32(o_t + c * 32, u);
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             {
                 uint32_t u[2][32];  // ping-pong: chunk c+1 is loading while chunk c computes
                 tmem_ld32(s_t, u[0]);
-                tmem_wait_ld();
+                tmem_wait_ld(u[0]);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (c < 3) tmem_ld32(s_t + (c + 1) * 32, u[(c + 1) & 1]);
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         pk[t] = pack_bf16x2(e.x, e.y);
                     }
                     tmem_st16(s_t + c * 16, pk);
-                    if (c < 3) tmem_wait_ld();
+                    if (c < 3) tmem_wait_ld(u[(c + 1) & 1]);
                 }
             }
             l += ((lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y)) + ((lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y));
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         for (int c = 0; c < 4; ++c) {
             uint32_t u[32];
             tmem_ld32(o_t + c * 32, u);
-            tmem_wait_ld();
+            tmem_wait_ld(u);
             if (num_tiles == 0) {
 #pragma unroll
                 for (int t = 0; t < 32; ++t) u[t] = 0u;

@@ -589,15 +589,22 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
                           (flags & VSP_O_HEAD_MAJOR) != 0};
     vsp_attn::SparseArgs sa{i_v, k_v, i_s, k_s, cap};
     cudaError_t e = cudaSuccess;
-    for (int g = 0; g < hkv && e == cudaSuccess; ++g) {
-        if (!touched[g]) continue;
+    // score, select and plan each contiguous run of touched heads with one launch per kernel
+    for (int g = 0; g < hkv && e == cudaSuccess;) {
+        if (!touched[g]) {
+            ++g;
+            continue;
+        }
+        int cnt = 1;
+        while (g + cnt < hkv && touched[g + cnt]) ++cnt;
         vsp_indexer::Args ia{k, v, n, hkv, d_h, w_u, b_u, w_v, b_v, w_s, b_s, slash_mapping == VSP_SLASH_REVERSE,
-                             nullptr, nullptr, lv, ls, g, 1};
+                             nullptr, nullptr, lv, ls, g, cnt};
         e = vsp_indexer::launch(ia, ws_ix, st);
         if (e == cudaSuccess)
             e = vsp_select_k::launch_from_logits(lv, ls, a_v, a_s, n, hkv, budgets, i_v, k_v, i_s, k_s, cap, ws_sel,
-                                                 st, g, 1);
-        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g, 1, 1);
+                                                 st, g, cnt);
+        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g, cnt, 1);
+        g += cnt;
     }
     for (int u = 0; u < nunits && e == cudaSuccess; ++u)
         e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, units[u].g, 1, 2, units[u].qb_lo, units[u].qb_hi);

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                 tc_fence_after();
                 uint32_t ub[2][32];  // ping-pong: the next 32 columns load while these compute
                 tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / 2), ub[0]);
-                tmem_wait_ld();
+                tmem_wait_ld(ub[0]);
 #pragma unroll
                 for (int q = 0; q < kChunkN / 64; ++q) {
                     uint32_t* u = ub[q & 1];
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                         lv1 = ffma2(z1, make_float2(wv.z, wv.w), lv1);
                         ls1 = ffma2(z1, make_float2(ws.z, ws.w), ls1);
                     }
-                    if (q + 1 < kChunkN / 64) tmem_wait_ld();
+                    if (q + 1 < kChunkN / 64) tmem_wait_ld(ub[(q + 1) & 1]);
                 }
                 tc_fence_before();
                 __syncwarp();

@@ -108,6 +108,20 @@ VSP_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_s
 VSP_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 VSP_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 VSP_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// tcgen05.ld writes its destination registers asynchronously; nothing tells the compiler
+// that they only hold the TMEM data after tcgen05.wait::ld, so uses could be scheduled
+// before the wait. This re-defines the registers right after the wait ("+r" on each), which
+// pins every use of them below it.
+template <int N>
+VSP_DEVICE void tmem_reg_fence(uint32_t (&r)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i])::"memory");
+}
+template <int N>
+VSP_DEVICE void tmem_wait_ld(uint32_t (&r)[N]) {
+    tmem_wait_ld();
+    tmem_reg_fence(r);
+}
 
 // 32 lanes x 32 bit, 16 consecutive columns per thread (thread t <-> lane base+t).
 VSP_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {

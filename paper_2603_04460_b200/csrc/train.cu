@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
             uint32_t u[2][32];
             tmem_ld32(t_y + lane_base + part * 64, u[0]);
             tmem_ld32(t_y + lane_base + part * 64 + 32, u[1]);
-            tmem_wait_ld();
+            tmem_wait_ld(u[0]);
+            tmem_reg_fence(u[1]);
             if (i >= 1) mbar_wait(&sm.bw_done, (i - 1) & 1);  // tile i-1's MMAs have read dY / Z / DL
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                 for (int h2 = 0; h2 < 2; ++h2) {
                     uint32_t w[32];
                     tmem_ld32(t_dw + mh * 128 + part * 64 + h2 * 32 + lane_base, w);
-                    tmem_wait_ld();
+                    tmem_wait_ld(w);
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         reinterpret_cast<float4*>(dst + h2 * 32)[q] =
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                              : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]), "=r"(e[6]),
                                "=r"(e[7])
                              : "r"(t_dwv + lane_base));
-                tmem_wait_ld();
+                tmem_wait_ld(e);
                 p.part_wv[vo] = __uint_as_float(e[0]);
                 p.part_ws[vo] = __uint_as_float(e[1]);
             } else {
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                              : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]), "=r"(e[6]),
                                "=r"(e[7])
                              : "r"(t_db + lane_base));
-                tmem_wait_ld();
+                tmem_wait_ld(e);
                 p.part_bu[vo] = __uint_as_float(e[0]);
             }
         }

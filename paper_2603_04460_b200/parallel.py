@@ -121,30 +121,50 @@ class VspComm:
             pass
 
 
-def balanced_units(cost, world: int, cta_overhead: float = 2.0) -> List[List[Tuple[int, int, int]]]:
-    """Cut the (KV head, query block) grid, walked head-major, into `world` contiguous runs of
-    near-equal cost. cost: [hkv, num_qb] predicted tiles per (head, block) (e.g. from
-    sparse_tile_counts on a calibration prompt); each block also pays `cta_overhead`
-    tile-equivalents. Returns per rank a list of units (g, qb_lo, qb_hi)."""
+def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: float = 2500.0
+                   ) -> List[List[Tuple[int, int, int]]]:
+    """Cut the (KV head, query block) grid, walked head-major, into `world` contiguous runs
+    minimising the most expensive run. cost: [hkv, num_qb] predicted tiles per (head, block)
+    (e.g. sparse_tile_counts on a calibration prompt); every block also pays `cta_overhead`
+    tile-equivalents and every head a run touches pays `head_overhead` (its scoring,
+    selection and planning). Smallest feasible bound by bisection with a greedy fill.
+    Returns per rank a list of units (g, qb_lo, qb_hi)."""
     rows = [[float(x) + cta_overhead for x in r] for r in (cost.tolist() if hasattr(cost, "tolist") else cost)]
     hkv, nqb = len(rows), len(rows[0])
-    total = sum(sum(r) for r in rows)
     flat = [(g, b, rows[g][b]) for g in range(hkv) for b in range(nqb)]
-    out: List[List[Tuple[int, int, int]]] = [[] for _ in range(world)]
-    acc, r = 0.0, 0
-    for g, b, c in flat:
-        # move to the next rank once this one reached its share (midpoint rule on the block)
-        while r < world - 1 and acc + 0.5 * c > total * (r + 1) / world:
-            r += 1
-        units = out[r]
-        if units and units[-1][0] == g and units[-1][2] == b:
-            units[-1] = (g, units[-1][1], b + 1)
+
+    def fill(bound: float):
+        out: List[List[Tuple[int, int, int]]] = [[]]
+        acc, cur_g = 0.0, -1
+        for g, b, c in flat:
+            add = c + (head_overhead if g != cur_g else 0.0)
+            if out[-1] and acc + add > bound:
+                out.append([])
+                acc, cur_g = 0.0, -1
+                add = c + head_overhead
+            units = out[-1]
+            if units and units[-1][0] == g and units[-1][2] == b:
+                units[-1] = (g, units[-1][1], b + 1)
+            else:
+                units.append((g, b, b + 1))
+            acc += add
+            cur_g = g
+        return out
+
+    lo = max(c for _, _, c in flat) + head_overhead
+    hi = sum(c for _, _, c in flat) + head_overhead * hkv
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if len(fill(mid)) <= world:
+            hi = mid
         else:
-            units.append((g, b, b + 1))
-        acc += c
-    return out
+            lo = mid
+    out = fill(hi)
+    return out + [[] for _ in range(world - len(out))]
 
 
-def units_cost(units, cost, cta_overhead: float = 2.0) -> float:
+def units_cost(units, cost, cta_overhead: float = 2.0, head_overhead: float = 0.0) -> float:
     rows = cost.tolist() if hasattr(cost, "tolist") else cost
-    return sum(float(rows[g][b]) + cta_overhead for g, lo, hi in units for b in range(lo, hi))
+    heads = {g for g, _, _ in units}
+    return (sum(float(rows[g][b]) + cta_overhead for g, lo, hi in units for b in range(lo, hi))
+            + head_overhead * len(heads))

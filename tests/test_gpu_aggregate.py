@@ -94,3 +94,15 @@ def test_aggregate_long_vs_torch(vsp):
     err_v = (a_v[0] - vert).abs()
     err_s = (a_s[0] - sl).abs()
     assert (err_v <= 2e-2 * vert + 2e-6).all() and (err_s <= 2e-2 * sl + 2e-6).all()
+
+
+def test_aggregate_is_bit_reproducible(vsp):
+    """Fixed-point integer accumulation: repeated runs give identical bits (the distillation
+    targets, and through them the calibrated budgets, must not depend on atomic order)."""
+    n, hq, hkv = 3000, 8, 2
+    q, k, _ = qkv(n, hq, hkv, seed=17, scale=0.7)
+    a0, s0 = vsp.aggregate_streaming(q, k)
+    for _ in range(3):
+        a1, s1 = vsp.aggregate_streaming(q, k)
+        torch.cuda.synchronize()
+        assert torch.equal(a0, a1) and torch.equal(s0, s1)

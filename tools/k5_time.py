@@ -1,6 +1,6 @@
 """Time K5 pass 2 alone (CUDA events) at a given n, 32Q/8KV."""
 import os, sys, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("VSP_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2603_04460_b200 as vsp
 from paper_2603_04460_b200.synth import planted_layer
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768

@@ -1,0 +1,83 @@
+"""Per-rank step times of the two multi-GPU splits of the 128k layer, measured on ONE B200.
+
+Each rank of an N-GPU job runs independent work (no collective on the data path), so the
+N-GPU step time is the max over ranks of that rank's own step. This tool times every rank's
+share on the single GPU (CUDA events, warm, same clocks) for N = 1, 2, 4, 8 and reports the
+predicted step (max over ranks) and tokens/s for
+  heads    : KV-head sharding (each rank vs_prefill on Hkv/N heads, the north-star split)
+  balanced : cost-balanced (KV head, query-block) units (vs_prefill_units, replicated inputs)
+The cost table of the balanced split comes from a separate validation prompt (not the timed
+one). Prints one JSON line.
+
+    python tools/scaling_sim.py [--n 131072] [bench.py options]
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2603_04460_b200 as vsp  # noqa: E402
+from paper_2603_04460_b200 import parallel  # noqa: E402
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    args = bench.parse()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    params, budget, _ = bench.prepare_indexer(args, dev, 0, 1)
+    n, hq, hkv = args.n, args.hq, args.hkv
+    # cost table from a validation prompt
+    qv, kv_, vv = bench.synth_layer(args, dev, seed=args.seed + 201)
+    a_v, a_s = vsp.indexer_forward(kv_, vv, params)
+    pat = vsp.select_pattern(a_v, a_s, budget)
+    vsp.sparse_attention(qv, kv_, vv, pat, validate=False)
+    cost = vsp.sparse_tile_counts(n, hkv, pat.i_v.shape[1], dev)
+    del qv, kv_, vv
+    q, k, v = bench.synth_layer(args, dev)
+    o_full = torch.empty(hq, n, 128, dtype=q.dtype, device=dev)
+    lse_full = torch.empty(hq, n, device=dev)
+    out = {"n": n, "hq": hq, "hkv": hkv, "tiles_per_head": cost.sum(1).tolist(), "splits": {}}
+    for world in (1, 2, 4, 8):
+        # heads: rank r = vs_prefill on its KV heads
+        t_heads = []
+        for r in range(world):
+            qs, ks, vs = (parallel.shard_heads(t, r, world) for t in (q, k, v))
+            ps = vsp.IndexerParams(*(parallel.shard_heads(t, r, world, dim=0)
+                                     for t in (params.w_u, params.b_u, params.w_v, params.b_v, params.w_s, params.b_s)))
+            bs = budget[r * hkv // world:(r + 1) * hkv // world]
+            slab, lslab = parallel.head_slab(o_full, r, world), parallel.head_slab(lse_full, r, world)
+            t_heads.append(timed(lambda: vsp.vs_prefill(qs, ks, vs, ps, bs, out=slab, lse=lslab, head_major=True)))
+            del qs, ks, vs
+        # balanced: rank r = vs_prefill_units on its units (full inputs)
+        units = parallel.balanced_units(cost, world)
+        t_bal = [timed(lambda u=u: vsp.vs_prefill_units(q, k, v, params, budget, u, out=o_full, lse=lse_full))
+                 for u in units]
+        out["splits"][world] = {
+            "heads_ms_per_rank": [round(x, 3) for x in t_heads], "heads_step_ms": round(max(t_heads), 3),
+            "heads_tok_s": n / (max(t_heads) * 1e-3),
+            "balanced_ms_per_rank": [round(x, 3) for x in t_bal], "balanced_step_ms": round(max(t_bal), 3),
+            "balanced_tok_s": n / (max(t_bal) * 1e-3), "balanced_units": units}
+    base_h = out["splits"][1]["heads_step_ms"]
+    for world, s in out["splits"].items():
+        s["heads_speedup"] = round(base_h / s["heads_step_ms"], 2)
+        s["balanced_speedup"] = round(base_h / s["balanced_step_ms"], 2)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
