@@ -52,11 +52,13 @@ def parse():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d-h", type=int, default=1024)
     ap.add_argument("--indexer", choices=["distilled", "random"], default="distilled")
-    ap.add_argument("--train-prompts", type=int, default=4)
-    ap.add_argument("--val-prompts", type=int, default=4)
-    ap.add_argument("--distill-steps", type=int, default=300)
+    ap.add_argument("--train-prompts", type=int, default=12)
+    ap.add_argument("--val-prompts", type=int, default=6)
+    ap.add_argument("--calib-aggregate", choices=["mean", "worst"], default="mean",
+                    help="score calibration grid points by the mean or the worst case over validation prompts")
+    ap.add_argument("--distill-steps", type=int, default=900)
     ap.add_argument("--recall-target", type=float, default=0.9)
-    ap.add_argument("--calib-margin", type=float, default=0.015,
+    ap.add_argument("--calib-margin", type=float, default=0.035,
                     help="calibrate the budget for recall_target + margin on the validation prompt")
     ap.add_argument("--tau-step", type=float, default=0.1,
                     help="grid step of the per-head (tau_v, tau_s) calibration over (0, 1)")
@@ -208,13 +210,14 @@ def prepare_indexer(args, device, rank, world):
             vals.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
             del q, k, v
         taus = tuple(round(args.tau_step * i, 4) for i in range(1, int(round(1 / args.tau_step))))
-        budget, pt = calibrate.calibrate_budget(vals, params=params, taus=taus,
+        budget, pt = calibrate.calibrate_budget(vals, params=params, taus=taus, aggregate=args.calib_aggregate,
                                                 recall_target=args.recall_target + args.calib_margin,
                                                 min_budget=args.min_budget,
                                                 max_budget=None if args.max_budget < 0 else args.max_budget)
         info["budget_source"] = (f"per-KV-head (tau_v, tau_s) on a {args.tau_step} grid, calibrated on "
                                  f"{args.val_prompts} validation prompts "
-                                 f"(worst case) for mean recall >= {args.recall_target} + {args.calib_margin}: "
+                                 f"({args.calib_aggregate}, cliff-weighted tiles) for mean recall >= "
+                                 f"{args.recall_target} + {args.calib_margin}: "
                                  f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
         del vals
     if args.indexer == "distilled":

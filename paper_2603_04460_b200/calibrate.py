@@ -49,14 +49,16 @@ def train_indexer(prompts: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tens
 
 def calibrate_budget(q, k=None, v=None, params: IndexerParams = None, recall_target: float = 0.9,
                      taus: Sequence[float] = DEFAULT_TAUS, min_budget: int = 1,
-                     max_budget: Optional[int] = None) -> Tuple[List[BudgetConfig], dict]:
+                     max_budget: Optional[int] = None, cliff_weight: float = 0.25,
+                     aggregate: str = "mean") -> Tuple[List[BudgetConfig], dict]:
     """Per KV head, grid over (tau_v, tau_s); then pick one grid point per head so that the
     total KV-tile count is minimal while the MEAN recall over heads reaches the target (the
     paper's accuracy target is an average; heads trade budget). Solved with a Lagrangian
     sweep: for multiplier lam each head minimises tiles - lam * recall, and lam is bisected
     to the cheapest feasible point. Returns one BudgetConfig per KV head (select_pattern
     accepts per-head budgets) and a summary. With several validation prompts each grid point
-    is scored by its worst case (most tiles, least recall) over them."""
+    is scored by the mean (aggregate="mean") or the worst case (most tiles, least recall) over
+    them; the tile cost also weighs the next-higher grid neighbours by cliff_weight (below)."""
     prompts = [(q, k, v)] if torch.is_tensor(q) else list(q)  # one prompt or a list of them
     n, hq, d = prompts[0][0].shape
     hkv = prompts[0][1].shape[1]
@@ -75,10 +77,31 @@ def calibrate_budget(q, k=None, v=None, params: IndexerParams = None, recall_tar
             _, dense_tiles, per_head = sparse_tile_stats(n, hkv, pat.i_v.shape[1], pq.device, per_head=True)
             rec_q = attention_recall(lse, lse_d).view(hkv, grp).mean(dim=1).tolist()
             for g in range(hkv):
-                w = worst.setdefault((g, gi), [0, 1.0])
+                w = worst.setdefault((g, gi), [0, 1.0, 0.0, 0.0, 0])
                 w[0] = max(w[0], per_head[g])
                 w[1] = min(w[1], rec_q[g])
-    points = [[(worst[(g, gi)][0], worst[(g, gi)][1], tv, ts) for gi, (tv, ts) in enumerate(grid)]
+                w[2] += per_head[g]
+                w[3] += rec_q[g]
+                w[4] += 1
+    if aggregate == "mean":  # expected tiles and recall over the validation prompts
+        for w in worst.values():
+            w[0], w[1] = w[2] / w[4], w[3] / w[4]
+    # Cliff-aware cost: a cumulative threshold just below a plateau of the score mass is
+    # fragile — on another prompt the same tau can need thousands more indices. A grid point
+    # is charged its expected tile count if, with probability cliff_weight per direction, the
+    # prompt shifts the mass by one grid step (its next-higher neighbour's worst count).
+    ti = {t: i for i, t in enumerate(taus)}
+    gidx = {(tv, ts): gi for gi, (tv, ts) in enumerate(grid)}
+
+    def cost(g, tv, ts):
+        base = worst[(g, gidx[(tv, ts)])][0]
+        if not cliff_weight:
+            return base
+        up_v = worst[(g, gidx[(taus[min(ti[tv] + 1, len(taus) - 1)], ts)])][0]
+        up_s = worst[(g, gidx[(tv, taus[min(ti[ts] + 1, len(taus) - 1)])])][0]
+        return base + cliff_weight * (max(up_v - base, 0) + max(up_s - base, 0))
+
+    points = [[(cost(g, tv, ts), worst[(g, gi)][1], tv, ts) for gi, (tv, ts) in enumerate(grid)]
               for g in range(hkv)]
 
     def pick(lam):
@@ -102,6 +125,6 @@ def calibrate_budget(q, k=None, v=None, params: IndexerParams = None, recall_tar
         chosen = [max(pts, key=lambda p: (p[1], -p[0])) for pts in points]
     budgets = [BudgetConfig(c[2], c[3], min_budget, max_budget) for c in chosen]
     summary = dict(recall=sum(c[1] for c in chosen) / hkv,
-                   tile_density=sum(c[0] for c in chosen) / dense_tiles,
+                   tile_density=sum(worst[(g, gidx[(c[2], c[3])])][0] for g, c in enumerate(chosen)) / dense_tiles,
                    per_head=[dict(tau_v=c[2], tau_s=c[3], recall=round(c[1], 4)) for c in chosen])
     return budgets, summary

@@ -1,7 +1,7 @@
 """Extract K3's DRAM traffic per launch from an `ncu --set full` capture of bench.py's timed
 region and write profiles/k3_traffic.json (read by bench.py's roofline.traffic).
 
-    ncu --section MemoryWorkloadAnalysis --section SpeedOfLight --clock-control none --nvtx --nvtx-include "timed/" \
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx --nvtx-include "timed/" \
         -k regex:attn_fwd_kernel -c 2 -o gpurun_out/prof_k3_traffic python bench.py --steps 1 --warmup 1 --no-e2e \
         --no-cpu-baseline
     python tools/k3_traffic.py gpurun_out/prof_k3_bench.ncu-rep
