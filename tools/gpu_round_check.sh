@@ -1,0 +1,10 @@
+# Full round check on one B200: GPU tests, smoke, the default bench line, the launch list and
+# K3 traffic of the bench's timed region. Outputs under gpurun_out/.
+set -x
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo TESTS_EXIT=$? >> gpurun_out/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo SMOKE_EXIT=$? >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo BENCH_EXIT=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/launch_bench.log 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx --nvtx-include "timed/" -k regex:attn_fwd_kernel -c 2 -o gpurun_out/prof_k3_traffic python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/prof_k3t.log 2>&1
+tail -3 gpurun_out/gpu_tests.log; tail -2 gpurun_out/smoke.log
