@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", choices=["auto", "heads", "balanced"], default="auto",
+                    help="multi-GPU split: KV heads (north star), or cost-balanced (KV head, query-block) "
+                         "units with replicated inputs; auto = heads at N=1, balanced at N>1")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
     ap.add_argument("--e2e-heads-per-chunk", type=int, default=1)
@@ -307,29 +310,47 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    assert args.hkv % world == 0, "KV heads must divide across ranks"
+    balanced = args.shard == "balanced" or (args.shard == "auto" and world > 1)
+    assert balanced or args.hkv % world == 0, "KV heads must divide across ranks"
     import paper_2603_04460_b200 as vsp
+    from paper_2603_04460_b200 import parallel
 
     n = args.n
-    params, budget, prep_info = prepare_indexer(args, dev, rank, world)
+    # balanced: every rank holds the whole layer and all heads' indexers/budgets (identical,
+    # deterministic preparation) and attends its cost-balanced (head, query-block) units
+    srank, sworld = (0, 1) if balanced else (rank, world)
+    params, budget, prep_info = prepare_indexer(args, dev, srank, sworld)
+    units = None
+    if balanced:
+        # static cost table: per (head, block) tiles of a validation prompt (not the timed one)
+        qv, kv_, vv = synth_layer(args, dev, seed=args.seed + 201)
+        a_v, a_s = vsp.indexer_forward(kv_, vv, params)
+        pat_v = vsp.select_pattern(a_v, a_s, budget)
+        vsp.sparse_attention(qv, kv_, vv, pat_v, validate=False)
+        cost = vsp.sparse_tile_counts(n, args.hkv, pat_v.i_v.shape[1], dev)
+        del qv, kv_, vv, a_v, a_s, pat_v
+        units = parallel.balanced_units(cost, world)[rank]
     q_full, k_full, v_full = synth_layer(args, dev)
-    hq_r, hkv_r = args.hq // world, args.hkv // world
-    q = shard(q_full, rank, world, 1)
-    k = shard(k_full, rank, world, 1)
-    v = shard(v_full, rank, world, 1)
-    if world > 1:
+    hq_r, hkv_r = args.hq // sworld, args.hkv // sworld
+    q = shard(q_full, srank, sworld, 1)
+    k = shard(k_full, srank, sworld, 1)
+    v = shard(v_full, srank, sworld, 1)
+    if world > 1 and not balanced:
         del q_full, k_full, v_full
     # O is written head-major straight into this rank's slab of the full [Hq, n, d] output
     # (VSP_O_HEAD_MAJOR): the slab is the in-place all-gather send buffer (parallel.py)
-    from paper_2603_04460_b200 import parallel
     o_full = torch.empty(args.hq, n, 128, dtype=q.dtype, device=dev)
     lse_full = torch.empty(args.hq, n, device=dev)
-    o = parallel.head_slab(o_full, rank, world)
-    lse = parallel.head_slab(lse_full, rank, world)
+    o = parallel.head_slab(o_full, srank, sworld)
+    lse = parallel.head_slab(lse_full, srank, sworld)
 
     hpc = args.heads_per_chunk
 
     def step():
+        if balanced:
+            # one C-ABI call (vsp_vs_prefill_units): scoring/selection/planning of the heads this
+            # rank's units touch, then attention of exactly its units
+            return vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
         # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3, pipelined over KV-head chunks
         _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse, head_major=True)
         return pat
@@ -408,7 +429,7 @@ def main():
     ks_list = pat.k_s.cpu().tolist()
 
     allgather_ms = None
-    if world > 1:
+    if world > 1 and not balanced:
         # one in-place ncclAllGather of the head-major slabs (O and LSE) through the C ABI
         comm = parallel.VspComm(dev)
         allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
@@ -420,10 +441,28 @@ def main():
         qh = q.cpu().pin_memory()
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
-        oh_ = torch.empty(q.shape, dtype=q.dtype).pin_memory()
-        lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+        if balanced:  # head-major host output; only this rank's unit regions come back
+            oh_ = torch.empty(o_full.shape, dtype=q.dtype).pin_memory()
+            lse_h = torch.empty(lse_full.shape, dtype=lse.dtype).pin_memory()
+        else:
+            oh_ = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+            lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+        grp_ = args.hq // args.hkv
+        d2h_units = sum(grp_ * (hi - lo) * 128 * (128 * 2 + 4) for _, lo, hi in (units or []))
 
         def e2e_step():
+            if balanced:
+                # replicated inputs: H2D of the whole layer, the rank's units, D2H of its regions
+                q.copy_(qh, non_blocking=True)
+                k.copy_(kh, non_blocking=True)
+                v.copy_(vh, non_blocking=True)
+                vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
+                for g_, lo, hi in units:
+                    hs = slice(g_ * grp_, (g_ + 1) * grp_)
+                    rs = slice(lo * 128, min(hi * 128, n))
+                    oh_[hs, rs].copy_(o_full[hs, rs], non_blocking=True)
+                    lse_h[hs, rs].copy_(lse_full[hs, rs], non_blocking=True)
+                return
             # one host-buffer C-ABI call: H2D of Q/K/V, K1->K2->K3, D2H of O and LSE, pipelined per chunk
             vsp.vs_prefill_host(qh, kh, vh, params, budget, heads_per_chunk=args.e2e_heads_per_chunk,
                                 out=oh_, lse=lse_h, device=dev)
@@ -442,8 +481,10 @@ def main():
             torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": n / (float(e2e_ms.item()) * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2),
-               "d2h_bytes_per_step": int(oh_.numel() * 2 + lse_h.numel() * 4), "ms_per_step": float(e2e_ms.item()),
-               "api": "vsp_vs_prefill_host (pinned host Q/K/V in, host O/LSE out)",
+               "d2h_bytes_per_step": int(d2h_units if balanced else oh_.numel() * 2 + lse_h.numel() * 4),
+               "ms_per_step": float(e2e_ms.item()),
+               "api": ("vs_prefill_units (pinned host Q/K/V in, this rank's O/LSE regions out)" if balanced else
+                       "vsp_vs_prefill_host (pinned host Q/K/V in, host O/LSE out)"),
                "heads_per_chunk": args.e2e_heads_per_chunk}
 
     cpu = None
@@ -466,7 +507,8 @@ def main():
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "config[2]: LLaMA-3.1-8B attention geometry single layer, KV-head sharded",
+            "config": {"workload": ("config[2]: LLaMA-3.1-8B attention geometry single layer, "
+                                    + ("cost-balanced (KV head, query-block) units" if balanced else "KV-head sharded")),
                        "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
                        "indexer": prep_info["indexer"],
                        "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
@@ -474,7 +516,10 @@ def main():
                                   "max": args.max_budget, "source": prep_info["budget_source"]},
                        "prep": {k_: v_ for k_, v_ in prep_info.items() if k_ not in ("indexer", "budget_source")},
                        "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
-                                 "> L2 so no flush between steps", "parallelism": f"kv-head shard x{world}"},
+                                 "> L2 so no flush between steps",
+                       "parallelism": (f"balanced units x{world} (replicated inputs, static cost table from a "
+                                       f"validation prompt; this rank: {units})" if balanced
+                                       else f"kv-head shard x{world}")},
             "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,
             "unfused_ms": ms_unfused, "heads_per_chunk": hpc,
             "indexer_ms": ms_indexer, "select_ms": ms_select, "recall": recall,

@@ -42,6 +42,10 @@ def main():
     for name in extra["--variants"].split(","):
         if name == "unfused":
             fns[name] = unfused
+        elif name == "units":  # vsp_vs_prefill_units over all heads: scoring, then one K3 launch per head
+            o_h = torch.empty(args.hq, args.n, 128, dtype=q.dtype, device=dev)
+            all_units = [(g, 0, (args.n + 127) // 128) for g in range(args.hkv)]
+            fns[name] = lambda o_h=o_h, u=all_units: vsp.vs_prefill_units(q, k, v, params, budget, u, out=o_h, lse=lse)
         elif name == "attn":
             a_v, a_s = vsp.indexer_forward(k, v, params)
             pat = vsp.select_pattern(a_v, a_s, budget)
