@@ -305,11 +305,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run N ranks on fewer GPUs (e.g. the N>1 code path on a 1-GPU box) with gloo
+    if os.environ.get("VSP_BENCH_DEVICES"):
+        local = local % int(os.environ["VSP_BENCH_DEVICES"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("VSP_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     balanced = args.shard == "balanced" or (args.shard == "auto" and world > 1)
     assert balanced or args.hkv % world == 0, "KV heads must divide across ranks"
     import paper_2603_04460_b200 as vsp
