@@ -105,3 +105,26 @@ def test_balanced_units_reassemble_the_layer_bit_exact(vsp, world):
         for g in {u[0] for u in units[r]}:
             assert pat.lists(g) == pat_ref.lists(g)
     assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)
+
+
+def test_units_api_errors_and_empty_units(vsp):
+    n, hq, hkv = 600, 4, 2
+    q, k, v = qkv(n, hq, hkv, seed=24)
+    p = _params(vsp, hkv, 6)
+    budgets = [vsp.BudgetConfig(0.5, 0.5, 1, None)] * hkv
+    o = torch.zeros(hq, n, 128, dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros(hq, n, device="cuda")
+    with pytest.raises(vsp.VspError, match="unit out of range"):
+        vsp.vs_prefill_units(q, k, v, p, budgets, [(hkv, 0, 1)], out=o, lse=lse)
+    with pytest.raises(vsp.VspError, match="unit out of range"):
+        vsp.vs_prefill_units(q, k, v, p, budgets, [(0, 3, 2)], out=o, lse=lse)
+    with pytest.raises(vsp.VspError, match="head-major"):
+        vsp.vs_prefill_units(q, k, v, p, budgets, [(0, 0, 1)], out=torch.empty_like(q), lse=lse)
+    # no units: nothing written
+    vsp.vs_prefill_units(q, k, v, p, budgets, [], out=o, lse=lse)
+    torch.cuda.synchronize()
+    assert not o.any() and not lse.any()
+    # an empty block range is a no-op for that unit
+    vsp.vs_prefill_units(q, k, v, p, budgets, [(1, 2, 2)], out=o, lse=lse)
+    torch.cuda.synchronize()
+    assert not o.any()
