@@ -355,7 +355,7 @@ def main():
             # one C-ABI call (vsp_vs_prefill_units): scoring/selection/planning of the heads this
             # rank's units touch, then attention of exactly its units
             return vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
-        # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3, pipelined over KV-head chunks
+        # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3 (automatic schedule unless --heads-per-chunk)
         _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse, head_major=True)
         return pat
 

@@ -163,10 +163,10 @@ VSP_API int vsp_adamw_step(vsp_ctx* ctx, float* params, const float* grads, floa
                            void* stream);
 
 /* ---- the whole VS-prefill layer: K1 -> K2 -> K3 in one call ------------------------
- * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads, but
- * pipelined over KV-head chunks of `heads_per_chunk` heads (0 = automatic: two halves): the scoring, selection and
- * tile planning of chunk c+1 run on a high-priority side stream while chunk c's attention
- * runs on `stream`. a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
+ * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads. With
+ * heads_per_chunk = 0 (automatic: one chunk) everything runs in order on `stream`; with
+ * KV-head chunks of `heads_per_chunk` heads the scoring, selection and tile planning of
+ * chunk c+1 run on a high-priority side stream while chunk c's attention runs on `stream`. a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
  * individual calls). Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp
  * :154-185) on the device. */
 VSP_API size_t vsp_vs_prefill_workspace_size(int n, int hkv, int d_h, int cap);

@@ -386,7 +386,8 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
                mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
                lse: Optional[torch.Tensor] = None, head_major: bool = False):
     """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
-    indexer -> selection -> sparse attention, pipelined over KV-head chunks so that the
+    indexer -> selection -> sparse attention; heads_per_chunk=0 runs them in order on the
+    current stream, heads_per_chunk>0 pipelines KV-head chunks so that the
     scoring/selection/planning of chunk c+1 overlaps chunk c's attention. Mirrors
     `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
     Same results as indexer_forward + select_pattern + sparse_attention.

@@ -22,7 +22,9 @@ struct __align__(64) AttnParams {
     const uint32_t* sbits;
     int list_stride;
     int pair0, npairs;   // Q-head pairs [pair0, pair0 + npairs) handled by this launch
-    int qb_hi;           // query blocks [qb_hi - gridDim.x / npairs, qb_hi) handled by this launch
+    int qb_hi;           // query blocks [qb_hi - items / npairs, qb_hi) handled by this launch
+    int items;           // work items (query block, head pair), pulled by persistent CTAs
+    int* work;           // {next item - gridDim.x, CTAs done}: zero at launch, reset by the last CTA
     int bm_words;
     int n, hq, hkv;
     float scale;

@@ -6,9 +6,10 @@
 //   vsp::sparse_attention     (reference attention.hpp:150-194) + merge_row_columns
 //                             (merge.hpp:18-56)                  -> sparse mode
 //
-// CTA = one 128-row query block x TWO Q heads of the same KV group (GQA: both Q tiles
-// share every K/V tile). 12 warps:
-//   warp 0      TMA producer (Q once, then K/V tiles through a ring)
+// Work item = one 128-row query block x TWO Q heads of the same KV group (GQA: both Q
+// tiles share every K/V tile). Persistent grid (one CTA per SM) pulling items heaviest
+// first from a global counter. 12 warps:
+//   warp 0      TMA producer (item fetch, Q per item, then K/V tiles through a ring)
 //   warp 1      MMA issuer: S_h = Q_h K^T (SS), O_h += P_h V (TS, P read from TMEM)
 //   warps 4-7   softmax/epilogue for Q tile 0 (thread = query row = TMEM lane)
 //   warps 8-11  softmax/epilogue for Q tile 1
@@ -49,12 +50,24 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+constexpr int kItemRing = 2;
+constexpr int kItemConsumers = 9;  // MMA warp + 8 softmax warps
+
 struct Smem {
-    uint64_t bar_q;
+    uint64_t q_full, q_free;                  // Q tiles of the current work item
     uint64_t k_full[kNumK], k_empty[kNumK];
     uint64_t v_full[kNumV], v_empty[kNumV];
     uint64_t s_full[2], p_full[2], o_done[2];
+    uint64_t o_free[2];                       // epilogue has read O_w (next item may PV into it)
+    uint64_t item_full[kItemRing], item_empty[kItemRing];
+    int item[kItemRing];                      // work item index, -1 = no more work
     uint32_t tmem_base;
+};
+
+// Work item it (heaviest query blocks first: causal work grows with the block index).
+struct Item {
+    int qb, h0, g, num_tiles, vcnt0;
+    const int* tiles;
 };
 
 // Bits [start, start+128) of a bitmap as four words, word k bit b <-> bit start+32k+b.
@@ -83,33 +96,44 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     uint8_t* sV = sK + kNumK * kTileBytes;               // kNumV tiles
     __shared__ Smem sm;
 
-    const int heads_per_pair = p.npairs;  // Q-head pairs in this launch, starting at p.pair0
     const int num_qb = (p.n + kBlock - 1) / kBlock;
-    // heaviest query blocks first (causal work grows with the block index)
-    const int qb = p.qb_hi - 1 - static_cast<int>(blockIdx.x) / heads_per_pair;
-    const int pair = p.pair0 + static_cast<int>(blockIdx.x) % heads_per_pair;
-    const int h0 = 2 * pair;
-    const int g = h0 / (p.hq / p.hkv);
-    const int i0 = qb * kBlock;
-
-    // ---- tile list
-    int num_tiles;
-    const int* tiles = nullptr;
-    int vcnt0 = 0;
-    if constexpr (kSparse) {
-        const int* hdr = p.tile_lists + (static_cast<size_t>(g) * num_qb + qb) * p.list_stride;
-        num_tiles = hdr[0];
-        vcnt0 = hdr[1];
-        tiles = hdr + 2;
-    } else {
-        num_tiles = qb + 1;
-    }
+    // Persistent: one CTA per SM pulls work items (heavy first) from a global counter; the
+    // producer publishes each item index through a two-slot smem ring, so the next item's Q
+    // load and first S MMA overlap this item's last PV and epilogue, and the fetch order keeps
+    // the dynamic load balance of a one-CTA-per-item grid.
+    auto item = [&](int it) {
+        Item x;
+        x.qb = p.qb_hi - 1 - it / p.npairs;
+        x.h0 = 2 * (p.pair0 + it % p.npairs);
+        x.g = x.h0 / (p.hq / p.hkv);
+        x.vcnt0 = 0;
+        x.tiles = nullptr;
+        if constexpr (kSparse) {
+            const int* hdr = p.tile_lists + (static_cast<size_t>(x.g) * num_qb + x.qb) * p.list_stride;
+            x.num_tiles = hdr[0];
+            x.vcnt0 = hdr[1];
+            x.tiles = hdr + 2;
+        } else {
+            x.num_tiles = x.qb + 1;
+        }
+        return x;
+    };
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    // consumer side of the item ring (MMA warp and softmax warps): item of round n_it, or -1
+    auto next_item = [&](int n_it) {
+        const int slot = n_it % kItemRing;
+        mbar_wait(&sm.item_full[slot], (n_it / kItemRing) & 1);
+        const int it = *reinterpret_cast<volatile int*>(&sm.item[slot]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.item_empty[slot]);
+        return it;
+    };
 
     if (warp == 0 && lane == 0) {
-        mbar_init(&sm.bar_q, 1);
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_free, 1);
         for (int s = 0; s < kNumK; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.k_empty[s], 1);
@@ -118,10 +142,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.v_empty[s], 1);
         }
+        for (int s = 0; s < kItemRing; ++s) {
+            mbar_init(&sm.item_full[s], 1);
+            mbar_init(&sm.item_empty[s], kItemConsumers);
+        }
         for (int w = 0; w < 2; ++w) {
             mbar_init(&sm.s_full[w], 1);
             mbar_init(&sm.p_full[w], 4);
             mbar_init(&sm.o_done[w], 1);
+            mbar_init(&sm.o_free[w], 4);
         }
         fence_barrier_init();
     }
@@ -130,7 +159,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    // register split: the producer/MMA warpgroup needs few, the softmax warpgroups hold a
 
     if (warp == 0) {
         // =========================== TMA producer (warp-uniform loop, elected issuer)
@@ -142,36 +170,56 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 tma_prefetch_desc(&p.map_kv);
                 tma_prefetch_desc(&p.map_vv);
             }
-            mbar_arrive_expect_tx(&sm.bar_q, 2 * kTileBytes);
-            for (int w = 0; w < 2; ++w)
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(sQ + w * kTileBytes + hf * kHalfBytes, &p.map_q, &sm.bar_q, hf * 64,
-                                h0 + w, i0);
         }
         __syncwarp();
-        for (int j = 0; j < num_tiles; ++j) {
-            int e = kSparse ? __ldg(tiles + j) : j * kBlock;
-            const bool gathered = kSparse && e < 0;
-            const int row = gathered ? (-e - 1) * kBlock : e;
-            const CUtensorMap* mk_ = gathered ? &p.map_kv : &p.map_k;
-            const CUtensorMap* mv_ = gathered ? &p.map_vv : &p.map_v;
-            const int c1 = gathered ? row : g, c2 = gathered ? g : row;
-            const int ks = j % kNumK;
-            if (j >= kNumK) mbar_wait(&sm.k_empty[ks], ((j / kNumK) & 1) ^ 1);
+        int gj = 0;  // K/V ring position, continuous across items
+        for (int n_it = 0;; ++n_it) {
+            const int slot = n_it % kItemRing;
+            if (n_it >= kItemRing) mbar_wait(&sm.item_empty[slot], ((n_it / kItemRing) - 1) & 1);
+            int it = 0;
+            if (lane == 0) {
+                it = n_it == 0 ? static_cast<int>(blockIdx.x) : atomicAdd(p.work + 0, 1) + static_cast<int>(gridDim.x);
+                if (it >= p.items) it = -1;
+                sm.item[slot] = it;
+                mbar_arrive(&sm.item_full[slot]);  // release: the item index is visible to waiters
+            }
+            it = __shfl_sync(0xffffffffu, it, 0);
+            if (it < 0) break;
+            const Item x = item(it);
+            // the previous item's last S MMA has read its Q tiles
+            if (n_it > 0) mbar_wait(&sm.q_free, (n_it - 1) & 1);
             if (elect_one()) {
-                mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, mk_, &sm.k_full[ks], hf * 64, c1, c2);
+                mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+                for (int w = 0; w < 2; ++w)
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_3d(sQ + w * kTileBytes + hf * kHalfBytes, &p.map_q, &sm.q_full, hf * 64,
+                                    x.h0 + w, x.qb * kBlock);
             }
             __syncwarp();
-            const int vs = j % kNumV;
-            if (j >= kNumV) mbar_wait(&sm.v_empty[vs], ((j / kNumV) & 1) ^ 1);
-            if (elect_one()) {
-                mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, mv_, &sm.v_full[vs], hf * 64, c1, c2);
+            for (int j = 0; j < x.num_tiles; ++j, ++gj) {
+                int e = kSparse ? __ldg(x.tiles + j) : j * kBlock;
+                const bool gathered = kSparse && e < 0;
+                const int row = gathered ? (-e - 1) * kBlock : e;
+                const CUtensorMap* mk_ = gathered ? &p.map_kv : &p.map_k;
+                const CUtensorMap* mv_ = gathered ? &p.map_vv : &p.map_v;
+                const int c1 = gathered ? row : x.g, c2 = gathered ? x.g : row;
+                const int ks = gj % kNumK;
+                if (gj >= kNumK) mbar_wait(&sm.k_empty[ks], ((gj / kNumK) & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, mk_, &sm.k_full[ks], hf * 64, c1, c2);
+                }
+                __syncwarp();
+                const int vs = gj % kNumV;
+                if (gj >= kNumV) mbar_wait(&sm.v_empty[vs], ((gj / kNumV) & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, mv_, &sm.v_full[vs], hf * 64, c1, c2);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         // =========================== MMA issuer
@@ -183,18 +231,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);
         const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
         const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sV), kHalfBytes, 1024);
-        auto issue_pv = [&](int w, int jj) {
-            const uint64_t vd = v_desc0 + static_cast<uint64_t>(((jj % kNumV) * kTileBytes) >> 4);
+        // gj: global tile index (ring slots and s/p barrier phases continue across items);
+        // first: the item's first PV overwrites O (accumulate = 0)
+        auto issue_pv = [&](int w, int gjj, bool first) {
+            const uint64_t vd = v_desc0 + static_cast<uint64_t>(((gjj % kNumV) * kTileBytes) >> 4);
             const uint32_t o_t = tmem + 256 + w * 128;
             const uint32_t p_t = tmem + w * 128;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
-                        (jj > 0 || k > 0) ? 1u : 0u);
+                        (!first || k > 0) ? 1u : 0u);
         };
-        auto issue_s = [&](int w, int jj) {
+        auto issue_s = [&](int w, int gjj) {
             const uint64_t qd = q_desc0 + static_cast<uint64_t>((w * kTileBytes) >> 4);
-            const uint64_t kd = k_desc0 + static_cast<uint64_t>(((jj % kNumK) * kTileBytes) >> 4);
+            const uint64_t kd = k_desc0 + static_cast<uint64_t>(((gjj % kNumK) * kTileBytes) >> 4);
             const uint32_t s_t = tmem + w * 128;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -202,57 +252,91 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 umma_ss(s_t, qd + off, kd + off, idesc_qk, k > 0 ? 1u : 0u);
             }
         };
-        mbar_wait(&sm.bar_q, 0);
-        if (num_tiles == 0) {  // nothing covered: release the epilogue
-            if (elect_one()) {
-                umma_commit(&sm.o_done[0]);
-                umma_commit(&sm.o_done[1]);
-            }
-            __syncwarp();
-        }
-        for (int j = 0; j < num_tiles; ++j) {
-            const int ks = j % kNumK;
-            mbar_wait(&sm.k_full[ks], (j / kNumK) & 1);
+        int gj = 0;
+        for (int n_it = 0;; ++n_it) {
+            const int it = next_item(n_it);
+            if (it < 0) break;
+            const Item x = item(it);
+            const int nt = x.num_tiles;
+            mbar_wait(&sm.q_full, n_it & 1);
             tc_fence_after();
-            for (int w = 0; w < 2; ++w) {
-                if (j > 0) {
-                    mbar_wait(&sm.p_full[w], (j - 1) & 1);
-                    if (w == 0) mbar_wait(&sm.v_full[(j - 1) % kNumV], ((j - 1) / kNumV) & 1);
-                    tc_fence_after();
+            if (nt == 0) {  // nothing covered: release the epilogue (O is not touched)
+                // keep o_free's phases in lock-step with the items (no parity aliasing)
+                if (n_it > 0) {
+                    mbar_wait(&sm.o_free[0], (n_it - 1) & 1);
+                    mbar_wait(&sm.o_free[1], (n_it - 1) & 1);
                 }
                 if (elect_one()) {
+                    umma_commit(&sm.q_free);
+                    umma_commit(&sm.o_done[0]);
+                    umma_commit(&sm.o_done[1]);
+                }
+                __syncwarp();
+                continue;
+            }
+            for (int j = 0; j < nt; ++j) {
+                const int G = gj + j;
+                const int ks = G % kNumK;
+                mbar_wait(&sm.k_full[ks], (G / kNumK) & 1);
+                tc_fence_after();
+                for (int w = 0; w < 2; ++w) {
                     if (j > 0) {
-                        issue_pv(w, j - 1);
-                        if (w == 1) umma_commit(&sm.v_empty[(j - 1) % kNumV]);
+                        mbar_wait(&sm.p_full[w], (G - 1) & 1);
+                        if (w == 0) mbar_wait(&sm.v_full[(G - 1) % kNumV], ((G - 1) / kNumV) & 1);
+                        // the item's first PV writes O_w: the previous item's epilogue must be done
+                        if (j == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
+                        tc_fence_after();
                     }
-                    issue_s(w, j);
-                    umma_commit(&sm.s_full[w]);
-                    if (w == 1) umma_commit(&sm.k_empty[ks]);
+                    if (elect_one()) {
+                        if (j > 0) {
+                            issue_pv(w, G - 1, j == 1);
+                            if (w == 1) umma_commit(&sm.v_empty[(G - 1) % kNumV]);
+                        }
+                        issue_s(w, G);
+                        umma_commit(&sm.s_full[w]);
+                        if (w == 1) {
+                            umma_commit(&sm.k_empty[ks]);
+                            if (j == nt - 1) umma_commit(&sm.q_free);  // Q of this item no longer read
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            const int GL = gj + nt - 1;
+            for (int w = 0; w < 2; ++w) {
+                mbar_wait(&sm.p_full[w], GL & 1);
+                if (w == 0) mbar_wait(&sm.v_full[GL % kNumV], (GL / kNumV) & 1);
+                if (nt == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    issue_pv(w, GL, nt == 1);
+                    umma_commit(&sm.o_done[w]);
+                    if (w == 1) umma_commit(&sm.v_empty[GL % kNumV]);
                 }
                 __syncwarp();
             }
-        }
-        const int jl = num_tiles - 1;
-        for (int w = 0; w < 2 && num_tiles > 0; ++w) {
-            mbar_wait(&sm.p_full[w], jl & 1);
-            if (w == 0) mbar_wait(&sm.v_full[jl % kNumV], (jl / kNumV) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                issue_pv(w, jl);
-                umma_commit(&sm.o_done[w]);
-            }
-            __syncwarp();
+            gj += nt;
         }
     } else if (warp >= 4) {
         // =========================== softmax + epilogue
         const int w = (warp - 4) >> 2;             // Q tile / head within the pair
         const int quarter = warp & 3;              // TMEM lane quarter
         const int r = quarter * 32 + lane;         // row within the block
-        const int i = i0 + r;                      // query row
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         const uint32_t s_t = lane_base + w * 128;
         const uint32_t o_t = lane_base + 256 + w * 128;
         const float sl2 = p.scale * kLog2e;
+        int gt = 0;  // global tile index: s_full / p_full phases continue across items
+        for (int n_it = 0;; ++n_it) {
+        const int it = next_item(n_it);
+        if (it < 0) break;
+        const Item x = item(it);
+        const int qb = x.qb, h0 = x.h0, g = x.g, num_tiles = x.num_tiles, vcnt0 = x.vcnt0;
+        const int* tiles = x.tiles;
+        (void)tiles;
+        (void)vcnt0;
+        const int i0 = qb * kBlock;
+        const int i = i0 + r;                      // query row
 
         // sparse: #{I_v <= i} = vcnt0 + popcount(vbits over [i0, i])
         int vcnt_i = 0;
@@ -319,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             // tcgen05.ld/st are warp-collective: the masked path must be warp-uniform (lanes
             // that need no mask carry all-ones words)
             masked = __any_sync(0xffffffffu, masked);
-            mbar_wait(&sm.s_full[w], j & 1);
+            mbar_wait(&sm.s_full[w], (gt + j) & 1);
             tc_fence_after();
             // pass 1: row max of the raw logits q.k (TMEM is re-read in pass 2 rather than
             // holding 128 values in registers)
@@ -405,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
 
         // ---- epilogue: O / l -> bf16 [n, Hq, d]; LSE (natural log of sum exp(scaled logits))
-        mbar_wait(&sm.o_done[w], 0);
+        mbar_wait(&sm.o_done[w], n_it & 1);
         tc_fence_after();
         const int h = h0 + w;
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
@@ -434,11 +518,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         if (i < p.n && p.lse != nullptr)
             p.lse[static_cast<size_t>(h) * p.n + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+        // O_w has been read: the next item's first PV may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.o_free[w]);
+        gt += num_tiles;
+        }
     }
 
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_free<512>(tmem);
+    // the last CTA out resets the work counter for the next launch on this stream
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+            __threadfence();
+        }
+    }
 }
 
 // ------------------------------------------------------------------ sparse planning
@@ -583,6 +682,17 @@ static bool make_qkv_maps(AttnParams& p, const void* q, const void* k, const voi
            vsp_host::make_map_bf16(&p.map_v, v, 3, dk, sk, box);
 }
 
+// work counters of the dense kernel (zero at module load, reset by each launch's last CTA)
+__device__ int g_dense_work[2];
+
+// persistent grid: one CTA per SM (the kernel's smem allows one), never more than the items
+int persistent_grid(int items) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, std::min(items, sms));
+}
+
 cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     AttnParams p{};
     p.n = a.n;
@@ -602,8 +712,11 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     p.pair0 = 0;
     p.npairs = a.hq / 2;
     p.qb_hi = num_qb;
-    dim3 grid(num_qb * p.npairs);
-    attn_fwd_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(p);
+    p.items = num_qb * p.npairs;
+    void* work = nullptr;
+    cudaGetSymbolAddress(&work, g_dense_work);
+    p.work = static_cast<int*>(work);
+    attn_fwd_kernel<false><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -618,6 +731,7 @@ size_t sparse_workspace_bytes(int n, int hkv, int cap) {
     add(static_cast<size_t>(hkv) * kvcap * kHeadDim * 2);  // Vv
     add(static_cast<size_t>(hkv) * bm_words * 4 * 2);      // bitmaps
     add(static_cast<size_t>(hkv) * num_qb * list_stride * 4);
+    add(static_cast<size_t>(hkv) * 2 * 4);                 // per-KV-head work counters
     return bytes;
 }
 
@@ -649,6 +763,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
     auto* vg = reinterpret_cast<__nv_bfloat16*>(take(static_cast<size_t>(a.hkv) * kvcap * kHeadDim * 2));
     auto* bits = reinterpret_cast<uint32_t*>(take(static_cast<size_t>(a.hkv) * bm_words * 4 * 2));
     auto* lists = reinterpret_cast<int*>(take(static_cast<size_t>(a.hkv) * num_qb * list_stride * 4));
+    int* work = reinterpret_cast<int*>(take(static_cast<size_t>(a.hkv) * 2 * 4));
     p.vbits = bits;
     p.sbits = bits + static_cast<size_t>(a.hkv) * bm_words;
     p.bm_words = bm_words;
@@ -667,6 +782,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         cudaError_t e = cudaMemsetAsync(bits + static_cast<size_t>(g0) * words, 0, count * words * 4, stream);
         if (e == cudaSuccess)
             e = cudaMemsetAsync(bits + (static_cast<size_t>(a.hkv) + g0) * words, 0, count * words * 4, stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(work + 2 * g0, 0, count * 2 * 4, stream);
         if (e != cudaSuccess) return e;
         build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, count), 256, 0, stream>>>(
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words, g0);
@@ -689,8 +805,9 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         p.qb_hi = qb_hi < 0 ? num_qb : std::min(qb_hi, num_qb);
         const int nqb = p.qb_hi - std::max(qb_lo, 0);
         if (nqb <= 0) return cudaGetLastError();
-        dim3 grid(nqb * p.npairs);
-        attn_fwd_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(p);
+        p.items = nqb * p.npairs;
+        p.work = work + 2 * g0;  // launches on different KV-head ranges never share a counter
+        attn_fwd_kernel<true><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
     }
     return cudaGetLastError();
 }

@@ -388,7 +388,10 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // hpc == 0 (automatic) uses two halves: the second half's scoring and selection overlap
 // the first half's attention, and each attention launch still spans enough heads to
 // balance its long and short CTAs (tools/sched_sweep.py: profiles/r01_schedule_sweep.json).
-int auto_hpc(int hkv) { return (hkv + 1) / 2; }
+// Automatic schedule: one chunk. K3 is a persistent kernel that holds every SM, so the
+// side-stream scoring of a later chunk (cluster launches need free SMs) could not overlap it
+// anyway; chunking pays only where copies overlap compute (the host-buffer entry).
+int auto_hpc(int hkv) { return hkv; }
 // hpc < 0: a lead chunk of -hpc heads (its scoring is the only exposed part), then the rest
 // as one chunk whose scoring overlaps the lead chunk's attention.
 int num_chunks(int hkv, int hpc) {
@@ -459,9 +462,15 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
     void* ws_attn = ws;
     float* lv = static_cast<float*>(ws_ix);  // logits [hkv, n] x 2 in the indexer workspace
     float* ls = lv + static_cast<size_t>(hkv) * n;
-    cudaStream_t side = ctx->side;
-    cudaError_t e = cudaEventRecord(ctx->ev_start, main);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
+    // One chunk on resident inputs: nothing to overlap (K3 is persistent and fills every SM),
+    // so the whole layer runs in order on the caller's stream without the event hops.
+    const bool serial = chunks == 1 && kv_ready == nullptr && q_ready == nullptr;
+    cudaStream_t side = serial ? main : ctx->side;
+    cudaError_t e = cudaSuccess;
+    if (!serial) {
+        e = cudaEventRecord(ctx->ev_start, main);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
+    }
     vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
     vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
@@ -476,12 +485,12 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
             e = vsp_select_k::launch_from_logits(lv, ls, p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s,
                                                  cap, ws_sel, side, g0, cnt);
         if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, side, g0, cnt, 1);
-        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[c], side);
+        if (e == cudaSuccess && !serial) e = cudaEventRecord(ctx->ev_chunk[c], side);
     }
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
         int g0, cnt;
         chunk_range(c, hkv, hpc, g0, cnt);
-        e = cudaStreamWaitEvent(main, ctx->ev_chunk[c], 0);
+        if (!serial) e = cudaStreamWaitEvent(main, ctx->ev_chunk[c], 0);
         if (e == cudaSuccess && q_ready) e = cudaStreamWaitEvent(main, q_ready[c], 0);
         if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, g0, cnt, 2);
         if (e == cudaSuccess && attn_done) e = cudaEventRecord(attn_done[c], main);

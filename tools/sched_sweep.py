@@ -67,6 +67,7 @@ def main():
             torch.cuda.synchronize()
             times[name].append(a.elapsed_time(b) / 3)
     print(json.dumps({name: round(statistics.median(t), 4) for name, t in times.items()}))
+    print(json.dumps({"min": {name: round(min(t), 4) for name, t in times.items()}}))
 
 
 if __name__ == "__main__":
