@@ -561,23 +561,27 @@ __global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __re
     }
 }
 
-// Kv[g][r] = K[I_v[g][r]][g], r < kvcap (rows >= k_v zero). grid (kvcap/16, hkv), 256 threads:
-// 16 rows per block, 16 threads x 16 B per 256 B row.
+// Kv[g][r] = K[I_v[g][r]][g] for r < k_v; rows [k_v, round_up(k_v, 128)) zero (the last
+// gathered tile is read whole: finite V rows keep 0 * V out of NaN); rows past that tile are
+// never read, so they are not written. grid (X, hkv), 256 threads, grid-stride over 16-row
+// groups: 16 threads x 16 B per 256 B row.
 __global__ void gather_vertical_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                                        const int* __restrict__ iv, const int* __restrict__ kv, int cap,
                                        int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg, int g0) {
     const int g = g0 + static_cast<int>(blockIdx.y);
-    const int r = blockIdx.x * 16 + (threadIdx.x >> 4);
     const int t = threadIdx.x & 15;
-    if (r >= kvcap) return;
-    uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-    if (r < kv[g]) {
-        const int j = min(max(iv[static_cast<size_t>(g) * cap + r], 0), n - 1);
-        a = reinterpret_cast<const uint4*>(k + (static_cast<size_t>(j) * hkv + g) * kHeadDim)[t];
-        b = reinterpret_cast<const uint4*>(v + (static_cast<size_t>(j) * hkv + g) * kHeadDim)[t];
+    const int cnt = min(kv[g], kvcap);
+    const int rows = min((cnt + kBlock - 1) / kBlock * kBlock, kvcap);
+    for (int r = blockIdx.x * 16 + (threadIdx.x >> 4); r < rows; r += gridDim.x * 16) {
+        uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+        if (r < cnt) {
+            const int j = min(max(__ldg(iv + static_cast<size_t>(g) * cap + r), 0), n - 1);
+            a = __ldg(reinterpret_cast<const uint4*>(k + (static_cast<size_t>(j) * hkv + g) * kHeadDim) + t);
+            b = __ldg(reinterpret_cast<const uint4*>(v + (static_cast<size_t>(j) * hkv + g) * kHeadDim) + t);
+        }
+        reinterpret_cast<uint4*>(kg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = a;
+        reinterpret_cast<uint4*>(vg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = b;
     }
-    reinterpret_cast<uint4*>(kg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = a;
-    reinterpret_cast<uint4*>(vg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = b;
 }
 
 VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
@@ -786,7 +790,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         if (e != cudaSuccess) return e;
         build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, count), 256, 0, stream>>>(
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words, g0);
-        gather_vertical_kernel<<<dim3(kvcap / 16, count), 256, 0, stream>>>(
+        gather_vertical_kernel<<<dim3(std::min(kvcap / 16, 128), count), 256, 0, stream>>>(
             static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
             a.n, a.hkv, kvcap, kg, vg, g0);
         vs_plan_kernel<<<dim3((num_qb + 3) / 4, count), 128, 0, stream>>>(
