@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             tc_fence_after();
             // pass 1: row max of the raw logits q.k (TMEM is re-read in pass 2 rather than
             // holding 128 values in registers)
-            float mx = -INFINITY;
+            float mx;
             {
                 uint32_t u[4][32];  // all four loads in flight before the first wait
 #pragma unroll
@@ -415,6 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_reg_fence(u[c]);
+                // eight independent max chains (a single chain is 64 dependent 3-input maxes)
+                float mxa[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mxa[t] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (masked) {  // write the masked logits back so pass 2 is mask-free
@@ -424,8 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         tmem_st32(s_t + c * 32, u[c]);
                     }
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) mx = fmaxf(mx, __uint_as_float(u[c][t]));
+                    for (int t = 0; t < 32; t += 2)
+                        mxa[(t >> 1) & 7] = fmaxf(mxa[(t >> 1) & 7], fmaxf(__uint_as_float(u[c][t]), __uint_as_float(u[c][t + 1])));
                 }
+                mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
             }
             if (masked) tmem_wait_st();
             const float m_new = fmaxf(m_used, mx * sl2);
