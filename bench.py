@@ -76,7 +76,7 @@ def parse():
                          "units with replicated inputs; auto = heads at N=1, balanced at N>1")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
-    ap.add_argument("--e2e-heads-per-chunk", type=int, default=1)
+    ap.add_argument("--e2e-heads-per-chunk", type=int, default=0)
     return ap.parse_args()
 
 

@@ -205,9 +205,11 @@ VSP_API int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, con
  * tools/vsprefill.cpp:154-185). This entry point does the same: Q/K/V are read from host
  * memory (pinned for asynchronous copies) and O [n, hq, 128] bf16, LSE [hq, n] (nullable)
  * and the per-head budgets k_v/k_s [hkv] (nullable) are written back to host memory. The
- * copies are pipelined with the compute per KV-head chunk: chunk c's K/V/Q travel on one
- * copy engine while chunk c-1 is scored and attended, and chunk c-1's O returns on the
- * other copy engine. workspace: device memory of vsp_vs_prefill_host_workspace_size bytes
+ * copies are pipelined with the compute on two copy engines. heads_per_chunk = 0
+ * (automatic): K and V first (two contiguous copies; scoring needs all n rows), then Q in 16
+ * query-row ranges; range r is attended as soon as its rows land and its O rows / LSE
+ * columns return while later ranges are still in flight. heads_per_chunk > 0: per KV-head
+ * chunk, chunk c's K/V/Q columns travel while chunk c-1 is scored and attended. workspace: device memory of vsp_vs_prefill_host_workspace_size bytes
  * (it holds the device copies of the inputs and outputs). Stream-ordered on `stream`. */
 VSP_API size_t vsp_vs_prefill_host_workspace_size(int n, int hq, int hkv, int d_h);
 VSP_API int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_h, const void* v_h, int n, int hq,

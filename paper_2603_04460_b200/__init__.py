@@ -475,11 +475,12 @@ def vs_prefill_units(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: 
 
 
 def vs_prefill_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
-                    mapping: str = "reverse", heads_per_chunk: int = 1, out: Optional[torch.Tensor] = None,
+                    mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
                     lse: Optional[torch.Tensor] = None, budgets_out: bool = False, device=None):
     """vs_prefill from HOST tensors (pinned CPU memory for overlap), like the reference's
     own operators which take host vectors: one C-ABI call (vsp_vs_prefill_host) that pipelines
-    H2D copies, scoring/selection, attention and the D2H of O per KV-head chunk.
+    H2D copies, scoring/selection, attention and the D2H of O — per query-row range
+    (heads_per_chunk=0: K/V first, then Q ranges) or per KV-head chunk (heads_per_chunk>0).
     Returns (O, LSE) as host tensors (+ (k_v, k_s) host tensors when budgets_out).
     Stream-ordered: synchronise the current stream before reading the results."""
     for t in (q, k, v):

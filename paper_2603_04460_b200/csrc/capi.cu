@@ -445,6 +445,53 @@ int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_map
     return VSP_OK;
 }
 
+// Query-block boundaries of the host-buffer entry's automatic schedule: 7/8 of the blocks in
+// 14 equal ranges, the last 1/8 in halving ranges (1/16, 1/32, ... down to one block), so
+// the exposed tail — the last range's attention and the D2H of its O rows — is one block.
+std::vector<int> row_chunk_bounds(int num_qb) {
+    std::vector<int> b{0};
+    const int tail = num_qb / 8;
+    const int head = num_qb - tail;
+    const int heads = std::min(14, head);
+    for (int c = 1; c <= heads; ++c) b.push_back(static_cast<int>(static_cast<long long>(head) * c / heads));
+    int left = tail;
+    while (left > 0) {
+        const int piece = std::max(1, left / 2);
+        b.push_back(b.back() + piece);
+        left -= piece;
+    }
+    return b;  // at most 14 + log2(num_qb / 8) + 1 ranges
+}
+
+void* attn_workspace(void* workspace, int n, int hkv, int d_h) {
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    ws += align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
+    ws += align256(vsp_select_k::workspace_bytes(n, hkv));
+    return ws;
+}
+
+// K1 (logits) -> K2 (softmax + selection) -> K3 plan for KV heads [g0, g0 + cnt) on `st`.
+cudaError_t enqueue_scoring(const PrefillDev& p, int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping,
+                            const vsp_budget* budgets, void* workspace, int g0, int cnt, cudaStream_t st) {
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    void* ws_ix = ws;
+    void* ws_sel = ws + align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
+    void* ws_attn = attn_workspace(workspace, n, hkv, d_h);
+    float* lv = static_cast<float*>(ws_ix);  // logits [hkv, n] x 2 in the indexer workspace
+    float* ls = lv + static_cast<size_t>(hkv) * n;
+    // logits only (a_v null); the selection clusters softmax them and write A_v / A_s
+    vsp_indexer::Args ia{p.k, p.v, n, hkv, d_h, p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s,
+                         slash_mapping == VSP_SLASH_REVERSE, nullptr, nullptr, lv, ls, g0, cnt};
+    cudaError_t e = vsp_indexer::launch(ia, ws_ix, st);
+    if (e == cudaSuccess)
+        e = vsp_select_k::launch_from_logits(lv, ls, p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s, cap,
+                                             ws_sel, st, g0, cnt);
+    vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
+    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+    if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g0, cnt, 1);
+    return e;
+}
+
 // Enqueue K1 -> K2 -> plan on the side stream and K3 on `main`, chunk by chunk. Chunk c's
 // scoring waits for kv_ready[c] and its attention for q_ready[c] (copy-engine events of
 // the host-buffer entry; null = inputs already resident); attn_done[c] is recorded after
@@ -454,14 +501,7 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
                             cudaStream_t main, const cudaEvent_t* kv_ready, const cudaEvent_t* q_ready,
                             const cudaEvent_t* attn_done) {
     const int chunks = num_chunks(hkv, hpc);
-    uint8_t* ws = static_cast<uint8_t*>(workspace);
-    void* ws_ix = ws;
-    ws += align256(vsp_indexer::workspace_bytes(n, hkv, d_h));
-    void* ws_sel = ws;
-    ws += align256(vsp_select_k::workspace_bytes(n, hkv));
-    void* ws_attn = ws;
-    float* lv = static_cast<float*>(ws_ix);  // logits [hkv, n] x 2 in the indexer workspace
-    float* ls = lv + static_cast<size_t>(hkv) * n;
+    void* ws_attn = attn_workspace(workspace, n, hkv, d_h);
     // One chunk on resident inputs: nothing to overlap (K3 is persistent and fills every SM),
     // so the whole layer runs in order on the caller's stream without the event hops.
     const bool serial = chunks == 1 && kv_ready == nullptr && q_ready == nullptr;
@@ -477,14 +517,8 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         int g0, cnt;
         chunk_range(c, hkv, hpc, g0, cnt);
         if (kv_ready) e = cudaStreamWaitEvent(side, kv_ready[c], 0);
-        // logits only (a_v null); the selection clusters softmax them and write A_v / A_s
-        vsp_indexer::Args ia{p.k, p.v, n, hkv, d_h, p.w_u, p.b_u, p.w_v, p.b_v, p.w_s, p.b_s,
-                             slash_mapping == VSP_SLASH_REVERSE, nullptr, nullptr, lv, ls, g0, cnt};
-        if (e == cudaSuccess) e = vsp_indexer::launch(ia, ws_ix, side);
         if (e == cudaSuccess)
-            e = vsp_select_k::launch_from_logits(lv, ls, p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s,
-                                                 cap, ws_sel, side, g0, cnt);
-        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, side, g0, cnt, 1);
+            e = enqueue_scoring(p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, g0, cnt, side);
         if (e == cudaSuccess && !serial) e = cudaEventRecord(ctx->ev_chunk[c], side);
     }
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
@@ -663,6 +697,56 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
     cudaError_t e = cudaEventRecord(ctx->ev_host0, main);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->h2d, ctx->ev_host0, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->d2h, ctx->ev_host0, 0);
+    PrefillDev p{q_d, k_d, v_d, w_u, b_u, w_v, b_v, w_s, b_s, av_d, as_d, iv_d, kv_d, is_d, ks_d, o_d, lse_d, false};
+    if (hpc == 0) {
+        // Query-row pipeline (automatic schedule): K and V go first as two contiguous copies
+        // (the scoring softmaxes over all n rows), then Q in row ranges; the attention of a
+        // range runs as soon as its Q rows land and its O rows / LSE columns go back while
+        // later Q ranges are still in flight. Every copy is a long contiguous run.
+        const std::vector<int> bounds = row_chunk_bounds((n + 127) / 128);
+        const int rc_chunks = static_cast<int>(bounds.size()) - 1;
+        auto rows_of = [&](int c, int& qb_lo, int& qb_hi) {
+            qb_lo = bounds[c];
+            qb_hi = bounds[c + 1];
+        };
+        const size_t kv_bytes = size_t(n) * hkv * row, q_row = size_t(hq) * row;
+        e = cudaMemcpyAsync(k_d, k_h, kv_bytes, cudaMemcpyHostToDevice, ctx->h2d);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(v_d, v_h, kv_bytes, cudaMemcpyHostToDevice, ctx->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_kv[0], ctx->h2d);
+        for (int c = 0; c < rc_chunks && e == cudaSuccess; ++c) {
+            int lo, hi;
+            rows_of(c, lo, hi);
+            const size_t r0 = size_t(lo) * 128, r1 = std::min(size_t(hi) * 128, size_t(n));
+            e = cudaMemcpyAsync(q_d + r0 * q_row, static_cast<const uint8_t*>(q_h) + r0 * q_row, (r1 - r0) * q_row,
+                                cudaMemcpyHostToDevice, ctx->h2d);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q[c], ctx->h2d);
+        }
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ctx->ev_kv[0], 0);
+        if (e == cudaSuccess)
+            e = enqueue_scoring(p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, 0, hkv, main);
+        vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), false};
+        vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+        void* ws_attn = attn_workspace(workspace, n, hkv, d_h);
+        for (int c = 0; c < rc_chunks && e == cudaSuccess; ++c) {
+            int lo, hi;
+            rows_of(c, lo, hi);
+            e = cudaStreamWaitEvent(main, ctx->ev_q[c], 0);
+            if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, 0, hkv, 2, lo, hi);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_attn[c], main);
+        }
+        for (int c = 0; c < rc_chunks && e == cudaSuccess; ++c) {
+            int lo, hi;
+            rows_of(c, lo, hi);
+            const size_t r0 = size_t(lo) * 128, r1 = std::min(size_t(hi) * 128, size_t(n));
+            e = cudaStreamWaitEvent(ctx->d2h, ctx->ev_attn[c], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<uint8_t*>(o_h) + r0 * q_row, o_d + r0 * q_row, (r1 - r0) * q_row,
+                                    cudaMemcpyDeviceToHost, ctx->d2h);
+            if (e == cudaSuccess && lse_h)  // LSE [hq, n]: columns [r0, r1) of every head row
+                e = cudaMemcpy2DAsync(lse_h + r0, size_t(n) * 4, lse_d + r0, size_t(n) * 4, (r1 - r0) * 4, hq,
+                                      cudaMemcpyDeviceToHost, ctx->d2h);
+        }
+    } else {
     // H2D per chunk: this chunk's K and V columns (strided rows of cnt heads), then its Q heads
     const uint8_t* qh = static_cast<const uint8_t*>(q_h);
     const uint8_t* kh = static_cast<const uint8_t*>(k_h);
@@ -680,7 +764,6 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
             e = cudaMemcpy2DAsync(q_d + qoff, qp, qh + qoff, qp, qw, n, cudaMemcpyHostToDevice, ctx->h2d);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q[c], ctx->h2d);
     }
-    PrefillDev p{q_d, k_d, v_d, w_u, b_u, w_v, b_v, w_s, b_s, av_d, as_d, iv_d, kv_d, is_d, ks_d, o_d, lse_d, false};
     if (e == cudaSuccess)
         e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, hpc, main, ctx->ev_kv,
                             ctx->ev_q, ctx->ev_attn);
@@ -696,6 +779,7 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
         if (e == cudaSuccess && lse_h)
             e = cudaMemcpyAsync(lse_h + size_t(g0) * grp * n, lse_d + size_t(g0) * grp * n,
                                 size_t(cnt) * grp * n * 4, cudaMemcpyDeviceToHost, ctx->d2h);
+    }
     }
     if (e == cudaSuccess && k_v_h) e = cudaMemcpyAsync(k_v_h, kv_d, size_t(hkv) * 4, cudaMemcpyDeviceToHost, ctx->d2h);
     if (e == cudaSuccess && k_s_h) e = cudaMemcpyAsync(k_s_h, ks_d, size_t(hkv) * 4, cudaMemcpyDeviceToHost, ctx->d2h);

@@ -284,12 +284,12 @@ def test_vs_prefill_rejects_bad_budget_count(vsp):
         vsp.vs_prefill(q, k, v, p, vsp.BudgetConfig(0.9, 0.0))
 
 
-@pytest.mark.parametrize("hpc", [1, 3])
-def test_vs_prefill_host_matches_device(vsp, hpc):
-    """The host-buffer layer call (pipelined H2D / compute / D2H per KV-head chunk) returns
-    exactly the device call's O, LSE and budgets."""
+@pytest.mark.parametrize("hpc,n", [(0, 1100), (0, 5000), (1, 1100), (3, 1100)])
+def test_vs_prefill_host_matches_device(vsp, hpc, n):
+    """The host-buffer layer call (pipelined H2D / compute / D2H per query-row range (hpc 0)
+    or per KV-head chunk) returns exactly the device call's O, LSE and budgets."""
     from helpers import qkv
-    n, hq, hkv = 1100, 8, 4
+    hq, hkv = 8, 4
     q, k, v = qkv(n, hq, hkv, seed=9)
     p = _params(vsp, hkv, 256, seed=6, sigma=0.5)
     budgets = [vsp.BudgetConfig(0.4 + 0.1 * g, 0.5, 1, None) for g in range(hkv)]
