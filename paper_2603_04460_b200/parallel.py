@@ -152,7 +152,8 @@ def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: f
         return out
 
     lo = max(c for _, _, c in flat) + head_overhead
-    hi = sum(c for _, _, c in flat) + head_overhead * hkv
+    # a bound every fill() meets in one run, whatever the float summation order
+    hi = (sum(c for _, _, c in flat) + head_overhead * hkv) * (1.0 + 1e-9) + 1.0
     for _ in range(60):
         mid = 0.5 * (lo + hi)
         if len(fill(mid)) <= world:
@@ -160,6 +161,7 @@ def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: f
         else:
             lo = mid
     out = fill(hi)
+    assert len(out) <= world
     return out + [[] for _ in range(world - len(out))]
 
 

@@ -195,3 +195,16 @@ def test_balanced_units_cover_grid_once_and_balance():
         # head sharding would put the heavy head's whole cost on one rank
         if world == 8:
             assert max(costs) < 0.5 * (float(cost[6].sum()) + 2.0 * nqb)
+
+
+def test_balanced_units_float_costs_never_exceed_world():
+    """Mean (non-integer) cost tables: the bisection's upper bound must fit in one run even
+    when float summation order differs, so world=1 gets exactly one run."""
+    from paper_2603_04460_b200 import parallel
+    rng = np.random.default_rng(11)
+    cost = rng.random((8, 1024)) * 97.3 + 0.1
+    for world in (1, 2, 8):
+        units = parallel.balanced_units(cost, world, cta_overhead=3.0, head_overhead=2000.0)
+        assert len(units) == world
+        assert sum(hi - lo for us in units for _, lo, hi in us) == cost.size
+    assert len(parallel.balanced_units(cost, 1)[0]) == 8  # one unit per head, one rank

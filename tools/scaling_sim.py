@@ -9,7 +9,7 @@ predicted step (max over ranks) and tokens/s for
 The cost table of the balanced split comes from a separate validation prompt (not the timed
 one). Prints one JSON line.
 
-    python tools/scaling_sim.py [--n 131072] [bench.py options]
+    python tools/scaling_sim.py [--cost-prompts K] [--cta-overhead C] [--head-overhead H] [bench.py options]
 """
 import json
 import os
@@ -36,22 +36,41 @@ def timed(fn, reps=3):
 
 
 def main():
+    argv = sys.argv[1:]
+    opts = {"--cost-prompts": "1", "--cta-overhead": "2.0", "--head-overhead": "2500"}
+    for key in list(opts):
+        if key in argv:
+            i = argv.index(key)
+            opts[key] = argv[i + 1]
+            del argv[i:i + 2]
+    sys.argv = [sys.argv[0]] + argv
     args = bench.parse()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     params, budget, _ = bench.prepare_indexer(args, dev, 0, 1)
     n, hq, hkv = args.n, args.hq, args.hkv
-    # cost table from a validation prompt
-    qv, kv_, vv = bench.synth_layer(args, dev, seed=args.seed + 201)
-    a_v, a_s = vsp.indexer_forward(kv_, vv, params)
-    pat = vsp.select_pattern(a_v, a_s, budget)
-    vsp.sparse_attention(qv, kv_, vv, pat, validate=False)
-    cost = vsp.sparse_tile_counts(n, hkv, pat.i_v.shape[1], dev)
-    del qv, kv_, vv
+    # cost table: mean tile counts of the first K validation prompts (K = --cost-prompts)
+    tables = []
+    for i in range(int(opts["--cost-prompts"])):
+        qv, kv_, vv = bench.synth_layer(args, dev, seed=args.seed + 201 + i)
+        a_v, a_s = vsp.indexer_forward(kv_, vv, params)
+        pat = vsp.select_pattern(a_v, a_s, budget)
+        vsp.sparse_attention(qv, kv_, vv, pat, validate=False)
+        tables.append(vsp.sparse_tile_counts(n, hkv, pat.i_v.shape[1], dev).double())
+        del qv, kv_, vv
+    cost = sum(tables) / len(tables)
     q, k, v = bench.synth_layer(args, dev)
     o_full = torch.empty(hq, n, 128, dtype=q.dtype, device=dev)
     lse_full = torch.empty(hq, n, device=dev)
-    out = {"n": n, "hq": hq, "hkv": hkv, "tiles_per_head": cost.sum(1).tolist(), "splits": {}}
+    # the held-out prompt's own table (what the split should have predicted)
+    a_v, a_s = vsp.indexer_forward(k, v, params)
+    pat_h = vsp.select_pattern(a_v, a_s, budget)
+    vsp.sparse_attention(q, k, v, pat_h, validate=False)
+    held = vsp.sparse_tile_counts(n, hkv, pat_h.i_v.shape[1], dev)
+    out = {"n": n, "hq": hq, "hkv": hkv, "cost_prompts": len(tables),
+           "cta_overhead": float(opts["--cta-overhead"]), "head_overhead": float(opts["--head-overhead"]),
+           "tiles_per_head_prompts": [t.sum(1).tolist() for t in tables],
+           "tiles_per_head_heldout": held.sum(1).tolist(), "splits": {}}
     for world in (1, 2, 4, 8):
         # heads: rank r = vs_prefill on its KV heads
         t_heads = []
@@ -64,7 +83,8 @@ def main():
             t_heads.append(timed(lambda: vsp.vs_prefill(qs, ks, vs, ps, bs, out=slab, lse=lslab, head_major=True)))
             del qs, ks, vs
         # balanced: rank r = vs_prefill_units on its units (full inputs)
-        units = parallel.balanced_units(cost, world)
+        units = parallel.balanced_units(cost, world, cta_overhead=float(opts["--cta-overhead"]),
+                                        head_overhead=float(opts["--head-overhead"]))
         t_bal = [timed(lambda u=u: vsp.vs_prefill_units(q, k, v, params, budget, u, out=o_full, lse=lse_full))
                  for u in units]
         out["splits"][world] = {
