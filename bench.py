@@ -380,10 +380,12 @@ def main():
         barrier()
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" captures this region
+        launches0 = vsp.kernel_launches()
         e0.record(stream)
         for _ in range(args.steps):
             pat = step()
         e1.record(stream)
+        timed_launches = vsp.kernel_launches() - launches0  # libvsp_gpu.so's own launch counter
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         barrier()
@@ -504,8 +506,6 @@ def main():
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
 
-    # per KV-head chunk: indexer gemm + softmax, select, bitmaps + gather + plan, attention
-    launches_per_step = 7 * (((hkv_r + hpc - 1) // hpc) if hpc > 0 else (2 if hkv_r > 1 else 1))
     if rank == 0:
         line = {
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
@@ -534,7 +534,7 @@ def main():
                          "traffic": k3_traffic(), "algorithmic_bytes": alg_bytes,
                          "peak_kind": f"{pk_kind} bf16 sustained",
                          "executed_tile_tflops": tile_tf, "executed_tile_frac": tile_tf / peak_tf},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": timed_launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -86,6 +86,9 @@ typedef struct vsp_ctx vsp_ctx;
 
 VSP_API const char* vsp_last_error(void);
 VSP_API const char* vsp_version(void);
+/* Kernels this library has launched in this process so far (every launch site counts), so a
+ * caller can attribute the device work of a region to libvsp_gpu.so. */
+VSP_API long long vsp_kernel_launches(void);
 
 VSP_API int vsp_create(vsp_ctx** ctx, int device);
 VSP_API int vsp_destroy(vsp_ctx* ctx);

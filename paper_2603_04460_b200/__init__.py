@@ -71,6 +71,7 @@ def load_library():
     vp, i, f, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t
     lib.vsp_last_error.restype = ctypes.c_char_p
     lib.vsp_version.restype = ctypes.c_char_p
+    lib.vsp_kernel_launches.restype = ctypes.c_longlong
     lib.vsp_create.argtypes = [ctypes.POINTER(vp), i]
     lib.vsp_destroy.argtypes = [vp]
     lib.vsp_indexer_workspace_size.restype = sz
@@ -424,6 +425,11 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
 
 class _Unit(ctypes.Structure):
     _fields_ = [("g", ctypes.c_int32), ("qb_lo", ctypes.c_int32), ("qb_hi", ctypes.c_int32)]
+
+
+def kernel_launches() -> int:
+    """Kernels libvsp_gpu.so has launched in this process (vsp_kernel_launches)."""
+    return int(load_library().vsp_kernel_launches())
 
 
 def sparse_tile_counts(n: int, hkv: int, cap: int, device) -> torch.Tensor:

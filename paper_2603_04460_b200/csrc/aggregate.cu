@@ -31,6 +31,7 @@
 #include <cmath>
 #include <type_traits>
 
+#include "vsp_launch.h"
 #include "aggregate.h"
 #include "attn.h"
 #include "sm100.cuh"
@@ -490,9 +491,11 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     }
     long long ctas = 0;
     for (int qc = 0; qc < p.num_qc; ++qc) ctas += static_cast<long long>(std::min(p.num_qb, kChunk * (qc + 1))) * a.hkv;
+    vsp_detail::count_launch();
     aggregate_kernel<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, stream>>>(p);
     const int grp = a.hq / a.hkv;
     const double total = (a.normalized ? 1.0 : static_cast<double>(a.n)) * (a.mean ? 1.0 : static_cast<double>(grp));
+    vsp_detail::count_launch();
     finalize_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(p.acc_v, p.acc_s, a.a_v, a.a_s, a.n, total);
     return cudaGetLastError();
 }

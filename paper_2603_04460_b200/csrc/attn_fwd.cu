@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "vsp_launch.h"
 #include "attn.h"
 #include "sm100.cuh"
 
@@ -727,6 +728,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     void* work = nullptr;
     cudaGetSymbolAddress(&work, g_dense_work);
     p.work = static_cast<int*>(work);
+    vsp_detail::count_launch();
     attn_fwd_kernel<false><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
     return cudaGetLastError();
 }
@@ -795,11 +797,14 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
             e = cudaMemsetAsync(bits + (static_cast<size_t>(a.hkv) + g0) * words, 0, count * words * 4, stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(work + 2 * g0, 0, count * 2 * 4, stream);
         if (e != cudaSuccess) return e;
+        vsp_detail::count_launch();
         build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, count), 256, 0, stream>>>(
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words, g0);
+        vsp_detail::count_launch();
         gather_vertical_kernel<<<dim3(std::min(kvcap / 16, 128), count), 256, 0, stream>>>(
             static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
             a.n, a.hkv, kvcap, kg, vg, g0);
+        vsp_detail::count_launch();
         vs_plan_kernel<<<dim3((num_qb + 3) / 4, count), 128, 0, stream>>>(
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists, g0);
     }
@@ -818,6 +823,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         if (nqb <= 0) return cudaGetLastError();
         p.items = nqb * p.npairs;
         p.work = work + 2 * g0;  // launches on different KV-head ranges never share a counter
+        vsp_detail::count_launch();
         attn_fwd_kernel<true><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
     }
     return cudaGetLastError();
@@ -854,6 +860,7 @@ cudaError_t sparse_tile_stats(int n, int hkv, int cap, const void* workspace, lo
     cudaError_t e = cudaMallocAsync(&d, sizeof(unsigned long long) * hkv, stream);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(d, 0, sizeof(unsigned long long) * hkv, stream);
+    vsp_detail::count_launch();
     tile_stats_kernel<<<hkv, 256, 0, stream>>>(lists, num_qb, list_stride, d);
     std::vector<unsigned long long> h(hkv);
     cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * hkv, cudaMemcpyDeviceToHost, stream);

@@ -7,8 +7,10 @@
 #include <cmath>
 #include <string>
 #include <initializer_list>
+#include <atomic>
 #include <vector>
 
+#include "vsp_launch.h"
 #include "../../include/vsp_gpu.h"
 #include "aggregate.h"
 #include "attn.h"
@@ -24,7 +26,11 @@ int set_err(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace vsp_detail
+
+extern "C" long long vsp_kernel_launches(void) { return vsp_detail::g_launches.load(std::memory_order_relaxed); }
 
 struct vsp_ctx {
     int device = 0;
@@ -201,6 +207,7 @@ int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, i
     cudaStream_t st = as_stream(stream);
     if (flags & VSP_VALIDATE) {
         if (hkv > 1024) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: too many heads to validate");
+        vsp_detail::count_launch();
         validate_pattern_kernel<<<hkv, 256, 0, st>>>(i_v, k_v, i_s, k_s, cap, ctx->d_flags);
         int hflags[1024];
         cudaError_t e = cudaMemcpyAsync(hflags, ctx->d_flags, sizeof(int) * hkv, cudaMemcpyDeviceToHost, st);
@@ -227,6 +234,7 @@ int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_
                         float* recall_per_head, void* stream) {
     VSP_CHECK_CTX(ctx);
     if (n < 1 || hq < 1) return set_err(VSP_EINVAL, "vsp_recall_from_lse: bad shape");
+    vsp_detail::count_launch();
     recall_kernel<<<hq, 512, 0, as_stream(stream)>>>(lse_sparse, lse_dense, n, recall_per_head);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_recall_from_lse");
@@ -590,6 +598,7 @@ extern "C" int vsp_vs_attn_tile_counts(vsp_ctx* ctx, int n, int hkv, int cap, co
     const int total = hkv * num_qb;
     cudaError_t e = cudaMallocAsync(&d, sizeof(int) * total, st);
     if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_tile_counts");
+    vsp_detail::count_launch();
     tile_counts_kernel<<<(total + 255) / 256, 256, 0, st>>>(lists, total, list_stride, d);
     e = cudaMemcpyAsync(counts, d, sizeof(int) * total, cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(d, st);

@@ -18,6 +18,7 @@
 // The softmax over n runs in the selection clusters (select.cu, fp64 normaliser).
 #include <cuda_bf16.h>
 
+#include "vsp_launch.h"
 #include "indexer.h"
 #include "select.h"
 #include "sm100.cuh"
@@ -309,6 +310,7 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int work = p.tiles * count;
+    vsp_detail::count_launch();
     indexer_gemm_kernel<<<work < sms ? work : sms, kThreads, kSmemBytes, stream>>>(p);
     cudaError_t e = cudaGetLastError();
     // A_v / A_s: the cluster softmax shared with the selection kernel (a_v null: logits only,

@@ -19,6 +19,7 @@
 
 #include <cmath>
 
+#include "vsp_launch.h"
 #include "rope.h"
 
 namespace vsp_rope {
@@ -175,6 +176,7 @@ cudaError_t launch(const Args& a, cudaStream_t stream) {
     // enough resident warps to cover HBM latency: 8 CTAs of 256 threads per SM, grid-stride
     const long long want = (work + kThreads - 1) / kThreads;
     const int grid = static_cast<int>(want < 8LL * sms ? (want > 0 ? want : 1) : 8LL * sms);
+    vsp_detail::count_launch();
     if (a.half_split) rope_half_kernel<<<grid, kThreads, 0, stream>>>(a, th);
     else rope_interleaved_kernel<<<grid, kThreads, 0, stream>>>(a, th);
     return cudaGetLastError();

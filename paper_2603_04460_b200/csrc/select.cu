@@ -38,6 +38,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 
+#include "vsp_launch.h"
 #include "select.h"
 
 namespace vsp_select_k {
@@ -700,6 +701,7 @@ cudaError_t launch_impl(const float* lv, const float* ls, const float* a_v, cons
     }
     p.g0 = g0;
     const dim3 grid(count * kCluster, 2);
+    vsp_detail::count_launch();
     if (cached_slice(n))
         select_kernel<true><<<grid, kThreads, smem_bytes(n), stream>>>(p);
     else
@@ -728,6 +730,7 @@ cudaError_t launch_softmax(const float* lv, const float* ls, float* a_v, float* 
         attr = true;
     }
     const dim3 grid(count * kCluster, 2);
+    vsp_detail::count_launch();
     if (cached_slice(n))
         softmax_kernel<true><<<grid, kThreads, smem_bytes(n), stream>>>(lv, ls, a_v, a_s, n, g0);
     else

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "vsp_launch.h"
 #include "indexer.h"
 #include "sm100.cuh"
 #include "tma_host.h"
@@ -464,6 +465,7 @@ cudaError_t loss_grad(const GradArgs& a, void* workspace, cudaStream_t stream) {
     cudaError_t e = vsp_indexer::launch(ia, ws_ix, stream);
     if (e != cudaSuccess) return e;
     // 2. loss and dlogit (fp64 softmax over n)
+    vsp_detail::count_launch();
     kl_grad_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(lv, ls, a.target_v, a.target_s, a.n, a.kl_eps, dv, ds,
                                                         loss2, dbias);
     // 3. backward GEMMs
@@ -498,12 +500,15 @@ cudaError_t loss_grad(const GradArgs& a, void* workspace, cudaStream_t stream) {
         cudaFuncSetAttribute(backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr = true;
     }
+    vsp_detail::count_launch();
     backward_kernel<<<a.hkv * (a.d_h / kHid) * nsplit, kThreads, kSmemBytes, stream>>>(p);
     // 4. fixed-order reduction into the flat gradient; per-head loss = KL_v + KL_s
+    vsp_detail::count_launch();
     reduce_grads_kernel<<<592, 256, 0, stream>>>(part_wu, part_bu, part_wv, part_ws, dbias, a.hkv, a.d_h, nsplit,
                                                  a.grads);
     e = cudaGetLastError();
     if (e == cudaSuccess && a.loss) {
+        vsp_detail::count_launch();
         sum_loss_kernel<<<1, 128, 0, stream>>>(loss2, a.hkv, a.loss);
         e = cudaGetLastError();
     }
@@ -514,6 +519,7 @@ cudaError_t adamw(const AdamArgs& a, cudaStream_t stream) {
     const double t = static_cast<double>(a.step_index + 1);
     const float bc1 = static_cast<float>(1.0 - std::pow(a.beta1, t));
     const float bc2 = static_cast<float>(1.0 - std::pow(a.beta2, t));
+    vsp_detail::count_launch();
     adamw_kernel<<<592, 256, 0, stream>>>(a.params, a.grads, a.m, a.v, a.count, static_cast<float>(a.lr),
                                           static_cast<float>(a.beta1), static_cast<float>(a.beta2), bc1, bc2,
                                           static_cast<float>(a.adam_eps), static_cast<float>(a.weight_decay),

@@ -152,3 +152,18 @@ def test_recall_from_lse_matches_reference_recall(vsp):
     for h in range(hq):
         ref = oracle.ref().attention_recall(qn[:, h], kn[:, 0], *lists[0])
         assert abs(rec[h] - ref) <= 1e-3
+
+
+def test_launch_counter_attributes_kernels(vsp):
+    """vsp_kernel_launches counts this library's launches: dense = one K4 launch; sparse =
+    bitmaps + vertical gather + tile plan + one persistent K3 launch."""
+    n, hq, hkv = 300, 4, 2
+    q, k, v = qkv(n, hq, hkv, seed=21)
+    pat = pattern_tensors([([0, 5, 77], [0, 1, 9]), ([0, 200], [0, 3])], n)
+    c0 = vsp.kernel_launches()
+    vsp.blockwise_attention(q, k, v)
+    c1 = vsp.kernel_launches()
+    vsp.sparse_attention(q, k, v, pat, validate=False)
+    c2 = vsp.kernel_launches()
+    assert c1 - c0 == 1
+    assert c2 - c1 == 4
