@@ -89,6 +89,13 @@ VSP_API const char* vsp_version(void);
 /* Kernels this library has launched in this process so far (every launch site counts), so a
  * caller can attribute the device work of a region to libvsp_gpu.so. */
 VSP_API long long vsp_kernel_launches(void);
+/* Live timing of the attention (K3) launches made by the layer entry points
+ * (vsp_vs_prefill, vsp_vs_prefill_host, vsp_vs_prefill_units): when enabled, every K3 launch
+ * is bracketed by a CUDA event pair on the stream it runs on (at most 512 per read).
+ * vsp_attn_timing(ctx, 1) enables and resets; vsp_attn_timing_read waits for the recorded
+ * launches and returns their summed duration (ms) and count, then resets. */
+VSP_API int vsp_attn_timing(vsp_ctx* ctx, int enable);
+VSP_API int vsp_attn_timing_read(vsp_ctx* ctx, double* total_ms, int* launches);
 
 VSP_API int vsp_create(vsp_ctx** ctx, int device);
 VSP_API int vsp_destroy(vsp_ctx* ctx);

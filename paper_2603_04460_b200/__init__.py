@@ -26,7 +26,7 @@ import ctypes
 import dataclasses
 import math
 import os
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import torch
 
@@ -72,6 +72,8 @@ def load_library():
     lib.vsp_last_error.restype = ctypes.c_char_p
     lib.vsp_version.restype = ctypes.c_char_p
     lib.vsp_kernel_launches.restype = ctypes.c_longlong
+    lib.vsp_attn_timing.argtypes = [vp, i]
+    lib.vsp_attn_timing_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i)]
     lib.vsp_create.argtypes = [ctypes.POINTER(vp), i]
     lib.vsp_destroy.argtypes = [vp]
     lib.vsp_indexer_workspace_size.restype = sz
@@ -430,6 +432,20 @@ class _Unit(ctypes.Structure):
 def kernel_launches() -> int:
     """Kernels libvsp_gpu.so has launched in this process (vsp_kernel_launches)."""
     return int(load_library().vsp_kernel_launches())
+
+
+def attn_timing(enable: bool, device=None) -> None:
+    """Bracket every K3 launch of the layer entry points with CUDA events (vsp_attn_timing)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    _check(load_library().vsp_attn_timing(_context(dev), 1 if enable else 0))
+
+
+def attn_timing_read(device=None) -> Tuple[float, int]:
+    """-> (summed K3 milliseconds, K3 launches) since attn_timing(True) or the last read."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ms, cnt = ctypes.c_double(), ctypes.c_int()
+    _check(load_library().vsp_attn_timing_read(_context(dev), ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value
 
 
 def sparse_tile_counts(n: int, hkv: int, cap: int, device) -> torch.Tensor:

@@ -45,6 +45,12 @@ struct vsp_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_host0 = nullptr, ev_host1 = nullptr;
     cudaEvent_t ev_kv[kMaxChunks] = {}, ev_q[kMaxChunks] = {}, ev_attn[kMaxChunks] = {};
+    // optional live timing of the K3 launches of the layer entry points (vsp_attn_timing):
+    // an event pair around every attention launch, summed by vsp_attn_timing_read
+    static constexpr int kTimingSlots = 512;
+    bool timing = false;
+    int timed = 0;
+    cudaEvent_t t_beg[kTimingSlots] = {}, t_end[kTimingSlots] = {};
 };
 
 namespace {
@@ -169,6 +175,9 @@ int vsp_destroy(vsp_ctx* ctx) {
     if (!ctx) return VSP_OK;
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_flags);
+    for (int i = 0; i < vsp_ctx::kTimingSlots; ++i)
+        for (cudaEvent_t ev : {ctx->t_beg[i], ctx->t_end[i]})
+            if (ev) cudaEventDestroy(ev);
     for (cudaStream_t st : {ctx->side, ctx->h2d, ctx->d2h})
         if (st) cudaStreamDestroy(st);
     for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_host0, ctx->ev_host1})
@@ -478,6 +487,17 @@ void* attn_workspace(void* workspace, int n, int hkv, int d_h) {
     return ws;
 }
 
+// K3 (attention phase) launch, bracketed by a timing event pair when vsp_attn_timing is on.
+cudaError_t timed_attention(vsp_ctx* ctx, const vsp_attn::AttnArgs& aa, const vsp_attn::SparseArgs& sa, void* ws,
+                            cudaStream_t st, int g0, int cnt, int qb_lo = 0, int qb_hi = -1) {
+    const bool t = ctx->timing && ctx->timed < vsp_ctx::kTimingSlots;
+    cudaError_t e = cudaSuccess;
+    if (t) e = cudaEventRecord(ctx->t_beg[ctx->timed], st);
+    if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws, st, g0, cnt, 2, qb_lo, qb_hi);
+    if (t && e == cudaSuccess) e = cudaEventRecord(ctx->t_end[ctx->timed++], st);
+    return e;
+}
+
 // K1 (logits) -> K2 (softmax + selection) -> K3 plan for KV heads [g0, g0 + cnt) on `st`.
 cudaError_t enqueue_scoring(const PrefillDev& p, int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping,
                             const vsp_budget* budgets, void* workspace, int g0, int cnt, cudaStream_t st) {
@@ -534,7 +554,7 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         chunk_range(c, hkv, hpc, g0, cnt);
         if (!serial) e = cudaStreamWaitEvent(main, ctx->ev_chunk[c], 0);
         if (e == cudaSuccess && q_ready) e = cudaStreamWaitEvent(main, q_ready[c], 0);
-        if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, g0, cnt, 2);
+        if (e == cudaSuccess) e = timed_attention(ctx, aa, sa, ws_attn, main, g0, cnt);
         if (e == cudaSuccess && attn_done) e = cudaEventRecord(attn_done[c], main);
     }
     return e;
@@ -659,7 +679,7 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
         g += cnt;
     }
     for (int u = 0; u < nunits && e == cudaSuccess; ++u)
-        e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, units[u].g, 1, 2, units[u].qb_lo, units[u].qb_hi);
+        e = timed_attention(ctx, aa, sa, ws_attn, st, units[u].g, 1, units[u].qb_lo, units[u].qb_hi);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_units");
 }
 
@@ -740,7 +760,7 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
             int lo, hi;
             rows_of(c, lo, hi);
             e = cudaStreamWaitEvent(main, ctx->ev_q[c], 0);
-            if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, main, 0, hkv, 2, lo, hi);
+            if (e == cudaSuccess) e = timed_attention(ctx, aa, sa, ws_attn, main, 0, hkv, lo, hi);
             if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_attn[c], main);
         }
         for (int c = 0; c < rc_chunks && e == cudaSuccess; ++c) {
@@ -795,4 +815,36 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
     if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_host1, ctx->d2h);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ctx->ev_host1, 0);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_host");
+}
+
+// ------------------------------------------------------------------ live K3 timing
+extern "C" int vsp_attn_timing(vsp_ctx* ctx, int enable) {
+    VSP_CHECK_CTX(ctx);
+    for (int i = 0; enable && i < vsp_ctx::kTimingSlots; ++i) {
+        for (cudaEvent_t* ev : {&ctx->t_beg[i], &ctx->t_end[i]}) {
+            if (*ev) continue;
+            const cudaError_t e = cudaEventCreate(ev);
+            if (e != cudaSuccess) return cuda_err(e, "vsp_attn_timing");
+        }
+    }
+    ctx->timing = enable != 0;
+    ctx->timed = 0;
+    return VSP_OK;
+}
+
+extern "C" int vsp_attn_timing_read(vsp_ctx* ctx, double* total_ms, int* launches) {
+    VSP_CHECK_CTX(ctx);
+    if (!total_ms || !launches) return set_err(VSP_EINVAL, "vsp_attn_timing_read: null output");
+    double sum = 0.0;
+    for (int i = 0; i < ctx->timed; ++i) {
+        cudaError_t e = cudaEventSynchronize(ctx->t_end[i]);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ctx->t_beg[i], ctx->t_end[i]);
+        if (e != cudaSuccess) return cuda_err(e, "vsp_attn_timing_read");
+        sum += ms;
+    }
+    *total_ms = sum;
+    *launches = ctx->timed;
+    ctx->timed = 0;
+    return VSP_OK;
 }

@@ -167,3 +167,22 @@ def test_launch_counter_attributes_kernels(vsp):
     c2 = vsp.kernel_launches()
     assert c1 - c0 == 1
     assert c2 - c1 == 4
+
+
+def test_attn_timing_brackets_layer_k3_launches(vsp):
+    """vsp_attn_timing: one event pair per K3 launch of the layer entry point."""
+    from paper_2603_04460_b200.synth import planted_layer
+    n, hq, hkv = 2048, 8, 4
+    q, k, v, _ = planted_layer(n, hq, hkv, seed=4)
+    g = torch.Generator().manual_seed(2)
+    params = vsp.make_indexer_params(hkv, 128, 256, g, head_sigma=0.4)
+    budget = vsp.BudgetConfig(0.5, 0.5, 1, None)
+    vsp.attn_timing(True)
+    for hpc in (0, 0, 1):  # one chunk, one chunk, four chunks
+        vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc)
+    ms, cnt = vsp.attn_timing_read()
+    vsp.attn_timing(False)
+    assert cnt == 1 + 1 + 4
+    assert ms > 0.0
+    vsp.vs_prefill(q, k, v, params, budget)
+    assert vsp.attn_timing_read() == (0.0, 0)
