@@ -58,7 +58,7 @@ struct Smem {
     uint64_t q_full, q_free;                  // Q tiles of the current work item
     uint64_t k_full[kNumK], k_empty[kNumK];
     uint64_t v_full[kNumV], v_empty[kNumV];
-    uint64_t s_full[2], p_full[2], o_done[2];
+    uint64_t s_full[2], p_half[2], p_full[2], o_done[2];  // p_half: P columns [0, 64) written
     uint64_t o_free[2];                       // epilogue has read O_w (next item may PV into it)
     uint64_t item_full[kItemRing], item_empty[kItemRing];
     int item[kItemRing];                      // work item index, -1 = no more work
@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         for (int w = 0; w < 2; ++w) {
             mbar_init(&sm.s_full[w], 1);
+            mbar_init(&sm.p_half[w], 4);
             mbar_init(&sm.p_full[w], 4);
             mbar_init(&sm.o_done[w], 1);
             mbar_init(&sm.o_free[w], 4);
@@ -234,12 +235,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sV), kHalfBytes, 1024);
         // gj: global tile index (ring slots and s/p barrier phases continue across items);
         // first: the item's first PV overwrites O (accumulate = 0)
-        auto issue_pv = [&](int w, int gjj, bool first) {
+        // half h of PV: K-steps [4h, 4h + 4), i.e. P columns [64h, 64h + 64) (TMEM [32h, 32h + 32))
+        // against V rows [64h, 64h + 64); the softmax publishes the two halves separately
+        auto issue_pv = [&](int w, int gjj, bool first, int h) {
             const uint64_t vd = v_desc0 + static_cast<uint64_t>(((gjj % kNumV) * kTileBytes) >> 4);
             const uint32_t o_t = tmem + 256 + w * 128;
             const uint32_t p_t = tmem + w * 128;
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 4 * h; k < 4 * h + 4; ++k)
                 umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
                         (!first || k > 0) ? 1u : 0u);
         };
@@ -282,15 +285,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 tc_fence_after();
                 for (int w = 0; w < 2; ++w) {
                     if (j > 0) {
-                        mbar_wait(&sm.p_full[w], (G - 1) & 1);
+                        // first half of P(j-1): its PV overlaps the softmax's second half
+                        mbar_wait(&sm.p_half[w], (G - 1) & 1);
                         if (w == 0) mbar_wait(&sm.v_full[(G - 1) % kNumV], ((G - 1) / kNumV) & 1);
                         // the item's first PV writes O_w: the previous item's epilogue must be done
                         if (j == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
                         tc_fence_after();
+                        if (elect_one()) issue_pv(w, G - 1, j == 1, 0);
+                        __syncwarp();
+                        mbar_wait(&sm.p_full[w], (G - 1) & 1);
+                        tc_fence_after();
                     }
                     if (elect_one()) {
                         if (j > 0) {
-                            issue_pv(w, G - 1, j == 1);
+                            issue_pv(w, G - 1, false, 1);
                             if (w == 1) umma_commit(&sm.v_empty[(G - 1) % kNumV]);
                         }
                         issue_s(w, G);
@@ -305,12 +313,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             }
             const int GL = gj + nt - 1;
             for (int w = 0; w < 2; ++w) {
-                mbar_wait(&sm.p_full[w], GL & 1);
+                mbar_wait(&sm.p_half[w], GL & 1);
                 if (w == 0) mbar_wait(&sm.v_full[GL % kNumV], (GL / kNumV) & 1);
                 if (nt == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
                 tc_fence_after();
+                if (elect_one()) issue_pv(w, GL, nt == 1, 0);
+                __syncwarp();
+                mbar_wait(&sm.p_full[w], GL & 1);
+                tc_fence_after();
                 if (elect_one()) {
-                    issue_pv(w, GL, nt == 1);
+                    issue_pv(w, GL, false, 1);
                     umma_commit(&sm.o_done[w]);
                     if (w == 1) umma_commit(&sm.v_empty[GL % kNumV]);
                 }
@@ -486,6 +498,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         pk[t] = pack_bf16x2(e.x, e.y);
                     }
                     tmem_st16(s_t + c * 16, pk);
+                    if (c == 1) {  // P columns [0, 64) are in TMEM: the first PV half may start
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&sm.p_half[w]);
+                    }
                     if (c < 3) tmem_wait_ld(u[(c + 1) & 1]);
                 }
             }
