@@ -16,7 +16,12 @@
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_h (bf16) aliases
 // the first 64 columns of S_h. The MMA order PV_h(j-1) -> S_h(j) keeps the alias safe
 // because tcgen05.mma executes in issue order; the S_full commit after S_h(j) therefore
-// also proves PV_h(j-1) finished, which is when the softmax warps may rescale O_h.
+// also proves PV_h(j-1) finished, which is when the softmax warps may rescale O_h. P is
+// published in two halves (p_half: keys 0-63, p_full: keys 64-127), so the first half of
+// PV_h(j-1) runs while the softmax still computes the second half's exponentials.
+// Cross-item barriers: q_full/q_free (the Q tiles of the current item), o_free (the
+// epilogue has read O_h, so the next item's first PV may overwrite it), and a two-slot smem
+// ring that carries each fetched item index from the producer to the other warps.
 // Online softmax runs in the exp2 domain with lazy rescaling (only when the running max
 // grows by more than 2^8), exactly the same math as the reference's per-row rescale.
 //
