@@ -270,6 +270,10 @@ def run_reference(args):
     q, k, v = synth_layer(args, dev)
     threads = os.cpu_count() or 1
     rows = args.cpu_sample
+    # keep the whole --steps K --warmup W run to a few minutes: past 5 samples the row prefix
+    # shrinks so that K + W samples cost about as much as 5 default ones
+    if args.steps + args.warmup > 5:
+        rows = max(2048, (args.cpu_sample * 5 // (args.steps + args.warmup)) // 128 * 128)
     for _ in range(args.warmup):
         cpu_reference(args, q, k, v, params, budget, rows, threads)
     ts = []
