@@ -158,11 +158,12 @@ inline SelectedIndices select_pattern(const VSScores& scores, const BudgetConfig
 namespace detail {
 inline AttentionOutput attend(const AttentionInputs& in, const SparsePattern* pat) {
     const int n = static_cast<int>(in.n()), d = static_cast<int>(in.d());
-    auto q = upload_bf16(in.q, 2), k = upload_bf16(in.k), v = upload_bf16(in.v);
-    Buf o(static_cast<size_t>(n) * 2 * d * 2), lse(static_cast<size_t>(n) * 2 * 4);
+    // one head: a single-head group (the kernels pair Q heads; an odd group's last pair holds one)
+    auto q = upload_bf16(in.q), k = upload_bf16(in.k), v = upload_bf16(in.v);
+    Buf o(static_cast<size_t>(n) * d * 2), lse(static_cast<size_t>(n) * 4);
     const float scale = static_cast<float>(in.scale);
     if (!pat) {
-        check(vsp_dense_attn_fwd(context(), q->p, k->p, v->p, n, 2, 1, d, scale, o.p, lse.as<float>(), nullptr));
+        check(vsp_dense_attn_fwd(context(), q->p, k->p, v->p, n, 1, 1, d, scale, o.p, lse.as<float>(), nullptr));
     } else {
         const int cap = static_cast<int>(std::max(pat->i_v.size(), pat->i_s.size())) + 1;
         std::vector<int> hv(cap, 0), hs(cap, 0);
@@ -174,12 +175,12 @@ inline AttentionOutput attend(const AttentionInputs& in, const SparsePattern* pa
         cuda(cudaMemcpy(is.p, hs.data(), cap * 4, cudaMemcpyHostToDevice));
         cuda(cudaMemcpy(kv.p, &cnt[0], 4, cudaMemcpyHostToDevice));
         cuda(cudaMemcpy(ks.p, &cnt[1], 4, cudaMemcpyHostToDevice));
-        check(vsp_vs_attn_fwd(context(), q->p, k->p, v->p, n, 2, 1, d, iv.as<int>(), kv.as<int>(), is.as<int>(),
+        check(vsp_vs_attn_fwd(context(), q->p, k->p, v->p, n, 1, 1, d, iv.as<int>(), kv.as<int>(), is.as<int>(),
                               ks.as<int>(), cap, scale, o.p, lse.as<float>(), wsp.p, VSP_VALIDATE, nullptr));
     }
     cuda(cudaDeviceSynchronize());
     AttentionOutput out;
-    out.o = download_head0(o, n, d, 2);
+    out.o = download_head0(o, n, d, 1);
     return out;
 }
 }  // namespace detail

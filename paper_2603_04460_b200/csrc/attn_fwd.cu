@@ -72,7 +72,7 @@ struct Smem {
 
 // Work item it (heaviest query blocks first: causal work grows with the block index).
 struct Item {
-    int qb, h0, g, num_tiles, vcnt0;
+    int qb, h0, h1, g, num_tiles, vcnt0;  // Q heads h0, h1 (h1 == h0: odd group, one head)
     const int* tiles;
 };
 
@@ -110,8 +110,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     auto item = [&](int it) {
         Item x;
         x.qb = p.qb_hi - 1 - it / p.npairs;
-        x.h0 = 2 * (p.pair0 + it % p.npairs);
-        x.g = x.h0 / (p.hq / p.hkv);
+        // pair index -> (KV group, pair within the group); an odd group's last pair carries
+        // one head (both Q tiles load it, only tile 0 writes)
+        const int grp = p.hq / p.hkv, ppg = (grp + 1) >> 1;
+        const int pi = p.pair0 + it % p.npairs;
+        x.g = pi / ppg;
+        x.h0 = x.g * grp + 2 * (pi % ppg);
+        x.h1 = min(x.h0 + 1, x.g * grp + grp - 1);
         x.vcnt0 = 0;
         x.tiles = nullptr;
         if constexpr (kSparse) {
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 for (int w = 0; w < 2; ++w)
                     for (int hf = 0; hf < 2; ++hf)
                         tma_load_3d(sQ + w * kTileBytes + hf * kHalfBytes, &p.map_q, &sm.q_full, hf * 64,
-                                    x.h0 + w, x.qb * kBlock);
+                                    w ? x.h1 : x.h0, x.qb * kBlock);
             }
             __syncwarp();
             for (int j = 0; j < x.num_tiles; ++j, ++gj) {
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const int it = next_item(n_it);
         if (it < 0) break;
         const Item x = item(it);
-        const int qb = x.qb, h0 = x.h0, g = x.g, num_tiles = x.num_tiles, vcnt0 = x.vcnt0;
+        const int qb = x.qb, g = x.g, num_tiles = x.num_tiles, vcnt0 = x.vcnt0;
         const int* tiles = x.tiles;
         (void)tiles;
         (void)vcnt0;
@@ -522,7 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // ---- epilogue: O / l -> bf16 [n, Hq, d]; LSE (natural log of sum exp(scaled logits))
         mbar_wait(&sm.o_done[w], n_it & 1);
         tc_fence_after();
-        const int h = h0 + w;
+        const int h = w ? x.h1 : x.h0;
+        const bool store = w == 0 || x.h1 != x.h0;  // a duplicated head is written once
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16* orow = p.o + static_cast<long long>(i) * p.o_tok_stride + static_cast<long long>(h) * p.o_head_stride;
 #pragma unroll
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #pragma unroll
                 for (int t = 0; t < 32; ++t) u[t] = 0u;
             }
-            if (i < p.n) {
+            if (i < p.n && store) {
                 uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -547,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 }
             }
         }
-        if (i < p.n && p.lse != nullptr)
+        if (i < p.n && store && p.lse != nullptr)
             p.lse[static_cast<size_t>(h) * p.n + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
         // O_w has been read: the next item's first PV may overwrite it
         tc_fence_before();
@@ -745,7 +751,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     }
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     p.pair0 = 0;
-    p.npairs = a.hq / 2;
+    p.npairs = a.hkv * ((a.hq / a.hkv + 1) / 2);
     p.qb_hi = num_qb;
     p.items = num_qb * p.npairs;
     void* work = nullptr;
@@ -837,7 +843,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
             cudaFuncSetAttribute(attn_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
             attr_set = true;
         }
-        const int pairs_per_group = (a.hq / a.hkv) / 2;
+        const int pairs_per_group = (a.hq / a.hkv + 1) / 2;
         p.pair0 = g0 * pairs_per_group;
         p.npairs = count * pairs_per_group;
         // query blocks [qb_lo, qb_hi) only (a balanced work unit of a multi-GPU split)

@@ -120,8 +120,6 @@ int check_attn_shapes(int n, int hq, int hkv, int d) {
     if (n < 1) return set_err(VSP_EINVAL, "attention inputs: empty sequence");
     if (hkv < 1 || hq < hkv || hq % hkv != 0)
         return set_err(VSP_EINVAL, "attention inputs: hq must be a positive multiple of hkv");
-    if ((hq / hkv) % 2 != 0)
-        return set_err(VSP_EINVAL, "vsp: GQA group size must be even (two Q heads per CTA)");
     if (d != 128) return set_err(VSP_EINVAL, "vsp: head dim must be 128");
     return VSP_OK;
 }

@@ -22,7 +22,8 @@ def vsp():
     return m
 
 
-@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (7, 4, 2), (128, 4, 1), (300, 4, 2), (512, 8, 2)])
+@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (7, 4, 2), (128, 4, 1), (300, 4, 2), (512, 8, 2),
+                                     (1, 1, 1), (200, 4, 4), (300, 3, 1), (130, 6, 2)])  # MHA and odd groups
 def test_dense_matches_oracle(vsp, n, hq, hkv):
     q, k, v = qkv(n, hq, hkv, seed=n)
     o, lse = vsp.blockwise_attention(q, k, v)
@@ -55,7 +56,8 @@ def _random_pattern(rng, n, kv, ks):
 
 
 @pytest.mark.parametrize("n,hq,hkv,kv,ks", [(64, 2, 1, 5, 4), (300, 4, 2, 20, 12), (512, 4, 1, 40, 30),
-                                            (700, 8, 2, 100, 60)])
+                                            (700, 8, 2, 100, 60),
+                                            (256, 2, 2, 10, 8), (300, 3, 1, 20, 12), (384, 6, 2, 30, 16)])
 def test_sparse_matches_masked_oracle(vsp, n, hq, hkv, kv, ks):
     rng = np.random.default_rng(n)
     q, k, v = qkv(n, hq, hkv, seed=n + 1)
@@ -186,3 +188,22 @@ def test_attn_timing_brackets_layer_k3_launches(vsp):
     assert ms > 0.0
     vsp.vs_prefill(q, k, v, params, budget)
     assert vsp.attn_timing_read() == (0.0, 0)
+
+
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (6, 2)])
+def test_layer_call_mha_and_odd_groups(vsp, hq, hkv):
+    """Group sizes 1 (MHA) and 3: the one-call layer equals the operator chain, and each Q head
+    matches the oracle on its KV head's pattern."""
+    n = 640
+    q, k, v = qkv(n, hq, hkv, seed=31)
+    g = torch.Generator().manual_seed(8)
+    params = vsp.make_indexer_params(hkv, 128, 256, g, head_sigma=0.5)
+    budget = vsp.BudgetConfig(0.5, 0.5, 1, None)
+    a_v, a_s = vsp.indexer_forward(k, v, params)
+    pat = vsp.select_pattern(a_v, a_s, budget)
+    o_ref, lse_ref = vsp.sparse_attention(q, k, v, pat)
+    o, lse, _ = vsp.vs_prefill(q, k, v, params, budget)
+    assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)
+    lists = [pat.lists(h) for h in range(hkv)]
+    o_or, lse_or = oracle_sparse(q, k, v, lists)
+    assert_attn_close(o, lse, o_or, lse_or)
