@@ -202,9 +202,9 @@ inline AttentionOutput blockwise_attention(const AttentionInputs& in, std::size_
 inline VSScores aggregate_streaming(const AttentionInputs& in, std::size_t block, bool normalized = true) {
     require(block >= 1, "aggregate_streaming: block must be >= 1");
     const int n = static_cast<int>(in.n()), d = static_cast<int>(in.d());
-    auto q = detail::upload_bf16(in.q, 2), k = detail::upload_bf16(in.k);
-    detail::Buf av(n * 4), as(n * 4), wsp(vsp_aggregate_workspace_size(n, 2));
-    detail::check(vsp_vs_aggregate(detail::context(), q->p, k->p, n, 2, 1, d, static_cast<float>(in.scale), nullptr,
+    auto q = detail::upload_bf16(in.q), k = detail::upload_bf16(in.k);
+    detail::Buf av(n * 4), as(n * 4), wsp(vsp_aggregate_workspace_size(n, 1));
+    detail::check(vsp_vs_aggregate(detail::context(), q->p, k->p, n, 1, 1, d, static_cast<float>(in.scale), nullptr,
                                    VSP_REDUCE_MEAN, normalized ? 1 : 0, av.as<float>(), as.as<float>(), wsp.p,
                                    nullptr));
     VSScores s;

@@ -46,7 +46,8 @@ def _close(got, want):
     assert (err <= 2e-2 * np.abs(want) + 2e-6).all(), f"max err {err.max():.3e}"
 
 
-@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (200, 2, 1), (300, 4, 2), (777, 4, 1), (1100, 8, 2)])
+@pytest.mark.parametrize("n,hq,hkv", [(1, 2, 1), (200, 2, 1), (300, 4, 2), (777, 4, 1), (1100, 8, 2),
+                                     (260, 1, 1), (300, 3, 1), (400, 6, 2)])  # MHA and odd groups
 def test_aggregate_matches_oracle(vsp, n, hq, hkv):
     q, k, _ = qkv(n, hq, hkv, seed=n, scale=0.7)
     a_v, a_s = vsp.aggregate_streaming(q, k)
