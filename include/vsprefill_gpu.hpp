@@ -9,6 +9,7 @@
 //   vsp::gpu::select_pattern       <- vsp::select_pattern       sparsity.hpp:105
 //   vsp::gpu::sparse_attention     <- vsp::sparse_attention     attention.hpp:150
 //   vsp::gpu::blockwise_attention  <- vsp::blockwise_attention  attention.hpp:96
+//   vsp::gpu::attention_recall     <- vsp::attention_recall     attention.hpp:198 (from inputs)
 //   vsp::gpu::aggregate_streaming  <- vsp::aggregate_streaming  vsaggregate.hpp:62
 //   vsp::gpu::apply_rope           <- vsp::apply_rope           rope.hpp:63-79
 //   vsp::gpu::indexer_backward     <- vsp::indexer_backward     indexer.hpp:275 (Forward KL)
@@ -23,7 +24,7 @@
 // reference's message, anything else -> std::runtime_error. `block` arguments are accepted
 // for signature compatibility; the GPU tiling is fixed (results do not depend on it, as in
 // the reference, test_attention.cpp:145-155). The single-head API runs on the batched
-// kernels with one KV head and the Q head duplicated (the CTA processes Q-head pairs).
+// kernels as one-head groups (one KV head, one Q head).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -156,11 +157,15 @@ inline SelectedIndices select_pattern(const VSScores& scores, const BudgetConfig
 }
 
 namespace detail {
-inline AttentionOutput attend(const AttentionInputs& in, const SparsePattern* pat) {
+// Runs K4 (pat null) or K3 on one head; the row LSEs stay on the device in `lse_out` when given.
+inline AttentionOutput attend(const AttentionInputs& in, const SparsePattern* pat,
+                              std::unique_ptr<Buf>* lse_out = nullptr) {
     const int n = static_cast<int>(in.n()), d = static_cast<int>(in.d());
     // one head: a single-head group (the kernels pair Q heads; an odd group's last pair holds one)
     auto q = upload_bf16(in.q), k = upload_bf16(in.k), v = upload_bf16(in.v);
-    Buf o(static_cast<size_t>(n) * d * 2), lse(static_cast<size_t>(n) * 4);
+    Buf o(static_cast<size_t>(n) * d * 2);
+    auto lse_buf = std::make_unique<Buf>(static_cast<size_t>(n) * 4);
+    Buf& lse = *lse_buf;
     const float scale = static_cast<float>(in.scale);
     if (!pat) {
         check(vsp_dense_attn_fwd(context(), q->p, k->p, v->p, n, 1, 1, d, scale, o.p, lse.as<float>(), nullptr));
@@ -181,6 +186,7 @@ inline AttentionOutput attend(const AttentionInputs& in, const SparsePattern* pa
     cuda(cudaDeviceSynchronize());
     AttentionOutput out;
     out.o = download_head0(o, n, d, 1);
+    if (lse_out) *lse_out = std::move(lse_buf);
     return out;
 }
 }  // namespace detail
@@ -196,6 +202,23 @@ inline AttentionOutput sparse_attention(const AttentionInputs& in, const SparseP
 inline AttentionOutput blockwise_attention(const AttentionInputs& in, std::size_t block) {
     require(block >= 1, "blockwise_attention: block must be >= 1");
     return detail::attend(in, nullptr);
+}
+
+// attention.hpp:198-215 without the n x n matrix: the reference takes the dense attention
+// weights A; on the device the covered mass of row i is exp(LSE_sparse_i - LSE_dense_i), so
+// this overload takes the inputs A was formed from and returns the same mean over rows
+// (vsp_recall_from_lse, exact up to the kernels' LSE tolerance).
+inline double attention_recall(const AttentionInputs& in, const SparsePattern& pat) {
+    const int n = static_cast<int>(in.n());
+    std::unique_ptr<detail::Buf> lse_s, lse_d;
+    detail::attend(in, &pat, &lse_s);
+    detail::attend(in, nullptr, &lse_d);
+    detail::Buf r(4);
+    detail::check(vsp_recall_from_lse(detail::context(), lse_s->as<float>(), lse_d->as<float>(), n, 1, r.as<float>(),
+                                      nullptr));
+    float h = 0.f;
+    detail::cuda(cudaMemcpy(&h, r.p, 4, cudaMemcpyDeviceToHost));
+    return h;
 }
 
 // vsaggregate.hpp:62-127 (one head; the group combine of the batched API is the identity)

@@ -57,6 +57,24 @@ int main() {
         det = "max|d|=" + std::to_string(worst);
         return worst <= 2e-2;
     });
+    // AttentionRecall (test_attention.cpp:172-235): the reference's recall over the dense
+    // weights A = attention_matrix(q, k) vs the device recall from the two LSEs
+    check("attention_recall_from_lse", [](std::string& det) {
+        Rng rng(99);
+        double worst = 0.0;
+        for (size_t n : {64, 257}) {
+            const AttentionInputs in(oracle::random_matrix(rng, n, 128), oracle::random_matrix(rng, n, 128),
+                                     oracle::random_matrix(rng, n, 128));
+            SparsePattern pat;
+            for (size_t j = 0; j < n; j += 5) pat.i_v.push_back(j);
+            pat.i_s = {0, 2, 7};
+            const double want = vsp::attention_recall(vsp::attention_matrix(in.q, in.k), pat);
+            const double got = vsp::gpu::attention_recall(in, pat);
+            worst = std::max(worst, std::fabs(got - want));
+        }
+        det = "max|d recall|=" + std::to_string(worst);
+        return worst <= 2e-3;
+    });
     // SparseAttention.UncoveredRowThrows (test_attention.cpp:157-170)
     check("uncovered_row_throws", [](std::string& det) {
         Rng rng(1);
