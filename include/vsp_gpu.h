@@ -37,6 +37,10 @@
  * text (e.g. "uncovered query row 0") in vsp_last_error() (thread-local). Calls are
  * stream-ordered and asynchronous unless a flag asks for validation. There is no CPU
  * fallback: without a sm_100 device every compute call returns VSP_ECUDA.
+ *
+ * Concurrency: calls on different streams may run concurrently as long as each in-flight
+ * call has its own workspace (the attention kernels keep their work-queue counters there;
+ * the dense kernel, which takes no workspace, rotates through 256 internal counters).
  */
 #ifndef VSP_GPU_H
 #define VSP_GPU_H

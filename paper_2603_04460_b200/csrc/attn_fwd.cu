@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "vsp_launch.h"
@@ -723,8 +724,12 @@ static bool make_qkv_maps(AttnParams& p, const void* q, const void* k, const voi
            vsp_host::make_map_bf16(&p.map_v, v, 3, dk, sk, box);
 }
 
-// work counters of the dense kernel (zero at module load, reset by each launch's last CTA)
-__device__ int g_dense_work[2];
+// work counters of the dense kernel (zero at module load, reset by each launch's last CTA);
+// every launch takes the next of kDenseSlots pairs, so launches in flight on different
+// streams (up to kDenseSlots of them) never share a counter
+constexpr int kDenseSlots = 256;
+__device__ int g_dense_work[2 * kDenseSlots];
+std::atomic<unsigned> g_dense_slot{0};
 
 // persistent grid: one CTA per SM (the kernel's smem allows one), never more than the items
 int persistent_grid(int items) {
@@ -756,7 +761,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     p.items = num_qb * p.npairs;
     void* work = nullptr;
     cudaGetSymbolAddress(&work, g_dense_work);
-    p.work = static_cast<int*>(work);
+    p.work = static_cast<int*>(work) + 2 * (g_dense_slot.fetch_add(1, std::memory_order_relaxed) % kDenseSlots);
     vsp_detail::count_launch();
     attn_fwd_kernel<false><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
     return cudaGetLastError();

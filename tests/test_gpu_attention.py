@@ -207,3 +207,26 @@ def test_layer_call_mha_and_odd_groups(vsp, hq, hkv):
     lists = [pat.lists(h) for h in range(hkv)]
     o_or, lse_or = oracle_sparse(q, k, v, lists)
     assert_attn_close(o, lse, o_or, lse_or)
+
+
+def test_concurrent_dense_launches_on_two_streams(vsp):
+    """The persistent kernel's work counter is per launch: overlapping launches on two
+    streams give the same bits as back-to-back ones."""
+    n, hq, hkv = 4096, 8, 2
+    q1, k1, v1 = qkv(n, hq, hkv, seed=41)
+    q2, k2, v2 = qkv(n, hq, hkv, seed=42)
+    ref1 = vsp.blockwise_attention(q1, k1, v1)
+    ref2 = vsp.blockwise_attention(q2, k2, v2)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            a = vsp.blockwise_attention(q1, k1, v1)
+        with torch.cuda.stream(s2):
+            b = vsp.blockwise_attention(q2, k2, v2)
+        outs.append((a, b))
+    torch.cuda.synchronize()
+    for a, b in outs:
+        assert torch.equal(a[0], ref1[0]) and torch.equal(a[1], ref1[1])
+        assert torch.equal(b[0], ref2[0]) and torch.equal(b[1], ref2[1])
