@@ -141,7 +141,10 @@ _ws_cache: dict = {}
 
 
 def _workspace(device, nbytes: int) -> torch.Tensor:
-    key = (str(device), "ws")
+    """Scratch for the calls on the current stream (one buffer per (device, stream), so calls
+    on different streams may overlap; the C ABI's contract is one workspace per in-flight call)."""
+    dev = torch.device(device)
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)

@@ -230,3 +230,24 @@ def test_concurrent_dense_launches_on_two_streams(vsp):
     for a, b in outs:
         assert torch.equal(a[0], ref1[0]) and torch.equal(a[1], ref1[1])
         assert torch.equal(b[0], ref2[0]) and torch.equal(b[1], ref2[1])
+
+
+def test_concurrent_sparse_calls_on_two_streams(vsp):
+    """Python-level workspaces are per stream: overlapping sparse calls stay correct."""
+    n, hq, hkv = 2048, 8, 2
+    rng = np.random.default_rng(5)
+    q, k, v = qkv(n, hq, hkv, seed=43)
+    pats = [pattern_tensors([_random_pattern(rng, n, 300, 40) for _ in range(hkv)], n) for _ in range(2)]
+    refs = [vsp.sparse_attention(q, k, v, p) for p in pats]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            a = vsp.sparse_attention(q, k, v, pats[0], validate=False)
+        with torch.cuda.stream(s2):
+            b = vsp.sparse_attention(q, k, v, pats[1], validate=False)
+        outs.append((a, b))
+    torch.cuda.synchronize()
+    for a, b in outs:
+        assert torch.equal(a[0], refs[0][0]) and torch.equal(b[0], refs[1][0])
