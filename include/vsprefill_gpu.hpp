@@ -7,6 +7,7 @@
 //
 //   vsp::gpu::indexer_forward      <- vsp::indexer_forward      indexer.hpp:116
 //   vsp::gpu::select_pattern       <- vsp::select_pattern       sparsity.hpp:105
+//   vsp::gpu::cumulative_budget    <- vsp::cumulative_budget    sparsity.hpp:51
 //   vsp::gpu::sparse_attention     <- vsp::sparse_attention     attention.hpp:150
 //   vsp::gpu::blockwise_attention  <- vsp::blockwise_attention  attention.hpp:96
 //   vsp::gpu::attention_recall     <- vsp::attention_recall     attention.hpp:198 (from inputs)
@@ -154,6 +155,24 @@ inline SelectedIndices select_pattern(const VSScores& scores, const BudgetConfig
     sel.i_v.assign(a.begin(), a.end());
     sel.i_s.assign(c.begin(), c.end());
     return sel;
+}
+
+// sparsity.hpp:51-79: k of one score vector under the cumulative threshold, computed by the
+// selection kernel (its vertical direction; the same exactness guard, so bit-identical k
+// for scores exactly representable in fp32). The slash direction is fed the same vector.
+inline std::size_t cumulative_budget(const std::vector<double>& scores, double tau, const BudgetConfig& cfg) {
+    cfg.check();
+    require(tau > 0.0 && tau <= 1.0, "cumulative_budget: tau must be in (0, 1]");
+    require(!scores.empty(), "cumulative_budget: empty scores");
+    const int n = static_cast<int>(scores.size());
+    auto a = detail::upload_f32(scores);
+    detail::Buf iv((n + 1) * 4), is((n + 1) * 4), kv(4), ks(4), wsp(vsp_select_workspace_size(n, 1));
+    vsp_budget b{tau, tau, static_cast<int64_t>(cfg.min_budget), cfg.max_budget ? static_cast<int64_t>(*cfg.max_budget) : -1};
+    detail::check(vsp_select(detail::context(), a->as<float>(), a->as<float>(), n, 1, &b, iv.as<int>(), kv.as<int>(),
+                             is.as<int>(), ks.as<int>(), n + 1, wsp.p, VSP_VALIDATE, nullptr));
+    int k = 0;
+    detail::cuda(cudaMemcpy(&k, kv.p, 4, cudaMemcpyDeviceToHost));
+    return static_cast<std::size_t>(k);
 }
 
 namespace detail {

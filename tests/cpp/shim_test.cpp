@@ -75,6 +75,37 @@ int main() {
         det = "max|d recall|=" + std::to_string(worst);
         return worst <= 2e-3;
     });
+    // CumulativeBudget.DyadicHandValues (test_sparsity.cpp:22-32) + random distributions
+    check("cumulative_budget_matches_reference", [](std::string& det) {
+        const std::vector<double> dy = {0.5, 0.25, 0.125, 0.125};
+        BudgetConfig cfg;
+        int bad = 0, trials = 0;
+        for (double tau : {0.1, 0.5, 0.6, 0.75, 0.8, 0.875, 0.9, 1.0}) {
+            ++trials;
+            if (vsp::gpu::cumulative_budget(dy, tau, cfg) != vsp::cumulative_budget(dy, tau, cfg)) ++bad;
+        }
+        Rng rng(17);
+        for (int t = 0; t < 12; ++t) {
+            std::vector<double> s = oracle::random_distribution(rng, 100 + 97 * t);
+            for (double& x : s) x = static_cast<double>(static_cast<float>(x));  // fp32-exact scores
+            double sum = 0.0;
+            for (double x : s) sum += x;
+            for (double& x : s) x /= sum;
+            for (double& x : s) x = static_cast<double>(static_cast<float>(x));
+            for (double tau : {0.3, 0.9}) {
+                BudgetConfig c2;
+                c2.min_budget = 2;
+                ++trials;
+                try {
+                    if (vsp::gpu::cumulative_budget(s, tau, c2) != vsp::cumulative_budget(s, tau, c2)) ++bad;
+                } catch (const std::invalid_argument&) {  // both must reject the same inputs
+                    try { vsp::cumulative_budget(s, tau, c2); ++bad; } catch (const std::invalid_argument&) {}
+                }
+            }
+        }
+        det = std::to_string(trials - bad) + "/" + std::to_string(trials) + " equal";
+        return bad == 0;
+    });
     // SparseAttention.UncoveredRowThrows (test_attention.cpp:157-170)
     check("uncovered_row_throws", [](std::string& det) {
         Rng rng(1);
