@@ -335,7 +335,7 @@ def sparse_tile_stats(n: int, hkv: int, cap: int, device, per_head: bool = False
     """(KV tiles visited by the last sparse_attention on `device`, tiles dense would visit)
     summed over query blocks and KV heads [, tiles per KV head]. Synchronises the stream."""
     lib = load_library()
-    ws = _ws_cache[(str(device), "ws")]
+    ws = _workspace(device, 0)  # the current stream's scratch, which holds that call's plan
     out = (ctypes.c_int64 * (2 + hkv))()
     _check(lib.vsp_vs_attn_tile_stats(_context(device), n, hkv, cap, _ptr(ws), out, _stream(device)))
     if per_head:
@@ -523,7 +523,7 @@ def vs_prefill_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: I
     lse = lse if lse is not None else torch.empty(hq, n, dtype=torch.float32, pin_memory=True)
     kv = torch.empty(hkv, dtype=torch.int32, pin_memory=True) if budgets_out else None
     ks = torch.empty(hkv, dtype=torch.int32, pin_memory=True) if budgets_out else None
-    key = (str(dev), "host_ws")
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, "host")
     need = lib.vsp_vs_prefill_host_workspace_size(n, hq, hkv, params.d_h)
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < need:

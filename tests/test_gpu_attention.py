@@ -251,3 +251,18 @@ def test_concurrent_sparse_calls_on_two_streams(vsp):
     torch.cuda.synchronize()
     for a, b in outs:
         assert torch.equal(a[0], refs[0][0]) and torch.equal(b[0], refs[1][0])
+
+
+def test_tile_stats_and_counts_describe_the_last_plan(vsp):
+    """sparse_tile_stats / sparse_tile_counts read the plan of the last sparse_attention on the
+    current stream: totals agree, per-head sums agree, and sparse never exceeds dense."""
+    n, hq, hkv = 1500, 4, 2
+    rng = np.random.default_rng(12)
+    q, k, v = qkv(n, hq, hkv, seed=12)
+    pat = pattern_tensors([_random_pattern(rng, n, 200, 30) for _ in range(hkv)], n)
+    vsp.sparse_attention(q, k, v, pat, validate=False)
+    tiles, dense, per_head = vsp.sparse_tile_stats(n, hkv, n + 1, q.device, per_head=True)
+    counts = vsp.sparse_tile_counts(n, hkv, n + 1, q.device)
+    assert 0 < tiles <= dense
+    assert sum(per_head) == tiles == int(counts.sum())
+    assert counts.sum(1).tolist() == per_head
