@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <vector>
 
@@ -92,7 +93,12 @@ VSP_DEVICE void window128(const uint32_t* __restrict__ bm, int start, int nwords
     for (int k = 0; k < 4; ++k) w[k] = __funnelshift_r(raw[k], raw[k + 1], sh);
 }
 
-template <bool kSparse>
+// kMc = 2: a two-CTA cluster runs the two Q-head pairs of a 4-head group on the same query
+// block in lockstep (identical tile lists); each CTA TMA-loads one half of every K/V tile and
+// multicasts it to both, halving the L2 -> SMEM traffic. Ring slots are released by both
+// CTAs' MMA commits (multicast tcgen05.commit), the item index travels from the leader's
+// producer to the peer through distributed shared memory.
+template <bool kSparse, int kMc>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // offset from smem_raw (not a cast through an integer) so the compiler keeps the
@@ -108,13 +114,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     // producer publishes each item index through a two-slot smem ring, so the next item's Q
     // load and first S MMA overlap this item's last PV and epilogue, and the fetch order keeps
     // the dynamic load balance of a one-CTA-per-item grid.
+    const uint32_t crank = kMc > 1 ? cluster_ctarank() : 0u;
+    const int cpairs = p.npairs / kMc;  // pair groups per query block (one per cluster item)
     auto item = [&](int it) {
         Item x;
-        x.qb = p.qb_hi - 1 - it / p.npairs;
+        x.qb = p.qb_hi - 1 - it / cpairs;
         // pair index -> (KV group, pair within the group); an odd group's last pair carries
         // one head (both Q tiles load it, only tile 0 writes)
         const int grp = p.hq / p.hkv, ppg = (grp + 1) >> 1;
-        const int pi = p.pair0 + it % p.npairs;
+        const int pi = p.pair0 + kMc * (it % cpairs) + static_cast<int>(crank);
         x.g = pi / ppg;
         x.h0 = x.g * grp + 2 * (pi % ppg);
         x.h1 = min(x.h0 + 1, x.g * grp + grp - 1);
@@ -139,7 +147,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         mbar_wait(&sm.item_full[slot], (n_it / kItemRing) & 1);
         const int it = *reinterpret_cast<volatile int*>(&sm.item[slot]);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.item_empty[slot]);
+        if (lane == 0) {
+            if (crank == 0) mbar_arrive(&sm.item_empty[slot]);
+            else mbar_arrive_cluster(mapa_shared(smem_u32(&sm.item_empty[slot]), 0));  // the leader's ring
+        }
         return it;
     };
 
@@ -148,15 +159,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         mbar_init(&sm.q_free, 1);
         for (int s = 0; s < kNumK; ++s) {
             mbar_init(&sm.k_full[s], 1);
-            mbar_init(&sm.k_empty[s], 1);
+            mbar_init(&sm.k_empty[s], kMc);  // every CTA's MMA releases the (multicast) slot
         }
         for (int s = 0; s < kNumV; ++s) {
             mbar_init(&sm.v_full[s], 1);
-            mbar_init(&sm.v_empty[s], 1);
+            mbar_init(&sm.v_empty[s], kMc);
         }
         for (int s = 0; s < kItemRing; ++s) {
             mbar_init(&sm.item_full[s], 1);
-            mbar_init(&sm.item_empty[s], kItemConsumers);
+            // the leader's slots are also consumed by the peer's warps and producer
+            mbar_init(&sm.item_empty[s], kItemConsumers + (kMc - 1) * (kItemConsumers + 1));
         }
         for (int w = 0; w < 2; ++w) {
             mbar_init(&sm.s_full[w], 1);
@@ -170,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
     tc_fence_before();
     __syncthreads();
+    if constexpr (kMc > 1) cluster_sync();  // peers' barriers exist before any remote arrive / multicast
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
@@ -188,15 +201,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         int gj = 0;  // K/V ring position, continuous across items
         for (int n_it = 0;; ++n_it) {
             const int slot = n_it % kItemRing;
-            if (n_it >= kItemRing) mbar_wait(&sm.item_empty[slot], ((n_it / kItemRing) - 1) & 1);
             int it = 0;
-            if (lane == 0) {
-                it = n_it == 0 ? static_cast<int>(blockIdx.x) : atomicAdd(p.work + 0, 1) + static_cast<int>(gridDim.x);
-                if (it >= p.items) it = -1;
-                sm.item[slot] = it;
-                mbar_arrive(&sm.item_full[slot]);  // release: the item index is visible to waiters
+            if (crank == 0) {
+                if (n_it >= kItemRing) mbar_wait(&sm.item_empty[slot], ((n_it / kItemRing) - 1) & 1);
+                if (lane == 0) {
+                    const int nclusters = static_cast<int>(gridDim.x) / kMc;
+                    it = n_it == 0 ? static_cast<int>(blockIdx.x) / kMc : atomicAdd(p.work + 0, 1) + nclusters;
+                    if (it >= p.items) it = -1;
+                    sm.item[slot] = it;
+                    mbar_arrive(&sm.item_full[slot]);  // release: the item index is visible to waiters
+                    if constexpr (kMc > 1) {
+                        st_cluster_u32(mapa_shared(smem_u32(&sm.item[slot]), 1), static_cast<uint32_t>(it));
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&sm.item_full[slot]), 1));
+                    }
+                }
+                it = __shfl_sync(0xffffffffu, it, 0);
+            } else {
+                it = next_item(n_it);  // the peer's producer consumes the leader's fetch
             }
-            it = __shfl_sync(0xffffffffu, it, 0);
             if (it < 0) break;
             const Item x = item(it);
             // the previous item's last S MMA has read its Q tiles
@@ -220,16 +242,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 if (gj >= kNumK) mbar_wait(&sm.k_empty[ks], ((gj / kNumK) & 1) ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
-                    for (int hf = 0; hf < 2; ++hf)
-                        tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, mk_, &sm.k_full[ks], hf * 64, c1, c2);
+                    if constexpr (kMc > 1)  // this CTA's half, multicast; the peer sends the other
+                        tma_load_3d_mc(sK + ks * kTileBytes + crank * kHalfBytes, mk_, &sm.k_full[ks],
+                                       static_cast<int>(crank) * 64, c1, c2, 0x3);
+                    else
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_3d(sK + ks * kTileBytes + hf * kHalfBytes, mk_, &sm.k_full[ks], hf * 64, c1, c2);
                 }
                 __syncwarp();
                 const int vs = gj % kNumV;
                 if (gj >= kNumV) mbar_wait(&sm.v_empty[vs], ((gj / kNumV) & 1) ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&sm.v_full[vs], kTileBytes);
-                    for (int hf = 0; hf < 2; ++hf)
-                        tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, mv_, &sm.v_full[vs], hf * 64, c1, c2);
+                    if constexpr (kMc > 1)
+                        tma_load_3d_mc(sV + vs * kTileBytes + crank * kHalfBytes, mv_, &sm.v_full[vs],
+                                       static_cast<int>(crank) * 64, c1, c2, 0x3);
+                    else
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_3d(sV + vs * kTileBytes + hf * kHalfBytes, mv_, &sm.v_full[vs], hf * 64, c1, c2);
                 }
                 __syncwarp();
             }
@@ -239,6 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // The whole warp walks the schedule (warp-uniform control flow keeps descriptors in
         // uniform registers); one elected lane issues each batch of tcgen05.mma / commit.
         const uint32_t idesc_qk = umma_idesc_bf16(128, 128, false, false);
+        // K/V ring slots are filled by both CTAs of a cluster: release to both
+        auto release = [&](uint64_t* bar) {
+            if constexpr (kMc > 1) umma_commit_mc(bar, 0x3);
+            else umma_commit(bar);
+        };
         const uint32_t idesc_pv = umma_idesc_bf16(128, 128, false, true);
         // descriptor bases; per-k offsets are added to the 14-bit start-address field
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sQ), 16, 1024);
@@ -310,12 +345,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     if (elect_one()) {
                         if (j > 0) {
                             issue_pv(w, G - 1, false, 1);
-                            if (w == 1) umma_commit(&sm.v_empty[(G - 1) % kNumV]);
+                            if (w == 1) release(&sm.v_empty[(G - 1) % kNumV]);
                         }
                         issue_s(w, G);
                         umma_commit(&sm.s_full[w]);
                         if (w == 1) {
-                            umma_commit(&sm.k_empty[ks]);
+                            release(&sm.k_empty[ks]);
                             if (j == nt - 1) umma_commit(&sm.q_free);  // Q of this item no longer read
                         }
                     }
@@ -335,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 if (elect_one()) {
                     issue_pv(w, GL, false, 1);
                     umma_commit(&sm.o_done[w]);
-                    if (w == 1) umma_commit(&sm.v_empty[GL % kNumV]);
+                    if (w == 1) release(&sm.v_empty[GL % kNumV]);
                 }
                 __syncwarp();
             }
@@ -567,6 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_free<512>(tmem);
+    // no CTA of a cluster leaves while its peer may still multicast into it or arrive on it
+    if constexpr (kMc > 1) cluster_sync();
     // the last CTA out resets the work counter for the next launch on this stream
     if (threadIdx.x == 0) {
         __threadfence();
@@ -731,12 +768,53 @@ constexpr int kDenseSlots = 256;
 __device__ int g_dense_work[2 * kDenseSlots];
 std::atomic<unsigned> g_dense_slot{0};
 
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v != nullptr && v[0] != '\0' && v[0] != '0';
+}
+
 // persistent grid: one CTA per SM (the kernel's smem allows one), never more than the items
 int persistent_grid(int items) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return std::max(1, std::min(items, sms));
+}
+
+// Launch the attention kernel: pairs of Q-head pairs in two-CTA clusters (K/V multicast) when
+// every KV group has an even number of pairs (group size a multiple of 4), else one CTA per
+// item. Grid: one CTA per SM, never more CTAs than items need.
+template <bool kSparse>
+cudaError_t launch_attn(AttnParams& p, int nqb, cudaStream_t stream) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(attn_fwd_kernel<kSparse, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(attn_fwd_kernel<kSparse, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr_set = true;
+    }
+    const int grp = p.hq / p.hkv;
+    const bool mc = ((grp + 1) / 2) % 2 == 0 && p.pair0 % 2 == 0 && p.npairs % 2 == 0 && !getenv_flag("VSP_NO_MULTICAST");
+    vsp_detail::count_launch();
+    if (!mc) {
+        p.items = nqb * p.npairs;
+        attn_fwd_kernel<kSparse, 1><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
+        return cudaGetLastError();
+    }
+    p.items = nqb * (p.npairs / 2);
+    const int clusters = std::max(1, std::min(p.items, persistent_grid(1 << 30) / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, attn_fwd_kernel<kSparse, 2>, p);
 }
 
 cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
@@ -749,22 +827,14 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     p.lse = a.lse;
     set_o_layout(p, a);
     if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attn_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr_set = true;
-    }
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     p.pair0 = 0;
     p.npairs = a.hkv * ((a.hq / a.hkv + 1) / 2);
     p.qb_hi = num_qb;
-    p.items = num_qb * p.npairs;
     void* work = nullptr;
     cudaGetSymbolAddress(&work, g_dense_work);
     p.work = static_cast<int*>(work) + 2 * (g_dense_slot.fetch_add(1, std::memory_order_relaxed) % kDenseSlots);
-    vsp_detail::count_launch();
-    attn_fwd_kernel<false><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
-    return cudaGetLastError();
+    return launch_attn<false>(p, num_qb, stream);
 }
 
 size_t sparse_workspace_bytes(int n, int hkv, int cap) {
@@ -843,11 +913,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists, g0);
     }
     if (phase & 2) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(attn_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-            attr_set = true;
-        }
+
         const int pairs_per_group = (a.hq / a.hkv + 1) / 2;
         p.pair0 = g0 * pairs_per_group;
         p.npairs = count * pairs_per_group;
@@ -855,10 +921,9 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         p.qb_hi = qb_hi < 0 ? num_qb : std::min(qb_hi, num_qb);
         const int nqb = p.qb_hi - std::max(qb_lo, 0);
         if (nqb <= 0) return cudaGetLastError();
-        p.items = nqb * p.npairs;
         p.work = work + 2 * g0;  // launches on different KV-head ranges never share a counter
-        vsp_detail::count_launch();
-        attn_fwd_kernel<true><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
+        cudaError_t e = launch_attn<true>(p, nqb, stream);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
