@@ -266,3 +266,18 @@ def test_tile_stats_and_counts_describe_the_last_plan(vsp):
     assert 0 < tiles <= dense
     assert sum(per_head) == tiles == int(counts.sum())
     assert counts.sum(1).tolist() == per_head
+
+
+def test_multicast_clusters_bit_identical(vsp, monkeypatch):
+    """K/V multicast (two-CTA clusters, group size 4) and independent CTAs give the same bits."""
+    n, hq, hkv = 1500, 8, 2
+    rng = np.random.default_rng(77)
+    q, k, v = qkv(n, hq, hkv, seed=77)
+    pat = pattern_tensors([_random_pattern(rng, n, 300, 40) for _ in range(hkv)], n)
+    o_mc, lse_mc = vsp.sparse_attention(q, k, v, pat, validate=False)
+    d_mc = vsp.blockwise_attention(q, k, v)
+    monkeypatch.setenv("VSP_NO_MULTICAST", "1")
+    o_1, lse_1 = vsp.sparse_attention(q, k, v, pat, validate=False)
+    d_1 = vsp.blockwise_attention(q, k, v)
+    assert torch.equal(o_mc, o_1) and torch.equal(lse_mc, lse_1)
+    assert torch.equal(d_mc[0], d_1[0]) and torch.equal(d_mc[1], d_1[1])
