@@ -180,7 +180,8 @@ VSP_API int vsp_adamw_step(vsp_ctx* ctx, float* params, const float* grads, floa
  * Same results as vsp_indexer_scores + vsp_select + vsp_vs_attn_fwd on all heads. With
  * heads_per_chunk = 0 (automatic: one chunk) everything runs in order on `stream`; with
  * KV-head chunks of `heads_per_chunk` heads the scoring, selection and tile planning of
- * chunk c+1 run on a high-priority side stream while chunk c's attention runs on `stream`. a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
+ * chunk c+1 run on a high-priority side stream while chunk c's attention runs on `stream`.
+ * a_v/a_s, i_v/k_v/i_s/k_s are outputs (caller-owned, as in the
  * individual calls). Mirrors `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp
  * :154-185) on the device. */
 VSP_API size_t vsp_vs_prefill_workspace_size(int n, int hkv, int d_h, int cap);
@@ -223,7 +224,8 @@ VSP_API int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, con
  * (automatic): K and V first (two contiguous copies; scoring needs all n rows), then Q in 16
  * query-row ranges; range r is attended as soon as its rows land and its O rows / LSE
  * columns return while later ranges are still in flight. heads_per_chunk > 0: per KV-head
- * chunk, chunk c's K/V/Q columns travel while chunk c-1 is scored and attended. workspace: device memory of vsp_vs_prefill_host_workspace_size bytes
+ * chunk, chunk c's K/V/Q columns travel while chunk c-1 is scored and attended. workspace:
+ * device memory of vsp_vs_prefill_host_workspace_size bytes
  * (it holds the device copies of the inputs and outputs). Stream-ordered on `stream`. */
 VSP_API size_t vsp_vs_prefill_host_workspace_size(int n, int hq, int hkv, int d_h);
 VSP_API int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_h, const void* v_h, int n, int hq,
