@@ -71,9 +71,10 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--shard", choices=["auto", "heads", "balanced"], default="auto",
+    ap.add_argument("--shard", choices=["auto", "heads", "balanced", "spread"], default="auto",
                     help="multi-GPU split: KV heads (north star), or cost-balanced (KV head, query-block) "
-                         "units with replicated inputs; auto = heads at N=1, balanced at N>1")
+                         "units with replicated inputs, or spread (every head split across the ranks); "
+                         "auto = heads at N=1, balanced at N>1")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
     ap.add_argument("--e2e-heads-per-chunk", type=int, default=0)
@@ -341,7 +342,7 @@ def main():
         import torch.distributed as dist
         backend = os.environ.get("VSP_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
-    balanced = args.shard == "balanced" or (args.shard == "auto" and world > 1)
+    balanced = args.shard in ("balanced", "spread") or (args.shard == "auto" and world > 1)
     assert balanced or args.hkv % world == 0, "KV heads must divide across ranks"
     import paper_2603_04460_b200 as vsp
     from paper_2603_04460_b200 import parallel
@@ -360,7 +361,8 @@ def main():
         vsp.sparse_attention(qv, kv_, vv, pat_v, validate=False)
         cost = vsp.sparse_tile_counts(n, args.hkv, pat_v.i_v.shape[1], dev)
         del qv, kv_, vv, a_v, a_s, pat_v
-        units = parallel.balanced_units(cost, world)[rank]
+        units = (parallel.spread_units(cost, world) if args.shard == "spread"
+                 else parallel.balanced_units(cost, world))[rank]
     q_full, k_full, v_full = synth_layer(args, dev)
     hq_r, hkv_r = args.hq // sworld, args.hkv // sworld
     q = shard(q_full, srank, sworld, 1)
@@ -546,7 +548,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": ("config[2]: LLaMA-3.1-8B attention geometry single layer, "
-                                    + ("cost-balanced (KV head, query-block) units" if balanced else "KV-head sharded")),
+                                    + (("every head split across ranks (spread units)" if args.shard == "spread"
+                                        else "cost-balanced (KV head, query-block) units") if balanced
+                                       else "KV-head sharded")),
                        "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
                        "indexer": prep_info["indexer"],
                        "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
@@ -555,7 +559,8 @@ def main():
                        "prep": {k_: v_ for k_, v_ in prep_info.items() if k_ not in ("indexer", "budget_source")},
                        "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
                                  "> L2 so no flush between steps",
-                       "parallelism": (f"balanced units x{world} (replicated inputs, static cost table from a "
+                       "parallelism": (f"{'spread' if args.shard == 'spread' else 'balanced'} units x{world} "
+                                       f"(replicated inputs, static cost table from a "
                                        f"validation prompt; this rank: {units})" if balanced
                                        else f"kv-head shard x{world}")},
             "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,

@@ -24,6 +24,8 @@ struct __align__(64) AttnParams {
     int pair0, npairs;   // Q-head pairs [pair0, pair0 + npairs) handled by this launch
     int qb_hi;           // query blocks [qb_hi - items / npairs, qb_hi) handled by this launch
     int items;           // work items (query block, head pair), pulled by persistent CTAs
+    const int* units;    // units mode (nunits > 0): [nunits][4] = (KV head, qb_lo, qb_hi, qb prefix)
+    int nunits;
     int* work;           // {next item - gridDim.x, CTAs done}: zero at launch, reset by the last CTA
     int bm_words;
     int n, hq, hkv;
@@ -53,6 +55,11 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream);
 size_t sparse_workspace_bytes(int n, int hkv, int cap);
 cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream,
                           int g0 = 0, int count = -1, int phase = 3, int qb_lo = 0, int qb_hi = -1);
+// Attention phase over a list of (KV head, qb_lo, qb_hi) units in ONE persistent launch (the
+// plans of their heads must exist in `workspace`); host_units: nunits x 3 ints.
+constexpr int kMaxUnits = 512;
+cudaError_t launch_sparse_units(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream,
+                                const int* host_units, int nunits);
 
 }  // namespace vsp_attn
 

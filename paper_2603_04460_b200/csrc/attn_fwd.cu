@@ -118,11 +118,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const int cpairs = p.npairs / kMc;  // pair groups per query block (one per cluster item)
     auto item = [&](int it) {
         Item x;
-        x.qb = p.qb_hi - 1 - it / cpairs;
         // pair index -> (KV group, pair within the group); an odd group's last pair carries
         // one head (both Q tiles load it, only tile 0 writes)
         const int grp = p.hq / p.hkv, ppg = (grp + 1) >> 1;
-        const int pi = p.pair0 + kMc * (it % cpairs) + static_cast<int>(crank);
+        int pi;
+        if (p.nunits > 0) {  // units mode: query-block runs of single KV heads, pairs = the group's
+            const int itq = it / cpairs;
+            int u = 0;
+            while (u + 1 < p.nunits && __ldg(p.units + 4 * (u + 1) + 3) <= itq) ++u;
+            const int g = __ldg(p.units + 4 * u);
+            x.qb = __ldg(p.units + 4 * u + 2) - 1 - (itq - __ldg(p.units + 4 * u + 3));
+            pi = g * ppg + kMc * (it % cpairs) + static_cast<int>(crank);
+        } else {
+            x.qb = p.qb_hi - 1 - it / cpairs;
+            pi = p.pair0 + kMc * (it % cpairs) + static_cast<int>(crank);
+        }
         x.g = pi / ppg;
         x.h0 = x.g * grp + 2 * (pi % ppg);
         x.h1 = min(x.h0 + 1, x.g * grp + grp - 1);
@@ -849,13 +859,15 @@ size_t sparse_workspace_bytes(int n, int hkv, int cap) {
     add(static_cast<size_t>(hkv) * bm_words * 4 * 2);      // bitmaps
     add(static_cast<size_t>(hkv) * num_qb * list_stride * 4);
     add(static_cast<size_t>(hkv) * 2 * 4);                 // per-KV-head work counters
+    add(2 * 4 + static_cast<size_t>(kMaxUnits) * 4 * 4);  // units launch: counters + unit table
     return bytes;
 }
 
 // phase: 1 = plan (bitmaps, vertical gather, tile lists), 2 = attention kernel, 3 = both;
 // only KV heads [g0, g0 + count) are touched, so head ranges can be pipelined on streams.
-cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
-                          int count, int phase, int qb_lo, int qb_hi) {
+namespace {
+cudaError_t launch_sparse_impl(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
+                               int count, int phase, int qb_lo, int qb_hi, const int* host_units, int nunits) {
     if (count < 0) count = a.hkv - g0;
     AttnParams p{};
     p.n = a.n;
@@ -881,6 +893,7 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
     auto* bits = reinterpret_cast<uint32_t*>(take(static_cast<size_t>(a.hkv) * bm_words * 4 * 2));
     auto* lists = reinterpret_cast<int*>(take(static_cast<size_t>(a.hkv) * num_qb * list_stride * 4));
     int* work = reinterpret_cast<int*>(take(static_cast<size_t>(a.hkv) * 2 * 4));
+    int* uwork = reinterpret_cast<int*>(take(2 * 4 + static_cast<size_t>(kMaxUnits) * 4 * 4));
     p.vbits = bits;
     p.sbits = bits + static_cast<size_t>(a.hkv) * bm_words;
     p.bm_words = bm_words;
@@ -912,8 +925,32 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         vs_plan_kernel<<<dim3((num_qb + 3) / 4, count), 128, 0, stream>>>(
             s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists, g0);
     }
+    if ((phase & 2) && nunits > 0) {
+        // one launch over all units: table (KV head, qb_lo, qb_hi, qb prefix) in the workspace
+        if (nunits > kMaxUnits) return cudaErrorInvalidValue;
+        std::vector<int> tab(static_cast<size_t>(nunits) * 4);
+        int total = 0;
+        for (int u = 0; u < nunits; ++u) {
+            const int lo = std::max(host_units[3 * u + 1], 0), hi = std::min(host_units[3 * u + 2], num_qb);
+            tab[4 * u] = host_units[3 * u];
+            tab[4 * u + 1] = lo;
+            tab[4 * u + 2] = hi;
+            tab[4 * u + 3] = total;
+            total += std::max(hi - lo, 0);
+        }
+        if (total == 0) return cudaGetLastError();
+        cudaError_t e = cudaMemcpyAsync(uwork + 2, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(uwork, 0, 2 * sizeof(int), stream);
+        if (e != cudaSuccess) return e;
+        p.units = uwork + 2;
+        p.nunits = nunits;
+        p.pair0 = 0;
+        p.npairs = (a.hq / a.hkv + 1) / 2;  // the pairs of one KV group
+        p.qb_hi = 0;
+        p.work = uwork;
+        return launch_attn<true>(p, total, stream);
+    }
     if (phase & 2) {
-
         const int pairs_per_group = (a.hq / a.hkv + 1) / 2;
         p.pair0 = g0 * pairs_per_group;
         p.npairs = count * pairs_per_group;
@@ -926,6 +963,17 @@ cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspac
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_sparse(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
+                          int count, int phase, int qb_lo, int qb_hi) {
+    return launch_sparse_impl(a, s, workspace, stream, g0, count, phase, qb_lo, qb_hi, nullptr, 0);
+}
+
+cudaError_t launch_sparse_units(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream,
+                                const int* host_units, int nunits) {
+    return launch_sparse_impl(a, s, workspace, stream, 0, a.hkv, 2, 0, -1, host_units, nunits);
 }
 
 }  // namespace vsp_attn

@@ -496,6 +496,23 @@ cudaError_t timed_attention(vsp_ctx* ctx, const vsp_attn::AttnArgs& aa, const vs
     return e;
 }
 
+// The attention of a list of units in one persistent launch, timed like timed_attention.
+cudaError_t timed_attention_units(vsp_ctx* ctx, const vsp_attn::AttnArgs& aa, const vsp_attn::SparseArgs& sa,
+                                  void* ws, cudaStream_t st, const vsp_unit* units, int nunits) {
+    std::vector<int> tab(static_cast<size_t>(nunits) * 3);
+    for (int u = 0; u < nunits; ++u) {
+        tab[3 * u] = units[u].g;
+        tab[3 * u + 1] = units[u].qb_lo;
+        tab[3 * u + 2] = units[u].qb_hi;
+    }
+    const bool t = ctx->timing && ctx->timed < vsp_ctx::kTimingSlots;
+    cudaError_t e = cudaSuccess;
+    if (t) e = cudaEventRecord(ctx->t_beg[ctx->timed], st);
+    if (e == cudaSuccess) e = vsp_attn::launch_sparse_units(aa, sa, ws, st, tab.data(), nunits);
+    if (t && e == cudaSuccess) e = cudaEventRecord(ctx->t_end[ctx->timed++], st);
+    return e;
+}
+
 // K1 (logits) -> K2 (softmax + selection) -> K3 plan for KV heads [g0, g0 + cnt) on `st`.
 cudaError_t enqueue_scoring(const PrefillDev& p, int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping,
                             const vsp_budget* budgets, void* workspace, int g0, int cnt, cudaStream_t st) {
@@ -638,6 +655,7 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
     if (rc) return rc;
     if (flags & ~VSP_O_HEAD_MAJOR) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: unknown flags");
     if (nunits < 0 || (nunits > 0 && !units)) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: bad units");
+    if (nunits > vsp_attn::kMaxUnits) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: at most 512 units per call");
     const int num_qb = (n + 127) / 128;
     std::vector<char> touched(hkv, 0);
     for (int u = 0; u < nunits; ++u) {
@@ -676,8 +694,8 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
         if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g, cnt, 1);
         g += cnt;
     }
-    for (int u = 0; u < nunits && e == cudaSuccess; ++u)
-        e = timed_attention(ctx, aa, sa, ws_attn, st, units[u].g, 1, units[u].qb_lo, units[u].qb_hi);
+    // all units' attention in one persistent launch (one work queue across the units)
+    if (e == cudaSuccess && nunits > 0) e = timed_attention_units(ctx, aa, sa, ws_attn, st, units, nunits);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_units");
 }
 

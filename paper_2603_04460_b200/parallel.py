@@ -165,6 +165,30 @@ def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: f
     return out + [[] for _ in range(world - len(out))]
 
 
+def spread_units(cost, world: int, cta_overhead: float = 2.0) -> List[List[Tuple[int, int, int]]]:
+    """Split EVERY KV head's query blocks into `world` contiguous runs of equal predicted cost
+    (tiles + per-block overhead) and give rank r the r-th run of each head. A rank's share is
+    then ~1/world of every head, so it does not depend on how the cost splits across heads —
+    the part of a static cost table that moves most from prompt to prompt — at the price of
+    every rank scoring every head. Returns per rank a list of units (g, qb_lo, qb_hi)."""
+    rows = [[float(x) + cta_overhead for x in r] for r in (cost.tolist() if hasattr(cost, "tolist") else cost)]
+    out: List[List[Tuple[int, int, int]]] = [[] for _ in range(world)]
+    for g, r in enumerate(rows):
+        total = sum(r)
+        bounds, acc, b = [0], 0.0, 0
+        for k in range(1, world):
+            target = total * k / world
+            while b < len(r) and acc + r[b] <= target:
+                acc += r[b]
+                b += 1
+            bounds.append(b)
+        bounds.append(len(r))
+        for k in range(world):
+            if bounds[k + 1] > bounds[k]:
+                out[k].append((g, bounds[k], bounds[k + 1]))
+    return out
+
+
 def units_cost(units, cost, cta_overhead: float = 2.0, head_overhead: float = 0.0) -> float:
     rows = cost.tolist() if hasattr(cost, "tolist") else cost
     heads = {g for g, _, _ in units}

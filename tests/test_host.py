@@ -208,3 +208,21 @@ def test_balanced_units_float_costs_never_exceed_world():
         assert len(units) == world
         assert sum(hi - lo for us in units for _, lo, hi in us) == cost.size
     assert len(parallel.balanced_units(cost, 1)[0]) == 8  # one unit per head, one rank
+
+
+def test_spread_units_cover_every_head_evenly():
+    from paper_2603_04460_b200 import parallel
+    rng = np.random.default_rng(5)
+    hkv, nqb = 8, 300
+    cost = rng.integers(0, 50, size=(hkv, nqb)) + np.arange(nqb)[None, :] // 10
+    for world in (1, 2, 3, 8):
+        units = parallel.spread_units(cost, world)
+        assert len(units) == world
+        seen = np.zeros((hkv, nqb), dtype=int)
+        for us in units:
+            for g, lo, hi in us:
+                seen[g, lo:hi] += 1
+        assert (seen == 1).all()
+        per_rank = [parallel.units_cost(us, cost) for us in units]
+        worst_block = float(cost.max()) + 2.0
+        assert max(per_rank) <= (float(cost.sum()) + 2.0 * cost.size) / world + hkv * worst_block

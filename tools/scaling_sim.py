@@ -6,6 +6,7 @@ share on the single GPU (CUDA events, warm, same clocks) for N = 1, 2, 4, 8 and 
 predicted step (max over ranks) and tokens/s for
   heads    : KV-head sharding (each rank vs_prefill on Hkv/N heads, the north-star split)
   balanced : cost-balanced (KV head, query-block) units (vs_prefill_units, replicated inputs)
+  spread   : every head's query blocks split evenly by cost across the ranks (vs_prefill_units)
 The cost table of the balanced split comes from a separate validation prompt (not the timed
 one). Prints one JSON line.
 
@@ -87,7 +88,13 @@ def main():
                                         head_overhead=float(opts["--head-overhead"]))
         t_bal = [timed(lambda u=u: vsp.vs_prefill_units(q, k, v, params, budget, u, out=o_full, lse=lse_full))
                  for u in units]
+        # spread: every head's query blocks split across the ranks (every rank scores every head)
+        sunits = parallel.spread_units(cost, world, cta_overhead=float(opts["--cta-overhead"]))
+        t_spr = [timed(lambda u=u: vsp.vs_prefill_units(q, k, v, params, budget, u, out=o_full, lse=lse_full))
+                 for u in sunits]
         out["splits"][world] = {
+            "spread_ms_per_rank": [round(x, 3) for x in t_spr], "spread_step_ms": round(max(t_spr), 3),
+            "spread_tok_s": n / (max(t_spr) * 1e-3),
             "heads_ms_per_rank": [round(x, 3) for x in t_heads], "heads_step_ms": round(max(t_heads), 3),
             "heads_tok_s": n / (max(t_heads) * 1e-3),
             "balanced_ms_per_rank": [round(x, 3) for x in t_bal], "balanced_step_ms": round(max(t_bal), 3),
@@ -96,6 +103,7 @@ def main():
     for world, s in out["splits"].items():
         s["heads_speedup"] = round(base_h / s["heads_step_ms"], 2)
         s["balanced_speedup"] = round(base_h / s["balanced_step_ms"], 2)
+        s["spread_speedup"] = round(base_h / s["spread_step_ms"], 2)
     print(json.dumps(out))
 
 
