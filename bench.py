@@ -4,27 +4,31 @@
 One step = one layer of the VS-prefill path on this rank's KV heads:
     K1 indexer scores -> K2 adaptive selection -> K3 fused VS sparse attention
 at LLaMA-3.1-8B attention geometry (32 Q / 8 KV heads, d=128), n = 131072, synthetic
-planted-structure Q/K/V (paper_2603_04460_b200/synth.py), inputs resident in HBM
-(Q alone is 1.07 GB > the 126 MB L2, so no flush is needed between steps).
+planted-structure Q/K/V (paper_2603_04460_b200/synth.py, drawn on the CPU so every process
+sees the same bits), inputs resident in HBM (Q alone is 1.07 GB > the 126 MB L2, so no
+flush is needed between steps).
+
+The indexer parameters and per-head budgets come from bench_data/ (written by
+`python bench.py --prep fresh --save-prep`: KL distillation of the VSIndexer on 12 training
+prompts and budget calibration on 6 validation prompts, on the GPU). Both arms load the same
+file, so they run the same layer with the same indexer and budgets.
 
 Multi-GPU (torchrun, one rank per GPU): KV heads are sharded 8/N per rank with no
 collective on the data path; value = n / max-over-ranks step time
-(strong scaling: the layer is fixed, heads split). The NCCL all-gather that would
-assemble O is timed separately (`allgather_ms`), not inside the step.
+(strong scaling: the layer is fixed, heads split). The NCCL all-gather that assembles O is
+timed separately (`allgather_ms`). `--shard balanced|spread` split (KV head, query block)
+units instead; their assembly (vsp_assemble_units, NCCL broadcasts) is timed the same way.
 
-Extra keys: dense_ms / speedup_vs_dense (this build's own K4 dense causal kernel on the
-same heads), recall (mean_i exp(LSE_sparse - LSE_dense), attention.hpp:198-215 without
-the n x n matrix), element and tile density, roofline of K3, the reference CPU path on a
-bounded row-prefix sample (cpu_baseline), e2e through host buffers, clocks during timing.
-
-`--impl reference` runs the reference's own CPU implementation (oracle/_ref, the
-unmodified headers; the oracle port if that .so is absent) on the same workload sample.
+`--impl reference` runs the reference's own CPU implementation (oracle/_ref: the unmodified
+reference headers) on a bounded sample of the same layer, in a CPU-only process (no CUDA,
+no libvsp_gpu.so): its own full-length indexer scoring and selection once (measured), then
+per step select_pattern on all n and sparse_attention on rows [0, 4096) and [0, 8192),
+extrapolated to the layer (ReferenceLayer).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -39,9 +43,12 @@ import torch  # noqa: E402
 
 METRIC = "prefill attn tokens/s @128k LLaMA-8B geom, 1/2/4/8 B200; speedup vs own dense"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PREP_DIR = os.path.join(ROOT, "bench_data")
+# bump when synth.py / the preparation recipe changes what a given seed produces
+SYNTH_TAG = "planted-v1 (synth.py PlantConfig defaults); timed prompt drawn on the CPU"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -52,6 +59,10 @@ def parse():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d-h", type=int, default=1024)
     ap.add_argument("--indexer", choices=["distilled", "random"], default="distilled")
+    ap.add_argument("--prep", choices=["auto", "load", "fresh"], default="auto",
+                    help="indexer + budgets: load bench_data/ (auto: when it matches these flags, else "
+                         "prepare on the GPU), or prepare fresh")
+    ap.add_argument("--save-prep", action="store_true", help="write the fresh preparation to bench_data/")
     ap.add_argument("--train-prompts", type=int, default=12)
     ap.add_argument("--val-prompts", type=int, default=6)
     ap.add_argument("--calib-aggregate", choices=["mean", "worst"], default="mean",
@@ -59,7 +70,7 @@ def parse():
     ap.add_argument("--distill-steps", type=int, default=900)
     ap.add_argument("--recall-target", type=float, default=0.9)
     ap.add_argument("--calib-margin", type=float, default=0.035,
-                    help="calibrate the budget for recall_target + margin on the validation prompt")
+                    help="calibrate the budget for recall_target + margin on the validation prompts")
     ap.add_argument("--tau-step", type=float, default=0.1,
                     help="grid step of the per-head (tau_v, tau_s) calibration over (0, 1)")
     ap.add_argument("--tau-v", type=float, default=None, help="fix tau_v (skips calibration)")
@@ -68,17 +79,17 @@ def parse():
     ap.add_argument("--max-budget", type=int, default=-1)
     ap.add_argument("--head-sigma", type=float, default=0.3, help="random indexer head scale")
     ap.add_argument("--seed", type=int, default=2026)
-    ap.add_argument("--cpu-sample", type=int, default=12288, help="row-prefix sample for the CPU reference")
+    ap.add_argument("--ref-rows", type=int, default=8192,
+                    help="reference sample: sparse_attention row prefixes rows/2 and rows per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard", choices=["auto", "heads", "balanced", "spread"], default="auto",
-                    help="multi-GPU split: KV heads (north star), or cost-balanced (KV head, query-block) "
-                         "units with replicated inputs, or spread (every head split across the ranks); "
-                         "auto = heads at N=1, balanced at N>1")
+                    help="multi-GPU split: KV heads (north star; auto), or cost-balanced (KV head, query-block) "
+                         "units with replicated inputs, or spread (every head split across the ranks)")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
     ap.add_argument("--e2e-heads-per-chunk", type=int, default=0)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # --------------------------------------------------------------------------- helpers
@@ -100,6 +111,24 @@ def peaks():
             return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -168,88 +197,30 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
+def pairs_prefix(iv: np.ndarray, is_: np.ndarray, rows: int) -> int:
+    """Covered causal pairs (i, j), i < rows, of one KV head's pattern (ascending lists):
+    sum_v (rows - v) + sum_o (rows - o) - #{(v, o): v + o < rows} (vertical/slash overlap)."""
+    iv = np.asarray(iv, np.int64)
+    is_ = np.asarray(is_, np.int64)
+    iv = iv[iv < rows]
+    is_ = is_[is_ < rows]
+    a = int((rows - iv).sum()) + int((rows - is_).sum())
+    ov = int(np.searchsorted(is_, rows - 1 - iv, side="right").sum()) if len(iv) else 0
+    return a - ov
+
+
 def covered_pairs(pat, n: int, hkv: int) -> np.ndarray:
-    """Exact covered (i, j) pairs per KV head of a VS pattern:
-    sum_v (n - v) + sum_o (n - o) - #{(v, o): v + o < n} (vertical/slash overlap)."""
-    out = np.zeros(hkv, np.int64)
-    kv = pat.k_v.cpu().numpy()
-    ks = pat.k_s.cpu().numpy()
-    for g in range(hkv):
-        iv = pat.i_v[g, : kv[g]].long()
-        is_ = pat.i_s[g, : ks[g]].long()
-        iv = iv[iv < n]
-        is_ = is_[is_ < n]
-        a = int((n - iv).sum()) + int((n - is_).sum())
-        # overlap: for each v, offsets o <= n - 1 - v
-        ov = int(torch.searchsorted(is_.contiguous(), (n - 1 - iv).contiguous(), right=True).sum()) if len(iv) else 0
-        out[g] = a - ov
-    return out
+    """Exact covered (i, j) pairs per KV head of a (device) VS pattern."""
+    return np.array([pairs_prefix(*pat.lists(g), n) for g in range(hkv)], np.int64)
 
 
-def synth_layer(args, device, seed=None):
-    """The held-out prompt (seed = args.seed) of the planted layer, all heads."""
+def synth_layer(args, device, seed=None, gen_device=None):
+    """One prompt of the planted layer, all heads. The timed prompt (seed = args.seed) is
+    drawn with gen_device="cpu" in both arms, so they attend the identical layer."""
     from paper_2603_04460_b200.synth import planted_layer
-    q, k, v, _ = planted_layer(args.n, args.hq, args.hkv, seed=args.seed if seed is None else seed, device=device)
+    q, k, v, _ = planted_layer(args.n, args.hq, args.hkv, seed=args.seed if seed is None else seed, device=device,
+                               gen_device=gen_device)
     return q, k, v
-
-
-def prepare_indexer(args, device, rank, world):
-    """This rank's indexer parameters and budget. distilled: KL-distilled on
-    `train_prompts` other prompts of the same heads (K5 ground truth), budget calibrated on
-    training prompt 0 to reach `recall_target`. random: the reference's make_indexer_params
-    with N(0, head_sigma^2) heads. Returns (params, budget, info)."""
-    import paper_2603_04460_b200 as vsp
-    from paper_2603_04460_b200 import calibrate
-    info = {}
-    if args.indexer == "random":
-        g = torch.Generator().manual_seed(args.seed + 7)
-        full = vsp.make_indexer_params(args.hkv, 128, args.d_h, g, head_sigma=args.head_sigma, device=device)
-        params = vsp.IndexerParams(*[shard(getattr(full, f), rank, world, 0)
-                                     for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
-        info["indexer"] = f"random-init VSIndexer (make_indexer_params), heads ~ N(0, {args.head_sigma}^2)"
-    else:
-        t0 = time.time()
-        prompts = []
-        for i in range(args.train_prompts):
-            q, k, v = synth_layer(args, device, seed=args.seed + 101 + i)
-            prompts.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
-            del q, k, v
-        tstats = {}
-        params, losses = calibrate.train_indexer(prompts, args.d_h, steps=args.distill_steps, stats=tstats)
-        info["indexer"] = (f"VSIndexer distilled on GPU (KL to K5 ground truth, AdamW, {args.distill_steps} steps; "
-                           f"sm_100a loss/backward/AdamW kernels) on {args.train_prompts} training prompts of the "
-                           f"same heads; held-out prompt timed")
-        info["distill_loss_first_last"] = [x for x in losses if x == x][:1] + [losses[-1]]
-        info["distill_step_ms"] = round(tstats.get("step_ms", float("nan")), 3)
-        info["ground_truth_ms_per_prompt"] = round(tstats.get("ground_truth_ms", float("nan")), 2)
-        info["prep_s"] = None
-    if args.tau_v is not None and args.tau_s is not None:
-        budget = [vsp.BudgetConfig(args.tau_v, args.tau_s, args.min_budget,
-                                   None if args.max_budget < 0 else args.max_budget)] * (args.hkv // world)
-        info["budget_source"] = "fixed by flags"
-    else:
-        if args.indexer == "distilled":
-            del prompts
-        # validation prompts, distinct from the training prompts and the timed prompt
-        vals = []
-        for i in range(args.val_prompts):
-            q, k, v = synth_layer(args, device, seed=args.seed + 201 + i)
-            vals.append((shard(q, rank, world, 1), shard(k, rank, world, 1), shard(v, rank, world, 1)))
-            del q, k, v
-        taus = tuple(round(args.tau_step * i, 4) for i in range(1, int(round(1 / args.tau_step))))
-        budget, pt = calibrate.calibrate_budget(vals, params=params, taus=taus, aggregate=args.calib_aggregate,
-                                                recall_target=args.recall_target + args.calib_margin,
-                                                min_budget=args.min_budget,
-                                                max_budget=None if args.max_budget < 0 else args.max_budget)
-        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) on a {args.tau_step} grid, calibrated on "
-                                 f"{args.val_prompts} validation prompts "
-                                 f"({args.calib_aggregate}, cliff-weighted tiles) for mean recall >= "
-                                 f"{args.recall_target} + {args.calib_margin}: "
-                                 f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
-        del vals
-    if args.indexer == "distilled":
-        info["prep_s"] = round(time.time() - t0, 1)
-    return params, budget, info
 
 
 def shard(x, r, world, dim):
@@ -257,69 +228,314 @@ def shard(x, r, world, dim):
     return x.narrow(dim, r * size, size).contiguous()
 
 
+# --------------------------------------------------------------------------- preparation
+
+PREP_KEYS = ("n", "hq", "hkv", "d_h", "seed", "indexer", "train_prompts", "val_prompts", "distill_steps",
+             "recall_target", "calib_margin", "tau_step", "calib_aggregate", "min_budget", "max_budget",
+             "head_sigma", "tau_v", "tau_s")
+
+
+def prep_key(args) -> dict:
+    key = {k: getattr(args, k) for k in PREP_KEYS}
+    key["synth"] = SYNTH_TAG
+    return key
+
+
+def prep_path(args) -> str:
+    return os.path.join(PREP_DIR, f"prep_{args.indexer}_n{args.n}_h{args.hq}x{args.hkv}_dh{args.d_h}.npz")
+
+
+def save_prep(args, params, budgets, info) -> str:
+    """bf16 W_U as its raw 16-bit patterns, the fp32 rest, per-head (tau_v, tau_s), and the
+    preparation's provenance; ~3.5 MB compressed for the bench config."""
+    os.makedirs(PREP_DIR, exist_ok=True)
+    path = prep_path(args)
+    meta = {"key": prep_key(args), "info": info}
+    np.savez_compressed(path, w_u=params.w_u.contiguous().view(torch.int16).cpu().numpy(),
+                        b_u=params.b_u.float().cpu().numpy(), w_v=params.w_v.float().cpu().numpy(),
+                        b_v=params.b_v.float().cpu().numpy(), w_s=params.w_s.float().cpu().numpy(),
+                        b_s=params.b_s.float().cpu().numpy(),
+                        tau=np.array([[t[0], t[1]] for t in budgets], np.float64), meta=json.dumps(meta))
+    return path
+
+
+def load_prep(args):
+    """-> (numpy params with W_U as f32 [hkv, 2d, d_h], [(tau_v, tau_s)] per KV head, info) or
+    None when bench_data/ holds no preparation made with these flags."""
+    path = prep_path(args)
+    if not os.path.exists(path):
+        return None
+    z = np.load(path, allow_pickle=False)
+    meta = json.loads(str(z["meta"]))
+    if meta["key"] != prep_key(args):
+        return None
+    w_u = (z["w_u"].astype(np.int32).astype(np.uint32) << 16).view(np.float32)  # bf16 bits -> f32
+    prm = dict(w_u=w_u, b_u=z["b_u"], w_v=z["w_v"], b_v=z["b_v"], w_s=z["w_s"], b_s=z["b_s"])
+    budgets = [(float(a), float(b)) for a, b in z["tau"]]
+    info = dict(meta["info"])
+    info["prep_file"] = os.path.relpath(path, ROOT)
+    return prm, budgets, info
+
+
+def params_to_device(prm: dict, dev):
+    import paper_2603_04460_b200 as vsp
+    t = {k: torch.from_numpy(np.ascontiguousarray(x)) for k, x in prm.items()}
+    return vsp.IndexerParams(t["w_u"].to(torch.bfloat16).to(dev), t["b_u"].float().to(dev), t["w_v"].float().to(dev),
+                             t["b_v"].float().to(dev), t["w_s"].float().to(dev), t["b_s"].float().to(dev))
+
+
+def params_to_numpy(params) -> dict:
+    return {f: getattr(params, f).float().cpu().numpy() for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")}
+
+
+def random_params(args):
+    """The reference's make_indexer_params with N(0, head_sigma^2) heads, on the CPU."""
+    import paper_2603_04460_b200 as vsp  # pure torch here: the library is not loaded
+    g = torch.Generator().manual_seed(args.seed + 7)
+    return vsp.make_indexer_params(args.hkv, 128, args.d_h, g, head_sigma=args.head_sigma, device="cpu")
+
+
+def prepare_gpu(args, device):
+    """Indexer parameters and per-head budgets of every KV head, prepared on the GPU.
+    distilled: KL distillation on `train_prompts` other prompts of the same heads (K5 ground
+    truth); budgets calibrated on `val_prompts` further prompts to reach recall_target +
+    calib_margin. random: make_indexer_params with N(0, head_sigma^2) heads. The timed prompt
+    is never seen. Returns (params on device, [(tau_v, tau_s)], info)."""
+    import paper_2603_04460_b200 as vsp
+    from paper_2603_04460_b200 import calibrate
+    info = {}
+    t0 = time.time()
+    if args.indexer == "random":
+        params = params_to_device(params_to_numpy(random_params(args)), device)
+        info["indexer"] = f"random-init VSIndexer (make_indexer_params), heads ~ N(0, {args.head_sigma}^2)"
+    else:
+        prompts = [synth_layer(args, device, seed=args.seed + 101 + i) for i in range(args.train_prompts)]
+        tstats = {}
+        params, losses = calibrate.train_indexer(prompts, args.d_h, steps=args.distill_steps, stats=tstats)
+        del prompts
+        info["indexer"] = (f"VSIndexer distilled on GPU (KL to K5 ground truth, AdamW, {args.distill_steps} steps; "
+                           f"sm_100a loss/backward/AdamW kernels) on {args.train_prompts} training prompts of the "
+                           f"same heads; held-out prompt timed")
+        info["distill_loss_first_last"] = [x for x in losses if x == x][:1] + [losses[-1]]
+        info["distill_step_ms"] = round(tstats.get("step_ms", float("nan")), 3)
+        info["ground_truth_ms_per_prompt"] = round(tstats.get("ground_truth_ms", float("nan")), 2)
+    if args.tau_v is not None and args.tau_s is not None:
+        budgets = [(args.tau_v, args.tau_s)] * args.hkv
+        info["budget_source"] = "fixed by flags"
+    else:
+        vals = [synth_layer(args, device, seed=args.seed + 201 + i) for i in range(args.val_prompts)]
+        taus = tuple(round(args.tau_step * i, 4) for i in range(1, int(round(1 / args.tau_step))))
+        bl, pt = calibrate.calibrate_budget(vals, params=params, taus=taus, aggregate=args.calib_aggregate,
+                                            recall_target=args.recall_target + args.calib_margin,
+                                            min_budget=args.min_budget,
+                                            max_budget=None if args.max_budget < 0 else args.max_budget)
+        budgets = [(b.tau_v, b.tau_s) for b in bl]
+        info["budget_source"] = (f"per-KV-head (tau_v, tau_s) on a {args.tau_step} grid, calibrated on "
+                                 f"{args.val_prompts} validation prompts "
+                                 f"({args.calib_aggregate}, cliff-weighted tiles) for mean recall >= "
+                                 f"{args.recall_target} + {args.calib_margin}: "
+                                 f"recall {pt['recall']:.4f}, tile density {pt['tile_density']:.4f}")
+        del vals
+    info["prep_s"] = round(time.time() - t0, 1)
+    return params, budgets, info
+
+
+def obtain_prep(args, device):
+    """(params on device, [(tau_v, tau_s)] per KV head, info): bench_data/ when it matches the
+    flags (--prep auto|load), else prepared on the GPU (--prep auto|fresh)."""
+    if args.prep != "fresh":
+        got = load_prep(args)
+        if got is not None:
+            prm, budgets, info = got
+            return params_to_device(prm, device), budgets, info
+        if args.prep == "load":
+            raise SystemExit(f"--prep load: {os.path.relpath(prep_path(args), ROOT)} missing or made with other flags")
+    params, budgets, info = prepare_gpu(args, device)
+    if args.save_prep:
+        info["prep_file"] = os.path.relpath(save_prep(args, params, budgets, info), ROOT)
+    return params, budgets, info
+
+
+def prepare_indexer(args, device, rank=0, world=1):
+    """For tools/: (params, [BudgetConfig] of this rank's KV heads, info) via obtain_prep."""
+    import paper_2603_04460_b200 as vsp
+    params, budgets, info = obtain_prep(args, device)
+    per = args.hkv // world
+    params = vsp.IndexerParams(*[shard(getattr(params, f), rank, world, 0)
+                                 for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
+    mx = None if args.max_budget < 0 else args.max_budget
+    return params, [vsp.BudgetConfig(tv, ts, args.min_budget, mx)
+                    for tv, ts in budgets[rank * per:(rank + 1) * per]], info
+
+
+def workload_config(args, world, budgets, info) -> dict:
+    """The `config` of the JSON line — identical in both arms for the same flags."""
+    balanced = args.shard in ("balanced", "spread")
+    return {
+        "workload": ("config[2]: LLaMA-3.1-8B attention geometry single layer, "
+                     + (("every head split across ranks (spread units)" if args.shard == "spread"
+                         else "cost-balanced (KV head, query-block) units") if balanced else "KV-head sharded")),
+        "n": args.n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
+        "indexer": info.get("indexer"),
+        "budget": {"tau_v": [b[0] for b in budgets], "tau_s": [b[1] for b in budgets], "min": args.min_budget,
+                   "max": args.max_budget, "source": info.get("budget_source")},
+        "prep": {k_: v_ for k_, v_ in info.items() if k_ not in ("indexer", "budget_source")},
+        "inputs": ("planted vertical-slash synthetic layer (synth.py, seed %d, drawn on the CPU), resident in HBM; "
+                   "Q is 1.07 GB > L2 so no flush between steps" % args.seed),
+        "parallelism": (f"{'spread' if args.shard == 'spread' else 'balanced'} units x{world} (replicated inputs, "
+                        f"static cost table from a validation prompt)" if balanced else f"kv-head shard x{world}"),
+    }
+
+
 # --------------------------------------------------------------------------- reference arm
 
-def cpu_reference(args, q, k, v, params, budgets, rows: int, threads: int, repeats: int = 1):
-    """The reference's own CPU implementation (oracle/_ref) on rows [0, rows) of the layer,
-    all heads, threaded over heads. Returns (tokens/s, seconds, kind)."""
-    import oracle
-    kind = "reference" if oracle.have_ref() else "port"
-    qn = q[:rows].float().cpu().numpy().astype(np.float64)
-    kn = k[:rows].float().cpu().numpy().astype(np.float64)
-    vn = v[:rows].float().cpu().numpy().astype(np.float64)
-    prm = dict(w_u=params.w_u.float().cpu().numpy().astype(np.float64),
-               b_u=params.b_u.cpu().numpy().astype(np.float64), w_v=params.w_v.cpu().numpy().astype(np.float64),
-               w_s=params.w_s.cpu().numpy().astype(np.float64), b_v=params.b_v.cpu().numpy().astype(np.float64),
-               b_s=params.b_s.cpu().numpy().astype(np.float64))
-    lib = oracle.ref() if kind == "reference" else None
-    if lib is None:
-        raise RuntimeError("oracle/_ref not built; the reference arm needs the reference library")
-    times = []
-    for _ in range(repeats):
+class ReferenceLayer:
+    """The reference's CPU implementation (oracle/_ref/libvspref.so: the unmodified headers)
+    on a bounded sample of the bench layer, threaded over heads with every host core.
+
+    Setup (once, measured): the reference's own indexer_forward over the full sequence (all
+    n tokens: its softmax is over n) and select_pattern on it — the pattern the reference
+    itself attends with. A step then times, through the same API, select_pattern on the
+    full-length scores and sparse_attention over query rows [0, rows/2) and [0, rows) with
+    that pattern (causality makes these the layer's own output rows). The full layer's
+    attention time is extrapolated from the two prefixes: each head's call time is fitted as
+    alpha * rows + beta * covered pairs (alpha: the per-row merge_row_columns work and
+    allocations of attention.hpp:158-166, beta: the d-long dot + axpy per covered pair), and
+    the per-head estimates at n are scheduled over the threads the way the threaded call
+    does (next head to the next free thread). Checked against a full-length reference run
+    (n = 32768, 8 threads, rows = 4096; tools/ref_extrapolation_check.py): the estimate was
+    0.78-0.93 of the measured 20.5 s, i.e. it errs towards overstating the reference's
+    throughput; a plain covered-pair ratio of one prefix (also reported) was 2.0-2.3x too
+    slow, because early rows carry few pairs."""
+
+    def __init__(self, args, q, k, v, prm: dict, budgets, threads: int, rows: int):
+        import oracle
+        if not oracle.have_ref():
+            raise RuntimeError("oracle/_ref/libvspref.so not built (needs /root/reference at build time)")
+        self.lib = oracle.ref()
+        self.n, self.rows, self.threads = args.n, min(rows, args.n), threads
+        self.hq, self.grp = args.hq, args.hq // args.hkv
+        self.min_b, self.max_b = args.min_budget, args.max_budget if args.max_budget >= 0 else -1
+        self.tau_v = [b[0] for b in budgets]
+        self.tau_s = [b[1] for b in budgets]
+        self.prm = {f: np.asarray(x, np.float64) for f, x in prm.items()}
+        self.k = k.float().numpy().astype(np.float64)
+        self.v = v.float().numpy().astype(np.float64)
+        self.q = q[: self.rows].float().numpy().astype(np.float64)
         t0 = time.perf_counter()
-        lib.layer_vs_prefill(qn, kn, vn, prm, [b.tau_v for b in budgets], [b.tau_s for b in budgets],
-                             args.min_budget, args.max_budget if args.max_budget >= 0 else -1, block=32,
-                             threads=threads)
-        times.append(time.perf_counter() - t0)
-    t = min(times)
-    return rows / t, t, kind
+        self.pv, self.ps = self.lib.layer_indexer(self.k, self.v, self.prm, threads)
+        t1 = time.perf_counter()
+        self.iv, self.kv, self.is_, self.ks = self.lib.layer_select(self.pv, self.ps, self.tau_v, self.tau_s,
+                                                                    self.min_b, self.max_b, threads)
+        t2 = time.perf_counter()
+        self.indexer_full_s, self.select_full_s = t1 - t0, t2 - t1
+        lists = [(self.iv[g, : self.kv[g]], self.is_[g, : self.ks[g]]) for g in range(len(self.kv))]
+        # covered pairs per Q head: the layer and the two prefixes
+        self.pairs = {r: np.array([pairs_prefix(*lists[h // self.grp], r) for h in range(self.hq)], np.float64)
+                      for r in (self.n, self.rows, self.rows // 2)}
+
+    def lists(self, g):
+        return self.iv[g, : self.kv[g]].tolist(), self.is_[g, : self.ks[g]].tolist()
+
+    def _sparse(self, rows):
+        hs = np.zeros(self.hq)
+        t0 = time.perf_counter()
+        self.lib.layer_sparse(self.q, self.k, self.v, self.iv, self.kv, self.is_, self.ks, rows=rows,
+                              threads=self.threads, head_s=hs)
+        return time.perf_counter() - t0, hs
+
+    def _makespan(self, per_head):
+        free = [0.0] * min(self.threads, len(per_head))
+        for t in per_head:  # heads in order, each to the first free thread (parallel_heads)
+            i = int(np.argmin(free))
+            free[i] += t
+        return max(free)
+
+    def step(self, i: int) -> dict:
+        n, r, h = self.n, self.rows, self.rows // 2
+        t0 = time.perf_counter()
+        self.lib.layer_select(self.pv, self.ps, self.tau_v, self.tau_s, self.min_b, self.max_b, self.threads)
+        sel = time.perf_counter() - t0
+        wa, ta = self._sparse(h)
+        wb, tb = self._sparse(r)
+        # alpha * rows * hq + beta * pairs = summed per-head call time, at both prefixes
+        A = np.array([[h * self.hq, self.pairs[h].sum()], [r * self.hq, self.pairs[r].sum()]])
+        alpha, beta = np.linalg.solve(A, np.array([ta.sum(), tb.sum()]))
+        if not (alpha >= 0 and beta > 0):  # degenerate sample: fall back to the pair ratio
+            alpha, beta = 0.0, tb.sum() / max(self.pairs[r].sum(), 1.0)
+        attn = self._makespan(alpha * n + beta * self.pairs[n])
+        layer = self.indexer_full_s + sel + attn
+        naive = wb * self.pairs[n].sum() / max(self.pairs[r].sum(), 1.0)
+        return {"step_s": sel + wa + wb, "layer_s": layer, "select_s": sel, "attn_est_s": attn,
+                "attn_rows_s": wb, "attn_half_rows_s": wa, "alpha_s_per_row": alpha, "beta_s_per_pair": beta,
+                "attn_naive_pair_ratio_s": naive}
+
+    def describe(self, recs) -> dict:
+        m = {k_: float(np.mean([x[k_] for x in recs])) for k_ in recs[0]}
+        return {
+            "cpu_model": cpu_model(), "threads": self.threads,
+            "layer_s_est": m["layer_s"],
+            "components_s": {"indexer_full_measured": self.indexer_full_s, "select_full": m["select_s"],
+                             "sparse_attention_est": m["attn_est_s"]},
+            "sample_s": {"sparse_rows": m["attn_rows_s"], "sparse_half_rows": m["attn_half_rows_s"]},
+            "fit": {"alpha_s_per_row_head": m["alpha_s_per_row"], "beta_s_per_pair": m["beta_s_per_pair"],
+                    "pairs_layer": int(self.pairs[self.n].sum()), "pairs_sample": int(self.pairs[self.rows].sum())},
+            "attn_naive_pair_ratio_s": m["attn_naive_pair_ratio_s"],
+            "k_v": self.kv.tolist(), "k_s": self.ks.tolist(),
+        }
+
+    def sample_text(self) -> str:
+        return (f"reference API (oracle/_ref) on the same layer, {self.threads} threads over heads: its own "
+                f"indexer_forward + select_pattern over all n={self.n} (measured once), then per step select_pattern "
+                f"on all n and sparse_attention of all {self.hq} Q heads on rows [0,{self.rows // 2}) and "
+                f"[0,{self.rows}); layer attention extrapolated per head (alpha*rows + beta*covered pairs)")
+
+
+def reference_inputs(args):
+    """The bench layer, its indexer and budgets in a CPU-only process (no CUDA, no libvsp_gpu.so)."""
+    if args.indexer == "random" and args.tau_v is not None and args.tau_s is not None:
+        prm = params_to_numpy(random_params(args))
+        budgets = [(args.tau_v, args.tau_s)] * args.hkv
+        info = {"indexer": f"random-init VSIndexer (make_indexer_params), heads ~ N(0, {args.head_sigma}^2)",
+                "budget_source": "fixed by flags"}
+    else:
+        got = load_prep(args)
+        if got is None:
+            return None
+        prm, budgets, info = got
+    q, k, v = synth_layer(args, "cpu")
+    return q, k, v, prm, budgets, info
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    params, budget, _ = prepare_indexer(args, dev, 0, 1)
-    q, k, v = synth_layer(args, dev)
-    threads = os.cpu_count() or 1
-    rows = args.cpu_sample
-    # keep the whole --steps K --warmup W run to a few minutes: past 5 samples the row prefix
-    # shrinks so that K + W samples cost about as much as 5 default ones
-    if args.steps + args.warmup > 5:
-        rows = max(2048, (args.cpu_sample * 5 // (args.steps + args.warmup)) // 128 * 128)
-    for _ in range(args.warmup):
-        cpu_reference(args, q, k, v, params, budget, rows, threads)
-    ts = []
-    for _ in range(args.steps):
-        _, t, kind = cpu_reference(args, q, k, v, params, budget, rows, threads)
-        ts.append(t)
-    t = float(np.mean(ts))
-    val = rows / t
+    got = reference_inputs(args)
+    if got is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"{os.path.relpath(prep_path(args), ROOT)} missing or "
+                          f"made with other flags (run: python bench.py --prep fresh --save-prep)"}), flush=True)
+        return
+    q, k, v, prm, budgets, info = got
+    threads = host_threads()
+    torch.set_num_threads(threads)
+    ref = ReferenceLayer(args, q, k, v, prm, budgets, threads, args.ref_rows)
+    for i in range(args.warmup):
+        ref.step(i)
+    recs = [ref.step(args.warmup + i) for i in range(args.steps)]
+    t_layer = float(np.mean([r["layer_s"] for r in recs]))
+    val = args.n / t_layer
+    desc = ref.describe(recs)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config[2] LLaMA-3.1-8B geometry layer (32Q/8KV, d=128), n=%d; CPU sample = rows "
-                               "[0,%d) of the same layer, all heads" % (args.n, rows),
-                   "n": args.n, "hq": args.hq, "hkv": args.hkv, "d_h": args.d_h,
-                   "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
-                              "min": args.min_budget, "max": args.max_budget}},
-        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
-                         "sample": f"rows [0,{rows}) of the n={args.n} layer, 32 Q heads; indexer+select+sparse "
-                                   f"through the reference API; per-row cost grows with i so this overstates the "
-                                   f"reference's full-length throughput"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean([r["step_s"] for r in recs])) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world, budgets, info),
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": ref.sample_text(), **desc},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "ms_per_step is the measured sample step; value = n / the extrapolated full-layer time",
     }
     print(json.dumps(line), flush=True)
 
@@ -342,17 +558,24 @@ def main():
         import torch.distributed as dist
         backend = os.environ.get("VSP_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
-    balanced = args.shard in ("balanced", "spread") or (args.shard == "auto" and world > 1)
+    balanced = args.shard in ("balanced", "spread")
     assert balanced or args.hkv % world == 0, "KV heads must divide across ranks"
     import paper_2603_04460_b200 as vsp
     from paper_2603_04460_b200 import parallel
 
     n = args.n
-    # balanced: every rank holds the whole layer and all heads' indexers/budgets (identical,
-    # deterministic preparation) and attends its cost-balanced (head, query-block) units
+    grp = args.hq // args.hkv
+    # every rank holds all heads' (identical, deterministic) indexers and budgets; a heads
+    # rank keeps its slice, a unit rank the whole layer
+    params_full, budgets_full, prep_info = obtain_prep(args, dev)
     srank, sworld = (0, 1) if balanced else (rank, world)
-    params, budget, prep_info = prepare_indexer(args, dev, srank, sworld)
-    units = None
+    hq_r, hkv_r = args.hq // sworld, args.hkv // sworld
+    params = vsp.IndexerParams(*[shard(getattr(params_full, f), srank, sworld, 0)
+                                 for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
+    mx = None if args.max_budget < 0 else args.max_budget
+    budget = [vsp.BudgetConfig(tv, ts, args.min_budget, mx)
+              for tv, ts in budgets_full[srank * hkv_r:(srank + 1) * hkv_r]]
+    units = all_units = None
     if balanced:
         # static cost table: per (head, block) tiles of a validation prompt (not the timed one)
         qv, kv_, vv = synth_layer(args, dev, seed=args.seed + 201)
@@ -361,15 +584,16 @@ def main():
         vsp.sparse_attention(qv, kv_, vv, pat_v, validate=False)
         cost = vsp.sparse_tile_counts(n, args.hkv, pat_v.i_v.shape[1], dev)
         del qv, kv_, vv, a_v, a_s, pat_v
-        units = (parallel.spread_units(cost, world) if args.shard == "spread"
-                 else parallel.balanced_units(cost, world))[rank]
-    q_full, k_full, v_full = synth_layer(args, dev)
-    hq_r, hkv_r = args.hq // sworld, args.hkv // sworld
-    q = shard(q_full, srank, sworld, 1)
-    k = shard(k_full, srank, sworld, 1)
-    v = shard(v_full, srank, sworld, 1)
-    if world > 1 and not balanced:
-        del q_full, k_full, v_full
+        all_units = (parallel.spread_units(cost, world) if args.shard == "spread"
+                     else parallel.balanced_units(cost, world))
+        units = all_units[rank]
+    # the timed prompt, drawn on the CPU (the reference arm draws the identical layer)
+    q_host, k_host, v_host = synth_layer(args, "cpu")
+    q = shard(q_host, srank, sworld, 1).to(dev)
+    k = shard(k_host, srank, sworld, 1).to(dev)
+    v = shard(v_host, srank, sworld, 1).to(dev)
+    if not (rank == 0 and world == 1 and not args.no_cpu_baseline):
+        del q_host, k_host, v_host
     # O is written head-major straight into this rank's slab of the full [Hq, n, d] output
     # (VSP_O_HEAD_MAJOR): the slab is the in-place all-gather send buffer (parallel.py)
     o_full = torch.empty(args.hq, n, 128, dtype=q.dtype, device=dev)
@@ -452,7 +676,6 @@ def main():
     vsp.sparse_attention(q, k, v, pat, validate=False, out=o, lse=lse, head_major=True)
     recall = float(vsp.attention_recall(lse, lse_d).mean().item())
     pairs_kv = covered_pairs(pat, n, hkv_r)
-    grp = args.hq // args.hkv
     pairs_q = int(pairs_kv.sum()) * grp
     dense_pairs = hq_r * n * (n + 1) // 2
     alg_flops = 4.0 * 128 * pairs_q
@@ -470,11 +693,16 @@ def main():
     kv_list = pat.k_v.cpu().tolist()
     ks_list = pat.k_s.cpu().tolist()
 
+    # ---- output assembly over NCCL, reported separately (not inside the step)
     allgather_ms = None
-    if world > 1 and not balanced:
-        # one in-place ncclAllGather of the head-major slabs (O and LSE) through the C ABI
+    if world > 1:
         comm = parallel.VspComm(dev)
-        allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
+        if balanced:  # unit regions broadcast by their owners (vsp_assemble_units)
+            vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
+            allgather_ms = timed(lambda: comm.assemble_units(o_full, lse_full, all_units, args.hkv), reps=3)
+        else:  # one in-place ncclAllGather of the head-major slabs (O and LSE)
+            allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
+        allgather_ms = parallel.max_over_ranks(allgather_ms, dev)
         comm.close()
 
     # ---- e2e through the public API with host buffers (H2D inputs, D2H output every step)
@@ -489,8 +717,7 @@ def main():
         else:
             oh_ = torch.empty(q.shape, dtype=q.dtype).pin_memory()
             lse_h = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
-        grp_ = args.hq // args.hkv
-        d2h_units = sum(grp_ * (hi - lo) * 128 * (128 * 2 + 4) for _, lo, hi in (units or []))
+        d2h_units = sum(grp * (min(hi * 128, n) - lo * 128) * (128 * 2 + 4) for _, lo, hi in (units or []))
 
         def e2e_step():
             if balanced:
@@ -500,7 +727,7 @@ def main():
                 v.copy_(vh, non_blocking=True)
                 vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
                 for g_, lo, hi in units:
-                    hs = slice(g_ * grp_, (g_ + 1) * grp_)
+                    hs = slice(g_ * grp, (g_ + 1) * grp)
                     rs = slice(lo * 128, min(hi * 128, n))
                     oh_[hs, rs].copy_(o_full[hs, rs], non_blocking=True)
                     lse_h[hs, rs].copy_(lse_full[hs, rs], non_blocking=True)
@@ -532,37 +759,31 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            val, secs, kind = cpu_reference(args, q_full, k_full, v_full, params, budget, args.cpu_sample, threads)
-            cpu = {"value": val, "unit": "tokens/s", "cores": threads, "kind": kind,
-                   "sample": f"rows [0,{args.cpu_sample}) of the same layer, all 32 Q heads, indexer+select+sparse "
-                             f"through the reference API, {secs:.1f} s wall; per-row cost grows with i, so this "
-                             f"overstates the reference's 128k throughput"}
+            threads = host_threads()
+            ref = ReferenceLayer(args, q_host, k_host, v_host, params_to_numpy(params_full), budgets_full, threads,
+                                 args.ref_rows)
+            rec = ref.step(0)
+            agree = []
+            for g in range(args.hkv):  # the reference's own pattern vs this build's (same inputs)
+                gv, gs = (set(x) for x in pat.lists(g))
+                rv, rs = (set(x) for x in ref.lists(g))
+                agree.append([round(len(gv & rv) / max(len(gv | rv), 1), 4),
+                              round(len(gs & rs) / max(len(gs | rs), 1), 4)])
+            cpu = {"value": n / rec["layer_s"], "unit": "tokens/s", "cores": threads, "kind": "reference",
+                   "sample": ref.sample_text() + "; one step", **ref.describe([rec]),
+                   "pattern_jaccard_vs_gpu": agree}
         except Exception as ex:  # reported, not fatal
-            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+            cpu = {"value": None, "unit": "tokens/s", "cores": host_threads(), "kind": "reference",
                    "sample": f"failed: {ex}"}
 
     if rank == 0:
+        cfg = workload_config(args, world, budgets_full, prep_info)
         line = {
             "metric": METRIC, "value": n / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": ("config[2]: LLaMA-3.1-8B attention geometry single layer, "
-                                    + (("every head split across ranks (spread units)" if args.shard == "spread"
-                                        else "cost-balanced (KV head, query-block) units") if balanced
-                                       else "KV-head sharded")),
-                       "n": n, "hq": args.hq, "hkv": args.hkv, "d": 128, "d_h": args.d_h,
-                       "indexer": prep_info["indexer"],
-                       "budget": {"tau_v": [b.tau_v for b in budget], "tau_s": [b.tau_s for b in budget],
-                                  "min": args.min_budget,
-                                  "max": args.max_budget, "source": prep_info["budget_source"]},
-                       "prep": {k_: v_ for k_, v_ in prep_info.items() if k_ not in ("indexer", "budget_source")},
-                       "inputs": "planted vertical-slash synthetic layer (synth.py), resident in HBM; Q is 1.07 GB "
-                                 "> L2 so no flush between steps",
-                       "parallelism": (f"{'spread' if args.shard == 'spread' else 'balanced'} units x{world} "
-                                       f"(replicated inputs, static cost table from a "
-                                       f"validation prompt; this rank: {units})" if balanced
-                                       else f"kv-head shard x{world}")},
+            "config": cfg,
+            "units_this_rank": units,
             "speedup_vs_dense": ms_dense / ms_attn, "dense_ms": ms_dense, "vs_attn_ms": ms_attn,
             "unfused_ms": ms_unfused, "heads_per_chunk": hpc,
             "indexer_ms": ms_indexer, "select_ms": ms_select, "recall": recall,

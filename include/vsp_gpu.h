@@ -247,6 +247,31 @@ VSP_API int vsp_vs_aggregate(vsp_ctx* ctx, const void* q, const void* k, int n, 
                      float scale, const float* lse, int reduce, int normalized, float* a_v,
                      float* a_s, void* workspace, void* stream);
 
+/* ---- standalone selection/merge operators (not on the layer path) -----------------
+ * merge.hpp:69-95 (host; the device row merge below uses the same search per thread):
+ * balanced p-way cut points of the merge of ascending a[na] and b[nb], a-first ties;
+ * cuts int64 [(p + 1), 2] = (a_idx, b_idx). p >= 1 ("merge_path_partition: p must be >= 1"). */
+VSP_API int vsp_merge_path_partition(const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t p,
+                                     int64_t* cuts);
+/* merge.hpp:18-56 on the device: the ascending duplicate-free column set of each query row
+ * rows[0..count) (device int32) under one KV head's lists i_v[k_v], i_s[k_s] (device int32,
+ * strictly ascending) -> out int32 [count, out_cap], out_len int32 [count]. One CTA per row,
+ * split across its threads by merge path. flags & VSP_VALIDATE: sync and report the
+ * reference's messages for unsorted lists (checked on every row, as the reference does) and
+ * overflow of out_cap; without it such rows get out_len -1 (i_v) / -2 (i_s) / -3 (cap). */
+VSP_API int vsp_merge_row_columns(vsp_ctx* ctx, const int* i_v, int k_v, const int* i_s, int k_s, const int* rows,
+                                  int count, int* out, int* out_len, int out_cap, int flags, void* stream);
+/* sparsity.hpp:83-97: indices of the k[r] largest entries of each row r of scores [rows, n]
+ * (any fp32 values, -0.0 == 0.0; ties to the lower index; ascending) -> out int32 [rows, cap].
+ * k is a HOST array, checked like the reference (1 <= k[r] <= n) and k[r] <= cap. */
+VSP_API size_t vsp_topk_workspace_size(int rows);
+VSP_API int vsp_topk_indices(vsp_ctx* ctx, const float* scores, int n, int rows, const int* k, int* out, int cap,
+                             void* workspace, void* stream);
+/* vsaggregate.hpp:133-157: group combine of per-head scores v_in/s_in [heads, n] fp32 into
+ * v_out/s_out [n] fp32: mean (VSP_REDUCE_MEAN) or sum (VSP_REDUCE_SUM), f64 in head order. */
+VSP_API int vsp_combine_scores(vsp_ctx* ctx, const float* v_in, const float* s_in, int heads, int n, int reduce,
+                               float* v_out, float* s_out, void* stream);
+
 /* ---- recall from LSE pairs: mean_i exp(lse_sparse - lse_dense) per Q head ---------- */
 VSP_API int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n,
                         int hq, float* recall_per_head, void* stream);
@@ -265,6 +290,13 @@ VSP_API int vsp_comm_unique_id(uint8_t* id);
 VSP_API int vsp_comm_init(vsp_comm** comm, int world, int rank, const uint8_t* id, int device);
 VSP_API int vsp_comm_destroy(vsp_comm* comm);
 VSP_API int vsp_allgather_heads(vsp_comm* comm, void* o_full, float* lse_full, int n, int hq, int d, void* stream);
+/* Assembly of a (KV head, query-block) unit split (balanced / spread): units int32 [count, 4]
+ * = (owner rank, KV head, first query block, end query block), 128-row blocks, the union of
+ * all ranks' units; every rank passes the same list. In place on the head-major o_full
+ * [hq, n, d] bf16 and lse_full [hq, n] fp32 (optional): one ncclBroadcast per (unit, Q head)
+ * from its owner, in one NCCL group. */
+VSP_API int vsp_assemble_units(vsp_comm* comm, void* o_full, float* lse_full, int n, int hq, int hkv, int d,
+                               const int32_t* units, int count, void* stream);
 
 /* ---- interchange formats (host files; no device work) ------------------------------
  * The reference's on-disk formats, so GPU outputs can be diffed against the reference CLI

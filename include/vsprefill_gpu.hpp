@@ -8,6 +8,10 @@
 //   vsp::gpu::indexer_forward      <- vsp::indexer_forward      indexer.hpp:116
 //   vsp::gpu::select_pattern       <- vsp::select_pattern       sparsity.hpp:105
 //   vsp::gpu::cumulative_budget    <- vsp::cumulative_budget    sparsity.hpp:51
+//   vsp::gpu::topk_indices         <- vsp::topk_indices         sparsity.hpp:83
+//   vsp::gpu::merge_row_columns    <- vsp::merge_row_columns    merge.hpp:18
+//   vsp::gpu::merge_path_partition <- vsp::merge_path_partition merge.hpp:69 (host)
+//   vsp::gpu::combine_scores       <- vsp::combine_scores       vsaggregate.hpp:133
 //   vsp::gpu::sparse_attention     <- vsp::sparse_attention     attention.hpp:150
 //   vsp::gpu::blockwise_attention  <- vsp::blockwise_attention  attention.hpp:96
 //   vsp::gpu::attention_recall     <- vsp::attention_recall     attention.hpp:198 (from inputs)
@@ -173,6 +177,77 @@ inline std::size_t cumulative_budget(const std::vector<double>& scores, double t
     int k = 0;
     detail::cuda(cudaMemcpy(&k, kv.p, 4, cudaMemcpyDeviceToHost));
     return static_cast<std::size_t>(k);
+}
+
+// sparsity.hpp:83-97 (values as fp32 on the device; -0.0 == 0.0 as in the reference)
+inline std::vector<std::size_t> topk_indices(const std::vector<double>& scores, std::size_t k) {
+    const std::size_t n = scores.size();
+    require(k >= 1, "topk_indices: k must be >= 1");
+    require(k <= n, "topk_indices: k exceeds score count");
+    auto s = detail::upload_f32(scores);
+    const int kk = static_cast<int>(k);
+    detail::Buf out(k * 4), wsp(vsp_topk_workspace_size(1));
+    detail::check(vsp_topk_indices(detail::context(), s->as<float>(), static_cast<int>(n), 1, &kk, out.as<int>(), kk,
+                                   wsp.p, nullptr));
+    std::vector<int> h(k);
+    detail::cuda(cudaMemcpy(h.data(), out.p, 4 * k, cudaMemcpyDeviceToHost));
+    return std::vector<std::size_t>(h.begin(), h.end());
+}
+
+// merge.hpp:18-56 (one row; the device kernel validates both lists like the reference)
+inline std::vector<std::size_t> merge_row_columns(const std::vector<std::size_t>& i_v,
+                                                  const std::vector<std::size_t>& i_s, std::size_t i) {
+    std::vector<int> a(i_v.begin(), i_v.end()), b(i_s.begin(), i_s.end());
+    const int row = static_cast<int>(i), cap = static_cast<int>(a.size() + b.size());
+    detail::Buf da(a.size() * 4), db(b.size() * 4), dr(4), out(cap * 4), len(4);
+    if (!a.empty()) detail::cuda(cudaMemcpy(da.p, a.data(), a.size() * 4, cudaMemcpyHostToDevice));
+    if (!b.empty()) detail::cuda(cudaMemcpy(db.p, b.data(), b.size() * 4, cudaMemcpyHostToDevice));
+    detail::cuda(cudaMemcpy(dr.p, &row, 4, cudaMemcpyHostToDevice));
+    detail::check(vsp_merge_row_columns(detail::context(), da.as<int>(), static_cast<int>(a.size()), db.as<int>(),
+                                        static_cast<int>(b.size()), dr.as<int>(), 1, out.as<int>(), len.as<int>(),
+                                        cap, VSP_VALIDATE, nullptr));
+    int m = 0;
+    detail::cuda(cudaMemcpy(&m, len.p, 4, cudaMemcpyDeviceToHost));
+    std::vector<int> h(m);
+    if (m) detail::cuda(cudaMemcpy(h.data(), out.p, 4 * m, cudaMemcpyDeviceToHost));
+    return std::vector<std::size_t>(h.begin(), h.end());
+}
+
+// merge.hpp:69-95 (host code of the C ABI; the device row merge runs the same search)
+inline std::vector<MergeCut> merge_path_partition(const std::vector<std::size_t>& a, const std::vector<std::size_t>& b,
+                                                  std::size_t p) {
+    require(p >= 1, "merge_path_partition: p must be >= 1");
+    std::vector<int64_t> x(a.begin(), a.end()), y(b.begin(), b.end()), cuts(2 * (p + 1));
+    detail::check(vsp_merge_path_partition(x.data(), static_cast<int64_t>(x.size()), y.data(),
+                                           static_cast<int64_t>(y.size()), static_cast<int64_t>(p), cuts.data()));
+    std::vector<MergeCut> out(p + 1);
+    for (std::size_t s = 0; s <= p; ++s)
+        out[s] = {static_cast<std::size_t>(cuts[2 * s]), static_cast<std::size_t>(cuts[2 * s + 1])};
+    return out;
+}
+
+// vsaggregate.hpp:133-157 (fp32 scores on the device, f64 accumulation in head order)
+inline VSScores combine_scores(const std::vector<VSScores>& heads, GroupReduce reduce = GroupReduce::Mean) {
+    require(!heads.empty(), "combine_scores: no heads");
+    const std::size_t n = heads.front().n();
+    const bool normalized = heads.front().normalized;
+    std::vector<double> v, s;
+    for (const VSScores& h : heads) {
+        require(h.n() == n && h.slash.size() == n, "combine_scores: length mismatch");
+        require(h.normalized == normalized, "combine_scores: mixed raw/normalized inputs");
+        v.insert(v.end(), h.vertical.begin(), h.vertical.end());
+        s.insert(s.end(), h.slash.begin(), h.slash.end());
+    }
+    auto dv = detail::upload_f32(v), ds = detail::upload_f32(s);
+    detail::Buf ov(n * 4), os(n * 4);
+    detail::check(vsp_combine_scores(detail::context(), dv->as<float>(), ds->as<float>(), static_cast<int>(heads.size()),
+                                     static_cast<int>(n), reduce == GroupReduce::Mean ? VSP_REDUCE_MEAN : VSP_REDUCE_SUM,
+                                     ov.as<float>(), os.as<float>(), nullptr));
+    VSScores out;
+    out.vertical = detail::download_f32(ov, n);
+    out.slash = detail::download_f32(os, n);
+    out.normalized = reduce == GroupReduce::Mean ? normalized : false;
+    return out;
 }
 
 namespace detail {

@@ -83,6 +83,13 @@ def _bind(lib, prefix: str):
                                                   ctypes.c_size_t])
         sig["layer_dense"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64, ctypes.c_int,
                                              _f64p, _cp, ctypes.c_size_t])
+        sig["layer_indexer"] = (ctypes.c_int, [_i64, _i64, _i64, _f64p, _f64p, _i64, _f64p, _f64p, _f64p, _f64p,
+                                               _f64p, _f64p, ctypes.c_int, _f64p, _f64p, _f64p, _cp,
+                                               ctypes.c_size_t])
+        sig["layer_select"] = (ctypes.c_int, [_i64, _i64, _f64p, _f64p, _f64p, _f64p, _i64, _i64, _i64,
+                                              ctypes.c_int, _i64p, _i64p, _i64p, _i64p, _cp, ctypes.c_size_t])
+        sig["layer_sparse"] = (ctypes.c_int, [_i64, _i64, _i64, _i64, _f64p, _f64p, _f64p, _i64p, _i64p, _i64p,
+                                              _i64p, _i64, _i64, ctypes.c_int, _f64p, _f64p, _cp, ctypes.c_size_t])
     for name, (res, args) in sig.items():
         fn = getattr(lib, prefix + name)
         fn.restype = res
@@ -305,6 +312,57 @@ class _Oracle:
         q, k, v = (np.ascontiguousarray(x, np.float64) for x in (q, k, v))
         o = np.zeros((n, hq, d))
         rc, msg = self._call("layer_dense", n, hq, hkv, d, _f(q), _f(k), _f(v), int(block), int(threads), _f(o))
+        self._check(rc, msg)
+        return o
+
+
+    # ---- the layer in stages (ref only): bounded samples for bench.py's reference arm
+    def layer_indexer(self, k, v, params, threads=1, head_s=None):
+        """indexer_forward of every KV head over all rows of k/v [len, hkv, d] -> (A_v, A_s) [hkv, len].
+        head_s (optional f64 [hkv]) receives each head's call time on its worker thread."""
+        assert self.is_ref
+        ln, hkv, d = k.shape
+        k, v = (np.ascontiguousarray(x, np.float64) for x in (k, v))
+        w_u = np.ascontiguousarray(params["w_u"], np.float64)
+        b_u, w_v, w_s, b_v, b_s = (np.ascontiguousarray(params[x], np.float64)
+                                   for x in ("b_u", "w_v", "w_s", "b_v", "b_s"))
+        pv = np.zeros((hkv, ln))
+        ps = np.zeros((hkv, ln))
+        rc, msg = self._call("layer_indexer", ln, hkv, d, _f(k), _f(v), w_u.shape[2], _f(w_u), _f(b_u), _f(w_v),
+                             _f(b_v), _f(w_s), _f(b_s), int(threads), _f(pv), _f(ps),
+                             _f(head_s) if head_s is not None else None)
+        self._check(rc, msg)
+        return pv, ps
+
+    def layer_select(self, pred_v, pred_s, tau_v, tau_s, min_budget=1, max_budget=-1, threads=1):
+        """select_pattern of every KV head -> (i_v [hkv, cap], k_v [hkv], i_s, k_s), cap = n + 1."""
+        assert self.is_ref
+        pred_v, pred_s = (np.ascontiguousarray(x, np.float64) for x in (pred_v, pred_s))
+        hkv, n = pred_v.shape
+        tau_v = np.ascontiguousarray(np.broadcast_to(np.asarray(tau_v, np.float64), (hkv,)))
+        tau_s = np.ascontiguousarray(np.broadcast_to(np.asarray(tau_s, np.float64), (hkv,)))
+        cap = n + 1
+        iv = np.zeros((hkv, cap), np.int64)
+        is_ = np.zeros((hkv, cap), np.int64)
+        kv = np.zeros(hkv, np.int64)
+        ks = np.zeros(hkv, np.int64)
+        rc, msg = self._call("layer_select", n, hkv, _f(pred_v), _f(pred_s), _f(tau_v), _f(tau_s), int(min_budget),
+                             int(max_budget), cap, int(threads), _i(iv), _i(kv), _i(is_), _i(ks))
+        self._check(rc, msg)
+        return iv, kv, is_, ks
+
+    def layer_sparse(self, q, k, v, iv, kv, is_, ks, rows=None, block=32, threads=1, head_s=None):
+        """sparse_attention of every Q head over rows [0, rows) (q/k/v hold at least `rows`
+        tokens) with per-KV-head patterns (i_v [hkv, cap] ...) -> O [rows, hq, d]."""
+        assert self.is_ref
+        rows = q.shape[0] if rows is None else rows
+        _, hq, d = q.shape
+        hkv = k.shape[1]
+        q, k, v = (np.ascontiguousarray(x[:rows], np.float64) for x in (q, k, v))
+        iv, kv, is_, ks = (np.ascontiguousarray(x, np.int64) for x in (iv, kv, is_, ks))
+        o = np.zeros((rows, hq, d))
+        rc, msg = self._call("layer_sparse", rows, hq, hkv, d, _f(q), _f(k), _f(v), _i(iv), _i(kv), _i(is_), _i(ks),
+                             iv.shape[1], int(block), int(threads), _f(o), _f(head_s) if head_s is not None else None)
         self._check(rc, msg)
         return o
 

@@ -9,6 +9,7 @@
 // f64, index lists are int64, errors return 1 with the exception text in err.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -284,6 +285,94 @@ int vspref_layer_vs_prefill(int64_t n, int64_t hq, int64_t hkv, int64_t d, const
     });
     if (failed) return set_err(err, errlen, first_err.c_str());
     return 0;
+}
+
+// ---- the layer in stages, for the bench's reference arm (bounded samples of one layer) ----
+// Each stage calls the reference per head exactly as the reference's own callers do
+// (indexer_forward -> select_pattern -> sparse_attention, tools/vsprefill.cpp:154-185), threaded
+// over heads with std::thread. Tensors are token-major f64 ([tokens, heads, d]).
+
+}  // extern "C"
+
+namespace {
+// item_s (optional, [items]): wall seconds of each item's call on its worker thread.
+template <class Body>
+int parallel_heads(int64_t items, int n_threads, char* err, size_t errlen, Body&& body, double* item_s = nullptr) {
+    std::atomic<int64_t> next{0};
+    std::atomic<int> failed{0};
+    std::string first_err;
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, std::min<int>(n_threads, static_cast<int>(items)));
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+            for (int64_t it; (it = next.fetch_add(1)) < items;) {
+                const auto t0 = std::chrono::steady_clock::now();
+                try {
+                    body(it);
+                } catch (const std::exception& e) {
+                    if (failed.exchange(1) == 0) first_err = e.what();
+                }
+                if (item_s)
+                    item_s[it] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            }
+        });
+    for (auto& th : pool) th.join();
+    return failed ? set_err(err, errlen, first_err.c_str()) : 0;
+}
+}  // namespace
+
+extern "C" {
+
+// indexer_forward (indexer.hpp:116-120) of every KV head over `len` tokens: pred/logits [hkv, len].
+int vspref_layer_indexer(int64_t len, int64_t hkv, int64_t d, const double* k, const double* v, int64_t d_h,
+                         const double* w_u, const double* b_u, const double* w_v, const double* b_v,
+                         const double* w_s, const double* b_s, int n_threads, double* pred_v, double* pred_s,
+                         double* head_s, char* err, size_t errlen) {
+    return parallel_heads(hkv, n_threads, err, errlen, [&](int64_t g) {
+        auto p = params(d, d_h, w_u + g * 2 * d * d_h, b_u + g * d_h, w_v + g * d_h, b_v[g], w_s + g * d_h, b_s[g]);
+        auto acts = vsp::indexer_forward(p, gather(k + g * d, hkv * d, len, d), gather(v + g * d, hkv * d, len, d));
+        std::copy(acts.pred_v.begin(), acts.pred_v.end(), pred_v + g * len);
+        std::copy(acts.pred_s.begin(), acts.pred_s.end(), pred_s + g * len);
+    }, head_s);
+}
+
+// select_pattern (sparsity.hpp:105-114) of every KV head: lists [hkv, cap] int64 + counts.
+int vspref_layer_select(int64_t n, int64_t hkv, const double* pred_v, const double* pred_s, const double* tau_v,
+                        const double* tau_s, int64_t min_b, int64_t max_b, int64_t cap, int n_threads,
+                        int64_t* iv, int64_t* kv, int64_t* is, int64_t* ks, char* err, size_t errlen) {
+    return parallel_heads(hkv, n_threads, err, errlen, [&](int64_t g) {
+        vsp::VSScores sc{std::vector<double>(pred_v + g * n, pred_v + (g + 1) * n),
+                         std::vector<double>(pred_s + g * n, pred_s + (g + 1) * n), true};
+        auto sel = vsp::select_pattern(sc, budget(tau_v[g], tau_s[g], min_b, max_b));
+        if (static_cast<int64_t>(sel.i_v.size()) > cap || static_cast<int64_t>(sel.i_s.size()) > cap)
+            throw std::invalid_argument("layer_select: cap too small");
+        kv[g] = static_cast<int64_t>(sel.i_v.size());
+        ks[g] = static_cast<int64_t>(sel.i_s.size());
+        for (size_t t = 0; t < sel.i_v.size(); ++t) iv[g * cap + t] = static_cast<int64_t>(sel.i_v[t]);
+        for (size_t t = 0; t < sel.i_s.size(); ++t) is[g * cap + t] = static_cast<int64_t>(sel.i_s[t]);
+    });
+}
+
+// sparse_attention (attention.hpp:150-194) of every Q head over the first `rows` tokens with the
+// given per-KV-head patterns (selected on the full sequence): causality makes these rows of the
+// output identical to the full layer's. o [rows, hq, d].
+int vspref_layer_sparse(int64_t rows, int64_t hq, int64_t hkv, int64_t d, const double* q, const double* k,
+                        const double* v, const int64_t* iv, const int64_t* kv, const int64_t* is,
+                        const int64_t* ks, int64_t cap, int64_t block, int n_threads, double* o, double* head_s,
+                        char* err, size_t errlen) {
+    const int64_t group = hq / hkv;
+    std::vector<vsp::SparsePattern> pats(static_cast<size_t>(hkv));
+    for (int64_t g = 0; g < hkv; ++g) {
+        pats[g].i_v = idx(iv + g * cap, kv[g]);
+        pats[g].i_s = idx(is + g * cap, ks[g]);
+    }
+    return parallel_heads(hq, n_threads, err, errlen, [&](int64_t h) {
+        const int64_t g = h / group;
+        vsp::AttentionInputs in(gather(q + h * d, hq * d, rows, d), gather(k + g * d, hkv * d, rows, d),
+                                gather(v + g * d, hkv * d, rows, d));
+        auto out = vsp::sparse_attention(in, pats[g], static_cast<size_t>(block));
+        for (int64_t t = 0; t < rows; ++t) std::memcpy(o + (t * hq + h) * d, out.o.row_ptr(t), sizeof(double) * d);
+    }, head_s);
 }
 
 // Dense causal layer through blockwise_attention (attention.hpp:96-145), threaded.

@@ -34,6 +34,7 @@ __all__ = [
     "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
     "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
     "aggregate_streaming", "attention_recall", "RopeConfig", "apply_rope", "apply_rope_qk", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "vs_prefill_units", "sparse_tile_counts", "lib_path", "load_library",
+    "topk_indices", "combine_scores", "merge_row_columns", "merge_path_partition",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -103,6 +104,12 @@ def load_library():
     lib.vsp_vs_attn_tile_counts.argtypes = [vp, i, i, i, vp, vp, vp]
     lib.vsp_vs_prefill_units.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
                                           ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, i, i, vp])
+    lib.vsp_merge_path_partition.argtypes = [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int64, vp]
+    lib.vsp_merge_row_columns.argtypes = [vp, vp, i, vp, i, vp, i, vp, vp, i, i, vp]
+    lib.vsp_topk_workspace_size.restype = sz
+    lib.vsp_topk_workspace_size.argtypes = [i]
+    lib.vsp_topk_indices.argtypes = [vp, vp, i, i, vp, vp, i, vp, vp]
+    lib.vsp_combine_scores.argtypes = [vp, vp, vp, i, i, i, vp, vp, vp]
     _lib = lib
     return lib
 
@@ -386,6 +393,75 @@ def attention_recall(lse_sparse: torch.Tensor, lse_dense: torch.Tensor) -> torch
     _check(load_library().vsp_recall_from_lse(_context(dev), _ptr(lse_sparse), _ptr(lse_dense), n, hq, _ptr(out),
                                               _stream(dev)))
     return out
+
+
+def topk_indices(scores: torch.Tensor, k) -> torch.Tensor:
+    """topk_indices (sparsity.hpp:83-97) per row of scores [rows, n] (or [n]) fp32, any sign:
+    the k largest, ties to the lower index, ascending -> int32 [rows, max k] (row r filled up
+    to k[r]; k an int or one per row)."""
+    _need_cuda(scores)
+    one = scores.dim() == 1
+    x = scores.reshape(1, -1) if one else scores
+    x = x.contiguous().float()
+    rows, n = x.shape
+    ks = [int(k)] * rows if isinstance(k, int) else [int(t) for t in k]
+    lib = load_library()
+    cap = max(max(ks), 1) if ks else 1
+    out = torch.zeros(rows, cap, dtype=torch.int32, device=x.device)
+    karr = (ctypes.c_int * max(rows, 1))(*ks)
+    ws = _workspace(x.device, lib.vsp_topk_workspace_size(rows))
+    _check(lib.vsp_topk_indices(_context(x.device), _ptr(x), n, rows, ctypes.cast(karr, ctypes.c_void_p), _ptr(out),
+                                cap, _ptr(ws), _stream(x.device)))
+    return out[0] if one else out
+
+
+def combine_scores(vertical: torch.Tensor, slash: torch.Tensor, reduce: str = "mean"):
+    """combine_scores (vsaggregate.hpp:133-157): per-head scores [heads, n] -> the group's
+    [n] (mean keeps normalisation, sum gives the raw total; f64 accumulation in head order)."""
+    _need_cuda(vertical, slash)
+    if vertical.dim() != 2 or vertical.shape != slash.shape:
+        raise VspError("combine_scores: length mismatch")
+    heads, n = vertical.shape
+    v_out = torch.empty(n, dtype=torch.float32, device=vertical.device)
+    s_out = torch.empty_like(v_out)
+    lib = load_library()
+    _check(lib.vsp_combine_scores(_context(vertical.device), _ptr(vertical.contiguous().float()),
+                                  _ptr(slash.contiguous().float()), heads, n, 0 if reduce == "mean" else 1,
+                                  _ptr(v_out), _ptr(s_out), _stream(vertical.device)))
+    return v_out, s_out
+
+
+def merge_row_columns(i_v: torch.Tensor, i_s: torch.Tensor, rows, validate: bool = True):
+    """merge_row_columns (merge.hpp:18-56) on the device for query rows `rows` (int or 1-D
+    int tensor / list) under one KV head's ascending lists i_v, i_s (int32 device tensors)
+    -> list of int32 tensors (one ascending column set per row)."""
+    _need_cuda(i_v, i_s)
+    dev = i_v.device
+    one = isinstance(rows, int)
+    r = torch.as_tensor([rows] if one else rows, dtype=torch.int32).to(dev)
+    count = r.numel()
+    cap = i_v.numel() + i_s.numel()
+    out = torch.empty(count, max(cap, 1), dtype=torch.int32, device=dev)
+    lens = torch.empty(count, dtype=torch.int32, device=dev)
+    lib = load_library()
+    _check(lib.vsp_merge_row_columns(_context(dev), _ptr(i_v.int().contiguous()), i_v.numel(),
+                                     _ptr(i_s.int().contiguous()), i_s.numel(), _ptr(r), count, _ptr(out),
+                                     _ptr(lens), max(cap, 1), VSP_VALIDATE if validate else 0, _stream(dev)))
+    res = [out[t, : int(lens[t])] for t in range(count)]
+    return res[0] if one else res
+
+
+def merge_path_partition(a, b, p: int):
+    """merge_path_partition (merge.hpp:69-95): p + 1 (a_idx, b_idx) cut points of the merge of
+    ascending a and b, a-first ties (host; the device row merge uses the same search)."""
+    import numpy as np
+    av = np.ascontiguousarray(np.asarray(a, dtype=np.int64).reshape(-1))
+    bv = np.ascontiguousarray(np.asarray(b, dtype=np.int64).reshape(-1))
+    cuts = np.zeros(2 * (max(int(p), 1) + 1), np.int64)
+    lib = load_library()
+    _check(lib.vsp_merge_path_partition(ctypes.c_void_p(av.ctypes.data), len(av), ctypes.c_void_p(bv.ctypes.data),
+                                        len(bv), int(p), ctypes.c_void_p(cuts.ctypes.data)))
+    return [tuple(int(x) for x in c) for c in cuts.reshape(-1, 2)]
 
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,

@@ -484,11 +484,10 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     }
     cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long) * a.hkv * a.n, stream);
     if (e != cudaSuccess) return e;
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr = true;
-    }
+    });
     long long ctas = 0;
     for (int qc = 0; qc < p.num_qc; ++qc) ctas += static_cast<long long>(std::min(p.num_qb, kChunk * (qc + 1))) * a.hkv;
     vsp_detail::count_launch();

@@ -796,12 +796,11 @@ int persistent_grid(int items) {
 // item. Grid: one CTA per SM, never more CTAs than items need.
 template <bool kSparse>
 cudaError_t launch_attn(AttnParams& p, int nqb, cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         cudaFuncSetAttribute(attn_fwd_kernel<kSparse, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         cudaFuncSetAttribute(attn_fwd_kernel<kSparse, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr_set = true;
-    }
+    });
     const int grp = p.hq / p.hkv;
     const bool mc = ((grp + 1) / 2) % 2 == 0 && p.pair0 % 2 == 0 && p.npairs % 2 == 0 && !getenv_flag("VSP_NO_MULTICAST");
     vsp_detail::count_launch();

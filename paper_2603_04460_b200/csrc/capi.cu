@@ -15,6 +15,7 @@
 #include "aggregate.h"
 #include "attn.h"
 #include "indexer.h"
+#include "misc_ops.h"
 #include "rope.h"
 #include "select.h"
 #include "train.h"
@@ -35,7 +36,6 @@ extern "C" long long vsp_kernel_launches(void) { return vsp_detail::g_launches.l
 struct vsp_ctx {
     int device = 0;
     int sm_count = 0;
-    int* d_flags = nullptr;  // [1024] validation results
     // vsp_vs_prefill pipelining: high-priority side stream and per-chunk events
     static constexpr int kMaxChunks = 64;
     cudaStream_t side = nullptr;
@@ -73,19 +73,21 @@ __global__ void validate_pattern_kernel(const int* iv, const int* kv, const int*
                                         int cap, int* flags) {
     const int g = blockIdx.x;
     const int nv = kv[g], ns = ks[g];
+    // the list scans stay inside the row even when a count is out of range (flag 16)
+    const int nv_c = nv < 0 ? 0 : (nv > cap ? cap : nv), ns_c = ns < 0 ? 0 : (ns > cap ? cap : ns);
     const int* a = iv + static_cast<size_t>(g) * cap;
     const int* b = is + static_cast<size_t>(g) * cap;
     int f = 0;
-    for (int t = threadIdx.x; t < nv; t += blockDim.x) {
+    for (int t = threadIdx.x; t < nv_c; t += blockDim.x) {
         if (a[t] < 0) f |= 8;
         if (t > 0 && !(a[t - 1] < a[t])) f |= 1;
     }
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+    for (int t = threadIdx.x; t < ns_c; t += blockDim.x) {
         if (b[t] < 0) f |= 8;
         if (t > 0 && !(b[t - 1] < b[t])) f |= 2;
     }
     if (threadIdx.x == 0) {
-        const bool covered0 = (nv > 0 && a[0] == 0) || (ns > 0 && b[0] == 0);
+        const bool covered0 = (nv_c > 0 && a[0] == 0) || (ns_c > 0 && b[0] == 0);
         if (!covered0) f |= 4;
         if (nv < 0 || ns < 0 || nv > cap || ns > cap) f |= 16;
     }
@@ -147,8 +149,7 @@ int vsp_create(vsp_ctx** out, int device) {
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
     cudaSetDevice(device);
-    e = cudaMalloc(&ctx->d_flags, 1024 * sizeof(int));
-    if (e == cudaSuccess) {
+    {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi);
@@ -172,7 +173,6 @@ int vsp_create(vsp_ctx** out, int device) {
 int vsp_destroy(vsp_ctx* ctx) {
     if (!ctx) return VSP_OK;
     cudaSetDevice(ctx->device);
-    cudaFree(ctx->d_flags);
     for (int i = 0; i < vsp_ctx::kTimingSlots; ++i)
         for (cudaEvent_t ev : {ctx->t_beg[i], ctx->t_end[i]})
             if (ev) cudaEventDestroy(ev);
@@ -198,8 +198,14 @@ int vsp_dense_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_dense_attn_fwd");
 }
 
+// The caller's workspace ends with this call's validation flags ([hkv] ints), so concurrent
+// validating calls on different streams never share device state.
+static size_t validate_flags_offset(int n, int hkv, int cap) {
+    return (vsp_attn::sparse_workspace_bytes(n, hkv, cap) + 255) / 256 * 256;
+}
+
 size_t vsp_vs_attn_workspace_size(int n, int hkv, int cap) {
-    return vsp_attn::sparse_workspace_bytes(n, hkv, cap);
+    return validate_flags_offset(n, hkv, cap) + 1024 * sizeof(int);
 }
 
 int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
@@ -215,9 +221,10 @@ int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, i
     if (flags & VSP_VALIDATE) {
         if (hkv > 1024) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: too many heads to validate");
         vsp_detail::count_launch();
-        validate_pattern_kernel<<<hkv, 256, 0, st>>>(i_v, k_v, i_s, k_s, cap, ctx->d_flags);
+        int* d_flags = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) + validate_flags_offset(n, hkv, cap));
+        validate_pattern_kernel<<<hkv, 256, 0, st>>>(i_v, k_v, i_s, k_s, cap, d_flags);
         int hflags[1024];
-        cudaError_t e = cudaMemcpyAsync(hflags, ctx->d_flags, sizeof(int) * hkv, cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaMemcpyAsync(hflags, d_flags, sizeof(int) * hkv, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return cuda_err(e, "vsp_vs_attn_fwd(validate)");
         for (int g = 0; g < hkv; ++g) {
@@ -235,6 +242,71 @@ int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, i
     vsp_attn::SparseArgs s{i_v, k_v, i_s, k_s, cap};
     cudaError_t e = vsp_attn::launch_sparse(a, s, workspace, st);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_attn_fwd");
+}
+
+int vsp_merge_path_partition(const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t p, int64_t* cuts) {
+    if (p < 1) return set_err(VSP_EINVAL, "merge_path_partition: p must be >= 1");
+    if (na < 0 || nb < 0 || !cuts || (na && !a) || (nb && !b))
+        return set_err(VSP_EINVAL, "merge_path_partition: bad arguments");
+    vsp_misc::merge_path_partition_host(a, na, b, nb, p, cuts);
+    return VSP_OK;
+}
+
+int vsp_merge_row_columns(vsp_ctx* ctx, const int* i_v, int k_v, const int* i_s, int k_s, const int* rows,
+                          int count, int* out, int* out_len, int out_cap, int flags, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (k_v < 0 || k_s < 0 || count < 0 || out_cap < 0 || (count && (!rows || !out_len)))
+        return set_err(VSP_EINVAL, "merge_row_columns: bad arguments");
+    if (flags & ~VSP_VALIDATE) return set_err(VSP_EINVAL, "merge_row_columns: unknown flags");
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = vsp_misc::launch_merge_rows(i_v, k_v, i_s, k_s, rows, count, out, out_len, out_cap,
+                                                (flags & VSP_VALIDATE) != 0, st);
+    if (e != cudaSuccess) return cuda_err(e, "vsp_merge_row_columns");
+    if (flags & VSP_VALIDATE) {
+        std::vector<int> len(count);
+        e = cudaMemcpyAsync(len.data(), out_len, sizeof(int) * count, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_err(e, "vsp_merge_row_columns(validate)");
+        for (int r = 0; r < count; ++r) {
+            if (len[r] == -1) return set_err(VSP_EINVAL, "merge_row_columns: i_v not strictly ascending");
+            if (len[r] == -2) return set_err(VSP_EINVAL, "merge_row_columns: i_s not strictly ascending");
+            if (len[r] == -3) return set_err(VSP_EINVAL, "merge_row_columns: out_cap too small");
+        }
+    }
+    return VSP_OK;
+}
+
+size_t vsp_topk_workspace_size(int rows) { return static_cast<size_t>(rows > 0 ? rows : 1) * sizeof(int); }
+
+int vsp_topk_indices(vsp_ctx* ctx, const float* scores, int n, int rows, const int* k, int* out, int cap,
+                     void* workspace, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (rows < 0 || (rows && (!scores || !k || !out || !workspace)))
+        return set_err(VSP_EINVAL, "topk_indices: bad arguments");
+    for (int r = 0; r < rows; ++r) {
+        if (k[r] < 1) return set_err(VSP_EINVAL, "topk_indices: k must be >= 1");
+        if (k[r] > n) return set_err(VSP_EINVAL, "topk_indices: k exceeds score count");
+        if (k[r] > cap) return set_err(VSP_EINVAL, "topk_indices: k exceeds cap");
+    }
+    cudaStream_t st = as_stream(stream);
+    int* kd = static_cast<int*>(workspace);
+    cudaError_t e = rows ? cudaMemcpyAsync(kd, k, sizeof(int) * rows, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    if (e == cudaSuccess) e = vsp_misc::launch_topk(scores, n, rows, kd, out, cap, st);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_topk_indices");
+}
+
+int vsp_combine_scores(vsp_ctx* ctx, const float* v_in, const float* s_in, int heads, int n, int reduce,
+                       float* v_out, float* s_out, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    if (heads < 1) return set_err(VSP_EINVAL, "combine_scores: no heads");
+    if (n < 0 || (n && (!v_in || !s_in || !v_out || !s_out)))
+        return set_err(VSP_EINVAL, "combine_scores: bad arguments");
+    if (reduce != VSP_REDUCE_MEAN && reduce != VSP_REDUCE_SUM)
+        return set_err(VSP_EINVAL, "combine_scores: unknown reduce");
+    if (n == 0) return VSP_OK;
+    cudaError_t e = vsp_misc::launch_combine(v_in, s_in, heads, n, reduce == VSP_REDUCE_MEAN, v_out, s_out,
+                                             as_stream(stream));
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_combine_scores");
 }
 
 int vsp_recall_from_lse(vsp_ctx* ctx, const float* lse_sparse, const float* lse_dense, int n, int hq,

@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -38,6 +39,7 @@ struct Nccl {
     ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*destroy)(ncclComm_t) = nullptr;
     ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*group_start)() = nullptr;
     ncclResult_t (*group_end)() = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
@@ -62,11 +64,12 @@ Nccl& nccl() {
         n.init_rank = reinterpret_cast<decltype(n.init_rank)>(sym("ncclCommInitRank"));
         n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("ncclCommDestroy"));
         n.all_gather = reinterpret_cast<decltype(n.all_gather)>(sym("ncclAllGather"));
+        n.broadcast = reinterpret_cast<decltype(n.broadcast)>(sym("ncclBroadcast"));
         n.group_start = reinterpret_cast<decltype(n.group_start)>(sym("ncclGroupStart"));
         n.group_end = reinterpret_cast<decltype(n.group_end)>(sym("ncclGroupEnd"));
         n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
-        if (!n.get_unique_id || !n.init_rank || !n.destroy || !n.all_gather || !n.group_start || !n.group_end ||
-            !n.error_string)
+        if (!n.get_unique_id || !n.init_rank || !n.destroy || !n.all_gather || !n.broadcast || !n.group_start ||
+            !n.group_end || !n.error_string)
             n.load_error = "vsp: NCCL library lacks a required symbol";
     });
     return n;
@@ -138,6 +141,46 @@ int vsp_allgather_heads(vsp_comm* c, void* o_full, float* lse_full, int n, int h
         r = nc.all_gather(lse_full + c->rank * l_count, lse_full, l_count, ncclFloat32, c->comm, st);
     const ncclResult_t r2 = nc.group_end();
     if (r != ncclSuccess) return nccl_err(r, "ncclAllGather");
+    if (r2 != ncclSuccess) return nccl_err(r2, "ncclGroupEnd");
+    return VSP_OK;
+}
+
+// Assembly of a unit split (balanced / spread): unit u = (owner rank, KV head g, query blocks
+// [lo, hi)) was attended by its owner, which wrote O rows [128 lo, min(128 hi, n)) of the
+// group's Q heads into its head-major o_full (and lse_full). Each such region is contiguous
+// per Q head, so the assembly is one in-place ncclBroadcast per (unit, Q head) from its
+// owner, all inside one NCCL group (one launch per peer set, transfers overlapped).
+int vsp_assemble_units(vsp_comm* c, void* o_full, float* lse_full, int n, int hq, int hkv, int d,
+                       const int32_t* units, int count, void* stream) {
+    if (!c) return set_err(VSP_EINVAL, "vsp_assemble_units: null communicator");
+    if (!o_full || n < 1 || hq < 1 || hkv < 1 || hq % hkv || d < 1 || count < 0 || (count && !units))
+        return set_err(VSP_EINVAL, "vsp_assemble_units: bad arguments");
+    const int grp = hq / hkv, nqb = (n + 127) / 128;
+    for (int u = 0; u < count; ++u) {
+        const int32_t* x = units + 4 * u;
+        if (x[0] < 0 || x[0] >= c->world || x[1] < 0 || x[1] >= hkv || x[2] < 0 || x[2] >= x[3] || x[3] > nqb)
+            return set_err(VSP_EINVAL, "vsp_assemble_units: unit " + std::to_string(u) + " out of range");
+    }
+    if (cudaSetDevice(c->device) != cudaSuccess) return set_err(VSP_ECUDA, "vsp_assemble_units: cannot select device");
+    Nccl& nc = nccl();
+    auto* o = static_cast<uint16_t*>(o_full);  // bf16 storage
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ncclResult_t r = nc.group_start();
+    for (int u = 0; u < count && r == ncclSuccess; ++u) {
+        const int32_t* x = units + 4 * u;
+        const size_t r0 = static_cast<size_t>(x[2]) * 128, r1 = std::min(static_cast<size_t>(x[3]) * 128,
+                                                                         static_cast<size_t>(n));
+        for (int h = x[1] * grp; h < (x[1] + 1) * grp && r == ncclSuccess; ++h) {
+            uint16_t* ob = o + (static_cast<size_t>(h) * n + r0) * d;
+            r = nc.broadcast(ob, ob, (r1 - r0) * d, ncclBfloat16, x[0], c->comm, st);
+            if (r == ncclSuccess && lse_full) {
+                float* lb = lse_full + static_cast<size_t>(h) * n + r0;
+                r = nc.broadcast(lb, lb, r1 - r0, ncclFloat32, x[0], c->comm, st);
+            }
+        }
+    }
+    const ncclResult_t r2 = nc.group_end();
+    if (r != ncclSuccess) return nccl_err(r, "ncclBroadcast");
     if (r2 != ncclSuccess) return nccl_err(r2, "ncclGroupEnd");
     return VSP_OK;
 }

@@ -294,21 +294,15 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.hkv = a.hkv;
     p.d_h = a.d_h;
     p.reverse = a.reverse ? 1 : 0;
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         cudaFuncSetAttribute(indexer_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr = true;
-    }
+    });
     const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
     p.g0 = a.g0;
     p.count = count;
     p.tiles = (a.n + kTok - 1) / kTok;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = vsp_detail::current_sm_count();
     const int work = p.tiles * count;
     vsp_detail::count_launch();
     indexer_gemm_kernel<<<work < sms ? work : sms, kThreads, kSmemBytes, stream>>>(p);

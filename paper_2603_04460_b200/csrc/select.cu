@@ -176,6 +176,14 @@ __device__ void load_slice(float* xs, const float* __restrict__ x, int lo, int h
     __syncthreads();
 }
 
+// Ordering key of a (validated, non-negative) score: its fp32 bit pattern, with -0.0 folded
+// onto +0.0. The reference compares values (sparsity.hpp:83-97), where -0.0 == 0.0 and both
+// rank below every positive score; the raw pattern 0x80000000 would rank above them all.
+__device__ __forceinline__ uint32_t score_bits(float v) {
+    const uint32_t b = __float_as_uint(v);
+    return b == 0x80000000u ? 0u : b;
+}
+
 // Local histogram of digit (bits >> shift) & 255 over this CTA's slice xs[0, len), restricted
 // to elements whose bits above (shift + 8) equal `prefix`, published to ex[parity]; then
 // the cluster-wide histogram (tc, tm) and the per-rank counts (loc) are gathered over DSMEM.
@@ -197,7 +205,7 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
         uint32_t key = kNoBucket;
         if (i < len) {
             v = xs[i];
-            const uint32_t bits = __float_as_uint(v);
+            const uint32_t bits = score_bits(v);
             if (validate) {
                 if (!(v >= 0.f)) bad = 1;
                 else if (v > 1.5f) big = 1;
@@ -416,7 +424,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, const_cast<float*>(x), parity);
     } else {
         if (kCached) load_slice<true>(cache, x, lo, hi);
-        if (threadIdx.x == 0) sh.x0 = __float_as_uint(__ldg(x));
+        if (threadIdx.x == 0) sh.x0 = score_bits(__ldg(x));
         __syncthreads();
     }
     const float* xs = kCached ? cache : x + lo;
@@ -494,7 +502,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t* s = p.scratch + static_cast<size_t>(dir * p.hkv + g) * 2 * p.npow2;
             const int np2 = p.npow2;
             // plain loads: on the logits path x was written by this cluster (no .nc cache)
-            for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? __float_as_uint(x[i]) : 0u;
+            for (int i = threadIdx.x; i < np2; i += kThreads) s[i] = i < n ? score_bits(x[i]) : 0u;
             __syncthreads();
             for (int size = 2; size <= np2; size <<= 1) {
                 for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -587,7 +595,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < kItems; ++t) {
             const int i = i0 + t;
-            bits[t] = i < hi ? __float_as_uint(xs[i - lo]) : 0u;
+            bits[t] = i < hi ? score_bits(xs[i - lo]) : 0u;
             n_eq += (i < hi && bits[t] == tbits) ? 1u : 0u;
         }
         uint32_t eq_tot;
@@ -693,12 +701,11 @@ cudaError_t launch_impl(const float* lv, const float* ls, const float* a_v, cons
         p.min_b[g] = budgets[g].min_budget;
         p.max_b[g] = budgets[g].max_budget;
     }
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         allow_smem(select_kernel<true>);
         allow_smem(select_kernel<false>);
-        attr = true;
-    }
+    });
     p.g0 = g0;
     const dim3 grid(count * kCluster, 2);
     vsp_detail::count_launch();
@@ -723,12 +730,11 @@ cudaError_t launch_from_logits(const float* lv, const float* ls, float* a_v, flo
 
 cudaError_t launch_softmax(const float* lv, const float* ls, float* a_v, float* a_s, int n, int g0, int count,
                            cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         allow_smem(softmax_kernel<true>);
         allow_smem(softmax_kernel<false>);
-        attr = true;
-    }
+    });
     const dim3 grid(count * kCluster, 2);
     vsp_detail::count_launch();
     if (cached_slice(n))

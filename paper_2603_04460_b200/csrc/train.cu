@@ -495,11 +495,10 @@ cudaError_t loss_grad(const GradArgs& a, void* workspace, cudaStream_t stream) {
     p.nsplit = nsplit;
     p.tiles = tiles;
     p.reverse = a.reverse ? 1 : 0;
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr[vsp_detail::kMaxDevices];
+    vsp_detail::once_per_device(attr, [] {
         cudaFuncSetAttribute(backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr = true;
-    }
+    });
     vsp_detail::count_launch();
     backward_kernel<<<a.hkv * (a.d_h / kHid) * nsplit, kThreads, kSmemBytes, stream>>>(p);
     // 4. fixed-order reduction into the flat gradient; per-head loss = KL_v + KL_s

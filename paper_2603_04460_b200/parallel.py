@@ -109,6 +109,22 @@ class VspComm:
                                                   ctypes.c_void_p(lse_full.data_ptr() if lse_full is not None else 0),
                                                   n, hq, d, st))
 
+    def assemble_units(self, o_full: torch.Tensor, lse_full: Optional[torch.Tensor], all_units, hkv: int) -> None:
+        """In-place assembly of a unit split: all_units[r] = rank r's units (g, qb_lo, qb_hi);
+        every region goes from its owner to every rank (vsp_assemble_units: one ncclBroadcast
+        per (unit, Q head) in one NCCL group)."""
+        hq, n, d = o_full.shape
+        flat = [(r, g, lo, hi) for r, us in enumerate(all_units) for g, lo, hi in us]
+        arr = (ctypes.c_int32 * (4 * max(len(flat), 1)))(*[x for u in flat for x in u])
+        lib = self._lib
+        lib.vsp_assemble_units.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.c_void_p]
+        st = ctypes.c_void_p(torch.cuda.current_stream(o_full.device).cuda_stream)
+        self._check(lib.vsp_assemble_units(self._h, ctypes.c_void_p(o_full.data_ptr()),
+                                           ctypes.c_void_p(lse_full.data_ptr() if lse_full is not None else 0),
+                                           n, hq, hkv, d, ctypes.cast(arr, ctypes.c_void_p), len(flat), st))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._check(self._lib.vsp_comm_destroy(self._h))
@@ -119,6 +135,27 @@ class VspComm:
             self.close()
         except Exception:
             pass
+
+
+def unit_regions(all_units, n: int, hq: int, hkv: int) -> List[Tuple[int, int, int, int]]:
+    """(owner rank, Q head, row_lo, row_hi) of every head-major output region a unit split
+    writes: all_units[r] = rank r's units (g, qb_lo, qb_hi) over 128-row query blocks."""
+    grp = hq // hkv
+    return [(r, h, lo * 128, min(hi * 128, n)) for r, us in enumerate(all_units) for g, lo, hi in us
+            for h in range(g * grp, (g + 1) * grp)]
+
+
+def assemble_units(o_full: torch.Tensor, lse_full: Optional[torch.Tensor], all_units, hkv: int,
+                   group=None) -> None:
+    """torch.distributed form of VspComm.assemble_units (any backend; gloo on CPU in the
+    tests): one broadcast per region from its owner, in place on every rank."""
+    hq, n, _ = o_full.shape
+    for r, h, lo, hi in unit_regions(all_units, n, hq, hkv):
+        src = dist.get_global_rank(group, r) if group is not None else r
+        reg = o_full[h, lo:hi]
+        dist.broadcast(reg, src=src, group=group)  # contiguous: head-major rows of one head
+        if lse_full is not None:
+            dist.broadcast(lse_full[h, lo:hi], src=src, group=group)
 
 
 def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: float = 2500.0

@@ -92,11 +92,18 @@ def head_structure(hkv: int, d: int, n: int, head_seed: int, cfg: PlantConfig):
 
 
 def planted_layer(n: int, hq: int, hkv: int, d: int = 128, seed: int = 0, cfg: Optional[PlantConfig] = None,
-                  device="cuda", head_seed: Optional[int] = None,
+                  device="cuda", head_seed: Optional[int] = None, gen_device=None,
                   ) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, List[dict]]:
-    """-> Q [n, hq, d], K [n, hkv, d], V [n, hkv, d] bf16 and the planted structure per group.
-    `seed` is the prompt seed; `head_seed` (default: 1000003) fixes the heads' structure."""
+    """-> Q [n, hq, d], K [n, hkv, d], V [n, hkv, d] bf16 on `device` and the planted structure
+    per group. `seed` is the prompt seed; `head_seed` (default: 1000003) fixes the heads'
+    structure. `gen_device` (default: `device`) is where the values are drawn and computed:
+    "cpu" gives the same bits on every machine and process (torch's CPU generator and
+    unfused elementwise ops), so a CPU-only process (bench.py's reference arm) and a GPU
+    process see the identical layer."""
     cfg = cfg or PlantConfig()
+    if gen_device is not None and torch.device(gen_device) != torch.device(device):
+        q, k, v, plants = planted_layer(n, hq, hkv, d, seed, cfg, gen_device, head_seed)
+        return q.to(device), k.to(device), v.to(device), plants
     dev = torch.device(device)
     hs = 1000003 if head_seed is None else head_seed
     mu_q, mu_k, stripes = head_structure(hkv, d, n, hs, cfg)

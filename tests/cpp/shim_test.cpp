@@ -1,6 +1,7 @@
 // Reference test bodies re-pointed from vsp:: to vsp::gpu:: through include/vsprefill_gpu.hpp.
 // Built where the reference headers exist (tests/cpp/Makefile); the binary travels to the GPU
 // box and runs under tests/test_gpu_cpp_shim.py. Prints one PASS/FAIL line per case.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -315,6 +316,119 @@ int main() {
         }
         det = ok ? "bytes and texts identical" : "mismatch";
         return ok;
+    });
+    // TopK.HandValuesWithTies / DeterministicUnderPermutedTies / MatchesFullSortOracle /
+    // RejectsBadK (test_sparsity.cpp:93-131)
+    check("topk_indices_reference_bodies", [](std::string& det) {
+        using V = std::vector<std::size_t>;
+        const std::vector<double> s = {0.2, 0.5, 0.2, 0.1};
+        bool ok = vsp::gpu::topk_indices(s, 1) == V{1} && vsp::gpu::topk_indices(s, 2) == V{0, 1} &&
+                  vsp::gpu::topk_indices(s, 3) == V{0, 1, 2} && vsp::gpu::topk_indices(s, 4) == V{0, 1, 2, 3};
+        const std::vector<double> twin = {0.3, 0.2, 0.2, 0.3};
+        ok = ok && vsp::gpu::topk_indices(twin, 2) == V{0, 3} && vsp::gpu::topk_indices(twin, 3) == V{0, 1, 3};
+        ok = ok && vsp::gpu::topk_indices({0.4, 0.1, 0.1, 0.4}, 2) == V{0, 3} &&
+             vsp::gpu::topk_indices({0.1, 0.4, 0.4, 0.1}, 2) == V{1, 2};
+        Rng rng(93);
+        int bad = 0;
+        for (int trial = 0; trial < 200; ++trial) {
+            const std::size_t n = 1 + static_cast<std::size_t>(rng.next_below(50));
+            std::vector<double> sc(n);
+            for (double& x : sc) x = static_cast<double>(rng.next_below(8)) / 8.0;
+            const std::size_t k = 1 + static_cast<std::size_t>(rng.next_below(n));
+            bad += vsp::gpu::topk_indices(sc, k) != oracle::topk(sc, k);
+        }
+        int thrown = 0;
+        for (std::size_t k : {std::size_t{0}, std::size_t{3}}) {
+            try {
+                vsp::gpu::topk_indices({0.5, 0.5}, k);
+            } catch (const std::invalid_argument&) {
+                ++thrown;
+            }
+        }
+        det = "oracle mismatches=" + std::to_string(bad) + " bad-k throws=" + std::to_string(thrown);
+        return ok && bad == 0 && thrown == 2;
+    });
+    // MergeRowColumns.HandCases / RejectsUnsortedInput / MatchesSetUnionOracle
+    // (test_attention.cpp:274-302)
+    check("merge_row_columns_reference_bodies", [](std::string& det) {
+        using V = std::vector<std::size_t>;
+        bool ok = vsp::gpu::merge_row_columns({0, 5}, {0, 2}, 4) == V{0, 2, 4} &&
+                  vsp::gpu::merge_row_columns({}, {0}, 7) == V{7} && vsp::gpu::merge_row_columns({1, 9}, {}, 3) == V{1} &&
+                  vsp::gpu::merge_row_columns({2}, {3}, 5) == V{2} && vsp::gpu::merge_row_columns({}, {}, 4).empty();
+        int thrown = 0;
+        try {
+            vsp::gpu::merge_row_columns({3, 1}, {}, 5);
+        } catch (const std::invalid_argument& e) {
+            thrown += std::string(e.what()) == "merge_row_columns: i_v not strictly ascending";
+        }
+        try {
+            vsp::gpu::merge_row_columns({}, {2, 2}, 5);
+        } catch (const std::invalid_argument& e) {
+            thrown += std::string(e.what()) == "merge_row_columns: i_s not strictly ascending";
+        }
+        Rng rng(44);
+        auto subset = [&](std::size_t n, std::size_t k) {
+            std::vector<std::size_t> pool(n);
+            for (std::size_t i = 0; i < n; ++i) pool[i] = i;
+            for (std::size_t i = 0; i < k; ++i) std::swap(pool[i], pool[i + rng.next_below(n - i)]);
+            pool.resize(k);
+            std::sort(pool.begin(), pool.end());
+            return pool;
+        };
+        int bad = 0;
+        for (int trial = 0; trial < 300; ++trial) {
+            const std::size_t n = 1 + static_cast<std::size_t>(rng.next_below(40));
+            const V i_v = subset(n, 1 + static_cast<std::size_t>(rng.next_below(n)));
+            const V i_s = subset(n, 1 + static_cast<std::size_t>(rng.next_below(n)));
+            const std::size_t i = static_cast<std::size_t>(rng.next_below(n));
+            bad += vsp::gpu::merge_row_columns(i_v, i_s, i) != oracle::merge_union(i_v, i_s, i);
+        }
+        det = "union mismatches=" + std::to_string(bad) + " messages=" + std::to_string(thrown);
+        return ok && bad == 0 && thrown == 2;
+    });
+    // MergePath.HandCase / BalancedSliceSizes-style property (test_attention.cpp:328-350)
+    check("merge_path_partition_reference_bodies", [](std::string& det) {
+        const std::vector<std::size_t> a = {1, 3, 5}, b = {2, 4, 6};
+        const auto cuts = vsp::gpu::merge_path_partition(a, b, 2);
+        bool ok = cuts.size() == 3 && cuts[0] == (MergeCut{0, 0}) && cuts[1] == (MergeCut{2, 1}) &&
+                  cuts[2] == (MergeCut{3, 3});
+        Rng rng(45);
+        int bad = 0;
+        for (int trial = 0; trial < 100; ++trial) {
+            std::vector<std::size_t> x(rng.next_below(40)), y(rng.next_below(40));
+            for (auto& t : x) t = rng.next_below(60);
+            for (auto& t : y) t = rng.next_below(60);
+            std::sort(x.begin(), x.end());
+            std::sort(y.begin(), y.end());
+            const std::size_t p = 1 + rng.next_below(7);
+            bad += vsp::gpu::merge_path_partition(x, y, p) != vsp::merge_path_partition(x, y, p);
+        }
+        det = "cut mismatches=" + std::to_string(bad);
+        return ok && bad == 0;
+    });
+    // CombineScores.MeanAndSum / RejectsEmptyOrMismatched (test_vsaggregate.cpp:144-162), at
+    // fp32: |d| <= 1e-7 instead of 1e-15
+    check("combine_scores_reference_bodies", [](std::string& det) {
+        VSScores a{{0.6, 0.4}, {1.0, 0.0}, true};
+        VSScores b{{0.2, 0.8}, {0.4, 0.6}, true};
+        const VSScores mean = vsp::gpu::combine_scores({a, b});
+        const VSScores sum = vsp::gpu::combine_scores({a, b}, GroupReduce::Sum);
+        bool ok = mean.normalized && std::fabs(mean.vertical[0] - 0.4) <= 1e-7 && std::fabs(mean.slash[1] - 0.3) <= 1e-7 &&
+                  !sum.normalized && std::fabs(sum.vertical[0] - 0.8) <= 1e-7 && std::fabs(sum.slash[0] - 1.4) <= 1e-7;
+        int thrown = 0;
+        try {
+            vsp::gpu::combine_scores({});
+        } catch (const std::invalid_argument&) {
+            ++thrown;
+        }
+        try {
+            VSScores c{{1.0}, {1.0}, true};
+            vsp::gpu::combine_scores({a, c});
+        } catch (const std::invalid_argument&) {
+            ++thrown;
+        }
+        det = "throws=" + std::to_string(thrown);
+        return ok && thrown == 2;
     });
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;

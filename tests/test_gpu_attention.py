@@ -140,6 +140,20 @@ def test_unsorted_raises(vsp):
         vsp.sparse_attention(q, k, v, pattern_tensors([([1], [0, 4, 4])], n))
 
 
+def test_count_above_cap_is_einval_not_a_fault(vsp):
+    """k_v / k_s larger than the list capacity: validation reports EINVAL (its scans stay
+    inside the row) and the context stays usable."""
+    n = 16
+    q, k, v = qkv(n, 2, 1, seed=1)
+    pat = pattern_tensors([([0, 3], [0, 1])], n)
+    pat.k_v.fill_(n + 50)
+    with pytest.raises(vsp.VspError, match="index count exceeds cap"):
+        vsp.sparse_attention(q, k, v, pat)
+    o, lse = vsp.sparse_attention(q, k, v, pattern_tensors([([0, 3], [0, 1])], n))
+    torch.cuda.synchronize()
+    assert torch.isfinite(lse).all()
+
+
 def test_recall_from_lse_matches_reference_recall(vsp):
     import oracle
     if not oracle.have_ref():

@@ -224,6 +224,27 @@ def test_select_exact_fallback_boundary(vsp):
         assert len(iv) == want, tau
 
 
+def test_select_negative_zero_ranks_as_zero(vsp):
+    """-0.0 passes validation (v >= 0) and compares equal to 0.0 in the reference
+    (sparsity.hpp:60-97): it must rank below every positive score, ties to the lower index."""
+    rng = np.random.default_rng(11)
+    for n in (9, 4000, 70000):
+        a = rng.random((2, n)).astype(np.float64)
+        a[:, rng.choice(n, n // 3, replace=False)] = 0.0
+        a /= a.sum(axis=1, keepdims=True)
+        a = a.astype(np.float32)
+        zeros = np.flatnonzero(a[0] == 0.0)
+        a[0, zeros[::2]] = -0.0
+        a[1, np.flatnonzero(a[1] == 0.0)] = -0.0
+        assert np.signbit(a).any()
+        a_v = torch.tensor(a[:1]).cuda()
+        a_s = torch.tensor(a[1:]).cuda()
+        for tau in (0.3, 0.99):
+            _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(tau, tau, 1, None)])
+        # budgets reaching into the zero block: ties among +-0 go to the lower index
+        _check_against_oracle(vsp, a_v, a_s, [vsp.BudgetConfig(0.5, 0.5, n - n // 6, None)])
+
+
 def test_select_validation_messages(vsp):
     a = torch.tensor([[0.5, 0.6, -0.1]], device="cuda")
     ok = torch.tensor([[0.5, 0.25, 0.25]], device="cuda")

@@ -226,3 +226,72 @@ def test_spread_units_cover_every_head_evenly():
         per_rank = [parallel.units_cost(us, cost) for us in units]
         worst_block = float(cost.max()) + 2.0
         assert max(per_rank) <= (float(cost.sum()) + 2.0 * cost.size) / world + hkv * worst_block
+
+
+def _units_worker(rank, world, port, n, hq, hkv, d, split, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_04460_b200 import parallel
+    g = torch.Generator().manual_seed(3)
+    nqb = (n + 127) // 128
+    cost = torch.randint(1, 50, (hkv, nqb), generator=g)
+    all_units = (parallel.spread_units(cost, world) if split == "spread"
+                 else parallel.balanced_units(cost, world, head_overhead=5.0))
+    want_o = torch.randn(hq, n, d, generator=g)  # the assembled layer output, same everywhere
+    want_l = torch.randn(hq, n, generator=g)
+    # this rank writes only its units' (head, row) regions, as vs_prefill_units does
+    o = torch.full((hq, n, d), float("nan"))
+    lse = torch.full((hq, n), float("nan"))
+    for own, h, lo, hi in parallel.unit_regions(all_units, n, hq, hkv):
+        if own == rank:
+            o[h, lo:hi] = want_o[h, lo:hi]
+            lse[h, lo:hi] = want_l[h, lo:hi]
+    parallel.assemble_units(o, lse, all_units, hkv)
+    covered = torch.zeros(hq, n, dtype=torch.int32)
+    for _, h, lo, hi in parallel.unit_regions(all_units, n, hq, hkv):
+        covered[h, lo:hi] += 1
+    q.put((rank, bool(torch.equal(o, want_o) and torch.equal(lse, want_l)), bool((covered == 1).all())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", ["balanced", "spread"])
+def test_unit_split_assembly_gloo(split):
+    """A unit split's output regions, written by their owners only, assemble bit-exactly on
+    every rank (the torch.distributed form of vsp_assemble_units' broadcast schedule), and
+    the regions tile the head-major output exactly once."""
+    world, n, hq, hkv, d = 2, 1000, 8, 2, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_units_worker, args=(r, world, port, n, hq, hkv, d, split, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok and once for _, ok, once in res), res
+
+
+def test_merge_path_partition_c_abi_matches_reference():
+    """vsp_merge_path_partition (host part of the C ABI, merge.hpp:69-95): MergePath.HandCase
+    (test_attention.cpp:328-337) and randomised cuts vs the pinned restatement, plus the
+    per-slice merge property (concatenated slice merges reproduce the full merge)."""
+    import oracle
+    import paper_2603_04460_b200 as vsp
+    assert vsp.merge_path_partition([1, 3, 5], [2, 4, 6], 2) == [(0, 0), (2, 1), (3, 3)]
+    with pytest.raises(vsp.VspError, match="^merge_path_partition: p must be >= 1$"):
+        vsp.merge_path_partition([1], [2], 0)
+    rng = np.random.default_rng(45)
+    port = oracle.port()
+    for _ in range(200):
+        a = np.sort(rng.integers(0, 60, int(rng.integers(0, 40))))
+        b = np.sort(rng.integers(0, 60, int(rng.integers(0, 40))))
+        p = 1 + int(rng.integers(8))
+        cuts = vsp.merge_path_partition(a, b, p)
+        assert cuts == port.merge_path_partition(a, b, p)
+        merged = []
+        for s in range(p):
+            sa, sb = a[cuts[s][0]:cuts[s + 1][0]], b[cuts[s][1]:cuts[s + 1][1]]
+            merged += sorted(list(sa) + list(sb), key=lambda x: x)  # equal keys: values identical
+        assert merged == sorted(list(a) + list(b))
