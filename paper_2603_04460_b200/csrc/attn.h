@@ -14,6 +14,7 @@ struct __align__(64) AttnParams {
     CUtensorMap map_v;
     CUtensorMap map_kv;  // gathered verticals [hkv, kvcap, 128], box {64, 128, 1}
     CUtensorMap map_vv;
+    CUtensorMap map_o;   // O for the epilogue's TMA stores: dims (128, hq, n) with the layout's strides
     __nv_bfloat16* o;    // row i of head h at o + i * o_tok_stride + h * o_head_stride
     float* lse;          // [hq, n] or null
     long long o_tok_stride, o_head_stride;  // elements: [n, hq, 128] -> (hq*128, 128); head-major -> (128, n*128)
@@ -28,6 +29,7 @@ struct __align__(64) AttnParams {
     int nunits;
     int* work;           // {next item - gridDim.x, CTAs done}: zero at launch, reset by the last CTA
     int bm_words;
+    int prefetch_q;      // L2-prefetch the next work item's Q tiles (VSP_NO_Q_PREFETCH=1 disables)
     int n, hq, hkv;
     float scale;
 };

@@ -25,17 +25,21 @@
 // Online softmax runs in the exp2 domain with lazy rescaling (only when the running max
 // grows by more than 2^8), exactly the same math as the reference's per-row rescale.
 //
-// Sparse mode: per (KV head, query block) a tile list built by vs_plan_kernel. Entry
-// e >= 0 is a "slash span" tile: K/V rows [e, e+128) of the original tensors, element
-// mask (i-j) in I_s  AND  j not in I_v  AND  j <= i  (from n-bit bitmaps). Entry e < 0
-// is gathered vertical tile t = -e-1: rows [128t, 128t+128) of K[I_v], V[I_v] (gathered
-// once per head), mask r < #{I_v <= i}. Every covered (i, j) pair is visited exactly once,
-// which is the reference's duplicate-free per-row union.
+// Sparse mode: per (KV head, query block) a tile list built by vs_plan_kernel. An entry is
+// (value, gathered flag, width): a "slash span" tile covers K/V rows [value, value+width) of
+// the original tensors with element mask (i-j) in I_s AND j not in I_v AND j <= i (from n-bit
+// bitmaps); a gathered vertical tile t = value covers rows [128t, 128t+width) of K[I_v], V[I_v]
+// (gathered once per head), mask r < #{I_v <= i}. Every covered (i, j) pair is visited exactly
+// once, which is the reference's duplicate-free per-row union. The last tile of a vertical run
+// or of a merged slash range is narrow (width = its used columns rounded up to 16): the S MMA
+// runs with N = width and PV with width/16 K-steps, so a 9-column remainder costs ~0.3 of a
+// full tile on the tensor core instead of 1.
 #include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
+#include <type_traits>
 #include <vector>
 
 #include "vsp_launch.h"
@@ -52,8 +56,13 @@ constexpr int kNumK = 2;        // K smem stages
 constexpr int kNumV = 2;        // V smem stages
 constexpr int kTileBytes = kBlock * kHeadDim * 2;   // 32 KB (two 16 KB d-halves)
 constexpr int kHalfBytes = kTileBytes / 2;
-constexpr int kSmemBytes = (2 + kNumK + kNumV) * kTileBytes + 1024;
+constexpr int kOStage = kHalfBytes;  // per Q tile: O staging for the TMA store, one 64-column half
+constexpr int kSmemBytes = (2 + kNumK + kNumV) * kTileBytes + 2 * kOStage + 1024;
 constexpr int kThreads = 384;
+// per-thread registers after setmaxnreg: launch cap 168 (65536 / 384); the producer/MMA
+// warpgroup gives back (168 - 64) x 128, the softmax warps take (216 - 168) x 256 of it
+constexpr uint32_t kRegsOther = 64;
+constexpr uint32_t kRegsSoftmax = 216;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -71,6 +80,17 @@ struct Smem {
     int item[kItemRing];                      // work item index, -1 = no more work
     uint32_t tmem_base;
 };
+
+// Tile-list entry: bits [0, 27) value, bit 27 gathered, bits [28, 31) width / 16 - 1.
+constexpr int kEntValueBits = 27;
+constexpr int kEntGathered = 1 << kEntValueBits;
+__host__ __device__ constexpr int ent_make(int value, bool gathered, int width) {
+    return value | (gathered ? kEntGathered : 0) | (((width >> 4) - 1) << 28);
+}
+VSP_DEVICE int ent_value(int e) { return e & (kEntGathered - 1); }
+VSP_DEVICE bool ent_gathered(int e) { return (e & kEntGathered) != 0; }
+VSP_DEVICE int ent_width(int e) { return ((e >> 28) + 1) << 4; }
+VSP_DEVICE int round16(int x) { return (x + 15) & ~15; }
 
 // Work item it (heaviest query blocks first: causal work grows with the block index).
 struct Item {
@@ -93,6 +113,127 @@ VSP_DEVICE void window128(const uint32_t* __restrict__ bm, int start, int nwords
     for (int k = 0; k < 4; ++k) w[k] = __funnelshift_r(raw[k], raw[k + 1], sh);
 }
 
+#ifdef VSP_K3_TRACE
+// Timeline probe (tools/k3_trace.py builds a separate library with -DVSP_K3_TRACE): clock64
+// stamps of CTA 0's pipeline events per (event, head w, global tile G).
+constexpr int kTraceTiles = 8192;
+__device__ unsigned long long g_k3_trace[12 * 2 * kTraceTiles];
+#define VSP_TRACE(ev, w, G)                                                                              \
+    do {                                                                                                 \
+        if (blockIdx.x == 0 && (G) < kTraceTiles && lane_id() == 0)                                      \
+            g_k3_trace[((ev) * 2 + (w)) * kTraceTiles + (G)] = clock64();                                \
+    } while (0)
+#else
+#define VSP_TRACE(ev, w, G) \
+    do {                    \
+    } while (0)
+#endif
+
+// One tile of the online softmax for one warp (thread = query row): read S from TMEM, mask,
+// row max, lazy rescale of O, exponentials -> bf16 P written back over S, p_half after the
+// first 64 columns. kM = the warp has masked columns (per-chunk modes dead/part, see caller).
+template <bool kM>
+VSP_DEVICE void softmax_tile(uint32_t s_t, uint32_t o_t, uint32_t dead, uint32_t part, uint4 mk4,
+                             int width, int j, float sl2, float& m_used, float& l, uint64_t* p_half_bar,
+                             int quarter, int w, int gtj) {
+    const uint32_t lane = lane_id();
+    const uint32_t mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+    (void)quarter;
+    (void)w;
+    (void)gtj;
+    // the S row is read from TMEM once and stays in registers (the softmax warps run with
+    // more registers, see setmaxnreg above)
+    uint32_t u[4][32];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld32(s_t + c * 32, u[c]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_reg_fence(u[c]);
+    float mx;
+    {
+        // eight independent max chains (a single chain is 64 dependent 3-input maxes)
+        float mxa[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mxa[t] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (kM && ((dead >> c) & 1u)) continue;
+            if (kM && ((part >> c) & 1u)) {
+#pragma unroll
+                for (int t = 0; t < 32; ++t)
+                    if (!((mk[c] >> t) & 1u)) u[c][t] = 0xff800000u;  // -inf
+            }
+#pragma unroll
+            for (int t = 0; t < 32; t += 2)
+                mxa[(t >> 1) & 7] = fmaxf(mxa[(t >> 1) & 7], fmaxf(__uint_as_float(u[c][t]), __uint_as_float(u[c][t + 1])));
+        }
+        mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                   fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+    }
+    const float m_new = fmaxf(m_used, mx * sl2);
+    const bool need = (m_used == -INFINITY) ? (m_new > -INFINITY) : (m_new > m_used + kRescaleThreshold);
+    if (__any_sync(0xffffffffu, need)) {
+        const float m_next = need ? m_new : m_used;
+        const float f = (m_used == -INFINITY) ? 0.f : ex2_approx(m_used - m_next);
+        l *= f;
+        m_used = m_next;
+        if (j > 0) {  // O holds PV(0..j-1); PV(j-1) is complete (see header)
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v[32];
+                tmem_ld32(o_t + c * 32, v);
+                tmem_wait_ld(v);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) v[t] = __float_as_uint(__uint_as_float(v[t]) * f);
+                tmem_st32(o_t + c * 32, v);
+            }
+        }
+    }
+    if (quarter == 0) VSP_TRACE(3, w, gtj);
+    const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
+    const float2 scl = make_float2(sl2, sl2);
+    const float2 neg_m = make_float2(-m_eff, -m_eff);
+    float2 lsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                      make_float2(0.f, 0.f)};
+    // p = 2^(s * scale * log2e - m), packed to bf16 pairs and written over the consumed
+    // S columns (chunk c's P lands in [16c, 16c+16))
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        if (!kM || c * 32 < width) {  // chunks past a narrow tile are never read by PV
+            uint32_t pk[16];
+            if (kM && ((dead >> c) & 1u)) {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) pk[t] = 0u;
+            } else {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const float2 y = ffma2(make_float2(__uint_as_float(u[c][2 * t]),
+                                                       __uint_as_float(u[c][2 * t + 1])),
+                                           scl, neg_m);
+                    float2 e;
+                    if ((0x5454u >> t) & 1u) {  // 3 pairs in 8 on the FMA pipe (MUFU/FMA balance)
+                        e = exp2_poly2(y);
+                    } else {
+                        e.x = ex2_approx(y.x);
+                        e.y = ex2_approx(y.y);
+                    }
+                    lsum[t & 3] = fadd2(lsum[t & 3], e);
+                    pk[t] = pack_bf16x2(e.x, e.y);
+                }
+            }
+            tmem_st16(s_t + c * 16, pk);
+        }
+        if (c == 1) {  // P columns [0, 64) are in TMEM: the first PV half may start
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_half_bar);
+            if (quarter == 0) VSP_TRACE(4, w, gtj);
+        }
+    }
+    l += ((lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y)) + ((lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y));
+}
+
 // kMc = 2: a two-CTA cluster runs the two Q-head pairs of a 4-head group on the same query
 // block in lockstep (identical tile lists); each CTA TMA-loads one half of every K/V tile and
 // multicasts it to both, halving the L2 -> SMEM traffic. Ring slots are released by both
@@ -107,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     uint8_t* sQ = base;                                  // 2 tiles
     uint8_t* sK = base + 2 * kTileBytes;                 // kNumK tiles
     uint8_t* sV = sK + kNumK * kTileBytes;               // kNumV tiles
+    uint8_t* sO = sV + kNumV * kTileBytes;               // 2 x kOStage: O staging per Q tile
     __shared__ Smem sm;
 
     const int num_qb = (p.n + kBlock - 1) / kBlock;
@@ -154,7 +296,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     // consumer side of the item ring (MMA warp and softmax warps): item of round n_it, or -1
     auto next_item = [&](int n_it) {
         const int slot = n_it % kItemRing;
+#ifdef VSP_K3_TRACE
+        if (warp == 1) VSP_TRACE(11, 0, n_it);
+#endif
         mbar_wait(&sm.item_full[slot], (n_it / kItemRing) & 1);
+#ifdef VSP_K3_TRACE
+        if (warp == 1) VSP_TRACE(11, 1, n_it);
+#endif
         const int it = *reinterpret_cast<volatile int*>(&sm.item[slot]);
         __syncwarp();
         if (lane == 0) {
@@ -195,7 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if constexpr (kMc > 1) cluster_sync();  // peers' barriers exist before any remote arrive / multicast
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-
+    // register split (per warpgroup, at the top of each role's branch so the allocator sees
+    // it): the producer / MMA warpgroup needs few, the softmax warps hold a whole S row (128
+    // fp32) in registers. setmaxnreg.inc waits for registers released by .dec inside the CTA:
+    // (168 - kRegsOther) x 128 >= (kRegsSoftmax - 168) x 256
+    if (warp < 4) {
+    setmaxnreg_dec<kRegsOther>();
     if (warp == 0) {
         // =========================== TMA producer (warp-uniform loop, elected issuer)
         if (elect_one()) {
@@ -209,7 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         __syncwarp();
         int gj = 0;  // K/V ring position, continuous across items
-        for (int n_it = 0;; ++n_it) {
+        // Producer side of the item ring, one round ahead of the item being loaded: the next
+        // item's Q tiles are prefetched into L2 while this item streams its K/V tiles, so the
+        // Q load at the item boundary (single-buffered, it waits for the last S MMA) hits L2.
+        auto fetch = [&](int n_it) {
             const int slot = n_it % kItemRing;
             int it = 0;
             if (crank == 0) {
@@ -229,10 +385,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             } else {
                 it = next_item(n_it);  // the peer's producer consumes the leader's fetch
             }
+            return it;
+        };
+        int it_next = fetch(0);
+        for (int n_it = 0;; ++n_it) {
+            const int it = it_next;
             if (it < 0) break;
+            it_next = fetch(n_it + 1);
+            VSP_TRACE(9, 0, gj);
+            if (it_next >= 0 && p.prefetch_q) {
+                const Item xn = item(it_next);
+                if (elect_one())
+                    for (int w = 0; w < 2; ++w)
+                        for (int hf = 0; hf < 2; ++hf) tma_prefetch_3d(&p.map_q, hf * 64, w ? xn.h1 : xn.h0, xn.qb * kBlock);
+                __syncwarp();
+            }
             const Item x = item(it);
             // the previous item's last S MMA has read its Q tiles
             if (n_it > 0) mbar_wait(&sm.q_free, (n_it - 1) & 1);
+            VSP_TRACE(7, 0, gj);
             if (elect_one()) {
                 mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
                 for (int w = 0; w < 2; ++w)
@@ -241,15 +412,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                                     w ? x.h1 : x.h0, x.qb * kBlock);
             }
             __syncwarp();
+            VSP_TRACE(9, 1, gj);
             for (int j = 0; j < x.num_tiles; ++j, ++gj) {
-                int e = kSparse ? __ldg(x.tiles + j) : j * kBlock;
-                const bool gathered = kSparse && e < 0;
-                const int row = gathered ? (-e - 1) * kBlock : e;
+                const int e = kSparse ? __ldg(x.tiles + j) : 0;
+                const bool gathered = kSparse && ent_gathered(e);
+                const int row = kSparse ? (gathered ? ent_value(e) * kBlock : ent_value(e)) : j * kBlock;
                 const CUtensorMap* mk_ = gathered ? &p.map_kv : &p.map_k;
                 const CUtensorMap* mv_ = gathered ? &p.map_vv : &p.map_v;
                 const int c1 = gathered ? row : x.g, c2 = gathered ? x.g : row;
                 const int ks = gj % kNumK;
                 if (gj >= kNumK) mbar_wait(&sm.k_empty[ks], ((gj / kNumK) & 1) ^ 1);
+                VSP_TRACE(10, 0, gj);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&sm.k_full[ks], kTileBytes);
                     if constexpr (kMc > 1)  // this CTA's half, multicast; the peer sends the other
@@ -293,32 +466,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // first: the item's first PV overwrites O (accumulate = 0)
         // half h of PV: K-steps [4h, 4h + 4), i.e. P columns [64h, 64h + 64) (TMEM [32h, 32h + 32))
         // against V rows [64h, 64h + 64); the softmax publishes the two halves separately
-        auto issue_pv = [&](int w, int gjj, bool first, int h) {
+        // nk: K-steps of the tile (width / 16; 8 for a full tile)
+        auto issue_pv = [&](int w, int gjj, bool first, int h, int nk) {
             const uint64_t vd = v_desc0 + static_cast<uint64_t>(((gjj % kNumV) * kTileBytes) >> 4);
             const uint32_t o_t = tmem + 256 + w * 128;
             const uint32_t p_t = tmem + w * 128;
 #pragma unroll
             for (int k = 4 * h; k < 4 * h + 4; ++k)
-                umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
-                        (!first || k > 0) ? 1u : 0u);
+                if (k < nk)
+                    umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
+                            (!first || k > 0) ? 1u : 0u);
         };
-        auto issue_s = [&](int w, int gjj) {
+        // S_w = Q_w K^T over the tile's first `width` keys (N = width)
+        auto issue_s = [&](int w, int gjj, int width) {
+            const uint32_t idesc = (idesc_qk & ~(0x3Fu << 17)) | (static_cast<uint32_t>(width >> 3) << 17);
             const uint64_t qd = q_desc0 + static_cast<uint64_t>((w * kTileBytes) >> 4);
             const uint64_t kd = k_desc0 + static_cast<uint64_t>(((gjj % kNumK) * kTileBytes) >> 4);
             const uint32_t s_t = tmem + w * 128;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint64_t off = static_cast<uint64_t>(((k >> 2) * kHalfBytes + (k & 3) * 32) >> 4);
-                umma_ss(s_t, qd + off, kd + off, idesc_qk, k > 0 ? 1u : 0u);
+                umma_ss(s_t, qd + off, kd + off, idesc, k > 0 ? 1u : 0u);
             }
         };
         int gj = 0;
         for (int n_it = 0;; ++n_it) {
+            VSP_TRACE(8, 0, gj);
             const int it = next_item(n_it);
+            VSP_TRACE(8, 1, gj);
             if (it < 0) break;
             const Item x = item(it);
             const int nt = x.num_tiles;
             mbar_wait(&sm.q_full, n_it & 1);
+            VSP_TRACE(7, 1, gj);
             tc_fence_after();
             if (nt == 0) {  // nothing covered: release the epilogue (O is not touched)
                 // keep o_free's phases in lock-step with the items (no parity aliasing)
@@ -334,30 +514,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 __syncwarp();
                 continue;
             }
+            int nk_prev = 8;  // K-steps of tile j-1
             for (int j = 0; j < nt; ++j) {
                 const int G = gj + j;
                 const int ks = G % kNumK;
+                const int width = kSparse ? ent_width(__ldg(x.tiles + j)) : kBlock;
                 mbar_wait(&sm.k_full[ks], (G / kNumK) & 1);
+                VSP_TRACE(1, 0, G);
                 tc_fence_after();
                 for (int w = 0; w < 2; ++w) {
                     if (j > 0) {
                         // first half of P(j-1): its PV overlaps the softmax's second half
                         mbar_wait(&sm.p_half[w], (G - 1) & 1);
+                        VSP_TRACE(6, w, G - 1);
                         if (w == 0) mbar_wait(&sm.v_full[(G - 1) % kNumV], ((G - 1) / kNumV) & 1);
                         // the item's first PV writes O_w: the previous item's epilogue must be done
                         if (j == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
                         tc_fence_after();
-                        if (elect_one()) issue_pv(w, G - 1, j == 1, 0);
+                        if (elect_one()) issue_pv(w, G - 1, j == 1, 0, nk_prev);
                         __syncwarp();
                         mbar_wait(&sm.p_full[w], (G - 1) & 1);
                         tc_fence_after();
                     }
+                    VSP_TRACE(0, w, G);
                     if (elect_one()) {
                         if (j > 0) {
-                            issue_pv(w, G - 1, false, 1);
+                            issue_pv(w, G - 1, false, 1, nk_prev);
                             if (w == 1) release(&sm.v_empty[(G - 1) % kNumV]);
                         }
-                        issue_s(w, G);
+                        issue_s(w, G, width);
                         umma_commit(&sm.s_full[w]);
                         if (w == 1) {
                             release(&sm.k_empty[ks]);
@@ -366,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     }
                     __syncwarp();
                 }
+                nk_prev = width >> 4;
             }
             const int GL = gj + nt - 1;
             for (int w = 0; w < 2; ++w) {
@@ -373,12 +559,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 if (w == 0) mbar_wait(&sm.v_full[GL % kNumV], (GL / kNumV) & 1);
                 if (nt == 1 && n_it > 0) mbar_wait(&sm.o_free[w], (n_it - 1) & 1);
                 tc_fence_after();
-                if (elect_one()) issue_pv(w, GL, nt == 1, 0);
+                if (elect_one()) issue_pv(w, GL, nt == 1, 0, nk_prev);
                 __syncwarp();
                 mbar_wait(&sm.p_full[w], GL & 1);
                 tc_fence_after();
                 if (elect_one()) {
-                    issue_pv(w, GL, false, 1);
+                    issue_pv(w, GL, false, 1, nk_prev);
                     umma_commit(&sm.o_done[w]);
                     if (w == 1) release(&sm.v_empty[GL % kNumV]);
                 }
@@ -386,7 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             }
             gj += nt;
         }
-    } else if (warp >= 4) {
+    }
+    } else {
+        setmaxnreg_inc<kRegsSoftmax>();
         // =========================== softmax + epilogue
         const int w = (warp - 4) >> 2;             // Q tile / head within the pair
         const int quarter = warp & 3;              // TMEM lane quarter
@@ -428,17 +616,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             // ---- mask for this tile: bit c of mk[c>>5] = column allowed
             uint32_t mk[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
             bool masked = false;
+            int width = kBlock;  // columns the S MMA wrote (the rest of S is stale)
+            auto prefix_word = [](int b) { return b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b))); };
             if constexpr (kSparse) {
-                const int e = __ldg(tiles + j);
-                if (e < 0) {
-                    const int lim = vcnt_i - (-e - 1) * kBlock;  // allowed gathered rows: c < lim
+                const int ee = __ldg(tiles + j);
+                const int e = ent_value(ee);
+                width = ent_width(ee);
+                if (ent_gathered(ee)) {
+                    // allowed gathered rows: c < lim (lim <= the tile's width by construction)
+                    const int lim = vcnt_i - e * kBlock;
                     if (lim < kBlock) {
                         masked = true;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int b = lim - 32 * k;
-                            mk[k] = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
-                        }
+                        for (int k = 0; k < 4; ++k) mk[k] = prefix_word(lim - 32 * k);
                     }
                 } else {
                     masked = true;
@@ -451,123 +641,46 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     } else {  // dense-masked block: verticals come from this tile too (j <= i)
                         const int lim = i - e + 1;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int b = lim - 32 * k;
-                            const uint32_t causal = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
-                            mk[k] = __brev(sw[3 - k]) | (vw[k] & causal);
-                        }
+                        for (int k = 0; k < 4; ++k) mk[k] = __brev(sw[3 - k]) | (vw[k] & prefix_word(lim - 32 * k));
                     }
+                    // columns past a narrow tile belong to the next tile of the range
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) mk[k] &= prefix_word(width - 32 * k);
                 }
             } else {
                 if (j == qb) {  // diagonal tile: c <= r
                     masked = true;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int b = r - 32 * k + 1;
-                        mk[k] = b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b)));
-                    }
+                    for (int k = 0; k < 4; ++k) mk[k] = prefix_word(r - 32 * k + 1);
                 }
             }
 
-            // tcgen05.ld/st are warp-collective: the masked path must be warp-uniform (lanes
-            // that need no mask carry all-ones words)
-            masked = __any_sync(0xffffffffu, masked);
+            masked = __any_sync(0xffffffffu, masked || width < kBlock);
+            // Masked tiles work per 32-column chunk with warp-uniform modes: a chunk masked for
+            // all 32 rows of the warp is skipped (no max, no exponentials; its P is written as
+            // zeros) — most of a slash tile, the tail of a vertical run; a partially masked chunk
+            // gets element selects; a fully allowed one neither. Unmasked tiles take a
+            // branch-free path.
+            uint32_t dead = 0u, part = 0u;
+            if (masked) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!__any_sync(0xffffffffu, mk[k] != 0u)) dead |= 1u << k;
+                    else if (__any_sync(0xffffffffu, mk[k] != 0xffffffffu)) part |= 1u << k;
+                }
+            }
             mbar_wait(&sm.s_full[w], (gt + j) & 1);
+            if (quarter == 0) VSP_TRACE(2, w, gt + j);
             tc_fence_after();
-            // pass 1: row max of the raw logits q.k (TMEM is re-read in pass 2 rather than
-            // holding 128 values in registers)
-            float mx;
-            {
-                uint32_t u[4][32];  // all four loads in flight before the first wait
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(s_t + c * 32, u[c]);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_reg_fence(u[c]);
-                // eight independent max chains (a single chain is 64 dependent 3-input maxes)
-                float mxa[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mxa[t] = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (masked) {  // write the masked logits back so pass 2 is mask-free
-#pragma unroll
-                        for (int t = 0; t < 32; ++t)
-                            if (!((mk[c] >> t) & 1u)) u[c][t] = 0xff800000u;  // -inf
-                        tmem_st32(s_t + c * 32, u[c]);
-                    }
-#pragma unroll
-                    for (int t = 0; t < 32; t += 2)
-                        mxa[(t >> 1) & 7] = fmaxf(mxa[(t >> 1) & 7], fmaxf(__uint_as_float(u[c][t]), __uint_as_float(u[c][t + 1])));
-                }
-                mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-            }
-            if (masked) tmem_wait_st();
-            const float m_new = fmaxf(m_used, mx * sl2);
-            const bool need = (m_used == -INFINITY) ? (m_new > -INFINITY) : (m_new > m_used + kRescaleThreshold);
-            if (__any_sync(0xffffffffu, need)) {
-                const float m_next = need ? m_new : m_used;
-                const float f = (m_used == -INFINITY) ? 0.f : ex2_approx(m_used - m_next);
-                l *= f;
-                m_used = m_next;
-                if (j > 0) {  // O holds PV(0..j-1); PV(j-1) is complete (see header)
-#pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t u[32];
-                        tmem_ld32(o_t + c * 32, u);
-                        tmem_wait_ld(u);
-#pragma unroll
-                        for (int t = 0; t < 32; ++t) u[t] = __float_as_uint(__uint_as_float(u[t]) * f);
-                        tmem_st32(o_t + c * 32, u);
-                    }
-                }
-            }
-            const float m_eff = (m_used == -INFINITY) ? 0.f : m_used;
-            const float2 scl = make_float2(sl2, sl2);
-            const float2 neg_m = make_float2(-m_eff, -m_eff);
-            float2 lsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                              make_float2(0.f, 0.f)};
-            // pass 2: p = 2^(s * scale * log2e - m), packed to bf16 pairs and written over the
-            // already-consumed S columns (chunk c's P lands in [16c, 16c+16) < 32c)
-            {
-                uint32_t u[2][32];  // ping-pong: chunk c+1 is loading while chunk c computes
-                tmem_ld32(s_t, u[0]);
-                tmem_wait_ld(u[0]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (c < 3) tmem_ld32(s_t + (c + 1) * 32, u[(c + 1) & 1]);
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        const float2 y = ffma2(make_float2(__uint_as_float(u[c & 1][2 * t]),
-                                                           __uint_as_float(u[c & 1][2 * t + 1])),
-                                               scl, neg_m);
-                        float2 e;
-                        if ((0x5454u >> t) & 1u) {  // 3 pairs in 8 on the FMA pipe (MUFU/FMA balance)
-                            e = exp2_poly2(y);
-                        } else {
-                            e.x = ex2_approx(y.x);
-                            e.y = ex2_approx(y.y);
-                        }
-                        lsum[t & 3] = fadd2(lsum[t & 3], e);
-                        pk[t] = pack_bf16x2(e.x, e.y);
-                    }
-                    tmem_st16(s_t + c * 16, pk);
-                    if (c == 1) {  // P columns [0, 64) are in TMEM: the first PV half may start
-                        tmem_wait_st();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&sm.p_half[w]);
-                    }
-                    if (c < 3) tmem_wait_ld(u[(c + 1) & 1]);
-                }
-            }
-            l += ((lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y)) + ((lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y));
+            if (masked)
+                softmax_tile<true>(s_t, o_t, dead, part, make_uint4(mk[0], mk[1], mk[2], mk[3]), width, j, sl2, m_used, l, &sm.p_half[w], quarter, w, gt + j);
+            else
+                softmax_tile<false>(s_t, o_t, dead, part, make_uint4(mk[0], mk[1], mk[2], mk[3]), width, j, sl2, m_used, l, &sm.p_half[w], quarter, w, gt + j);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full[w]);
+            if (quarter == 0) VSP_TRACE(5, w, gt + j);
         }
 
         // ---- epilogue: O / l -> bf16 [n, Hq, d]; LSE (natural log of sum exp(scaled logits))
@@ -576,37 +689,51 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const int h = w ? x.h1 : x.h0;
         const bool store = w == 0 || x.h1 != x.h0;  // a duplicated head is written once
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow = p.o + static_cast<long long>(i) * p.o_tok_stride + static_cast<long long>(h) * p.o_head_stride;
+        // O -> bf16 through a swizzled 16 KB staging half per Q tile and TMA stores (one 64-column
+        // half at a time): per-thread row stores (rows 256 B apart) clogged the LSU/MIO pipe for
+        // thousands of cycles at every item end. Rows past n are clipped by the TMA unit.
+        uint8_t* stage = sO + w * kOStage;
+        const bool issuer = quarter == 0 && lane == 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t u[32];
-            tmem_ld32(o_t + c * 32, u);
-            tmem_wait_ld(u);
-            if (num_tiles == 0) {
-#pragma unroll
-                for (int t = 0; t < 32; ++t) u[t] = 0u;
+        for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v[2][32];
+            tmem_ld32(o_t + hf * 64, v[0]);
+            tmem_ld32(o_t + hf * 64 + 32, v[1]);
+            tmem_wait_ld();
+            tmem_reg_fence(v[0]);
+            tmem_reg_fence(v[1]);
+            if (hf == 1) {  // O_w has been read: the next item's first PV may overwrite it
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.o_free[w]);
             }
-            if (i < p.n && store) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+            if (store) {
+                // the previous TMA store from this buffer has finished reading it
+                if (issuer) bulk_wait_read0();
+                named_bar_sync(1 + w, 128);
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    uint4 v;
-                    v.x = pack_bf16x2(__uint_as_float(u[8 * t + 0]) * inv_l, __uint_as_float(u[8 * t + 1]) * inv_l);
-                    v.y = pack_bf16x2(__uint_as_float(u[8 * t + 2]) * inv_l, __uint_as_float(u[8 * t + 3]) * inv_l);
-                    v.z = pack_bf16x2(__uint_as_float(u[8 * t + 4]) * inv_l, __uint_as_float(u[8 * t + 5]) * inv_l);
-                    v.w = pack_bf16x2(__uint_as_float(u[8 * t + 6]) * inv_l, __uint_as_float(u[8 * t + 7]) * inv_l);
-                    dst[t] = v;
+                for (int u8 = 0; u8 < 8; ++u8) {  // 16-byte unit u8 of the row's 128-byte half
+                    uint4 q4;
+                    const uint32_t* src = &v[u8 >> 2][(u8 & 3) * 8];
+                    q4.x = num_tiles ? pack_bf16x2(__uint_as_float(src[0]) * inv_l, __uint_as_float(src[1]) * inv_l) : 0u;
+                    q4.y = num_tiles ? pack_bf16x2(__uint_as_float(src[2]) * inv_l, __uint_as_float(src[3]) * inv_l) : 0u;
+                    q4.z = num_tiles ? pack_bf16x2(__uint_as_float(src[4]) * inv_l, __uint_as_float(src[5]) * inv_l) : 0u;
+                    q4.w = num_tiles ? pack_bf16x2(__uint_as_float(src[6]) * inv_l, __uint_as_float(src[7]) * inv_l) : 0u;
+                    *reinterpret_cast<uint4*>(stage + r * 128 + ((u8 ^ (r & 7)) << 4)) = q4;  // SWIZZLE_128B
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + w, 128);
+                if (issuer && !(p.prefetch_q & 2)) {
+                    tma_store_3d(&p.map_o, stage, hf * 64, h, i0);
+                    bulk_commit_group();
                 }
             }
         }
         if (i < p.n && store && p.lse != nullptr)
             p.lse[static_cast<size_t>(h) * p.n + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
-        // O_w has been read: the next item's first PV may overwrite it
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.o_free[w]);
         gt += num_tiles;
         }
+        if (quarter == 0 && lane == 0) bulk_wait0();  // this tile's O stores are complete
     }
 
     tc_fence_before();
@@ -704,16 +831,19 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
     const int cv = upper_bound_i(ivg, k_v, ilast);
     const int vc0 = upper_bound_i(ivg, k_v, i0 - 1);
     const int ntv = (cv + kBlock - 1) / kBlock;
-    for (int t = lane; t < ntv; t += 32) out[2 + t] = -(t + 1);
+    // the run's last gathered tile is narrow: its used rows rounded up to 16
+    for (int t = lane; t < ntv; t += 32)
+        out[2 + t] = ent_make(t, true, t == ntv - 1 ? round16(cv - t * kBlock) : kBlock);
     int cnt = ntv;
     const int s = upper_bound_i(isg, k_s, ilast);
     int cur = 0, a = -1, b = -1;  // open range [a, b] (lane-uniform state)
     auto emit = [&](int lo, int hi) {  // lane-uniform: every lane computes, lanes write
         const int st0 = max(lo, cur);
         const int m = st0 <= hi ? (hi - st0) / kBlock + 1 : 0;
-        for (int x = lane; x < m; x += 32) out[2 + cnt + x] = st0 + x * kBlock;
+        const int wl = round16(hi - (st0 + (m - 1) * kBlock) + 1);  // narrow last tile of the range
+        for (int x = lane; x < m; x += 32) out[2 + cnt + x] = ent_make(st0 + x * kBlock, false, x == m - 1 ? wl : kBlock);
         cnt += m;
-        if (m) cur = st0 + m * kBlock;
+        if (m) cur = st0 + (m - 1) * kBlock + wl;
     };
     const int limit = qb + 1;  // stop as soon as dense-masked mode is certain
     for (int base = s - 1; base >= 0 && cnt < limit; base -= 32) {
@@ -744,7 +874,7 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
         // switch this block to dense-masked mode (header vcnt0 = -1), columns [0, i0+127]
         // with mask (j in I_v OR i-j in I_s) AND j <= i — never slower than K4.
         __syncwarp();
-        for (int t = lane; t < limit; t += 32) out[2 + t] = t * kBlock;
+        for (int t = lane; t < limit; t += 32) out[2 + t] = ent_make(t * kBlock, false, kBlock);
         cnt = limit;
     }
     if (lane == 0) {
@@ -755,9 +885,13 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
 
 // ------------------------------------------------------------------ host launchers
 
-static void set_o_layout(AttnParams& p, const AttnArgs& a) {
+static bool set_o_layout(AttnParams& p, const AttnArgs& a) {
     p.o_tok_stride = a.o_head_major ? kHeadDim : static_cast<long long>(a.hq) * kHeadDim;
     p.o_head_stride = a.o_head_major ? static_cast<long long>(a.n) * kHeadDim : kHeadDim;
+    const uint32_t box[3] = {64, 1, kBlock};
+    const uint64_t dims[3] = {kHeadDim, (uint64_t)a.hq, (uint64_t)a.n};
+    const uint64_t strides[2] = {static_cast<uint64_t>(p.o_head_stride) * 2, static_cast<uint64_t>(p.o_tok_stride) * 2};
+    return vsp_host::make_map_bf16(&p.map_o, a.o, 3, dims, strides, box);
 }
 
 static bool make_qkv_maps(AttnParams& p, const void* q, const void* k, const void* v) {
@@ -803,6 +937,7 @@ cudaError_t launch_attn(AttnParams& p, int nqb, cudaStream_t stream) {
     });
     const int grp = p.hq / p.hkv;
     const bool mc = ((grp + 1) / 2) % 2 == 0 && p.pair0 % 2 == 0 && p.npairs % 2 == 0 && !getenv_flag("VSP_NO_MULTICAST");
+    p.prefetch_q = (getenv_flag("VSP_NO_Q_PREFETCH") ? 0 : 1) | (getenv_flag("VSP_DEBUG_NO_O_STORE") ? 2 : 0);
     vsp_detail::count_launch();
     if (!mc) {
         p.items = nqb * p.npairs;
@@ -834,8 +969,7 @@ cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream) {
     p.scale = a.scale;
     p.o = static_cast<__nv_bfloat16*>(a.o);
     p.lse = a.lse;
-    set_o_layout(p, a);
-    if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
+    if (!set_o_layout(p, a) || !make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     p.pair0 = 0;
     p.npairs = a.hkv * ((a.hq / a.hkv + 1) / 2);
@@ -868,6 +1002,7 @@ namespace {
 cudaError_t launch_sparse_impl(const AttnArgs& a, const SparseArgs& s, void* workspace, cudaStream_t stream, int g0,
                                int count, int phase, int qb_lo, int qb_hi, const int* host_units, int nunits) {
     if (count < 0) count = a.hkv - g0;
+    if (a.n >= kEntGathered) return cudaErrorInvalidValue;  // tile-list entries hold rows in 27 bits
     AttnParams p{};
     p.n = a.n;
     p.hq = a.hq;
@@ -875,8 +1010,7 @@ cudaError_t launch_sparse_impl(const AttnArgs& a, const SparseArgs& s, void* wor
     p.scale = a.scale;
     p.o = static_cast<__nv_bfloat16*>(a.o);
     p.lse = a.lse;
-    set_o_layout(p, a);
-    if (!make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
+    if (!set_o_layout(p, a) || !make_qkv_maps(p, a.q, a.k, a.v)) return cudaErrorInvalidValue;
     const int num_qb = (a.n + kBlock - 1) / kBlock;
     const int kvcap = ((s.cap + kBlock - 1) / kBlock) * kBlock;
     const int bm_words = (a.n + 31) / 32 + 1;
@@ -976,6 +1110,12 @@ cudaError_t launch_sparse_units(const AttnArgs& a, const SparseArgs& s, void* wo
 }
 
 }  // namespace vsp_attn
+
+#ifdef VSP_K3_TRACE
+extern "C" __attribute__((visibility("default"))) int vsp_k3_trace_read(void* host, size_t bytes) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, vsp_attn::g_k3_trace, bytes));
+}
+#endif
 
 namespace vsp_attn {
 
