@@ -73,9 +73,14 @@ enum { VSP_REDUCE_MEAN = 0, VSP_REDUCE_SUM = 1 };
 /* vsp_vs_attn_fwd flags */
 enum {
     VSP_VALIDATE = 1,     /* sync + check sortedness/range/coverage like the reference */
-    VSP_O_HEAD_MAJOR = 2  /* write O head-major [hq, n, 128] (the reference's per-head n x d
+    VSP_O_HEAD_MAJOR = 2, /* write O head-major [hq, n, 128] (the reference's per-head n x d
                              matrices) instead of token-major [n, hq, 128]; a rank's heads are
                              then one contiguous slab, the in-place all-gather send buffer */
+    VSP_DENSE_SWITCH = 4  /* opt-in (vsp_vs_attn_fwd, vsp_vs_prefill, vsp_vs_prefill_units): a
+                             query block whose vertical-slash tiles would visit every causal
+                             tile anyway runs unmasked causal attention (blockwise_attention's
+                             rows) instead of the masked pattern — same tiles, no mask work, recall
+                             1 on those rows. Off = the reference's sparse_attention exactly. */
 };
 
 /* Reference BudgetConfig (sparsity.hpp:22-36). max_budget < 0 means "no maximum". */

@@ -41,7 +41,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_PKG, "libvsp_gpu.so")
 
 VSP_OK, VSP_EINVAL, VSP_ERUNTIME, VSP_ECUDA, VSP_ENCCL = range(5)
-VSP_VALIDATE, VSP_O_HEAD_MAJOR = 1, 2
+VSP_VALIDATE, VSP_O_HEAD_MAJOR, VSP_DENSE_SWITCH = 1, 2, 4
 
 
 class VspError(ValueError):
@@ -316,11 +316,14 @@ def select_pattern(a_v: torch.Tensor, a_s: torch.Tensor, budget, validate: bool 
 
 def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern: SelectedIndices,
                      validate: bool = True, out: Optional[torch.Tensor] = None,
-                     lse: Optional[torch.Tensor] = None, head_major: bool = False):
+                     lse: Optional[torch.Tensor] = None, head_major: bool = False,
+                     dense_switch: bool = False):
     """sparse_attention (attention.hpp:150-194) for every Q head -> (O [n, Hq, d] bf16,
     LSE [Hq, n] fp32). validate=True reproduces the reference's checks and messages
     (merge.hpp:21-26, attention.hpp:161-163) at the cost of one stream sync.
-    head_major=True writes O as [Hq, n, d] (the reference's per-head matrices)."""
+    head_major=True writes O as [Hq, n, d] (the reference's per-head matrices).
+    dense_switch=True (opt-in, not the reference's semantics): query blocks whose pattern
+    already visits every causal tile run unmasked causal attention (VSP_DENSE_SWITCH)."""
     _need_cuda(q, k, v)
     n, hq, d = q.shape
     hkv = k.shape[1]
@@ -334,7 +337,8 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pattern:
     _check(lib.vsp_vs_attn_fwd(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, _ptr(pattern.i_v),
                                _ptr(pattern.k_v), _ptr(pattern.i_s), _ptr(pattern.k_s), cap,
                                1.0 / math.sqrt(d), _ptr(o), _ptr(lse), _ptr(ws),
-                               (1 if validate else 0) | (VSP_O_HEAD_MAJOR if head_major else 0), _stream(dev)))
+                               (1 if validate else 0) | (VSP_O_HEAD_MAJOR if head_major else 0)
+                               | (VSP_DENSE_SWITCH if dense_switch else 0), _stream(dev)))
     return o, lse
 
 
@@ -466,7 +470,7 @@ def merge_path_partition(a, b, p: int):
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
                mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
-               lse: Optional[torch.Tensor] = None, head_major: bool = False):
+               lse: Optional[torch.Tensor] = None, head_major: bool = False, dense_switch: bool = False):
     """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
     indexer -> selection -> sparse attention; heads_per_chunk=0 runs them in order on the
     current stream, heads_per_chunk>0 pipelines KV-head chunks so that the
@@ -474,6 +478,7 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
     `vsprefill select` + `vsprefill attend` (tools/vsprefill.cpp:154-185) on device.
     Same results as indexer_forward + select_pattern + sparse_attention.
     head_major=True writes O as [Hq, n, d] (e.g. a slab of the full output on a shard rank).
+    dense_switch=True: see sparse_attention (opt-in; off = the reference's semantics).
     Returns (O, LSE, SelectedIndices)."""
     _need_cuda(q, k, v)
     n, hq, d = q.shape
@@ -499,7 +504,8 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
                               _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
                               _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
                               _ptr(a_v), _ptr(a_s), _ptr(i_v), _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(o),
-                              _ptr(lse), _ptr(ws), int(heads_per_chunk), VSP_O_HEAD_MAJOR if head_major else 0,
+                              _ptr(lse), _ptr(ws), int(heads_per_chunk),
+                              (VSP_O_HEAD_MAJOR if head_major else 0) | (VSP_DENSE_SWITCH if dense_switch else 0),
                               _stream(dev)))
     return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
 

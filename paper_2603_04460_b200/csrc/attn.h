@@ -51,6 +51,7 @@ struct SparseArgs {
     const int* is;  // [hkv, cap] ascending slash offsets
     const int* ks;  // [hkv]
     int cap;
+    bool dense_switch = false;  // blocks whose VS tiles reach the dense count run unmasked causal
 };
 
 cudaError_t launch_dense(const AttnArgs& a, cudaStream_t stream);

@@ -25,7 +25,7 @@
 // Online softmax runs in the exp2 domain with lazy rescaling (only when the running max
 // grows by more than 2^8), exactly the same math as the reference's per-row rescale.
 //
-// Sparse mode: per (KV head, query block) a tile list built by vs_plan_kernel. An entry is
+// Sparse mode: per (KV head, query block) a tile list built by vs_prep_kernel. An entry is
 // (value, gathered flag, width): a "slash span" tile covers K/V rows [value, value+width) of
 // the original tensors with element mask (i-j) in I_s AND j not in I_v AND j <= i (from n-bit
 // bitmaps); a gathered vertical tile t = value covers rows [128t, 128t+width) of K[I_v], V[I_v]
@@ -78,6 +78,8 @@ struct Smem {
     uint64_t o_free[2];                       // epilogue has read O_w (next item may PV into it)
     uint64_t item_full[kItemRing], item_empty[kItemRing];
     int item[kItemRing];                      // work item index, -1 = no more work
+    int item_nt[kItemRing], item_vc[kItemRing];  // sparse: the item's tile-list header (the
+                                                 // producer reads it one item ahead)
     uint32_t tmem_base;
 };
 
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     // the dynamic load balance of a one-CTA-per-item grid.
     const uint32_t crank = kMc > 1 ? cluster_ctarank() : 0u;
     const int cpairs = p.npairs / kMc;  // pair groups per query block (one per cluster item)
-    auto item = [&](int it) {
+    auto item = [&](int it, int hdr_nt, int hdr_vc) {
         Item x;
         // pair index -> (KV group, pair within the group); an odd group's last pair carries
         // one head (both Q tiles load it, only tile 0 writes)
@@ -281,10 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         x.vcnt0 = 0;
         x.tiles = nullptr;
         if constexpr (kSparse) {
-            const int* hdr = p.tile_lists + (static_cast<size_t>(x.g) * num_qb + x.qb) * p.list_stride;
-            x.num_tiles = hdr[0];
-            x.vcnt0 = hdr[1];
-            x.tiles = hdr + 2;
+            x.num_tiles = hdr_nt;
+            x.vcnt0 = hdr_vc;
+            x.tiles = p.tile_lists + (static_cast<size_t>(x.g) * num_qb + x.qb) * p.list_stride + 2;
         } else {
             x.num_tiles = x.qb + 1;
         }
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
     // consumer side of the item ring (MMA warp and softmax warps): item of round n_it, or -1
-    auto next_item = [&](int n_it) {
+    auto next_item = [&](int n_it, int& nt, int& vc) {
         const int slot = n_it % kItemRing;
 #ifdef VSP_K3_TRACE
         if (warp == 1) VSP_TRACE(11, 0, n_it);
@@ -304,6 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         if (warp == 1) VSP_TRACE(11, 1, n_it);
 #endif
         const int it = *reinterpret_cast<volatile int*>(&sm.item[slot]);
+        nt = *reinterpret_cast<volatile int*>(&sm.item_nt[slot]);
+        vc = *reinterpret_cast<volatile int*>(&sm.item_vc[slot]);
         __syncwarp();
         if (lane == 0) {
             if (crank == 0) mbar_arrive(&sm.item_empty[slot]);
@@ -342,6 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     __syncthreads();
     if constexpr (kMc > 1) cluster_sync();  // peers' barriers exist before any remote arrive / multicast
     tc_fence_after();
+    // launched as a programmatic dependent of the planning grid: everything above overlapped
+    // its tail; the tile lists, bitmaps, gathered rows and work counters are read below
+    griddep_wait();
     const uint32_t tmem = sm.tmem_base;
     // register split (per warpgroup, at the top of each role's branch so the allocator sees
     // it): the producer / MMA warpgroup needs few, the softmax warps hold a whole S row (128
@@ -365,7 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         // Producer side of the item ring, one round ahead of the item being loaded: the next
         // item's Q tiles are prefetched into L2 while this item streams its K/V tiles, so the
         // Q load at the item boundary (single-buffered, it waits for the last S MMA) hits L2.
-        auto fetch = [&](int n_it) {
+        // The leader also reads the item's tile-list header here, so the consumers take it
+        // from shared memory instead of each paying an L2 round trip at the item boundary
+        // (both CTAs of a cluster run the same (KV head, query block): same header).
+        auto fetch = [&](int n_it, int& nt, int& vc) {
             const int slot = n_it % kItemRing;
             int it = 0;
             if (crank == 0) {
@@ -374,33 +383,47 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                     const int nclusters = static_cast<int>(gridDim.x) / kMc;
                     it = n_it == 0 ? static_cast<int>(blockIdx.x) / kMc : atomicAdd(p.work + 0, 1) + nclusters;
                     if (it >= p.items) it = -1;
+                    nt = 0;
+                    vc = 0;
+                    if (kSparse && it >= 0) {
+                        const int* hdr = item(it, 0, 0).tiles - 2;
+                        nt = __ldcg(hdr);
+                        vc = __ldcg(hdr + 1);
+                    }
                     sm.item[slot] = it;
-                    mbar_arrive(&sm.item_full[slot]);  // release: the item index is visible to waiters
+                    sm.item_nt[slot] = nt;
+                    sm.item_vc[slot] = vc;
+                    mbar_arrive(&sm.item_full[slot]);  // release: the item is visible to waiters
                     if constexpr (kMc > 1) {
                         st_cluster_u32(mapa_shared(smem_u32(&sm.item[slot]), 1), static_cast<uint32_t>(it));
+                        st_cluster_u32(mapa_shared(smem_u32(&sm.item_nt[slot]), 1), static_cast<uint32_t>(nt));
+                        st_cluster_u32(mapa_shared(smem_u32(&sm.item_vc[slot]), 1), static_cast<uint32_t>(vc));
                         mbar_arrive_cluster(mapa_shared(smem_u32(&sm.item_full[slot]), 1));
                     }
                 }
                 it = __shfl_sync(0xffffffffu, it, 0);
+                nt = __shfl_sync(0xffffffffu, nt, 0);
+                vc = __shfl_sync(0xffffffffu, vc, 0);
             } else {
-                it = next_item(n_it);  // the peer's producer consumes the leader's fetch
+                it = next_item(n_it, nt, vc);  // the peer's producer consumes the leader's fetch
             }
             return it;
         };
-        int it_next = fetch(0);
+        int nt_next = 0, vc_next = 0;
+        int it_next = fetch(0, nt_next, vc_next);
         for (int n_it = 0;; ++n_it) {
-            const int it = it_next;
+            const int it = it_next, it_nt = nt_next, it_vc = vc_next;
             if (it < 0) break;
-            it_next = fetch(n_it + 1);
+            it_next = fetch(n_it + 1, nt_next, vc_next);
             VSP_TRACE(9, 0, gj);
             if (it_next >= 0 && p.prefetch_q) {
-                const Item xn = item(it_next);
+                const Item xn = item(it_next, nt_next, vc_next);
                 if (elect_one())
                     for (int w = 0; w < 2; ++w)
                         for (int hf = 0; hf < 2; ++hf) tma_prefetch_3d(&p.map_q, hf * 64, w ? xn.h1 : xn.h0, xn.qb * kBlock);
                 __syncwarp();
             }
-            const Item x = item(it);
+            const Item x = item(it, it_nt, it_vc);
             // the previous item's last S MMA has read its Q tiles
             if (n_it > 0) mbar_wait(&sm.q_free, (n_it - 1) & 1);
             VSP_TRACE(7, 0, gj);
@@ -414,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             __syncwarp();
             VSP_TRACE(9, 1, gj);
             for (int j = 0; j < x.num_tiles; ++j, ++gj) {
-                const int e = kSparse ? __ldg(x.tiles + j) : 0;
+                // dense-mode blocks (vcnt0 < 0) list tiles 0..qb in order: no entry load
+                const int e = (kSparse && x.vcnt0 >= 0) ? __ldg(x.tiles + j) : ent_make(j * kBlock, false, kBlock);
                 const bool gathered = kSparse && ent_gathered(e);
                 const int row = kSparse ? (gathered ? ent_value(e) * kBlock : ent_value(e)) : j * kBlock;
                 const CUtensorMap* mk_ = gathered ? &p.map_kv : &p.map_k;
@@ -471,15 +495,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             const uint64_t vd = v_desc0 + static_cast<uint64_t>(((gjj % kNumV) * kTileBytes) >> 4);
             const uint32_t o_t = tmem + 256 + w * 128;
             const uint32_t p_t = tmem + w * 128;
+            if (nk == 8) {  // full tile (every dense tile, most sparse ones): straight-line issue
 #pragma unroll
-            for (int k = 4 * h; k < 4 * h + 4; ++k)
-                if (k < nk)
+                for (int k = 4 * h; k < 4 * h + 4; ++k)
                     umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
                             (!first || k > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+                for (int k = 4 * h; k < 4 * h + 4; ++k)
+                    if (k < nk)
+                        umma_ts(o_t, p_t + k * 8, vd + static_cast<uint64_t>((k * 2048) >> 4), idesc_pv,
+                                (!first || k > 0) ? 1u : 0u);
+            }
         };
         // S_w = Q_w K^T over the tile's first `width` keys (N = width)
         auto issue_s = [&](int w, int gjj, int width) {
-            const uint32_t idesc = (idesc_qk & ~(0x3Fu << 17)) | (static_cast<uint32_t>(width >> 3) << 17);
+            const uint32_t idesc =
+                width == kBlock ? idesc_qk : (idesc_qk & ~(0x3Fu << 17)) | (static_cast<uint32_t>(width >> 3) << 17);
             const uint64_t qd = q_desc0 + static_cast<uint64_t>((w * kTileBytes) >> 4);
             const uint64_t kd = k_desc0 + static_cast<uint64_t>(((gjj % kNumK) * kTileBytes) >> 4);
             const uint32_t s_t = tmem + w * 128;
@@ -492,10 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         int gj = 0;
         for (int n_it = 0;; ++n_it) {
             VSP_TRACE(8, 0, gj);
-            const int it = next_item(n_it);
+            int it_nt, it_vc;
+            const int it = next_item(n_it, it_nt, it_vc);
             VSP_TRACE(8, 1, gj);
             if (it < 0) break;
-            const Item x = item(it);
+            const Item x = item(it, it_nt, it_vc);
             const int nt = x.num_tiles;
             mbar_wait(&sm.q_full, n_it & 1);
             VSP_TRACE(7, 1, gj);
@@ -518,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             for (int j = 0; j < nt; ++j) {
                 const int G = gj + j;
                 const int ks = G % kNumK;
-                const int width = kSparse ? ent_width(__ldg(x.tiles + j)) : kBlock;
+                const int width = (kSparse && x.vcnt0 >= 0) ? ent_width(__ldg(x.tiles + j)) : kBlock;
                 mbar_wait(&sm.k_full[ks], (G / kNumK) & 1);
                 VSP_TRACE(1, 0, G);
                 tc_fence_after();
@@ -585,9 +618,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const float sl2 = p.scale * kLog2e;
         int gt = 0;  // global tile index: s_full / p_full phases continue across items
         for (int n_it = 0;; ++n_it) {
-        const int it = next_item(n_it);
+        int it_nt, it_vc;
+        const int it = next_item(n_it, it_nt, it_vc);
         if (it < 0) break;
-        const Item x = item(it);
+        const Item x = item(it, it_nt, it_vc);
         const int qb = x.qb, g = x.g, num_tiles = x.num_tiles, vcnt0 = x.vcnt0;
         const int* tiles = x.tiles;
         (void)tiles;
@@ -597,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
         // sparse: #{I_v <= i} = vcnt0 + popcount(vbits over [i0, i])
         int vcnt_i = 0;
-        if constexpr (kSparse) {
+        if (kSparse && vcnt0 >= 0) {
             uint32_t vw[4];
             window128(p.vbits + static_cast<size_t>(g) * p.bm_words, i0, p.bm_words, vw);
             int c = 0;
@@ -619,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             int width = kBlock;  // columns the S MMA wrote (the rest of S is stale)
             auto prefix_word = [](int b) { return b <= 0 ? 0u : (b >= 32 ? 0xffffffffu : (0xffffffffu >> (32 - b))); };
             if constexpr (kSparse) {
-                const int ee = __ldg(tiles + j);
+                const int ee = vcnt0 >= 0 ? __ldg(tiles + j) : ent_make(j * kBlock, false, kBlock);
                 const int e = ent_value(ee);
                 width = ent_width(ee);
                 if (ent_gathered(ee)) {
@@ -629,6 +663,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                         masked = true;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) mk[k] = prefix_word(lim - 32 * k);
+                    }
+                } else if (vcnt0 == -2) {  // dense switch: unmasked causal block
+                    if (e == i0) {
+                        masked = true;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mk[k] = prefix_word(r - 32 * k + 1);
                     }
                 } else {
                     masked = true;
@@ -754,57 +794,94 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
 // ------------------------------------------------------------------ sparse planning
 
-// Bitmaps (bit j of vbits[g] <=> j in I_v[g]; bit o of sbits[g] <=> o in I_s[g]).
-// Caller zeroes them first. grid (ceil(cap/256), hkv).
-__global__ void build_bitmaps_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
-                                     const int* __restrict__ is, const int* __restrict__ ks, int cap,
-                                     int n, int bm_words, uint32_t* vbits, uint32_t* sbits, int g0) {
-    const int g = g0 + static_cast<int>(blockIdx.y);
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < kv[g]) {
-        const int j = iv[static_cast<size_t>(g) * cap + t];
-        if (j >= 0 && j < n)  // columns >= n are never reached by any row (j <= i < n)
-            atomicOr(vbits + static_cast<size_t>(g) * bm_words + (j >> 5), 1u << (j & 31));
+// #{a[t] <= x} for ascending a[0, n), by the whole warp: a 32-ary search (one pivot per lane,
+// a ballot narrows the range 32x per step), so 4 dependent L2 round trips at n = 128k
+// instead of the 17 of a binary search. Warp-uniform arguments.
+VSP_DEVICE int warp_upper_bound(const int* a, int n, int x) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n;  // answer in [lo, hi]
+    while (lo < hi) {
+        const int step = (hi - lo + 31) >> 5;
+        const int pv = lo + (lane + 1) * step - 1;
+        const bool t = pv < hi && __ldg(a + pv) <= x;
+        const int nlo = lo + __popc(__ballot_sync(0xffffffffu, t)) * step;
+        hi = min(hi, nlo + step - 1);
+        lo = nlo;
     }
-    if (t < ks[g]) {
-        const int o = is[static_cast<size_t>(g) * cap + t];
-        if (o >= 0 && o < n)
-            atomicOr(sbits + static_cast<size_t>(g) * bm_words + (o >> 5), 1u << (o & 31));
+    return lo;
+}
+
+// Sparse planning in ONE launch (it replaced two memsets and three kernels): blockIdx.x
+// selects the role, blockIdx.y the KV head, 128 threads.
+//   [0, 2 nbw)            bitmaps: block c of direction d owns bitmap words [128c, 128c+128)
+//                         (bit j of vbits[g] <=> j in I_v[g]; bit o of sbits[g] <=> o in I_s[g]);
+//                         the words are built in shared memory from the sorted index run
+//                         that falls into them and stored whole, so no memset is needed
+//   [2 nbw, 2 nbw + ngb)  vertical gather (gather_vertical below)
+//   [.., + nplan)         tile lists, four query blocks per block (plan_block below); the
+//                         first plan block also zeroes the head's attention work counters
+// The attention kernel is launched as a programmatic dependent of this grid: every block
+// triggers at entry, so K3's CTAs take over the SMs as this grid drains and run their
+// prologue before their griddepcontrol.wait.
+struct PrepArgs {
+    const int* iv;
+    const int* kv;
+    const int* is;
+    const int* ks;
+    int cap, n, bm_words, hkv, kvcap, num_qb, list_stride, g0;
+    int nbw, ngb;  // bitmap blocks per direction, gather blocks
+    int dense_switch;
+    uint32_t* vbits;
+    uint32_t* sbits;
+    const __nv_bfloat16* k;
+    const __nv_bfloat16* v;
+    __nv_bfloat16* kg;
+    __nv_bfloat16* vg;
+    int* lists;
+    int* work;
+};
+
+VSP_DEVICE void build_bitmap_block(const int* __restrict__ idx, int count, int n, int bm_words, int c,
+                                   uint32_t* __restrict__ bits, uint32_t* sw) {
+    const int w0 = c * 128;
+    sw[threadIdx.x] = 0u;
+    __shared__ int range[2];
+    const int wid = threadIdx.x >> 5;
+    if (wid < 2) {
+        // index run [lo, hi) of the sorted list inside columns [32 w0, 32 (w0 + 128)) and < n
+        const int col = min(32 * (w0 + 128 * wid), n);
+        const int lo = warp_upper_bound(idx, count, col - 1);  // #{idx < col}
+        if ((threadIdx.x & 31) == 0) range[wid] = lo;
     }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = range[0] + static_cast<int>(threadIdx.x); t < range[1]; t += blockDim.x) {
+        const int j = __ldg(idx + t);
+        if (j >= 0) atomicOr(sw + ((j >> 5) - w0), 1u << (j & 31));  // columns >= n never set
+    }
+    __syncthreads();
+    if (w0 + static_cast<int>(threadIdx.x) < bm_words) bits[w0 + threadIdx.x] = sw[threadIdx.x];
 }
 
 // Kv[g][r] = K[I_v[g][r]][g] for r < k_v; rows [k_v, round_up(k_v, 128)) zero (the last
 // gathered tile is read whole: finite V rows keep 0 * V out of NaN); rows past that tile are
-// never read, so they are not written. grid (X, hkv), 256 threads, grid-stride over 16-row
-// groups: 16 threads x 16 B per 256 B row.
-__global__ void gather_vertical_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                                       const int* __restrict__ iv, const int* __restrict__ kv, int cap,
-                                       int n, int hkv, int kvcap, __nv_bfloat16* kg, __nv_bfloat16* vg, int g0) {
-    const int g = g0 + static_cast<int>(blockIdx.y);
+// never read, so they are not written. 16 threads x 16 B per 256 B row, 8 rows per step.
+VSP_DEVICE void gather_vertical(const PrepArgs& a, int g, int b, int nb) {
     const int t = threadIdx.x & 15;
-    const int cnt = min(kv[g], kvcap);
-    const int rows = min((cnt + kBlock - 1) / kBlock * kBlock, kvcap);
-    for (int r = blockIdx.x * 16 + (threadIdx.x >> 4); r < rows; r += gridDim.x * 16) {
-        uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+    const int cnt = min(a.kv[g], a.kvcap);
+    const int rows = min((cnt + kBlock - 1) / kBlock * kBlock, a.kvcap);
+    for (int r = b * 8 + (threadIdx.x >> 4); r < rows; r += nb * 8) {
+        uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
         if (r < cnt) {
-            const int j = min(max(__ldg(iv + static_cast<size_t>(g) * cap + r), 0), n - 1);
-            a = __ldg(reinterpret_cast<const uint4*>(k + (static_cast<size_t>(j) * hkv + g) * kHeadDim) + t);
-            b = __ldg(reinterpret_cast<const uint4*>(v + (static_cast<size_t>(j) * hkv + g) * kHeadDim) + t);
+            const int j = min(max(__ldg(a.iv + static_cast<size_t>(g) * a.cap + r), 0), a.n - 1);
+            x = __ldg(reinterpret_cast<const uint4*>(a.k + (static_cast<size_t>(j) * a.hkv + g) * kHeadDim) + t);
+            y = __ldg(reinterpret_cast<const uint4*>(a.v + (static_cast<size_t>(j) * a.hkv + g) * kHeadDim) + t);
         }
-        reinterpret_cast<uint4*>(kg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = a;
-        reinterpret_cast<uint4*>(vg + (static_cast<size_t>(g) * kvcap + r) * kHeadDim)[t] = b;
+        reinterpret_cast<uint4*>(a.kg + (static_cast<size_t>(g) * a.kvcap + r) * kHeadDim)[t] = x;
+        reinterpret_cast<uint4*>(a.vg + (static_cast<size_t>(g) * a.kvcap + r) * kHeadDim)[t] = y;
     }
 }
 
-VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) <= x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
 
 // Per (KV head g, query block qb): header {num_tiles, vcnt0} then entries (see file
 // header). Slash spans: for offsets o <= i_last (ascending I_s walked from the largest
@@ -815,11 +892,9 @@ VSP_DEVICE int upper_bound_i(const int* a, int n, int x) {  // #{a[t] <= x}
 // merged range is [lo of its first interval, hi of its last] and a range breaks exactly where
 // lo_next > hi_prev + 1. 32 offsets are classified per step (coalesced loads, ballot of the
 // breaks); lane 0 emits the finished ranges' tiles in order. grid (ceil(num_qb/4), hkv), 128.
-__global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict__ kv,
-                               const int* __restrict__ is, const int* __restrict__ ks, int cap, int n,
-                               int num_qb, int list_stride, int* __restrict__ lists, int g0) {
-    const int g = g0 + static_cast<int>(blockIdx.y);
-    const int qb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+VSP_DEVICE void plan_block(const int* __restrict__ iv, const int* __restrict__ kv, const int* __restrict__ is,
+                           const int* __restrict__ ks, int cap, int n, int num_qb, int list_stride,
+                           int* __restrict__ lists, int g, int qb, int dense_switch) {
     const int lane = threadIdx.x & 31;
     if (qb >= num_qb) return;
     const int i0 = qb * kBlock;
@@ -828,14 +903,14 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
     const int* isg = is + static_cast<size_t>(g) * cap;
     const int k_v = kv[g], k_s = ks[g];
     int* out = lists + (static_cast<size_t>(g) * num_qb + qb) * list_stride;
-    const int cv = upper_bound_i(ivg, k_v, ilast);
-    const int vc0 = upper_bound_i(ivg, k_v, i0 - 1);
+    const int cv = warp_upper_bound(ivg, k_v, ilast);
+    const int vc0 = warp_upper_bound(ivg, k_v, i0 - 1);
     const int ntv = (cv + kBlock - 1) / kBlock;
     // the run's last gathered tile is narrow: its used rows rounded up to 16
     for (int t = lane; t < ntv; t += 32)
         out[2 + t] = ent_make(t, true, t == ntv - 1 ? round16(cv - t * kBlock) : kBlock);
     int cnt = ntv;
-    const int s = upper_bound_i(isg, k_s, ilast);
+    const int s = warp_upper_bound(isg, k_s, ilast);
     int cur = 0, a = -1, b = -1;  // open range [a, b] (lane-uniform state)
     auto emit = [&](int lo, int hi) {  // lane-uniform: every lane computes, lanes write
         const int st0 = max(lo, cur);
@@ -846,40 +921,84 @@ __global__ void vs_plan_kernel(const int* __restrict__ iv, const int* __restrict
         if (m) cur = st0 + (m - 1) * kBlock + wl;
     };
     const int limit = qb + 1;  // stop as soon as dense-masked mode is certain
-    for (int base = s - 1; base >= 0 && cnt < limit; base -= 32) {
-        const int t = base - lane;
-        const bool valid = t >= 0;
-        const int o = valid ? __ldg(isg + t) : 0;
-        const int lo = max(0, i0 - o), hi = ilast - o;
-        const int prev_hi = __shfl_up_sync(0xffffffffu, hi, 1);
-        bool brk = valid && (lane == 0 ? (a >= 0 && lo > b + 1) : (lo > prev_hi + 1));
-        const unsigned bm = __ballot_sync(0xffffffffu, brk);
-        const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        if (a < 0) a = __shfl_sync(0xffffffffu, lo, 0);  // first interval opens the first range
-        unsigned rem = bm;
-        while (rem) {  // close the open range at each break, open the next one
-            const int e = __ffs(rem) - 1;
-            rem &= rem - 1;
-            const int b_close = e == 0 ? b : __shfl_sync(0xffffffffu, hi, e - 1);
-            emit(a, b_close);
-            a = __shfl_sync(0xffffffffu, lo, e);
+    {
+        // m offsets <= i0 give m length-128 intervals with distinct starts: their union spans
+        // >= m + 127 columns, so the slash tiles alone number >= ceil(m / 128)
+        const int m = warp_upper_bound(isg, k_s, i0);
+        if (cnt + (m + 127) / kBlock >= limit) cnt = limit;
+    }
+    // four 32-offset chunks per round: their loads are issued together (one L2 round trip per
+    // 128 offsets instead of per 32), then the chunks are merged in order
+    for (int base4 = s - 1; base4 >= 0 && cnt < limit; base4 -= 128) {
+        int ov[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = base4 - 32 * q - lane;
+            ov[q] = t >= 0 ? __ldg(isg + t) : 0;
         }
-        const int last = 31 - __clz(vm);
-        b = __shfl_sync(0xffffffffu, hi, last);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int base = base4 - 32 * q;
+            if (base < 0 || cnt >= limit) break;
+            const bool valid = base - lane >= 0;
+            const int o = ov[q];
+            const int lo = max(0, i0 - o), hi = ilast - o;
+            const int prev_hi = __shfl_up_sync(0xffffffffu, hi, 1);
+            bool brk = valid && (lane == 0 ? (a >= 0 && lo > b + 1) : (lo > prev_hi + 1));
+            const unsigned bm = __ballot_sync(0xffffffffu, brk);
+            const unsigned vm = __ballot_sync(0xffffffffu, valid);
+            if (a < 0) a = __shfl_sync(0xffffffffu, lo, 0);  // first interval opens the first range
+            unsigned rem = bm;
+            while (rem) {  // close the open range at each break, open the next one
+                const int e = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const int b_close = e == 0 ? b : __shfl_sync(0xffffffffu, hi, e - 1);
+                emit(a, b_close);
+                a = __shfl_sync(0xffffffffu, lo, e);
+            }
+            const int last = 31 - __clz(vm);
+            b = __shfl_sync(0xffffffffu, hi, last);
+            // the open range only grows: once it alone would reach the limit, the block is
+            // dense (long runs of consecutive offsets otherwise walk the whole list)
+            const int st0 = max(a, cur);
+            if (b >= st0 && cnt + (b - st0) / kBlock + 1 >= limit) cnt = limit;
+        }
     }
     if (a >= 0 && cnt < limit) emit(a, b);
     const bool dense_mode = cnt >= limit;
     if (dense_mode) {
         // the VS tiles would visit at least as many tiles as the dense causal row of tiles:
         // switch this block to dense-masked mode (header vcnt0 = -1), columns [0, i0+127]
-        // with mask (j in I_v OR i-j in I_s) AND j <= i — never slower than K4.
+        // with mask (j in I_v OR i-j in I_s) AND j <= i. With the dense switch (opt-in,
+        // VSP_DENSE_SWITCH) the block runs unmasked causal attention instead (vcnt0 = -2):
+        // the same tiles, no mask work, every causal pair of its rows covered.
         __syncwarp();
         for (int t = lane; t < limit; t += 32) out[2 + t] = ent_make(t * kBlock, false, kBlock);
         cnt = limit;
     }
     if (lane == 0) {
         out[0] = cnt;
-        out[1] = dense_mode ? -1 : vc0;
+        out[1] = dense_mode ? (dense_switch ? -2 : -1) : vc0;
+    }
+}
+
+__global__ void __launch_bounds__(128) vs_prep_kernel(const __grid_constant__ PrepArgs a) {
+    griddep_launch_dependents();
+    const int g = a.g0 + static_cast<int>(blockIdx.y);
+    const int b = blockIdx.x;
+    __shared__ uint32_t sw[128];
+    if (b < 2 * a.nbw) {
+        const bool slash = b >= a.nbw;
+        build_bitmap_block(slash ? a.is + static_cast<size_t>(g) * a.cap : a.iv + static_cast<size_t>(g) * a.cap,
+                           slash ? a.ks[g] : a.kv[g], a.n, a.bm_words, slash ? b - a.nbw : b,
+                           (slash ? a.sbits : a.vbits) + static_cast<size_t>(g) * a.bm_words, sw);
+    } else if (b < 2 * a.nbw + a.ngb) {
+        gather_vertical(a, g, b - 2 * a.nbw, a.ngb);
+    } else {
+        const int pb = b - 2 * a.nbw - a.ngb;
+        if (pb == 0 && threadIdx.x < 2) a.work[2 * g + threadIdx.x] = 0;
+        plan_block(a.iv, a.kv, a.is, a.ks, a.cap, a.n, a.num_qb, a.list_stride, a.lists, g, pb * 4 + (threadIdx.x >> 5),
+                   a.dense_switch);
     }
 }
 
@@ -941,8 +1060,17 @@ cudaError_t launch_attn(AttnParams& p, int nqb, cudaStream_t stream) {
     vsp_detail::count_launch();
     if (!mc) {
         p.items = nqb * p.npairs;
-        attn_fwd_kernel<kSparse, 1><<<persistent_grid(p.items), kThreads, kSmemBytes, stream>>>(p);
-        return cudaGetLastError();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(persistent_grid(p.items));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = kSparse ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, attn_fwd_kernel<kSparse, 1>, p);
     }
     p.items = nqb * (p.npairs / 2);
     const int clusters = std::max(1, std::min(p.items, persistent_grid(1 << 30) / 2));
@@ -951,13 +1079,15 @@ cudaError_t launch_attn(AttnParams& p, int nqb, cudaStream_t stream) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = kSparse ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, attn_fwd_kernel<kSparse, 2>, p);
 }
 
@@ -1041,22 +1171,32 @@ cudaError_t launch_sparse_impl(const AttnArgs& a, const SparseArgs& s, void* wor
         return cudaErrorInvalidValue;
 
     if (phase & 1) {
-        const size_t words = static_cast<size_t>(bm_words);
-        cudaError_t e = cudaMemsetAsync(bits + static_cast<size_t>(g0) * words, 0, count * words * 4, stream);
-        if (e == cudaSuccess)
-            e = cudaMemsetAsync(bits + (static_cast<size_t>(a.hkv) + g0) * words, 0, count * words * 4, stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(work + 2 * g0, 0, count * 2 * 4, stream);
-        if (e != cudaSuccess) return e;
+        PrepArgs pa{};
+        pa.iv = s.iv;
+        pa.kv = s.kv;
+        pa.is = s.is;
+        pa.ks = s.ks;
+        pa.cap = s.cap;
+        pa.n = a.n;
+        pa.bm_words = bm_words;
+        pa.hkv = a.hkv;
+        pa.kvcap = kvcap;
+        pa.num_qb = num_qb;
+        pa.list_stride = list_stride;
+        pa.g0 = g0;
+        pa.nbw = (bm_words + 127) / 128;
+        pa.ngb = std::max(1, std::min(kvcap / 8, 256));
+        pa.dense_switch = s.dense_switch ? 1 : 0;
+        pa.vbits = bits;
+        pa.sbits = bits + static_cast<size_t>(a.hkv) * bm_words;
+        pa.k = static_cast<const __nv_bfloat16*>(a.k);
+        pa.v = static_cast<const __nv_bfloat16*>(a.v);
+        pa.kg = kg;
+        pa.vg = vg;
+        pa.lists = lists;
+        pa.work = work;
         vsp_detail::count_launch();
-        build_bitmaps_kernel<<<dim3((s.cap + 255) / 256, count), 256, 0, stream>>>(
-            s.iv, s.kv, s.is, s.ks, s.cap, a.n, bm_words, bits, bits + static_cast<size_t>(a.hkv) * bm_words, g0);
-        vsp_detail::count_launch();
-        gather_vertical_kernel<<<dim3(std::min(kvcap / 16, 128), count), 256, 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(a.k), static_cast<const __nv_bfloat16*>(a.v), s.iv, s.kv, s.cap,
-            a.n, a.hkv, kvcap, kg, vg, g0);
-        vsp_detail::count_launch();
-        vs_plan_kernel<<<dim3((num_qb + 3) / 4, count), 128, 0, stream>>>(
-            s.iv, s.kv, s.is, s.ks, s.cap, a.n, num_qb, list_stride, lists, g0);
+        vs_prep_kernel<<<dim3(2 * pa.nbw + pa.ngb + (num_qb + 3) / 4, count), 128, 0, stream>>>(pa);
     }
     if ((phase & 2) && nunits > 0) {
         // one launch over all units: table (KV head, qb_lo, qb_hi, qb prefix) in the workspace

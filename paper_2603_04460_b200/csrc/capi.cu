@@ -237,9 +237,10 @@ int vsp_vs_attn_fwd(vsp_ctx* ctx, const void* q, const void* k, const void* v, i
             if (hflags[g] & 4) return set_err(VSP_EINVAL, "uncovered query row 0");
         }
     }
-    if (flags & ~(VSP_VALIDATE | VSP_O_HEAD_MAJOR)) return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: unknown flags");
+    if (flags & ~(VSP_VALIDATE | VSP_O_HEAD_MAJOR | VSP_DENSE_SWITCH))
+        return set_err(VSP_EINVAL, "vsp_vs_attn_fwd: unknown flags");
     vsp_attn::AttnArgs a{q, k, v, o, lse, n, hq, hkv, scale, (flags & VSP_O_HEAD_MAJOR) != 0};
-    vsp_attn::SparseArgs s{i_v, k_v, i_s, k_s, cap};
+    vsp_attn::SparseArgs s{i_v, k_v, i_s, k_s, cap, (flags & VSP_DENSE_SWITCH) != 0};
     cudaError_t e = vsp_attn::launch_sparse(a, s, workspace, st);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_attn_fwd");
 }
@@ -507,6 +508,7 @@ struct PrefillDev {
     void* o;
     float* lse;
     bool o_head_major;
+    bool dense_switch = false;
 };
 
 int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping, const vsp_budget* budgets,
@@ -602,7 +604,7 @@ cudaError_t enqueue_scoring(const PrefillDev& p, int n, int hq, int hkv, int d, 
         e = vsp_select_k::launch_from_logits(lv, ls, p.a_v, p.a_s, n, hkv, budgets, p.i_v, p.k_v, p.i_s, p.k_s, cap,
                                              ws_sel, st, g0, cnt);
     vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
-    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap, p.dense_switch};
     if (e == cudaSuccess) e = vsp_attn::launch_sparse(aa, sa, ws_attn, st, g0, cnt, 1);
     return e;
 }
@@ -627,7 +629,7 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
     }
     vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
-    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+    vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap, p.dense_switch};
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
         int g0, cnt;
         chunk_range(c, hkv, hpc, g0, cnt);
@@ -669,9 +671,9 @@ extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const 
     int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, heads_per_chunk,
                            "vsp_vs_prefill");
     if (rc) return rc;
-    if (flags & ~VSP_O_HEAD_MAJOR) return set_err(VSP_EINVAL, "vsp_vs_prefill: unknown flags");
+    if (flags & ~(VSP_O_HEAD_MAJOR | VSP_DENSE_SWITCH)) return set_err(VSP_EINVAL, "vsp_vs_prefill: unknown flags");
     PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse,
-                 (flags & VSP_O_HEAD_MAJOR) != 0};
+                 (flags & VSP_O_HEAD_MAJOR) != 0, (flags & VSP_DENSE_SWITCH) != 0};
     cudaError_t e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace,
                                     heads_per_chunk, as_stream(stream), nullptr, nullptr,
                                     nullptr);
@@ -725,7 +727,8 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
     VSP_CHECK_CTX(ctx);
     int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, 0, "vsp_vs_prefill_units");
     if (rc) return rc;
-    if (flags & ~VSP_O_HEAD_MAJOR) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: unknown flags");
+    if (flags & ~(VSP_O_HEAD_MAJOR | VSP_DENSE_SWITCH))
+        return set_err(VSP_EINVAL, "vsp_vs_prefill_units: unknown flags");
     if (nunits < 0 || (nunits > 0 && !units)) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: bad units");
     if (nunits > vsp_attn::kMaxUnits) return set_err(VSP_EINVAL, "vsp_vs_prefill_units: at most 512 units per call");
     const int num_qb = (n + 127) / 128;
@@ -747,7 +750,7 @@ extern "C" int vsp_vs_prefill_units(vsp_ctx* ctx, const void* q, const void* k, 
     cudaStream_t st = as_stream(stream);
     vsp_attn::AttnArgs aa{q, k, v, o, lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)),
                           (flags & VSP_O_HEAD_MAJOR) != 0};
-    vsp_attn::SparseArgs sa{i_v, k_v, i_s, k_s, cap};
+    vsp_attn::SparseArgs sa{i_v, k_v, i_s, k_s, cap, (flags & VSP_DENSE_SWITCH) != 0};
     cudaError_t e = cudaSuccess;
     // score, select and plan each contiguous run of touched heads with one launch per kernel
     for (int g = 0; g < hkv && e == cudaSuccess;) {
@@ -842,7 +845,7 @@ extern "C" int vsp_vs_prefill_host(vsp_ctx* ctx, const void* q_h, const void* k_
         if (e == cudaSuccess)
             e = enqueue_scoring(p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, 0, hkv, main);
         vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), false};
-        vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap};
+        vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap, p.dense_switch};
         void* ws_attn = attn_workspace(workspace, n, hkv, d_h);
         for (int c = 0; c < rc_chunks && e == cudaSuccess; ++c) {
             int lo, hi;

@@ -18,6 +18,10 @@ VSP_DEVICE uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Programmatic dependent launch: a primary grid lets its dependent launch early; the
+// dependent waits for the primary's completion (and memory) before touching its outputs.
+VSP_DEVICE void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+VSP_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 VSP_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
 VSP_DEVICE uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 

@@ -1,10 +1,9 @@
 set -x
 mkdir -p gpurun_out
-timeout 120 ./tools/mma_rate > gpurun_out/mma_rate.json 2>&1
-cat gpurun_out/mma_rate.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" -k regex:attn_fwd_kernel -c 1 -o gpurun_out/prof_k3_bench python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/prof_k3.log 2>&1
 timeout 600 python tools/bench_configs.py c1 c2 c5 > gpurun_out/configs_c125.jsonl 2> gpurun_out/configs.err
 timeout 1200 python tools/dense_anchor.py > gpurun_out/dense_anchor.jsonl 2> gpurun_out/dense_anchor.err
 tail -c 4000 gpurun_out/dense_anchor.jsonl
+cat gpurun_out/configs_c125.jsonl
 ls gpurun_out
