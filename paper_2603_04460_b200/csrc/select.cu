@@ -7,7 +7,8 @@
 //         output ascending
 //   inject_offset_zero(I_s)               (:99-101)
 //
-// One 8-CTA thread-block cluster per (head, direction); each CTA owns a contiguous 1/8 of
+// One 4-CTA thread-block cluster per (head, direction) (8-CTA clusters did not all fit on the
+// GPCs at once: half of them ran in a second wave); each CTA owns a contiguous 1/4 of
 // the n scores, keeps it in shared memory for all passes, the CTAs exchange their radix
 // histograms through distributed shared memory and every CTA takes the same decisions.
 // On the layer path the kernel starts from the indexer's logits and performs the softmax
@@ -19,7 +20,7 @@
 //      u64 fixed point x*2^62 (exact to 2^-62 per element, deterministic integer sums);
 //      the lanes of a warp that share the warp's most common buckets are merged with
 //      full-warp reductions first, so the concentrated score distributions of real layers
-//      do not serialise on one bucket.
+//      do not serialise on one bucket (match.any grouping measured 2x slower).
 //      The crossing value v*, the count and mass strictly above it give k. The first pass
 //      also performs the reference's score validation.
 //   2. exactness guard: the reference sums the sorted doubles sequentially in f64. If our
@@ -45,12 +46,14 @@ namespace vsp_select_k {
 
 namespace cg = cooperative_groups;
 
-constexpr int kCluster = 8;
+#ifndef VSP_SELECT_CLUSTER
+#define VSP_SELECT_CLUSTER 4  // 4-CTA clusters: all (head, direction) clusters co-resident
+#endif
+constexpr int kCluster = VSP_SELECT_CLUSTER;
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;
-constexpr int kMaxHeads = 128;
 constexpr int kMergeRounds = 2;
+constexpr int kMaxHeads = 128;
 constexpr uint32_t kNoBucket = 256u;
 constexpr double kFixScale = 4611686018427387904.0;  // 2^62
 constexpr int kMaxCachedSlice = 36864;                 // floats of one CTA's slice kept in smem
@@ -88,7 +91,7 @@ struct Shared {
     uint32_t loc[kCluster][256]; // per-rank counts of the current pass
     uint32_t rank_above[kCluster];
     uint32_t rank_eq[kCluster];
-    uint32_t scan[64];
+    uint32_t warp_gt[kWarps], warp_eq[kWarps];  // compaction: per-warp counts > T and == T
     unsigned long long red[kWarps];
     double red_d[kWarps];
     float red_f[kWarps];
@@ -98,9 +101,42 @@ struct Shared {
     long long base_pos, eq_base;
 };
 
+#ifdef VSP_SELECT_TRACE
+// Phase probe (tools/k2_trace.py builds a separate library with -DVSP_SELECT_TRACE): globaltimer
+// stamps of every CTA's phase boundaries, [cta][event].
+constexpr int kTraceEvents = 18;  // events: clock64; 16, 17: globaltimer at start / end
+__device__ unsigned long long g_k2_trace[4096 * kTraceEvents];
+#define VSP_K2_TRACE(ev)                                                                                 \
+    do {                                                                                                 \
+        if (threadIdx.x == 0) {                                                                          \
+            const unsigned long long t_ = clock64();                                                     \
+            g_k2_trace[((blockIdx.y * gridDim.x) + blockIdx.x) * kTraceEvents + (ev)] = t_;              \
+        }                                                                                                \
+    } while (0)
+__device__ unsigned long long g_k2_scan[4096 * 8];
+#define VSP_K2_SCAN(ev)                                                                                  \
+    do {                                                                                                 \
+        if (threadIdx.x == 0) g_k2_scan[((blockIdx.y * gridDim.x) + blockIdx.x) * 8 + (ev)] = clock64();  \
+    } while (0)
+#else
+#define VSP_K2_SCAN(ev) \
+    do {                \
+    } while (0)
+#define VSP_K2_TRACE(ev) \
+    do {                 \
+    } while (0)
+#endif
+
 __device__ __forceinline__ unsigned long long to_fix(float x) {
-    // inputs are validated scores in [0, 1]; clamp keeps invalid ones from overflowing 2^64
-    return static_cast<unsigned long long>(__float2ull_rz(fminf(x, 2.0f) * 4611686018427387904.0f));
+    // floor(min(x, 2) * 2^62) from the bit pattern with integer shifts (the float -> u64
+    // conversion is a slow multi-cycle instruction on the histogram loop's critical path);
+    // identical to __float2ull_rz(fminf(x, 2) * 2^62): NaN -> 2^63, negatives -> 0
+    const uint32_t b = __float_as_uint(fminf(x, 2.0f));
+    if (b >> 31) return 0ull;
+    const uint32_t e = b >> 23;
+    const unsigned long long m = (b & 0x7fffffu) | (e ? 0x800000u : 0u);
+    const int sh = static_cast<int>(e ? e : 1u) - 88;  // x * 2^62 = m * 2^(e - 88)
+    return sh >= 0 ? (m << sh) : (sh > -64 ? (m >> -sh) : 0ull);
 }
 
 __device__ __forceinline__ int slice_of(int n, int rank, int& lo, int& hi) {
@@ -198,24 +234,27 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
     __syncwarp();
     const uint32_t hi_mask = (shift + 8 >= 32) ? 0u : (0xffffffffu << (shift + 8));
     int bad = 0, big = 0;
-    const int iters = len > 0 ? (len + kThreads - 1) / kThreads : 0;  // uniform across the CTA
-    for (int it = 0; it < iters; ++it) {
-        const int i = it * kThreads + threadIdx.x;
-        float v = 0.f;
-        uint32_t key = kNoBucket;
-        if (i < len) {
-            v = xs[i];
-            const uint32_t bits = score_bits(v);
-            if (validate) {
-                if (!(v >= 0.f)) bad = 1;
-                else if (v > 1.5f) big = 1;
-            }
-            if ((bits & hi_mask) == (prefix & hi_mask)) key = (bits >> shift) & 255u;
+    // Per-thread two-slot cache of (bucket, count, mass): the elements of one thread mostly
+    // fall into a few buckets (scores concentrate in a few exponents), so the loop is
+    // lane-independent register work; a miss flushes the oldest slot with shared-memory
+    // atomics, and the slots are merged across the warp once at the end.
+    auto flush_atomic = [&](uint32_t key, uint32_t cnt, unsigned long long m) {
+        atomicAdd(&sh.hc[warp][key], cnt);
+        if (with_mass) {
+            // 64-bit add as two native 32-bit adds, the carry from the returned low word (a
+            // 64-bit shared atomic add is a CAS spin loop on this part)
+            uint32_t* h32 = reinterpret_cast<uint32_t*>(&sh.hm[warp][key]);
+            const uint32_t lo = static_cast<uint32_t>(m);
+            const uint32_t old = atomicAdd(h32, lo);
+            const uint32_t hi = static_cast<uint32_t>(m >> 32) + (old + lo < old ? 1u : 0u);
+            if (hi) atomicAdd(h32 + 1, hi);
         }
-        const unsigned long long f = (with_mass && key != kNoBucket) ? to_fix(v) : 0ull;
+    };
+    // lanes sharing the first remaining lane's bucket are merged with full-warp reductions
+    // (mass exact: three 21/21/22-bit pieces summed in u32), at most kMergeRounds times; the
+    // rest go through flush_atomic
+    auto merge_slot = [&](uint32_t key, uint32_t cnt, unsigned long long f) {
         uint32_t rem = __ballot_sync(0xffffffffu, key != kNoBucket);
-        // merge the lanes sharing the first remaining lane's bucket with full-warp reductions
-        // (mass exact: three 21-bit pieces summed in u32), at most kMergeRounds times
 #pragma unroll
         for (int round = 0; round < kMergeRounds; ++round) {
             if (!rem) break;
@@ -223,6 +262,7 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
             const uint32_t k0 = __shfl_sync(0xffffffffu, key, src);
             const bool mine = key == k0;
             const uint32_t grp = __ballot_sync(0xffffffffu, mine);
+            const uint32_t c = __reduce_add_sync(0xffffffffu, mine ? cnt : 0u);
             if (with_mass) {
                 const uint32_t s0 = __reduce_add_sync(0xffffffffu, mine ? static_cast<uint32_t>(f & 0x1fffffu) : 0u);
                 const uint32_t s1 =
@@ -232,23 +272,76 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
                     sh.hm[warp][k0] += static_cast<unsigned long long>(s0) + (static_cast<unsigned long long>(s1) << 21) +
                                        (static_cast<unsigned long long>(s2) << 42);
             }
-            if (lane == src) sh.hc[warp][k0] += __popc(grp);
+            if (lane == src) sh.hc[warp][k0] += c;
             rem &= ~grp;
+            __syncwarp();
         }
+        if ((rem >> lane) & 1u) flush_atomic(key, cnt, f);
         __syncwarp();
-        // the rest (spread buckets, rarely conflicting) go through shared-memory atomics
-        if ((rem >> lane) & 1u) {
-            atomicAdd(&sh.hc[warp][key], 1u);
-            if (with_mass) atomicAdd(&sh.hm[warp][key], f);
-        }
-        __syncwarp();
+    };
+    constexpr int kSlots = 2;
+    constexpr int kBatch = 4;  // elements loaded and keyed together (independent chains), then
+                               // folded into the slots
+    uint32_t ks[kSlots], cs[kSlots];
+    unsigned long long ms[kSlots];
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+        ks[q] = kNoBucket;
+        cs[q] = 0;
+        ms[q] = 0;
     }
+    for (int i0 = threadIdx.x; i0 < len; i0 += kBatch * kThreads) {
+        uint32_t key[kBatch];
+        unsigned long long f[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int i = i0 + u * kThreads;
+            const float v = i < len ? xs[i] : 0.f;
+            const uint32_t bits = score_bits(v);
+            if (validate && i < len) {
+                if (!(v >= 0.f)) bad = 1;
+                else if (v > 1.5f) big = 1;
+            }
+            key[u] = (i < len && (bits & hi_mask) == (prefix & hi_mask)) ? (bits >> shift) & 255u : kNoBucket;
+            f[u] = (with_mass && key[u] != kNoBucket) ? to_fix(v) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            if (key[u] == kNoBucket) continue;
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {  // branch-free hit update
+                const bool h = key[u] == ks[q];
+                cs[q] += h ? 1u : 0u;
+                ms[q] += h ? f[u] : 0ull;
+                hit |= h;
+            }
+            if (!hit) {  // miss: flush the oldest slot, shift, take slot 0
+                if (ks[kSlots - 1] != kNoBucket) flush_atomic(ks[kSlots - 1], cs[kSlots - 1], ms[kSlots - 1]);
+#pragma unroll
+                for (int q = kSlots - 1; q > 0; --q) {
+                    ks[q] = ks[q - 1];
+                    cs[q] = cs[q - 1];
+                    ms[q] = ms[q - 1];
+                }
+                ks[0] = key[u];
+                cs[0] = 1;
+                ms[0] = f[u];
+            }
+        }
+    }
+    if (validate) VSP_K2_TRACE(14);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) merge_slot(ks[q], cs[q], ms[q]);
+    if (validate) VSP_K2_TRACE(15);
     if (validate) {
         bad = __syncthreads_or(bad);
         big = __syncthreads_or(big);
     } else {
         __syncthreads();
     }
+    if (validate) VSP_K2_TRACE(13);
     Exchange& mine = sh.ex[parity];
     if (threadIdx.x < 256) {
         uint32_t c = 0;
@@ -298,6 +391,7 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
 // (or -1) and the totals strictly above it.
 __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long target, bool use_mass,
                          int& bucket, uint32_t& above_cnt, unsigned long long& above_mass) {
+    VSP_K2_SCAN(0);
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         // lane L owns buckets 255-8L ... 248-8L (descending)
@@ -320,6 +414,7 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
                 prem += am;
             }
         }
+        VSP_K2_SCAN(1);
         pre -= seg;
         prec -= segc;
         prem -= segm;
@@ -350,7 +445,9 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
         }
         __syncwarp();
     }
+    VSP_K2_SCAN(2);
     __syncthreads();
+    VSP_K2_SCAN(3);
     bucket = sh.found;
     above_cnt = bucket >= 0 ? static_cast<uint32_t>(sh.red[1]) : 0;
     above_mass = bucket >= 0 ? sh.red[2] : 0;
@@ -365,34 +462,9 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
             sh.rank_eq[warp] = sh.loc[warp][bucket];
         }
     }
+    VSP_K2_SCAN(4);
     __syncthreads();
-}
-
-// Block-wide exclusive scan of one u32 per thread; returns exclusive prefix, total via ref.
-__device__ uint32_t block_scan(uint32_t v, uint32_t* buf, uint32_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t inc = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += a;
-    }
-    if (lane == 31) buf[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < kWarps ? buf[lane] : 0u;
-        uint32_t wi = w;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t a = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += a;
-        }
-        buf[lane] = wi - w;
-        if (lane == 31) buf[32] = wi;
-    }
-    __syncthreads();
-    const uint32_t res = buf[warp] + inc - v;
-    total = buf[32];
-    __syncthreads();
-    return res;
+    VSP_K2_SCAN(5);
 }
 
 template <bool kCached>
@@ -411,6 +483,14 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     const double tau = p.tau[dir][g];
     int lo, hi;
     slice_of(n, rank, lo, hi);
+    VSP_K2_TRACE(0);
+#ifdef VSP_SELECT_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        g_k2_trace[((blockIdx.y * gridDim.x) + blockIdx.x) * kTraceEvents + 16] = t_;
+    }
+#endif
     if (threadIdx.x < kCluster) {
         sh.rank_above[threadIdx.x] = 0;
         sh.rank_eq[threadIdx.x] = 0;
@@ -421,6 +501,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     if (p.logits[dir]) {
         const float* lg = p.logits[dir] + static_cast<size_t>(g) * n;
         if (kCached) load_slice<true>(cache, lg, lo, hi);
+        VSP_K2_TRACE(1);
         cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, const_cast<float*>(x), parity);
     } else {
         if (kCached) load_slice<true>(cache, x, lo, hi);
@@ -429,6 +510,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     }
     const float* xs = kCached ? cache : x + lo;
     const int len = hi - lo;
+    VSP_K2_TRACE(2);
 
     // ---- 1. mass radix-select; pass 0 also validates (sparsity.hpp:60-61)
     const double thr = tau - 1e-12;
@@ -436,9 +518,15 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t prefix = 0, cnt_above = 0;
     unsigned long long mass_above = 0, total_fx = 0;
     bool never = false;
+    // min >= max clamps k to max whatever the mass says (fixed top-k, sparsity.hpp:75-78): only
+    // pass 0 runs (the reference's score checks); the count select reuses its histogram
+    long long up0 = n;
+    if (p.max_b[g] >= 0 && p.max_b[g] < up0) up0 = p.max_b[g];
+    const bool fixed_k = (p.min_b[g] < n ? p.min_b[g] : static_cast<long long>(n)) >= up0;
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         cluster_histogram(sh, cluster, xs, len, prefix, shift, true, pass == 0, parity);
+        VSP_K2_TRACE(3 + 2 * pass);
         if (pass == 0) {
             if (threadIdx.x < 32) {
                 unsigned long long t = 0;
@@ -458,11 +546,13 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
                 cluster.sync();  // no CTA leaves while others may still read its histograms
                 return;
             }
+            if (fixed_k) break;
         }
         int bucket;
         unsigned long long am;
         uint32_t ac;
         scan_top(sh, mass_above, thr_fx, true, bucket, ac, am);
+        VSP_K2_TRACE(4 + 2 * pass);
         if (bucket < 0) {
             never = true;
             break;
@@ -475,7 +565,9 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     bool ambiguous = false;
     // worst-case |reference sequential f64 sum - our exact fixed-point sum|, doubled
     const double k_err = 2.0 * static_cast<double>(n) * (1.1102230246251565e-16 + 2.168404344971009e-19);
-    if (never) {
+    if (fixed_k) {
+        k = up0;
+    } else if (never) {
         // the whole vector's mass stays below the threshold: k = n unless that is within
         // rounding of the reference's sequential sum (then the exact fallback decides)
         k = n;
@@ -546,14 +638,15 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     if (k > upper) k = upper;
 
     // ---- 3. count radix-select for the k-th largest value (only if pass 1 does not give it)
-    if (never || ambiguous || k != k_mass) {
+    if (fixed_k || never || ambiguous || k != k_mass) {
         if (threadIdx.x < kCluster) sh.rank_above[threadIdx.x] = 0;
         __syncthreads();
         prefix = 0;
         uint32_t gt = 0;
         for (int pass = 0; pass < 4; ++pass) {
             const int shift = 24 - 8 * pass;
-            cluster_histogram(sh, cluster, xs, len, prefix, shift, false, false, parity);
+            // pass 0 of a fixed k: the mass pass's histogram (prefix 0, same digit) is in place
+            if (!(fixed_k && pass == 0)) cluster_histogram(sh, cluster, xs, len, prefix, shift, false, false, parity);
             int bucket;
             unsigned long long am;
             uint32_t ac;
@@ -565,6 +658,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     }
     const uint32_t tbits = prefix;
 
+    VSP_K2_TRACE(11);
     // ---- 4. ordered compaction: this CTA's offset from the per-rank counts
     if (threadIdx.x == 0) {
         long long pos = 0, eqb = 0;
@@ -585,49 +679,59 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         zero_sel = (b0 > tbits) || (b0 == tbits && need_eq > 0);
     }
     const int shift_out = (inject && !zero_sel) ? 1 : 0;
-    long long sel_base = sh.base_pos + shift_out;
-    long long eq_base = sh.eq_base;
-    const int chunk = kThreads * kItems;
-    for (int c0 = lo; c0 < hi; c0 += chunk) {
-        const int i0 = c0 + threadIdx.x * kItems;
-        uint32_t bits[kItems];
-        uint32_t n_eq = 0;
-#pragma unroll
-        for (int t = 0; t < kItems; ++t) {
-            const int i = i0 + t;
-            bits[t] = i < hi ? score_bits(xs[i - lo]) : 0u;
-            n_eq += (i < hi && bits[t] == tbits) ? 1u : 0u;
+    // Each warp owns a contiguous run of the slice and walks it 32 elements at a time (lane
+    // order = index order, conflict-free shared loads): a counting walk, one exchange of the
+    // 16 warp totals, then a writing walk whose positions come from ballot prefixes.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lanes_lt = (1u << lane) - 1u;
+    const int per_warp = (((hi - lo) + kWarps - 1) / kWarps + 31) & ~31;
+    const int w_lo = min(hi - lo, warp * per_warp), w_hi = min(hi - lo, w_lo + per_warp);
+    {
+        uint32_t cgt = 0, ceq = 0;
+        for (int b = w_lo; b < w_hi; b += 32) {
+            const int j = b + lane;
+            const uint32_t bits = j < w_hi ? score_bits(xs[j]) : 0u;
+            cgt += __popc(__ballot_sync(0xffffffffu, j < w_hi && bits > tbits));
+            ceq += __popc(__ballot_sync(0xffffffffu, j < w_hi && bits == tbits));
         }
-        uint32_t eq_tot;
-        long long eq_pre = block_scan(n_eq, sh.scan, eq_tot) + eq_base;
-        uint32_t n_sel = 0, flags = 0;
-#pragma unroll
-        for (int t = 0; t < kItems; ++t) {
-            const int i = i0 + t;
-            bool s = false;
-            if (i < hi) {
-                if (bits[t] > tbits) s = true;
-                else if (bits[t] == tbits) {
-                    s = eq_pre < need_eq;
-                    ++eq_pre;
-                }
-            }
-            flags |= (s ? 1u : 0u) << t;
-            n_sel += s ? 1u : 0u;
+        if (lane == 0) {
+            sh.warp_gt[warp] = cgt;
+            sh.warp_eq[warp] = ceq;
         }
-        uint32_t sel_tot;
-        long long pos = block_scan(n_sel, sh.scan, sel_tot) + sel_base;
-#pragma unroll
-        for (int t = 0; t < kItems; ++t)
-            if ((flags >> t) & 1u) out[pos++] = i0 + t;
-        sel_base += sel_tot;
-        eq_base += eq_tot;
+    }
+    __syncthreads();
+    long long eq_run = sh.eq_base, sel_run = sh.base_pos + shift_out;
+    for (int w = 0; w < warp; ++w) {  // ties are taken lowest index first across the warps
+        const long long take = min(static_cast<long long>(sh.warp_eq[w]), max(0ll, need_eq - eq_run));
+        sel_run += sh.warp_gt[w] + take;
+        eq_run += sh.warp_eq[w];
+    }
+    for (int b = w_lo; b < w_hi; b += 32) {
+        const int j = b + lane;
+        const uint32_t bits = j < w_hi ? score_bits(xs[j]) : 0u;
+        const bool gt = j < w_hi && bits > tbits;
+        const bool eq = j < w_hi && bits == tbits;
+        const uint32_t eqm = __ballot_sync(0xffffffffu, eq);
+        const bool take = eq && eq_run + __popc(eqm & lanes_lt) < need_eq;
+        const uint32_t selm = __ballot_sync(0xffffffffu, gt || take);
+        if (gt || take) out[sel_run + __popc(selm & lanes_lt)] = lo + j;
+        eq_run += __popc(eqm);
+        sel_run += __popc(selm);
     }
     if (rank == 0 && threadIdx.x == 0) {
         if (shift_out) out[0] = 0;
         p.cnt[dir][g] = static_cast<int>(k) + shift_out;
     }
+    VSP_K2_TRACE(12);
     cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
+    VSP_K2_TRACE(13);
+#ifdef VSP_SELECT_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        g_k2_trace[((blockIdx.y * gridDim.x) + blockIdx.x) * kTraceEvents + 17] = t_;
+    }
+#endif
 }
 
 // Standalone cluster softmax of logit rows (vsp_indexer_scores): the same code as the
@@ -750,3 +854,12 @@ const int* status_ptr(void* workspace, int n, int hkv) {
 }
 
 }  // namespace vsp_select_k
+
+#ifdef VSP_SELECT_TRACE
+extern "C" __attribute__((visibility("default"))) int vsp_k2_trace_read(void* host, size_t bytes) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, vsp_select_k::g_k2_trace, bytes));
+}
+extern "C" __attribute__((visibility("default"))) int vsp_k2_scan_read(void* host, size_t bytes) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, vsp_select_k::g_k2_scan, bytes));
+}
+#endif
