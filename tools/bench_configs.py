@@ -67,7 +67,8 @@ def c1():
     return {"config": "C1 4k Qwen3-4B geometry, random-init indexer, fixed top-k 256", **r}
 
 
-def trained(n, hq=32, hkv=8, train_prompts=8, val_prompts=4, steps=600, margin=0.035, head_seed=None, seed0=100):
+def trained(n, hq=32, hkv=8, train_prompts=8, val_prompts=4, steps=600, margin=0.035, head_seed=None, seed0=100,
+            aggregate="mean"):
     """The bench's preparation at another size: distil on `train_prompts`, calibrate per-head
     budgets on `val_prompts` other prompts (mean recall >= 0.9 + margin); all prompts differ
     from the timed one."""
@@ -75,7 +76,7 @@ def trained(n, hq=32, hkv=8, train_prompts=8, val_prompts=4, steps=600, margin=0
     params, _ = calibrate.train_indexer(prompts, 1024, steps=steps)
     del prompts
     vals = [planted_layer(n, hq, hkv, seed=seed0 + 1000 + i, head_seed=head_seed)[:3] for i in range(val_prompts)]
-    budget, pt = calibrate.calibrate_budget(vals, params=params, recall_target=0.9 + margin)
+    budget, pt = calibrate.calibrate_budget(vals, params=params, recall_target=0.9 + margin, aggregate=aggregate)
     return params, budget, pt
 
 
@@ -89,24 +90,30 @@ def c2():
             "tau": [[b.tau_v, b.tau_s] for b in budget], **r}
 
 
+C4_MARGIN = float(os.environ.get("C4_MARGIN", "0.03"))
+C4_AGGREGATE = os.environ.get("C4_AGGREGATE", "worst")
+
+
 def c4(layers=36):
     """36 layers at 128k on one GPU: each layer its own heads (head_seed) and prompts; per layer
     the indexer is distilled on 3 training prompts and the budget calibrated on 4 validation
-    prompts for mean recall >= 0.9 + 0.05 (untimed); the timed region runs the 36 layers' paths
+    prompts for recall >= 0.9 + C4_MARGIN, each grid point scored by its worst prompt
+    (C4_AGGREGATE; untimed); the timed region runs the 36 layers' paths
     back to back (inputs regenerated per layer: 36 x 1.6 GB would not fit). Every layer's
     recall is measured exactly on its timed prompt (dense LSE)."""
     n = 131072
     stack = []
     for layer in range(layers):
         hs = 5000 + layer
-        params, budget, _ = trained(n, train_prompts=3, val_prompts=4, steps=300, margin=0.05, head_seed=hs,
-                                    seed0=300 + 17 * layer)
+        params, budget, _ = trained(n, train_prompts=3, val_prompts=4, steps=300, margin=C4_MARGIN, head_seed=hs,
+                                    seed0=300 + 17 * layer, aggregate=C4_AGGREGATE)
         stack.append((params, budget, hs))
     total_ms, dense_ms, recalls, dens = 0.0, 0.0, [], []
     for layer, (params, budget, hs) in enumerate(stack):
         q, k, v, _ = planted_layer(n, 32, 8, seed=2026 + layer, head_seed=hs)
         total_ms += ev_time(lambda: vsp.vs_prefill(q, k, v, params, budget), reps=2)
         o, lse, pat = vsp.vs_prefill(q, k, v, params, budget)
+        vsp.sparse_attention(q, k, v, pat, validate=False)  # the tile statistics read this call's plan
         tiles, dt = vsp.sparse_tile_stats(n, 8, pat.i_v.shape[1], q.device)
         od, lse_d = vsp.blockwise_attention(q, k, v)
         recalls.append(round(float(vsp.attention_recall(lse, lse_d).mean()), 4))
@@ -114,7 +121,8 @@ def c4(layers=36):
         if layer % 6 == 0:
             dense_ms += ev_time(lambda: vsp.blockwise_attention(q, k, v, out=od, lse=lse_d), reps=1) * 6
         del q, k, v, o, od
-    return {"config": f"C4 {layers}-layer stack at 128k, one B200, per-layer distilled indexers and budgets",
+    return {"config": f"C4 {layers}-layer stack at 128k, one B200, per-layer distilled indexers and budgets "
+                      f"(calibration: {C4_AGGREGATE} over 4 prompts, target 0.9 + {C4_MARGIN})",
             "total_ms": total_ms, "tokens_per_s": n / (total_ms * 1e-3), "est_dense_ms": dense_ms,
             "speedup_vs_dense_est": dense_ms / total_ms, "recall_per_layer": recalls,
             "recall_min": min(recalls), "recall_mean": sum(recalls) / len(recalls),
