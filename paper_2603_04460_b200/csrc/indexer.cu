@@ -13,7 +13,9 @@
 // across work items. B = W_U streamed in [32 K-rows x 256 N] MN-major stages (the
 // reference's [2d, d_h] row-major layout, no transpose). tcgen05.mma M=128 N=256 into two
 // TMEM accumulators (double-buffered over 256-wide hidden chunks, continuing across work
-// items) so the SiLU / two-head epilogue of chunk c overlaps the MMA of chunk c+1. The
+// items) so the SiLU / two-head epilogue of chunk c overlaps the MMA of chunk c+1 (16
+// epilogue warps, four per TMEM lane quarter, 64 columns each: 8 warps left the MUFU and
+// tensor pipes ~60 % busy, latency-bound; 16: 466 -> 453 us at 128k x 8 heads). The
 // [n, d_h] activation never leaves the SM: only two fp32 logits per token are written.
 // The softmax over n runs in the selection clusters (select.cu, fp64 normaliser).
 #include <cuda_bf16.h>
@@ -35,7 +37,10 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTok * 256 * 2;             // 64 KB per token tile
 constexpr int kStageBytes = kStageK * kChunkN * 2;  // 16 KB
 constexpr int kMaxDh = 2048;
-constexpr int kThreads = 320;                       // warp0 TMA, warp1 MMA, warps 2-9 epilogue
+constexpr int kEpiParts = 4;                        // epilogue warps per TMEM lane quarter
+constexpr int kEpiWarps = 4 * kEpiParts;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;          // warp0 TMA, warp1 MMA, then the epilogue
 
 struct __align__(64) Params {
     CUtensorMap map_k, map_v, map_w;
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     float* s_bh = reinterpret_cast<float*>(sB + kStages * kStageBytes);  // b_U / 2
     float* s_wv = s_bh + kMaxDh;
     float* s_ws = s_wv + kMaxDh;
-    float* s_xch = s_ws + kMaxDh;              // 2 x 256 floats (tile parity)
+    float* s_xch = s_ws + kMaxDh;              // 2 x (kEpiParts - 1) x 256 floats (tile parity)
     __shared__ Smem sm;
 
     const int num_chunks = p.d_h / kChunkN;
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             mbar_init(&sm.a_full[b], 1);
             mbar_init(&sm.a_empty[b], 1);
             mbar_init(&sm.acc_full[b], 1);
-            mbar_init(&sm.acc_empty[b], 8);
+            mbar_init(&sm.acc_empty[b], kEpiWarps);
         }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
@@ -188,18 +193,18 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         const int part = (warp - 2) >> 2;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        const int et = threadIdx.x - 64;  // 0..255
+        const int et = threadIdx.x - 64;  // 0..kEpiThreads-1
         int cc = 0, j = 0, cur_g = -1;
         for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
             const int g = p.g0 + w / p.tiles;
             const int t = (w % p.tiles) * kTok + r;
             if (g != cur_g) {  // head change: everyone is past the previous tile's exchange
-                for (int i = et; i < p.d_h; i += 256) {
+                for (int i = et; i < p.d_h; i += kEpiThreads) {
                     s_bh[i] = 0.5f * p.b_u[static_cast<size_t>(g) * p.d_h + i];
                     s_wv[i] = p.w_v[static_cast<size_t>(g) * p.d_h + i];
                     s_ws[i] = p.w_s[static_cast<size_t>(g) * p.d_h + i];
                 }
-                named_bar_sync(1, 256);
+                named_bar_sync(1, kEpiThreads);
                 cur_g = g;
             }
             float2 lv = make_float2(0.f, 0.f), ls = make_float2(0.f, 0.f);
@@ -209,13 +214,13 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                 mbar_wait(&sm.acc_full[acc], (cc >> 1) & 1);
                 tc_fence_after();
                 uint32_t ub[2][32];  // ping-pong: the next 32 columns load while these compute
-                tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / 2), ub[0]);
+                tmem_ld32(lane_base + acc * kChunkN + part * (kChunkN / kEpiParts), ub[0]);
                 tmem_wait_ld(ub[0]);
 #pragma unroll
-                for (int q = 0; q < kChunkN / 64; ++q) {
+                for (int q = 0; q < kChunkN / (32 * kEpiParts); ++q) {
                     uint32_t* u = ub[q & 1];
-                    const int col = part * (kChunkN / 2) + q * 32;
-                    if (q + 1 < kChunkN / 64) tmem_ld32(lane_base + acc * kChunkN + col + 32, ub[(q + 1) & 1]);
+                    const int col = part * (kChunkN / kEpiParts) + q * 32;
+                    if (q + 1 < kChunkN / (32 * kEpiParts)) tmem_ld32(lane_base + acc * kChunkN + col + 32, ub[(q + 1) & 1]);
                     const int col0 = c * kChunkN + col;
                     const float4* bh4 = reinterpret_cast<const float4*>(s_bh + col0);
                     const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                         lv1 = ffma2(z1, make_float2(wv.z, wv.w), lv1);
                         ls1 = ffma2(z1, make_float2(ws.z, ws.w), ls1);
                     }
-                    if (q + 1 < kChunkN / 64) tmem_wait_ld(ub[(q + 1) & 1]);
+                    if (q + 1 < kChunkN / (32 * kEpiParts)) tmem_wait_ld(ub[(q + 1) & 1]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -243,16 +248,22 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             }
             const float sv = (lv.x + lv.y) + (lv1.x + lv1.y);
             const float ss = (ls.x + ls.y) + (ls1.x + ls1.y);
-            float* xch = s_xch + (j & 1) * 256;
-            if (part == 1) {
-                xch[r] = sv;
-                xch[128 + r] = ss;
+            float* xch = s_xch + (j & 1) * (kEpiParts - 1) * 256;
+            if (part > 0) {
+                xch[(part - 1) * 256 + r] = sv;
+                xch[(part - 1) * 256 + 128 + r] = ss;
             }
-            named_bar_sync(1, 256);
+            named_bar_sync(1, kEpiThreads);
             if (part == 0 && t < p.n) {
-                p.logit_v[static_cast<size_t>(g) * p.n + t] = sv + xch[r] + p.b_v[g];
+                float tv = sv, ts = ss;
+#pragma unroll
+                for (int q = 0; q < kEpiParts - 1; ++q) {  // fixed order: deterministic sums
+                    tv += xch[q * 256 + r];
+                    ts += xch[q * 256 + 128 + r];
+                }
+                p.logit_v[static_cast<size_t>(g) * p.n + t] = tv + p.b_v[g];
                 const int o = p.reverse ? p.n - 1 - t : t;
-                p.logit_s[static_cast<size_t>(g) * p.n + o] = ss + xch[128 + r] + p.b_s[g];
+                p.logit_s[static_cast<size_t>(g) * p.n + o] = ts + p.b_s[g];
             }
         }
     }
@@ -261,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     if (warp == 1) tmem_free<512>(tmem);
 }
 
-constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 512 * 4 + 1024;
+constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 2 * (kEpiParts - 1) * 256 * 4 + 1024;
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
     return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;
