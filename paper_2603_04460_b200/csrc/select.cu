@@ -30,10 +30,10 @@
 //      verbatim: bitonic sort of the scores in scratch, then a sequential f64 sum.
 //   3. only when min/max clamping or the fallback moved k: count radix-select for the k-th
 //      largest value T (otherwise T = v* and the ties to take follow from pass 1).
-//   4. ordered compaction: per-CTA counts of elements above T and equal to T are known from
-//      the exchanged histograms, so each CTA writes its slice's indices ascending at its
-//      own offset (two block scans per chunk), ties to T lowest index first; offset 0 is
-//      injected for slash.
+//   4. ordered compaction: per-CTA and per-warp counts of elements above T and equal to T
+//      are known from the radix passes (the histogram loops walk the same warp-contiguous
+//      runs), so each warp writes its run's indices ascending at its own offset with ballot
+//      prefixes, ties to T lowest index first; offset 0 is injected for slash.
 #include <cuda_runtime.h>
 
 #include <cooperative_groups.h>
@@ -156,35 +156,44 @@ __device__ void cluster_softmax(Shared& sh, cg::cluster_group& cluster, const fl
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int len = hi - lo;
     auto src = [&](int i) { return kCached ? xs[i] : __ldg(logits + lo + i); };
+    // ONE cluster exchange: each CTA publishes its slice's max m_r and fp64 sum
+    // s_r = sum exp(x - m_r); the global max is M = max m_r and the normaliser
+    // sum_r s_r * exp(m_r - M) (fp64) — the same terms as sum exp(x - M), regrouped per CTA
     float mx = -INFINITY;
     for (int i = threadIdx.x; i < len; i += kThreads) mx = fmaxf(mx, src(i));
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) sh.red_f[warp] = mx;
     __syncthreads();
-    Exchange& e1 = sh.ex[parity];
-    if (threadIdx.x == 0) {
-        float v = -INFINITY;
-        for (int w = 0; w < kWarps; ++w) v = fmaxf(v, sh.red_f[w]);
-        e1.mx = v;
-    }
-    cluster.sync();
-    float m = -INFINITY;
-    for (int r = 0; r < kCluster; ++r) m = fmaxf(m, cluster.map_shared_rank(&e1, r)->mx);
-    parity ^= 1;
+    float mloc = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) mloc = fmaxf(mloc, sh.red_f[w]);
     double s = 0.0;
-    for (int i = threadIdx.x; i < len; i += kThreads) s += static_cast<double>(expf(src(i) - m));
+    for (int i = threadIdx.x; i < len; i += kThreads) s += static_cast<double>(expf(src(i) - mloc));
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) sh.red_d[warp] = s;
     __syncthreads();
-    Exchange& e2 = sh.ex[parity];
+    Exchange& e1 = sh.ex[parity];
     if (threadIdx.x == 0) {
         double v = 0.0;
         for (int w = 0; w < kWarps; ++w) v += sh.red_d[w];
-        e2.sum = v;
+        e1.mx = mloc;
+        e1.sum = v;
     }
     cluster.sync();
+    float m = -INFINITY;
+    float mr[kCluster];
+    double sr[kCluster];
+#pragma unroll
+    for (int r = 0; r < kCluster; ++r) {
+        const Exchange* e = cluster.map_shared_rank(&e1, r);
+        mr[r] = e->mx;
+        sr[r] = e->sum;
+        m = fmaxf(m, mr[r]);
+    }
     double tot = 0.0;
-    for (int r = 0; r < kCluster; ++r) tot += cluster.map_shared_rank(&e2, r)->sum;
+#pragma unroll
+    for (int r = 0; r < kCluster; ++r)  // fixed rank order: every CTA (and both callers) agree
+        if (sr[r] > 0.0) tot += sr[r] * exp(static_cast<double>(mr[r]) - static_cast<double>(m));
     parity ^= 1;
     const double inv = 1.0 / tot;
     if (threadIdx.x == 0) sh.x0 = __float_as_uint(static_cast<float>(static_cast<double>(expf(__ldg(logits) - m)) * inv));
@@ -210,6 +219,15 @@ __device__ void load_slice(float* xs, const float* __restrict__ x, int lo, int h
     }
     for (; i < len; i += kThreads) xs[i] = __ldg(x + lo + i);
     __syncthreads();
+}
+
+// Contiguous element run of warp w in a slice of len elements (a multiple of 32 per warp):
+// the histogram loops and the compaction use the same runs, so per-warp bucket counts are
+// the compaction's per-warp counts.
+__device__ __forceinline__ void warp_range(int len, int w, int& w_lo, int& w_hi) {
+    const int per_warp = ((len + kWarps - 1) / kWarps + 31) & ~31;
+    w_lo = min(len, w * per_warp);
+    w_hi = min(len, w_lo + per_warp);
 }
 
 // Ordering key of a (validated, non-negative) score: its fp32 bit pattern, with -0.0 folded
@@ -290,19 +308,22 @@ __device__ void cluster_histogram(Shared& sh, cg::cluster_group& cluster, const 
         cs[q] = 0;
         ms[q] = 0;
     }
-    for (int i0 = threadIdx.x; i0 < len; i0 += kBatch * kThreads) {
+    // each warp owns a contiguous run of the slice (the compaction's order), lanes interleaved
+    int w_lo, w_hi;
+    warp_range(len, warp, w_lo, w_hi);
+    for (int i0 = w_lo + lane; i0 < w_hi; i0 += kBatch * 32) {
         uint32_t key[kBatch];
         unsigned long long f[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
-            const int i = i0 + u * kThreads;
-            const float v = i < len ? xs[i] : 0.f;
+            const int i = i0 + u * 32;
+            const float v = i < w_hi ? xs[i] : 0.f;
             const uint32_t bits = score_bits(v);
-            if (validate && i < len) {
+            if (validate && i < w_hi) {
                 if (!(v >= 0.f)) bad = 1;
                 else if (v > 1.5f) big = 1;
             }
-            key[u] = (i < len && (bits & hi_mask) == (prefix & hi_mask)) ? (bits >> shift) & 255u : kNoBucket;
+            key[u] = (i < w_hi && (bits & hi_mask) == (prefix & hi_mask)) ? (bits >> shift) & 255u : kNoBucket;
             f[u] = (with_mass && key[u] != kNoBucket) ? to_fix(v) : 0ull;
         }
 #pragma unroll
@@ -451,8 +472,18 @@ __device__ void scan_top(Shared& sh, unsigned long long base, unsigned long long
     bucket = sh.found;
     above_cnt = bucket >= 0 ? static_cast<uint32_t>(sh.red[1]) : 0;
     above_mass = bucket >= 0 ? sh.red[2] : 0;
-    // per-rank counts strictly above the chosen bucket, and (last pass) equal to it
+    // per-rank counts strictly above the chosen bucket, and (last pass) equal to it; per warp
+    // the same from its private histogram (this pass's elements of its run)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (bucket >= 0) {
+        uint32_t s = 0;
+        for (int b = bucket + 1 + lane; b < 256; b += 32) s += sh.hc[warp][b];
+        s = __reduce_add_sync(0xffffffffu, s);
+        if (lane == 0) {
+            sh.warp_gt[warp] += s;
+            sh.warp_eq[warp] = sh.hc[warp][bucket];
+        }
+    }
     if (bucket >= 0 && warp < kCluster) {
         uint32_t s = 0;
         for (int b = bucket + 1 + lane; b < 256; b += 32) s += sh.loc[warp][b];
@@ -494,6 +525,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x < kCluster) {
         sh.rank_above[threadIdx.x] = 0;
         sh.rank_eq[threadIdx.x] = 0;
+    }
+    if (threadIdx.x < kWarps) {
+        sh.warp_gt[threadIdx.x] = 0;
+        sh.warp_eq[threadIdx.x] = 0;
     }
     __syncthreads();
     int parity = 0;
@@ -640,6 +675,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     // ---- 3. count radix-select for the k-th largest value (only if pass 1 does not give it)
     if (fixed_k || never || ambiguous || k != k_mass) {
         if (threadIdx.x < kCluster) sh.rank_above[threadIdx.x] = 0;
+        if (threadIdx.x < kWarps) sh.warp_gt[threadIdx.x] = 0;
         __syncthreads();
         prefix = 0;
         uint32_t gt = 0;
@@ -679,27 +715,13 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         zero_sel = (b0 > tbits) || (b0 == tbits && need_eq > 0);
     }
     const int shift_out = (inject && !zero_sel) ? 1 : 0;
-    // Each warp owns a contiguous run of the slice and walks it 32 elements at a time (lane
-    // order = index order, conflict-free shared loads): a counting walk, one exchange of the
-    // 16 warp totals, then a writing walk whose positions come from ballot prefixes.
+    // Each warp owns a contiguous run of the slice (warp_range) and walks it 32 elements at a
+    // time (lane order = index order, conflict-free shared loads); its counts above / equal to
+    // T came with the radix passes (scan_top), so positions follow from ballot prefixes.
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lanes_lt = (1u << lane) - 1u;
-    const int per_warp = (((hi - lo) + kWarps - 1) / kWarps + 31) & ~31;
-    const int w_lo = min(hi - lo, warp * per_warp), w_hi = min(hi - lo, w_lo + per_warp);
-    {
-        uint32_t cgt = 0, ceq = 0;
-        for (int b = w_lo; b < w_hi; b += 32) {
-            const int j = b + lane;
-            const uint32_t bits = j < w_hi ? score_bits(xs[j]) : 0u;
-            cgt += __popc(__ballot_sync(0xffffffffu, j < w_hi && bits > tbits));
-            ceq += __popc(__ballot_sync(0xffffffffu, j < w_hi && bits == tbits));
-        }
-        if (lane == 0) {
-            sh.warp_gt[warp] = cgt;
-            sh.warp_eq[warp] = ceq;
-        }
-    }
-    __syncthreads();
+    int w_lo, w_hi;
+    warp_range(hi - lo, warp, w_lo, w_hi);
     long long eq_run = sh.eq_base, sel_run = sh.base_pos + shift_out;
     for (int w = 0; w < warp; ++w) {  // ties are taken lowest index first across the warps
         const long long take = min(static_cast<long long>(sh.warp_eq[w]), max(0ll, need_eq - eq_run));
