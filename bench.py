@@ -555,9 +555,11 @@ def main():
         local = local % int(os.environ["VSP_BENCH_DEVICES"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("VSP_BENCH_BACKEND", "nccl")
+    # cross-rank reductions of host-side numbers: on the GPU for NCCL, on the CPU for gloo
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("VSP_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     balanced = args.shard in ("balanced", "spread")
     assert balanced or args.hkv % world == 0, "KV heads must divide across ranks"
@@ -647,10 +649,7 @@ def main():
         vsp.attn_timing(False, dev)
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    t_max = torch.tensor([ms], device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
-    ms_step = float(t_max.item())
+    ms_step = parallel.max_over_ranks(ms, red_dev) if world > 1 else ms
 
     # ---- component timings (same heads, untimed by the contract, for the roofline)
     def timed(fn, reps=3):
@@ -696,7 +695,7 @@ def main():
 
     # ---- output assembly over NCCL, reported separately (not inside the step)
     allgather_ms = None
-    if world > 1:
+    if world > 1 and backend == "nccl":
         comm = parallel.VspComm(dev)
         if balanced:  # unit regions broadcast by their owners (vsp_assemble_units)
             vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
@@ -705,6 +704,18 @@ def main():
             allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
         allgather_ms = parallel.max_over_ranks(allgather_ms, dev)
         comm.close()
+    elif world > 1:  # shared-GPU test mode (VSP_BENCH_DEVICES, gloo): CPU-staged assembly
+        o_c, l_c = o_full.cpu(), lse_full.cpu()
+        if balanced:
+            parallel.assemble_units(o_c, l_c, all_units, args.hkv)
+        else:
+            lo_h, hi_h = parallel.head_range(args.hq, rank, world)
+            for t in (o_c, l_c):
+                parts = list(t.chunk(world, 0))
+                torch.distributed.all_gather(parts, t[lo_h:hi_h].clone())
+                t.copy_(torch.cat(parts, 0))
+        o_full.copy_(o_c)
+        lse_full.copy_(l_c)
 
     # ---- e2e through the public API with host buffers (H2D inputs, D2H output every step)
     e2e = None
@@ -746,13 +757,12 @@ def main():
             e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": n / (float(e2e_ms.item()) * 1e-3), "unit": "tokens/s",
+        e2e_t = a.elapsed_time(b) / args.steps
+        e2e_t = parallel.max_over_ranks(e2e_t, red_dev) if world > 1 else e2e_t
+        e2e = {"value": n / (e2e_t * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2),
                "d2h_bytes_per_step": int(d2h_units if balanced else oh_.numel() * 2 + lse_h.numel() * 4),
-               "ms_per_step": float(e2e_ms.item()),
+               "ms_per_step": float(e2e_t),
                "api": ("vs_prefill_units (pinned host Q/K/V in, this rank's O/LSE regions out)" if balanced else
                        "vsp_vs_prefill_host (pinned host Q/K/V in, host O/LSE out)"),
                "heads_per_chunk": args.e2e_heads_per_chunk}
