@@ -154,7 +154,26 @@ __device__ void cluster_softmax(Shared& sh, cg::cluster_group& cluster, const fl
     // s_r = sum exp(x - m_r); the global max is M = max m_r and the normaliser
     // sum_r s_r * exp(m_r - M) (fp64) — the same terms as sum exp(x - M), regrouped per CTA
     float mx = -INFINITY;
-    for (int i = threadIdx.x; i < len; i += kThreads) mx = fmaxf(mx, src(i));
+    if (kCached) {  // fill this CTA's slice cache from global while taking the max (one pass)
+        int i = threadIdx.x;
+        for (; i + 3 * kThreads < len; i += 4 * kThreads) {
+            const float a = __ldg(logits + lo + i), b = __ldg(logits + lo + i + kThreads),
+                        c = __ldg(logits + lo + i + 2 * kThreads), d = __ldg(logits + lo + i + 3 * kThreads);
+            xs[i] = a;
+            xs[i + kThreads] = b;
+            xs[i + 2 * kThreads] = c;
+            xs[i + 3 * kThreads] = d;
+            mx = fmaxf(mx, fmaxf(fmaxf(a, b), fmaxf(c, d)));
+        }
+        for (; i < len; i += kThreads) {
+            const float a = __ldg(logits + lo + i);
+            xs[i] = a;
+            mx = fmaxf(mx, a);
+        }
+        // the next pass reads back only this thread's own elements (same i pattern)
+    } else {
+        for (int i = threadIdx.x; i < len; i += kThreads) mx = fmaxf(mx, src(i));
+    }
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) sh.red_f[warp] = mx;
     __syncthreads();
@@ -520,6 +539,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
         sh.rank_above[threadIdx.x] = 0;
         sh.rank_eq[threadIdx.x] = 0;
     }
+    if (threadIdx.x == 0) {
+        sh.bad = 0;
+        sh.big = 0;
+    }
     if (threadIdx.x < kWarps) {
         sh.warp_gt[threadIdx.x] = 0;
         sh.warp_eq[threadIdx.x] = 0;
@@ -529,7 +552,6 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     // this CTA's slice of the scores: shared memory when it fits, else global (L2)
     if (p.logits[dir]) {
         const float* lg = p.logits[dir] + static_cast<size_t>(g) * n;
-        if (kCached) load_slice<true>(cache, lg, lo, hi);
         VSP_K2_TRACE(1);
         cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, const_cast<float*>(x), parity);
     } else {
@@ -554,7 +576,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     const bool fixed_k = (p.min_b[g] < n ? p.min_b[g] : static_cast<long long>(n)) >= up0;
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
-        cluster_histogram(sh, cluster, xs, len, prefix, shift, true, pass == 0, parity);
+        // per-element score checks only for caller-supplied scores: the logits path's scores
+        // come from the softmax above (non-negative, <= 1 by construction); the sum check
+        // below uses the histogram's exact total either way
+        cluster_histogram(sh, cluster, xs, len, prefix, shift, true, pass == 0 && !p.logits[dir], parity);
         VSP_K2_TRACE(3 + 2 * pass);
         if (pass == 0) {
             if (threadIdx.x < 32) {
@@ -767,7 +792,6 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
     int lo, hi;
     slice_of(n, rank, lo, hi);
     int parity = 0;
-    if (kCached) load_slice<true>(cache, lg, lo, hi);
     cluster_softmax<kCached>(sh, cluster, lg, cache, lo, hi, out, parity);
     cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
