@@ -36,6 +36,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# A/B hook: VSP_ROOT=<dir> benches the package copy under <dir> (same inputs, same process setup)
+if os.environ.get("VSP_ROOT"):
+    sys.path.insert(0, os.path.abspath(os.environ["VSP_ROOT"]))
 if ROOT not in sys.path:  # tools may put another build of the package ahead (A/B)
     sys.path.insert(0, ROOT)
 

@@ -67,6 +67,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+#ifndef VSP_POLY_MASK
+#define VSP_POLY_MASK 0x5454u  // exp2 pairs (of 16 per 32-column chunk) evaluated by the FMA-pipe polynomial
+#endif
+
 constexpr int kItemRing = 2;
 constexpr int kItemConsumers = 9;  // MMA warp + 8 softmax warps
 
@@ -213,7 +217,7 @@ VSP_DEVICE void softmax_tile(uint32_t s_t, uint32_t o_t, uint32_t dead, uint32_t
                                                        __uint_as_float(u[c][2 * t + 1])),
                                            scl, neg_m);
                     float2 e;
-                    if ((0x5454u >> t) & 1u) {  // 3 pairs in 8 on the FMA pipe (MUFU/FMA balance)
+                    if ((VSP_POLY_MASK >> t) & 1u) {  // 3 pairs in 8 on the FMA pipe (MUFU/FMA balance)
                         e = exp2_poly2(y);
                     } else {
                         e.x = ex2_approx(y.x);
