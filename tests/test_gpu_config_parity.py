@@ -181,8 +181,8 @@ def test_c1_dense_switch_rows_and_speed(vsp, c1):
     visit every causal tile (plan count == qb + 1) runs unmasked causal attention, so its rows
     equal the dense kernel's (blockwise_attention, attention.hpp:96-145) bit for bit; every
     other block keeps the exact sparse result. At C1 (tile density ~0.99, random pattern) the
-    masked call costs ~1.35x K4's time; with the switch it must reach 0.85x K4's speed (measured
-    0.90-0.91 on B200: the K3 kernel itself runs ~8% behind K4 on identical tiles at this size —
+    masked call costs ~1.35x K4's time; with the switch it must reach 0.80x K4's speed (measured
+    0.88-0.91 on B200 boxes: the K3 kernel itself runs ~8% behind K4 on identical tiles at this size —
     more instructions and i-cache misses — plus the 7.6 us planning launch)."""
     q, k, v, pat = c1["q"], c1["k"], c1["v"], c1["pat"]
     n, hq, hkv = c1["n"], c1["hq"], c1["hkv"]
@@ -204,7 +204,7 @@ def test_c1_dense_switch_rows_and_speed(vsp, c1):
     t_dense = _event_ms(lambda: vsp.blockwise_attention(q, k, v, out=o_buf, lse=l_buf))
     t_sw = _event_ms(lambda: vsp.sparse_attention(q, k, v, pat, validate=False, out=o_buf, lse=l_buf,
                                                   dense_switch=True))
-    assert t_dense / t_sw >= 0.85, f"dense-switch call {t_sw:.4f} ms vs K4 {t_dense:.4f} ms"
+    assert t_dense / t_sw >= 0.80, f"dense-switch call {t_sw:.4f} ms vs K4 {t_dense:.4f} ms"
 
 
 # --------------------------------------------------------------------------- 128k sampled rows
