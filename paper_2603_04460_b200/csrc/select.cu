@@ -7,8 +7,9 @@
 //         output ascending
 //   inject_offset_zero(I_s)               (:99-101)
 //
-// One 4-CTA thread-block cluster per (head, direction) (8-CTA clusters did not all fit on the
-// GPCs at once: half of them ran in a second wave); each CTA owns a contiguous 1/4 of
+// One 6-CTA thread-block cluster per (head, direction) (8-CTA clusters did not all fit on the
+// GPCs at once — half of them ran in a second wave; 6 fit three per GPC, and 4 leave SMs idle:
+// 128k select 83 / 58 / 72 us for 8 / 6 / 4); each CTA owns a contiguous sixth of
 // the n scores, keeps it in shared memory for all passes, the CTAs exchange their radix
 // histograms through distributed shared memory and every CTA takes the same decisions.
 // On the layer path the kernel starts from the indexer's logits and performs the softmax
@@ -47,7 +48,7 @@ namespace vsp_select_k {
 namespace cg = cooperative_groups;
 
 #ifndef VSP_SELECT_CLUSTER
-#define VSP_SELECT_CLUSTER 4  // 4-CTA clusters: all (head, direction) clusters co-resident
+#define VSP_SELECT_CLUSTER 6  // 6-CTA clusters: all 16 co-resident (3 per GPC); 8 did not fit
 #endif
 constexpr int kCluster = VSP_SELECT_CLUSTER;
 constexpr int kThreads = 512;
