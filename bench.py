@@ -90,6 +90,8 @@ def parse(argv=None):
     ap.add_argument("--shard", choices=["auto", "heads", "balanced", "spread"], default="auto",
                     help="multi-GPU split: KV heads (north star; auto), or cost-balanced (KV head, query-block) "
                          "units with replicated inputs, or spread (every head split across the ranks)")
+    ap.add_argument("--head-placement", choices=["cost", "contiguous"], default="cost",
+                    help="heads split at N>1: whole KV heads placed by predicted cost (default) or contiguous slabs")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
     ap.add_argument("--e2e-heads-per-chunk", type=int, default=0)
@@ -387,7 +389,10 @@ def workload_config(args, world, budgets, info) -> dict:
         "inputs": ("planted vertical-slash synthetic layer (synth.py, seed %d, drawn on the CPU), resident in HBM; "
                    "Q is 1.07 GB > L2 so no flush between steps" % args.seed),
         "parallelism": (f"{'spread' if args.shard == 'spread' else 'balanced'} units x{world} (replicated inputs, "
-                        f"static cost table from a validation prompt)" if balanced else f"kv-head shard x{world}"),
+                        f"static cost table from a validation prompt)" if balanced else
+                        f"kv-head shard x{world}" + (" (whole KV heads placed by the predicted cost of a validation "
+                                                     "prompt, equal counts)" if world > 1 and args.head_placement == "cost"
+                                                     else "")),
     }
 
 
@@ -576,11 +581,26 @@ def main():
     params_full, budgets_full, prep_info = obtain_prep(args, dev)
     srank, sworld = (0, 1) if balanced else (rank, world)
     hq_r, hkv_r = args.hq // sworld, args.hkv // sworld
-    params = vsp.IndexerParams(*[shard(getattr(params_full, f), srank, sworld, 0)
-                                 for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
     mx = None if args.max_budget < 0 else args.max_budget
-    budget = [vsp.BudgetConfig(tv, ts, args.min_budget, mx)
-              for tv, ts in budgets_full[srank * hkv_r:(srank + 1) * hkv_r]]
+    # heads split at N > 1: whole KV heads, equal counts, placed by the predicted cost of a
+    # validation prompt (parallel.balanced_head_sets); my_kv = this rank's KV heads
+    head_sets = None
+    my_kv = list(range(srank * hkv_r, (srank + 1) * hkv_r))
+    if not balanced and world > 1 and args.head_placement == "cost":
+        qv, kv_, vv = synth_layer(args, dev, seed=args.seed + 201)
+        budget_all = [vsp.BudgetConfig(tv, ts, args.min_budget, mx) for tv, ts in budgets_full]
+        a_v, a_s = vsp.indexer_forward(kv_, vv, params_full)
+        pat_v = vsp.select_pattern(a_v, a_s, budget_all)
+        vsp.sparse_attention(qv, kv_, vv, pat_v, validate=False)
+        head_cost = vsp.sparse_tile_counts(n, args.hkv, pat_v.i_v.shape[1], dev).sum(dim=1).double() + 2500.0
+        del qv, kv_, vv, a_v, a_s, pat_v
+        head_sets = parallel.balanced_head_sets(head_cost.cpu(), world)
+        my_kv = head_sets[rank]
+    kv_idx = torch.tensor(my_kv, dtype=torch.long)
+    q_idx = torch.tensor(parallel.q_heads_of(my_kv, grp), dtype=torch.long)
+    params = vsp.IndexerParams(*[getattr(params_full, f).index_select(0, kv_idx.to(getattr(params_full, f).device))
+                                 .contiguous() for f in ("w_u", "b_u", "w_v", "b_v", "w_s", "b_s")])
+    budget = [vsp.BudgetConfig(*budgets_full[g], args.min_budget, mx) for g in my_kv]
     units = all_units = None
     if balanced:
         # static cost table: per (head, block) tiles of a validation prompt (not the timed one)
@@ -595,9 +615,9 @@ def main():
         units = all_units[rank]
     # the timed prompt, drawn on the CPU (the reference arm draws the identical layer)
     q_host, k_host, v_host = synth_layer(args, "cpu")
-    q = shard(q_host, srank, sworld, 1).to(dev)
-    k = shard(k_host, srank, sworld, 1).to(dev)
-    v = shard(v_host, srank, sworld, 1).to(dev)
+    q = q_host.index_select(1, q_idx).contiguous().to(dev)
+    k = k_host.index_select(1, kv_idx).contiguous().to(dev)
+    v = v_host.index_select(1, kv_idx).contiguous().to(dev)
     if not (rank == 0 and world == 1 and not args.no_cpu_baseline):
         del q_host, k_host, v_host
     # O is written head-major straight into this rank's slab of the full [Hq, n, d] output
@@ -703,8 +723,19 @@ def main():
         if balanced:  # unit regions broadcast by their owners (vsp_assemble_units)
             vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
             allgather_ms = timed(lambda: comm.assemble_units(o_full, lse_full, all_units, args.hkv), reps=3)
-        else:  # one in-place ncclAllGather of the head-major slabs (O and LSE)
+        elif head_sets is None:  # one in-place ncclAllGather of the head-major slabs (O and LSE)
             allgather_ms = timed(lambda: comm.allgather_heads(o_full, lse_full), reps=3)
+        else:  # slabs in placement order, then one permutation into head order
+            perm = torch.tensor([q for hs in head_sets for q in parallel.q_heads_of(hs, grp)], device=dev)
+            o_out = torch.empty_like(o_full)
+            lse_out = torch.empty_like(lse_full)
+
+            def assemble():
+                comm.allgather_heads(o_full, lse_full)
+                o_out.index_copy_(0, perm, o_full)
+                lse_out.index_copy_(0, perm, lse_full)
+
+            allgather_ms = timed(assemble, reps=3)
         allgather_ms = parallel.max_over_ranks(allgather_ms, dev)
         comm.close()
     elif world > 1:  # shared-GPU test mode (VSP_BENCH_DEVICES, gloo): CPU-staged assembly

@@ -10,6 +10,10 @@ in-place ncclAllGather over NVLink/NVSwitch through the C ABI (vsp_allgather_hea
 permute and no staging copy. `assemble_heads` is the torch.distributed equivalent for a
 token-major shard.
 
+Cost-aware head placement (`balanced_head_sets`): the heads split keeps whole KV heads and
+equal head counts per rank, but places them by predicted cost instead of in contiguous
+slabs; O is then all-gathered in the placement order and permuted once.
+
 Balanced split (SURVEY.md §8e refinement, `balanced_units`): adaptive per-head budgets make
 KV heads unequal — in the 128k bench one head carries ~40% of the tiles, so 8-way head
 sharding would run at ~2.5x instead of 8x. With replicated Q/K/V, the (KV head, query
@@ -156,6 +160,32 @@ def assemble_units(o_full: torch.Tensor, lse_full: Optional[torch.Tensor], all_u
         dist.broadcast(reg, src=src, group=group)  # contiguous: head-major rows of one head
         if lse_full is not None:
             dist.broadcast(lse_full[h, lo:hi], src=src, group=group)
+
+
+def balanced_head_sets(head_cost, world: int) -> List[List[int]]:
+    """KV-head sharding with cost-aware placement: every rank gets hkv / world WHOLE KV heads
+    (the all-gather slabs stay equal), chosen so the most expensive rank is as cheap as the
+    greedy longest-first rule makes it (heads by descending cost, each to the cheapest rank
+    that still has room; ties to the lower rank). head_cost: predicted cost per KV head
+    (e.g. tile counts of a calibration prompt plus a per-head overhead). Deterministic, so
+    every rank computes the same sets. Returns per rank its heads, ascending."""
+    costs = [float(c) for c in (head_cost.tolist() if hasattr(head_cost, "tolist") else head_cost)]
+    hkv = len(costs)
+    if hkv % world:
+        raise ValueError(f"{hkv} KV heads do not split across {world} ranks")
+    per = hkv // world
+    load = [0.0] * world
+    sets: List[List[int]] = [[] for _ in range(world)]
+    for g in sorted(range(hkv), key=lambda h: (-costs[h], h)):
+        r = min((r for r in range(world) if len(sets[r]) < per), key=lambda r: (load[r], r))
+        sets[r].append(g)
+        load[r] += costs[g]
+    return [sorted(x) for x in sets]
+
+
+def q_heads_of(kv_heads: List[int], grp: int) -> List[int]:
+    """The Q heads (GQA groups of size grp) of the given KV heads, in order."""
+    return [g * grp + j for g in kv_heads for j in range(grp)]
 
 
 def balanced_units(cost, world: int, cta_overhead: float = 2.0, head_overhead: float = 2500.0

@@ -295,3 +295,18 @@ def test_merge_path_partition_c_abi_matches_reference():
             sa, sb = a[cuts[s][0]:cuts[s + 1][0]], b[cuts[s][1]:cuts[s + 1][1]]
             merged += sorted(list(sa) + list(sb), key=lambda x: x)  # equal keys: values identical
         assert merged == sorted(list(a) + list(b))
+
+
+def test_balanced_head_sets_equal_counts_and_balance():
+    """Cost-aware KV-head placement: equal counts per rank, every head once, and never a worse
+    maximum than contiguous slabs on the round-2 bench costs (tiles per KV head)."""
+    from paper_2603_04460_b200 import parallel
+    costs = [12320, 3069, 3069, 5269, 3069, 38092, 73503, 13852]
+    for world in (1, 2, 4, 8):
+        sets = parallel.balanced_head_sets(costs, world)
+        assert sorted(h for s_ in sets for h in s_) == list(range(8))
+        assert all(len(s_) == 8 // world for s_ in sets)
+        best = max(sum(costs[h] for h in s_) for s_ in sets)
+        contig = max(sum(costs[r * (8 // world):(r + 1) * (8 // world)]) for r in range(world))
+        assert best <= contig
+    assert parallel.q_heads_of([1, 3], 4) == [4, 5, 6, 7, 12, 13, 14, 15]

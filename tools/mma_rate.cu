@@ -9,7 +9,7 @@
 
 using namespace vsp_sm100;
 
-__global__ void __launch_bounds__(128, 1) rate_kernel(int n_mma, int N, int ts, unsigned long long* out) {
+__global__ void __launch_bounds__(128, 1) rate_kernel(int n_mma, int N, int ts, unsigned long long* out, int bmn = 0) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar;
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int n_mma, int N, int ts, 
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
     if (warp == 0) {
-        const uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+        const uint32_t idesc = umma_idesc_bf16(128, N, false, bmn != 0);
         const uint64_t a = umma_desc_sw128(smem_u32(smem), 16, 1024);
         const uint64_t b = umma_desc_sw128(smem_u32(smem + 32768), 16, 1024);
         unsigned long long t0 = 0, t1 = 0;
@@ -61,17 +61,18 @@ int main() {
     const int n_mma = 20000;
     printf("{\"probe\": \"tcgen05.mma M=128 cta_group::1 bf16, back-to-back into one accumulator, %d instr, %d CTAs\", \"rows\": [", n_mma, sms);
     bool first = true;
-    for (int ts = 0; ts < 2; ++ts)
+    for (int mode = 0; mode < 4; ++mode)
         for (int N : {16, 32, 64, 96, 128, 192, 256}) {
-            rate_kernel<<<sms, 128, smem>>>(n_mma, N, ts, d);
-            rate_kernel<<<sms, 128, smem>>>(n_mma, N, ts, d);
+            const int ts = mode & 1, bmn = mode >> 1;
+            rate_kernel<<<sms, 128, smem>>>(n_mma, N, ts, d, bmn);
+            rate_kernel<<<sms, 128, smem>>>(n_mma, N, ts, d, bmn);
             cudaError_t e = cudaDeviceSynchronize();
             unsigned long long h[1024];
             cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
             unsigned long long mx = 0;
             for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
-            printf("%s{\"form\": \"%s\", \"N\": %d, \"clk_per_mma\": %.2f, \"floor_formula\": %.1f, \"err\": \"%s\"}",
-                   first ? "" : ", ", ts ? "TS" : "SS", N, double(mx) / n_mma, 128.0 * N / 256.0, cudaGetErrorString(e));
+            printf("%s{\"form\": \"%s%s\", \"N\": %d, \"clk_per_mma\": %.2f, \"floor_formula\": %.1f, \"err\": \"%s\"}",
+                   first ? "" : ", ", ts ? "TS" : "SS", bmn ? "-Bmn" : "", N, double(mx) / n_mma, 128.0 * N / 256.0, cudaGetErrorString(e));
             first = false;
         }
     printf("]}\n");

@@ -83,6 +83,21 @@ def main():
             slab, lslab = parallel.head_slab(o_full, r, world), parallel.head_slab(lse_full, r, world)
             t_heads.append(timed(lambda: vsp.vs_prefill(qs, ks, vs, ps, bs, out=slab, lse=lslab, head_major=True)))
             del qs, ks, vs
+        # heads_cost: whole KV heads placed by the predicted cost (what bench.py --head-placement cost does)
+        hsets = parallel.balanced_head_sets(cost.sum(1) + float(opts["--head-overhead"]), world)
+        grp = hq // hkv
+        t_hc = []
+        for hs in hsets:
+            kvi = torch.tensor(hs, device=dev)
+            qi = torch.tensor(parallel.q_heads_of(hs, grp), device=dev)
+            qs, ks, vs = q.index_select(1, qi), k.index_select(1, kvi), v.index_select(1, kvi)
+            ps = vsp.IndexerParams(*(t.index_select(0, kvi)
+                                     for t in (params.w_u, params.b_u, params.w_v, params.b_v, params.w_s, params.b_s)))
+            bs = [budget[g] for g in hs]
+            o_r = torch.empty(len(qi), n, 128, dtype=q.dtype, device=dev)
+            l_r = torch.empty(len(qi), n, device=dev)
+            t_hc.append(timed(lambda: vsp.vs_prefill(qs, ks, vs, ps, bs, out=o_r, lse=l_r, head_major=True)))
+            del qs, ks, vs, o_r, l_r
         # balanced: rank r = vs_prefill_units on its units (full inputs)
         units = parallel.balanced_units(cost, world, cta_overhead=float(opts["--cta-overhead"]),
                                         head_overhead=float(opts["--head-overhead"]))
@@ -96,12 +111,15 @@ def main():
             "spread_ms_per_rank": [round(x, 3) for x in t_spr], "spread_step_ms": round(max(t_spr), 3),
             "spread_tok_s": n / (max(t_spr) * 1e-3),
             "heads_ms_per_rank": [round(x, 3) for x in t_heads], "heads_step_ms": round(max(t_heads), 3),
+            "heads_cost_ms_per_rank": [round(x, 3) for x in t_hc], "heads_cost_step_ms": round(max(t_hc), 3),
+            "heads_cost_sets": hsets,
             "heads_tok_s": n / (max(t_heads) * 1e-3),
             "balanced_ms_per_rank": [round(x, 3) for x in t_bal], "balanced_step_ms": round(max(t_bal), 3),
             "balanced_tok_s": n / (max(t_bal) * 1e-3), "balanced_units": units}
     base_h = out["splits"][1]["heads_step_ms"]
     for world, s in out["splits"].items():
         s["heads_speedup"] = round(base_h / s["heads_step_ms"], 2)
+        s["heads_cost_speedup"] = round(base_h / s["heads_cost_step_ms"], 2)
         s["balanced_speedup"] = round(base_h / s["balanced_step_ms"], 2)
         s["spread_speedup"] = round(base_h / s["spread_step_ms"], 2)
     print(json.dumps(out))
