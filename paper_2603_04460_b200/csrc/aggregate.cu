@@ -41,15 +41,33 @@ using namespace vsp_sm100;
 
 namespace vsp_aggregate {
 
+#ifndef VSP_K5_TS
+#define VSP_K5_TS 0      // S^T as a TS MMA: the CTA's K tile resident in TMEM (A operand)
+#endif
+#ifndef VSP_K5_SBUFS
+#define VSP_K5_SBUFS 3
+#endif
+#ifndef VSP_K5_CHUNK
+#define VSP_K5_CHUNK 14
+#endif
+#ifndef VSP_K5_PBUFS
+#define VSP_K5_PBUFS 1   // 2: one coarse P buffer per softmax warpgroup (TS form only)
+#endif
+
 constexpr int kBlock = 128;
 constexpr int kTile = kBlock * 128 * 2;  // 32 KB bf16 tile
 constexpr int kHalf = kTile / 2;
-constexpr int kChunk = 14;               // query blocks per CTA (15 coarse blocks in TMEM)
-constexpr int kQStages = 3;
+constexpr int kChunk = VSP_K5_CHUNK;     // query blocks per CTA (kChunk + 1 coarse blocks in TMEM)
+constexpr int kPBufs = VSP_K5_PBUFS;
+static_assert(kPBufs == 1 || (kPBufs == 2 && VSP_K5_TS), "two P buffers reuse the K tile's smem");
+constexpr int kQStages = kPBufs == 2 ? 2 : 3;
 constexpr int kLStages = 6;              // LSE rows: released late (after the exps), so deeper
 constexpr int kThreads = 384;            // warp0 TMA, warp1 MMA, warps 4-11 two softmax groups
 constexpr int kAccCols = 8;              // N = 8 selector columns per coarse accumulator
-constexpr int kSBufs = 3;                // S^T TMEM buffers (items rotate through them)
+constexpr int kSBufs = VSP_K5_SBUFS;     // S^T TMEM buffers (items rotate through them)
+constexpr bool kTsS = VSP_K5_TS != 0;
+constexpr int kKCol = 448;               // TS form: K tile as packed bf16 pairs, columns [448, 512)
+static_assert(kSBufs * 128 + (kChunk + 1) * kAccCols <= (kTsS ? kKCol : 512), "aggregate TMEM budget");
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct __align__(64) Params {
@@ -68,15 +86,18 @@ struct Smem {
     uint64_t q_full[kQStages], q_empty[kQStages];
     uint64_t l_full[kLStages], l_empty[kLStages];
     uint64_t s_full[kSBufs], s_free[kSBufs];
-    uint64_t p_full, p_free[2], all_done;  // p_free[b]: reductions of items with k & 1 == b done
+    uint64_t p_full[2], p_free[2], all_done;  // [b]: items with k & 1 == b (P written / reduced)
+    uint64_t k_tmem;                        // TS form: the K tile is in TMEM
     uint32_t tmem_base;
 };
 
 // smem: K 32K | Q ring 3 x 32K | P coarse 64K (4 x [128 x 64] SW128 blocks) | selector 4K |
 //       lse ring 6 x 512 B | vertical exchange 512 B | flush staging 2 x 136 x 8 floats
+// two P buffers: P1 = [0, 64K) takes over the K tile once it is in TMEM; the Q ring has 2 stages
 constexpr int kOffK = 0;
-constexpr int kOffQ = kTile;
+constexpr int kOffQ = kPBufs == 2 ? 2 * kTile : kTile;
 constexpr int kOffP = kOffQ + kQStages * kTile;
+constexpr int kOffP1 = kPBufs == 2 ? 0 : kOffP;
 constexpr int kOffSel = kOffP + 2 * kTile;
 constexpr int kOffLse = kOffSel + 4096;
 constexpr int kOffVx = kOffLse + kLStages * 512;
@@ -133,10 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             mbar_init(&sm.s_full[b], 1);
             mbar_init(&sm.s_free[b], 4);
         }
-        mbar_init(&sm.p_full, 4);
+        mbar_init(&sm.p_full[0], 4);
+        mbar_init(&sm.p_full[1], 4);
         mbar_init(&sm.p_free[0], 1);
         mbar_init(&sm.p_free[1], 1);
         mbar_init(&sm.all_done, 1);
+        mbar_init(&sm.k_tmem, 4);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
@@ -145,6 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     {
         uint4* pz = reinterpret_cast<uint4*>(base + kOffP);
         for (int i = threadIdx.x; i < 2 * kTile / 16; i += kThreads) pz[i] = make_uint4(0, 0, 0, 0);
+        if (kPBufs == 2) {  // the upper half of P1 (the lower half holds K until it is in TMEM)
+            uint4* pz1 = reinterpret_cast<uint4*>(base + kOffP1 + kTile);
+            for (int i = threadIdx.x; i < kTile / 16; i += kThreads) pz1[i] = make_uint4(0, 0, 0, 0);
+        }
         uint16_t* sel = reinterpret_cast<uint16_t*>(base + kOffSel);
         for (int i = threadIdx.x; i < 16 * 128; i += kThreads) {
             const int f = i >> 7, c = i & 127;
@@ -158,8 +185,10 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    // TMEM: S^T buffers [0, 384); coarse accumulators: slot s at columns 384 + 8 s (15 slots)
+    // TMEM: S^T buffers [0, 128 kSBufs); coarse accumulators: slot s at columns 128 kSBufs + 8 s
+    // (kChunk + 1 slots); TS form: K (A operand, lane = key, column = packed d pair) at [448, 512)
     const uint32_t t_acc = tmem + kSBufs * 128;
+    const uint32_t t_k = tmem + kKCol;
 
     if (warp == 0) {
         // =========================== producer: K once; per item the Q tile (TMA) + LSE row
@@ -206,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(base + kOffQ), 16, 1024);
         const uint64_t sel_desc0 = umma_desc_sw128(smem_u32(base + kOffSel), 16, 1024);
         const uint32_t p_addr = smem_u32(base + kOffP);
+        const uint32_t p_addr1 = smem_u32(base + kOffP1);
         auto issue_s = [&](int k) {  // S^T = K Q^T into TMEM buffer k % 3
             const int s = k % kQStages;
             const int b = k % kSBufs;
@@ -216,8 +246,12 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t off = static_cast<uint64_t>(((kk >> 2) * kHalf + (kk & 3) * 32) >> 4);
-                    umma_ss(tmem + b * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
-                            idesc_s, kk > 0 ? 1u : 0u);
+                    if constexpr (kTsS)
+                        umma_ts(tmem + b * 128, t_k + kk * 8, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
+                                idesc_s, kk > 0 ? 1u : 0u);
+                    else
+                        umma_ss(tmem + b * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
+                                idesc_s, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&sm.s_full[b]);
                 umma_commit(&sm.q_empty[s]);
@@ -225,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             __syncwarp();
         };
         // D[slot] (+)= Pc[:, half]^T . Sel   (M = 128 coarse columns, K = 128 keys)
-        auto issue_red = [&](int slot, int half, bool acc) {
-            const uint64_t a0 = umma_desc_sw128(p_addr + half * 2 * kHalf, kHalf, 1024);
+        auto issue_red = [&](uint32_t pa, int slot, int half, bool acc) {
+            const uint64_t a0 = umma_desc_sw128(pa + half * 2 * kHalf, kHalf, 1024);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
                 umma_ss(t_acc + slot * kAccCols, a0 + static_cast<uint64_t>((kk * 2048) >> 4),
@@ -234,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                         (acc || kk > 0) ? 1u : 0u);
         };
         mbar_wait(&sm.bar_k, 0);
+        if constexpr (kTsS) mbar_wait(&sm.k_tmem, 0);
         for (int k = 0; k < kSBufs && k < num_items; ++k) issue_s(k);
         for (int k = 0; k < num_items; ++k) {
             const int tl = k / grp, hh = k % grp;
@@ -241,12 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             // tcgen05.mma runs in issue order, so the reduction of item k goes in right after
             // its P is written (the next warpgroup waits for p_free), and S(k+3) — needed only
             // after the other warpgroup's next item — goes in behind it
-            mbar_wait(&sm.p_full, k & 1);
+            mbar_wait(&sm.p_full[k & 1], (k >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
+                const uint32_t pa = (kPBufs == 2 && (k & 1)) ? p_addr1 : p_addr;
                 // lower half -> coarse block t-1 (slot tl), upper half -> block t (slot tl+1)
-                if (t >= 1) issue_red(tl, 0, tl > 0 || hh > 0);
-                issue_red(tl + 1, 1, hh > 0);
+                if (t >= 1) issue_red(pa, tl, 0, tl > 0 || hh > 0);
+                issue_red(pa, tl + 1, 1, hh > 0);
                 umma_commit(&sm.p_free[k & 1]);
                 if (k == num_items - 1) umma_commit(&sm.all_done);
             }
@@ -261,9 +297,39 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.scale * kLog2e;
         // this thread's row of the coarse buffer starts at chunk 16 - c/8 (column 128 - 8 floor(c/8))
-        uint8_t* prow = base + kOffP + c * 128;
+        uint8_t* prow = base + (kPBufs == 2 && w == 1 ? kOffP1 : kOffP) + c * 128;
         const int a0 = 16 - (c >> 3);
         float2 vacc = make_float2(0.f, 0.f);
+        if (kTsS && w == 0) {
+            // K row c (SW128: 16-byte chunk q of d-half hf at chunk q ^ (c & 7)) -> TMEM lane c,
+            // column hf * 32 + 4 q + e = packed (d, d + 1) pairs, the TS A-operand layout
+            mbar_wait(&sm.bar_k, 0);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t u[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(base + kOffK + hf * kHalf + c * 128 + ((q ^ (c & 7)) << 4));
+                    u[4 * q] = x.x;
+                    u[4 * q + 1] = x.y;
+                    u[4 * q + 2] = x.z;
+                    u[4 * q + 3] = x.w;
+                }
+                tmem_st32(t_k + lane_base + hf * 32, u);
+            }
+            tmem_wait_st();
+            if constexpr (kPBufs == 2) {  // the K tile's smem becomes the lower half of P1
+                __syncwarp();
+                named_bar_sync(4, 128);
+                uint4* pz1 = reinterpret_cast<uint4*>(base + kOffP1);
+                for (int i = c; i < kTile / 16; i += 128) pz1[i] = make_uint4(0, 0, 0, 0);
+                fence_proxy_async_smem();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.k_tmem);
+        }
+        if (kPBufs == 2 && w == 1) mbar_wait(&sm.k_tmem, 0);
         for (int k = w; k < num_items; k += 2) {
             const int tl = k / grp;
             const int t = t0 + tl;
@@ -339,7 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             // the reduction of item k-1 (the other warpgroup's) must have read the P buffer.
             // One barrier per item parity: a single barrier would let this warpgroup, one item
             // ahead, match the parity of item k-3's completion and overwrite P too early.
-            if (k >= 1) mbar_wait(&sm.p_free[(k - 1) & 1], ((k - 1) >> 1) & 1);
+            if constexpr (kPBufs == 2) {
+                if (k >= 2) mbar_wait(&sm.p_free[k & 1], ((k - 2) >> 1) & 1);  // own buffer, item k-2
+            } else {
+                if (k >= 1) mbar_wait(&sm.p_free[(k - 1) & 1], ((k - 1) >> 1) & 1);
+            }
             // row c of the coarse buffer: 16 aligned 16-byte chunks, chunk q -> coarse column
             // 128 - 8 floor(c/8) + 8q
 #pragma unroll
@@ -359,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             if (lane == 0) mbar_arrive(&sm.s_free[sb]);
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.p_full);
+            if (lane == 0) mbar_arrive(&sm.p_full[k & 1]);
         }
 
         // ---- flush (once per CTA)
