@@ -18,13 +18,15 @@
 //     vector stores, no per-element skew), and the tensor core reduces the columns against a
 //     SELECTOR B[c][f] = (f == c & 7) (M=128 coarse columns, N=8, K=128 keys): D[x][f] =
 //     sum over keys with c & 7 == f. The true diagonal is slash[o] = sum_f E[o + f][f], with
-//     E the coarse accumulator; that 8-term combination runs once per CTA in the flush.
-// CTA = one 128-key block J (K tile resident), one KV group, a chunk of up to 14 query
-// blocks, all Q heads of the group (two softmax warpgroups take alternate heads and
-// ping-pong against the tensor core). Every coarse offset block the CTA touches keeps its own
-// TMEM accumulator (15 x 8 columns), so nothing is flushed until the CTA ends. CTAs are
-// ordered (query chunk, group, key block) so concurrently resident CTAs stream the same Q
-// tiles from L2.
+//     E the coarse accumulator; that 8-term combination runs once per unit in the flush.
+// Unit = one 128-key block J (K tile resident), one KV group, a chunk of up to 14 query
+// blocks, all Q heads of the group; its items (query block, head) rotate through three softmax
+// warpgroups that ping-pong against the tensor core. Every coarse offset block the unit touches
+// keeps its own TMEM accumulator (15 x 8 columns), flushed once per unit. The kernel is
+// persistent: one CTA per SM walks units b, b + #SMs, ... (ordered (query chunk, group, key
+// block), so the units running concurrently stream the same Q tiles from L2); a unit's K tile
+// loads as soon as the previous unit's last S^T has read the old one, and its first S^T tiles
+// overlap the previous unit's flush.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -41,33 +43,31 @@ using namespace vsp_sm100;
 
 namespace vsp_aggregate {
 
-#ifndef VSP_K5_TS
-#define VSP_K5_TS 0      // S^T as a TS MMA: the CTA's K tile resident in TMEM (A operand)
-#endif
 #ifndef VSP_K5_SBUFS
 #define VSP_K5_SBUFS 3
 #endif
 #ifndef VSP_K5_CHUNK
 #define VSP_K5_CHUNK 14
 #endif
-#ifndef VSP_K5_PBUFS
-#define VSP_K5_PBUFS 1   // 2: one coarse P buffer per softmax warpgroup (TS form only)
+#ifndef VSP_K5_WGS
+#define VSP_K5_WGS 3     // softmax warpgroups (items rotate through them)
+#endif
+#ifndef VSP_K5_PERSIST
+#define VSP_K5_PERSIST 1  // one CTA per SM looping over the (chunk, group, key block) units
 #endif
 
 constexpr int kBlock = 128;
 constexpr int kTile = kBlock * 128 * 2;  // 32 KB bf16 tile
 constexpr int kHalf = kTile / 2;
-constexpr int kChunk = VSP_K5_CHUNK;     // query blocks per CTA (kChunk + 1 coarse blocks in TMEM)
-constexpr int kPBufs = VSP_K5_PBUFS;
-static_assert(kPBufs == 1 || (kPBufs == 2 && VSP_K5_TS), "two P buffers reuse the K tile's smem");
-constexpr int kQStages = kPBufs == 2 ? 2 : 3;
+constexpr int kChunk = VSP_K5_CHUNK;     // query blocks per unit (kChunk + 1 coarse blocks in TMEM)
+constexpr int kQStages = 3;
 constexpr int kLStages = 6;              // LSE rows: released late (after the exps), so deeper
-constexpr int kThreads = 384;            // warp0 TMA, warp1 MMA, warps 4-11 two softmax groups
+constexpr int kWgs = VSP_K5_WGS;
+static_assert(kWgs == 2 || kWgs == 3, "softmax warpgroups");
+constexpr int kThreads = 128 + 128 * kWgs;  // warp0 TMA, warp1 MMA, warps 4.. softmax groups
 constexpr int kAccCols = 8;              // N = 8 selector columns per coarse accumulator
 constexpr int kSBufs = VSP_K5_SBUFS;     // S^T TMEM buffers (items rotate through them)
-constexpr bool kTsS = VSP_K5_TS != 0;
-constexpr int kKCol = 448;               // TS form: K tile as packed bf16 pairs, columns [448, 512)
-static_assert(kSBufs * 128 + (kChunk + 1) * kAccCols <= (kTsS ? kKCol : 512), "aggregate TMEM budget");
+static_assert(kSBufs * 128 + (kChunk + 1) * kAccCols <= 512, "aggregate TMEM budget");
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct __align__(64) Params {
@@ -75,73 +75,77 @@ struct __align__(64) Params {
     const float* lse;  // [hq, n]
     unsigned long long* acc_v;  // [hkv, n] fixed-point (2^52) accumulators: integer atomics are
     unsigned long long* acc_s;  // order-independent, so the aggregates are bit-reproducible
-    int n, hq, hkv, num_qb, num_qc;
+    int n, hq, hkv, num_qb, num_qc, num_units;
     float scale;       // 1/sqrt(d)
     float out_scale;   // (normalized ? 1/n : 1) * (mean ? 1/group : 1)
     double fix_scale;  // 2^52 / (power of two >= the expected total of one profile)
 };
 
 struct Smem {
-    uint64_t bar_k;
+    uint64_t bar_k, k_free;                 // K tile of the unit loaded / last S^T of the unit done
     uint64_t q_full[kQStages], q_empty[kQStages];
     uint64_t l_full[kLStages], l_empty[kLStages];
     uint64_t s_full[kSBufs], s_free[kSBufs];
-    uint64_t p_full[2], p_free[2], all_done;  // [b]: items with k & 1 == b (P written / reduced)
-    uint64_t k_tmem;                        // TS form: the K tile is in TMEM
+    uint64_t p_full[3], p_free[3];          // [b]: items with k % kWgs == b (P written / reduced)
+    uint64_t all_done, acc_free;            // unit's reductions done / unit's flush read TMEM
     uint32_t tmem_base;
 };
 
 // smem: K 32K | Q ring 3 x 32K | P coarse 64K (4 x [128 x 64] SW128 blocks) | selector 4K |
-//       lse ring 6 x 512 B | vertical exchange 512 B | flush staging 2 x 136 x 8 floats
-// two P buffers: P1 = [0, 64K) takes over the K tile once it is in TMEM; the Q ring has 2 stages
+//       lse ring 6 x 512 B | vertical exchange 1 KB | flush staging kWgs x 136 x 8 floats
 constexpr int kOffK = 0;
-constexpr int kOffQ = kPBufs == 2 ? 2 * kTile : kTile;
+constexpr int kOffQ = kTile;
 constexpr int kOffP = kOffQ + kQStages * kTile;
-constexpr int kOffP1 = kPBufs == 2 ? 0 : kOffP;
 constexpr int kOffSel = kOffP + 2 * kTile;
 constexpr int kOffLse = kOffSel + 4096;
 constexpr int kOffVx = kOffLse + kLStages * 512;
-constexpr int kOffStage = kOffVx + 512;
+constexpr int kOffStage = kOffVx + 1024;
 constexpr int kStageFloats = 136 * 8;
-constexpr int kSmemBytes = kOffStage + 2 * kStageFloats * 4 + 1024;
+constexpr int kSmemBytes = kOffStage + kWgs * kStageFloats * 4 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "aggregate smem");
 
 VSP_DEVICE unsigned long long to_fixed(float x, double scale) {
     return static_cast<unsigned long long>(__double2ll_rn(static_cast<double>(x) * scale));
 }
 
-// (query chunk, group, key block) of this CTA; chunk qc covers query blocks
+// Unit = (query chunk qc, group g, key block jb); chunk qc covers query blocks
 // [kChunk*qc, kChunk*qc + kChunk) and pairs with key blocks J < min(num_qb, kChunk*(qc+1)).
-VSP_DEVICE void decode_cta(const Params& p, int& qc, int& g, int& jb) {
-    int b = blockIdx.x;
+struct Unit {
+    int g, j0, i_first, t0, nblk, num_items;
+};
+VSP_DEVICE Unit decode_unit(const Params& p, int b, int grp) {
+    int qc;
     for (qc = 0; qc < p.num_qc; ++qc) {
         const int per = min(p.num_qb, kChunk * (qc + 1)) * p.hkv;
         if (b < per) break;
         b -= per;
     }
     const int nj = min(p.num_qb, kChunk * (qc + 1));
-    g = b / nj;
-    jb = b % nj;
+    Unit u;
+    u.g = b / nj;
+    const int jb = b % nj;
+    u.j0 = jb * kBlock;
+    u.i_first = max(jb, kChunk * qc);
+    u.t0 = u.i_first - jb;                            // first t = I - J of the unit
+    u.nblk = min(p.num_qb, kChunk * (qc + 1)) - u.i_first;  // query blocks (>= 1)
+    u.num_items = u.nblk * grp;
+    return u;
 }
 
+// Persistent: CTA b walks units b, b + gridDim.x, ...; ring slots and barrier phases use the
+// CTA-global item index kg (items of all its units in order), the K tile and the coarse slots
+// one phase per unit.
 __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ Smem sm;
     const int grp = p.hq / p.hkv;
-    int qc, g, jb;
-    decode_cta(p, qc, g, jb);
-    const int i_first = max(jb, kChunk * qc);
-    const int i_end = min(p.num_qb, kChunk * (qc + 1));
-    const int t0 = i_first - jb;              // first t = I - J of this CTA
-    const int nblk = i_end - i_first;         // query blocks (>= 1)
-    const int num_items = nblk * grp;
-    const int j0 = jb * kBlock;
     const uint32_t warp = warp_id(), lane = lane_id();
     float* lse_ring = reinterpret_cast<float*>(base + kOffLse);
 
     if (warp == 0 && lane == 0) {
         mbar_init(&sm.bar_k, 1);
+        mbar_init(&sm.k_free, 1);
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&sm.q_full[s], 1);
             mbar_init(&sm.q_empty[s], 1);
@@ -154,12 +158,12 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
             mbar_init(&sm.s_full[b], 1);
             mbar_init(&sm.s_free[b], 4);
         }
-        mbar_init(&sm.p_full[0], 4);
-        mbar_init(&sm.p_full[1], 4);
-        mbar_init(&sm.p_free[0], 1);
-        mbar_init(&sm.p_free[1], 1);
+        for (int b = 0; b < kWgs; ++b) {
+            mbar_init(&sm.p_full[b], 4);
+            mbar_init(&sm.p_free[b], 1);
+        }
         mbar_init(&sm.all_done, 1);
-        mbar_init(&sm.k_tmem, 4);
+        mbar_init(&sm.acc_free, 4 * kWgs);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
@@ -168,10 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     {
         uint4* pz = reinterpret_cast<uint4*>(base + kOffP);
         for (int i = threadIdx.x; i < 2 * kTile / 16; i += kThreads) pz[i] = make_uint4(0, 0, 0, 0);
-        if (kPBufs == 2) {  // the upper half of P1 (the lower half holds K until it is in TMEM)
-            uint4* pz1 = reinterpret_cast<uint4*>(base + kOffP1 + kTile);
-            for (int i = threadIdx.x; i < kTile / 16; i += kThreads) pz1[i] = make_uint4(0, 0, 0, 0);
-        }
         uint16_t* sel = reinterpret_cast<uint16_t*>(base + kOffSel);
         for (int i = threadIdx.x; i < 16 * 128; i += kThreads) {
             const int f = i >> 7, c = i & 127;
@@ -186,46 +186,54 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
     // TMEM: S^T buffers [0, 128 kSBufs); coarse accumulators: slot s at columns 128 kSBufs + 8 s
-    // (kChunk + 1 slots); TS form: K (A operand, lane = key, column = packed d pair) at [448, 512)
+    // (kChunk + 1 slots, reused by every unit after its flush)
     const uint32_t t_acc = tmem + kSBufs * 128;
-    const uint32_t t_k = tmem + kKCol;
 
     if (warp == 0) {
-        // =========================== producer: K once; per item the Q tile (TMA) + LSE row
+        // =========================== producer: per unit the K tile; per item the Q tile + LSE row
         if (elect_one()) {
             tma_prefetch_desc(&p.map_q);
             tma_prefetch_desc(&p.map_k);
-            mbar_arrive_expect_tx(&sm.bar_k, kTile);
-            for (int hf = 0; hf < 2; ++hf)
-                tma_load_3d(base + kOffK + hf * kHalf, &p.map_k, &sm.bar_k, hf * 64, g, j0);
         }
         __syncwarp();
-        for (int k = 0; k < num_items; ++k) {
-            const int ib = i_first + k / grp;
-            const int h = g * grp + k % grp;
-            const int s = k % kQStages;
-            if (k >= kQStages) mbar_wait(&sm.q_empty[s], ((k / kQStages) - 1) & 1);
+        int kg = 0;
+        for (int u = blockIdx.x, ul = 0; u < p.num_units; u += gridDim.x, ++ul) {
+            const Unit U = decode_unit(p, u, grp);
+            // the previous unit's S^T MMAs have read the K tile
+            if (ul > 0) mbar_wait(&sm.k_free, (ul - 1) & 1);
             if (elect_one()) {
-                mbar_arrive_expect_tx(&sm.q_full[s], kTile);
+                mbar_arrive_expect_tx(&sm.bar_k, kTile);
                 for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
-                                ib * kBlock);
+                    tma_load_3d(base + kOffK + hf * kHalf, &p.map_k, &sm.bar_k, hf * 64, U.g, U.j0);
             }
             __syncwarp();
-            // LSE of the tile's rows in log2 units; rows past n get +inf (weight exactly 0)
-            const int ls = k % kLStages;
-            if (k >= kLStages) mbar_wait(&sm.l_empty[ls], ((k / kLStages) - 1) & 1);
-            float4 l4;
-            const int i = ib * kBlock + 4 * lane;
-            const float* src = p.lse + static_cast<size_t>(h) * p.n;
-            l4.x = i + 0 < p.n ? __ldg(src + i + 0) * kLog2e : INFINITY;
-            l4.y = i + 1 < p.n ? __ldg(src + i + 1) * kLog2e : INFINITY;
-            l4.z = i + 2 < p.n ? __ldg(src + i + 2) * kLog2e : INFINITY;
-            l4.w = i + 3 < p.n ? __ldg(src + i + 3) * kLog2e : INFINITY;
-            reinterpret_cast<float4*>(lse_ring + ls * kBlock)[lane] = l4;
-            __syncwarp();
-            if (elect_one()) mbar_arrive(&sm.l_full[ls]);
-            __syncwarp();
+            for (int k = 0; k < U.num_items; ++k, ++kg) {
+                const int ib = U.i_first + k / grp;
+                const int h = U.g * grp + k % grp;
+                const int s = kg % kQStages;
+                if (kg >= kQStages) mbar_wait(&sm.q_empty[s], ((kg / kQStages) - 1) & 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.q_full[s], kTile);
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_3d(base + kOffQ + s * kTile + hf * kHalf, &p.map_q, &sm.q_full[s], hf * 64, h,
+                                    ib * kBlock);
+                }
+                __syncwarp();
+                // LSE of the tile's rows in log2 units; rows past n get +inf (weight exactly 0)
+                const int ls = kg % kLStages;
+                if (kg >= kLStages) mbar_wait(&sm.l_empty[ls], ((kg / kLStages) - 1) & 1);
+                float4 l4;
+                const int i = ib * kBlock + 4 * lane;
+                const float* src = p.lse + static_cast<size_t>(h) * p.n;
+                l4.x = i + 0 < p.n ? __ldg(src + i + 0) * kLog2e : INFINITY;
+                l4.y = i + 1 < p.n ? __ldg(src + i + 1) * kLog2e : INFINITY;
+                l4.z = i + 2 < p.n ? __ldg(src + i + 2) * kLog2e : INFINITY;
+                l4.w = i + 3 < p.n ? __ldg(src + i + 3) * kLog2e : INFINITY;
+                reinterpret_cast<float4*>(lse_ring + ls * kBlock)[lane] = l4;
+                __syncwarp();
+                if (elect_one()) mbar_arrive(&sm.l_full[ls]);
+                __syncwarp();
+            }
         }
     } else if (warp == 1) {
         // =========================== MMA issuer (warp-uniform loop, elected lane issues)
@@ -235,248 +243,233 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(base + kOffQ), 16, 1024);
         const uint64_t sel_desc0 = umma_desc_sw128(smem_u32(base + kOffSel), 16, 1024);
         const uint32_t p_addr = smem_u32(base + kOffP);
-        const uint32_t p_addr1 = smem_u32(base + kOffP1);
-        auto issue_s = [&](int k) {  // S^T = K Q^T into TMEM buffer k % 3
-            const int s = k % kQStages;
-            const int b = k % kSBufs;
-            mbar_wait(&sm.q_full[s], (k / kQStages) & 1);
-            if (k >= kSBufs) mbar_wait(&sm.s_free[b], ((k / kSBufs) - 1) & 1);
+        auto issue_s = [&](int kg, bool last) {  // S^T = K Q^T into TMEM buffer kg % kSBufs
+            const int s = kg % kQStages;
+            const int b = kg % kSBufs;
+            mbar_wait(&sm.q_full[s], (kg / kQStages) & 1);
+            if (kg >= kSBufs) mbar_wait(&sm.s_free[b], ((kg / kSBufs) - 1) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t off = static_cast<uint64_t>(((kk >> 2) * kHalf + (kk & 3) * 32) >> 4);
-                    if constexpr (kTsS)
-                        umma_ts(tmem + b * 128, t_k + kk * 8, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
-                                idesc_s, kk > 0 ? 1u : 0u);
-                    else
-                        umma_ss(tmem + b * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
-                                idesc_s, kk > 0 ? 1u : 0u);
+                    umma_ss(tmem + b * 128, k_desc0 + off, q_desc0 + static_cast<uint64_t>((s * kTile) >> 4) + off,
+                            idesc_s, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&sm.s_full[b]);
                 umma_commit(&sm.q_empty[s]);
+                if (last) umma_commit(&sm.k_free);  // the unit's K tile may be replaced
             }
             __syncwarp();
         };
         // D[slot] (+)= Pc[:, half]^T . Sel   (M = 128 coarse columns, K = 128 keys)
-        auto issue_red = [&](uint32_t pa, int slot, int half, bool acc) {
-            const uint64_t a0 = umma_desc_sw128(pa + half * 2 * kHalf, kHalf, 1024);
+        auto issue_red = [&](int slot, int half, bool acc) {
+            const uint64_t a0 = umma_desc_sw128(p_addr + half * 2 * kHalf, kHalf, 1024);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
                 umma_ss(t_acc + slot * kAccCols, a0 + static_cast<uint64_t>((kk * 2048) >> 4),
                         sel_desc0 + static_cast<uint64_t>(((kk >> 2) * 2048 + (kk & 3) * 32) >> 4), idesc_red,
                         (acc || kk > 0) ? 1u : 0u);
         };
-        mbar_wait(&sm.bar_k, 0);
-        if constexpr (kTsS) mbar_wait(&sm.k_tmem, 0);
-        for (int k = 0; k < kSBufs && k < num_items; ++k) issue_s(k);
-        for (int k = 0; k < num_items; ++k) {
-            const int tl = k / grp, hh = k % grp;
-            const int t = t0 + tl;
-            // tcgen05.mma runs in issue order, so the reduction of item k goes in right after
-            // its P is written (the next warpgroup waits for p_free), and S(k+3) — needed only
-            // after the other warpgroup's next item — goes in behind it
-            mbar_wait(&sm.p_full[k & 1], (k >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t pa = (kPBufs == 2 && (k & 1)) ? p_addr1 : p_addr;
-                // lower half -> coarse block t-1 (slot tl), upper half -> block t (slot tl+1)
-                if (t >= 1) issue_red(pa, tl, 0, tl > 0 || hh > 0);
-                issue_red(pa, tl + 1, 1, hh > 0);
-                umma_commit(&sm.p_free[k & 1]);
-                if (k == num_items - 1) umma_commit(&sm.all_done);
+        int kg0 = 0;  // global index of the unit's first item
+        for (int u = blockIdx.x, ul = 0; u < p.num_units; u += gridDim.x, ++ul) {
+            const Unit U = decode_unit(p, u, grp);
+            const int n_it = U.num_items;
+            // the unit's first S^T tiles go in as soon as its K tile is loaded; they overlap the
+            // softmax warps' flush of the previous unit
+            mbar_wait(&sm.bar_k, ul & 1);
+            for (int k = 0; k < kSBufs && k < n_it; ++k) issue_s(kg0 + k, k == n_it - 1);
+            for (int k = 0; k < n_it; ++k) {
+                const int kg = kg0 + k;
+                const int tl = k / grp, hh = k % grp;
+                const int t = U.t0 + tl;
+                // tcgen05.mma runs in issue order, so the reduction of item kg goes in right after
+                // its P is written (the next warpgroup waits for p_free), and S(kg + kSBufs) —
+                // needed only after the other warpgroups' next items — goes in behind it
+                mbar_wait(&sm.p_full[kg % kWgs], (kg / kWgs) & 1);
+                // a unit's first reduction overwrites the coarse slots: the previous unit's flush
+                // must have read them
+                if (k == 0 && ul > 0) mbar_wait(&sm.acc_free, (ul - 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    // lower half -> coarse block t-1 (slot tl), upper half -> block t (slot tl+1)
+                    if (t >= 1) issue_red(tl, 0, tl > 0 || hh > 0);
+                    issue_red(tl + 1, 1, hh > 0);
+                    umma_commit(&sm.p_free[kg % kWgs]);
+                    if (k == n_it - 1) umma_commit(&sm.all_done);
+                }
+                __syncwarp();
+                if (k + kSBufs < n_it) issue_s(kg + kSBufs, k + kSBufs == n_it - 1);
             }
-            __syncwarp();
-            if (k + kSBufs < num_items) issue_s(k + kSBufs);
+            kg0 += n_it;
         }
     } else if (warp >= 4) {
-        // =========================== softmax groups: WG w takes items k with k & 1 == w
+        // =========================== softmax groups: WG w takes items with kg % kWgs == w
         const int w = (warp - 4) >> 2;
         const int quarter = warp & 3;
         const int c = quarter * 32 + lane;  // key row (TMEM lane) within block J
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.scale * kLog2e;
         // this thread's row of the coarse buffer starts at chunk 16 - c/8 (column 128 - 8 floor(c/8))
-        uint8_t* prow = base + (kPBufs == 2 && w == 1 ? kOffP1 : kOffP) + c * 128;
+        uint8_t* prow = base + kOffP + c * 128;
         const int a0 = 16 - (c >> 3);
-        float2 vacc = make_float2(0.f, 0.f);
-        if (kTsS && w == 0) {
-            // K row c (SW128: 16-byte chunk q of d-half hf at chunk q ^ (c & 7)) -> TMEM lane c,
-            // column hf * 32 + 4 q + e = packed (d, d + 1) pairs, the TS A-operand layout
-            mbar_wait(&sm.bar_k, 0);
+        float* vx = reinterpret_cast<float*>(base + kOffVx);
+        float* stage = reinterpret_cast<float*>(base + kOffStage) + w * kStageFloats;
+        int kg0 = 0;  // global index of the unit's first item
+        for (int u = blockIdx.x, ul = 0; u < p.num_units; u += gridDim.x, ++ul) {
+            const Unit U = decode_unit(p, u, grp);
+            float2 vacc = make_float2(0.f, 0.f);
+            for (int k = ((w - kg0) % kWgs + kWgs) % kWgs; k < U.num_items; k += kWgs) {
+                const int kg = kg0 + k;
+                const int tl = k / grp;
+                const int t = U.t0 + tl;
+                const int ls = kg % kLStages;
+                const bool plain = t > 0 && (U.i_first + tl + 1) * kBlock <= p.n;  // no causal mask, full rows
+                mbar_wait(&sm.l_full[ls], (kg / kLStages) & 1);
+                const int sb = kg % kSBufs;
+                mbar_wait(&sm.s_full[sb], (kg / kSBufs) & 1);
+                tc_fence_after();
+                const float4* l4 = reinterpret_cast<const float4*>(lse_ring + ls * kBlock);
+                // The exp pass is straight-line code per 32-column chunk (no per-element branches:
+                // the two variants are separate instantiations), so the scheduler can interleave
+                // the MUFU / FMA chains of 32 independent elements. Packed bf16 weights of chunk cq
+                // go back into TMEM columns [16 cq, 16 cq + 16) of the same S^T buffer (already
+                // consumed), so the row is not held in registers while waiting for the P buffer.
+                const uint32_t s_t = tmem + lane_base + sb * 128;
+                auto exp_pass = [&](auto plain_tag) {
+                    constexpr bool kPlain = decltype(plain_tag)::value;
+                    // diagonal tile: keep r >= c; elsewhere nothing is masked (ragged rows carry
+                    // lse = +inf and come out exactly 0 on the MUFU path)
+                    const int lim = t == 0 ? c : 0;
+                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                     make_float2(0.f, 0.f)};
+                    uint32_t uu[2][32];
+                    tmem_ld32(s_t, uu[0]);
+                    tmem_wait_ld(uu[0]);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                uint32_t u[32];
+                    for (int cq = 0; cq < 4; ++cq) {
+                        if (cq < 3) tmem_ld32(s_t + (cq + 1) * 32, uu[(cq + 1) & 1]);
+                        const uint32_t* x = uu[cq & 1];
+                        uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint4 x = *reinterpret_cast<const uint4*>(base + kOffK + hf * kHalf + c * 128 + ((q ^ (c & 7)) << 4));
-                    u[4 * q] = x.x;
-                    u[4 * q + 1] = x.y;
-                    u[4 * q + 2] = x.z;
-                    u[4 * q + 3] = x.w;
-                }
-                tmem_st32(t_k + lane_base + hf * 32, u);
-            }
-            tmem_wait_st();
-            if constexpr (kPBufs == 2) {  // the K tile's smem becomes the lower half of P1
-                __syncwarp();
-                named_bar_sync(4, 128);
-                uint4* pz1 = reinterpret_cast<uint4*>(base + kOffP1);
-                for (int i = c; i < kTile / 16; i += 128) pz1[i] = make_uint4(0, 0, 0, 0);
-                fence_proxy_async_smem();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.k_tmem);
-        }
-        if (kPBufs == 2 && w == 1) mbar_wait(&sm.k_tmem, 0);
-        for (int k = w; k < num_items; k += 2) {
-            const int tl = k / grp;
-            const int t = t0 + tl;
-            const int ls = k % kLStages;
-            const bool plain = t > 0 && (i_first + tl + 1) * kBlock <= p.n;  // no causal mask, full rows
-            mbar_wait(&sm.l_full[ls], (k / kLStages) & 1);
-            const int sb = k % kSBufs;
-            mbar_wait(&sm.s_full[sb], (k / kSBufs) & 1);
-            tc_fence_after();
-            const float4* l4 = reinterpret_cast<const float4*>(lse_ring + ls * kBlock);
-            // The exp pass is straight-line code per 32-column chunk (no per-element branches:
-            // the two variants are separate instantiations), so the scheduler can interleave
-            // the MUFU / FMA chains of 32 independent elements. Packed bf16 weights of chunk cq
-            // go back into TMEM columns [16 cq, 16 cq + 16) of the same S^T buffer (already
-            // consumed), so the row is not held in registers while waiting for the P buffer.
-            const uint32_t s_t = tmem + lane_base + sb * 128;
-            auto exp_pass = [&](auto plain_tag) {
-                constexpr bool kPlain = decltype(plain_tag)::value;
-                // diagonal tile: keep r >= c; elsewhere nothing is masked (ragged rows carry
-                // lse = +inf and come out exactly 0 on the MUFU path)
-                const int lim = t == 0 ? c : 0;
-                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                 make_float2(0.f, 0.f)};
-                uint32_t u[2][32];
-                tmem_ld32(s_t, u[0]);
-                tmem_wait_ld(u[0]);
-#pragma unroll
-                for (int cq = 0; cq < 4; ++cq) {
-                    if (cq < 3) tmem_ld32(s_t + (cq + 1) * 32, u[(cq + 1) & 1]);
-                    const uint32_t* x = u[cq & 1];
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e4 = 0; e4 < 8; ++e4) {
-                        const float4 l = l4[cq * 8 + e4];
-                        const int r = cq * 32 + e4 * 4;
-                        float2 y0 = ffma2(make_float2(__uint_as_float(x[4 * e4]), __uint_as_float(x[4 * e4 + 1])),
-                                          make_float2(sl2, sl2), make_float2(-l.x, -l.y));
-                        float2 y1 = ffma2(make_float2(__uint_as_float(x[4 * e4 + 2]), __uint_as_float(x[4 * e4 + 3])),
-                                          make_float2(sl2, sl2), make_float2(-l.z, -l.w));
-                        float2 e0, e1;
-                        if constexpr (kPlain) {
-                            // 3 pairs in 8 on the FMA pipe, the rest on MUFU (the K4 balance)
-                            if ((0x54u >> e4) & 1u) {
-                                e0 = exp2_poly2(y0);
-                                e1 = exp2_poly2(y1);
+                        for (int e4 = 0; e4 < 8; ++e4) {
+                            const float4 l = l4[cq * 8 + e4];
+                            const int r = cq * 32 + e4 * 4;
+                            float2 y0 = ffma2(make_float2(__uint_as_float(x[4 * e4]), __uint_as_float(x[4 * e4 + 1])),
+                                              make_float2(sl2, sl2), make_float2(-l.x, -l.y));
+                            float2 y1 = ffma2(make_float2(__uint_as_float(x[4 * e4 + 2]), __uint_as_float(x[4 * e4 + 3])),
+                                              make_float2(sl2, sl2), make_float2(-l.z, -l.w));
+                            float2 e0, e1;
+                            if constexpr (kPlain) {
+                                // 3 pairs in 8 on the FMA pipe, the rest on MUFU (the K4 balance)
+                                if ((0x54u >> e4) & 1u) {
+                                    e0 = exp2_poly2(y0);
+                                    e1 = exp2_poly2(y1);
+                                } else {
+                                    e0 = make_float2(ex2_approx(y0.x), ex2_approx(y0.y));
+                                    e1 = make_float2(ex2_approx(y1.x), ex2_approx(y1.y));
+                                }
                             } else {
+                                y0.x = r + 0 >= lim ? y0.x : -INFINITY;
+                                y0.y = r + 1 >= lim ? y0.y : -INFINITY;
+                                y1.x = r + 2 >= lim ? y1.x : -INFINITY;
+                                y1.y = r + 3 >= lim ? y1.y : -INFINITY;
                                 e0 = make_float2(ex2_approx(y0.x), ex2_approx(y0.y));
                                 e1 = make_float2(ex2_approx(y1.x), ex2_approx(y1.y));
                             }
-                        } else {
-                            y0.x = r + 0 >= lim ? y0.x : -INFINITY;
-                            y0.y = r + 1 >= lim ? y0.y : -INFINITY;
-                            y1.x = r + 2 >= lim ? y1.x : -INFINITY;
-                            y1.y = r + 3 >= lim ? y1.y : -INFINITY;
-                            e0 = make_float2(ex2_approx(y0.x), ex2_approx(y0.y));
-                            e1 = make_float2(ex2_approx(y1.x), ex2_approx(y1.y));
+                            acc[(2 * e4) & 3] = fadd2(acc[(2 * e4) & 3], e0);
+                            acc[(2 * e4 + 1) & 3] = fadd2(acc[(2 * e4 + 1) & 3], e1);
+                            pk[2 * e4] = pack_bf16x2(e0.x, e0.y);
+                            pk[2 * e4 + 1] = pack_bf16x2(e1.x, e1.y);
                         }
-                        acc[(2 * e4) & 3] = fadd2(acc[(2 * e4) & 3], e0);
-                        acc[(2 * e4 + 1) & 3] = fadd2(acc[(2 * e4 + 1) & 3], e1);
-                        pk[2 * e4] = pack_bf16x2(e0.x, e0.y);
-                        pk[2 * e4 + 1] = pack_bf16x2(e1.x, e1.y);
+                        tmem_st16(s_t + cq * 16, pk);
+                        if (cq < 3) tmem_wait_ld(uu[(cq + 1) & 1]);
                     }
-                    tmem_st16(s_t + cq * 16, pk);
-                    if (cq < 3) tmem_wait_ld(u[(cq + 1) & 1]);
-                }
-                vacc = fadd2(vacc, fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
-            };
-            if (plain) exp_pass(std::true_type{});
-            else exp_pass(std::false_type{});
-            tmem_wait_st();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.l_empty[ls]);
-            // the reduction of item k-1 (the other warpgroup's) must have read the P buffer.
-            // One barrier per item parity: a single barrier would let this warpgroup, one item
-            // ahead, match the parity of item k-3's completion and overwrite P too early.
-            if constexpr (kPBufs == 2) {
-                if (k >= 2) mbar_wait(&sm.p_free[k & 1], ((k - 2) >> 1) & 1);  // own buffer, item k-2
-            } else {
-                if (k >= 1) mbar_wait(&sm.p_free[(k - 1) & 1], ((k - 1) >> 1) & 1);
-            }
-            // row c of the coarse buffer: 16 aligned 16-byte chunks, chunk q -> coarse column
-            // 128 - 8 floor(c/8) + 8q
+                    vacc = fadd2(vacc, fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
+                };
+                if (plain) exp_pass(std::true_type{});
+                else exp_pass(std::false_type{});
+                tmem_wait_st();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.l_empty[ls]);
+                // the reduction of item kg-1 (another warpgroup's) must have read the P buffer.
+                // Per-warpgroup barriers: red(kg - 1) is the phase after red(kg - 1 - kWgs), which
+                // this warpgroup's own previous P (item kg - kWgs) already waited for.
+                if (kg >= 1) mbar_wait(&sm.p_free[(kg - 1) % kWgs], ((kg - 1) / kWgs) & 1);
+                // row c of the coarse buffer: 16 aligned 16-byte chunks, chunk q -> coarse column
+                // 128 - 8 floor(c/8) + 8q
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t pk[32];
-                tmem_ld32(s_t + h2 * 32, pk);
-                tmem_wait_ld(pk);
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    uint32_t pk[32];
+                    tmem_ld32(s_t + h2 * 32, pk);
+                    tmem_wait_ld(pk);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int a = a0 + h2 * 8 + q;  // absolute 8-column chunk, 1..31
-                    *reinterpret_cast<uint4*>(prow + (a >> 3) * kHalf + (((a & 7) ^ (c & 7)) << 4)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    for (int q = 0; q < 8; ++q) {
+                        const int a = a0 + h2 * 8 + q;  // absolute 8-column chunk, 1..31
+                        *reinterpret_cast<uint4*>(prow + (a >> 3) * kHalf + (((a & 7) ^ (c & 7)) << 4)) =
+                            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.s_free[sb]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.p_full[kg % kWgs]);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.s_free[sb]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.p_full[k & 1]);
-        }
 
-        // ---- flush (once per CTA)
-        float* vx = reinterpret_cast<float*>(base + kOffVx);
-        if (w == 1) vx[c] = vacc.x + vacc.y;
-        mbar_wait(&sm.all_done, 0);
-        tc_fence_after();
-        named_bar_sync(1, 256);
-        if (w == 0) {
-            const int j = j0 + c;
-            if (j < p.n && num_items > 0)
-                atomicAdd(p.acc_v + static_cast<size_t>(g) * p.n + j, to_fixed((vacc.x + vacc.y + vx[c]) * p.out_scale, p.fix_scale));
-        }
-        // slash block b = sum_f E[128 b + x + f][f]; E block b lives in slot b - t0 + 1 (slot 0
-        // only when t0 >= 1). WG w flushes blocks with (b - b_lo) % 2 == w.
-        float* stage = reinterpret_cast<float*>(base + kOffStage) + w * kStageFloats;
-        const int nslots = nblk + 1;
-        const int b_lo = max(0, t0 - 2);
-        const int b_hi = t0 + nblk - 1;
-        for (int b = b_lo + w; b <= b_hi; b += 2) {
-            const int s0 = b - t0 + 1;
-            const bool v0 = s0 >= 0 && s0 < nslots && !(s0 == 0 && t0 == 0);
-            const bool v1 = s0 + 1 >= 0 && s0 + 1 < nslots && !(s0 + 1 == 0 && t0 == 0);
-            uint32_t e[16];
-            if (v0) {
-                tmem_ld16(t_acc + s0 * kAccCols + lane_base, e);
-                tmem_wait_ld(e);
-            }
+            // ---- flush of the unit (the next unit's S^T / exponentials overlap it)
+            if (w >= 1) vx[(w - 1) * 128 + c] = vacc.x + vacc.y;
+            mbar_wait(&sm.all_done, ul & 1);
+            tc_fence_after();
+            named_bar_sync(1, 128 * kWgs);
+            if (w == 0) {
+                const int j = U.j0 + c;
+                float v = vacc.x + vacc.y;
 #pragma unroll
-            for (int f = 0; f < 8; ++f) stage[c * 8 + f] = v0 ? __uint_as_float(e[f]) : 0.f;
-            if (quarter == 0) {  // rows 128..135 of the window: first rows of block b+1
-                if (v1) {
-                    tmem_ld16(t_acc + (s0 + 1) * kAccCols + lane_base, e);
+                for (int x = 0; x < kWgs - 1; ++x) v += vx[x * 128 + c];
+                if (j < p.n) atomicAdd(p.acc_v + static_cast<size_t>(U.g) * p.n + j, to_fixed(v * p.out_scale, p.fix_scale));
+            }
+            // slash block b = sum_f E[128 b + x + f][f]; E block b lives in slot b - t0 + 1 (slot 0
+            // only when t0 >= 1). WG w flushes blocks with (b - b_lo) % kWgs == w.
+            const int nslots = U.nblk + 1;
+            const int b_lo = max(0, U.t0 - 2);
+            const int b_hi = U.t0 + U.nblk - 1;
+            for (int b = b_lo + w; b <= b_hi; b += kWgs) {
+                const int s0 = b - U.t0 + 1;
+                const bool v0 = s0 >= 0 && s0 < nslots && !(s0 == 0 && U.t0 == 0);
+                const bool v1 = s0 + 1 >= 0 && s0 + 1 < nslots && !(s0 + 1 == 0 && U.t0 == 0);
+                uint32_t e[16];
+                if (v0) {
+                    tmem_ld16(t_acc + s0 * kAccCols + lane_base, e);
                     tmem_wait_ld(e);
                 }
-                if (lane < 8) {
 #pragma unroll
-                    for (int f = 0; f < 8; ++f) stage[(128 + lane) * 8 + f] = v1 ? __uint_as_float(e[f]) : 0.f;
+                for (int f = 0; f < 8; ++f) stage[c * 8 + f] = v0 ? __uint_as_float(e[f]) : 0.f;
+                if (quarter == 0) {  // rows 128..135 of the window: first rows of block b+1
+                    if (v1) {
+                        tmem_ld16(t_acc + (s0 + 1) * kAccCols + lane_base, e);
+                        tmem_wait_ld(e);
+                    }
+                    if (lane < 8) {
+#pragma unroll
+                        for (int f = 0; f < 8; ++f) stage[(128 + lane) * 8 + f] = v1 ? __uint_as_float(e[f]) : 0.f;
+                    }
                 }
-            }
-            named_bar_sync(2 + w, 128);
-            float sum = 0.f;
+                named_bar_sync(2 + w, 128);
+                float sum = 0.f;
 #pragma unroll
-            for (int f = 0; f < 8; ++f) sum += stage[(c + f) * 8 + f];
-            const int o = b * kBlock + c;
-            if (o < p.n && sum != 0.f) atomicAdd(p.acc_s + static_cast<size_t>(g) * p.n + o, to_fixed(sum * p.out_scale, p.fix_scale));
-            named_bar_sync(2 + w, 128);
+                for (int f = 0; f < 8; ++f) sum += stage[(c + f) * 8 + f];
+                const int o = b * kBlock + c;
+                if (o < p.n && sum != 0.f) atomicAdd(p.acc_s + static_cast<size_t>(U.g) * p.n + o, to_fixed(sum * p.out_scale, p.fix_scale));
+                named_bar_sync(2 + w, 128);
+            }
+            // the coarse slots may be overwritten by the next unit's first reduction; vx is
+            // rewritten only after the next unit's all_done, which follows WG 0's read above
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.acc_free);
+            kg0 += U.num_items;
         }
     }
     tc_fence_before();
@@ -558,10 +551,14 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     vsp_detail::once_per_device(attr, [] {
         cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     });
-    long long ctas = 0;
-    for (int qc = 0; qc < p.num_qc; ++qc) ctas += static_cast<long long>(std::min(p.num_qb, kChunk * (qc + 1))) * a.hkv;
+    long long units = 0;
+    for (int qc = 0; qc < p.num_qc; ++qc) units += static_cast<long long>(std::min(p.num_qb, kChunk * (qc + 1))) * a.hkv;
+    p.num_units = static_cast<int>(units);
+    // persistent: one CTA per SM walks units blockIdx.x, + grid, ... (consecutive units run
+    // concurrently across the SMs, so they stream the same Q tiles from L2)
+    const long long grid = VSP_K5_PERSIST ? std::min<long long>(units, vsp_detail::current_sm_count()) : units;
     vsp_detail::count_launch();
-    aggregate_kernel<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, stream>>>(p);
+    aggregate_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, stream>>>(p);
     const int grp = a.hq / a.hkv;
     const double total = (a.normalized ? 1.0 : static_cast<double>(a.n)) * (a.mean ? 1.0 : static_cast<double>(grp));
     vsp_detail::count_launch();
