@@ -92,7 +92,7 @@ struct Smem {
 };
 
 // smem: K 32K | Q ring 3 x 32K | P coarse 64K (4 x [128 x 64] SW128 blocks) | selector 4K |
-//       lse ring 6 x 512 B | vertical exchange 1 KB | flush staging kWgs x 136 x 8 floats
+//       lse ring 6 x 512 B | vertical exchange 1 KB | flush staging kWgs x 136 x 9 floats
 constexpr int kOffK = 0;
 constexpr int kOffQ = kTile;
 constexpr int kOffP = kOffQ + kQStages * kTile;
@@ -100,7 +100,8 @@ constexpr int kOffSel = kOffP + 2 * kTile;
 constexpr int kOffLse = kOffSel + 4096;
 constexpr int kOffVx = kOffLse + kLStages * 512;
 constexpr int kOffStage = kOffVx + 1024;
-constexpr int kStageFloats = 136 * 8;
+constexpr int kStageStride = 9;          // flush staging row pitch (odd: conflict-free)
+constexpr int kStageFloats = 136 * kStageStride;
 constexpr int kSmemBytes = kOffStage + kWgs * kStageFloats * 4 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "aggregate smem");
 
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                     tmem_wait_ld(e);
                 }
 #pragma unroll
-                for (int f = 0; f < 8; ++f) stage[c * 8 + f] = v0 ? __uint_as_float(e[f]) : 0.f;
+                for (int f = 0; f < 8; ++f) stage[c * kStageStride + f] = v0 ? __uint_as_float(e[f]) : 0.f;
                 if (quarter == 0) {  // rows 128..135 of the window: first rows of block b+1
                     if (v1) {
                         tmem_ld16(t_acc + (s0 + 1) * kAccCols + lane_base, e);
@@ -453,13 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1) aggregate_kernel(const __grid_con
                     }
                     if (lane < 8) {
 #pragma unroll
-                        for (int f = 0; f < 8; ++f) stage[(128 + lane) * 8 + f] = v1 ? __uint_as_float(e[f]) : 0.f;
+                        for (int f = 0; f < 8; ++f) stage[(128 + lane) * kStageStride + f] = v1 ? __uint_as_float(e[f]) : 0.f;
                     }
                 }
                 named_bar_sync(2 + w, 128);
                 float sum = 0.f;
 #pragma unroll
-                for (int f = 0; f < 8; ++f) sum += stage[(c + f) * 8 + f];
+                for (int f = 0; f < 8; ++f) sum += stage[(c + f) * kStageStride + f];
                 const int o = b * kBlock + c;
                 if (o < p.n && sum != 0.f) atomicAdd(p.acc_s + static_cast<size_t>(U.g) * p.n + o, to_fixed(sum * p.out_scale, p.fix_scale));
                 named_bar_sync(2 + w, 128);
