@@ -82,11 +82,13 @@ def trained(n, hq=32, hkv=8, train_prompts=8, val_prompts=4, steps=600, margin=0
 
 def c2():
     n = 32768
-    params, budget, pt = trained(n, train_prompts=12, val_prompts=6, steps=900, margin=0.05)
+    # every validation prompt must reach 0.92 ("worst"): a mean target (0.95) left the held-out
+    # prompt at 0.88-0.91 depending on the distillation run (tools/dev/c2_calib.py)
+    params, budget, pt = trained(n, train_prompts=12, val_prompts=6, steps=900, margin=0.02, aggregate="worst")
     q, k, v, _ = planted_layer(n, 32, 8, seed=2026)
     r = layer_stats(q, k, v, params, budget)
     return {"config": "C2 32k adaptive budget (distilled indexer on 12 prompts, tau calibrated on 6 validation "
-                      "prompts for mean recall >= 0.95; held-out prompt timed)",
+                      "prompts for recall >= 0.92 on every one of them; held-out prompt timed)",
             "tau": [[b.tau_v, b.tau_s] for b in budget], **r}
 
 
