@@ -197,6 +197,31 @@ VSP_API int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const voi
                            int* k_s, int cap, void* o, float* lse, void* workspace, int heads_per_chunk,
                            int flags, void* stream);
 
+/* ---- heads split without an all-gather: mirrored outputs ----------------------------
+ * vsp_vs_prefill, and K3's epilogue also stores every O tile (TMA) and LSE row, at the same
+ * offsets, into n_mirrors (<= 7) other buffers laid out like o / lse — in the KV-head split,
+ * the other ranks' full-layer outputs mapped into this process with vsp_ipc_open (peer HBM
+ * over NVLink/NVSwitch). Each rank then holds the assembled layer once every rank's call has
+ * completed (a stream-ordered barrier, e.g. a 1-element NCCL all-reduce): the all-gather of
+ * vsp_allgather_heads happens inside the attention kernel, overlapped with the math, instead
+ * of after it. With n_mirrors = 0 it is vsp_vs_prefill. lse_mirrors must be given iff lse is.
+ * Replaces: nothing in the reference (single-process, vsprefill.cpp:176-185); it is the
+ * multi-GPU assembly of SURVEY.md §8e. */
+VSP_API int vsp_vs_prefill_mirrored(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                                    int hkv, int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                                    const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                                    const vsp_budget* budgets, float* a_v, float* a_s, int* i_v, int* k_v, int* i_s,
+                                    int* k_s, int cap, void* o, float* lse, void* workspace, int heads_per_chunk,
+                                    int flags, int n_mirrors, void* const* o_mirrors, float* const* lse_mirrors,
+                                    void* stream);
+/* CUDA IPC for the mirrors: vsp_ipc_alloc allocates device memory on ctx's GPU and returns its
+ * 64-byte handle; another process opens it with vsp_ipc_open (peer access enabled lazily);
+ * vsp_ipc_close unmaps an opened handle, vsp_ipc_free releases an allocation. */
+VSP_API int vsp_ipc_alloc(vsp_ctx* ctx, size_t bytes, void** ptr, unsigned char* handle);
+VSP_API int vsp_ipc_open(vsp_ctx* ctx, const unsigned char* handle, void** ptr);
+VSP_API int vsp_ipc_close(void* ptr);
+VSP_API int vsp_ipc_free(void* ptr);
+
 /* ---- balanced multi-GPU split (SURVEY.md §8e refinement) -----------------------------
  * Adaptive per-head budgets make KV heads unequal (one head can carry 40% of a layer's
  * tiles), so plain head sharding leaves ranks idle. A unit is one KV head g (with its Q

@@ -34,7 +34,7 @@ __all__ = [
     "VspError", "BudgetConfig", "IndexerParams", "SelectedIndices", "make_indexer_params",
     "indexer_forward", "select_pattern", "sparse_attention", "blockwise_attention",
     "aggregate_streaming", "attention_recall", "RopeConfig", "apply_rope", "apply_rope_qk", "vs_prefill", "vs_prefill_host", "vs_prefill_unfused", "vs_prefill_units", "sparse_tile_counts", "lib_path", "load_library",
-    "topk_indices", "combine_scores", "merge_row_columns", "merge_path_partition",
+    "topk_indices", "combine_scores", "merge_row_columns", "merge_path_partition", "IpcBuffer",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -100,6 +100,13 @@ def load_library():
     lib.vsp_vs_prefill_workspace_size.argtypes = [i, i, i, i]
     lib.vsp_vs_prefill.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
                                     ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, i, vp])
+    lib.vsp_vs_prefill_mirrored.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
+                                             ctypes.POINTER(_Budget), vp, vp, vp, vp, vp, vp, i, vp, vp, vp, i, i,
+                                             i, vp, vp, vp])
+    lib.vsp_ipc_alloc.argtypes = [vp, sz, ctypes.POINTER(vp), ctypes.c_char_p]
+    lib.vsp_ipc_open.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.vsp_ipc_close.argtypes = [vp]
+    lib.vsp_ipc_free.argtypes = [vp]
     lib.vsp_apply_rope.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, vp, ctypes.c_double, i, vp]
     lib.vsp_vs_attn_tile_counts.argtypes = [vp, i, i, i, vp, vp, vp]
     lib.vsp_vs_prefill_units.argtypes = ([vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp, vp, vp, vp, i,
@@ -470,7 +477,8 @@ def merge_path_partition(a, b, p: int):
 
 def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: IndexerParams, budget,
                mapping: str = "reverse", heads_per_chunk: int = 0, out: Optional[torch.Tensor] = None,
-               lse: Optional[torch.Tensor] = None, head_major: bool = False, dense_switch: bool = False):
+               lse: Optional[torch.Tensor] = None, head_major: bool = False, dense_switch: bool = False,
+               mirrors=None):
     """The whole VS-prefill hot path of one layer in ONE C-ABI call (vsp_vs_prefill):
     indexer -> selection -> sparse attention; heads_per_chunk=0 runs them in order on the
     current stream, heads_per_chunk>0 pipelines KV-head chunks so that the
@@ -479,6 +487,9 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
     Same results as indexer_forward + select_pattern + sparse_attention.
     head_major=True writes O as [Hq, n, d] (e.g. a slab of the full output on a shard rank).
     dense_switch=True: see sparse_attention (opt-in; off = the reference's semantics).
+    mirrors: optional list of (o_ptr, lse_ptr) device addresses (ints or tensors) laid out like
+    `out` / `lse` — e.g. the same slab of other ranks' outputs mapped with IpcBuffer.open: the
+    attention epilogue stores every O tile and LSE row there too (vsp_vs_prefill_mirrored).
     Returns (O, LSE, SelectedIndices)."""
     _need_cuda(q, k, v)
     n, hq, d = q.shape
@@ -500,6 +511,18 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
                                      else torch.empty_like(q))
     lse = lse if lse is not None else torch.empty(hq, n, device=dev, dtype=torch.float32)
     ws = _workspace(dev, lib.vsp_vs_prefill_workspace_size(n, hkv, params.d_h, cap))
+    flags = (VSP_O_HEAD_MAJOR if head_major else 0) | (VSP_DENSE_SWITCH if dense_switch else 0)
+    if mirrors:
+        addr = lambda x: None if x is None else (x.data_ptr() if isinstance(x, torch.Tensor) else int(x))
+        om = (ctypes.c_void_p * len(mirrors))(*[addr(m[0]) for m in mirrors])
+        lm = (ctypes.c_void_p * len(mirrors))(*[addr(m[1]) for m in mirrors])
+        _check(lib.vsp_vs_prefill_mirrored(
+            _context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h, _ptr(params.w_u), _ptr(params.b_u),
+            _ptr(params.w_v), _ptr(params.b_v), _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1,
+            arr, _ptr(a_v), _ptr(a_s), _ptr(i_v), _ptr(k_v), _ptr(i_s), _ptr(k_s), cap, _ptr(o), _ptr(lse), _ptr(ws),
+            int(heads_per_chunk), flags, len(mirrors), ctypes.cast(om, ctypes.c_void_p),
+            ctypes.cast(lm, ctypes.c_void_p), _stream(dev)))
+        return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
     _check(lib.vsp_vs_prefill(_context(dev), _ptr(q), _ptr(k), _ptr(v), n, hq, hkv, d, params.d_h,
                               _ptr(params.w_u), _ptr(params.b_u), _ptr(params.w_v), _ptr(params.b_v),
                               _ptr(params.w_s), _ptr(params.b_s), 0 if mapping == "reverse" else 1, arr,
@@ -508,6 +531,60 @@ def vs_prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, params: Indexe
                               (VSP_O_HEAD_MAJOR if head_major else 0) | (VSP_DENSE_SWITCH if dense_switch else 0),
                               _stream(dev)))
     return o, lse, SelectedIndices(i_v, k_v, i_s, k_s)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (torch.as_tensor wraps it, no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "strides": None, "version": 3}
+        self._owner = owner
+
+
+class IpcBuffer:
+    """Device memory another process can map (vsp_ipc_alloc / vsp_ipc_open): the KV-head split's
+    full-layer output, into which every rank's attention epilogue stores its slab directly
+    (vs_prefill(mirrors=...)). `handle` (64 bytes) travels to the other ranks, which call
+    IpcBuffer.open(handle, nbytes, device)."""
+
+    def __init__(self, nbytes: int, device, _ptr_handle=None):
+        self.device = torch.device(device)
+        self.nbytes = int(nbytes)
+        lib = load_library()
+        ptr = ctypes.c_void_p()
+        if _ptr_handle is None:
+            hbuf = ctypes.create_string_buffer(64)
+            _check(lib.vsp_ipc_alloc(_context(self.device), self.nbytes, ctypes.byref(ptr), hbuf))
+            self.handle, self.opened = hbuf.raw, False
+        else:
+            self.handle = bytes(_ptr_handle)
+            _check(lib.vsp_ipc_open(_context(self.device), self.handle, ctypes.byref(ptr)))
+            self.opened = True
+        self.ptr = int(ptr.value)
+
+    @classmethod
+    def open(cls, handle: bytes, nbytes: int, device) -> "IpcBuffer":
+        return cls(nbytes, device, _ptr_handle=handle)
+
+    def tensor(self, dtype: torch.dtype, shape, offset_bytes: int = 0) -> torch.Tensor:
+        """A torch view of [offset, offset + numel * itemsize) (bf16 through an int16 view)."""
+        numel = 1
+        for x in shape:
+            numel *= int(x)
+        item = torch.empty((), dtype=dtype).element_size()
+        if offset_bytes + numel * item > self.nbytes:
+            raise VspError("IpcBuffer.tensor: view exceeds the buffer")
+        code = {torch.bfloat16: "<i2", torch.float16: "<f2", torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+        t = torch.as_tensor(_CudaArray(self.ptr + offset_bytes, shape, code, self), device=self.device)
+        return t.view(dtype) if dtype == torch.bfloat16 else t
+
+    def close(self):
+        if self.ptr:
+            lib = load_library()
+            _check(lib.vsp_ipc_close(ctypes.c_void_p(self.ptr)) if self.opened else
+                   lib.vsp_ipc_free(ctypes.c_void_p(self.ptr)))
+            self.ptr = 0
 
 
 class _Unit(ctypes.Structure):

@@ -8,6 +8,11 @@
 
 namespace vsp_attn {
 
+// Output mirrors: every O tile / LSE row is also stored, at the same offsets, into up to
+// kMaxMirrors other buffers of the same layout (peer GPUs' outputs mapped over NVLink, so the
+// heads split needs no all-gather after the layer).
+constexpr int kMaxMirrors = 7;
+
 struct __align__(64) AttnParams {
     CUtensorMap map_q;   // [n, hq, 128] bf16, box {64, 1, 128}
     CUtensorMap map_k;   // [n, hkv, 128]
@@ -15,6 +20,9 @@ struct __align__(64) AttnParams {
     CUtensorMap map_kv;  // gathered verticals [hkv, kvcap, 128], box {64, 128, 1}
     CUtensorMap map_vv;
     CUtensorMap map_o;   // O for the epilogue's TMA stores: dims (128, hq, n) with the layout's strides
+    CUtensorMap map_o_mirror[kMaxMirrors];  // the same map over each mirror buffer
+    float* lse_mirror[kMaxMirrors];
+    int n_mirrors;
     __nv_bfloat16* o;    // row i of head h at o + i * o_tok_stride + h * o_head_stride
     float* lse;          // [hq, n] or null
     long long o_tok_stride, o_head_stride;  // elements: [n, hq, 128] -> (hq*128, 128); head-major -> (128, n*128)
@@ -43,6 +51,9 @@ struct AttnArgs {
     int n, hq, hkv;
     float scale;
     bool o_head_major = false;
+    int n_mirrors = 0;                      // <= kMaxMirrors
+    void* const* o_mirrors = nullptr;       // [n_mirrors] buffers shaped like o
+    float* const* lse_mirrors = nullptr;    // [n_mirrors] like lse (entries may be null)
 };
 
 struct SparseArgs {

@@ -803,17 +803,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 named_bar_sync(1 + w, 128);
                 if (issuer && !(p.prefetch_q & 2)) {
                     tma_store_3d(&p.map_o, stage, hf * 64, h, i0);
+                    for (int m = 0; m < p.n_mirrors; ++m)  // the same tile into every mirror (peer HBM over NVLink)
+                        tma_store_3d(&p.map_o_mirror[m], stage, hf * 64, h, i0);
                     bulk_commit_group();
                 }
             }
         }
-        if (i < p.n && store && p.lse != nullptr)
-            p.lse[static_cast<size_t>(h) * p.n + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+        if (i < p.n && store) {
+            const float lse_i = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+            if (p.lse != nullptr) p.lse[static_cast<size_t>(h) * p.n + i] = lse_i;
+            for (int m = 0; m < p.n_mirrors; ++m)
+                if (p.lse_mirror[m] != nullptr) p.lse_mirror[m][static_cast<size_t>(h) * p.n + i] = lse_i;
+        }
         gt += num_tiles;
         }
         if (quarter == 0 && lane == 0) bulk_wait0();  // this tile's O stores are complete
     }
 
+    // mirrored outputs live in other GPUs' memory: make this CTA's stores (the TMA stores have
+    // completed, bulk_wait0 above) visible system-wide before the launch can be seen as done
+    if (p.n_mirrors > 0) __threadfence_system();
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_free<512>(tmem);
@@ -1048,6 +1057,14 @@ static bool set_o_layout(AttnParams& p, const AttnArgs& a) {
     const uint32_t box[3] = {64, 1, kBlock};
     const uint64_t dims[3] = {kHeadDim, (uint64_t)a.hq, (uint64_t)a.n};
     const uint64_t strides[2] = {static_cast<uint64_t>(p.o_head_stride) * 2, static_cast<uint64_t>(p.o_tok_stride) * 2};
+    if (a.n_mirrors < 0 || a.n_mirrors > kMaxMirrors || (a.n_mirrors > 0 && a.o_mirrors == nullptr)) return false;
+    p.n_mirrors = a.n_mirrors;
+    for (int m = 0; m < a.n_mirrors; ++m) {
+        if (a.o_mirrors[m] == nullptr ||
+            !vsp_host::make_map_bf16(&p.map_o_mirror[m], a.o_mirrors[m], 3, dims, strides, box))
+            return false;
+        p.lse_mirror[m] = a.lse_mirrors ? a.lse_mirrors[m] : nullptr;
+    }
     return vsp_host::make_map_bf16(&p.map_o, a.o, 3, dims, strides, box);
 }
 

@@ -1,6 +1,7 @@
 // capi.cu — the C ABI (include/vsp_gpu.h): argument checks with the reference's error
 // texts, workspace sizing, and dispatch to the sm_100a kernels. No CPU fallback.
 #include <cuda_runtime.h>
+#include <cstring>
 
 #include <cstdio>
 #include <algorithm>
@@ -509,6 +510,9 @@ struct PrefillDev {
     float* lse;
     bool o_head_major;
     bool dense_switch = false;
+    int n_mirrors = 0;                    // vsp_vs_prefill_mirrored: O / LSE also written here
+    void* const* o_mirrors = nullptr;
+    float* const* lse_mirrors = nullptr;
 };
 
 int check_prefill(int n, int hq, int hkv, int d, int d_h, int cap, int slash_mapping, const vsp_budget* budgets,
@@ -629,6 +633,9 @@ cudaError_t enqueue_prefill(vsp_ctx* ctx, const PrefillDev& p, int n, int hq, in
         if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_start, 0);
     }
     vsp_attn::AttnArgs aa{p.q, p.k, p.v, p.o, p.lse, n, hq, hkv, 1.0f / sqrtf(static_cast<float>(d)), p.o_head_major};
+    aa.n_mirrors = p.n_mirrors;
+    aa.o_mirrors = p.o_mirrors;
+    aa.lse_mirrors = p.lse_mirrors;
     vsp_attn::SparseArgs sa{p.i_v, p.k_v, p.i_s, p.k_s, cap, p.dense_switch};
     for (int c = 0; c < chunks && e == cudaSuccess; ++c) {
         int g0, cnt;
@@ -678,6 +685,70 @@ extern "C" int vsp_vs_prefill(vsp_ctx* ctx, const void* q, const void* k, const 
                                     heads_per_chunk, as_stream(stream), nullptr, nullptr,
                                     nullptr);
     return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill");
+}
+
+extern "C" int vsp_vs_prefill_mirrored(vsp_ctx* ctx, const void* q, const void* k, const void* v, int n, int hq,
+                                       int hkv, int d, int d_h, const void* w_u, const float* b_u, const float* w_v,
+                                       const float* b_v, const float* w_s, const float* b_s, int slash_mapping,
+                                       const vsp_budget* budgets, float* a_v, float* a_s, int* i_v, int* k_v,
+                                       int* i_s, int* k_s, int cap, void* o, float* lse, void* workspace,
+                                       int heads_per_chunk, int flags, int n_mirrors, void* const* o_mirrors,
+                                       float* const* lse_mirrors, void* stream) {
+    VSP_CHECK_CTX(ctx);
+    int rc = check_prefill(n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace, heads_per_chunk,
+                           "vsp_vs_prefill_mirrored");
+    if (rc) return rc;
+    if (flags & ~(VSP_O_HEAD_MAJOR | VSP_DENSE_SWITCH))
+        return set_err(VSP_EINVAL, "vsp_vs_prefill_mirrored: unknown flags");
+    if (n_mirrors < 0 || n_mirrors > vsp_attn::kMaxMirrors)
+        return set_err(VSP_EINVAL, "vsp_vs_prefill_mirrored: at most 7 mirrors");
+    if (n_mirrors > 0 && o_mirrors == nullptr) return set_err(VSP_EINVAL, "vsp_vs_prefill_mirrored: null mirror list");
+    for (int m = 0; m < n_mirrors; ++m) {
+        if (o_mirrors[m] == nullptr) return set_err(VSP_EINVAL, "vsp_vs_prefill_mirrored: null O mirror");
+        if ((lse == nullptr) != (lse_mirrors == nullptr || lse_mirrors[m] == nullptr))
+            return set_err(VSP_EINVAL, "vsp_vs_prefill_mirrored: LSE mirrors must match lse");
+    }
+    PrefillDev p{q, k, v, w_u, b_u, w_v, b_v, w_s, b_s, a_v, a_s, i_v, k_v, i_s, k_s, o, lse,
+                 (flags & VSP_O_HEAD_MAJOR) != 0, (flags & VSP_DENSE_SWITCH) != 0};
+    p.n_mirrors = n_mirrors;
+    p.o_mirrors = o_mirrors;
+    p.lse_mirrors = lse_mirrors;
+    cudaError_t e = enqueue_prefill(ctx, p, n, hq, hkv, d, d_h, cap, slash_mapping, budgets, workspace,
+                                    heads_per_chunk, as_stream(stream), nullptr, nullptr, nullptr);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_vs_prefill_mirrored");
+}
+
+// ---- CUDA IPC: device buffers another process (a peer GPU's rank) can map
+extern "C" int vsp_ipc_alloc(vsp_ctx* ctx, size_t bytes, void** ptr, unsigned char* handle) {
+    VSP_CHECK_CTX(ctx);
+    if (!ptr || !handle || bytes == 0) return set_err(VSP_EINVAL, "vsp_ipc_alloc: bad arguments");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e == cudaSuccess) e = cudaMalloc(ptr, bytes);
+    cudaIpcMemHandle_t h;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, *ptr);
+    if (e != cudaSuccess) return cuda_err(e, "vsp_ipc_alloc");
+    std::memcpy(handle, &h, sizeof(h));
+    return VSP_OK;
+}
+
+extern "C" int vsp_ipc_open(vsp_ctx* ctx, const unsigned char* handle, void** ptr) {
+    VSP_CHECK_CTX(ctx);
+    if (!ptr || !handle) return set_err(VSP_EINVAL, "vsp_ipc_open: bad arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_ipc_open");
+}
+
+extern "C" int vsp_ipc_close(void* ptr) {
+    const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_ipc_close");
+}
+
+extern "C" int vsp_ipc_free(void* ptr) {
+    const cudaError_t e = cudaFree(ptr);
+    return e == cudaSuccess ? VSP_OK : cuda_err(e, "vsp_ipc_free");
 }
 
 // per (KV head, query block) tile counts of the last plan on `workspace` -> host [hkv, num_qb]
