@@ -92,6 +92,10 @@ def parse(argv=None):
                          "units with replicated inputs, or spread (every head split across the ranks)")
     ap.add_argument("--head-placement", choices=["cost", "contiguous"], default="cost",
                     help="heads split at N>1: whole KV heads placed by predicted cost (default) or contiguous slabs")
+    ap.add_argument("--assemble", choices=["nccl", "mirror"], default="nccl",
+                    help="heads split at N>1: assemble O with an NCCL all-gather after the layer (timed "
+                         "separately), or inside K3 — every rank's epilogue also stores its slab into the other "
+                         "ranks' outputs (CUDA IPC over NVLink; vsp_vs_prefill_mirrored) — inside the timed step")
     ap.add_argument("--heads-per-chunk", type=int, default=0,
                     help="KV heads per pipeline chunk of vsp_vs_prefill (indexer/select of chunk c+1 overlap attention of c)")
     ap.add_argument("--e2e-heads-per-chunk", type=int, default=0)
@@ -392,7 +396,10 @@ def workload_config(args, world, budgets, info) -> dict:
                         f"static cost table from a validation prompt)" if balanced else
                         f"kv-head shard x{world}" + (" (whole KV heads placed by the predicted cost of a validation "
                                                      "prompt, equal counts)" if world > 1 and args.head_placement == "cost"
-                                                     else "")),
+                                                     else "") +
+                        ("; O assembled inside the attention kernel (epilogue stores into the peers' outputs over "
+                         "CUDA IPC, one 1-element all-reduce barrier per step), timed in the step"
+                         if world > 1 and getattr(args, "assemble", "nccl") == "mirror" else "")),
     }
 
 
@@ -622,8 +629,25 @@ def main():
         del q_host, k_host, v_host
     # O is written head-major straight into this rank's slab of the full [Hq, n, d] output
     # (VSP_O_HEAD_MAJOR): the slab is the in-place all-gather send buffer (parallel.py)
-    o_full = torch.empty(args.hq, n, 128, dtype=q.dtype, device=dev)
-    lse_full = torch.empty(args.hq, n, device=dev)
+    mirror = world > 1 and not balanced and args.assemble == "mirror"
+    mirrors = ipc_bufs = None
+    if mirror:
+        # the full outputs are CUDA-IPC allocations; every rank maps the others' and K3 stores
+        # its slab (placement order) into all of them (vsp_vs_prefill_mirrored)
+        obytes, lbytes = args.hq * n * 128 * 2, args.hq * n * 4
+        ipc_bufs = [vsp.IpcBuffer(obytes, dev), vsp.IpcBuffer(lbytes, dev)]
+        handles = [None] * world
+        torch.distributed.all_gather_object(handles, [ipc_bufs[0].handle, ipc_bufs[1].handle])
+        peers = [(vsp.IpcBuffer.open(h[0], obytes, dev), vsp.IpcBuffer.open(h[1], lbytes, dev))
+                 for r_, h in enumerate(handles) if r_ != rank]
+        slab_o, slab_l = rank * hq_r * n * 128 * 2, rank * hq_r * n * 4
+        mirrors = [(po.ptr + slab_o, pl.ptr + slab_l) for po, pl in peers]
+        o_full = ipc_bufs[0].tensor(torch.bfloat16, (args.hq, n, 128))
+        lse_full = ipc_bufs[1].tensor(torch.float32, (args.hq, n))
+        flag = torch.zeros(1, device=dev)
+    else:
+        o_full = torch.empty(args.hq, n, 128, dtype=q.dtype, device=dev)
+        lse_full = torch.empty(args.hq, n, device=dev)
     o = parallel.head_slab(o_full, srank, sworld)
     lse = parallel.head_slab(lse_full, srank, sworld)
 
@@ -635,7 +659,14 @@ def main():
             # rank's units touch, then attention of exactly its units
             return vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
         # one C-ABI call (vsp_vs_prefill): K1 -> K2 -> plan -> K3 (automatic schedule unless --heads-per-chunk)
-        _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse, head_major=True)
+        _, _, pat = vsp.vs_prefill(q, k, v, params, budget, heads_per_chunk=hpc, out=o, lse=lse, head_major=True,
+                                   mirrors=mirrors)
+        if mirror:  # every rank's stores have landed once every rank's layer has finished
+            if backend == "nccl":
+                torch.distributed.all_reduce(flag)  # stream-ordered
+            else:  # shared-GPU test mode (gloo)
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
         return pat
 
     def step_unfused():
@@ -718,7 +749,17 @@ def main():
 
     # ---- output assembly over NCCL, reported separately (not inside the step)
     allgather_ms = None
-    if world > 1 and backend == "nccl":
+    mirror_check = None
+    if mirror:
+        # every rank must hold identical slabs: compare per-slab checksums across the ranks
+        step()
+        torch.cuda.synchronize()
+        sums = torch.stack([s_.double().sum() for s_ in o_full.view(torch.int16).float().chunk(world, 0)])
+        sums = sums.to(red_dev)
+        all_sums = [torch.zeros_like(sums) for _ in range(world)]
+        torch.distributed.all_gather(all_sums, sums)
+        mirror_check = bool(all(torch.equal(a.cpu(), all_sums[0].cpu()) for a in all_sums))
+    elif world > 1 and backend == "nccl":
         comm = parallel.VspComm(dev)
         if balanced:  # unit regions broadcast by their owners (vsp_assemble_units)
             vsp.vs_prefill_units(q, k, v, params, budget, units, out=o_full, lse=lse_full)
@@ -834,6 +875,9 @@ def main():
             "indexer_ms": ms_indexer, "select_ms": ms_select, "recall": recall,
             "density": pairs_q / dense_pairs, "tile_density": tiles / tiles_dense,
             "k_v": kv_list, "k_s": ks_list, "dense_tflops": dense_tf, "allgather_ms": allgather_ms,
+            "assembly": ("mirrored K3 stores (inside the step)" if mirror else
+                         ("NCCL after the step (allgather_ms)" if world > 1 else None)),
+            "mirror_check": mirror_check,
             "roofline": {"bound": "tensor", "kernel": "vs_attn_fwd (K3)", "achieved": achieved_tf,
                          "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                          "traffic": k3_traffic(), "algorithmic_bytes": alg_bytes,
