@@ -225,6 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                     const float4* bh4 = reinterpret_cast<const float4*>(s_bh + col0);
                     const float4* wv4 = reinterpret_cast<const float4*>(s_wv + col0);
                     const float4* ws4 = reinterpret_cast<const float4*>(s_ws + col0);
+#ifdef VSP_K1_NOEPI  // probe (tools/dev/gpu_k1probe.sh): accumulator hand-off only, no SiLU / dots
+                    lv.x += __uint_as_float(u[0]);
+                    if (false)
+#endif
 #pragma unroll
                     for (int x4 = 0; x4 < 8; ++x4) {
                         const float4 b = bh4[x4], wv = wv4[x4], ws = ws4[x4];
