@@ -41,6 +41,7 @@ constexpr int kEpiParts = 4;                        // epilogue warps per TMEM l
 constexpr int kEpiWarps = 4 * kEpiParts;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;          // warp0 TMA, warp1 MMA, then the epilogue
+constexpr int kDefaultMc = 1;                       // W_U multicast cluster size
 
 struct __align__(64) Params {
     CUtensorMap map_k, map_v, map_w;
@@ -76,6 +77,18 @@ VSP_DEVICE float tanh_f(float h) {
 // W_U from L2. The X tile is double-buffered across work items and the W_U stream and the
 // TMEM accumulators run continuously across them, so loads, MMAs and the epilogue of
 // consecutive tiles overlap.
+//
+// kMc > 1 (opt-in, VSP_K1_MC = 2 / 4): clusters of kMc CTAs take kMc consecutive token tiles of one head (a tile group)
+// and share the W_U stream: each CTA TMA-loads 4/kMc of the four 64-column boxes of every
+// stage and multicasts them to the whole cluster, so the W_U bytes read from L2 per token
+// drop kMc-fold (at 128k x 8 heads the 512 KB-per-tile stream was ~14 TB/s of L2 reads). A
+// ring slot is released by every CTA's MMA (multicast tcgen05.commit, kMc arrivals) before
+// any CTA refills it. Tiles past the head's end (tiles % kMc != 0) load tile 0 again and store
+// nothing, so every CTA of a cluster consumes the same stream. Measured at 128k x 8 heads
+// (tools/dev/gpu_k1mc.sh, ncu): L2 bytes 4.43 -> 3.26 / 2.20 GB but 465 -> 481 / 835 us (the
+// lockstep of the pair costs more than the L2 traffic; 4-CTA clusters do not all fit), so the
+// W_U stream's L2 bandwidth is not what bounds K1 and the default stays one CTA per tile.
+template <int kMc>
 __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // offset from smem_raw (not a cast through an integer) so the compiler keeps the
@@ -90,7 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     __shared__ Smem sm;
 
     const int num_chunks = p.d_h / kChunkN;
-    const int total = p.tiles * p.count;
+    const int groups_per_head = (p.tiles + kMc - 1) / kMc;
+    const int total = groups_per_head * p.count;  // tile groups, one per cluster at a time
+    const int cl = static_cast<int>(blockIdx.x) / kMc;
+    const int ncl = static_cast<int>(gridDim.x) / kMc;
+    const int rank = kMc > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
@@ -103,13 +120,14 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], 1);
+            mbar_init(&sm.empty[s], kMc);  // every CTA's MMA releases the (multicast) slot
         }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
     tc_fence_before();
     __syncthreads();
+    if constexpr (kMc > 1) cluster_sync();  // peers' barriers exist before any multicast / remote commit
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
@@ -122,9 +140,10 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         }
         __syncwarp();
         int it = 0, j = 0;
-        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
-            const int g = p.g0 + w / p.tiles;
-            const int t0 = (w % p.tiles) * kTok;
+        for (int w = cl; w < total; w += ncl, ++j) {
+            const int g = p.g0 + w / groups_per_head;
+            const int tile = (w % groups_per_head) * kMc + rank;
+            const int t0 = (tile < p.tiles ? tile : 0) * kTok;  // past the end: any valid tile, no store
             const int buf = j & 1;
             if (j >= 2) mbar_wait(&sm.a_empty[buf], ((j >> 1) & 1) ^ 1);
             if (elect_one()) {
@@ -141,21 +160,33 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                     const int s = it % kStages;
                     if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
-                        for (int nb = 0; nb < kChunkN / 64; ++nb)
-                            tma_load_3d(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
-                                        c * kChunkN + nb * 64, ks * kStageK, g);
+                        mbar_arrive_expect_tx(&sm.full[s], kStageBytes);  // all kMc CTAs' boxes land here
+                        if constexpr (kMc == 1) {
+                            for (int nb = 0; nb < kChunkN / 64; ++nb)
+                                tma_load_3d(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
+                                            c * kChunkN + nb * 64, ks * kStageK, g);
+                        } else {
+                            for (int nb = rank; nb < kChunkN / 64; nb += kMc)
+                                tma_load_3d_mc(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
+                                               c * kChunkN + nb * 64, ks * kStageK, g, (1u << kMc) - 1u);
+                        }
                     }
                     __syncwarp();
                 }
             }
+        }
+        if constexpr (kMc > 1) {
+            // drain: every CTA's commit for the last use of each slot has arrived here before
+            // the cluster may exit (no remote arrive left in flight towards this CTA)
+            for (int i = it; i < it + kStages; ++i)
+                if (i >= kStages) mbar_wait(&sm.empty[i % kStages], ((i / kStages) & 1) ^ 1);
         }
     } else if (warp == 1) {
         // MMA issuer: warp-uniform loop, one elected lane issues each batch
         const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
         const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), kStageK * 128, 1024);
         int it = 0, cc = 0, j = 0;
-        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
+        for (int w = cl; w < total; w += ncl, ++j) {
             const int buf = j & 1;
             const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + buf * kABytes), 16, 1024);
             mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
@@ -176,7 +207,10 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                             const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kStageBytes + kk * 2048) >> 4);
                             umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
                         }
-                        umma_commit(&sm.empty[s]);
+                        if constexpr (kMc == 1)
+                            umma_commit(&sm.empty[s]);
+                        else
+                            umma_commit_mc(&sm.empty[s], (1u << kMc) - 1u);
                         if (ks == 256 / kStageK - 1) {
                             umma_commit(&sm.acc_full[acc]);
                             if (c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
@@ -195,9 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         const int et = threadIdx.x - 64;  // 0..kEpiThreads-1
         int cc = 0, j = 0, cur_g = -1;
-        for (int w = blockIdx.x; w < total; w += gridDim.x, ++j) {
-            const int g = p.g0 + w / p.tiles;
-            const int t = (w % p.tiles) * kTok + r;
+        for (int w = cl; w < total; w += ncl, ++j) {
+            const int g = p.g0 + w / groups_per_head;
+            const int t = ((w % groups_per_head) * kMc + rank) * kTok + r;  // >= n past the end: no store
             if (g != cur_g) {  // head change: everyone is past the previous tile's exchange
                 for (int i = et; i < p.d_h; i += kEpiThreads) {
                     s_bh[i] = 0.5f * p.b_u[static_cast<size_t>(g) * p.d_h + i];
@@ -274,6 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_free<512>(tmem);
+    // no CTA of a cluster leaves while a peer may still multicast into it or arrive on it
+    if constexpr (kMc > 1) cluster_sync();
 }
 
 constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 2 * (kEpiParts - 1) * 256 * 4 + 1024;
@@ -311,17 +347,39 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.reverse = a.reverse ? 1 : 0;
     static std::once_flag attr[vsp_detail::kMaxDevices];
     vsp_detail::once_per_device(attr, [] {
-        cudaFuncSetAttribute(indexer_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     });
     const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
     p.g0 = a.g0;
     p.count = count;
     p.tiles = (a.n + kTok - 1) / kTok;
     const int sms = vsp_detail::current_sm_count();
-    const int work = p.tiles * count;
+    // W_U multicast cluster size (VSP_K1_MC = 1 / 2 / 4); single tiles need no sharing
+    int mc = kDefaultMc;
+    if (const char* s = getenv("VSP_K1_MC")) mc = atoi(s);
+    if (mc != 1 && mc != 2 && mc != 4) mc = kDefaultMc;
+    if (p.tiles < 2) mc = 1;
+    const int groups = ((p.tiles + mc - 1) / mc) * count;
+    const int clusters = std::max(1, std::min(groups, sms / mc));
     vsp_detail::count_launch();
-    indexer_gemm_kernel<<<work < sms ? work : sms, kThreads, kSmemBytes, stream>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * mc);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = mc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = mc == 4   ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<4>, p)
+                    : mc == 2 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<2>, p)
+                              : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<1>, p);
+    if (e == cudaSuccess) e = cudaGetLastError();
     // A_v / A_s: the cluster softmax shared with the selection kernel (a_v null: logits only,
     // the layer path softmaxes inside selection)
     if (e == cudaSuccess && a.a_v) e = vsp_select_k::launch_softmax(lv, ls, a.a_v, a.a_s, a.n, a.g0, count, stream);

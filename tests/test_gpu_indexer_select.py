@@ -333,3 +333,22 @@ def test_vs_prefill_host_rejects_device_tensors(vsp):
     p = _params(vsp, 2, 256, seed=1, sigma=0.5)
     with pytest.raises(vsp.VspError, match="contiguous host tensors"):
         vsp.vs_prefill_host(q, k.cpu(), v.cpu(), p, vsp.BudgetConfig())
+
+
+@pytest.mark.parametrize("n,hkv", [(129, 2), (300, 3), (641, 2), (4099, 3), (131072, 1)])
+def test_indexer_w_multicast_clusters_identical(vsp, n, hkv, monkeypatch):
+    """K1 shares the W_U stream across clusters of VSP_K1_MC CTAs (TMA multicast); ragged tile
+    counts leave phantom tiles in the last group. Every cluster size gives the same bits."""
+    g = torch.Generator().manual_seed(n + hkv)
+    k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    p = _params(vsp, hkv, 512, seed=n)
+    outs = []
+    for mc in ("1", "2", "4"):
+        monkeypatch.setenv("VSP_K1_MC", mc)
+        _, _, lv, ls = vsp.indexer_forward(k, v, p, want_logits=True)
+        torch.cuda.synchronize()
+        outs.append((lv.clone(), ls.clone()))
+    for lv, ls in outs[1:]:
+        assert torch.equal(lv, outs[0][0]) and torch.equal(ls, outs[0][1])
+    assert bool(torch.isfinite(outs[0][0]).all())
