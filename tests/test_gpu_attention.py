@@ -295,3 +295,18 @@ def test_multicast_clusters_bit_identical(vsp, monkeypatch):
     d_1 = vsp.blockwise_attention(q, k, v)
     assert torch.equal(o_mc, o_1) and torch.equal(lse_mc, lse_1)
     assert torch.equal(d_mc[0], d_1[0]) and torch.equal(d_mc[1], d_1[1])
+
+
+@pytest.mark.parametrize("n,hq", [(1, 3), (7, 2), (4099, 5), (131075, 32)])
+def test_recall_from_lse_cluster_sum_matches_fp64(vsp, n, hq):
+    """vsp_recall_from_lse splits each head over an 8-CTA cluster (fixed slices, partials added
+    in rank order): equal to the fp64 mean of exp(LSE_s - LSE_d), rounded once to fp32, and
+    identical across calls."""
+    g = torch.Generator().manual_seed(n)
+    ld = torch.randn(hq, n, generator=g) * 3.0
+    ls = ld - torch.rand(hq, n, generator=g) * 2.0
+    rec = vsp.attention_recall(ls.cuda(), ld.cuda())
+    rec2 = vsp.attention_recall(ls.cuda(), ld.cuda())
+    want = torch.exp(ls.double() - ld.double()).mean(dim=1)
+    assert torch.equal(rec, rec2)
+    assert float(((rec.cpu().double() - want).abs() / want).max()) <= 2e-7
