@@ -32,16 +32,16 @@ namespace vsp_indexer {
 
 constexpr int kTok = 128;
 constexpr int kChunkN = 256;
-constexpr int kStageK = 32;
-constexpr int kStages = 4;
+constexpr int kDefaultStageK = 32;                  // W_U K-rows per ring stage (VSP_K1_STAGEK)
 constexpr int kABytes = kTok * 256 * 2;             // 64 KB per token tile
-constexpr int kStageBytes = kStageK * kChunkN * 2;  // 16 KB
+constexpr int kRingBytes = 64 * 1024;               // W_U ring: 4 x 16 KB (one CTA) / 8 x 8 KB (pair)
+constexpr int kMaxStages = 8;
 constexpr int kMaxDh = 2048;
 constexpr int kEpiParts = 4;                        // epilogue warps per TMEM lane quarter
 constexpr int kEpiWarps = 4 * kEpiParts;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;          // warp0 TMA, warp1 MMA, then the epilogue
-constexpr int kDefaultMc = 1;                       // W_U multicast cluster size
+constexpr int kDefaultMc = 1;                       // 1: one CTA per tile; 2: CTA pairs (cta_group::2)
 
 struct __align__(64) Params {
     CUtensorMap map_k, map_v, map_w;
@@ -60,7 +60,7 @@ struct __align__(64) Params {
 
 struct Smem {
     uint64_t a_full[2], a_empty[2];
-    uint64_t full[kStages], empty[kStages];
+    uint64_t full[kMaxStages], empty[kMaxStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
 };
@@ -78,25 +78,35 @@ VSP_DEVICE float tanh_f(float h) {
 // TMEM accumulators run continuously across them, so loads, MMAs and the epilogue of
 // consecutive tiles overlap.
 //
-// kMc > 1 (opt-in, VSP_K1_MC = 2 / 4): clusters of kMc CTAs take kMc consecutive token tiles of one head (a tile group)
-// and share the W_U stream: each CTA TMA-loads 4/kMc of the four 64-column boxes of every
-// stage and multicasts them to the whole cluster, so the W_U bytes read from L2 per token
-// drop kMc-fold (at 128k x 8 heads the 512 KB-per-tile stream was ~14 TB/s of L2 reads). A
-// ring slot is released by every CTA's MMA (multicast tcgen05.commit, kMc arrivals) before
-// any CTA refills it. Tiles past the head's end (tiles % kMc != 0) load tile 0 again and store
-// nothing, so every CTA of a cluster consumes the same stream. Measured at 128k x 8 heads
-// (tools/dev/gpu_k1mc.sh, ncu): L2 bytes 4.43 -> 3.26 / 2.20 GB but 465 -> 481 / 835 us (the
-// lockstep of the pair costs more than the L2 traffic; 4-CTA clusters do not all fit), so the
-// W_U stream's L2 bandwidth is not what bounds K1 and the default stays one CTA per tile.
-template <int kMc>
+// Opt-in variants (parity-green and bit-identical to the default, measured slower):
+//   kPair (VSP_K1_MC = 2): CTA pairs (one cluster, one TPC) take two consecutive token tiles of
+//   one head and run M = 256 tcgen05.mma.cta_group::2 MMAs issued by the leader: each CTA holds
+//   its own 128-token X tile and HALF of every W_U stage (128 of the chunk's 256 columns), so
+//   each SM receives half the W_U bytes per unit of MMA work. The peer's TMA loads complete on
+//   the leader's barriers (cta_group::2 TMA), its epilogue warps release the accumulators on
+//   the leader's acc_empty, and the leader's commits arrive on both CTAs' barriers. Tiles past
+//   a head's end (odd tile counts) load tile 0 again and store nothing.
+//   kStageK (VSP_K1_STAGEK = 32 / 64): W_U K-rows per ring stage (the ring stays 64 KB).
+// Measured at 128k x 8 heads (ncu, two rounds each, tools/dev/gpu_k1pair.sh): one CTA 32 / 64
+// K-rows 466 / 472 us, pairs 556 / 548 us. The bound probe (tools/dev/gpu_k1probe2.sh): 454 us;
+// epilogue off 388; half the MMAs 391; both 329 — the W_U/X stream pace sets a ~330 us floor,
+// but neither halving the W_U bytes per SM (pairs), nor halving the L2 reads (an earlier
+// multicast variant: 481 us), nor fewer, larger stages moves it; the pair's lockstep (both
+// epilogues must release an accumulator) costs more than it saves.
+template <bool kPair, int kStageK>
 __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
+    constexpr int kMc = kPair ? 2 : 1;
+    constexpr int kNCta = kChunkN / kMc;      // W_U columns of a stage held by this CTA
+    constexpr int kSB = kStageK * kNCta * 2;  // stage bytes per CTA: 16 KB / 8 KB
+    constexpr int kNS = kRingBytes / kSB;     // stages: 4 / 8
+    static_assert(kNS <= kMaxStages, "indexer ring");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // offset from smem_raw (not a cast through an integer) so the compiler keeps the
     // shared state space and emits LDS/STS rather than generic LD/ST
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = base;                        // 2 x 64 KB
-    uint8_t* sB = base + 2 * kABytes;          // kStages x 16 KB
-    float* s_bh = reinterpret_cast<float*>(sB + kStages * kStageBytes);  // b_U / 2
+    uint8_t* sB = base + 2 * kABytes;          // W_U ring, kRingBytes
+    float* s_bh = reinterpret_cast<float*>(sB + kRingBytes);  // b_U / 2
     float* s_wv = s_bh + kMaxDh;
     float* s_ws = s_wv + kMaxDh;
     float* s_xch = s_ws + kMaxDh;              // 2 x (kEpiParts - 1) x 256 floats (tile parity)
@@ -107,7 +117,8 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     const int total = groups_per_head * p.count;  // tile groups, one per cluster at a time
     const int cl = static_cast<int>(blockIdx.x) / kMc;
     const int ncl = static_cast<int>(gridDim.x) / kMc;
-    const int rank = kMc > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int rank = kPair ? static_cast<int>(cluster_ctarank()) : 0;
+    const bool leader = rank == 0;
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
@@ -116,18 +127,23 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             mbar_init(&sm.a_full[b], 1);
             mbar_init(&sm.a_empty[b], 1);
             mbar_init(&sm.acc_full[b], 1);
-            mbar_init(&sm.acc_empty[b], kEpiWarps);
+            mbar_init(&sm.acc_empty[b], kEpiWarps * kMc);  // both CTAs' epilogues (leader's copy)
         }
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kNS; ++s) {
             mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], kMc);  // every CTA's MMA releases the (multicast) slot
+            mbar_init(&sm.empty[s], 1);
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+    if (warp == 1) {
+        if constexpr (kPair)
+            tmem_alloc_pair<512>(&sm.tmem_base);
+        else
+            tmem_alloc<512>(&sm.tmem_base);
+    }
     tc_fence_before();
     __syncthreads();
-    if constexpr (kMc > 1) cluster_sync();  // peers' barriers exist before any multicast / remote commit
+    if constexpr (kPair) cluster_sync();  // the peer's barriers exist before any remote arrive / commit
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
@@ -147,77 +163,108 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             const int buf = j & 1;
             if (j >= 2) mbar_wait(&sm.a_empty[buf], ((j >> 1) & 1) ^ 1);
             if (elect_one()) {
-                mbar_arrive_expect_tx(&sm.a_full[buf], kABytes);
                 uint8_t* a = sA + buf * kABytes;
-                for (int hf = 0; hf < 2; ++hf) {
-                    tma_load_3d(a + hf * 16384, &p.map_k, &sm.a_full[buf], hf * 64, g, t0);
-                    tma_load_3d(a + (2 + hf) * 16384, &p.map_v, &sm.a_full[buf], hf * 64, g, t0);
+                if (leader) {
+                    mbar_arrive_expect_tx(&sm.a_full[buf], kMc * kABytes);  // the pair's tiles land on the leader's barrier
+                    for (int hf = 0; hf < 2; ++hf) {
+                        tma_load_3d(a + hf * 16384, &p.map_k, &sm.a_full[buf], hf * 64, g, t0);
+                        tma_load_3d(a + (2 + hf) * 16384, &p.map_v, &sm.a_full[buf], hf * 64, g, t0);
+                    }
+                } else if constexpr (kPair) {
+                    const uint32_t bar = mapa_shared(smem_u32(&sm.a_full[buf]), 0);
+                    for (int hf = 0; hf < 2; ++hf) {
+                        tma_load_3d_pair(a + hf * 16384, &p.map_k, bar, hf * 64, g, t0);
+                        tma_load_3d_pair(a + (2 + hf) * 16384, &p.map_v, bar, hf * 64, g, t0);
+                    }
                 }
             }
             __syncwarp();
             for (int c = 0; c < num_chunks; ++c) {
                 for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                    const int s = it % kStages;
-                    if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+                    const int s = it % kNS;
+                    if (it >= kNS) mbar_wait(&sm.empty[s], ((it / kNS) & 1) ^ 1);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(&sm.full[s], kStageBytes);  // all kMc CTAs' boxes land here
-                        if constexpr (kMc == 1) {
-                            for (int nb = 0; nb < kChunkN / 64; ++nb)
-                                tma_load_3d(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
-                                            c * kChunkN + nb * 64, ks * kStageK, g);
-                        } else {
-                            for (int nb = rank; nb < kChunkN / 64; nb += kMc)
-                                tma_load_3d_mc(sB + s * kStageBytes + nb * (kStageK * 128), &p.map_w, &sm.full[s],
-                                               c * kChunkN + nb * 64, ks * kStageK, g, (1u << kMc) - 1u);
+                        uint8_t* dst = sB + s * kSB;
+                        const int n0 = c * kChunkN + rank * kNCta;  // this CTA's columns of the chunk
+                        if (leader) {
+                            mbar_arrive_expect_tx(&sm.full[s], kMc * kSB);
+                            for (int nb = 0; nb < kNCta / 64; ++nb)
+                                tma_load_3d(dst + nb * (kStageK * 128), &p.map_w, &sm.full[s], n0 + nb * 64,
+                                            ks * kStageK, g);
+                        } else if constexpr (kPair) {
+                            const uint32_t bar = mapa_shared(smem_u32(&sm.full[s]), 0);
+                            for (int nb = 0; nb < kNCta / 64; ++nb)
+                                tma_load_3d_pair(dst + nb * (kStageK * 128), &p.map_w, bar, n0 + nb * 64, ks * kStageK, g);
                         }
                     }
                     __syncwarp();
                 }
             }
         }
-        if constexpr (kMc > 1) {
-            // drain: every CTA's commit for the last use of each slot has arrived here before
-            // the cluster may exit (no remote arrive left in flight towards this CTA)
-            for (int i = it; i < it + kStages; ++i)
-                if (i >= kStages) mbar_wait(&sm.empty[i % kStages], ((i / kStages) & 1) ^ 1);
+        if constexpr (kPair) {
+            // drain: the leader's commits for the last uses of every ring slot and X buffer have
+            // arrived here before the pair may exit (no remote arrive left in flight)
+            for (int i = it; i < it + kNS; ++i)
+                if (i >= kNS) mbar_wait(&sm.empty[i % kNS], ((i / kNS) & 1) ^ 1);
+            for (int jj = j; jj < j + 2; ++jj)
+                if (jj >= 2) mbar_wait(&sm.a_empty[jj & 1], ((jj >> 1) & 1) ^ 1);
         }
     } else if (warp == 1) {
-        // MMA issuer: warp-uniform loop, one elected lane issues each batch
-        const uint32_t idesc = umma_idesc_bf16(128, kChunkN, false, true);
-        const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), kStageK * 128, 1024);
-        int it = 0, cc = 0, j = 0;
-        for (int w = cl; w < total; w += ncl, ++j) {
-            const int buf = j & 1;
-            const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + buf * kABytes), 16, 1024);
-            mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
-            for (int c = 0; c < num_chunks; ++c, ++cc) {
-                const int acc = cc & 1;
-                if (cc >= 2) mbar_wait(&sm.acc_empty[acc], ((cc >> 1) & 1) ^ 1);
-                tc_fence_after();
-                for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
-                    const int s = it % kStages;
-                    mbar_wait(&sm.full[s], (it / kStages) & 1);
+        // MMA issuer (the pair's leader only): warp-uniform loop, one elected lane issues each batch
+        if (leader) {
+            const uint32_t idesc = umma_idesc_bf16(128 * kMc, kChunkN, false, true);
+            const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), kStageK * 128, 1024);
+            int it = 0, cc = 0, j = 0;
+            for (int w = cl; w < total; w += ncl, ++j) {
+                const int buf = j & 1;
+                const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + buf * kABytes), 16, 1024);
+                mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
+                for (int c = 0; c < num_chunks; ++c, ++cc) {
+                    const int acc = cc & 1;
+                    if (cc >= 2) mbar_wait(&sm.acc_empty[acc], ((cc >> 1) & 1) ^ 1);
                     tc_fence_after();
-                    if (elect_one()) {
+                    for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                        const int s = it % kNS;
+                        mbar_wait(&sm.full[s], (it / kNS) & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < kStageK / 16; ++kk) {
-                            const int kg = ks * kStageK + kk * 16;  // global K index (feature)
-                            const uint64_t adesc =
-                                a_desc0 + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4);
-                            const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kStageBytes + kk * 2048) >> 4);
-                            umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, (ks > 0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < kStageK / 16; ++kk) {
+#ifdef VSP_K1_HALF_MMA  // probe (tools/dev/gpu_k1probe2.sh): half the MMAs, same W/X stream
+                                if (kk & 1) continue;
+#endif
+                                const int kg = ks * kStageK + kk * 16;  // global K index (feature)
+                                const uint64_t adesc =
+                                    a_desc0 + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4);
+                                const uint64_t bdesc = b_desc0 + static_cast<uint64_t>((s * kSB + kk * 2048) >> 4);
+                                const uint32_t accum = (ks > 0 || kk > 0) ? 1u : 0u;
+                                if constexpr (kPair)
+                                    umma_ss_pair(tmem + acc * kChunkN, adesc, bdesc, idesc, accum);
+                                else
+                                    umma_ss(tmem + acc * kChunkN, adesc, bdesc, idesc, accum);
+                            }
+                            if constexpr (kPair) {
+                                umma_commit_pair_mc(&sm.empty[s], 3);
+                                if (ks == 256 / kStageK - 1) {
+                                    umma_commit_pair_mc(&sm.acc_full[acc], 3);
+                                    if (c == num_chunks - 1) umma_commit_pair_mc(&sm.a_empty[buf], 3);
+                                }
+                            } else {
+                                umma_commit(&sm.empty[s]);
+                                if (ks == 256 / kStageK - 1) {
+                                    umma_commit(&sm.acc_full[acc]);
+                                    if (c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
+                                }
+                            }
                         }
-                        if constexpr (kMc == 1)
-                            umma_commit(&sm.empty[s]);
-                        else
-                            umma_commit_mc(&sm.empty[s], (1u << kMc) - 1u);
-                        if (ks == 256 / kStageK - 1) {
-                            umma_commit(&sm.acc_full[acc]);
-                            if (c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
-                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
                 }
+            }
+            if constexpr (kPair) {
+                // drain: both epilogues' releases of the last two accumulators have arrived
+                for (int c2 = cc; c2 < cc + 2; ++c2)
+                    if (c2 >= 2) mbar_wait(&sm.acc_empty[c2 & 1], ((c2 >> 1) & 1) ^ 1);
             }
         }
     } else {
@@ -282,7 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
+                if (lane == 0) {
+                    if constexpr (kPair)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&sm.acc_empty[acc]), 0));  // the leader's
+                    else
+                        mbar_arrive(&sm.acc_empty[acc]);
+                }
             }
             const float sv = (lv.x + lv.y) + (lv1.x + lv1.y);
             const float ss = (ls.x + ls.y) + (ls1.x + ls1.y);
@@ -307,12 +359,15 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_free<512>(tmem);
-    // no CTA of a cluster leaves while a peer may still multicast into it or arrive on it
-    if constexpr (kMc > 1) cluster_sync();
+    if constexpr (kPair) {
+        cluster_sync();  // both CTAs are done with the pair's TMEM and barriers
+        if (warp == 1) tmem_free_pair<512>(tmem);
+    } else {
+        if (warp == 1) tmem_free<512>(tmem);
+    }
 }
 
-constexpr int kSmemBytes = 2 * kABytes + kStages * kStageBytes + 3 * kMaxDh * 4 + 2 * (kEpiParts - 1) * 256 * 4 + 1024;
+constexpr int kSmemBytes = 2 * kABytes + kRingBytes + 3 * kMaxDh * 4 + 2 * (kEpiParts - 1) * 256 * 4 + 1024;
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
     return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;
@@ -325,12 +380,10 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     static_assert(kSmemBytes <= 227 * 1024, "indexer smem");
     const uint64_t dk[3] = {128, (uint64_t)a.hkv, (uint64_t)a.n};
     const uint64_t sk[2] = {128 * 2, (uint64_t)a.hkv * 128 * 2};
-    const uint32_t wbox[3] = {64, kStageK, 1};
     const uint64_t dw[3] = {(uint64_t)a.d_h, 256, (uint64_t)a.hkv};
     const uint64_t sw[2] = {(uint64_t)a.d_h * 2, (uint64_t)a.d_h * 256 * 2};
     if (!vsp_host::make_map_bf16(&p.map_k, a.k, 3, dk, sk, box) ||
-        !vsp_host::make_map_bf16(&p.map_v, a.v, 3, dk, sk, box) ||
-        !vsp_host::make_map_bf16(&p.map_w, a.w_u, 3, dw, sw, wbox))
+        !vsp_host::make_map_bf16(&p.map_v, a.v, 3, dk, sk, box))
         return cudaErrorInvalidValue;
     float* lv = a.logits_v ? a.logits_v : static_cast<float*>(workspace);
     float* ls = a.logits_s ? a.logits_s : static_cast<float*>(workspace) + static_cast<size_t>(a.hkv) * a.n;
@@ -347,20 +400,26 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.reverse = a.reverse ? 1 : 0;
     static std::once_flag attr[vsp_detail::kMaxDevices];
     vsp_detail::once_per_device(attr, [] {
-        cudaFuncSetAttribute(indexer_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(indexer_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(indexer_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     });
     const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
     p.g0 = a.g0;
     p.count = count;
     p.tiles = (a.n + kTok - 1) / kTok;
     const int sms = vsp_detail::current_sm_count();
-    // W_U multicast cluster size (VSP_K1_MC = 1 / 2 / 4); single tiles need no sharing
-    int mc = kDefaultMc;
+    // VSP_K1_MC = 1: one CTA per tile; 2: CTA pairs (cta_group::2); single tiles need no pair.
+    // VSP_K1_STAGEK = 32 / 64: W_U K-rows per ring stage (the ring stays 64 KB)
+    int mc = kDefaultMc, stage_k = kDefaultStageK;
     if (const char* s = getenv("VSP_K1_MC")) mc = atoi(s);
-    if (mc != 1 && mc != 2 && mc != 4) mc = kDefaultMc;
+    if (const char* s = getenv("VSP_K1_STAGEK")) stage_k = atoi(s);
+    if (mc != 1 && mc != 2) mc = kDefaultMc;
+    if (stage_k != 32 && stage_k != 64) stage_k = kDefaultStageK;
     if (p.tiles < 2) mc = 1;
+    const uint32_t wbox[3] = {64, static_cast<uint32_t>(stage_k), 1};
+    if (!vsp_host::make_map_bf16(&p.map_w, a.w_u, 3, dw, sw, wbox)) return cudaErrorInvalidValue;
     const int groups = ((p.tiles + mc - 1) / mc) * count;
     const int clusters = std::max(1, std::min(groups, sms / mc));
     vsp_detail::count_launch();
@@ -376,9 +435,10 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = mc == 4   ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<4>, p)
-                    : mc == 2 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<2>, p)
-                              : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<1>, p);
+    cudaError_t e = mc == 2 ? (stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 64>, p)
+                                        : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 32>, p))
+                            : (stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 64>, p)
+                                        : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 32>, p));
     if (e == cudaSuccess) e = cudaGetLastError();
     // A_v / A_s: the cluster softmax shared with the selection kernel (a_v null: logits only,
     // the layer path softmaxes inside selection)

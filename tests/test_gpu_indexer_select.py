@@ -336,16 +336,19 @@ def test_vs_prefill_host_rejects_device_tensors(vsp):
 
 
 @pytest.mark.parametrize("n,hkv", [(129, 2), (300, 3), (641, 2), (4099, 3), (131072, 1)])
-def test_indexer_w_multicast_clusters_identical(vsp, n, hkv, monkeypatch):
-    """K1 shares the W_U stream across clusters of VSP_K1_MC CTAs (TMA multicast); ragged tile
-    counts leave phantom tiles in the last group. Every cluster size gives the same bits."""
+def test_indexer_cta_pairs_identical(vsp, n, hkv, monkeypatch):
+    """VSP_K1_MC = 2 runs K1 on CTA pairs (cta_group::2, M = 256, each CTA holding half of every
+    W_U stage); odd tile counts leave a phantom tile in a head's last pair. Same bits as one CTA
+    per tile (identical K order of the fp32 accumulation), for both W_U stage depths
+    (VSP_K1_STAGEK = 32 / 64 K-rows)."""
     g = torch.Generator().manual_seed(n + hkv)
     k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     p = _params(vsp, hkv, 512, seed=n)
     outs = []
-    for mc in ("1", "2", "4"):
+    for mc, sk in (("1", "32"), ("1", "64"), ("2", "32"), ("2", "64")):
         monkeypatch.setenv("VSP_K1_MC", mc)
+        monkeypatch.setenv("VSP_K1_STAGEK", sk)
         _, _, lv, ls = vsp.indexer_forward(k, v, p, want_logits=True)
         torch.cuda.synchronize()
         outs.append((lv.clone(), ls.clone()))
