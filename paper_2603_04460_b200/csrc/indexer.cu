@@ -35,12 +35,14 @@ constexpr int kChunkN = 256;
 constexpr int kDefaultStageK = 32;                  // W_U K-rows per ring stage (VSP_K1_STAGEK)
 constexpr int kABytes = kTok * 256 * 2;             // 64 KB per token tile
 constexpr int kRingBytes = 64 * 1024;               // W_U ring: 4 x 16 KB (one CTA) / 8 x 8 KB (pair)
+constexpr int kSplitRingBytes = 128 * 1024;         // split-X mode: one X tile, 8 x 16 KB W_U stages
 constexpr int kMaxStages = 8;
 constexpr int kMaxDh = 2048;
 constexpr int kEpiParts = 4;                        // epilogue warps per TMEM lane quarter
 constexpr int kEpiWarps = 4 * kEpiParts;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;          // warp0 TMA, warp1 MMA, then the epilogue
+constexpr int kDefaultSplit = 1;                    // split-X layout (VSP_K1_SPLIT)
 constexpr int kDefaultMc = 1;                       // 1: one CTA per tile; 2: CTA pairs (cta_group::2)
 
 struct __align__(64) Params {
@@ -59,7 +61,7 @@ struct __align__(64) Params {
 };
 
 struct Smem {
-    uint64_t a_full[2], a_empty[2];
+    uint64_t a_full[4], a_empty[4];  // per X buffer (2), or per 64-feature X box (split mode, 4)
     uint64_t full[kMaxStages], empty[kMaxStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
@@ -78,6 +80,10 @@ VSP_DEVICE float tanh_f(float h) {
 // TMEM accumulators run continuously across them, so loads, MMAs and the epilogue of
 // consecutive tiles overlap.
 //
+// Default layout kSplit (VSP_K1_SPLIT = 1): ONE X tile in four 16 KB boxes with per-box
+// barriers (the next item's box b loads as soon as the last chunk has consumed it), which
+// frees 64 KB for a 128 KB W_U ring: 462 -> 429 us at 128k x 8 heads (the W_U bytes in flight
+// per SM, not L2 bandwidth, bound the stream; see the probe numbers below).
 // Opt-in variants (parity-green and bit-identical to the default, measured slower):
 //   kPair (VSP_K1_MC = 2): CTA pairs (one cluster, one TPC) take two consecutive token tiles of
 //   one head and run M = 256 tcgen05.mma.cta_group::2 MMAs issued by the leader: each CTA holds
@@ -93,20 +99,22 @@ VSP_DEVICE float tanh_f(float h) {
 // but neither halving the W_U bytes per SM (pairs), nor halving the L2 reads (an earlier
 // multicast variant: 481 us), nor fewer, larger stages moves it; the pair's lockstep (both
 // epilogues must release an accumulator) costs more than it saves.
-template <bool kPair, int kStageK>
+template <bool kPair, int kStageK, bool kSplit>
 __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_constant__ Params p) {
+    static_assert(!kSplit || (!kPair && kStageK == 32), "split-X mode: one CTA, 32-row stages");
     constexpr int kMc = kPair ? 2 : 1;
     constexpr int kNCta = kChunkN / kMc;      // W_U columns of a stage held by this CTA
     constexpr int kSB = kStageK * kNCta * 2;  // stage bytes per CTA: 16 KB / 8 KB
-    constexpr int kNS = kRingBytes / kSB;     // stages: 4 / 8
+    constexpr int kRing = kSplit ? kSplitRingBytes : kRingBytes;
+    constexpr int kNS = kRing / kSB;          // stages: 4 / 8 (pairs, split-X)
     static_assert(kNS <= kMaxStages, "indexer ring");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // offset from smem_raw (not a cast through an integer) so the compiler keeps the
     // shared state space and emits LDS/STS rather than generic LD/ST
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* sA = base;                        // 2 x 64 KB
-    uint8_t* sB = base + 2 * kABytes;          // W_U ring, kRingBytes
-    float* s_bh = reinterpret_cast<float*>(sB + kRingBytes);  // b_U / 2
+    uint8_t* sA = base;                        // 2 x 64 KB (split-X: 1 x 64 KB)
+    uint8_t* sB = base + (kSplit ? 1 : 2) * kABytes;  // W_U ring
+    float* s_bh = reinterpret_cast<float*>(sB + kRing);  // b_U / 2
     float* s_wv = s_bh + kMaxDh;
     float* s_ws = s_wv + kMaxDh;
     float* s_xch = s_ws + kMaxDh;              // 2 x (kEpiParts - 1) x 256 floats (tile parity)
@@ -123,9 +131,11 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
     const uint32_t lane = lane_id();
 
     if (warp == 0 && lane == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(&sm.a_full[b], 1);
             mbar_init(&sm.a_empty[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(&sm.acc_full[b], 1);
             mbar_init(&sm.acc_empty[b], kEpiWarps * kMc);  // both CTAs' epilogues (leader's copy)
         }
@@ -156,6 +166,56 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
         }
         __syncwarp();
         int it = 0, j = 0;
+        if constexpr (kSplit) {
+            // One X tile in four 16 KB boxes (features 0-63 / 64-127 of K, then of V), each with
+            // its own full/empty barrier: the MMA releases box b of item j as soon as the last
+            // chunk's stages over features [64b, 64b + 64) have run, and box b of item j + 1 is
+            // loaded then, while the rest of the last chunk runs. The freed 64 KB doubles the
+            // W_U ring. Boxes are polled without blocking between W_U stages; all four must be
+            // issued before any stage that only the item's later chunks (or the next item) need.
+            uint32_t pend = 0;
+            int jp = 0, gp = 0, t0p = 0;
+            auto issue_x = [&](bool block) {
+                for (int b = 0; b < 4; ++b) {
+                    if (!((pend >> b) & 1u)) continue;
+                    if (jp >= 1) {
+                        const uint32_t par = static_cast<uint32_t>((jp - 1) & 1);
+                        if (block)
+                            mbar_wait(&sm.a_empty[b], par);
+                        else if (!__all_sync(0xffffffffu, mbar_test(&sm.a_empty[b], par)))
+                            break;  // released in box order
+                    }
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&sm.a_full[b], 16384);
+                        tma_load_3d(sA + b * 16384, b < 2 ? &p.map_k : &p.map_v, &sm.a_full[b], (b & 1) * 64, gp, t0p);
+                    }
+                    __syncwarp();
+                    pend &= ~(1u << b);
+                }
+            };
+            for (int w = cl; w < total; w += ncl, ++j) {
+                const int g = p.g0 + w / groups_per_head;
+                const int t0 = (w % groups_per_head) * kTok;
+                issue_x(true);  // the previous item's boxes (single-chunk items)
+                jp = j, gp = g, t0p = t0, pend = 0xFu;
+                issue_x(false);
+                for (int c = 0; c < num_chunks; ++c) {
+                    for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
+                        if (pend) issue_x(c >= 1);
+                        const int s = it % kNS;
+                        if (it >= kNS) mbar_wait(&sm.empty[s], ((it / kNS) & 1) ^ 1);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&sm.full[s], kSB);
+                            for (int nb = 0; nb < kChunkN / 64; ++nb)
+                                tma_load_3d(sB + s * kSB + nb * (kStageK * 128), &p.map_w, &sm.full[s],
+                                            c * kChunkN + nb * 64, ks * kStageK, g);
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            issue_x(true);
+        } else
         for (int w = cl; w < total; w += ncl, ++j) {
             const int g = p.g0 + w / groups_per_head;
             const int tile = (w % groups_per_head) * kMc + rank;
@@ -216,9 +276,9 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
             const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), kStageK * 128, 1024);
             int it = 0, cc = 0, j = 0;
             for (int w = cl; w < total; w += ncl, ++j) {
-                const int buf = j & 1;
+                const int buf = kSplit ? 0 : (j & 1);
                 const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + buf * kABytes), 16, 1024);
-                mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
+                if constexpr (!kSplit) mbar_wait(&sm.a_full[buf], (j >> 1) & 1);
                 for (int c = 0; c < num_chunks; ++c, ++cc) {
                     const int acc = cc & 1;
                     if (cc >= 2) mbar_wait(&sm.acc_empty[acc], ((cc >> 1) & 1) ^ 1);
@@ -226,6 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                     for (int ks = 0; ks < 256 / kStageK; ++ks, ++it) {
                         const int s = it % kNS;
                         mbar_wait(&sm.full[s], (it / kNS) & 1);
+                        if constexpr (kSplit)  // first stage over X box b in this item
+                            if (c == 0 && ((ks * kStageK) & 63) == 0) mbar_wait(&sm.a_full[(ks * kStageK) >> 6], j & 1);
                         tc_fence_after();
                         if (elect_one()) {
 #pragma unroll
@@ -251,9 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
                                 }
                             } else {
                                 umma_commit(&sm.empty[s]);
+                                if constexpr (kSplit)  // last chunk done with X box b: release it
+                                    if (c == num_chunks - 1 && ((ks * kStageK + kStageK) & 63) == 0)
+                                        umma_commit(&sm.a_empty[(ks * kStageK) >> 6]);
                                 if (ks == 256 / kStageK - 1) {
                                     umma_commit(&sm.acc_full[acc]);
-                                    if (c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
+                                    if (!kSplit && c == num_chunks - 1) umma_commit(&sm.a_empty[buf]);
                                 }
                             }
                         }
@@ -368,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) indexer_gemm_kernel(const __grid_
 }
 
 constexpr int kSmemBytes = 2 * kABytes + kRingBytes + 3 * kMaxDh * 4 + 2 * (kEpiParts - 1) * 256 * 4 + 1024;
+static_assert(2 * kABytes + kRingBytes == kABytes + kSplitRingBytes, "both X/W_U layouts fill the same bytes");
 
 size_t workspace_bytes(int n, int hkv, int /*d_h*/) {
     return 2 * static_cast<size_t>(hkv) * n * sizeof(float) + 256;
@@ -400,10 +466,11 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     p.reverse = a.reverse ? 1 : 0;
     static std::once_flag attr[vsp_detail::kMaxDevices];
     vsp_detail::once_per_device(attr, [] {
-        cudaFuncSetAttribute(indexer_gemm_kernel<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(indexer_gemm_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(indexer_gemm_kernel<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(indexer_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<false, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<false, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<true, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<true, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(indexer_gemm_kernel<false, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     });
     const int count = a.count < 0 ? a.hkv - a.g0 : a.count;
     p.g0 = a.g0;
@@ -412,12 +479,14 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     const int sms = vsp_detail::current_sm_count();
     // VSP_K1_MC = 1: one CTA per tile; 2: CTA pairs (cta_group::2); single tiles need no pair.
     // VSP_K1_STAGEK = 32 / 64: W_U K-rows per ring stage (the ring stays 64 KB)
-    int mc = kDefaultMc, stage_k = kDefaultStageK;
+    int mc = kDefaultMc, stage_k = kDefaultStageK, split = kDefaultSplit;
     if (const char* s = getenv("VSP_K1_MC")) mc = atoi(s);
+    if (const char* s = getenv("VSP_K1_SPLIT")) split = atoi(s) != 0;
     if (const char* s = getenv("VSP_K1_STAGEK")) stage_k = atoi(s);
     if (mc != 1 && mc != 2) mc = kDefaultMc;
     if (stage_k != 32 && stage_k != 64) stage_k = kDefaultStageK;
     if (p.tiles < 2) mc = 1;
+    if (mc != 1 || stage_k != 32) split = 0;  // split-X: one CTA per tile, 32-row stages
     const uint32_t wbox[3] = {64, static_cast<uint32_t>(stage_k), 1};
     if (!vsp_host::make_map_bf16(&p.map_w, a.w_u, 3, dw, sw, wbox)) return cudaErrorInvalidValue;
     const int groups = ((p.tiles + mc - 1) / mc) * count;
@@ -435,10 +504,11 @@ cudaError_t launch(const Args& a, void* workspace, cudaStream_t stream) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = mc == 2 ? (stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 64>, p)
-                                        : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 32>, p))
-                            : (stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 64>, p)
-                                        : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 32>, p));
+    cudaError_t e = split         ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 32, true>, p)
+                    : mc == 2     ? (stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 64, false>, p)
+                                                   : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<true, 32, false>, p))
+                    : stage_k == 64 ? cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 64, false>, p)
+                                    : cudaLaunchKernelEx(&cfg, indexer_gemm_kernel<false, 32, false>, p);
     if (e == cudaSuccess) e = cudaGetLastError();
     // A_v / A_s: the cluster softmax shared with the selection kernel (a_v null: logits only,
     // the layer path softmaxes inside selection)

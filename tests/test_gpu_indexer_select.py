@@ -340,15 +340,17 @@ def test_indexer_cta_pairs_identical(vsp, n, hkv, monkeypatch):
     """VSP_K1_MC = 2 runs K1 on CTA pairs (cta_group::2, M = 256, each CTA holding half of every
     W_U stage); odd tile counts leave a phantom tile in a head's last pair. Same bits as one CTA
     per tile (identical K order of the fp32 accumulation), for both W_U stage depths
-    (VSP_K1_STAGEK = 32 / 64 K-rows)."""
+    (VSP_K1_STAGEK = 32 / 64 K-rows), and for the split-X layout (VSP_K1_SPLIT = 1: one X tile
+    in four per-box-barrier boxes, 128 KB W_U ring)."""
     g = torch.Generator().manual_seed(n + hkv)
     k = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     v = torch.randn(n, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     p = _params(vsp, hkv, 512, seed=n)
     outs = []
-    for mc, sk in (("1", "32"), ("1", "64"), ("2", "32"), ("2", "64")):
+    for mc, sk, split in (("1", "32", "0"), ("1", "64", "0"), ("2", "32", "0"), ("2", "64", "0"), ("1", "32", "1")):
         monkeypatch.setenv("VSP_K1_MC", mc)
         monkeypatch.setenv("VSP_K1_STAGEK", sk)
+        monkeypatch.setenv("VSP_K1_SPLIT", split)
         _, _, lv, ls = vsp.indexer_forward(k, v, p, want_logits=True)
         torch.cuda.synchronize()
         outs.append((lv.clone(), ls.clone()))
