@@ -38,55 +38,75 @@ namespace vsp_train {
 
 // ------------------------------------------------------------------ KL loss + dlogit
 
-// grid (hkv, 2): y = 0 vertical, 1 slash (offset order). 1024 threads.
-__global__ void __launch_bounds__(1024) kl_grad_kernel(const float* __restrict__ logits_v,
-                                                       const float* __restrict__ logits_s,
-                                                       const float* __restrict__ target_v,
-                                                       const float* __restrict__ target_s, int n, double eps,
-                                                       float* dlogit_v, float* dlogit_s, double* loss,
-                                                       double* dbias) {
-    const int g = blockIdx.x, dir = blockIdx.y;
+// grid (hkv * kKlCluster, 2) in clusters of kKlCluster CTAs along x: one cluster per (KV
+// head, direction), y = 0 vertical, 1 slash (offset order), 1024 threads per CTA. Each CTA
+// strides over its share of the n tokens; the four fp64 reductions (max, sum-exp, KL and
+// <p, dpred>, sum dlogit) are block sums published to shared memory and combined by every
+// CTA over DSMEM in rank order, so all CTAs hold bit-identical totals (deterministic).
+constexpr int kKlCluster = 8;
+
+VSP_DEVICE double ld_cluster_f64(uint32_t cluster_addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
+    return v;
+}
+
+__global__ void __cluster_dims__(kKlCluster, 1, 1) __launch_bounds__(1024)
+    kl_grad_kernel(const float* __restrict__ logits_v, const float* __restrict__ logits_s,
+                   const float* __restrict__ target_v, const float* __restrict__ target_s, int n, double eps,
+                   float* dlogit_v, float* dlogit_s, double* loss, double* dbias) {
+    const int rank = static_cast<int>(cluster_ctarank());
+    const int g = blockIdx.x / kKlCluster, dir = blockIdx.y, heads = gridDim.x / kKlCluster;
     const float* l = (dir ? logits_s : logits_v) + static_cast<size_t>(g) * n;
     const float* t = (dir ? target_s : target_v) + static_cast<size_t>(g) * n;
     float* dl = (dir ? dlogit_s : dlogit_v) + static_cast<size_t>(g) * n;
     __shared__ double red[32];
-    auto block_sum = [&](double x) {
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    __shared__ double xch[5];  // one slot per exchange: max, z, kl, inner, db
+    const int i0 = rank * 1024 + static_cast<int>(threadIdx.x), step = kKlCluster * 1024;
+    auto block_red = [&](double x, bool is_max) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, x, o);
+            x = is_max ? fmax(x, y) : x + y;
+        }
         __syncthreads();
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
         __syncthreads();
-        double s = 0.0;
-        for (int w = 0; w < 32; ++w) s += red[w];
+        double s = is_max ? -INFINITY : 0.0;
+        for (int w = 0; w < 32; ++w) s = is_max ? fmax(s, red[w]) : s + red[w];
         return s;
     };
-    auto block_max = [&](double x) {
-        for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-        __syncthreads();
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
-        __syncthreads();
-        double s = -INFINITY;
-        for (int w = 0; w < 32; ++w) s = fmax(s, red[w]);
+    // block value -> cluster total (slot k), identical in every CTA
+    auto cluster_red = [&](double x, int k, bool is_max) {
+        x = block_red(x, is_max);
+        if (threadIdx.x == 0) xch[k] = x;
+        cluster_sync();
+        const uint32_t a = smem_u32(&xch[k]);
+        double s = is_max ? -INFINITY : 0.0;
+        for (int r = 0; r < kKlCluster; ++r) {
+            const double y = ld_cluster_f64(mapa_shared(a, static_cast<uint32_t>(r)));
+            s = is_max ? fmax(s, y) : s + y;
+        }
         return s;
     };
     double m = -INFINITY;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, static_cast<double>(l[i]));
-    m = block_max(m);
+    for (int i = i0; i < n; i += step) m = fmax(m, static_cast<double>(l[i]));
+    m = cluster_red(m, 0, true);
     double z = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) z += exp(static_cast<double>(l[i]) - m);
-    const double log_z = log(block_sum(z));
+    for (int i = i0; i < n; i += step) z += exp(static_cast<double>(l[i]) - m);
+    const double log_z = log(cluster_red(z, 1, false));
     // loss = sum p (log p - log(t + eps)); inner = sum p * dpred (dpred = log p + 1 - log(t + eps))
     double kl = 0.0, inner = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = i0; i < n; i += step) {
         const double lp = static_cast<double>(l[i]) - m - log_z;
         const double p = exp(lp);
         const double lt = log(static_cast<double>(t[i]) + eps);
         if (p > 0.0) kl += p * (lp - lt);
         inner += p * ((p > 0.0 ? lp : log(1e-300)) + 1.0 - lt);
     }
-    kl = block_sum(kl);
-    inner = block_sum(inner);
+    kl = cluster_red(kl, 2, false);
+    inner = cluster_red(inner, 3, false);
     double db = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = i0; i < n; i += step) {
         const double lp = static_cast<double>(l[i]) - m - log_z;
         const double p = exp(lp);
         const double dp = (p > 0.0 ? lp : log(1e-300)) + 1.0 - log(static_cast<double>(t[i]) + eps);
@@ -94,11 +114,12 @@ __global__ void __launch_bounds__(1024) kl_grad_kernel(const float* __restrict__
         dl[i] = static_cast<float>(d);
         db += d;
     }
-    db = block_sum(db);
-    if (threadIdx.x == 0) {
-        loss[dir * gridDim.x + g] = kl;
-        dbias[dir * gridDim.x + g] = db;
+    db = cluster_red(db, 4, false);
+    if (rank == 0 && threadIdx.x == 0) {
+        loss[dir * heads + g] = kl;
+        dbias[dir * heads + g] = db;
     }
+    cluster_sync();  // no CTA exits while a peer may still read its xch
 }
 
 // ------------------------------------------------------------------ backward GEMM (tcgen05)
@@ -135,7 +156,7 @@ struct __align__(64) BwdParams {
 };
 
 struct BwdSmem {
-    uint64_t w_full, x_full, x_empty, y_full, ep_done, bw_done, all_done;
+    uint64_t w_full, x_full[2], x_empty[2], y_full, ep_done, bw_done, all_done;  // x_*[h]: K / V half of X
     uint32_t tmem_base;
 };
 
@@ -158,8 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
 
     if (warp == 0 && lane == 0) {
         mbar_init(&sm.w_full, 1);
-        mbar_init(&sm.x_full, 1);
-        mbar_init(&sm.x_empty, 1);
+        mbar_init(&sm.x_full[0], 1);
+        mbar_init(&sm.x_full[1], 1);
+        mbar_init(&sm.x_empty[0], 1);
+        mbar_init(&sm.x_empty[1], 1);
         mbar_init(&sm.y_full, 1);
         mbar_init(&sm.ep_done, 8);
         mbar_init(&sm.bw_done, 1);
@@ -204,17 +227,22 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                 tma_load_3d(base + kOffW + nb * (kWBytes / 2), &p.map_w, &sm.w_full, hc * kHid + nb * 64, 0, g);
         }
         __syncwarp();
+        // X in two halves (K features -> boxes 0-1, V features -> boxes 2-3), each with its own
+        // full/empty pair: the K half of tile i+1 loads while the MMAs of tile i still read the V
+        // half, and the first half of Y(i+1) runs while the V half is in flight.
         for (int i = 0; i < ntiles; ++i) {
-            if (i >= 1) mbar_wait(&sm.x_empty, (i - 1) & 1);
-            if (elect_one()) {
-                const int t0 = (tile_lo + i) * kTok;
-                mbar_arrive_expect_tx(&sm.x_full, kXBytes);
-                for (int hf = 0; hf < 2; ++hf) {
-                    tma_load_3d(base + kOffX + hf * 16384, &p.map_k, &sm.x_full, hf * 64, g, t0);
-                    tma_load_3d(base + kOffX + (2 + hf) * 16384, &p.map_v, &sm.x_full, hf * 64, g, t0);
+            const int t0 = (tile_lo + i) * kTok;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                if (i >= 1) mbar_wait(&sm.x_empty[h], (i - 1) & 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.x_full[h], kXBytes / 2);
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_3d(base + kOffX + (2 * h + hf) * 16384, h ? &p.map_v : &p.map_k, &sm.x_full[h],
+                                    hf * 64, g, t0);
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         const uint32_t idesc_y = umma_idesc_bf16(128, kHid, false, true);
@@ -230,32 +258,46 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
         const uint64_t ones_k = umma_desc_sw128(smem_u32(base + kOffOnes), 16, 1024);
         mbar_wait(&sm.w_full, 0);
         for (int i = 0; i < ntiles; ++i) {
-            mbar_wait(&sm.x_full, i & 1);
-            if (i >= 1) mbar_wait(&sm.ep_done, (i - 1) & 1);  // Y(i-1) has been read out of TMEM
-            tc_fence_after();
-            if (elect_one()) {
+            // Y = X W_U: K-feature half, then V-feature half as it lands
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                mbar_wait(&sm.x_full[h], i & 1);
+                if (h == 0 && i >= 1) mbar_wait(&sm.ep_done, (i - 1) & 1);  // Y(i-1) has been read out of TMEM
+                tc_fence_after();
+                if (elect_one()) {
 #pragma unroll
-                for (int kg = 0; kg < 256; kg += 16)
-                    umma_ss(t_y, x_k + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4),
-                            w_mn + static_cast<uint64_t>((kg * 128) >> 4), idesc_y, kg > 0 ? 1u : 0u);
-                umma_commit(&sm.y_full);
+                    for (int kg = 128 * h; kg < 128 * h + 128; kg += 16)
+                        umma_ss(t_y, x_k + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4),
+                                w_mn + static_cast<uint64_t>((kg * 128) >> 4), idesc_y, kg > 0 ? 1u : 0u);
+                    if (h == 1) umma_commit(&sm.y_full);
+                }
+                __syncwarp();
             }
-            __syncwarp();
             mbar_wait(&sm.ep_done, i & 1);  // dY, Z, DL of tile i are in smem
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t acc0 = i > 0 ? 1u : 0u;
+                // dW_U rows of the K half first so its X boxes are released before the V half's
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);  // 16 tokens
+                    umma_ss(t_dw, x_mn0 + off, dy_mn + off, idesc_dw, (acc0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&sm.x_empty[0]);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);
                     const uint32_t acc = (acc0 || kk > 0) ? 1u : 0u;
-                    umma_ss(t_dw, x_mn0 + off, dy_mn + off, idesc_dw, acc);
-                    umma_ss(t_dw + 128, x_mn1 + off, dy_mn + off, idesc_dw, acc);
                     const uint64_t koff = static_cast<uint64_t>(((kk >> 2) * 1024 + (kk & 3) * 32) >> 4);
                     umma_ss(t_dwv, z_mn + off, dl_k + koff, idesc_n8, acc);
                     umma_ss(t_db, dy_mn + off, ones_k + koff, idesc_n8, acc);
                 }
-                umma_commit(&sm.x_empty);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);
+                    umma_ss(t_dw + 128, x_mn1 + off, dy_mn + off, idesc_dw, (acc0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&sm.x_empty[1]);
                 umma_commit(&sm.bw_done);
                 if (i == ntiles - 1) umma_commit(&sm.all_done);
             }
@@ -416,13 +458,25 @@ __global__ void sum_loss_kernel(const double* loss2, int hkv, float* loss) {
 
 // ------------------------------------------------------------------ host
 
+// Token splits per (KV head, hidden chunk) unit: minimise waves x tiles per CTA (one CTA
+// per SM) plus a per-CTA prologue and a per-split reduction cost, in tile units. 128k x 8
+// heads (64 units, 1024 tiles): 9 splits = 576 CTAs in 4 full-ish waves of 114 tiles,
+// against 5 splits = 320 CTAs in 3 waves (the last 16 % full) of 205 tiles.
 static int splits_for(int hkv, int d_h, int tiles) {
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = vsp_detail::current_sm_count();
     const int units = hkv * (d_h / kHid);
-    int s = std::max(1, (2 * sms + units - 1) / units);
-    return std::min(s, std::max(1, tiles));
+    int best = 1;
+    double best_cost = 1e300;
+    for (int s = 1; s <= std::min(64, std::max(1, tiles)); ++s) {
+        const int waves = (units * s + sms - 1) / sms;
+        const int per = (tiles + s - 1) / s;
+        const double cost = static_cast<double>(waves) * (per + 2) + 0.5 * s;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = s;
+        }
+    }
+    return best;
 }
 
 size_t workspace_bytes(int n, int hkv, int d_h) {
@@ -466,7 +520,7 @@ cudaError_t loss_grad(const GradArgs& a, void* workspace, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     // 2. loss and dlogit (fp64 softmax over n)
     vsp_detail::count_launch();
-    kl_grad_kernel<<<dim3(a.hkv, 2), 1024, 0, stream>>>(lv, ls, a.target_v, a.target_s, a.n, a.kl_eps, dv, ds,
+    kl_grad_kernel<<<dim3(a.hkv * kKlCluster, 2), 1024, 0, stream>>>(lv, ls, a.target_v, a.target_s, a.n, a.kl_eps, dv, ds,
                                                         loss2, dbias);
     // 3. backward GEMMs
     BwdParams p{};
