@@ -12,11 +12,11 @@
 //   kl_grad_kernel   one CTA per (KV head, direction): max / sum-exp / KL / dlogit over n in
 //                    fp64 (the softmax over all n tokens), plus the bias gradient sum(dlogit).
 //   backward_kernel  tcgen05: per (KV head, 128-wide hidden chunk, token split) the CTA keeps
-//                    its W_U chunk resident, recomputes Y = X W_U for each 128-token tile in
-//                    TMEM (never stored), turns it into dY = (dlv w_v + dls w_s) * silu'(Y)
-//                    and Z = silu(Y) (bf16 tiles in smem), and accumulates in TMEM
-//                      dW_U += X^T dY   (M = 2 x 128 features, N = 128, K = 128 tokens)
-//                      [dw_v dw_s] += Z^T [dlv dls]   and   db_U += dY^T 1   (N = 8)
+//                    its W_U chunk resident and, per 128-token tile, recomputes Y^T = W_U^T X^T
+//                    in TMEM (hidden units on lanes, double-buffered), forms
+//                    dY = (dlv w_v + dls w_s) * silu'(Y) as bf16 K-major rows in smem and
+//                    accumulates dW_U^T += dY^T X (M = 128 hidden, N = 256 features) in TMEM;
+//                    dw_v, dw_s and db_U are per-thread fp32 sums (a thread owns a hidden unit).
 //                    Partials per token split are summed in a fixed order (deterministic).
 //   adamw_kernel     optimizer_step over the flat fp32 master parameters; refreshes the bf16
 //                    W_U copy the K1 forward reads.
@@ -124,21 +124,30 @@ __global__ void __cluster_dims__(kKlCluster, 1, 1) __launch_bounds__(1024)
 
 // ------------------------------------------------------------------ backward GEMM (tcgen05)
 
+// Transposed form (hidden units on TMEM lanes): per 128-token tile
+//   Y^T  = W_U^T X^T      A = W_U chunk (smem, MN-major, M = 128 hidden), B = X (K-major, N = 128 tokens),
+//                         K = 256 features; double-buffered in TMEM (cols 0 / 128)
+//   dY^T = (dlv w_v + dls w_s) * silu'(Y)   epilogue, thread = hidden unit, bf16 K-major rows in smem
+//   dW^T += dY^T X        A = dY^T (smem, K-major, M = 128 hidden), B = X (MN-major, N = 256 features),
+//                         K = 128 tokens; fp32 in TMEM cols 256..511
+// and, since a thread owns one hidden unit, dw_v = sum_t silu(y) dlv, dw_s = sum_t silu(y) dls and
+// db_U = sum_t dY accumulate in fp32 registers (no N = 8 MMAs, no Z tile). X is double-buffered
+// (two 64 KB slots, each in K / V halves) so Y^T(i+1) runs on the tensor core while the
+// epilogue of tile i computes; the epilogue does its math before waiting for dW(i-1) to
+// release the single dY tile.
 constexpr int kTok = 128;
 constexpr int kHid = 128;                   // hidden chunk per CTA
-constexpr int kXBytes = kTok * 256 * 2;     // 64 KB: 4 SW128 boxes [128 tok x 64 feat]
-constexpr int kWBytes = 256 * kHid * 2;     // 64 KB: 2 N-blocks [256 feat x 64 hid]
-constexpr int kTBytes = kTok * kHid * 2;    // 32 KB: dY / Z tiles, 2 blocks [128 tok x 64 hid]
-constexpr int kNBytes = 2048;               // [8 x 128] K-major B operands (DL, ones)
-constexpr int kOffX = 0;
-constexpr int kOffW = kOffX + kXBytes;
+constexpr int kXBytes = kTok * 256 * 2;     // 64 KB per X slot: 4 SW128 boxes [128 tok x 64 feat] (K0 K1 V0 V1)
+constexpr int kWBytes = 256 * kHid * 2;     // 64 KB: 2 blocks [256 feat x 64 hid]
+constexpr int kTBytes = kHid * kTok * 2;    // 32 KB: dY^T, 2 boxes [128 hid x 64 tok]
+constexpr int kOffX = 0;                    // slots at 0 / kXBytes
+constexpr int kOffW = 2 * kXBytes;
 constexpr int kOffDY = kOffW + kWBytes;
-constexpr int kOffZ = kOffDY + kTBytes;
-constexpr int kOffDL = kOffZ + kTBytes;
-constexpr int kOffOnes = kOffDL + kNBytes;
-constexpr int kOffVec = kOffOnes + kNBytes;  // b_U, w_v, w_s of the chunk: 3 x 128 floats
-constexpr int kSmemBytes = kOffVec + 3 * kHid * 4 + 1024;
+constexpr int kOffDL = kOffDY + kTBytes;    // float2 {dlv, dls} per token of the current tile
+constexpr int kOffBar = kOffDL + kTok * 8;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;
 constexpr int kThreads = 384;               // warp0 TMA, warp1 MMA, warps 4-11 epilogue
+constexpr uint32_t kEpiBar = 1;             // named barrier of the 8 epilogue warps
 static_assert(kSmemBytes <= 227 * 1024, "train smem");
 
 struct __align__(64) BwdParams {
@@ -156,7 +165,7 @@ struct __align__(64) BwdParams {
 };
 
 struct BwdSmem {
-    uint64_t w_full, x_full[2], x_empty[2], y_full, ep_done, bw_done, all_done;  // x_*[h]: K / V half of X
+    uint64_t w_full, x_full[2][2], x_empty[2][2], y_full[2], y_free[2], ep_done, dy_free, all_done;
     uint32_t tmem_base;
 };
 
@@ -165,7 +174,7 @@ VSP_DEVICE uint32_t sw128(int row, int chunk) { return static_cast<uint32_t>(row
 __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_constant__ BwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ BwdSmem sm;
+    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(base + kOffBar);
     const int nchunks = p.d_h / kHid;
     const int sp = blockIdx.x % p.nsplit;
     const int rest = blockIdx.x / p.nsplit;
@@ -175,47 +184,29 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
     const int tile_hi = static_cast<int>(static_cast<long long>(p.tiles) * (sp + 1) / p.nsplit);
     const int ntiles = tile_hi - tile_lo;
     const uint32_t warp = warp_id(), lane = lane_id();
-    float* vec = reinterpret_cast<float*>(base + kOffVec);  // [b_U | w_v | w_s] of the chunk
 
     if (warp == 0 && lane == 0) {
         mbar_init(&sm.w_full, 1);
-        mbar_init(&sm.x_full[0], 1);
-        mbar_init(&sm.x_full[1], 1);
-        mbar_init(&sm.x_empty[0], 1);
-        mbar_init(&sm.x_empty[1], 1);
-        mbar_init(&sm.y_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.x_full[s][0], 1);
+            mbar_init(&sm.x_full[s][1], 1);
+            mbar_init(&sm.x_empty[s][0], 1);
+            mbar_init(&sm.x_empty[s][1], 1);
+            mbar_init(&sm.y_full[s], 1);
+            mbar_init(&sm.y_free[s], 8);
+        }
         mbar_init(&sm.ep_done, 8);
-        mbar_init(&sm.bw_done, 1);
+        mbar_init(&sm.dy_free, 1);
         mbar_init(&sm.all_done, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
-    {
-        // DL rows 2..7 and the ones operand (row 0 = 1) are constant; DL rows 0/1 are rewritten
-        uint32_t* dl = reinterpret_cast<uint32_t*>(base + kOffDL);
-        for (int i = threadIdx.x; i < kNBytes / 4; i += kThreads) dl[i] = 0u;
-        uint16_t* ones = reinterpret_cast<uint16_t*>(base + kOffOnes);
-        for (int i = threadIdx.x; i < 8 * 128; i += kThreads) {
-            const int nrow = i >> 7, tok = i & 127;
-            const uint32_t off = (tok >> 6) * 1024 + sw128(nrow, (tok & 63) >> 3) + ((tok & 7) << 1);
-            ones[off >> 1] = nrow == 0 ? 0x3f80u : 0u;
-        }
-        for (int i = threadIdx.x; i < kHid; i += kThreads) {
-            const size_t o = static_cast<size_t>(g) * p.d_h + hc * kHid + i;
-            vec[i] = p.b_u[o];
-            vec[kHid + i] = p.w_v[o];
-            vec[2 * kHid + i] = p.w_s[o];
-        }
-        fence_proxy_async_smem();
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    const uint32_t t_y = tmem;            // Y chunk [128 tok x 128 hid]
-    const uint32_t t_dw = tmem + 128;     // dW_U: feature halves at +0 / +128, [128 feat x 128 hid]
-    const uint32_t t_dwv = tmem + 384;    // [128 hid x 8]: col 0 dw_v, col 1 dw_s
-    const uint32_t t_db = tmem + 392;     // [128 hid x 8]: col 0 db_U
+    const uint32_t t_y = tmem;         // Y^T slots [128 hid x 128 tok] at +0 / +128
+    const uint32_t t_dw = tmem + 256;  // dW^T [128 hid x 256 feat]
 
     if (warp == 0) {
         if (elect_one()) {
@@ -227,179 +218,158 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                 tma_load_3d(base + kOffW + nb * (kWBytes / 2), &p.map_w, &sm.w_full, hc * kHid + nb * 64, 0, g);
         }
         __syncwarp();
-        // X in two halves (K features -> boxes 0-1, V features -> boxes 2-3), each with its own
-        // full/empty pair: the K half of tile i+1 loads while the MMAs of tile i still read the V
-        // half, and the first half of Y(i+1) runs while the V half is in flight.
         for (int i = 0; i < ntiles; ++i) {
-            const int t0 = (tile_lo + i) * kTok;
+            const int t0 = (tile_lo + i) * kTok, s = i & 1;
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
-                if (i >= 1) mbar_wait(&sm.x_empty[h], (i - 1) & 1);
+                if (i >= 2) mbar_wait(&sm.x_empty[s][h], ((i >> 1) - 1) & 1);
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(&sm.x_full[h], kXBytes / 2);
+                    mbar_arrive_expect_tx(&sm.x_full[s][h], kXBytes / 2);
                     for (int hf = 0; hf < 2; ++hf)
-                        tma_load_3d(base + kOffX + (2 * h + hf) * 16384, h ? &p.map_v : &p.map_k, &sm.x_full[h],
-                                    hf * 64, g, t0);
+                        tma_load_3d(base + kOffX + s * kXBytes + (2 * h + hf) * 16384, h ? &p.map_v : &p.map_k,
+                                    &sm.x_full[s][h], hf * 64, g, t0);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc_y = umma_idesc_bf16(128, kHid, false, true);
-        const uint32_t idesc_dw = umma_idesc_bf16(128, kHid, true, true);
-        const uint32_t idesc_n8 = umma_idesc_bf16(128, 8, true, false);
-        const uint64_t x_k = umma_desc_sw128(smem_u32(base + kOffX), 16, 1024);          // X, K-major
-        const uint64_t w_mn = umma_desc_sw128(smem_u32(base + kOffW), kWBytes / 2, 1024);  // W chunk, MN-major
-        const uint64_t x_mn0 = umma_desc_sw128(smem_u32(base + kOffX), 16384, 1024);       // X^T, features 0..127
-        const uint64_t x_mn1 = umma_desc_sw128(smem_u32(base + kOffX + 32768), 16384, 1024);
-        const uint64_t dy_mn = umma_desc_sw128(smem_u32(base + kOffDY), 16384, 1024);
-        const uint64_t z_mn = umma_desc_sw128(smem_u32(base + kOffZ), 16384, 1024);
-        const uint64_t dl_k = umma_desc_sw128(smem_u32(base + kOffDL), 16, 1024);
-        const uint64_t ones_k = umma_desc_sw128(smem_u32(base + kOffOnes), 16, 1024);
+        const uint32_t idesc_y = umma_idesc_bf16(128, kTok, true, false);  // A MN-major, B K-major
+        const uint32_t idesc_dw = umma_idesc_bf16(128, 256, false, true);  // A K-major, B MN-major
+        const uint64_t w_mn = umma_desc_sw128(smem_u32(base + kOffW), kWBytes / 2, 1024);
+        const uint64_t dy_k = umma_desc_sw128(smem_u32(base + kOffDY), 16, 1024);
         mbar_wait(&sm.w_full, 0);
-        for (int i = 0; i < ntiles; ++i) {
-            // Y = X W_U: K-feature half, then V-feature half as it lands
+        for (int i = 0; i <= ntiles; ++i) {
+            if (i < ntiles) {
+                const int s = i & 1;
+                const uint64_t x_k = umma_desc_sw128(smem_u32(base + kOffX + s * kXBytes), 16, 1024);
+                if (i >= 2) mbar_wait(&sm.y_free[s], ((i >> 1) - 1) & 1);  // Y(i-2) read out of slot s
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                mbar_wait(&sm.x_full[h], i & 1);
-                if (h == 0 && i >= 1) mbar_wait(&sm.ep_done, (i - 1) & 1);  // Y(i-1) has been read out of TMEM
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait(&sm.x_full[s][h], (i >> 1) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kg = 128 * h; kg < 128 * h + 128; kg += 16)
+                            umma_ss(t_y + s * 128, w_mn + static_cast<uint64_t>((kg * 128) >> 4),
+                                    x_k + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4), idesc_y,
+                                    kg > 0 ? 1u : 0u);
+                        if (h == 1) umma_commit(&sm.y_full[s]);
+                    }
+                    __syncwarp();
+                }
+            }
+            if (i >= 1) {
+                const int j = i - 1, sj = j & 1;
+                const uint64_t x_mn = umma_desc_sw128(smem_u32(base + kOffX + sj * kXBytes), 16384, 1024);
+                mbar_wait(&sm.ep_done, j & 1);  // dY^T of tile j is in smem
                 tc_fence_after();
                 if (elect_one()) {
 #pragma unroll
-                    for (int kg = 128 * h; kg < 128 * h + 128; kg += 16)
-                        umma_ss(t_y, x_k + static_cast<uint64_t>(((kg >> 6) * 16384 + (kg & 63) * 2) >> 4),
-                                w_mn + static_cast<uint64_t>((kg * 128) >> 4), idesc_y, kg > 0 ? 1u : 0u);
-                    if (h == 1) umma_commit(&sm.y_full);
+                    for (int kk = 0; kk < 8; ++kk)  // 16 tokens per MMA
+                        umma_ss(t_dw, dy_k + static_cast<uint64_t>(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+                                x_mn + static_cast<uint64_t>((kk * 2048) >> 4), idesc_dw, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&sm.x_empty[sj][0]);
+                    umma_commit(&sm.x_empty[sj][1]);
+                    umma_commit(&sm.dy_free);
+                    if (j == ntiles - 1) umma_commit(&sm.all_done);
                 }
                 __syncwarp();
             }
-            mbar_wait(&sm.ep_done, i & 1);  // dY, Z, DL of tile i are in smem
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t acc0 = i > 0 ? 1u : 0u;
-                // dW_U rows of the K half first so its X boxes are released before the V half's
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);  // 16 tokens
-                    umma_ss(t_dw, x_mn0 + off, dy_mn + off, idesc_dw, (acc0 || kk > 0) ? 1u : 0u);
-                }
-                umma_commit(&sm.x_empty[0]);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);
-                    const uint32_t acc = (acc0 || kk > 0) ? 1u : 0u;
-                    const uint64_t koff = static_cast<uint64_t>(((kk >> 2) * 1024 + (kk & 3) * 32) >> 4);
-                    umma_ss(t_dwv, z_mn + off, dl_k + koff, idesc_n8, acc);
-                    umma_ss(t_db, dy_mn + off, ones_k + koff, idesc_n8, acc);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t off = static_cast<uint64_t>((kk * 2048) >> 4);
-                    umma_ss(t_dw + 128, x_mn1 + off, dy_mn + off, idesc_dw, (acc0 || kk > 0) ? 1u : 0u);
-                }
-                umma_commit(&sm.x_empty[1]);
-                umma_commit(&sm.bw_done);
-                if (i == ntiles - 1) umma_commit(&sm.all_done);
-            }
-            __syncwarp();
         }
     } else if (warp >= 4) {
         const int quarter = warp & 3;
-        const int part = (warp - 4) >> 2;  // hidden columns [64 part, 64 part + 64)
-        const int r = quarter * 32 + lane;
+        const int part = (warp - 4) >> 2;  // tokens [64 part, 64 part + 64) of each tile
+        const int r = quarter * 32 + lane;  // hidden unit (TMEM lane)
+        const int e = (warp - 4) * 32 + lane;  // 0..255: loader of dlv (e < 128) / dls of token e & 127
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+        const size_t ho = static_cast<size_t>(g) * p.d_h + hc * kHid + r;
+        const float bu = p.b_u[ho], wv = p.w_v[ho], ws = p.w_s[ho];
         uint8_t* dyb = base + kOffDY + part * 16384;
-        uint8_t* zb = base + kOffZ + part * 16384;
-        uint16_t* dlb = reinterpret_cast<uint16_t*>(base + kOffDL);
+        float* dl = reinterpret_cast<float*>(base + kOffDL);  // [tok][2]
+        auto load_dl = [&](int i) {
+            const int t = (tile_lo + i) * kTok + (e & 127);
+            if (i >= ntiles || t >= p.n) return 0.f;
+            return e < 128 ? p.dlogit_v[static_cast<size_t>(g) * p.n + t]
+                           : p.dlogit_s[static_cast<size_t>(g) * p.n + (p.reverse ? p.n - 1 - t : t)];
+        };
+        float dwv = 0.f, dws = 0.f, db = 0.f;
+        float nxt = load_dl(0);
         for (int i = 0; i < ntiles; ++i) {
-            const int t = (tile_lo + i) * kTok + r;
-            float dlv = 0.f, dls = 0.f;
-            if (t < p.n) {
-                dlv = p.dlogit_v[static_cast<size_t>(g) * p.n + t];
-                dls = p.dlogit_s[static_cast<size_t>(g) * p.n + (p.reverse ? p.n - 1 - t : t)];
-            }
-            mbar_wait(&sm.y_full, i & 1);
+            const int s = i & 1;
+            named_bar_sync(kEpiBar, 256);  // every epilogue thread is done with tile i-1's dl
+            dl[(e & 127) * 2 + (e >> 7)] = nxt;
+            named_bar_sync(kEpiBar, 256);
+            nxt = load_dl(i + 1);
+            mbar_wait(&sm.y_full[s], (i >> 1) & 1);
             tc_fence_after();
             uint32_t u[2][32];
-            tmem_ld32(t_y + lane_base + part * 64, u[0]);
-            tmem_ld32(t_y + lane_base + part * 64 + 32, u[1]);
+            tmem_ld32(t_y + s * 128 + lane_base + part * 64, u[0]);
+            tmem_ld32(t_y + s * 128 + lane_base + part * 64 + 32, u[1]);
             tmem_wait_ld(u[0]);
             tmem_reg_fence(u[1]);
-            if (i >= 1) mbar_wait(&sm.bw_done, (i - 1) & 1);  // tile i-1's MMAs have read dY / Z / DL
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-                uint32_t dyw[4], zw[4];
-#pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                    float dy2[2], z2[2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int col = ch * 8 + e2 * 2 + h;  // 0..63 within this part
-                        const int j = part * 64 + col;
-                        const float y = __uint_as_float(u[col >> 5][col & 31]) + vec[j];
-                        const float hh = 0.5f * y;
-                        float th;
-                        asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(hh));
-                        const float sg = 0.5f + 0.5f * th;           // sigmoid(y)
-                        z2[h] = hh + hh * th;                       // y * sigmoid(y)
-                        const float dsilu = sg * (1.f + y * (1.f - sg));
-                        dy2[h] = (dlv * vec[kHid + j] + dls * vec[2 * kHid + j]) * dsilu;
-                    }
-                    dyw[e2] = pack_bf16x2(dy2[0], dy2[1]);
-                    zw[e2] = pack_bf16x2(z2[0], z2[1]);
-                }
-                *reinterpret_cast<uint4*>(dyb + sw128(r, ch)) = make_uint4(dyw[0], dyw[1], dyw[2], dyw[3]);
-                *reinterpret_cast<uint4*>(zb + sw128(r, ch)) = make_uint4(zw[0], zw[1], zw[2], zw[3]);
-            }
-            if (part == 0) {  // DL[0][tok] = dlv, DL[1][tok] = dls (K-major [8 x 128])
-                const uint32_t o0 = (r >> 6) * 1024 + sw128(0, (r & 63) >> 3) + ((r & 7) << 1);
-                const uint32_t o1 = (r >> 6) * 1024 + sw128(1, (r & 63) >> 3) + ((r & 7) << 1);
-                dlb[o0 >> 1] = __bfloat16_as_ushort(__float2bfloat16_rn(dlv));
-                dlb[o1 >> 1] = __bfloat16_as_ushort(__float2bfloat16_rn(dls));
-            }
-            fence_proxy_async_smem();
             tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.y_free[s]);
+            uint32_t dyw[32];
+#pragma unroll
+            for (int c2 = 0; c2 < 32; ++c2) {
+                float dy2[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = 2 * c2 + h;  // token within this part
+                    const float2 d = *reinterpret_cast<const float2*>(dl + (part * 64 + col) * 2);
+                    const float y = __uint_as_float(u[col >> 5][col & 31]) + bu;
+                    const float hh = 0.5f * y;
+                    float th;
+                    asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(hh));
+                    const float sg = 0.5f + 0.5f * th;  // sigmoid(y)
+                    const float z = hh + hh * th;       // y * sigmoid(y)
+                    const float dsilu = sg * (1.f + y * (1.f - sg));
+                    dy2[h] = (d.x * wv + d.y * ws) * dsilu;
+                    dwv += z * d.x;
+                    dws += z * d.y;
+                    db += dy2[h];
+                }
+                dyw[c2] = pack_bf16x2(dy2[0], dy2[1]);
+            }
+            if (i >= 1) mbar_wait(&sm.dy_free, (i - 1) & 1);  // dW(i-1) has read the dY^T tile
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+                *reinterpret_cast<uint4*>(dyb + sw128(r, ch)) =
+                    make_uint4(dyw[4 * ch], dyw[4 * ch + 1], dyw[4 * ch + 2], dyw[4 * ch + 3]);
+            fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.ep_done);
         }
-        // ---- write the partial gradients of this token split (fixed-order sum in adamw)
+        // ---- partial gradients of this token split (summed over splits in a fixed order)
+        float* red = reinterpret_cast<float*>(base + kOffW);  // [3][128]: W is free once the last Y^T landed
+        named_bar_sync(kEpiBar, 256);
+        if (part == 1) {
+            red[r] = dwv;
+            red[128 + r] = dws;
+            red[256 + r] = db;
+        }
         if (ntiles > 0) {
             mbar_wait(&sm.all_done, 0);
             tc_fence_after();
-            const size_t hbase = static_cast<size_t>(hc) * kHid + part * 64;
-            for (int mh = 0; mh < 2; ++mh) {
-                const int f = mh * 128 + r;  // feature row (TMEM lane)
-                float* dst = p.part_wu + ((static_cast<size_t>(sp) * p.hkv + g) * 256 + f) * p.d_h + hbase;
+            const size_t hid = static_cast<size_t>(hc) * kHid + r;
+            float* dst = p.part_wu + (static_cast<size_t>(sp) * p.hkv + g) * 256 * p.d_h + hid;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                const int f0 = part * 128 + c * 32;
+                uint32_t w[32];
+                tmem_ld32(t_dw + lane_base + f0, w);
+                tmem_wait_ld(w);
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    uint32_t w[32];
-                    tmem_ld32(t_dw + mh * 128 + part * 64 + h2 * 32 + lane_base, w);
-                    tmem_wait_ld(w);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<float4*>(dst + h2 * 32)[q] =
-                            make_float4(__uint_as_float(w[4 * q]), __uint_as_float(w[4 * q + 1]),
-                                        __uint_as_float(w[4 * q + 2]), __uint_as_float(w[4 * q + 3]));
-                }
+                for (int q = 0; q < 32; ++q) dst[static_cast<size_t>(f0 + q) * p.d_h] = __uint_as_float(w[q]);
             }
-            uint32_t e[8];
+        }
+        named_bar_sync(kEpiBar, 256);
+        if (part == 0) {
             const size_t vo = (static_cast<size_t>(sp) * p.hkv + g) * p.d_h + static_cast<size_t>(hc) * kHid + r;
-            if (part == 0) {
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]), "=r"(e[6]),
-                               "=r"(e[7])
-                             : "r"(t_dwv + lane_base));
-                tmem_wait_ld(e);
-                p.part_wv[vo] = __uint_as_float(e[0]);
-                p.part_ws[vo] = __uint_as_float(e[1]);
-            } else {
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]), "=r"(e[6]),
-                               "=r"(e[7])
-                             : "r"(t_db + lane_base));
-                tmem_wait_ld(e);
-                p.part_bu[vo] = __uint_as_float(e[0]);
-            }
+            p.part_wv[vo] = dwv + red[r];
+            p.part_ws[vo] = dws + red[128 + r];
+            p.part_bu[vo] = db + red[256 + r];
         }
     }
     tc_fence_before();
