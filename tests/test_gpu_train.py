@@ -3,9 +3,11 @@
 * vsp_indexer_loss_grad vs the f64 restatement of indexer_backward_loss (pinned bit-exact to
   the reference in tests/test_oracle.py), on the same bf16 K, V, W_U values:
   loss within 1e-3 relative; each gradient tensor within 3e-2 relative Frobenius error
-  (bf16 X / W_U / dY / Z operands on the tensor core, fp32 accumulation); the bias
+  (bf16 X / W_U / dY operands on the tensor core, fp32 accumulation; dw_v, dw_s, db_U as
+  fp32 register sums); sizes up to 4 token tiles per backward CTA; the bias
   gradients sum(dlogit) are ~0 analytically (|g| <= 1e-4).
 * vsp_adamw_step vs the f64 optimizer_step restatement (fp32 state: 1e-5 relative).
+* Two calls give bit-identical loss and gradients (fixed-order reductions).
 * A short distillation run lowers the loss like the fp32 torch-autograd reference.
 """
 import numpy as np
@@ -38,7 +40,10 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
-@pytest.mark.parametrize("n,hkv,d_h,reverse", [(300, 2, 256, True), (1000, 1, 512, False), (128, 2, 256, True)])
+# (4096, 1, 256) and (2500, 2, 256) give every backward CTA 4 token tiles (both X / Y^T buffer
+# slots reused, ragged last tile); the others 1-2 tiles per CTA
+@pytest.mark.parametrize("n,hkv,d_h,reverse", [(300, 2, 256, True), (1000, 1, 512, False), (128, 2, 256, True),
+                                               (4096, 1, 256, False), (2500, 2, 256, True)])
 def test_loss_grad_matches_oracle(distill, n, hkv, d_h, reverse):
     g = torch.Generator().manual_seed(n + d_h)
     k = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
@@ -71,6 +76,26 @@ def test_loss_grad_matches_oracle(distill, n, hkv, d_h, reverse):
         bv = float(gr[tr.nw + 3 * tr.nv + h])
         bs = float(gr[tr.nw + 3 * tr.nv + hkv + h])
         assert abs(bv - want["b_v"]) <= 1e-4 and abs(bs - want["b_s"]) <= 1e-4
+
+
+def test_loss_grad_deterministic(distill):
+    """Fixed-order reductions everywhere (cluster DSMEM sums in kl_grad, per-split partials summed
+    in order): two calls on the same inputs give bit-identical loss and gradients."""
+    n, hkv, d_h = 5000, 2, 256
+    g = torch.Generator().manual_seed(11)
+    k = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    v = torch.randn(n, hkv, 128, generator=g).bfloat16().cuda()
+    tv, ts = _targets(hkv, n, seed=12)
+    tr = distill.IndexerTrainer(hkv, 128, d_h, "cuda", seed=5)
+    tr.view("w_v").copy_(torch.randn(hkv, d_h, generator=g) * 0.3)
+    tr.view("w_s").copy_(torch.randn(hkv, d_h, generator=g) * 0.3)
+    tr.w_u_bf16.copy_(tr.view("w_u").bfloat16())
+    l1 = tr.loss_grad(k, v, tv, ts).clone()
+    g1 = tr.grads.clone()
+    l2 = tr.loss_grad(k, v, tv, ts).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(l1, l2)
+    assert torch.equal(g1, tr.grads)
 
 
 def test_adamw_matches_oracle(distill):
