@@ -382,15 +382,36 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
 __global__ void reduce_grads_kernel(const float* __restrict__ part_wu, const float* __restrict__ part_bu,
                                     const float* __restrict__ part_wv, const float* __restrict__ part_ws,
                                     const double* __restrict__ dbias, int hkv, int d_h, int nsplit, float* grads) {
-    const long long nw = static_cast<long long>(hkv) * 256 * d_h;
+    const long long nw = static_cast<long long>(hkv) * 256 * d_h;  // multiple of 4 (d_h % 256 == 0)
     const long long nv = static_cast<long long>(hkv) * d_h;
     const long long total = nw + 3 * nv + 2 * hkv;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    // W_U: float4 lanes, all nsplit loads issued before the in-order sum (HBM-latency bound otherwise)
+    const float4* pw = reinterpret_cast<const float4*>(part_wu);
+    const long long nw4 = nw / 4;
+    for (long long i = t0; i < nw4; i += stride) {
+        float4 v[16];
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k0 = 0; k0 < nsplit; k0 += 16) {
+            const int kn = min(16, nsplit - k0);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (k < kn) v[k] = __ldcs(pw + (k0 + k) * nw4 + i);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (k < kn) {
+                    s.x += v[k].x;
+                    s.y += v[k].y;
+                    s.z += v[k].z;
+                    s.w += v[k].w;
+                }
+        }
+        reinterpret_cast<float4*>(grads)[i] = s;
+    }
+    for (long long i = nw + t0; i < total; i += stride) {
         float s = 0.f;
-        if (i < nw) {
-            for (int k = 0; k < nsplit; ++k) s += part_wu[k * nw + i];
-        } else if (i < nw + 3 * nv) {
+        if (i < nw + 3 * nv) {
             const long long j = i - nw;
             const int which = static_cast<int>(j / nv);
             const long long o = j % nv;
