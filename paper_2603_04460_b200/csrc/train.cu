@@ -146,8 +146,9 @@ constexpr int kOffDY = kOffW + kWBytes;
 constexpr int kOffDL = kOffDY + kTBytes;    // float2 {dlv, dls} per token of the current tile
 constexpr int kOffBar = kOffDL + kTok * 8;
 constexpr int kSmemBytes = kOffBar + 256 + 1024;
-constexpr int kThreads = 384;               // warp0 TMA, warp1 MMA, warps 4-11 epilogue
-constexpr uint32_t kEpiBar = 1;             // named barrier of the 8 epilogue warps
+constexpr int kThreads = 640;               // warp0 TMA, warp1 MMA, warps 4-19 epilogue
+constexpr int kEpiWarps = 16;               // 4 lane quarters x 4 token quarters
+constexpr uint32_t kEpiBar = 1;             // named barrier of the epilogue warps
 static_assert(kSmemBytes <= 227 * 1024, "train smem");
 
 struct __align__(64) BwdParams {
@@ -193,9 +194,9 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
             mbar_init(&sm.x_empty[s][0], 1);
             mbar_init(&sm.x_empty[s][1], 1);
             mbar_init(&sm.y_full[s], 1);
-            mbar_init(&sm.y_free[s], 8);
+            mbar_init(&sm.y_free[s], kEpiWarps);
         }
-        mbar_init(&sm.ep_done, 8);
+        mbar_init(&sm.ep_done, kEpiWarps);
         mbar_init(&sm.dy_free, 1);
         mbar_init(&sm.all_done, 1);
         fence_barrier_init();
@@ -278,17 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
         }
     } else if (warp >= 4) {
         const int quarter = warp & 3;
-        const int part = (warp - 4) >> 2;  // tokens [64 part, 64 part + 64) of each tile
+        const int part = (warp - 4) >> 2;  // tokens [32 part, 32 part + 32) of each tile
         const int r = quarter * 32 + lane;  // hidden unit (TMEM lane)
-        const int e = (warp - 4) * 32 + lane;  // 0..255: loader of dlv (e < 128) / dls of token e & 127
+        const int e = (warp - 4) * 32 + lane;  // 0..511: e < 256 loads dlv (e < 128) / dls of token e & 127
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const size_t ho = static_cast<size_t>(g) * p.d_h + hc * kHid + r;
         const float bu = p.b_u[ho], wv = p.w_v[ho], ws = p.w_s[ho];
-        uint8_t* dyb = base + kOffDY + part * 16384;
+        uint8_t* dyb = base + kOffDY + (part >> 1) * 16384;  // the 64-token box holding these tokens
         float* dl = reinterpret_cast<float*>(base + kOffDL);  // [tok][2]
         auto load_dl = [&](int i) {
             const int t = (tile_lo + i) * kTok + (e & 127);
-            if (i >= ntiles || t >= p.n) return 0.f;
+            if (e >= 256 || i >= ntiles || t >= p.n) return 0.f;
             return e < 128 ? p.dlogit_v[static_cast<size_t>(g) * p.n + t]
                            : p.dlogit_s[static_cast<size_t>(g) * p.n + (p.reverse ? p.n - 1 - t : t)];
         };
@@ -296,29 +297,27 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
         float nxt = load_dl(0);
         for (int i = 0; i < ntiles; ++i) {
             const int s = i & 1;
-            named_bar_sync(kEpiBar, 256);  // every epilogue thread is done with tile i-1's dl
-            dl[(e & 127) * 2 + (e >> 7)] = nxt;
-            named_bar_sync(kEpiBar, 256);
+            named_bar_sync(kEpiBar, 32 * kEpiWarps);  // every epilogue thread is done with tile i-1's dl
+            if (e < 256) dl[(e & 127) * 2 + (e >> 7)] = nxt;
+            named_bar_sync(kEpiBar, 32 * kEpiWarps);
             nxt = load_dl(i + 1);
             mbar_wait(&sm.y_full[s], (i >> 1) & 1);
             tc_fence_after();
-            uint32_t u[2][32];
-            tmem_ld32(t_y + s * 128 + lane_base + part * 64, u[0]);
-            tmem_ld32(t_y + s * 128 + lane_base + part * 64 + 32, u[1]);
-            tmem_wait_ld(u[0]);
-            tmem_reg_fence(u[1]);
+            uint32_t u[32];
+            tmem_ld32(t_y + s * 128 + lane_base + part * 32, u);
+            tmem_wait_ld(u);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.y_free[s]);
-            uint32_t dyw[32];
+            uint32_t dyw[16];
 #pragma unroll
-            for (int c2 = 0; c2 < 32; ++c2) {
+            for (int c2 = 0; c2 < 16; ++c2) {
                 float dy2[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int col = 2 * c2 + h;  // token within this part
-                    const float2 d = *reinterpret_cast<const float2*>(dl + (part * 64 + col) * 2);
-                    const float y = __uint_as_float(u[col >> 5][col & 31]) + bu;
+                    const float2 d = *reinterpret_cast<const float2*>(dl + (part * 32 + col) * 2);
+                    const float y = __uint_as_float(u[col]) + bu;
                     const float hh = 0.5f * y;
                     float th;
                     asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(hh));
@@ -334,29 +333,28 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
             }
             if (i >= 1) mbar_wait(&sm.dy_free, (i - 1) & 1);  // dW(i-1) has read the dY^T tile
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-                *reinterpret_cast<uint4*>(dyb + sw128(r, ch)) =
+            for (int ch = 0; ch < 4; ++ch)
+                *reinterpret_cast<uint4*>(dyb + sw128(r, (part & 1) * 4 + ch)) =
                     make_uint4(dyw[4 * ch], dyw[4 * ch + 1], dyw[4 * ch + 2], dyw[4 * ch + 3]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.ep_done);
         }
         // ---- partial gradients of this token split (summed over splits in a fixed order)
-        float* red = reinterpret_cast<float*>(base + kOffW);  // [3][128]: W is free once the last Y^T landed
-        named_bar_sync(kEpiBar, 256);
-        if (part == 1) {
-            red[r] = dwv;
-            red[128 + r] = dws;
-            red[256 + r] = db;
-        }
+        float* red = reinterpret_cast<float*>(base + kOffW);  // [part][3][128]: W is free once the last Y^T landed
+        mbar_wait(&sm.w_full, 0);  // (a split without tiles: the W load must not land on red)
+        named_bar_sync(kEpiBar, 32 * kEpiWarps);
+        red[(part * 3 + 0) * 128 + r] = dwv;
+        red[(part * 3 + 1) * 128 + r] = dws;
+        red[(part * 3 + 2) * 128 + r] = db;
         if (ntiles > 0) {
             mbar_wait(&sm.all_done, 0);
             tc_fence_after();
             const size_t hid = static_cast<size_t>(hc) * kHid + r;
             float* dst = p.part_wu + (static_cast<size_t>(sp) * p.hkv + g) * 256 * p.d_h + hid;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                const int f0 = part * 128 + c * 32;
+            for (int c = 0; c < 2; ++c) {
+                const int f0 = part * 64 + c * 32;
                 uint32_t w[32];
                 tmem_ld32(t_dw + lane_base + f0, w);
                 tmem_wait_ld(w);
@@ -364,12 +362,16 @@ __global__ void __launch_bounds__(kThreads, 1) backward_kernel(const __grid_cons
                 for (int q = 0; q < 32; ++q) dst[static_cast<size_t>(f0 + q) * p.d_h] = __uint_as_float(w[q]);
             }
         }
-        named_bar_sync(kEpiBar, 256);
-        if (part == 0) {
+        named_bar_sync(kEpiBar, 32 * kEpiWarps);
+        if (part == 0) {  // token quarters summed in order
             const size_t vo = (static_cast<size_t>(sp) * p.hkv + g) * p.d_h + static_cast<size_t>(hc) * kHid + r;
-            p.part_wv[vo] = dwv + red[r];
-            p.part_ws[vo] = dws + red[128 + r];
-            p.part_bu[vo] = db + red[256 + r];
+            float a[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                a[k] = ((red[k * 128 + r] + red[(3 + k) * 128 + r]) + red[(6 + k) * 128 + r]) + red[(9 + k) * 128 + r];
+            p.part_wv[vo] = a[0];
+            p.part_ws[vo] = a[1];
+            p.part_bu[vo] = a[2];
         }
     }
     tc_fence_before();
